@@ -1,0 +1,263 @@
+"""Python face of the CPU oracle (TEST INFRASTRUCTURE ONLY).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs may import this package.  The product package
+``paper_2210_03523_b200`` never imports it.
+
+Thin ctypes marshalling around ``liboracle.so`` (built from
+``dgsem_oracle.c`` by :func:`build`); all arithmetic lives in the C file,
+whose functions cite PAPER.md line by line.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "liboracle.so")
+_SRC = os.path.join(_HERE, "dgsem_oracle.c")
+
+EULER, NS = 0, 1
+ROE, LLF = 0, 1
+NONISOLATED, ISOLATED = 0, 1
+TAU_NEW, TAU_TRADITIONAL = 0, 1
+JUMP_A, JUMP_B = 0, 1
+TAU_STRIDE = 9
+SENTINEL = 1e30
+NMAX = 16
+
+
+def build(force: bool = False) -> str:
+    hdr = os.path.join(_HERE, "dgsem_oracle.h")
+    stale = not os.path.exists(_SO) or max(os.path.getmtime(_SRC), os.path.getmtime(hdr)) > os.path.getmtime(_SO)
+    if force or stale:
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", _SO, _SRC, "-lm"])
+    return _SO
+
+
+class _Phys(C.Structure):
+    _fields_ = [("gamma", C.c_double), ("physics", C.c_int), ("flux", C.c_int),
+                ("mu", C.c_double), ("Pr", C.c_double), ("qinf", C.c_double * 5)]
+
+
+class _Mesh(C.Structure):
+    _fields_ = [("E", C.c_int), ("nbr", C.c_void_p), ("gorder", C.c_void_p), ("geo", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        _lib.orc_compute_dt.restype = C.c_double
+    return _lib
+
+
+def _p(a):
+    return C.c_void_p(a.ctypes.data)
+
+
+def phys(physics=EULER, flux=ROE, gamma=1.4, mu=0.0, Pr=0.72, qinf=None):
+    ph = _Phys()
+    ph.gamma = gamma
+    ph.physics = physics
+    ph.flux = flux
+    ph.mu = mu
+    ph.Pr = Pr
+    qi = np.zeros(5) if qinf is None else np.asarray(qinf, np.float64)
+    for v in range(5):
+        ph.qinf[v] = qi[v]
+    return ph
+
+
+class Problem:
+    """Holds the mesh arrays alive for the C side."""
+
+    def __init__(self, mesh, ph=None):
+        self.nbr = np.ascontiguousarray(mesh.nbr, np.int32)
+        self.gorder = np.ascontiguousarray(mesh.gorder, np.int32)
+        self.geo = np.ascontiguousarray(mesh.geo, np.float64)
+        self.E = int(self.nbr.shape[0])
+        self.m = _Mesh(self.E, _p(self.nbr).value, _p(self.gorder).value, _p(self.geo).value)
+        self.ph = ph if ph is not None else phys()
+
+    # -- helpers -------------------------------------------------------
+    @staticmethod
+    def _ord(orders):
+        return np.ascontiguousarray(orders, np.int32)
+
+    @staticmethod
+    def size(orders, ncomp=5):
+        return int(ncomp * np.prod(np.asarray(orders, np.int64) + 1, axis=1).sum())
+
+    # -- operators -----------------------------------------------------
+    def node_coords(self, orders):
+        o = self._ord(orders)
+        X = np.empty(self.size(o, 3))
+        lib().orc_node_coords(C.byref(self.m), _p(o), _p(X))
+        return X
+
+    def mass(self, orders):
+        o = self._ord(orders)
+        M = np.empty(self.size(o, 1))
+        lib().orc_mass(C.byref(self.m), _p(o), _p(M))
+        return M
+
+    def rhs(self, orders, q, variant=NONISOLATED):
+        o = self._ord(orders)
+        q = np.ascontiguousarray(q, np.float64)
+        out = np.empty_like(q)
+        rc = lib().orc_rhs(C.byref(self.m), _p(o), _p(q), int(variant), C.byref(self.ph), _p(out))
+        if rc:
+            raise ValueError("orc_rhs failed")
+        return out
+
+    def gradient(self, orders, q, variant=NONISOLATED):
+        o = self._ord(orders)
+        q = np.ascontiguousarray(q, np.float64)
+        out = np.empty(self.size(o, 15))
+        lib().orc_gradient(C.byref(self.m), _p(o), _p(q), int(variant), C.byref(self.ph), _p(out))
+        return out
+
+    def dt(self, orders, q, cfl, dfl=None):
+        o = self._ord(orders)
+        q = np.ascontiguousarray(q, np.float64)
+        return lib().orc_compute_dt(C.byref(self.m), _p(o), _p(q), C.byref(self.ph), C.c_double(cfl),
+                                    C.c_double(cfl if dfl is None else dfl))
+
+    def rk3_step(self, orders, q, dt):
+        o = self._ord(orders)
+        q = np.array(q, np.float64, copy=True)
+        rc = lib().orc_rk3_step(C.byref(self.m), _p(o), _p(q), C.c_double(dt), C.byref(self.ph))
+        if rc:
+            raise ValueError("orc_rk3_step failed")
+        return q
+
+    def tau_estimate(self, orders, q, qdot_ref, formulation=TAU_NEW):
+        o = self._ord(orders)
+        q = np.ascontiguousarray(q, np.float64)
+        r = np.ascontiguousarray(qdot_ref, np.float64)
+        tau = np.empty((self.E, 3, TAU_STRIDE))
+        lib().orc_tau_estimate(C.byref(self.m), _p(o), _p(q), _p(r), int(formulation), C.byref(self.ph), _p(tau))
+        return tau
+
+    def tau_field(self, orders, q, qdot_ref, e, d, p, formulation=TAU_NEW):
+        o = self._ord(orders)
+        q = np.ascontiguousarray(q, np.float64)
+        r = np.ascontiguousarray(qdot_ref, np.float64)
+        out = np.empty(5 * 17 ** 3)
+        nc = lib().orc_tau_field(C.byref(self.m), _p(o), _p(q), _p(r), int(e), int(d), int(p), int(formulation),
+                                 C.byref(self.ph), _p(out))
+        return out[: 5 * nc].reshape(5, nc)
+
+
+# -- basis ---------------------------------------------------------------
+
+def basis(N):
+    x = np.empty(N + 1); w = np.empty(N + 1)
+    D = np.empty((N + 1) * (N + 1)); Dh = np.empty((N + 1) * (N + 1))
+    lm = np.empty(N + 1); lp = np.empty(N + 1)
+    if lib().orc_basis(int(N), _p(x), _p(w), _p(D), _p(Dh), _p(lm), _p(lp)):
+        raise ValueError(N)
+    return dict(x=x, w=w, D=D.reshape(N + 1, N + 1), Dhat=Dh.reshape(N + 1, N + 1), lm1=lm, lp1=lp)
+
+
+def interp_matrix(Nf, Nt):
+    T = np.empty((Nt + 1) * (Nf + 1))
+    lib().orc_interp_matrix(int(Nf), int(Nt), _p(T))
+    return T.reshape(Nt + 1, Nf + 1)
+
+
+def projection_matrix(M, s):
+    P = np.empty((s + 1) * (M + 1))
+    lib().orc_projection_matrix(int(M), int(s), _p(P))
+    return P.reshape(s + 1, M + 1)
+
+
+# -- point fluxes ----------------------------------------------------------
+
+def euler_flux(q, k, gamma=1.4):
+    q = np.ascontiguousarray(q, np.float64); f = np.empty(5)
+    lib().orc_euler_flux(_p(q), int(k), C.c_double(gamma), _p(f))
+    return f
+
+
+def roe_flux(qL, qR, n, gamma=1.4):
+    qL = np.ascontiguousarray(qL, np.float64); qR = np.ascontiguousarray(qR, np.float64)
+    n = np.ascontiguousarray(n, np.float64); F = np.empty(5)
+    lib().orc_roe_flux(_p(qL), _p(qR), _p(n), C.c_double(gamma), _p(F))
+    return F
+
+
+def llf_flux(qL, qR, n, gamma=1.4):
+    qL = np.ascontiguousarray(qL, np.float64); qR = np.ascontiguousarray(qR, np.float64)
+    n = np.ascontiguousarray(n, np.float64); F = np.empty(5)
+    lib().orc_llf_flux(_p(qL), _p(qR), _p(n), C.c_double(gamma), _p(F))
+    return F
+
+
+def viscous_flux(q, g, k, ph):
+    q = np.ascontiguousarray(q, np.float64); g = np.ascontiguousarray(g, np.float64); f = np.empty(5)
+    lib().orc_viscous_flux(_p(q), _p(g), int(k), C.byref(ph), _p(f))
+    return f
+
+
+# -- map / selection / jump / transfer --------------------------------------
+
+def build_map(orders, tau, Nmin, Nmax):
+    o = np.ascontiguousarray(orders, np.int32)
+    tau = np.ascontiguousarray(tau, np.float64)
+    E = o.shape[0]; K = Nmax - Nmin + 1
+    mp = np.empty((E, K, K, K)); sl = np.empty((E, 3))
+    if lib().orc_build_map(E, _p(o), _p(tau), int(Nmin), int(Nmax), _p(mp), _p(sl)):
+        raise ValueError("bad order range")
+    return mp, sl  # mp[e, n3, n2, n1]
+
+
+def combine_max(total, mp):
+    total = np.ascontiguousarray(total, np.float64)
+    mp = np.ascontiguousarray(mp, np.float64)
+    lib().orc_combine_max(C.c_size_t(total.size), _p(total), _p(mp))
+    return total
+
+
+def select_from_map(mp, Nmin, Nmax, tau_max):
+    mp = np.ascontiguousarray(mp, np.float64)
+    E = mp.shape[0]
+    out = np.empty((E, 3), np.int32); mg = np.empty(E)
+    lib().orc_select_from_map(E, _p(mp), int(Nmin), int(Nmax), C.c_double(tau_max), _p(out), _p(mg))
+    return out, mg
+
+
+def decrease_cap(cur, sel, cap=1):
+    cur = np.ascontiguousarray(cur, np.int32); sel = np.array(sel, np.int32, copy=True)
+    lib().orc_decrease_cap(cur.shape[0], _p(cur), int(cap), _p(sel))
+    return sel
+
+
+def jump_fixpoint(nbr, orders, rule, Nmax):
+    nbr = np.ascontiguousarray(nbr, np.int32); o = np.array(orders, np.int32, copy=True)
+    sweeps = lib().orc_jump_fixpoint(o.shape[0], _p(nbr), int(rule), int(Nmax), _p(o))
+    return o, sweeps
+
+
+def transfer(old_orders, q, new_orders, ncomp=5):
+    oo = np.ascontiguousarray(old_orders, np.int32); on = np.ascontiguousarray(new_orders, np.int32)
+    q = np.ascontiguousarray(q, np.float64)
+    out = np.empty(Problem.size(on, ncomp))
+    lib().orc_transfer(oo.shape[0], _p(oo), _p(q), _p(on), _p(out), int(ncomp))
+    return out
+
+
+def select_dynamic(orders, tau, nbr, tau_max, Nmin, Nmax, rule=JUMP_B, cap=1):
+    """Dynamic adaptation stage (Fig. 1; cap P:672; jump P:511-520)."""
+    mp, _ = build_map(orders, tau, Nmin, Nmax)
+    sel, mg = select_from_map(mp, Nmin, Nmax, tau_max)
+    sel = decrease_cap(orders, sel, cap)
+    sel, _ = jump_fixpoint(nbr, sel, rule, Nmax)
+    return sel, mg
