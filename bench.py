@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path on BASELINE.json configs[1] (cfg2):
+
+  Euler density pulse, fp64, periodic cube 16^3 elements, fine N=(6,6,6),
+  pulse centre seeded in [0.3,0.7]^3, width 0.08; dynamic p-adaptation with
+  tau_estimate every 50 RK steps, tolerance 1e-4.
+
+One bench STEP = one estimation interval of that run = every row of the hot
+path once over the cfg2 layout:
+  50 x (CFL dt on device + one Williamson RK3 step = 3 fused residual/RK-stage
+  launches)  ->  reference residual (SOLVER, non-isolated)  ->  batched
+  tau-estimation over all coarse orders  ->  dynamic order selection with the
+  jump fixpoint  ->  projection of the state onto the selected orders.
+The layout is kept at N=6 across steps so that every step does identical
+work (the projected state is the step's adaptation output).
+
+metric: DGSEM residual GDOF/s (fp64), whole job: NDOF x residual evaluations
+in the step (151) / step time, all ranks.  Also reported: tau-estimation
+elements/s and the residual-kernel roofline.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads as W  # noqa: E402
+
+RK_PER_STEP = 50
+CFL = 0.5
+TAU_MAX = 1e-4
+NMIN, NMAX = 3, 8
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def cfg2_inputs(S):
+    X = S.node_coords()
+    return W.pulse_state(X, S.orders, center=W.cfg2_center(), sigma=0.08)
+
+
+def make_solver(dg, mesh, orders):
+    S = dg.Solver(mesh)
+    S.set_orders(orders)
+    return S
+
+
+def run_gpu(args, rank, world):
+    import torch
+
+    import paper_2210_03523_b200 as dg
+
+    dg.build()
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    mesh = W.cube_mesh(16)
+    orders = W.orders_uniform(mesh.E, 6)
+    S = make_solver(dg, mesh, orders)
+    ndof = S.ndof
+    q0_host = cfg2_inputs(S)
+    q0 = torch.from_numpy(q0_host).to(dev)
+    qa = q0.clone()
+    qb = torch.empty_like(qa)
+    g = torch.empty_like(qa)
+    ref = torch.empty_like(qa)
+    tau = torch.empty((mesh.E, 3, 9), dtype=torch.float64, device=dev)
+    dt = torch.zeros(1, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(timers=None):
+        nonlocal qa, qb
+        t0 = ev() if timers else None
+        rk_ms = 0.0
+        for _ in range(RK_PER_STEP):
+            S.compute_dt(qa, CFL, dt)
+            if timers:
+                e0, e1 = ev(), ev()
+                e0.record(stream)
+            S.rk_step(qa, qb, g, dt)
+            if timers:
+                e1.record(stream)
+                timers["rk"].append((e0, e1))
+            qa, qb = qb, qa
+        if timers:
+            e0, e1 = ev(), ev()
+            e0.record(stream)
+        S.rhs_eval(qa, ref)
+        S.tau_estimate(qa, ref, reference=dg.REF_SOLVER, tau=tau)
+        if timers:
+            e1.record(stream)
+            timers["tau"].append((e0, e1))
+        sel, _ = S.select_orders(tau, TAU_MAX, NMIN, NMAX, mode=dg.SELECT_DYNAMIC, jump_rule=dg.JUMP_B, dec_cap=1)
+        qn = S.transfer(sel, qa)
+        return sel, qn
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # timed region
+    timers = {"rk": [], "tau": []}
+    launches0 = S.launches
+    clocks = ClockSampler(dev.index)
+    if rank == 0:
+        clocks.start()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, end = ev(), ev()
+    start.record(stream)
+    for _ in range(args.steps):
+        sel, qn = step(timers)
+    end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop() if rank == 0 else None
+    launches = S.launches - launches0
+    total_ms = start.elapsed_time(end)
+    rk_ms = sum(a.elapsed_time(b) for a, b in timers["rk"])
+    tau_ms = sum(a.elapsed_time(b) for a, b in timers["tau"])
+    if world > 1:
+        t = torch.tensor([total_ms, rk_ms, tau_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, rk_ms, tau_ms = t.tolist()
+    evals_per_step = 3 * RK_PER_STEP + 1
+    value = world * ndof * evals_per_step * args.steps / (total_ms * 1e-3) / 1e9
+    # roofline of the dominant kernel: fused residual + RK-stage (k_residual)
+    # algorithmic bytes per DOF: stage 1 reads q, writes g and q' (A_1 = 0: g
+    # not read) = 120 B; stages 2-3 read q, g and write g, q' = 160 B.
+    bytes_rk_step = ndof * (120 + 160 + 160)
+    rk_count = RK_PER_STEP * args.steps
+    achieved = bytes_rk_step * rk_count / (rk_ms * 1e-3) / 1e9
+    peak, peak_kind = load_peaks()
+    tau_elems = mesh.E * args.steps / (tau_ms * 1e-3)
+
+    # end-to-end through the public API with host buffers: H2D of the step's
+    # input state from pinned memory, the step, D2H of the adapted state + orders
+    e2e = None
+    if not args.no_e2e:
+        pinned = torch.from_numpy(q0_host).pin_memory()
+        out_pinned = torch.empty(S.state_len, dtype=torch.float64).pin_memory()
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        d2h = 0
+        for _ in range(args.steps):
+            qa.copy_(pinned, non_blocking=True)
+            sel, qn = step()
+            o = out_pinned[: qn.numel()]
+            o.copy_(qn, non_blocking=True)
+            d2h += qn.numel() * 8 + sel.nbytes
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1)
+        e2e = {"value": world * ndof * evals_per_step * args.steps / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s",
+               "h2d_bytes_per_step": int(q0_host.nbytes), "d2h_bytes_per_step": int(d2h // args.steps)}
+
+    return dict(value=value, total_ms=total_ms, rk_ms=rk_ms, tau_ms=tau_ms, ndof=ndof, E=mesh.E,
+                achieved=achieved, peak=peak, peak_kind=peak_kind, tau_elems=tau_elems, clocks=clk,
+                launches=launches, e2e=e2e, rk_count=rk_count, bytes_rk_step=bytes_rk_step)
+
+
+def oracle_baseline(sample_rk_steps=1, with_tau=True):
+    """The CPU oracle as it stands on this host's cores: a bounded sample of
+    the same workload (cfg2 layout): RK3 steps + one tau-estimate."""
+    import oracle
+
+    mesh = W.cube_mesh(16)
+    orders = W.orders_uniform(mesh.E, 6)
+    P = oracle.Problem(mesh)
+    X = P.node_coords(orders)
+    q = W.pulse_state(X, orders, center=W.cfg2_center(), sigma=0.08)
+    ndof = W.ndof(orders)
+    t0 = time.perf_counter()
+    for _ in range(sample_rk_steps):
+        dt = P.dt(orders, q, CFL)
+        q = P.rk3_step(orders, q, dt)
+    t1 = time.perf_counter()
+    tau_s = None
+    if with_tau:
+        r = P.rhs(orders, q)
+        P.tau_estimate(orders, q, r)
+        tau_s = time.perf_counter() - t1
+    gdofs = ndof * 3 * sample_rk_steps / (t1 - t0) / 1e9
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
+    return dict(value=gdofs, seconds=t1 - t0, tau_s=tau_s, tau_elems=mesh.E / tau_s if tau_s else None, cores=cores,
+                sample=f"{sample_rk_steps} RK3 step(s) (3 residuals each) on the cfg2 layout (16^3 elements, N=6, "
+                       f"{ndof} DOF)" + (" + 1 SOLVER residual + 1 tau-estimate" if with_tau else ""))
+
+
+def config_block(world, extra=None):
+    c = {"workload": "cfg2: Euler density pulse, periodic 16^3 affine hexes, N=(6,6,6) Gauss-Lobatto, "
+                     "50 RK3 steps (CFL 0.5) + SOLVER-reference tau-estimate + dynamic select (tau_max 1e-4, "
+                     "N in [3,8], jump rule b, decrease cap 1) + transfer per step",
+         "elements": 4096, "orders": [6, 6, 6], "ndof": 4096 * 343, "residuals_per_step": 3 * RK_PER_STEP + 1,
+         "l2": "inputs larger than L2: each RK stage touches q, g, q' = 3 x 56.2 MB = 169 MB > 126 MB L2",
+         "parallelism": f"replicas{world}" if world > 1 else "single"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        if args.impl == "ours":
+            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group(backend=backend)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        # The reference arm for this tier is the CPU oracle, timed as it stands.
+        import oracle
+
+        oracle.build()
+        for _ in range(args.warmup):
+            oracle_baseline(1, with_tau=False)
+        ts = []
+        for _ in range(args.steps):
+            r = oracle_baseline(1, with_tau=False)
+            ts.append(r["seconds"])
+        total = sum(ts)
+        ndof = 4096 * 343
+        value = ndof * 3 * args.steps / total / 1e9
+        line = {"impl": "reference", "metric": "DGSEM residual GDOF/s (fp64)", "value": value, "unit": "GDOF/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config_block(1, {"reference_step": "1 RK3 step (3 residuals) per step, CPU oracle"}),
+                "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": r["cores"], "kind": "oracle",
+                                 "sample": r["sample"]},
+                "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    res = run_gpu(args, rank, world)
+    if rank != 0:
+        return
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        import oracle
+
+        oracle.build()
+        cb = oracle_baseline(1, with_tau=True)
+        cpu = {"value": cb["value"], "unit": "GDOF/s", "cores": cb["cores"], "kind": "oracle", "sample": cb["sample"],
+               "tau_elems_per_s": cb["tau_elems"]}
+    line = {
+        "metric": "DGSEM residual GDOF/s (fp64) + tau-estimation elems/s",
+        "value": res["value"], "unit": "GDOF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": res["total_ms"] / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_block(world),
+        "tau_elems_per_s": res["tau_elems"] * world,
+        "rhs_rk_gdof_s": world * res["ndof"] * 3 * res["rk_count"] / (res["rk_ms"] * 1e-3) / 1e9,
+        "roofline": {"kernel": "k_residual (fused residual + RK stage)", "bound": "hbm", "achieved": res["achieved"],
+                     "peak": res["peak"], "unit": "GB/s", "frac": res["achieved"] / res["peak"],
+                     "peak_source": res["peak_kind"], "traffic": None,
+                     "bytes_per_dof": "120 (stage 1) / 160 (stages 2,3)"},
+        "cpu_baseline": cpu,
+        "e2e": res["e2e"],
+        "gpu_launches": res["launches"],
+        "clocks": res["clocks"],
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

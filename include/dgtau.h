@@ -1,0 +1,173 @@
+/*
+ * dgtau.h -- C ABI of the B200 (sm_100a) hot path of tau-estimation-driven
+ * anisotropic p-adaptation for the DGSEM (arXiv 2210.03523,
+ * /root/reference/PAPER.md; "P:<n>" below = PAPER.md line n).
+ *
+ * Plain C types only.  Pointers named *_dev are CUDA device pointers owned by
+ * the caller (e.g. torch tensors); pointers named *_host are host memory,
+ * read (or written) during the call only.  `stream` is a cudaStream_t passed
+ * as void*; every device call is stream-ordered on it and does not
+ * synchronise it unless stated.  Every entry point returns a dg_status; on
+ * error the context keeps a message readable with dg_last_error().  Nothing
+ * aborts or throws across the ABI.
+ *
+ * Layouts (canonical, shared with the host):
+ *   orders      int32 [E][3]        (N1,N2,N3) per element, 1 <= N_d <= 8
+ *   state q     fp64  [e][v][k][j][i], elements back to back, v = (rho,
+ *               rho u, rho v, rho w, E), node i fastest; element e starts at
+ *               5 * sum_{e'<e} prod_d (N_d(e')+1)
+ *   tau         fp64  [E][3][9]: tau[e][d][p] for 1 <= p <= N_d-1 (P:229:
+ *               "estimated in all coarser meshes"), tau[e][d][0] =
+ *               ||Qdot_ref,e||_inf (noise scale), other entries NaN
+ *   neighbours  int32 [E][6], face f = 2d+s (d = xi,eta,zeta; s = 0 for the
+ *               -1 side, 1 for the +1 side); >= 0 element id, -1 no-slip
+ *               adiabatic wall, -2 far field
+ *   geometry    fp64  [E][3][(g3+1)(g2+1)(g1+1)] coordinates of the
+ *               geometry nodes (Gauss-Lobatto nodes of orders g)
+ */
+#ifndef DGTAU_H
+#define DGTAU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DG_OK = 0,
+    DG_EINVAL = -1,       /* bad argument / size / order out of range           */
+    DG_ENOMEM = -2,       /* device or host allocation failed                  */
+    DG_ECUDA = -3,        /* CUDA runtime error (message has the CUDA text)    */
+    DG_EADMISSIBLE = -5,  /* rho <= 0 or p <= 0 met (reading A25)              */
+    DG_ESTATE = -7,       /* call made before mesh / orders were set           */
+    DG_EUNSUPPORTED = -8  /* geometry or physics not available in this build   */
+} dg_status;
+
+enum { DG_EULER = 0, DG_NS = 1 };
+enum { DG_FLUX_ROE = 0, DG_FLUX_LLF = 1 };
+enum { DG_NONISOLATED = 0, DG_ISOLATED = 1 };
+enum { DG_TAU_NEW = 0, DG_TAU_TRADITIONAL = 1 };
+enum { DG_REF_SOLVER = 0, DG_REF_SAME = 1 };
+enum { DG_JUMP_A = 0, DG_JUMP_B = 1 };
+enum { DG_SELECT_DYNAMIC = 0, DG_SELECT_STATIC_ACCUM = 1, DG_SELECT_STATIC_FINAL = 2 };
+
+#define DG_NMAX 8
+#define DG_TAU_STRIDE 9
+
+typedef struct dg_ctx dg_ctx;
+
+/* Physics (readings A7-A10).  gamma ratio of specific heats; for
+ * DG_NS mu = 1/Re, Pr, and qinf the far-field conserved state. */
+typedef struct {
+    int physics;   /* DG_EULER | DG_NS */
+    int flux;      /* DG_FLUX_ROE | DG_FLUX_LLF (flag, A7) */
+    double gamma;
+    double mu, Pr;
+    double qinf[5];
+} dg_params;
+
+/* tau-estimation options. */
+typedef struct {
+    int formulation; /* DG_TAU_NEW (eq TEtildedef) | DG_TAU_TRADITIONAL (eq TEdef) */
+    int reference;   /* DG_REF_SOLVER: qdot_ref_dev is the non-isolated residual
+                        -M^-1 F^N(q); DG_REF_SAME: the isolated
+                        fine residual, computed in-kernel (reading A4) */
+} dg_tau_opts;
+
+/* Order-selection policy (readings A13-A16). */
+typedef struct {
+    int mode;        /* DG_SELECT_DYNAMIC | _STATIC_ACCUM | _STATIC_FINAL */
+    double tau_max;  /* threshold, strict "<" (Table 1 header)       */
+    int Nmin, Nmax;  /* 1 <= Nmin <= Nmax <= 8                              */
+    int jump_rule;   /* DG_JUMP_A (eq N23) | DG_JUMP_B (eq N_1)             */
+    int dec_cap;     /* dynamic decrease cap per direction, >= 0    */
+} dg_adapt_policy;
+
+/* Create a context on the current CUDA device.  Returns DG_EINVAL for bad
+ * parameters.  The context owns mesh tables, plans and basis tables. */
+dg_status dg_create(const dg_params* params, dg_ctx** out);
+void dg_destroy(dg_ctx* ctx);
+const char* dg_last_error(const dg_ctx* ctx);
+
+/* Upload the mesh (copied).  gorder[3] geometry orders (1..4).  Elements
+ * whose 8 geometry corners form an axis-aligned box are "affine"; others are
+ * curved (metric terms from the geometry polynomial).  The local
+ * axes of neighbours must be aligned (reading: SURVEY 8(c).1 step 2). */
+dg_status dg_mesh_upload(dg_ctx* ctx, int E, const int32_t* nbr_host, const int32_t* gorder_host,
+                         const double* geo_host);
+
+/* Set the per-element orders (int32 [E][3], 1..8).  Builds offsets, the
+ * (N1,N2,N3) bucket work list and the mortar face plan.  Synchronous. */
+dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host);
+
+/* Number of doubles in a state vector for the current orders (5 * NDOF). */
+int64_t dg_state_len(const dg_ctx* ctx);
+/* NDOF = sum_e prod_d (N_d+1). */
+int64_t dg_ndof(const dg_ctx* ctx);
+
+/* Node coordinates at the solution nodes, host [e][3][n] (for building
+ * initial conditions).  Synchronous. */
+dg_status dg_node_coords(dg_ctx* ctx, double* X_host);
+
+/* Qdot = -(M^N)^-1 F^N(q)  (eq DGMassMatrixRight).  variant
+ * DG_NONISOLATED uses the numerical fluxes at faces (mortars between unequal
+ * orders, reading A6); DG_ISOLATED uses the inner trace flux. */
+dg_status dg_rhs_eval(dg_ctx* ctx, int variant, const double* q_dev, double* qdot_dev, void* stream);
+
+/* CFL time step (reading A11) from q, written to dt_dev[0]
+ * (device, 1 double); if dt_host != NULL the stream is synchronised and the
+ * value returned there too. */
+dg_status dg_compute_dt(dg_ctx* ctx, const double* q_dev, double cfl, double* dt_dev, double* dt_host,
+                        void* stream);
+
+/* One Williamson low-storage RK3 step: for k = 1..3
+ *   g <- A_k g + dt Qdot(q);  q <- q + B_k g.
+ * q_in holds q^n on entry and is used as scratch; q_out receives q^{n+1};
+ * g_dev is a register of the same length (no initialisation needed).
+ * dt_dev: device pointer to dt (e.g. from dg_compute_dt); the step reads it
+ * on the device, so no host synchronisation is needed. */
+dg_status dg_rk_step(dg_ctx* ctx, double* q_in_dev, double* q_out_dev, double* g_dev, const double* dt_dev,
+                     void* stream);
+
+/* Batched tau-estimation over all coarse orders p < N_d of every element and
+ * direction, isolated coarse residuals, in one launch.  qdot_ref_dev
+ * is required for DG_REF_SOLVER and ignored for DG_REF_SAME.  tau_dev is
+ * [E][3][9] (see layout). */
+dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* opts, const double* q_dev, const double* qdot_ref_dev,
+                          double* tau_dev, void* stream);
+
+/* Order selection from tau.
+ *   DYNAMIC:       map -> min-NDOF feasible -> decrease cap -> jump fixpoint
+ *   STATIC_ACCUM:  total_map_dev <- max(total_map_dev, map)  (approach 2,
+ *                  F_max, eq totalTruncMap); orders_out unchanged
+ *   STATIC_FINAL:  as STATIC_ACCUM, then select on the total map -> jump
+ * total_map_dev: fp64 [E][K][K][K], K = Nmax-Nmin+1, caller-owned, must be
+ * zero-filled before the first STATIC_ACCUM (unused for DYNAMIC, may be NULL).
+ * orders_out_host: int32 [E][3] (written for DYNAMIC / STATIC_FINAL).
+ * margin_host: optional fp64 [E], min |map - tau_max| / tau_max (parity aid).
+ * Synchronises the stream. */
+dg_status dg_select_orders(dg_ctx* ctx, const dg_adapt_policy* pol, const double* tau_dev, double* total_map_dev,
+                           int32_t* orders_out_host, double* margin_host, void* stream);
+
+/* Project a state from the current orders to new_orders (P:299-301:
+ * "the solution projected in the new polynomial spaces"; per-direction
+ * Lagrange interpolation, reading A3).  q_new_dev must hold 5*NDOF(new)
+ * doubles.  Does not change the context's orders: call dg_set_orders next. */
+dg_status dg_transfer(dg_ctx* ctx, const int32_t* new_orders_host, const double* q_old_dev, double* q_new_dev,
+                      void* stream);
+
+/* Diagnostics: per-variable sum of M * v over all nodes (conservation check,
+ * fp64 [5]) and min rho / min p of q; synchronises the stream. */
+dg_status dg_diagnostics(dg_ctx* ctx, const double* q_dev, const double* v_dev, double* sums_host,
+                         double* min_rho_p_host, void* stream);
+
+/* Count of kernel launches issued by this context since creation (the bench
+ * reports launches inside its timed region). */
+int64_t dg_launch_count(const dg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DGTAU_H */

@@ -1,0 +1,236 @@
+"""B200-native (sm_100a) hot path of tau-estimation-driven anisotropic
+p-adaptation for the DGSEM (arXiv 2210.03523).
+
+Thin Python binding over the C ABI in ``include/dgtau.h`` (``libdgtau.so``,
+built in-tree by :func:`build`).  Argument marshalling only: every numerical
+step runs in the library's CUDA kernels.  PyTorch provides device memory and
+streams.  There is no CPU fallback: importing works without a GPU (so the
+CPU test-suite can check the exported symbols), but every compute call
+raises if the library or a CUDA device is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libdgtau.so")
+_CSRC = os.path.join(_HERE, "csrc")
+_INC = os.path.join(os.path.dirname(_HERE), "include")
+
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared"]
+
+EULER, NS = 0, 1
+ROE, LLF = 0, 1
+NONISOLATED, ISOLATED = 0, 1
+TAU_NEW, TAU_TRADITIONAL = 0, 1
+REF_SOLVER, REF_SAME = 0, 1
+JUMP_A, JUMP_B = 0, 1
+SELECT_DYNAMIC, SELECT_STATIC_ACCUM, SELECT_STATIC_FINAL = 0, 1, 2
+TAU_STRIDE = 9
+NMAX = 8
+
+EXPORTS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_upload", "dg_set_orders", "dg_state_len", "dg_ndof",
+           "dg_node_coords", "dg_rhs_eval", "dg_compute_dt", "dg_rk_step", "dg_tau_estimate", "dg_select_orders",
+           "dg_transfer", "dg_diagnostics", "dg_launch_count"]
+
+
+def sources():
+    return [os.path.join(_CSRC, f) for f in sorted(os.listdir(_CSRC)) if f.endswith((".cu", ".cpp", ".cuh", ".h"))] + \
+        [os.path.join(_INC, "dgtau.h")]
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile libdgtau.so for sm_100a with nvcc (cross-compiles without a GPU)."""
+    srcs = sources()
+    stale = not os.path.exists(_SO) or max(os.path.getmtime(s) for s in srcs) > os.path.getmtime(_SO)
+    if force or stale:
+        cmd = ["nvcc", *NVCC_FLAGS, "-o", _SO, os.path.join(_CSRC, "dgtau.cu"), os.path.join(_CSRC, "basis.cpp")]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+        subprocess.check_call(cmd)
+    return _SO
+
+
+class DGError(RuntimeError):
+    pass
+
+
+class _Params(C.Structure):
+    _fields_ = [("physics", C.c_int), ("flux", C.c_int), ("gamma", C.c_double), ("mu", C.c_double),
+                ("Pr", C.c_double), ("qinf", C.c_double * 5)]
+
+
+class _TauOpts(C.Structure):
+    _fields_ = [("formulation", C.c_int), ("reference", C.c_int)]
+
+
+class _Policy(C.Structure):
+    _fields_ = [("mode", C.c_int), ("tau_max", C.c_double), ("Nmin", C.c_int), ("Nmax", C.c_int),
+                ("jump_rule", C.c_int), ("dec_cap", C.c_int)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libdgtau.so; raises if it is missing (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_SO):
+            raise DGError(f"{_SO} not built: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(_SO)
+        L.dg_last_error.restype = C.c_char_p
+        L.dg_state_len.restype = C.c_int64
+        L.dg_ndof.restype = C.c_int64
+        L.dg_launch_count.restype = C.c_int64
+        for name in EXPORTS:
+            getattr(L, name)
+        _lib = L
+    return _lib
+
+
+def _ptr(t):
+    """device pointer of a torch tensor (or None)."""
+    return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _np(a, dtype):
+    return np.ascontiguousarray(a, dtype)
+
+
+def _stream(stream):
+    import torch
+
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+class Solver:
+    """One DGSEM discretisation on the current CUDA device.
+
+    mesh: object with ``nbr`` [E][6] int32, ``gorder`` (3,), ``geo`` [E][3][ng]
+    (see workloads.Mesh).  State tensors are fp64 CUDA tensors in the
+    canonical layout of include/dgtau.h.
+    """
+
+    def __init__(self, mesh, physics=EULER, flux=ROE, gamma=1.4, mu=0.0, Pr=0.72, qinf=None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise DGError("no CUDA device: the DGSEM path runs only on the GPU (no CPU fallback)")
+        self.L = lib()
+        p = _Params()
+        p.physics, p.flux, p.gamma, p.mu, p.Pr = physics, flux, gamma, mu, Pr
+        qi = np.zeros(5) if qinf is None else np.asarray(qinf, np.float64)
+        for v in range(5):
+            p.qinf[v] = qi[v]
+        self.ctx = C.c_void_p()
+        torch.cuda.current_device()
+        self._check(self.L.dg_create(C.byref(p), C.byref(self.ctx)), "dg_create")
+        self.nbr = _np(mesh.nbr, np.int32)
+        self.E = int(self.nbr.shape[0])
+        gord = _np(mesh.gorder, np.int32)
+        geo = _np(mesh.geo, np.float64)
+        self._check(self.L.dg_mesh_upload(self.ctx, self.E, self.nbr.ctypes.data_as(C.c_void_p),
+                                          gord.ctypes.data_as(C.c_void_p), geo.ctypes.data_as(C.c_void_p)),
+                    "dg_mesh_upload")
+        self.orders = None
+        self._dt = torch.zeros(1, dtype=torch.float64, device="cuda")
+
+    def _check(self, rc, what):
+        if rc != 0:
+            msg = self.L.dg_last_error(self.ctx).decode() if self.ctx else ""
+            raise DGError(f"{what} failed ({rc}): {msg}")
+
+    def __del__(self):
+        try:
+            if self.ctx:
+                self.L.dg_destroy(self.ctx)
+        except Exception:
+            pass
+
+    # -- layout ----------------------------------------------------------
+    def set_orders(self, orders):
+        o = _np(orders, np.int32)
+        self._check(self.L.dg_set_orders(self.ctx, o.ctypes.data_as(C.c_void_p)), "dg_set_orders")
+        self.orders = o.copy()
+
+    @property
+    def state_len(self) -> int:
+        return int(self.L.dg_state_len(self.ctx))
+
+    @property
+    def ndof(self) -> int:
+        return int(self.L.dg_ndof(self.ctx))
+
+    @property
+    def launches(self) -> int:
+        return int(self.L.dg_launch_count(self.ctx))
+
+    def node_coords(self):
+        X = np.empty(3 * self.ndof)
+        self._check(self.L.dg_node_coords(self.ctx, X.ctypes.data_as(C.c_void_p)), "dg_node_coords")
+        return X
+
+    def new_state(self):
+        import torch
+
+        return torch.empty(self.state_len, dtype=torch.float64, device="cuda")
+
+    # -- operators --------------------------------------------------------
+    def rhs_eval(self, q, qdot=None, variant=NONISOLATED, stream=None):
+        qdot = self.new_state() if qdot is None else qdot
+        self._check(self.L.dg_rhs_eval(self.ctx, int(variant), _ptr(q), _ptr(qdot), _stream(stream)), "dg_rhs_eval")
+        return qdot
+
+    def compute_dt(self, q, cfl, dt=None, sync=False, stream=None):
+        dt = self._dt if dt is None else dt
+        host = C.c_double(0.0)
+        self._check(self.L.dg_compute_dt(self.ctx, _ptr(q), C.c_double(cfl), _ptr(dt),
+                                         C.byref(host) if sync else None, _stream(stream)), "dg_compute_dt")
+        return host.value if sync else dt
+
+    def rk_step(self, q_in, q_out, g, dt, stream=None):
+        self._check(self.L.dg_rk_step(self.ctx, _ptr(q_in), _ptr(q_out), _ptr(g), _ptr(dt), _stream(stream)),
+                    "dg_rk_step")
+
+    def tau_estimate(self, q, qdot_ref=None, formulation=TAU_NEW, reference=REF_SOLVER, tau=None, stream=None):
+        import torch
+
+        o = _TauOpts(int(formulation), int(reference))
+        tau = torch.empty((self.E, 3, TAU_STRIDE), dtype=torch.float64, device="cuda") if tau is None else tau
+        self._check(self.L.dg_tau_estimate(self.ctx, C.byref(o), _ptr(q), _ptr(qdot_ref), _ptr(tau),
+                                           _stream(stream)), "dg_tau_estimate")
+        return tau
+
+    def select_orders(self, tau, tau_max, Nmin, Nmax, mode=SELECT_DYNAMIC, jump_rule=JUMP_B, dec_cap=1,
+                      total_map=None, stream=None):
+        pol = _Policy(int(mode), float(tau_max), int(Nmin), int(Nmax), int(jump_rule), int(dec_cap))
+        out = np.zeros((self.E, 3), np.int32)
+        margin = np.zeros(self.E)
+        self._check(self.L.dg_select_orders(self.ctx, C.byref(pol), _ptr(tau), _ptr(total_map),
+                                            out.ctypes.data_as(C.c_void_p), margin.ctypes.data_as(C.c_void_p),
+                                            _stream(stream)), "dg_select_orders")
+        return out, margin
+
+    def transfer(self, new_orders, q_old, stream=None):
+        import torch
+
+        no = _np(new_orders, np.int32)
+        n = int((5 * np.prod(no.astype(np.int64) + 1, axis=1)).sum())
+        q_new = torch.empty(n, dtype=torch.float64, device="cuda")
+        self._check(self.L.dg_transfer(self.ctx, no.ctypes.data_as(C.c_void_p), _ptr(q_old), _ptr(q_new),
+                                       _stream(stream)), "dg_transfer")
+        return q_new
+
+    def diagnostics(self, q, v=None, stream=None):
+        sums = np.zeros(5)
+        mn = np.zeros(2)
+        self._check(self.L.dg_diagnostics(self.ctx, _ptr(q), _ptr(v), sums.ctypes.data_as(C.c_void_p),
+                                          mn.ctypes.data_as(C.c_void_p), _stream(stream)), "dg_diagnostics")
+        return sums, mn

@@ -1,0 +1,601 @@
+// dgtau.cu -- C ABI (include/dgtau.h) and host-side plans of the B200 hot path.
+//
+// Host work is O(E) plan building only (offsets, (N1,N2,N3) bucket work list,
+// mortar face list); every step of the numerical path runs in the kernels of
+// kernels.cuh.  There is no CPU fallback: without a CUDA device every call
+// returns DG_ECUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/dgtau.h"
+#include "basis.h"
+#include "kernels.cuh"
+
+using namespace dgtau;
+
+struct dg_ctx {
+    std::string err;
+    dg_params prm{};
+    int device = 0;
+    // mesh
+    int E = 0;
+    int gorder[3] = {1, 1, 1};
+    std::vector<int> nbr;
+    std::vector<double> geo;
+    std::vector<double> h;  // affine box sizes [E][3]
+    // orders / plans
+    bool have_orders = false;
+    std::vector<int> orders;
+    std::vector<long long> off;
+    long long ndof = 0;
+    int nwork = 0;
+    size_t res_smem = 0;
+    int nmortar = 0;
+    long long mortar_len = 0;
+    int maxn = 0;
+    // device
+    Tables* d_tab = nullptr;
+    int* d_nbr = nullptr;
+    double* d_h = nullptr;
+    int* d_orders = nullptr;
+    long long* d_off = nullptr;
+    WorkItem* d_work = nullptr;
+    int* d_elist = nullptr;
+    MortarItem* d_mortar = nullptr;
+    long long* d_moff = nullptr;
+    double* d_mortarG = nullptr;
+    unsigned long long* d_scratch = nullptr;  // [8]
+    int* d_flag = nullptr;                    // [4]
+    int* d_sel = nullptr;                     // [2][E][3]
+    double* d_margin = nullptr;               // [E]
+    double* d_sums = nullptr;                 // [5]
+    long long launches = 0;
+};
+
+namespace {
+
+dg_status fail(dg_ctx* c, dg_status s, const std::string& msg)
+{
+    if (c) c->err = msg;
+    return s;
+}
+
+dg_status cuda_check(dg_ctx* c, cudaError_t e, const char* what)
+{
+    if (e == cudaSuccess) return DG_OK;
+    return fail(c, DG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr)                                                       \
+    do {                                                               \
+        dg_status _s = cuda_check(ctx, (expr), #expr);                 \
+        if (_s != DG_OK) return _s;                                    \
+    } while (0)
+
+template <class T>
+void dfree(T*& p)
+{
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+template <class T>
+cudaError_t upload(T*& d, const std::vector<T>& h)
+{
+    dfree(d);
+    if (h.empty()) return cudaSuccess;
+    cudaError_t e = cudaMalloc(&d, sizeof(T) * h.size());
+    if (e != cudaSuccess) return e;
+    return cudaMemcpy(d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice);
+}
+
+PhysDev phys_dev(const dg_params& p)
+{
+    PhysDev ph;
+    ph.gamma = p.gamma;
+    ph.gm1 = p.gamma - 1.0;
+    ph.flux = p.flux;
+    ph.physics = p.physics;
+    ph.mu = p.mu;
+    ph.Pr = p.Pr;
+    for (int v = 0; v < 5; ++v) ph.qinf[v] = p.qinf[v];
+    return ph;
+}
+
+inline int npts(const int* N) { return (N[0] + 1) * (N[1] + 1) * (N[2] + 1); }
+
+dg_status check_stream_error(dg_ctx* ctx, const char* what)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(ctx, DG_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return DG_OK;
+}
+
+// Gauss-Lobatto nodes of the geometry orders, for evaluating node coordinates.
+const Tables& host_tables()
+{
+    static Tables* t = nullptr;
+    if (!t) {
+        t = new Tables;
+        build_tables(t);
+    }
+    return *t;
+}
+
+}  // namespace
+
+extern "C" {
+
+dg_status dg_create(const dg_params* params, dg_ctx** out)
+{
+    if (!params || !out) return DG_EINVAL;
+    *out = nullptr;
+    if (!(params->gamma > 1.0)) return DG_EINVAL;
+    if (params->physics != DG_EULER && params->physics != DG_NS) return DG_EINVAL;
+    if (params->flux != DG_FLUX_ROE && params->flux != DG_FLUX_LLF) return DG_EINVAL;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return DG_ECUDA;
+    dg_ctx* ctx = new dg_ctx;
+    ctx->prm = *params;
+    cudaGetDevice(&ctx->device);
+    const Tables& t = host_tables();
+    dg_status s;
+    if ((s = cuda_check(ctx, cudaMalloc(&ctx->d_tab, sizeof(Tables)), "cudaMalloc tables")) != DG_OK ||
+        (s = cuda_check(ctx, cudaMemcpy(ctx->d_tab, &t, sizeof(Tables), cudaMemcpyHostToDevice), "tables")) != DG_OK ||
+        (s = cuda_check(ctx, cudaMalloc(&ctx->d_scratch, 8 * sizeof(unsigned long long)), "scratch")) != DG_OK ||
+        (s = cuda_check(ctx, cudaMalloc(&ctx->d_flag, 4 * sizeof(int)), "flag")) != DG_OK ||
+        (s = cuda_check(ctx, cudaMemset(ctx->d_flag, 0, 4 * sizeof(int)), "flag")) != DG_OK ||
+        (s = cuda_check(ctx, cudaMalloc(&ctx->d_sums, 8 * sizeof(double)), "sums")) != DG_OK) {
+        dg_destroy(ctx);
+        return s;
+    }
+    if (params->physics == DG_NS) {
+        ctx->err = "Navier-Stokes path not in this build";
+    }
+    // large dynamic shared memory for the element kernels
+    cudaFuncSetAttribute(k_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_tau, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_transfer, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    *out = ctx;
+    return DG_OK;
+}
+
+void dg_destroy(dg_ctx* ctx)
+{
+    if (!ctx) return;
+    dfree(ctx->d_tab);
+    dfree(ctx->d_nbr);
+    dfree(ctx->d_h);
+    dfree(ctx->d_orders);
+    dfree(ctx->d_off);
+    dfree(ctx->d_work);
+    dfree(ctx->d_elist);
+    dfree(ctx->d_mortar);
+    dfree(ctx->d_moff);
+    dfree(ctx->d_mortarG);
+    dfree(ctx->d_scratch);
+    dfree(ctx->d_flag);
+    dfree(ctx->d_sel);
+    dfree(ctx->d_margin);
+    dfree(ctx->d_sums);
+    delete ctx;
+}
+
+const char* dg_last_error(const dg_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int64_t dg_launch_count(const dg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+dg_status dg_mesh_upload(dg_ctx* ctx, int E, const int32_t* nbr_host, const int32_t* gorder_host, const double* geo_host)
+{
+    if (!ctx) return DG_EINVAL;
+    if (E <= 0 || !nbr_host || !gorder_host || !geo_host) return fail(ctx, DG_EINVAL, "mesh: bad arguments");
+    for (int d = 0; d < 3; ++d)
+        if (gorder_host[d] < 1 || gorder_host[d] > NMAX) return fail(ctx, DG_EINVAL, "mesh: geometry order out of range");
+    for (long long i = 0; i < 6LL * E; ++i)
+        if (nbr_host[i] >= E || nbr_host[i] < -2) return fail(ctx, DG_EINVAL, "mesh: neighbour id out of range");
+    // aligned-axes check: e's face f neighbour must see e across the opposite face
+    for (int e = 0; e < E; ++e)
+        for (int f = 0; f < 6; ++f) {
+            int nb = nbr_host[6 * e + f];
+            if (nb >= 0 && nbr_host[6 * nb + (f ^ 1)] != e)
+                return fail(ctx, DG_EINVAL, "mesh: neighbour local axes not aligned (face " + std::to_string(f) +
+                                                " of element " + std::to_string(e) + ")");
+        }
+    ctx->E = E;
+    for (int d = 0; d < 3; ++d) ctx->gorder[d] = gorder_host[d];
+    const int ng = (gorder_host[0] + 1) * (gorder_host[1] + 1) * (gorder_host[2] + 1);
+    ctx->nbr.assign(nbr_host, nbr_host + 6LL * E);
+    ctx->geo.assign(geo_host, geo_host + 3LL * ng * E);
+    // affine detection: geometry order (1,1,1), corners of an axis-aligned box
+    ctx->h.assign(3LL * E, 0.0);
+    bool affine = gorder_host[0] == 1 && gorder_host[1] == 1 && gorder_host[2] == 1;
+    for (int e = 0; e < E && affine; ++e) {
+        const double* G = geo_host + 3LL * ng * e;
+        for (int c = 0; c < 3; ++c) {
+            const double lo = G[c * 8 + 0];
+            const double hi = G[c * 8 + (c == 0 ? 1 : (c == 1 ? 2 : 4))];
+            for (int k = 0; k < 8; ++k) {
+                const int bit = (k >> c) & 1;
+                const double want = bit ? hi : lo;
+                if (G[c * 8 + k] != want) affine = false;
+            }
+            ctx->h[3LL * e + c] = hi - lo;
+            if (!(hi > lo)) affine = false;
+        }
+    }
+    if (!affine) return fail(ctx, DG_EUNSUPPORTED, "mesh: curved / non-axis-aligned geometry not in this build");
+    CK(upload(ctx->d_nbr, ctx->nbr));
+    CK(upload(ctx->d_h, ctx->h));
+    ctx->have_orders = false;
+    return DG_OK;
+}
+
+dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
+{
+    if (!ctx) return DG_EINVAL;
+    if (ctx->E == 0) return fail(ctx, DG_ESTATE, "set_orders: no mesh");
+    const int E = ctx->E;
+    for (long long i = 0; i < 3LL * E; ++i)
+        if (orders_host[i] < 1 || orders_host[i] > NMAX) return fail(ctx, DG_EINVAL, "set_orders: order out of 1..8");
+    ctx->orders.assign(orders_host, orders_host + 3LL * E);
+    ctx->off.assign(E + 1, 0);
+    ctx->ndof = 0;
+    ctx->maxn = 0;
+    for (int e = 0; e < E; ++e) {
+        const int n = npts(&ctx->orders[3 * e]);
+        ctx->off[e + 1] = ctx->off[e] + (long long)NV * n;
+        ctx->ndof += n;
+        ctx->maxn = std::max(ctx->maxn, n);
+    }
+    // (N1,N2,N3) buckets -> work items of up to floor(256/n) elements, ordered
+    // by their first element id (spatially coherent sweep, neighbour traces hit L2)
+    std::map<int, std::vector<int>> buckets;
+    for (int e = 0; e < E; ++e) {
+        const int* N = &ctx->orders[3 * e];
+        buckets[N[0] | (N[1] << 8) | (N[2] << 16)].push_back(e);
+    }
+    std::vector<int> elist;
+    elist.reserve(E);
+    std::vector<WorkItem> work;
+    size_t smem = 0;
+    for (auto& kv : buckets) {
+        const int ord = kv.first;
+        const int N[3] = {ord & 255, (ord >> 8) & 255, (ord >> 16) & 255};
+        const int n = npts(N);
+        const int k = std::max(1, std::min(MAXSLOTS, BLOCK / n));
+        const int nfs = 2 * ((N[1] + 1) * (N[2] + 1) + (N[0] + 1) * (N[2] + 1) + (N[0] + 1) * (N[1] + 1));
+        for (size_t i = 0; i < kv.second.size(); i += k) {
+            WorkItem w;
+            w.start = (int)elist.size();
+            w.count = (int)std::min<size_t>(k, kv.second.size() - i);
+            w.ord = ord;
+            w.pad = kv.second[i];
+            for (int j = 0; j < w.count; ++j) elist.push_back(kv.second[i + j]);
+            work.push_back(w);
+            const size_t bytes = sizeof(double) * (3 * NP * NP + (size_t)w.count * NV * (2 * n + nfs));
+            smem = std::max(smem, bytes);
+        }
+    }
+    std::stable_sort(work.begin(), work.end(), [](const WorkItem& a, const WorkItem& b) { return a.pad < b.pad; });
+    ctx->nwork = (int)work.size();
+    ctx->res_smem = smem;
+    // mortar faces: + side of L against - side of R, tangential orders differ
+    std::vector<MortarItem> mort;
+    std::vector<long long> moff(6LL * E, -1);
+    long long mlen = 0;
+    static const int TA[3] = {1, 0, 0}, TB[3] = {2, 2, 1};
+    for (int e = 0; e < E; ++e)
+        for (int d = 0; d < 3; ++d) {
+            const int nb = ctx->nbr[6 * e + 2 * d + 1];
+            if (nb < 0) continue;
+            const int* NL = &ctx->orders[3 * e];
+            const int* NR = &ctx->orders[3 * nb];
+            if (NL[TA[d]] == NR[TA[d]] && NL[TB[d]] == NR[TB[d]]) continue;
+            mort.push_back(MortarItem{e, nb, d, 0});
+            moff[6LL * e + 2 * d + 1] = mlen;
+            mlen += (long long)NV * (NL[TA[d]] + 1) * (NL[TB[d]] + 1);
+            moff[6LL * nb + 2 * d] = mlen;
+            mlen += (long long)NV * (NR[TA[d]] + 1) * (NR[TB[d]] + 1);
+        }
+    ctx->nmortar = (int)mort.size();
+    ctx->mortar_len = mlen;
+    std::vector<int> ord_i(ctx->orders.begin(), ctx->orders.end());
+    CK(upload(ctx->d_orders, ord_i));
+    CK(upload(ctx->d_off, ctx->off));
+    CK(upload(ctx->d_work, work));
+    CK(upload(ctx->d_elist, elist));
+    CK(upload(ctx->d_mortar, mort));
+    CK(upload(ctx->d_moff, moff));
+    dfree(ctx->d_mortarG);
+    if (mlen > 0) CK(cudaMalloc(&ctx->d_mortarG, sizeof(double) * mlen));
+    dfree(ctx->d_sel);
+    dfree(ctx->d_margin);
+    CK(cudaMalloc(&ctx->d_sel, sizeof(int) * 6LL * E));
+    CK(cudaMalloc(&ctx->d_margin, sizeof(double) * E));
+    ctx->have_orders = true;
+    return DG_OK;
+}
+
+int64_t dg_state_len(const dg_ctx* ctx) { return ctx && ctx->have_orders ? ctx->off[ctx->E] : 0; }
+int64_t dg_ndof(const dg_ctx* ctx) { return ctx && ctx->have_orders ? ctx->ndof : 0; }
+
+dg_status dg_node_coords(dg_ctx* ctx, double* X)
+{
+    if (!ctx || !X) return DG_EINVAL;
+    if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "node_coords: orders not set");
+    const Tables& t = host_tables();
+    long long o = 0;
+    for (int e = 0; e < ctx->E; ++e) {
+        const int* N = &ctx->orders[3 * e];
+        const int n = npts(N);
+        const double* G = &ctx->geo[24LL * e];
+        for (int c = 0; c < 3; ++c) {
+            const double lo = G[c * 8], hh = ctx->h[3LL * e + c];
+            for (int k = 0; k <= N[2]; ++k)
+                for (int j = 0; j <= N[1]; ++j)
+                    for (int i = 0; i <= N[0]; ++i) {
+                        const int ijk[3] = {i, j, k};
+                        const double xi = t.x[N[c]][ijk[c]];
+                        X[o + (long long)c * n + i + (N[0] + 1) * (j + (N[1] + 1) * k)] = lo + 0.5 * (xi + 1.0) * hh;
+                    }
+        }
+        o += 3LL * n;
+    }
+    return DG_OK;
+}
+
+static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, double* out, double* g, const double* dt,
+                                 double A, double B, int mode, cudaStream_t st)
+{
+    if (variant == DG_NONISOLATED && ctx->nmortar > 0) {
+        MortarParams M;
+        M.q = q;
+        M.orders = ctx->d_orders;
+        M.off = ctx->d_off;
+        M.items = ctx->d_mortar;
+        M.moff = ctx->d_moff;
+        M.mortarG = ctx->d_mortarG;
+        M.tab = ctx->d_tab;
+        M.ph = phys_dev(ctx->prm);
+        k_mortar<<<ctx->nmortar, 128, 0, st>>>(M);
+        ctx->launches++;
+    }
+    ResParams P;
+    P.q = q;
+    P.out = out;
+    P.g = g;
+    P.dt = dt;
+    P.rkA = A;
+    P.rkB = B;
+    P.mode = mode;
+    P.variant = variant;
+    P.orders = ctx->d_orders;
+    P.off = ctx->d_off;
+    P.nbr = ctx->d_nbr;
+    P.hgeo = ctx->d_h;
+    P.work = ctx->d_work;
+    P.elist = ctx->d_elist;
+    P.mortarG = ctx->d_mortarG;
+    P.moff = ctx->d_moff;
+    P.tab = ctx->d_tab;
+    P.ph = phys_dev(ctx->prm);
+    P.flag = ctx->d_flag;
+    k_residual<<<ctx->nwork, BLOCK, ctx->res_smem, st>>>(P);
+    ctx->launches++;
+    return check_stream_error(ctx, "k_residual launch");
+}
+
+dg_status dg_rhs_eval(dg_ctx* ctx, int variant, const double* q_dev, double* qdot_dev, void* stream)
+{
+    if (!ctx || !q_dev || !qdot_dev) return DG_EINVAL;
+    if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "rhs_eval: orders not set");
+    if (variant != DG_NONISOLATED && variant != DG_ISOLATED) return fail(ctx, DG_EINVAL, "rhs_eval: variant");
+    if (ctx->prm.physics != DG_EULER) return fail(ctx, DG_EUNSUPPORTED, "rhs_eval: NS not in this build");
+    return launch_residual(ctx, variant, q_dev, qdot_dev, nullptr, nullptr, 0.0, 0.0, 0, (cudaStream_t)stream);
+}
+
+dg_status dg_compute_dt(dg_ctx* ctx, const double* q_dev, double cfl, double* dt_dev, double* dt_host, void* stream)
+{
+    if (!ctx || !q_dev || !dt_dev || !(cfl > 0)) return DG_EINVAL;
+    if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "compute_dt: orders not set");
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaMemsetAsync(ctx->d_scratch, 0, sizeof(unsigned long long), st));
+    DtParams P;
+    P.q = q_dev;
+    P.work = ctx->d_work;
+    P.elist = ctx->d_elist;
+    P.off = ctx->d_off;
+    P.hgeo = ctx->d_h;
+    P.gamma = ctx->prm.gamma;
+    P.maxbits = ctx->d_scratch;
+    k_dt<<<ctx->nwork, BLOCK, 0, st>>>(P);
+    k_dt_final<<<1, 1, 0, st>>>(ctx->d_scratch, cfl, dt_dev);
+    ctx->launches += 2;
+    dg_status s = check_stream_error(ctx, "k_dt launch");
+    if (s != DG_OK) return s;
+    if (dt_host) {
+        CK(cudaMemcpyAsync(dt_host, dt_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    return DG_OK;
+}
+
+dg_status dg_rk_step(dg_ctx* ctx, double* q_in, double* q_out, double* g, const double* dt_dev, void* stream)
+{
+    if (!ctx || !q_in || !q_out || !g || !dt_dev || q_in == q_out) return DG_EINVAL;
+    if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "rk_step: orders not set");
+    if (ctx->prm.physics != DG_EULER) return fail(ctx, DG_EUNSUPPORTED, "rk_step: NS not in this build");
+    // Williamson (1980) low-storage RK3 coefficients
+    static const double A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
+    static const double B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
+    cudaStream_t st = (cudaStream_t)stream;
+    // stage 1: q_in -> q_out, stage 2: q_out -> q_in, stage 3: q_in -> q_out
+    double* src[3] = {q_in, q_out, q_in};
+    double* dst[3] = {q_out, q_in, q_out};
+    for (int k = 0; k < 3; ++k) {
+        dg_status s = launch_residual(ctx, DG_NONISOLATED, src[k], dst[k], g, dt_dev, A[k], B[k], 1, st);
+        if (s != DG_OK) return s;
+    }
+    return DG_OK;
+}
+
+dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev, const double* qref_dev, double* tau_dev,
+                          void* stream)
+{
+    if (!ctx || !o || !q_dev || !tau_dev) return DG_EINVAL;
+    if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "tau_estimate: orders not set");
+    if (o->reference == DG_REF_SOLVER && !qref_dev) return fail(ctx, DG_EINVAL, "tau_estimate: SOLVER needs qdot_ref");
+    if (ctx->prm.physics != DG_EULER) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: NS not in this build");
+    TauParams P;
+    P.q = q_dev;
+    P.qref = o->reference == DG_REF_SOLVER ? qref_dev : nullptr;
+    P.tau = tau_dev;
+    P.orders = ctx->d_orders;
+    P.off = ctx->d_off;
+    P.hgeo = ctx->d_h;
+    P.tab = ctx->d_tab;
+    P.formulation = o->formulation;
+    P.ph = phys_dev(ctx->prm);
+    const size_t smem = sizeof(double) * 3 * NV * (size_t)ctx->maxn;
+    k_tau<<<ctx->E, BLOCK, smem, (cudaStream_t)stream>>>(P);
+    ctx->launches++;
+    return check_stream_error(ctx, "k_tau launch");
+}
+
+dg_status dg_select_orders(dg_ctx* ctx, const dg_adapt_policy* pol, const double* tau_dev, double* total_dev,
+                           int32_t* orders_out, double* margin_host, void* stream)
+{
+    if (!ctx || !pol || !tau_dev) return DG_EINVAL;
+    if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "select_orders: orders not set");
+    if (pol->Nmin < 1 || pol->Nmax > NMAX || pol->Nmin > pol->Nmax || !(pol->tau_max > 0) || pol->dec_cap < 0)
+        return fail(ctx, DG_EINVAL, "select_orders: bad policy");
+    if (pol->mode != DG_SELECT_DYNAMIC && !total_dev) return fail(ctx, DG_EINVAL, "select_orders: static needs total map");
+    if (pol->mode != DG_SELECT_STATIC_ACCUM && !orders_out) return fail(ctx, DG_EINVAL, "select_orders: orders_out");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int E = ctx->E;
+    SelParams P;
+    P.tau = tau_dev;
+    P.orders = ctx->d_orders;
+    P.total = total_dev;
+    P.sel = ctx->d_sel;
+    P.margin = ctx->d_margin;
+    P.E = E;
+    P.mode = pol->mode;
+    P.tau_max = pol->tau_max;
+    P.Nmin = pol->Nmin;
+    P.Nmax = pol->Nmax;
+    P.dec_cap = pol->dec_cap;
+    k_select<<<(E + 127) / 128, 128, 0, st>>>(P);
+    ctx->launches++;
+    dg_status s = check_stream_error(ctx, "k_select launch");
+    if (s != DG_OK) return s;
+    if (pol->mode == DG_SELECT_STATIC_ACCUM) return DG_OK;
+    // jump-condition fixpoint: Jacobi sweeps until no element changes
+    int* a = ctx->d_sel;
+    int* b = ctx->d_sel + 3LL * E;
+    for (int sweep = 0; sweep < 64; ++sweep) {
+        CK(cudaMemsetAsync(ctx->d_flag + 2, 0, sizeof(int), st));
+        k_jump<<<(E + 127) / 128, 128, 0, st>>>(ctx->d_nbr, a, b, E, pol->jump_rule == DG_JUMP_A ? 0 : 1, pol->Nmax,
+                                                 ctx->d_flag + 2);
+        ctx->launches++;
+        int changed = 0;
+        CK(cudaMemcpyAsync(&changed, ctx->d_flag + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        std::swap(a, b);
+        if (!changed) break;
+    }
+    CK(cudaMemcpyAsync(orders_out, a, sizeof(int) * 3LL * E, cudaMemcpyDeviceToHost, st));
+    if (margin_host) CK(cudaMemcpyAsync(margin_host, ctx->d_margin, sizeof(double) * E, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return DG_OK;
+}
+
+dg_status dg_transfer(dg_ctx* ctx, const int32_t* new_orders, const double* q_old, double* q_new, void* stream)
+{
+    if (!ctx || !new_orders || !q_old || !q_new) return DG_EINVAL;
+    if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "transfer: orders not set");
+    const int E = ctx->E;
+    std::vector<long long> offn(E + 1, 0);
+    for (int e = 0; e < E; ++e) {
+        for (int d = 0; d < 3; ++d)
+            if (new_orders[3 * e + d] < 1 || new_orders[3 * e + d] > NMAX) return fail(ctx, DG_EINVAL, "transfer: order");
+        offn[e + 1] = offn[e] + (long long)NV * npts(&new_orders[3 * e]);
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    int* d_on = nullptr;
+    long long* d_offn = nullptr;
+    std::vector<int> on(new_orders, new_orders + 3LL * E);
+    CK(upload(d_on, on));
+    CK(upload(d_offn, offn));
+    TransferParams P;
+    P.qold = q_old;
+    P.qnew = q_new;
+    P.oold = ctx->d_orders;
+    P.onew = d_on;
+    P.offold = ctx->d_off;
+    P.offnew = d_offn;
+    P.tab = ctx->d_tab;
+    k_transfer<<<E, BLOCK, sizeof(double) * 3 * NV * NP * NP * NP, st>>>(P);
+    ctx->launches++;
+    dg_status s = check_stream_error(ctx, "k_transfer launch");
+    CK(cudaStreamSynchronize(st));
+    dfree(d_on);
+    dfree(d_offn);
+    return s;
+}
+
+dg_status dg_diagnostics(dg_ctx* ctx, const double* q_dev, const double* v_dev, double* sums_host, double* minrp_host,
+                         void* stream)
+{
+    if (!ctx || !q_dev) return DG_EINVAL;
+    if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "diagnostics: orders not set");
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaMemsetAsync(ctx->d_sums, 0, 5 * sizeof(double), st));
+    CK(cudaMemsetAsync(ctx->d_scratch + 1, 0xff, 2 * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(ctx->d_flag + 3, 0, sizeof(int), st));
+    DiagParams P;
+    P.q = q_dev;
+    P.v = v_dev;
+    P.orders = ctx->d_orders;
+    P.off = ctx->d_off;
+    P.hgeo = ctx->d_h;
+    P.tab = ctx->d_tab;
+    P.gamma = ctx->prm.gamma;
+    P.sums = ctx->d_sums;
+    P.minbits = ctx->d_scratch + 1;
+    P.neg = ctx->d_flag + 3;
+    k_diag<<<ctx->E, 128, 0, st>>>(P);
+    ctx->launches++;
+    dg_status s = check_stream_error(ctx, "k_diag launch");
+    if (s != DG_OK) return s;
+    double sums[5];
+    unsigned long long mb[2];
+    int neg = 0, flag[2];
+    CK(cudaMemcpyAsync(sums, ctx->d_sums, sizeof(sums), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(mb, ctx->d_scratch + 1, sizeof(mb), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&neg, ctx->d_flag + 3, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(flag, ctx->d_flag, sizeof(flag), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (sums_host) std::memcpy(sums_host, sums, sizeof(sums));
+    if (minrp_host) {
+        long long b0 = (long long)mb[0], b1 = (long long)mb[1];
+        std::memcpy(&minrp_host[0], &b0, sizeof(double));
+        std::memcpy(&minrp_host[1], &b1, sizeof(double));
+    }
+    if (neg > 0 || flag[0] > 0) {
+        CK(cudaMemsetAsync(ctx->d_flag, 0, 2 * sizeof(int), st));
+        return fail(ctx, DG_EADMISSIBLE,
+                    "inadmissible state (rho<=0 or p<=0) at " + std::to_string(neg) + " nodes; first flagged element " +
+                        std::to_string(flag[1]));
+    }
+    return DG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,919 @@
+// kernels.cuh -- sm_100a fp64 kernels of the DGSEM / tau-estimation hot path.
+//
+// PAPER.md references: P:129-155 (DGSEM weak form, diagonal mass matrix),
+// P:217-218 (isolated truncation error), P:225-241 (tau-estimation with the
+// variational reference term), P:404-423 + P:461-463 (maps, approach 2,
+// sentinel), P:472-475 (Roe flux, Williamson RK3, CFL step), P:511-520 (jump
+// conditions), P:672 (decrease cap).  Readings A1-A25 are those of
+// DESIGN.md / SURVEY.md 8(c).2.
+//
+// Formulation on the device: the strong form of the GL-DGSEM, which equals the
+// weak form (eq DGSEMsystem:1) exactly for Gauss-Lobatto nodes (summation by
+// parts, W D + D^T W = B):
+//   Qdot_abc = -(1/J) sum_d [ sum_m D^{N_d}_{a_d m} Ft^d(..m..)
+//               + (delta_{a_d N_d} (G^d_+ - Ft^d_+) - delta_{a_d 0} (G^d_- - Ft^d_-)) / w_{a_d} ].
+// For the isolated variant G == Ft (own trace) so the surface term vanishes.
+// Affine axis-aligned elements: Ja^d = (prod_{d'!=d} h_d'/2) e_d, J =
+// prod h_d / 8, so Ft^d / J = (2/h_d) f_d.
+#pragma once
+
+#include <cstdint>
+
+#include "basis.h"
+
+namespace dgtau {
+
+constexpr int NV = 5;
+constexpr int BLOCK = 256;     // threads per CTA for the element kernels
+constexpr int NPT = 3;         // nodes per thread (256 * 3 >= 729 = 9^3)
+constexpr int MAXSLOTS = 32;   // elements per work item (n >= 8)
+constexpr int DG_TAU_STRIDE_DEV = 9;  // tau[e][d][0..8]
+
+struct PhysDev {
+    double gamma, gm1;
+    int flux;
+    int physics;
+    double mu, Pr;
+    double qinf[5];
+};
+
+struct WorkItem {
+    int start;  // index into elist
+    int count;  // elements in this item (all with the same orders)
+    int ord;    // N1 | N2 << 8 | N3 << 16
+    int pad;
+};
+
+struct MortarItem {
+    int L, R, d, pad;
+};
+
+__device__ __forceinline__ void unpack_ord(int ord, int& N1, int& N2, int& N3)
+{
+    N1 = ord & 255;
+    N2 = (ord >> 8) & 255;
+    N3 = (ord >> 16) & 255;
+}
+
+// ---------------------------------------------------------------------------
+// Pointwise physics
+// ---------------------------------------------------------------------------
+
+// Euler flux in Cartesian direction d.  Returns pressure in *pout.
+__device__ __forceinline__ void flux_dir(const double* q, double gm1, int d, double* f, double* pout)
+{
+    const double ir = 1.0 / q[0];
+    const double p = gm1 * (q[4] - 0.5 * ir * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]));
+    const double ud = q[1 + d] * ir;
+    f[0] = q[1 + d];
+    f[1] = q[1] * ud;
+    f[2] = q[2] * ud;
+    f[3] = q[3] * ud;
+    f[1 + d] += p;
+    f[4] = (q[4] + p) * ud;
+    *pout = p;
+}
+
+// Roe approximate Riemann solver, closed form of the wave
+// decomposition (acoustic waves u_n -/+ c, entropy + shear waves u_n),
+// no entropy fix (reading A7).  n unit normal.
+__device__ __forceinline__ void roe_flux(const double* qL, const double* qR, const double* n, double gamma,
+                                         double* F)
+{
+    const double gm1 = gamma - 1.0;
+    const double irL = 1.0 / qL[0], irR = 1.0 / qR[0];
+    double uL[3], uR[3];
+    for (int k = 0; k < 3; ++k) { uL[k] = qL[1 + k] * irL; uR[k] = qR[1 + k] * irR; }
+    const double pL = gm1 * (qL[4] - 0.5 * qL[0] * (uL[0] * uL[0] + uL[1] * uL[1] + uL[2] * uL[2]));
+    const double pR = gm1 * (qR[4] - 0.5 * qR[0] * (uR[0] * uR[0] + uR[1] * uR[1] + uR[2] * uR[2]));
+    const double HL = (qL[4] + pL) * irL, HR = (qR[4] + pR) * irR;
+    const double sL = sqrt(qL[0]), sR = sqrt(qR[0]);
+    const double is = 1.0 / (sL + sR);
+    double u[3];
+    for (int k = 0; k < 3; ++k) u[k] = (sL * uL[k] + sR * uR[k]) * is;
+    const double H = (sL * HL + sR * HR) * is;
+    const double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+    const double c2 = gm1 * (H - 0.5 * uu);
+    const double c = sqrt(c2);
+    const double un = u[0] * n[0] + u[1] * n[1] + u[2] * n[2];
+    const double unL = uL[0] * n[0] + uL[1] * n[1] + uL[2] * n[2];
+    const double unR = uR[0] * n[0] + uR[1] * n[1] + uR[2] * n[2];
+    const double rho = sL * sR;
+    const double dr = qR[0] - qL[0], dp = pR - pL, dun = unR - unL;
+    double du[3];
+    for (int k = 0; k < 3; ++k) du[k] = uR[k] - uL[k];
+    const double ic2 = 1.0 / c2;
+    const double a1 = 0.5 * (dp - rho * c * dun) * ic2;
+    const double a5 = 0.5 * (dp + rho * c * dun) * ic2;
+    const double a2 = dr - dp * ic2;
+    const double l1 = fabs(un - c), l2 = fabs(un), l5 = fabs(un + c);
+    const double w1 = l1 * a1, w5 = l5 * a5;
+    const double udu = u[0] * du[0] + u[1] * du[1] + u[2] * du[2];
+    F[0] = 0.5 * (qL[0] * unL + qR[0] * unR) - 0.5 * (w1 + l2 * a2 + w5);
+    for (int k = 0; k < 3; ++k) {
+        const double fk = 0.5 * (qL[1 + k] * unL + pL * n[k] + qR[1 + k] * unR + pR * n[k]);
+        const double dk = w1 * (u[k] - c * n[k]) + l2 * (a2 * u[k] + rho * (du[k] - dun * n[k])) +
+                          w5 * (u[k] + c * n[k]);
+        F[1 + k] = fk - 0.5 * dk;
+    }
+    const double fe = 0.5 * ((qL[4] + pL) * unL + (qR[4] + pR) * unR);
+    const double de = w1 * (H - un * c) + l2 * (a2 * 0.5 * uu + rho * (udu - un * dun)) + w5 * (H + un * c);
+    F[4] = fe - 0.5 * de;
+}
+
+// Local Lax-Friedrichs (flag, reading A7).
+__device__ __forceinline__ void llf_flux(const double* qL, const double* qR, const double* n, double gamma,
+                                         double* F)
+{
+    const double gm1 = gamma - 1.0;
+    double fL[5], fR[5];
+    const double irL = 1.0 / qL[0], irR = 1.0 / qR[0];
+    const double pL = gm1 * (qL[4] - 0.5 * irL * (qL[1] * qL[1] + qL[2] * qL[2] + qL[3] * qL[3]));
+    const double pR = gm1 * (qR[4] - 0.5 * irR * (qR[1] * qR[1] + qR[2] * qR[2] + qR[3] * qR[3]));
+    const double unL = (qL[1] * n[0] + qL[2] * n[1] + qL[3] * n[2]) * irL;
+    const double unR = (qR[1] * n[0] + qR[2] * n[1] + qR[3] * n[2]) * irR;
+    fL[0] = qL[0] * unL; fR[0] = qR[0] * unR;
+    for (int k = 0; k < 3; ++k) { fL[1 + k] = qL[1 + k] * unL + pL * n[k]; fR[1 + k] = qR[1 + k] * unR + pR * n[k]; }
+    fL[4] = (qL[4] + pL) * unL; fR[4] = (qR[4] + pR) * unR;
+    const double lam = fmax(fabs(unL) + sqrt(gamma * pL * irL), fabs(unR) + sqrt(gamma * pR * irR));
+    for (int v = 0; v < 5; ++v) F[v] = 0.5 * (fL[v] + fR[v]) - 0.5 * lam * (qR[v] - qL[v]);
+}
+
+__device__ __forceinline__ void riemann(const double* qL, const double* qR, const double* n, const PhysDev& ph,
+                                        double* F)
+{
+    if (ph.flux == 1) llf_flux(qL, qR, n, ph.gamma, F);
+    else roe_flux(qL, qR, n, ph.gamma, F);
+}
+
+// Boundary ghost states (reading A10): wall = mirrored momentum, far field = q_inf.
+__device__ __forceinline__ void ghost_state(const double* qin, int bc, const PhysDev& ph, double* qg)
+{
+    if (bc == -1) {
+        qg[0] = qin[0]; qg[1] = -qin[1]; qg[2] = -qin[2]; qg[3] = -qin[3]; qg[4] = qin[4];
+    } else {
+        for (int v = 0; v < 5; ++v) qg[v] = ph.qinf[v];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Block reductions
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double warp_max(double v)
+{
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// all threads receive the block max; uses red[32]
+__device__ __forceinline__ double block_max(double v, double* red)
+{
+    v = warp_max(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    const int nw = (blockDim.x + 31) >> 5;
+    double r = lane < nw ? red[lane] : 0.0;
+    r = warp_max(r);
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// Residual / RK-stage kernel: one CTA per work item (1..32 elements of the
+// same orders, from one (N1,N2,N3) bucket).
+// ---------------------------------------------------------------------------
+
+struct ResParams {
+    const double* q;        // state read (neighbour traces come from here too)
+    double* out;            // mode 0: qdot; mode 1: q_out = q + B g
+    double* g;              // RK register (mode 1)
+    const double* dt;       // device dt (mode 1)
+    double rkA, rkB;
+    int mode;
+    int variant;            // 0 non-isolated, 1 isolated
+    const int* orders;      // [E][3]
+    const long long* off;   // [E+1]
+    const int* nbr;         // [E][6]
+    const double* hgeo;     // [E][3]
+    const WorkItem* work;
+    const int* elist;
+    const double* mortarG;  // projected Riemann fluxes for mortar faces
+    const long long* moff;  // [E][6] offset into mortarG or -1
+    const Tables* tab;
+    PhysDev ph;
+    int* flag;              // [0] admissibility violations, [1] element id
+};
+
+__device__ __forceinline__ void node_ijk(int node, int n1, int n2, int& i, int& j, int& k)
+{
+    i = node % n1;
+    const int r = node / n1;
+    j = r % n2;
+    k = r / n2;
+}
+
+__global__ void __launch_bounds__(BLOCK) k_residual(ResParams P)
+{
+    extern __shared__ double sm[];
+    __shared__ long long s_off[MAXSLOTS];
+    __shared__ int s_e[MAXSLOTS];
+    __shared__ double s_h[MAXSLOTS][3];
+
+    const WorkItem w = P.work[blockIdx.x];
+    int N[3];
+    unpack_ord(w.ord, N[0], N[1], N[2]);
+    const int n1 = N[0] + 1, n2 = N[1] + 1, n3 = N[2] + 1;
+    const int n = n1 * n2 * n3;
+    const int cnt = w.count;
+    const int nf[3] = {n2 * n3, n1 * n3, n1 * n2};
+    const int fsz = 2 * (nf[0] + nf[1] + nf[2]);  // face points per element (6 faces)
+    int foff[6];
+    {
+        int acc = 0;
+        for (int f = 0; f < 6; ++f) { foff[f] = acc; acc += NV * nf[f >> 1]; }
+    }
+    double* Dsm = sm;                  // 3 x 81
+    double* qs = Dsm + 3 * NP * NP;    // cnt x 5 x n
+    double* Fs = qs + cnt * NV * n;    // cnt x 5 x n
+    double* Gs = Fs + cnt * NV * n;    // cnt x 5 x fsz
+
+    const int tid = threadIdx.x;
+    if (tid < cnt) {
+        const int e = P.elist[w.start + tid];
+        s_e[tid] = e;
+        s_off[tid] = P.off[e];
+        for (int d = 0; d < 3; ++d) s_h[tid][d] = P.hgeo[3 * e + d];
+    }
+    for (int t = tid; t < 3 * NP * NP; t += BLOCK) {
+        const int d = t / (NP * NP), r = t % (NP * NP);
+        const int nd = N[d] + 1;
+        if (r < nd * nd) Dsm[d * NP * NP + r] = P.tab->D[N[d]][r];
+    }
+    __syncthreads();
+    for (int t = tid; t < cnt * NV * n; t += BLOCK) {
+        const int slot = t / (NV * n), r = t - slot * NV * n;
+        qs[t] = P.q[s_off[slot] + r];
+    }
+    __syncthreads();
+
+    const double gm1 = P.ph.gm1;
+    double acc[NPT][NV];
+#pragma unroll
+    for (int it = 0; it < NPT; ++it)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[it][v] = 0.0;
+
+    // ---- volume term: sum_d (2/h_d) D^{N_d} f_d -------------------------
+    for (int d = 0; d < 3; ++d) {
+        for (int t = tid; t < cnt * n; t += BLOCK) {
+            const int slot = t / n, node = t - slot * n;
+            double qv[NV], f[NV], p;
+            for (int v = 0; v < NV; ++v) qv[v] = qs[(slot * NV + v) * n + node];
+            flux_dir(qv, gm1, d, f, &p);
+            if (d == 0 && !(qv[0] > 0.0 && p > 0.0)) {
+                if (atomicAdd(P.flag, 1) == 0) P.flag[1] = s_e[slot];
+            }
+            for (int v = 0; v < NV; ++v) Fs[(slot * NV + v) * n + node] = f[v];
+        }
+        __syncthreads();
+        const int nd = N[d] + 1;
+        const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
+        const double* Dd = Dsm + d * NP * NP;
+#pragma unroll
+        for (int it = 0; it < NPT; ++it) {
+            const int t = tid + it * BLOCK;
+            if (t < cnt * n) {
+                const int slot = t / n, node = t - slot * n;
+                int ijk[3];
+                node_ijk(node, n1, n2, ijk[0], ijk[1], ijk[2]);
+                const int a = ijk[d];
+                const int base = node - a * stride;
+                const double sc = 2.0 / s_h[slot][d];
+                for (int v = 0; v < NV; ++v) {
+                    const double* Fl = Fs + (slot * NV + v) * n + base;
+                    double s = 0.0;
+                    for (int m = 0; m < nd; ++m) s += Dd[a * nd + m] * Fl[m * stride];
+                    acc[it][v] += sc * s;
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- surface: Gs = G - f_own (strong form) on the 6 faces ----------
+    if (P.variant == 0) {
+        for (int t = tid; t < cnt * fsz; t += BLOCK) {
+            const int slot = t / fsz;
+            int r = t - slot * fsz;
+            int f = 0;
+            while (r >= nf[f >> 1]) { r -= nf[f >> 1]; ++f; }
+            const int d = f >> 1, s = f & 1, pt = r;
+            const int e = s_e[slot];
+            // own boundary node
+            int ijk[3];
+            const int ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
+            const int nta = N[ta] + 1;
+            ijk[ta] = pt % nta;
+            ijk[tb] = pt / nta;
+            ijk[d] = s ? N[d] : 0;
+            const int node = ijk[0] + n1 * (ijk[1] + n2 * ijk[2]);
+            double qo[NV], fo[NV], p;
+            for (int v = 0; v < NV; ++v) qo[v] = qs[(slot * NV + v) * n + node];
+            flux_dir(qo, gm1, d, fo, &p);
+            double Gv[NV];
+            const int nb = P.nbr[6 * e + f];
+            double nrm[3] = {0.0, 0.0, 0.0};
+            nrm[d] = 1.0;
+            if (nb < 0) {
+                double qg[NV];
+                ghost_state(qo, nb, P.ph, qg);
+                if (s) riemann(qo, qg, nrm, P.ph, Gv); else riemann(qg, qo, nrm, P.ph, Gv);
+            } else {
+                const long long mo = P.moff[6 * e + f];
+                if (mo >= 0) {
+                    for (int v = 0; v < NV; ++v) Gv[v] = P.mortarG[mo + (long long)v * nf[d] + pt];
+                } else {
+                    const int B1 = P.orders[3 * nb] + 1, B2 = P.orders[3 * nb + 1] + 1, B3 = P.orders[3 * nb + 2] + 1;
+                    int jb[3] = {ijk[0], ijk[1], ijk[2]};
+                    const int Bd = d == 0 ? B1 : (d == 1 ? B2 : B3);
+                    jb[d] = s ? 0 : Bd - 1;
+                    const int nbn = B1 * B2 * B3;
+                    const long long ob = P.off[nb] + jb[0] + B1 * (jb[1] + B2 * jb[2]);
+                    double qn[NV];
+                    for (int v = 0; v < NV; ++v) qn[v] = P.q[ob + (long long)v * nbn];
+                    if (s) riemann(qo, qn, nrm, P.ph, Gv); else riemann(qn, qo, nrm, P.ph, Gv);
+                }
+            }
+            double* Gd = Gs + slot * NV * fsz + foff[f];
+            for (int v = 0; v < NV; ++v) Gd[v * nf[d] + pt] = Gv[v] - fo[v];
+        }
+        __syncthreads();
+        // lifting onto the boundary nodes
+#pragma unroll
+        for (int it = 0; it < NPT; ++it) {
+            const int t = tid + it * BLOCK;
+            if (t < cnt * n) {
+                const int slot = t / n, node = t - slot * n;
+                int ijk[3];
+                node_ijk(node, n1, n2, ijk[0], ijk[1], ijk[2]);
+                for (int d = 0; d < 3; ++d) {
+                    const int a = ijk[d];
+                    if (a != 0 && a != N[d]) continue;
+                    const int ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
+                    const int pt = ijk[ta] + (N[ta] + 1) * ijk[tb];
+                    const int f = 2 * d + (a == N[d] ? 1 : 0);
+                    const double sgn = a == N[d] ? 1.0 : -1.0;
+                    const double sc = sgn * 2.0 / (s_h[slot][d] * P.tab->w[N[d]][a]);
+                    const double* Gd = Gs + slot * NV * fsz + foff[f];
+                    for (int v = 0; v < NV; ++v) acc[it][v] += sc * Gd[v * nf[d] + pt];
+                }
+            }
+        }
+    }
+
+    // ---- output: Qdot = -acc, or the fused low-storage RK update -------
+    if (P.mode == 0) {
+#pragma unroll
+        for (int it = 0; it < NPT; ++it) {
+            const int t = tid + it * BLOCK;
+            if (t < cnt * n) {
+                const int slot = t / n, node = t - slot * n;
+                for (int v = 0; v < NV; ++v) P.out[s_off[slot] + (long long)v * n + node] = -acc[it][v];
+            }
+        }
+    } else {
+        const double dt = *P.dt;
+#pragma unroll
+        for (int it = 0; it < NPT; ++it) {
+            const int t = tid + it * BLOCK;
+            if (t < cnt * n) {
+                const int slot = t / n, node = t - slot * n;
+                for (int v = 0; v < NV; ++v) {
+                    const long long ix = s_off[slot] + (long long)v * n + node;
+                    const double gn = (P.rkA == 0.0 ? 0.0 : P.rkA * P.g[ix]) - dt * acc[it][v];
+                    P.g[ix] = gn;
+                    P.out[ix] = qs[(slot * NV + v) * n + node] + P.rkB * gn;
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Mortar kernel (reading A6): one CTA per face whose tangential orders differ.
+// Traces interpolated to the mortar (orders max per tangential direction),
+// Riemann flux there, exact L2 projection back to both sides.
+// ---------------------------------------------------------------------------
+
+struct MortarParams {
+    const double* q;
+    const int* orders;
+    const long long* off;
+    const MortarItem* items;
+    const long long* moff;
+    double* mortarG;
+    const Tables* tab;
+    PhysDev ph;
+};
+
+__global__ void __launch_bounds__(128) k_mortar(MortarParams P)
+{
+    __shared__ double GM[NV][NP * NP];
+    const MortarItem it = P.items[blockIdx.x];
+    const int d = it.d;
+    const int ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
+    int NL[3], NR[3];
+    for (int k = 0; k < 3; ++k) { NL[k] = P.orders[3 * it.L + k]; NR[k] = P.orders[3 * it.R + k]; }
+    const int M1 = max(NL[ta], NR[ta]), M2 = max(NL[tb], NR[tb]);
+    const int nm = (M1 + 1) * (M2 + 1);
+    const int nL = (NL[0] + 1) * (NL[1] + 1) * (NL[2] + 1), nR = (NR[0] + 1) * (NR[1] + 1) * (NR[2] + 1);
+    const long long oL = P.off[it.L], oR = P.off[it.R];
+    const double* TL1 = P.tab->T[NL[ta]][M1];
+    const double* TL2 = P.tab->T[NL[tb]][M2];
+    const double* TR1 = P.tab->T[NR[ta]][M1];
+    const double* TR2 = P.tab->T[NR[tb]][M2];
+    double nrm[3] = {0.0, 0.0, 0.0};
+    nrm[d] = 1.0;
+    for (int t = threadIdx.x; t < nm; t += blockDim.x) {
+        const int m1 = t % (M1 + 1), m2 = t / (M1 + 1);
+        double qL[NV] = {0, 0, 0, 0, 0}, qR[NV] = {0, 0, 0, 0, 0};
+        // L's +1 face and R's -1 face, interpolated along both tangential directions
+        for (int b = 0; b <= NL[tb]; ++b)
+            for (int a = 0; a <= NL[ta]; ++a) {
+                int ijk[3];
+                ijk[d] = NL[d]; ijk[ta] = a; ijk[tb] = b;
+                const long long ix = oL + ijk[0] + (NL[0] + 1) * (ijk[1] + (NL[1] + 1) * ijk[2]);
+                const double wgt = TL1[m1 * (NL[ta] + 1) + a] * TL2[m2 * (NL[tb] + 1) + b];
+                for (int v = 0; v < NV; ++v) qL[v] += wgt * P.q[ix + (long long)v * nL];
+            }
+        for (int b = 0; b <= NR[tb]; ++b)
+            for (int a = 0; a <= NR[ta]; ++a) {
+                int ijk[3];
+                ijk[d] = 0; ijk[ta] = a; ijk[tb] = b;
+                const long long ix = oR + ijk[0] + (NR[0] + 1) * (ijk[1] + (NR[1] + 1) * ijk[2]);
+                const double wgt = TR1[m1 * (NR[ta] + 1) + a] * TR2[m2 * (NR[tb] + 1) + b];
+                for (int v = 0; v < NV; ++v) qR[v] += wgt * P.q[ix + (long long)v * nR];
+            }
+        double F[NV];
+        riemann(qL, qR, nrm, P.ph, F);
+        for (int v = 0; v < NV; ++v) GM[v][t] = F[v];
+    }
+    __syncthreads();
+    // project back: side X with tangential orders (S1, S2)
+    for (int side = 0; side < 2; ++side) {
+        const int* NS = side == 0 ? NL : NR;
+        const int S1 = NS[ta], S2 = NS[tb];
+        const int ns = (S1 + 1) * (S2 + 1);
+        const long long mo = P.moff[6 * (side == 0 ? it.L : it.R) + 2 * d + (side == 0 ? 1 : 0)];
+        const double* P1 = P.tab->P[M1][S1];
+        const double* P2 = P.tab->P[M2][S2];
+        for (int t = threadIdx.x; t < ns; t += blockDim.x) {
+            const int a = t % (S1 + 1), b = t / (S1 + 1);
+            double s[NV] = {0, 0, 0, 0, 0};
+            for (int m2 = 0; m2 <= M2; ++m2)
+                for (int m1 = 0; m1 <= M1; ++m1) {
+                    const double wgt = P1[a * (M1 + 1) + m1] * P2[b * (M2 + 1) + m2];
+                    for (int v = 0; v < NV; ++v) s[v] += wgt * GM[v][m1 + (M1 + 1) * m2];
+                }
+            for (int v = 0; v < NV; ++v) P.mortarG[mo + (long long)v * ns + t] = s[v];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// CFL time step (reading A11): affine
+//   lambda = sum_d (|u_d| + c) (N_d+1)^2 / h_d,  dt = CFL / max lambda.
+// ---------------------------------------------------------------------------
+
+struct DtParams {
+    const double* q;
+    const WorkItem* work;
+    const int* elist;
+    const long long* off;
+    const double* hgeo;
+    double gamma;
+    unsigned long long* maxbits;
+};
+
+__global__ void __launch_bounds__(BLOCK) k_dt(DtParams P)
+{
+    __shared__ double red[32];
+    const WorkItem w = P.work[blockIdx.x];
+    int N[3];
+    unpack_ord(w.ord, N[0], N[1], N[2]);
+    const int n = (N[0] + 1) * (N[1] + 1) * (N[2] + 1);
+    double lmax = 0.0;
+    for (int t = threadIdx.x; t < w.count * n; t += BLOCK) {
+        const int slot = t / n, node = t - slot * n;
+        const int e = P.elist[w.start + slot];
+        const long long o = P.off[e] + node;
+        double q[NV];
+        for (int v = 0; v < NV; ++v) q[v] = P.q[o + (long long)v * n];
+        const double ir = 1.0 / q[0];
+        const double p = (P.gamma - 1.0) * (q[4] - 0.5 * ir * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]));
+        const double c = sqrt(P.gamma * p * ir);
+        double lam = 0.0;
+        for (int d = 0; d < 3; ++d) {
+            const double np1 = N[d] + 1.0;
+            lam += (fabs(q[1 + d] * ir) + c) * np1 * np1 / P.hgeo[3 * e + d];
+        }
+        lmax = fmax(lmax, lam);
+    }
+    lmax = block_max(lmax, red);
+    if (threadIdx.x == 0) atomicMax(P.maxbits, (unsigned long long)__double_as_longlong(lmax));
+}
+
+__global__ void k_dt_final(const unsigned long long* maxbits, double cfl, double* dt)
+{
+    dt[0] = cfl / __longlong_as_double((long long)maxbits[0]);
+}
+
+// ---------------------------------------------------------------------------
+// tau-estimation (eqs TEtildedef / TEdef; isolated coarse
+// residuals P:469; decoupled directional levels, reading A12).  One CTA per
+// element: for each direction d and coarse order p < N_d, the fine state is
+// interpolated along d (I, reading A3), the isolated residual at the coarse
+// orders is formed on chip, and
+//   tau~ = I(Qdot_ref) - Qdot_c,   tau = J w w w tau~ (traditional),
+//   tau[e][d][p] = max over coarse nodes and variables |tau|.
+// ---------------------------------------------------------------------------
+
+struct TauParams {
+    const double* q;
+    const double* qref;   // SOLVER reference or nullptr (SAME)
+    double* tau;          // [E][3][9]
+    const int* orders;
+    const long long* off;
+    const double* hgeo;
+    const Tables* tab;
+    int formulation;
+    PhysDev ph;
+};
+
+// Isolated strong-form residual at orders O of a state held in registers for
+// the CTA's owned nodes (t = tid + it*BLOCK < nO):  acc = sum_d (2/h_d) D f_d,
+// i.e. Qdot = -acc.  Fs is scratch of 5*nO doubles.
+__device__ __forceinline__ void iso_residual_regs(const int O[3], int nO, const double (&qc)[NPT][NV],
+                                                  double (&acc)[NPT][NV], double* Fs, const double* h,
+                                                  const Tables* tab, double gm1)
+{
+    const int tid = threadIdx.x;
+    const int o1 = O[0] + 1, o2 = O[1] + 1;
+#pragma unroll
+    for (int it = 0; it < NPT; ++it)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[it][v] = 0.0;
+    for (int d = 0; d < 3; ++d) {
+#pragma unroll
+        for (int it = 0; it < NPT; ++it) {
+            const int t = tid + it * BLOCK;
+            if (t < nO) {
+                double f[NV], p;
+                flux_dir(qc[it], gm1, d, f, &p);
+                for (int v = 0; v < NV; ++v) Fs[v * nO + t] = f[v];
+            }
+        }
+        __syncthreads();
+        const int nd = O[d] + 1;
+        const int stride = d == 0 ? 1 : (d == 1 ? o1 : o1 * o2);
+        const double* Dd = tab->D[O[d]];
+        const double sc = 2.0 / h[d];
+#pragma unroll
+        for (int it = 0; it < NPT; ++it) {
+            const int t = tid + it * BLOCK;
+            if (t < nO) {
+                int ijk[3];
+                node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
+                const int a = ijk[d];
+                const int base = t - a * stride;
+                for (int v = 0; v < NV; ++v) {
+                    double s = 0.0;
+                    for (int m = 0; m < nd; ++m) s += __ldg(&Dd[a * nd + m]) * Fs[v * nO + base + m * stride];
+                    acc[it][v] += sc * s;
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(BLOCK) k_tau(TauParams P)
+{
+    extern __shared__ double sm[];
+    __shared__ double red[32];
+    const int e = blockIdx.x;
+    const int tid = threadIdx.x;
+    int N[3] = {P.orders[3 * e], P.orders[3 * e + 1], P.orders[3 * e + 2]};
+    const int n1 = N[0] + 1, n2 = N[1] + 1, n3 = N[2] + 1;
+    const int n = n1 * n2 * n3;
+    double h[3] = {P.hgeo[3 * e], P.hgeo[3 * e + 1], P.hgeo[3 * e + 2]};
+    const long long o = P.off[e];
+    double* qs = sm;           // 5n
+    double* Rs = qs + NV * n;  // 5n
+    double* Fs = Rs + NV * n;  // 5n
+    for (int t = tid; t < NV * n; t += BLOCK) qs[t] = P.q[o + t];
+    const double gm1 = P.ph.gm1;
+    double qc[NPT][NV], acc[NPT][NV];
+    if (P.qref) {
+        for (int t = tid; t < NV * n; t += BLOCK) Rs[t] = P.qref[o + t];
+        __syncthreads();
+    } else {  // SAME reference: isolated fine residual (reading A4)
+        __syncthreads();
+#pragma unroll
+        for (int it = 0; it < NPT; ++it) {
+            const int t = tid + it * BLOCK;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) qc[it][v] = t < n ? qs[v * n + t] : 1.0;
+        }
+        iso_residual_regs(N, n, qc, acc, Fs, h, P.tab, gm1);
+#pragma unroll
+        for (int it = 0; it < NPT; ++it) {
+            const int t = tid + it * BLOCK;
+            if (t < n)
+                for (int v = 0; v < NV; ++v) Rs[v * n + t] = -acc[it][v];
+        }
+        __syncthreads();
+    }
+    double rn = 0.0;
+    for (int t = tid; t < NV * n; t += BLOCK) rn = fmax(rn, fabs(Rs[t]));
+    rn = block_max(rn, red);
+    if (tid == 0)
+        for (int d = 0; d < 3; ++d) {
+            P.tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV + 0] = rn;
+            for (int p = N[d]; p < DG_TAU_STRIDE_DEV; ++p)
+                P.tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV + p] = __longlong_as_double(0x7ff8000000000000LL);
+        }
+    const double Jel = h[0] * h[1] * h[2] / 8.0;
+    for (int d = 0; d < 3; ++d) {
+        const int nd = N[d] + 1;
+        const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
+        for (int p = 1; p < N[d]; ++p) {
+            int O[3] = {N[0], N[1], N[2]};
+            O[d] = p;
+            const int o1 = O[0] + 1, o2 = O[1] + 1;
+            const int nO = o1 * o2 * (O[2] + 1);
+            const double* T = P.tab->T[N[d]][p];
+            // q_c = T^{N_d -> p} q along d
+#pragma unroll
+            for (int it = 0; it < NPT; ++it) {
+                const int t = tid + it * BLOCK;
+                if (t < nO) {
+                    int ijk[3];
+                    node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
+                    const int ic = ijk[d];
+                    ijk[d] = 0;
+                    const int base = ijk[0] + n1 * (ijk[1] + n2 * ijk[2]);
+                    for (int v = 0; v < NV; ++v) {
+                        double s = 0.0;
+                        for (int a = 0; a < nd; ++a) s += __ldg(&T[ic * nd + a]) * qs[v * n + base + a * stride];
+                        qc[it][v] = s;
+                    }
+                } else {
+                    for (int v = 0; v < NV; ++v) qc[it][v] = 1.0;
+                }
+            }
+            iso_residual_regs(O, nO, qc, acc, Fs, h, P.tab, gm1);
+            double tmax = 0.0;
+#pragma unroll
+            for (int it = 0; it < NPT; ++it) {
+                const int t = tid + it * BLOCK;
+                if (t < nO) {
+                    int ijk[3];
+                    node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
+                    const int ic = ijk[d];
+                    double scale = 1.0;
+                    if (P.formulation == 1)
+                        scale = Jel * P.tab->w[O[0]][ijk[0]] * P.tab->w[O[1]][ijk[1]] * P.tab->w[O[2]][ijk[2]];
+                    ijk[d] = 0;
+                    const int base = ijk[0] + n1 * (ijk[1] + n2 * ijk[2]);
+                    for (int v = 0; v < NV; ++v) {
+                        double s = 0.0;
+                        for (int a = 0; a < nd; ++a) s += __ldg(&T[ic * nd + a]) * Rs[v * n + base + a * stride];
+                        tmax = fmax(tmax, fabs(scale * (s + acc[it][v])));
+                    }
+                }
+            }
+            tmax = block_max(tmax, red);
+            if (tid == 0) P.tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV + p] = tmax;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Map, extrapolation and selection (
+// readings A12-A16).  One thread per element.
+// ---------------------------------------------------------------------------
+
+struct SelParams {
+    const double* tau;
+    const int* orders;
+    double* total;     // [E][K^3] (static modes)
+    int* sel;          // [E][3]
+    double* margin;    // [E]
+    int E;
+    int mode;
+    double tau_max;
+    int Nmin, Nmax, dec_cap;
+};
+
+__device__ void directional_estimate(int Nd, const double* td, double* hat /* [NP+1] indexed by n */)
+{
+    const double SENT = 1e30;
+    const double eps = 1e-13 * fmax(1.0, td[0]);
+    double tmax = 0.0;
+    for (int p = 1; p < Nd; ++p) tmax = fmax(tmax, td[p]);
+    if (Nd <= 1) {  // not estimable: keep the order
+        for (int m = 1; m <= NMAX; ++m) hat[m] = (m == Nd) ? 0.0 : SENT;
+        return;
+    }
+    if (tmax <= eps) {  // resolved direction (A14)
+        for (int m = 1; m <= NMAX; ++m) hat[m] = 0.0;
+        return;
+    }
+    bool asym = false;
+    double a = 0.0, b = 0.0;
+    if (Nd >= 3) {  // ordinary least squares of log10 tau_d(p) on p (A13)
+        const int K = Nd - 1;
+        double sp = 0.0, sy = 0.0, spp = 0.0, spy = 0.0;
+        for (int p = 1; p < Nd; ++p) {
+            const double y = log10(fmax(td[p], 1e-300));
+            sp += p;
+            sy += y;
+            spp += (double)p * p;
+            spy += p * y;
+        }
+        b = (K * spy - sp * sy) / (K * spp - sp * sp);
+        a = (sy - b * sp) / K;
+        asym = b < 0.0;
+    }
+    for (int m = 1; m <= NMAX; ++m) {
+        if (m < Nd) hat[m] = td[m];
+        else hat[m] = asym ? pow(10.0, a + b * m) : SENT;
+    }
+}
+
+__global__ void k_select(SelParams P)
+{
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= P.E) return;
+    double hat[3][NP + 1];
+    int Ne[3];
+    for (int d = 0; d < 3; ++d) {
+        Ne[d] = P.orders[3 * e + d];
+        directional_estimate(Ne[d], P.tau + (3 * (long long)e + d) * DG_TAU_STRIDE_DEV, hat[d]);
+    }
+    const int Nmin = P.Nmin, Nmax = P.Nmax, K = Nmax - Nmin + 1;
+    double* tot = P.total ? P.total + (long long)e * K * K * K : nullptr;
+    if (P.mode != 0) {  // approach 2, F_max: running max of the maps (eq totalTruncMap)
+        for (int n3 = Nmin; n3 <= Nmax; ++n3)
+            for (int n2 = Nmin; n2 <= Nmax; ++n2)
+                for (int n1 = Nmin; n1 <= Nmax; ++n1) {
+                    const int ix = (n1 - Nmin) + K * ((n2 - Nmin) + K * (n3 - Nmin));
+                    tot[ix] = fmax(tot[ix], hat[0][n1] + hat[1][n2] + hat[2][n3]);
+                }
+        if (P.mode == 1) return;
+    }
+    int best[3] = {Nmax, Nmax, Nmax};
+    long bestp = -1, bests = 0;
+    double mg = INFINITY;
+    for (int n1 = Nmin; n1 <= Nmax; ++n1)
+        for (int n2 = Nmin; n2 <= Nmax; ++n2)
+            for (int n3 = Nmin; n3 <= Nmax; ++n3) {
+                const double v = P.mode == 0 ? hat[0][n1] + hat[1][n2] + hat[2][n3]
+                                             : tot[(n1 - Nmin) + K * ((n2 - Nmin) + K * (n3 - Nmin))];
+                mg = fmin(mg, fabs(v - P.tau_max) / P.tau_max);
+                if (!(v < P.tau_max)) continue;
+                const long pr = (long)(n1 + 1) * (n2 + 1) * (n3 + 1), sm = n1 + n2 + n3;
+                if (bestp < 0 || pr < bestp || (pr == bestp && sm < bests)) {
+                    bestp = pr;
+                    bests = sm;
+                    best[0] = n1; best[1] = n2; best[2] = n3;
+                }
+            }
+    if (P.mode == 0)  // decrease cap
+        for (int d = 0; d < 3; ++d) best[d] = max(best[d], Ne[d] - P.dec_cap);
+    for (int d = 0; d < 3; ++d) P.sel[3 * e + d] = best[d];
+    if (P.margin) P.margin[e] = mg;
+}
+
+// Jump condition (eqs N23 / N_1): one Jacobi sweep of the monotone fixpoint.
+__global__ void k_jump(const int* nbr, const int* in, int* out, int E, int rule, int Nmax, int* changed)
+{
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    for (int d = 0; d < 3; ++d) {
+        const int cur = in[3 * e + d];
+        int v = cur;
+        for (int f = 0; f < 6; ++f) {
+            const int j = nbr[6 * e + f];
+            if (j < 0) continue;
+            const int x = in[3 * j + d];
+            const int r = rule == 0 ? (2 * x) / 3 : x - 1;
+            v = max(v, r);
+        }
+        v = max(cur, min(v, Nmax));
+        out[3 * e + d] = v;
+        if (v != cur) atomicOr(changed, 1);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Transfer: q_new = T_z T_y T_x q_old per element.
+// ---------------------------------------------------------------------------
+
+struct TransferParams {
+    const double* qold;
+    double* qnew;
+    const int* oold;
+    const int* onew;
+    const long long* offold;
+    const long long* offnew;
+    const Tables* tab;
+};
+
+__global__ void __launch_bounds__(BLOCK) k_transfer(TransferParams P)
+{
+    extern __shared__ double sm[];
+    const int e = blockIdx.x;
+    int A[3], B[3];
+    for (int d = 0; d < 3; ++d) { A[d] = P.oold[3 * e + d] + 1; B[d] = P.onew[3 * e + d] + 1; }
+    const int nA = A[0] * A[1] * A[2];
+    const int n1 = B[0] * A[1] * A[2], n2 = B[0] * B[1] * A[2], nB = B[0] * B[1] * B[2];
+    double* s0 = sm;
+    double* s1 = s0 + NV * NP * NP * NP;
+    double* s2 = s1 + NV * NP * NP * NP;
+    const long long oa = P.offold[e], ob = P.offnew[e];
+    for (int t = threadIdx.x; t < NV * nA; t += blockDim.x) s0[t] = P.qold[oa + t];
+    __syncthreads();
+    const double* Tx = P.tab->T[A[0] - 1][B[0] - 1];
+    for (int t = threadIdx.x; t < NV * n1; t += blockDim.x) {
+        const int v = t / n1, r = t % n1;
+        const int i = r % B[0], jk = r / B[0];
+        double s = 0.0;
+        for (int a = 0; a < A[0]; ++a) s += Tx[i * A[0] + a] * s0[v * nA + a + A[0] * jk];
+        s1[t] = s;
+    }
+    __syncthreads();
+    const double* Ty = P.tab->T[A[1] - 1][B[1] - 1];
+    for (int t = threadIdx.x; t < NV * n2; t += blockDim.x) {
+        const int v = t / n2, r = t % n2;
+        const int i = r % B[0], j = (r / B[0]) % B[1], k = r / (B[0] * B[1]);
+        double s = 0.0;
+        for (int b = 0; b < A[1]; ++b) s += Ty[j * A[1] + b] * s1[v * n1 + i + B[0] * (b + A[1] * k)];
+        s2[t] = s;
+    }
+    __syncthreads();
+    const double* Tz = P.tab->T[A[2] - 1][B[2] - 1];
+    for (int t = threadIdx.x; t < NV * nB; t += blockDim.x) {
+        const int v = t / nB, r = t % nB;
+        const int ij = r % (B[0] * B[1]), k = r / (B[0] * B[1]);
+        double s = 0.0;
+        for (int c = 0; c < A[2]; ++c) s += Tz[k * A[2] + c] * s2[v * n2 + ij + B[0] * B[1] * c];
+        P.qnew[ob + t] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Diagnostics: sum over nodes of (J w w w) v per variable; min rho, min p.
+// ---------------------------------------------------------------------------
+
+struct DiagParams {
+    const double* q;
+    const double* v;
+    const int* orders;
+    const long long* off;
+    const double* hgeo;
+    const Tables* tab;
+    double gamma;
+    double* sums;                  // [5]
+    unsigned long long* minbits;   // [2] (as ordered bits of positive doubles; negative -> 0)
+    int* neg;                      // count of non-positive rho/p
+};
+
+__global__ void __launch_bounds__(BLOCK) k_diag(DiagParams P)
+{
+    const int e = blockIdx.x;
+    int N[3] = {P.orders[3 * e], P.orders[3 * e + 1], P.orders[3 * e + 2]};
+    const int n1 = N[0] + 1, n2 = N[1] + 1, n = n1 * n2 * (N[2] + 1);
+    const long long o = P.off[e];
+    const double J = P.hgeo[3 * e] * P.hgeo[3 * e + 1] * P.hgeo[3 * e + 2] / 8.0;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        int i, j, k;
+        node_ijk(t, n1, n2, i, j, k);
+        const double m = J * P.tab->w[N[0]][i] * P.tab->w[N[1]][j] * P.tab->w[N[2]][k];
+        if (P.v)
+            for (int v = 0; v < NV; ++v) atomicAdd(&P.sums[v], m * P.v[o + (long long)v * n + t]);
+        double q[NV];
+        for (int v = 0; v < NV; ++v) q[v] = P.q[o + (long long)v * n + t];
+        const double p = (P.gamma - 1.0) * (q[4] - 0.5 * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]) / q[0]);
+        if (!(q[0] > 0.0) || !(p > 0.0)) atomicAdd(P.neg, 1);
+        else {
+            atomicMin(&P.minbits[0], (unsigned long long)__double_as_longlong(q[0]));
+            atomicMin(&P.minbits[1], (unsigned long long)__double_as_longlong(p));
+        }
+    }
+}
+
+}  // namespace dgtau

@@ -1,0 +1,254 @@
+"""GPU (C-ABI) vs CPU oracle parity, element by element on the same seeded
+inputs (BASELINE.json north_star tolerances: relative L_inf 1e-11 on
+residuals and RK states, 1e-9 on tau, exact integer orders)."""
+import math
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+RES_TOL = 1e-11
+TAU_TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def dg():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2210_03523_b200 as m
+
+    m.build()
+    return m
+
+
+def per_var(a, orders):
+    """list of 5 arrays: variable v over all nodes (canonical layout)."""
+    off = W.offsets(orders)
+    out = [[] for _ in range(5)]
+    for e in range(len(orders)):
+        n = (off[e + 1] - off[e]) // 5
+        blk = a[off[e]:off[e + 1]].reshape(5, n)
+        for v in range(5):
+            out[v].append(blk[v])
+    return [np.concatenate(x) for x in out]
+
+
+def rel_linf(gpu, orc, orders):
+    """max over variables of ||gpu_v - orc_v||_inf / ||orc_v||_inf."""
+    g, o = per_var(gpu, orders), per_var(orc, orders)
+    worst = 0.0
+    for v in range(5):
+        den = np.abs(o[v]).max()
+        num = np.abs(g[v] - o[v]).max()
+        worst = max(worst, num / den if den > 0 else num)
+    return worst
+
+
+def setup(dg, orc, mesh, orders, ic="pulse", **kw):
+    import torch
+
+    P = orc.Problem(mesh)
+    X = P.node_coords(orders)
+    if ic == "pulse":
+        q = W.pulse_state(X, orders, **kw)
+    else:
+        q = W.uniform_state(orders)
+    S = dg.Solver(mesh)
+    S.set_orders(orders)
+    return P, S, q, torch.from_numpy(q).cuda()
+
+
+CASES = {
+    "cfg1": lambda: (W.cube_mesh(4), W.orders_uniform(64, 3), dict(sigma=0.1)),
+    "cfg2_uniform6": lambda: (W.cube_mesh(16), W.orders_uniform(4096, 6), dict(center=W.cfg2_center(), sigma=0.08)),
+    "cfg3_subbox_mixed": lambda: (W.cube_mesh(8), W.orders_random(512, 2, 7, 3), dict(sigma=0.1)),
+    "ragged_1to8": lambda: (W.cube_mesh(5, 3, 2), W.orders_random(30, 1, 8, 9), dict(sigma=0.2)),
+    "single_element": lambda: (W.cube_mesh(1), np.array([[8, 5, 1]], np.int32), dict(sigma=0.3)),
+    "all_order1": lambda: (W.cube_mesh(6), W.orders_uniform(216, 1), dict(sigma=0.2)),
+    "all_order8": lambda: (W.cube_mesh(3), W.orders_uniform(27, 8), dict(sigma=0.15)),
+}
+
+
+@pytest.mark.parametrize("case", list(CASES))
+@pytest.mark.parametrize("variant", [0, 1])
+def test_rhs_parity(dg, orc, case, variant):
+    mesh, orders, kw = CASES[case]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, **kw)
+    r = S.rhs_eval(qd, variant=variant).cpu().numpy()
+    ro = P.rhs(orders, q, variant)
+    assert rel_linf(r, ro, orders) < RES_TOL
+
+
+@pytest.mark.parametrize("case", ["cfg3_subbox_mixed", "ragged_1to8"])
+def test_freestream_and_conservation_gpu(dg, orc, case):
+    import torch
+
+    mesh, orders, kw = CASES[case]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, ic="uniform")
+    r = S.rhs_eval(qd).cpu().numpy()
+    assert np.abs(r).max() < 1e-11
+    _, _, q, qd = setup(dg, orc, mesh, orders, **kw)
+    r = S.rhs_eval(qd)
+    sums, mn = S.diagnostics(qd, r)
+    M = P.mass(orders)
+    ab = np.zeros(5)
+    for v, arr in enumerate(per_var(r.cpu().numpy(), orders)):
+        ab[v] = np.abs(arr * M).sum()
+    assert np.all(np.abs(sums) < 1e-13 * ab)
+    assert mn[0] > 0.9 and mn[1] > 0.9
+
+
+def test_rk3_cfg1_trajectory(dg, orc):
+    """cfg1 [B:7]: 10 RK3 steps at CFL 0.5 (dt recomputed each step)."""
+    import torch
+
+    mesh, orders, kw = CASES["cfg1"]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, **kw)
+    qa, qb, g = qd.clone(), torch.empty_like(qd), torch.empty_like(qd)
+    qo = q.copy()
+    for step in range(10):
+        dto = P.dt(orders, qo, 0.5)
+        dtg = S.compute_dt(qa, 0.5, sync=True)
+        assert abs(dtg - dto) <= 4e-16 * dto
+        S.rk_step(qa, qb, g, S._dt)
+        qa, qb = qb, qa
+        qo = P.rk3_step(orders, qo, dto)
+    assert rel_linf(qa.cpu().numpy(), qo, orders) < RES_TOL
+
+
+def test_rk3_mixed_orders(dg, orc):
+    import torch
+
+    mesh, orders, kw = CASES["ragged_1to8"]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, **kw)
+    qa, qb, g = qd.clone(), torch.empty_like(qd), torch.empty_like(qd)
+    qo = q.copy()
+    dt = torch.tensor([2e-4], dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        S.rk_step(qa, qb, g, dt)
+        qa, qb = qb, qa
+        qo = P.rk3_step(orders, qo, 2e-4)
+    assert rel_linf(qa.cpu().numpy(), qo, orders) < RES_TOL
+
+
+def tau_rel(tg, to):
+    ok = np.isfinite(to)
+    assert np.array_equal(ok, np.isfinite(tg))
+    worst = 0.0
+    for d in range(3):
+        m = ok[:, d, 1:]
+        if not m.any():
+            continue
+        a, b = tg[:, d, 1:][m], to[:, d, 1:][m]
+        worst = max(worst, np.abs(a - b).max() / np.abs(b).max())
+    # slot 0 = ||Qdot_ref||_inf
+    worst = max(worst, np.abs(tg[:, :, 0] - to[:, :, 0]).max() / np.abs(to[:, :, 0]).max())
+    return worst
+
+
+@pytest.mark.parametrize("case", ["cfg1", "cfg2_uniform6", "cfg3_subbox_mixed", "ragged_1to8", "all_order8"])
+@pytest.mark.parametrize("ref", ["solver", "same"])
+@pytest.mark.parametrize("form", [0, 1])
+def test_tau_parity(dg, orc, case, ref, form):
+    mesh, orders, kw = CASES[case]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, **kw)
+    if ref == "solver":
+        rg = S.rhs_eval(qd)
+        tg = S.tau_estimate(qd, rg, formulation=form, reference=dg.REF_SOLVER).cpu().numpy()
+        to = P.tau_estimate(orders, q, P.rhs(orders, q), form)
+    else:
+        tg = S.tau_estimate(qd, None, formulation=form, reference=dg.REF_SAME).cpu().numpy()
+        to = P.tau_estimate(orders, q, P.rhs(orders, q, orc.ISOLATED), form)
+    assert tau_rel(tg, to) < TAU_TOL
+
+
+@pytest.mark.parametrize("case", ["cfg2_uniform6", "cfg3_subbox_mixed", "ragged_1to8"])
+@pytest.mark.parametrize("rule", [0, 1])
+def test_select_dynamic_exact(dg, orc, case, rule):
+    """Selection parity on identical tau input (the oracle's), exact."""
+    import torch
+
+    mesh, orders, kw = CASES[case]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, **kw)
+    to = P.tau_estimate(orders, q, P.rhs(orders, q))
+    Nmin, Nmax = (3, 8) if case == "cfg2_uniform6" else (1, 8)
+    for tmax in (1e-2, 1e-4):
+        sel_o, mg_o = orc.select_dynamic(orders, to, mesh.nbr, tmax, Nmin, Nmax, rule=rule, cap=1)
+        sel_g, mg_g = S.select_orders(torch.from_numpy(to).cuda(), tmax, Nmin, Nmax, mode=dg.SELECT_DYNAMIC,
+                                      jump_rule=rule, dec_cap=1)
+        assert np.array_equal(sel_g, sel_o)
+        assert np.allclose(mg_g, mg_o, rtol=1e-12, atol=0)
+
+
+def test_select_static_exact(dg, orc):
+    import torch
+
+    mesh, orders, kw = CASES["cfg3_subbox_mixed"]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, **kw)
+    Nmin, Nmax = 2, 8
+    K = Nmax - Nmin + 1
+    total_o = np.zeros((mesh.E, K, K, K))
+    total_g = torch.zeros((mesh.E, K, K, K), dtype=torch.float64, device="cuda")
+    qo = q.copy()
+    for s in range(3):  # three estimation stages, F_max (approach 2)
+        to = P.tau_estimate(orders, qo, P.rhs(orders, qo))
+        mp, _ = orc.build_map(orders, to, Nmin, Nmax)
+        total_o = orc.combine_max(total_o, mp)
+        S.select_orders(torch.from_numpy(to).cuda(), 1e-3, Nmin, Nmax, mode=dg.SELECT_STATIC_ACCUM,
+                        total_map=total_g)
+        qo = P.rk3_step(orders, qo, 2e-3)
+    assert np.array_equal(total_g.cpu().numpy(), total_o)
+    sel_o, _ = orc.select_from_map(total_o, Nmin, Nmax, 1e-3)
+    sel_o, _ = orc.jump_fixpoint(mesh.nbr, sel_o, orc.JUMP_B, Nmax)
+    dummy = torch.zeros((mesh.E, 3, 9), dtype=torch.float64, device="cuda")
+    # FINAL: pass a stage whose map is all zeros -> total unchanged
+    dummy[:, :, 0] = 1.0
+    dummy[:, :, 1:] = 0.0
+    sel_g, _ = S.select_orders(dummy, 1e-3, Nmin, Nmax, mode=dg.SELECT_STATIC_FINAL, total_map=total_g)
+    assert np.array_equal(sel_g, sel_o)
+
+
+def test_transfer_parity(dg, orc):
+    mesh, orders, kw = CASES["ragged_1to8"]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, **kw)
+    new = W.orders_random(mesh.E, 1, 8, 77)
+    qn = S.transfer(new, qd).cpu().numpy()
+    qo = orc.transfer(orders, q, new)
+    assert rel_linf(qn, qo, new) < 1e-13
+
+
+def test_dynamic_adaptation_cycle_cfg2_like(dg, orc):
+    """Dynamic loop (Fig. 1) on a cfg2-like problem at reduced
+    size: advance, estimate (SOLVER ref), select, transfer; orders exact and
+    states within tolerance through two adaptations."""
+    import torch
+
+    mesh = W.cube_mesh(6)
+    orders = W.orders_uniform(mesh.E, 6)
+    P, S, q, qd = setup(dg, orc, mesh, orders, center=(0.45, 0.5, 0.55), sigma=0.12)
+    qo = q.copy()
+    for stage in range(2):
+        qa, qb, g = qd.clone(), torch.empty_like(qd), torch.empty_like(qd)
+        for _ in range(5):
+            dto = P.dt(orders, qo, 0.5)
+            S.compute_dt(qa, 0.5)
+            S.rk_step(qa, qb, g, S._dt)
+            qa, qb = qb, qa
+            qo = P.rk3_step(orders, qo, dto)
+        assert rel_linf(qa.cpu().numpy(), qo, orders) < RES_TOL
+        to = P.tau_estimate(orders, qo, P.rhs(orders, qo))
+        tg = S.tau_estimate(qa, S.rhs_eval(qa))
+        assert tau_rel(tg.cpu().numpy(), to) < TAU_TOL
+        sel_o, _ = orc.select_dynamic(orders, to, mesh.nbr, 1e-4, 3, 8, rule=1, cap=1)
+        sel_g, _ = S.select_orders(torch.from_numpy(to).cuda(), 1e-4, 3, 8)
+        assert np.array_equal(sel_g, sel_o)
+        qd = S.transfer(sel_g, qa)
+        qo = orc.transfer(orders, qo, sel_o)
+        orders = sel_o
+        S.set_orders(orders)
+        assert rel_linf(qd.cpu().numpy(), qo, orders) < RES_TOL
