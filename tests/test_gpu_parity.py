@@ -114,7 +114,7 @@ def test_rk3_cfg1_trajectory(dg, orc):
     for step in range(10):
         dto = P.dt(orders, qo, 0.5)
         dtg = S.compute_dt(qa, 0.5, sync=True)
-        assert abs(dtg - dto) <= 4e-16 * dto
+        assert abs(dtg - dto) <= 1e-14 * dto  # a few ulp (different reduction order)
         S.rk_step(qa, qb, g, S._dt)
         qa, qb = qb, qa
         qo = P.rk3_step(orders, qo, dto)
