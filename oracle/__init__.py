@@ -31,10 +31,16 @@ NMAX = 16
 
 
 def build(force: bool = False) -> str:
+    import hashlib
+
     hdr = os.path.join(_HERE, "dgsem_oracle.h")
-    stale = not os.path.exists(_SO) or max(os.path.getmtime(_SRC), os.path.getmtime(hdr)) > os.path.getmtime(_SO)
-    if force or stale:
+    dig = hashlib.sha1(open(_SRC, "rb").read() + open(hdr, "rb").read()).hexdigest()
+    stamp = _SO + ".stamp"
+    fresh = os.path.exists(_SO) and os.path.exists(stamp) and open(stamp).read().strip() == dig
+    if force or not fresh:
         subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", _SO, _SRC, "-lm"])
+        with open(stamp, "w") as f:
+            f.write(dig)
     return _SO
 
 

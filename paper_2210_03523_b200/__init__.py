@@ -44,16 +44,52 @@ def sources():
         [os.path.join(_INC, "dgtau.h")]
 
 
+def _digest(srcs):
+    import hashlib
+
+    h = hashlib.sha1()
+    for s in srcs:
+        h.update(os.path.basename(s).encode())
+        h.update(open(s, "rb").read())
+    h.update(" ".join(NVCC_FLAGS).encode())
+    return h.hexdigest()
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile libdgtau.so for sm_100a with nvcc (cross-compiles without a GPU)."""
+    """Compile libdgtau.so for sm_100a with nvcc (cross-compiles without a GPU).
+    Skipped when the library's stamp matches the sources' content hash."""
     srcs = sources()
-    stale = not os.path.exists(_SO) or max(os.path.getmtime(s) for s in srcs) > os.path.getmtime(_SO)
-    if force or stale:
-        cmd = ["nvcc", *NVCC_FLAGS, "-o", _SO, os.path.join(_CSRC, "dgtau.cu"), os.path.join(_CSRC, "basis.cpp")]
-        if verbose:
-            cmd.insert(1, "-Xptxas=-v")
-        subprocess.check_call(cmd)
+    stamp = _SO + ".stamp"
+    dig = _digest(srcs)
+    fresh = os.path.exists(_SO) and os.path.exists(stamp) and open(stamp).read().strip() == dig
+    if force or not fresh:
+        _compile(srcs, verbose)
+        with open(stamp, "w") as f:
+            f.write(dig)
     return _SO
+
+
+def _compile(srcs, verbose=False, force_all=False):
+    """Objects in parallel (the 8 order-specialised units dominate), then link."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    objdir = os.path.join(_HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    units = [s for s in srcs if s.endswith((".cu", ".cpp"))]
+    hdr_t = max(os.path.getmtime(s) for s in srcs if s.endswith((".cuh", ".h")))
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        if not force_all and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(src), hdr_t):
+            return obj
+        cmd = ["nvcc", *cflags, "-c", src, "-o", obj] + (["-Xptxas=-v"] if verbose else [])
+        subprocess.check_call(cmd)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(one, units))
+    subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", _SO, *objs])
 
 
 class DGError(RuntimeError):

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -17,8 +18,24 @@
 #include "../../include/dgtau.h"
 #include "basis.h"
 #include "kernels.cuh"
+#include "residual_t.cuh"
 
 using namespace dgtau;
+
+namespace dgtau {
+cudaError_t res_setup_1(const Tables*, res_launcher (*)[NP][NP]);
+cudaError_t res_setup_2(const Tables*, res_launcher (*)[NP][NP]);
+cudaError_t res_setup_3(const Tables*, res_launcher (*)[NP][NP]);
+cudaError_t res_setup_4(const Tables*, res_launcher (*)[NP][NP]);
+cudaError_t res_setup_5(const Tables*, res_launcher (*)[NP][NP]);
+cudaError_t res_setup_6(const Tables*, res_launcher (*)[NP][NP]);
+cudaError_t res_setup_7(const Tables*, res_launcher (*)[NP][NP]);
+cudaError_t res_setup_8(const Tables*, res_launcher (*)[NP][NP]);
+}  // namespace dgtau
+
+struct Bucket {
+    int ord, item0, nitems;
+};
 
 struct dg_ctx {
     std::string err;
@@ -57,6 +74,9 @@ struct dg_ctx {
     double* d_margin = nullptr;               // [E]
     double* d_sums = nullptr;                 // [5]
     long long launches = 0;
+    std::vector<Bucket> buckets;
+    res_launcher rtab[NP][NP][NP] = {};
+    bool generic = false;  // DGTAU_GENERIC=1: runtime-order residual kernel (A/B testing)
 };
 
 namespace {
@@ -156,8 +176,17 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         dg_destroy(ctx);
         return s;
     }
-    if (params->physics == DG_NS) {
-        ctx->err = "Navier-Stokes path not in this build";
+    {
+        typedef cudaError_t (*setup_fn)(const Tables*, res_launcher (*)[NP][NP]);
+        const setup_fn fns[8] = {res_setup_1, res_setup_2, res_setup_3, res_setup_4,
+                                 res_setup_5, res_setup_6, res_setup_7, res_setup_8};
+        for (int i = 0; i < 8; ++i)
+            if ((s = cuda_check(ctx, fns[i](&t, ctx->rtab), "residual setup")) != DG_OK) {
+                dg_destroy(ctx);
+                return s;
+            }
+        const char* g = getenv("DGTAU_GENERIC");
+        ctx->generic = g && g[0] == '1';
     }
     // large dynamic shared memory for the element kernels
     cudaFuncSetAttribute(k_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -269,7 +298,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
         const int ord = kv.first;
         const int N[3] = {ord & 255, (ord >> 8) & 255, (ord >> 16) & 255};
         const int n = npts(N);
-        const int k = std::max(1, std::min(MAXSLOTS, BLOCK / n));
+        const int k = std::max(1, std::min(MAXSLOTS, 512 / n));  // = Shape<N>::CNT
         const int nfs = 2 * ((N[1] + 1) * (N[2] + 1) + (N[0] + 1) * (N[2] + 1) + (N[0] + 1) * (N[1] + 1));
         for (size_t i = 0; i < kv.second.size(); i += k) {
             WorkItem w;
@@ -283,7 +312,13 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
             smem = std::max(smem, bytes);
         }
     }
-    std::stable_sort(work.begin(), work.end(), [](const WorkItem& a, const WorkItem& b) { return a.pad < b.pad; });
+    // items are grouped per bucket (one specialised launch each), element order inside
+    ctx->buckets.clear();
+    for (size_t i = 0; i < work.size(); ++i) {
+        if (ctx->buckets.empty() || ctx->buckets.back().ord != work[i].ord)
+            ctx->buckets.push_back(Bucket{work[i].ord, (int)i, 0});
+        ctx->buckets.back().nitems++;
+    }
     ctx->nwork = (int)work.size();
     ctx->res_smem = smem;
     // mortar faces: + side of L against - side of R, tangential orders differ
@@ -387,8 +422,15 @@ static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, doub
     P.tab = ctx->d_tab;
     P.ph = phys_dev(ctx->prm);
     P.flag = ctx->d_flag;
-    k_residual<<<ctx->nwork, BLOCK, ctx->res_smem, st>>>(P);
-    ctx->launches++;
+    if (ctx->generic) {
+        k_residual<<<ctx->nwork, BLOCK, ctx->res_smem, st>>>(P);
+        ctx->launches++;
+    } else {
+        for (const Bucket& b : ctx->buckets) {
+            ctx->rtab[b.ord & 255][(b.ord >> 8) & 255][(b.ord >> 16) & 255](P, b.item0, b.nitems, st);
+            ctx->launches++;
+        }
+    }
     return check_stream_error(ctx, "k_residual launch");
 }
 

@@ -1,0 +1,320 @@
+// residual_t.cuh -- order-specialised fused DGSEM residual / RK-stage kernel.
+//
+// One template instance per (N1,N2,N3) bucket; a CTA processes CNT elements of
+// that bucket (work items of the plan, spatially ordered).  Same numerics as
+// the generic path (strong-form GL-DGSEM, see kernels.cuh header; PAPER.md
+// P:129-155), arranged for the sm_100a fp64 pipes:
+//   * element state read once from HBM into registers of node-owner threads
+//     (ir = 1/rho and p computed once per node);
+//   * per direction d the node owners write f_d to shared memory, then one
+//     thread per (line, variable) holds the line in registers and applies
+//     D^{N_d} with compile-time loops; D comes from __constant__ memory with
+//     compile-time offsets (constant-bank operands of DFMA);
+//   * surface: one thread per (face, face point), packed over the 6 faces of
+//     all CTA elements; Roe flux with the neighbour trace read from L2;
+//     (G - f_own) * lifting scale goes to shared memory;
+//   * epilogue per node: Qdot = -(volume + lifting), or the Williamson
+//     low-storage update g <- A g + dt Qdot, q' <- q + B g.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace dgtau {
+
+// D^{N}[a][m] at c_D[N*NP*NP + a*(N+1) + m] and GL weights; one private copy
+// per translation unit (internal linkage), filled by res_setup_* at startup.
+static __constant__ double c_D[NP * NP * NP];
+static __constant__ double c_w[NP][NP];
+
+__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+
+template <int N1, int N2, int N3>
+struct Shape {
+    static constexpr int n1 = N1 + 1, n2 = N2 + 1, n3 = N3 + 1;
+    static constexpr int n = n1 * n2 * n3;
+    static constexpr int CNT = cmax(1, cmin(MAXSLOTS, 512 / n));
+    static constexpr int T = CNT * n;
+    static constexpr int NPT = (T + 255) / 256;
+    static constexpr int BS = ((T + NPT - 1) / NPT + 31) / 32 * 32;
+    static constexpr int nf0 = n2 * n3, nf1 = n1 * n3, nf2 = n1 * n2;
+    static constexpr int FS = 2 * (nf0 + nf1 + nf2);
+    static constexpr size_t smem_bytes = sizeof(double) * (size_t)(2 * NV * T + NV * CNT * FS);
+};
+
+// f . e_d for the Euler flux, from q with precomputed 1/rho and p
+template <int d>
+__device__ __forceinline__ void flux_axis(const double* q, double ir, double p, double* f)
+{
+    const double ud = q[1 + d] * ir;
+    f[0] = q[1 + d];
+    f[1] = q[1] * ud;
+    f[2] = q[2] * ud;
+    f[3] = q[3] * ud;
+    f[1 + d] += p;
+    f[4] = (q[4] + p) * ud;
+}
+
+// Euler flux along a unit normal given as three scalars (no dynamic indexing)
+__device__ __forceinline__ void flux_normal(const double* q, double nx, double ny, double nz, double gm1, double* f)
+{
+    const double ir = 1.0 / q[0];
+    const double p = gm1 * (q[4] - 0.5 * ir * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]));
+    const double un = (q[1] * nx + q[2] * ny + q[3] * nz) * ir;
+    f[0] = q[0] * un;
+    f[1] = q[1] * un + p * nx;
+    f[2] = q[2] * un + p * ny;
+    f[3] = q[3] * un + p * nz;
+    f[4] = (q[4] + p) * un;
+}
+
+template <int L, int d>
+__device__ __forceinline__ void dmul_line(const double* Fl, int stride, double sc, double* out)
+{
+    constexpr int DO = (L - 1) * NP * NP;  // offset of D^{L-1}
+    double v[L];
+#pragma unroll
+    for (int m = 0; m < L; ++m) v[m] = Fl[m * stride];
+#pragma unroll
+    for (int a = 0; a < L; ++a) {
+        double s = 0.0;
+#pragma unroll
+        for (int m = 0; m < L; ++m) s = fma(c_D[DO + a * L + m], v[m], s);
+        out[a] = sc * s;
+    }
+}
+
+template <int N1, int N2, int N3>
+__global__ void __launch_bounds__(Shape<N1, N2, N3>::BS) k_res_t(ResParams P, int item0)
+{
+    using S = Shape<N1, N2, N3>;
+    constexpr int n = S::n, n1 = S::n1, n2 = S::n2, n3 = S::n3, BS = S::BS, NPTT = S::NPT, FS = S::FS;
+    constexpr int T = S::T;
+    extern __shared__ double sm[];
+    double* F = sm;               // [slot][v][node]  one direction's flux
+    double* A = F + NV * T;       // [slot][v][node]  volume accumulator
+    double* Gs = A + NV * T;      // [slot][v][face point]  lifting terms
+    __shared__ long long s_off[S::CNT];
+    __shared__ int s_e[S::CNT];
+    __shared__ double s_sc[S::CNT][3];
+
+    const WorkItem w = P.work[item0 + blockIdx.x];
+    const int cnt = w.count;
+    const int tid = threadIdx.x;
+    if (tid < cnt) {
+        const int e = P.elist[w.start + tid];
+        s_e[tid] = e;
+        s_off[tid] = P.off[e];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) s_sc[tid][d] = 2.0 / P.hgeo[3 * e + d];
+    }
+    __syncthreads();
+    const double gm1 = P.ph.gm1;
+    const int ntot = cnt * n;
+
+    // ---- node owners: state into registers ------------------------------
+    double q[NPTT][NV], ir[NPTT], pr[NPTT];
+#pragma unroll
+    for (int it = 0; it < NPTT; ++it) {
+        const int t = tid + it * BS;
+        if (t < ntot) {
+            const int slot = t / n, node = t - slot * n;
+            const double* qe = P.q + s_off[slot] + node;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) q[it][v] = qe[v * n];
+            ir[it] = 1.0 / q[it][0];
+            pr[it] = gm1 * (q[it][4] - 0.5 * ir[it] * (q[it][1] * q[it][1] + q[it][2] * q[it][2] + q[it][3] * q[it][3]));
+            if (!(q[it][0] > 0.0 && pr[it] > 0.0)) {
+                if (atomicAdd(P.flag, 1) == 0) P.flag[1] = s_e[slot];
+            }
+        } else {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) q[it][v] = 0.0;
+            ir[it] = 0.0;
+            pr[it] = 0.0;
+        }
+    }
+
+    // ---- surface terms (non-isolated): Gs = +-(G - f_own) 2/(h_d w_end) ---
+    if (P.variant == 0) {
+        for (int t = tid; t < cnt * FS; t += BS) {
+            const int slot = t / FS;
+            const int r = t - slot * FS;
+            int f, pt;
+            if (r < 2 * S::nf0) { f = r < S::nf0 ? 0 : 1; pt = r - f * S::nf0; }
+            else if (r < 2 * (S::nf0 + S::nf1)) {
+                const int r1 = r - 2 * S::nf0;
+                f = r1 < S::nf1 ? 2 : 3;
+                pt = r1 - (f - 2) * S::nf1;
+            } else {
+                const int r2 = r - 2 * (S::nf0 + S::nf1);
+                f = r2 < S::nf2 ? 4 : 5;
+                pt = r2 - (f - 4) * S::nf2;
+            }
+            const int d = f >> 1, s = f & 1;
+            // own boundary node (i,j,k) and lifting scale
+            int i, j, k, Nd;
+            if (d == 0) { i = s ? N1 : 0; j = pt % n2; k = pt / n2; Nd = N1; }
+            else if (d == 1) { i = pt % n1; j = s ? N2 : 0; k = pt / n1; Nd = N2; }
+            else { i = pt % n1; j = pt / n1; k = s ? N3 : 0; Nd = N3; }
+            const int node = i + n1 * (j + n2 * k);
+            const int e = s_e[slot];
+            const double* qe = P.q + s_off[slot] + node;
+            double qo[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) qo[v] = qe[v * n];
+            const double nx = d == 0 ? 1.0 : 0.0, ny = d == 1 ? 1.0 : 0.0, nz = d == 2 ? 1.0 : 0.0;
+            double fo[NV], G[NV];
+            flux_normal(qo, nx, ny, nz, gm1, fo);
+            const int nb = P.nbr[6 * e + f];
+            const double nrm[3] = {nx, ny, nz};
+            if (nb < 0) {
+                double qg[NV];
+                ghost_state(qo, nb, P.ph, qg);
+                if (s) riemann(qo, qg, nrm, P.ph, G); else riemann(qg, qo, nrm, P.ph, G);
+            } else {
+                const long long mo = P.moff[6 * e + f];
+                if (mo >= 0) {
+                    const int nfd = d == 0 ? S::nf0 : (d == 1 ? S::nf1 : S::nf2);
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) G[v] = P.mortarG[mo + (long long)v * nfd + pt];
+                } else {
+                    const int B1 = P.orders[3 * nb] + 1, B2 = P.orders[3 * nb + 1] + 1, B3 = P.orders[3 * nb + 2] + 1;
+                    int ib = i, jb = j, kb = k;
+                    if (d == 0) ib = s ? 0 : B1 - 1;
+                    else if (d == 1) jb = s ? 0 : B2 - 1;
+                    else kb = s ? 0 : B3 - 1;
+                    const int nbn = B1 * B2 * B3;
+                    const double* qn_p = P.q + P.off[nb] + ib + B1 * (jb + B2 * kb);
+                    double qn[NV];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) qn[v] = qn_p[(long long)v * nbn];
+                    if (s) riemann(qo, qn, nrm, P.ph, G); else riemann(qn, qo, nrm, P.ph, G);
+                }
+            }
+            const double sc = (s ? 1.0 : -1.0) * s_sc[slot][d] / c_w[Nd][0];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) Gs[(slot * NV + v) * FS + r] = sc * (G[v] - fo[v]);
+        }
+    }
+
+    // ---- volume term, direction by direction -----------------------------
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+#pragma unroll
+        for (int it = 0; it < NPTT; ++it) {
+            const int t = tid + it * BS;
+            if (t < ntot) {
+                const int slot = t / n, node = t - slot * n;
+                double f[NV];
+                if (d == 0) flux_axis<0>(q[it], ir[it], pr[it], f);
+                else if (d == 1) flux_axis<1>(q[it], ir[it], pr[it], f);
+                else flux_axis<2>(q[it], ir[it], pr[it], f);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) F[(slot * NV + v) * n + node] = f[v];
+            }
+        }
+        __syncthreads();
+        const int L = d == 0 ? n1 : (d == 1 ? n2 : n3);
+        const int nlines = n / L;
+        for (int task = tid; task < cnt * NV * nlines; task += BS) {
+            const int sv = task / nlines;          // slot * NV + v
+            const int l = task - sv * nlines;
+            const int slot = sv / NV;
+            int base, stride;
+            if (d == 0) { base = l * n1; stride = 1; }
+            else if (d == 1) { const int ii = l % n1, kk = l / n1; base = ii + n1 * n2 * kk; stride = n1; }
+            else { base = l; stride = n1 * n2; }
+            const double sc = s_sc[slot][d];
+            const double* Fl = F + sv * n + base;
+            double* Al = A + sv * n + base;
+            double out[NP];
+            if (d == 0) dmul_line<n1, 0>(Fl, stride, sc, out);
+            else if (d == 1) dmul_line<n2, 1>(Fl, stride, sc, out);
+            else dmul_line<n3, 2>(Fl, stride, sc, out);
+            if (d == 0) {
+#pragma unroll
+                for (int a = 0; a < n1; ++a) Al[a * stride] = out[a];
+            } else if (d == 1) {
+#pragma unroll
+                for (int a = 0; a < n2; ++a) Al[a * stride] += out[a];
+            } else {
+#pragma unroll
+                for (int a = 0; a < n3; ++a) Al[a * stride] += out[a];
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- epilogue per node ----------------------------------------------
+    const double dt = P.mode ? *P.dt : 0.0;
+#pragma unroll
+    for (int it = 0; it < NPTT; ++it) {
+        const int t = tid + it * BS;
+        if (t >= ntot) continue;
+        const int slot = t / n, node = t - slot * n;
+        const int i = node % n1, j = (node / n1) % n2, k = node / (n1 * n2);
+        double acc[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v] = A[(slot * NV + v) * n + node];
+        if (P.variant == 0) {
+            const double* Gb = Gs + slot * NV * FS;
+            if (i == 0 || i == N1) {
+                const int r = (i == 0 ? 0 : S::nf0) + j + n2 * k;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) acc[v] += Gb[v * FS + r];
+            }
+            if (j == 0 || j == N2) {
+                const int r = 2 * S::nf0 + (j == 0 ? 0 : S::nf1) + i + n1 * k;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) acc[v] += Gb[v * FS + r];
+            }
+            if (k == 0 || k == N3) {
+                const int r = 2 * (S::nf0 + S::nf1) + (k == 0 ? 0 : S::nf2) + i + n1 * j;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) acc[v] += Gb[v * FS + r];
+            }
+        }
+        double* o = P.out + s_off[slot] + node;
+        if (P.mode == 0) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) o[v * n] = -acc[v];
+        } else {
+            double* g = P.g + s_off[slot] + node;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const double gn = (P.rkA == 0.0 ? 0.0 : P.rkA * g[v * n]) - dt * acc[v];
+                g[v * n] = gn;
+                o[v * n] = q[it][v] + P.rkB * gn;
+            }
+        }
+    }
+}
+
+// host-side: launcher table filled by the instantiation units
+typedef void (*res_launcher)(const ResParams& P, int item0, int nitems, cudaStream_t st);
+
+static inline cudaError_t res_copy_constants(const Tables* host)
+{
+    cudaError_t e = cudaMemcpyToSymbol(c_D, host->D, sizeof(c_D));
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyToSymbol(c_w, host->w, sizeof(c_w));
+}
+
+template <int N1, int N2, int N3>
+void launch_res_t(const ResParams& P, int item0, int nitems, cudaStream_t st)
+{
+    using S = Shape<N1, N2, N3>;
+    k_res_t<N1, N2, N3><<<nitems, S::BS, S::smem_bytes, st>>>(P, item0);
+}
+
+template <int N1, int N2, int N3>
+cudaError_t attr_res_t()
+{
+    using S = Shape<N1, N2, N3>;
+    return cudaFuncSetAttribute(k_res_t<N1, N2, N3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::smem_bytes);
+}
+
+}  // namespace dgtau
