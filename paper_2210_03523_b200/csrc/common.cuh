@@ -185,6 +185,16 @@ __device__ __forceinline__ double block_max(double v, double* red)
 // Residual launch parameters (generic and order-specialised kernels)
 // ---------------------------------------------------------------------------
 
+// Per element-face source of the outer state / flux (built by the host plan):
+//   kind 0 conforming neighbour: trace value of variable v at own face point
+//          (ta, tb) is q[off + v*n + base + ta*sa + tb*sb];
+//   kind 1 mortar: projected Riemann flux at mortarG[off + v*n + pt];
+//   kind 2 wall, kind 3 far field (ghost state from the own trace).
+struct FaceInfo {
+    long long off;
+    int kind, n, base, sa, sb, pad;
+};
+
 struct ResParams {
     const double* q;        // state read (neighbour traces come from here too)
     double* out;            // mode 0: qdot; mode 1: q_out = q + B g
@@ -201,6 +211,7 @@ struct ResParams {
     const int* elist;
     const double* mortarG;  // projected Riemann fluxes for mortar faces
     const long long* moff;  // [E][6] offset into mortarG or -1
+    const FaceInfo* finfo;  // [E][6]
     const Tables* tab;
     PhysDev ph;
     int* flag;              // [0] admissibility violations, [1] element id

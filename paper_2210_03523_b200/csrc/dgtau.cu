@@ -67,6 +67,7 @@ struct dg_ctx {
     int* d_elist = nullptr;
     MortarItem* d_mortar = nullptr;
     long long* d_moff = nullptr;
+    FaceInfo* d_finfo = nullptr;
     double* d_mortarG = nullptr;
     unsigned long long* d_scratch = nullptr;  // [8]
     int* d_flag = nullptr;                    // [4]
@@ -208,6 +209,7 @@ void dg_destroy(dg_ctx* ctx)
     dfree(ctx->d_elist);
     dfree(ctx->d_mortar);
     dfree(ctx->d_moff);
+    dfree(ctx->d_finfo);
     dfree(ctx->d_mortarG);
     dfree(ctx->d_scratch);
     dfree(ctx->d_flag);
@@ -341,6 +343,33 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
         }
     ctx->nmortar = (int)mort.size();
     ctx->mortar_len = mlen;
+    // per element-face source descriptors of the outer state (see FaceInfo)
+    std::vector<FaceInfo> finfo(6LL * E);
+    for (int e = 0; e < E; ++e)
+        for (int f = 0; f < 6; ++f) {
+            const int d = f >> 1, s = f & 1;
+            FaceInfo fi{};
+            const int nb = ctx->nbr[6 * e + f];
+            const int* No = &ctx->orders[3 * e];
+            if (nb == -1) fi.kind = 2;
+            else if (nb == -2) fi.kind = 3;
+            else if (moff[6LL * e + f] >= 0) {
+                fi.kind = 1;
+                fi.off = moff[6LL * e + f];
+                fi.n = (No[TA[d]] + 1) * (No[TB[d]] + 1);
+            } else {
+                const int* B = &ctx->orders[3 * nb];
+                const int st[3] = {1, B[0] + 1, (B[0] + 1) * (B[1] + 1)};
+                fi.kind = 0;
+                fi.off = ctx->off[nb];
+                fi.n = npts(B);
+                fi.base = (s ? 0 : B[d]) * st[d];
+                fi.sa = st[TA[d]];
+                fi.sb = st[TB[d]];
+            }
+            finfo[6LL * e + f] = fi;
+        }
+    CK(upload(ctx->d_finfo, finfo));
     std::vector<int> ord_i(ctx->orders.begin(), ctx->orders.end());
     CK(upload(ctx->d_orders, ord_i));
     CK(upload(ctx->d_off, ctx->off));
@@ -419,6 +448,7 @@ static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, doub
     P.elist = ctx->d_elist;
     P.mortarG = ctx->d_mortarG;
     P.moff = ctx->d_moff;
+    P.finfo = ctx->d_finfo;
     P.tab = ctx->d_tab;
     P.ph = phys_dev(ctx->prm);
     P.flag = ctx->d_flag;

@@ -41,7 +41,8 @@ struct Shape {
     static constexpr int BS = ((T + NPT - 1) / NPT + 31) / 32 * 32;
     static constexpr int nf0 = n2 * n3, nf1 = n1 * n3, nf2 = n1 * n2;
     static constexpr int FS = 2 * (nf0 + nf1 + nf2);
-    static constexpr size_t smem_bytes = sizeof(double) * (size_t)(2 * NV * T + NV * CNT * FS);
+    // Q (5T) + F (5T) + IR,P (2T) + outer traces / lifting terms (5 FS per element)
+    static constexpr size_t smem_bytes = sizeof(double) * (size_t)(12 * T + NV * CNT * FS);
 };
 
 // f . e_d for the Euler flux, from q with precomputed 1/rho and p
@@ -70,19 +71,44 @@ __device__ __forceinline__ void flux_normal(const double* q, double nx, double n
     f[4] = (q[4] + p) * un;
 }
 
-template <int L, int d>
-__device__ __forceinline__ void dmul_line(const double* Fl, int stride, double sc, double* out)
+// In-place derivative of one line held in shared memory: F[m*stride] <- sum_m D_am F_m.
+template <int L>
+__device__ __forceinline__ void dline_inplace(double* Fl, int stride)
 {
-    constexpr int DO = (L - 1) * NP * NP;  // offset of D^{L-1}
+    constexpr int DO = (L - 1) * NP * NP;  // offset of D^{L-1} in c_D
     double v[L];
 #pragma unroll
     for (int m = 0; m < L; ++m) v[m] = Fl[m * stride];
 #pragma unroll
     for (int a = 0; a < L; ++a) {
-        double s = 0.0;
+        double s = c_D[DO + a * L] * v[0];
 #pragma unroll
-        for (int m = 0; m < L; ++m) s = fma(c_D[DO + a * L + m], v[m], s);
-        out[a] = sc * s;
+        for (int m = 1; m < L; ++m) s = fma(c_D[DO + a * L + m], v[m], s);
+        Fl[a * stride] = s;
+    }
+}
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+
+// decode face task r in [0, FS) -> face f and point pt
+template <class S>
+__device__ __forceinline__ void face_of(int r, int& f, int& pt)
+{
+    if (r < 2 * S::nf0) {
+        f = r < S::nf0 ? 0 : 1;
+        pt = r - f * S::nf0;
+    } else if (r < 2 * (S::nf0 + S::nf1)) {
+        const int r1 = r - 2 * S::nf0;
+        f = r1 < S::nf1 ? 2 : 3;
+        pt = r1 - (f - 2) * S::nf1;
+    } else {
+        const int r2 = r - 2 * (S::nf0 + S::nf1);
+        f = r2 < S::nf2 ? 4 : 5;
+        pt = r2 - (f - 4) * S::nf2;
     }
 }
 
@@ -93,9 +119,11 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS) k_res_t(ResParams P, in
     constexpr int n = S::n, n1 = S::n1, n2 = S::n2, n3 = S::n3, BS = S::BS, NPTT = S::NPT, FS = S::FS;
     constexpr int T = S::T;
     extern __shared__ double sm[];
-    double* F = sm;               // [slot][v][node]  one direction's flux
-    double* A = F + NV * T;       // [slot][v][node]  volume accumulator
-    double* Gs = A + NV * T;      // [slot][v][face point]  lifting terms
+    double* Q = sm;               // [slot][v][node]  state
+    double* F = Q + NV * T;       // [slot][v][node]  flux of one direction, then its derivative
+    double* IR = F + NV * T;      // [slot*n + node]  1/rho
+    double* PR = IR + T;          // [slot*n + node]  pressure
+    double* X = PR + T;           // [slot][v][face point]  outer traces, then lifting terms
     __shared__ long long s_off[S::CNT];
     __shared__ int s_e[S::CNT];
     __shared__ double s_sc[S::CNT][3];
@@ -113,181 +141,181 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS) k_res_t(ResParams P, in
     __syncthreads();
     const double gm1 = P.ph.gm1;
     const int ntot = cnt * n;
+    const bool surf = P.variant == 0;
 
-    // ---- node owners: state into registers ------------------------------
-    double q[NPTT][NV], ir[NPTT], pr[NPTT];
+    // ---- outer traces / mortar fluxes: asynchronous gather into X ---------
+    if (surf) {
+        for (int t = tid; t < cnt * FS; t += BS) {
+            const int slot = t / FS;
+            const int r = t - slot * FS;
+            int f, pt;
+            face_of<S>(r, f, pt);
+            const FaceInfo fi = P.finfo[6 * s_e[slot] + f];
+            const int nta = f < 2 ? n2 : n1;
+            const int ta = pt % nta, tb = pt / nta;
+            if (fi.kind == 0) {
+                const double* src = P.q + fi.off + fi.base + ta * fi.sa + tb * fi.sb;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) cp_async8(&X[(slot * NV + v) * FS + r], src + (long long)v * fi.n);
+            } else if (fi.kind == 1) {
+                const double* src = P.mortarG + fi.off + pt;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) cp_async8(&X[(slot * NV + v) * FS + r], src + (long long)v * fi.n);
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    }
+
+    // ---- state into shared memory (coalesced), 1/rho and p once per node -
 #pragma unroll
     for (int it = 0; it < NPTT; ++it) {
         const int t = tid + it * BS;
         if (t < ntot) {
             const int slot = t / n, node = t - slot * n;
             const double* qe = P.q + s_off[slot] + node;
+            double qv[NV];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) q[it][v] = qe[v * n];
-            ir[it] = 1.0 / q[it][0];
-            pr[it] = gm1 * (q[it][4] - 0.5 * ir[it] * (q[it][1] * q[it][1] + q[it][2] * q[it][2] + q[it][3] * q[it][3]));
-            if (!(q[it][0] > 0.0 && pr[it] > 0.0)) {
+            for (int v = 0; v < NV; ++v) {
+                qv[v] = qe[v * n];
+                Q[(slot * NV + v) * n + node] = qv[v];
+            }
+            const double ir = 1.0 / qv[0];
+            const double p = gm1 * (qv[4] - 0.5 * ir * (qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]));
+            IR[t] = ir;
+            PR[t] = p;
+            if (!(qv[0] > 0.0 && p > 0.0)) {
                 if (atomicAdd(P.flag, 1) == 0) P.flag[1] = s_e[slot];
             }
-        } else {
-#pragma unroll
-            for (int v = 0; v < NV; ++v) q[it][v] = 0.0;
-            ir[it] = 0.0;
-            pr[it] = 0.0;
         }
     }
 
-    // ---- surface terms (non-isolated): Gs = +-(G - f_own) 2/(h_d w_end) ---
-    if (P.variant == 0) {
-        for (int t = tid; t < cnt * FS; t += BS) {
-            const int slot = t / FS;
-            const int r = t - slot * FS;
-            int f, pt;
-            if (r < 2 * S::nf0) { f = r < S::nf0 ? 0 : 1; pt = r - f * S::nf0; }
-            else if (r < 2 * (S::nf0 + S::nf1)) {
-                const int r1 = r - 2 * S::nf0;
-                f = r1 < S::nf1 ? 2 : 3;
-                pt = r1 - (f - 2) * S::nf1;
-            } else {
-                const int r2 = r - 2 * (S::nf0 + S::nf1);
-                f = r2 < S::nf2 ? 4 : 5;
-                pt = r2 - (f - 4) * S::nf2;
-            }
-            const int d = f >> 1, s = f & 1;
-            // own boundary node (i,j,k) and lifting scale
-            int i, j, k, Nd;
-            if (d == 0) { i = s ? N1 : 0; j = pt % n2; k = pt / n2; Nd = N1; }
-            else if (d == 1) { i = pt % n1; j = s ? N2 : 0; k = pt / n1; Nd = N2; }
-            else { i = pt % n1; j = pt / n1; k = s ? N3 : 0; Nd = N3; }
-            const int node = i + n1 * (j + n2 * k);
-            const int e = s_e[slot];
-            const double* qe = P.q + s_off[slot] + node;
-            double qo[NV];
+    // ---- volume term, direction by direction ------------------------------
+    double acc[NPTT][NV];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) qo[v] = qe[v * n];
-            const double nx = d == 0 ? 1.0 : 0.0, ny = d == 1 ? 1.0 : 0.0, nz = d == 2 ? 1.0 : 0.0;
-            double fo[NV], G[NV];
-            flux_normal(qo, nx, ny, nz, gm1, fo);
-            const int nb = P.nbr[6 * e + f];
-            const double nrm[3] = {nx, ny, nz};
-            if (nb < 0) {
-                double qg[NV];
-                ghost_state(qo, nb, P.ph, qg);
-                if (s) riemann(qo, qg, nrm, P.ph, G); else riemann(qg, qo, nrm, P.ph, G);
-            } else {
-                const long long mo = P.moff[6 * e + f];
-                if (mo >= 0) {
-                    const int nfd = d == 0 ? S::nf0 : (d == 1 ? S::nf1 : S::nf2);
+    for (int it = 0; it < NPTT; ++it)
 #pragma unroll
-                    for (int v = 0; v < NV; ++v) G[v] = P.mortarG[mo + (long long)v * nfd + pt];
-                } else {
-                    const int B1 = P.orders[3 * nb] + 1, B2 = P.orders[3 * nb + 1] + 1, B3 = P.orders[3 * nb + 2] + 1;
-                    int ib = i, jb = j, kb = k;
-                    if (d == 0) ib = s ? 0 : B1 - 1;
-                    else if (d == 1) jb = s ? 0 : B2 - 1;
-                    else kb = s ? 0 : B3 - 1;
-                    const int nbn = B1 * B2 * B3;
-                    const double* qn_p = P.q + P.off[nb] + ib + B1 * (jb + B2 * kb);
-                    double qn[NV];
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) qn[v] = qn_p[(long long)v * nbn];
-                    if (s) riemann(qo, qn, nrm, P.ph, G); else riemann(qn, qo, nrm, P.ph, G);
-                }
-            }
-            const double sc = (s ? 1.0 : -1.0) * s_sc[slot][d] / c_w[Nd][0];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) Gs[(slot * NV + v) * FS + r] = sc * (G[v] - fo[v]);
-        }
-    }
+        for (int v = 0; v < NV; ++v) acc[it][v] = 0.0;
 
-    // ---- volume term, direction by direction -----------------------------
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
+        if (d > 0) __syncthreads();  // previous direction's derivatives consumed
 #pragma unroll
         for (int it = 0; it < NPTT; ++it) {
             const int t = tid + it * BS;
             if (t < ntot) {
                 const int slot = t / n, node = t - slot * n;
-                double f[NV];
-                if (d == 0) flux_axis<0>(q[it], ir[it], pr[it], f);
-                else if (d == 1) flux_axis<1>(q[it], ir[it], pr[it], f);
-                else flux_axis<2>(q[it], ir[it], pr[it], f);
+                double qv[NV], f[NV];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) qv[v] = Q[(slot * NV + v) * n + node];
+                if (d == 0) flux_axis<0>(qv, IR[t], PR[t], f);
+                else if (d == 1) flux_axis<1>(qv, IR[t], PR[t], f);
+                else flux_axis<2>(qv, IR[t], PR[t], f);
 #pragma unroll
                 for (int v = 0; v < NV; ++v) F[(slot * NV + v) * n + node] = f[v];
             }
         }
         __syncthreads();
-        const int L = d == 0 ? n1 : (d == 1 ? n2 : n3);
-        const int nlines = n / L;
+        constexpr int Ld[3] = {n1, n2, n3};
+        const int nlines = n / Ld[d];
         for (int task = tid; task < cnt * NV * nlines; task += BS) {
-            const int sv = task / nlines;          // slot * NV + v
+            const int sv = task / nlines;  // slot * NV + v
             const int l = task - sv * nlines;
-            const int slot = sv / NV;
-            int base, stride;
-            if (d == 0) { base = l * n1; stride = 1; }
-            else if (d == 1) { const int ii = l % n1, kk = l / n1; base = ii + n1 * n2 * kk; stride = n1; }
-            else { base = l; stride = n1 * n2; }
-            const double sc = s_sc[slot][d];
-            const double* Fl = F + sv * n + base;
-            double* Al = A + sv * n + base;
-            double out[NP];
-            if (d == 0) dmul_line<n1, 0>(Fl, stride, sc, out);
-            else if (d == 1) dmul_line<n2, 1>(Fl, stride, sc, out);
-            else dmul_line<n3, 2>(Fl, stride, sc, out);
-            if (d == 0) {
+            if (d == 0) dline_inplace<n1>(F + sv * n + l * n1, 1);
+            else if (d == 1) dline_inplace<n2>(F + sv * n + (l % n1) + n1 * n2 * (l / n1), n1);
+            else dline_inplace<n3>(F + sv * n + l, n1 * n2);
+        }
+        __syncthreads();
 #pragma unroll
-                for (int a = 0; a < n1; ++a) Al[a * stride] = out[a];
-            } else if (d == 1) {
+        for (int it = 0; it < NPTT; ++it) {
+            const int t = tid + it * BS;
+            if (t < ntot) {
+                const int slot = t / n, node = t - slot * n;
+                const double sc = s_sc[slot][d];
 #pragma unroll
-                for (int a = 0; a < n2; ++a) Al[a * stride] += out[a];
-            } else {
-#pragma unroll
-                for (int a = 0; a < n3; ++a) Al[a * stride] += out[a];
+                for (int v = 0; v < NV; ++v) acc[it][v] = fma(sc, F[(slot * NV + v) * n + node], acc[it][v]);
             }
+        }
+    }
+
+    // ---- surface: lifting terms +-(G - f_own) 2/(h_d w_end) into X ---------
+    if (surf) {
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncthreads();
+        for (int t = tid; t < cnt * FS; t += BS) {
+            const int slot = t / FS;
+            const int r = t - slot * FS;
+            int f, pt;
+            face_of<S>(r, f, pt);
+            const int d = f >> 1, s = f & 1;
+            const int nta = d == 0 ? n2 : n1;
+            const int ta = pt % nta, tb = pt / nta;
+            int i, j, k, Nd;
+            if (d == 0) { i = s ? N1 : 0; j = ta; k = tb; Nd = N1; }
+            else if (d == 1) { i = ta; j = s ? N2 : 0; k = tb; Nd = N2; }
+            else { i = ta; j = tb; k = s ? N3 : 0; Nd = N3; }
+            const int node = i + n1 * (j + n2 * k);
+            double qo[NV], fo[NV], G[NV], qx[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                qo[v] = Q[(slot * NV + v) * n + node];
+                qx[v] = X[(slot * NV + v) * FS + r];
+            }
+            const double nx = d == 0 ? 1.0 : 0.0, ny = d == 1 ? 1.0 : 0.0, nz = d == 2 ? 1.0 : 0.0;
+            flux_normal(qo, nx, ny, nz, gm1, fo);
+            const double nrm[3] = {nx, ny, nz};
+            const int kind = P.finfo[6 * s_e[slot] + f].kind;
+            if (kind == 1) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v) G[v] = qx[v];
+            } else {
+                if (kind >= 2) ghost_state(qo, kind == 2 ? -1 : -2, P.ph, qx);
+                if (s) riemann(qo, qx, nrm, P.ph, G);
+                else riemann(qx, qo, nrm, P.ph, G);
+            }
+            const double sc = (s ? 1.0 : -1.0) * s_sc[slot][d] / c_w[Nd][0];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) X[(slot * NV + v) * FS + r] = sc * (G[v] - fo[v]);
         }
         __syncthreads();
     }
 
-    // ---- epilogue per node ----------------------------------------------
+    // ---- epilogue per node --------------------------------------------------
     const double dt = P.mode ? *P.dt : 0.0;
 #pragma unroll
     for (int it = 0; it < NPTT; ++it) {
         const int t = tid + it * BS;
         if (t >= ntot) continue;
         const int slot = t / n, node = t - slot * n;
-        const int i = node % n1, j = (node / n1) % n2, k = node / (n1 * n2);
-        double acc[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) acc[v] = A[(slot * NV + v) * n + node];
-        if (P.variant == 0) {
-            const double* Gb = Gs + slot * NV * FS;
+        if (surf) {
+            const int i = node % n1, j = (node / n1) % n2, k = node / (n1 * n2);
+            const double* Xb = X + slot * NV * FS;
             if (i == 0 || i == N1) {
                 const int r = (i == 0 ? 0 : S::nf0) + j + n2 * k;
 #pragma unroll
-                for (int v = 0; v < NV; ++v) acc[v] += Gb[v * FS + r];
+                for (int v = 0; v < NV; ++v) acc[it][v] += Xb[v * FS + r];
             }
             if (j == 0 || j == N2) {
                 const int r = 2 * S::nf0 + (j == 0 ? 0 : S::nf1) + i + n1 * k;
 #pragma unroll
-                for (int v = 0; v < NV; ++v) acc[v] += Gb[v * FS + r];
+                for (int v = 0; v < NV; ++v) acc[it][v] += Xb[v * FS + r];
             }
             if (k == 0 || k == N3) {
                 const int r = 2 * (S::nf0 + S::nf1) + (k == 0 ? 0 : S::nf2) + i + n1 * j;
 #pragma unroll
-                for (int v = 0; v < NV; ++v) acc[v] += Gb[v * FS + r];
+                for (int v = 0; v < NV; ++v) acc[it][v] += Xb[v * FS + r];
             }
         }
         double* o = P.out + s_off[slot] + node;
         if (P.mode == 0) {
 #pragma unroll
-            for (int v = 0; v < NV; ++v) o[v * n] = -acc[v];
+            for (int v = 0; v < NV; ++v) o[v * n] = -acc[it][v];
         } else {
             double* g = P.g + s_off[slot] + node;
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
-                const double gn = (P.rkA == 0.0 ? 0.0 : P.rkA * g[v * n]) - dt * acc[v];
+                const double gn = (P.rkA == 0.0 ? 0.0 : P.rkA * g[v * n]) - dt * acc[it][v];
                 g[v * n] = gn;
-                o[v * n] = q[it][v] + P.rkB * gn;
+                o[v * n] = Q[(slot * NV + v) * n + node] + P.rkB * gn;
             }
         }
     }
