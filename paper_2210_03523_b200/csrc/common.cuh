@@ -195,6 +195,14 @@ struct FaceInfo {
     int kind, n, base, sa, sb, pad;
 };
 
+// Per work-item slot: element id, state offset and the affine metric scales
+// 2/h_d (so the kernels need one dependent load instead of three).
+struct SlotInfo {
+    long long off;
+    int e, pad;
+    double sc[3];
+};
+
 struct ResParams {
     const double* q;        // state read (neighbour traces come from here too)
     double* out;            // mode 0: qdot; mode 1: q_out = q + B g
@@ -212,6 +220,7 @@ struct ResParams {
     const double* mortarG;  // projected Riemann fluxes for mortar faces
     const long long* moff;  // [E][6] offset into mortarG or -1
     const FaceInfo* finfo;  // [E][6]
+    const SlotInfo* slots;  // [elist length], parallel to elist
     const Tables* tab;
     PhysDev ph;
     int* flag;              // [0] admissibility violations, [1] element id

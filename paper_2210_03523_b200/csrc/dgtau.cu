@@ -68,6 +68,7 @@ struct dg_ctx {
     MortarItem* d_mortar = nullptr;
     long long* d_moff = nullptr;
     FaceInfo* d_finfo = nullptr;
+    SlotInfo* d_slots = nullptr;
     double* d_mortarG = nullptr;
     unsigned long long* d_scratch = nullptr;  // [8]
     int* d_flag = nullptr;                    // [4]
@@ -210,6 +211,7 @@ void dg_destroy(dg_ctx* ctx)
     dfree(ctx->d_mortar);
     dfree(ctx->d_moff);
     dfree(ctx->d_finfo);
+    dfree(ctx->d_slots);
     dfree(ctx->d_mortarG);
     dfree(ctx->d_scratch);
     dfree(ctx->d_flag);
@@ -370,6 +372,15 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
             finfo[6LL * e + f] = fi;
         }
     CK(upload(ctx->d_finfo, finfo));
+    std::vector<SlotInfo> slots(elist.size());
+    for (size_t i = 0; i < elist.size(); ++i) {
+        const int e = elist[i];
+        slots[i].off = ctx->off[e];
+        slots[i].e = e;
+        slots[i].pad = 0;
+        for (int dd = 0; dd < 3; ++dd) slots[i].sc[dd] = 2.0 / ctx->h[3LL * e + dd];
+    }
+    CK(upload(ctx->d_slots, slots));
     std::vector<int> ord_i(ctx->orders.begin(), ctx->orders.end());
     CK(upload(ctx->d_orders, ord_i));
     CK(upload(ctx->d_off, ctx->off));
@@ -449,6 +460,7 @@ static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, doub
     P.mortarG = ctx->d_mortarG;
     P.moff = ctx->d_moff;
     P.finfo = ctx->d_finfo;
+    P.slots = ctx->d_slots;
     P.tab = ctx->d_tab;
     P.ph = phys_dev(ctx->prm);
     P.flag = ctx->d_flag;

@@ -27,6 +27,13 @@ namespace dgtau {
 // per translation unit (internal linkage), filled by res_setup_* at startup.
 static __constant__ double c_D[NP * NP * NP];
 static __constant__ double c_w[NP][NP];
+// even-odd (centro-antisymmetric, D_{N-a,N-m} = -D_{a,m}) split of D^N,
+// H = floor((N+1)/2):  P[a][m] = (D_am - D_{a,N-m})/2, Q[a][m] = (D_am + D_{a,N-m})/2
+// for a, m < H;  Qm[a] = D_{a,mid} (odd N+1);  M[m] = D_{mid,m} (odd N+1).
+static __constant__ double c_EOP[NP][16];
+static __constant__ double c_EOQ[NP][16];
+static __constant__ double c_EOQm[NP][4];
+static __constant__ double c_EOM[NP][4];
 
 __host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
@@ -41,8 +48,9 @@ struct Shape {
     static constexpr int BS = ((T + NPT - 1) / NPT + 31) / 32 * 32;
     static constexpr int nf0 = n2 * n3, nf1 = n1 * n3, nf2 = n1 * n2;
     static constexpr int FS = 2 * (nf0 + nf1 + nf2);
-    // Q (5T) + F (5T) + IR,P (2T) + outer traces / lifting terms (5 FS per element)
-    static constexpr size_t smem_bytes = sizeof(double) * (size_t)(12 * T + NV * CNT * FS);
+    // Q (5T) + F (5T) + RK register g (5T) + IR,P (2T) + outer traces / lifting terms (5 FS per element)
+    static constexpr size_t smem_bytes = sizeof(double) * (size_t)(17 * T + NV * CNT * FS);
+    static constexpr int MINB = BS <= 128 ? 4 : (BS <= 192 ? 3 : 2);
 };
 
 // f . e_d for the Euler flux, from q with precomputed 1/rho and p
@@ -71,20 +79,45 @@ __device__ __forceinline__ void flux_normal(const double* q, double nx, double n
     f[4] = (q[4] + p) * un;
 }
 
-// In-place derivative of one line held in shared memory: F[m*stride] <- sum_m D_am F_m.
+// In-place derivative of one line held in shared memory, F[m*stride] <-
+// sum_m D_am F_m, by the even-odd decomposition of the GL differentiation
+// matrix (about half the multiply-adds of the direct product):
+//   o_m = v_m - v_{N-m}, e_m = v_m + v_{N-m}  (m < H),
+//   out_a = sum_m P_am o_m + (sum_m Q_am e_m + Qm_a v_mid),
+//   out_{N-a} = sum_m P_am o_m - (sum_m Q_am e_m + Qm_a v_mid),
+//   out_mid = sum_m M_m o_m.
 template <int L>
 __device__ __forceinline__ void dline_inplace(double* Fl, int stride)
 {
-    constexpr int DO = (L - 1) * NP * NP;  // offset of D^{L-1} in c_D
+    constexpr int N = L - 1, H = L / 2;
+    constexpr bool odd = (L & 1) != 0;
     double v[L];
 #pragma unroll
     for (int m = 0; m < L; ++m) v[m] = Fl[m * stride];
+    double o[H], ev[H];
 #pragma unroll
-    for (int a = 0; a < L; ++a) {
-        double s = c_D[DO + a * L] * v[0];
+    for (int m = 0; m < H; ++m) {
+        o[m] = v[m] - v[N - m];
+        ev[m] = v[m] + v[N - m];
+    }
 #pragma unroll
-        for (int m = 1; m < L; ++m) s = fma(c_D[DO + a * L + m], v[m], s);
-        Fl[a * stride] = s;
+    for (int a = 0; a < H; ++a) {
+        double p = c_EOP[N][a * H] * o[0];
+        double q = c_EOQ[N][a * H] * ev[0];
+#pragma unroll
+        for (int m = 1; m < H; ++m) {
+            p = fma(c_EOP[N][a * H + m], o[m], p);
+            q = fma(c_EOQ[N][a * H + m], ev[m], q);
+        }
+        if (odd) q = fma(c_EOQm[N][a], v[H], q);
+        Fl[a * stride] = p + q;
+        Fl[(N - a) * stride] = p - q;
+    }
+    if (odd) {
+        double s = c_EOM[N][0] * o[0];
+#pragma unroll
+        for (int m = 1; m < H; ++m) s = fma(c_EOM[N][m], o[m], s);
+        Fl[H * stride] = s;
     }
 }
 
@@ -113,7 +146,7 @@ __device__ __forceinline__ void face_of(int r, int& f, int& pt)
 }
 
 template <int N1, int N2, int N3>
-__global__ void __launch_bounds__(Shape<N1, N2, N3>::BS) k_res_t(ResParams P, int item0)
+__global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB) k_res_t(ResParams P, int item0)
 {
     using S = Shape<N1, N2, N3>;
     constexpr int n = S::n, n1 = S::n1, n2 = S::n2, n3 = S::n3, BS = S::BS, NPTT = S::NPT, FS = S::FS;
@@ -123,7 +156,8 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS) k_res_t(ResParams P, in
     double* F = Q + NV * T;       // [slot][v][node]  flux of one direction, then its derivative
     double* IR = F + NV * T;      // [slot*n + node]  1/rho
     double* PR = IR + T;          // [slot*n + node]  pressure
-    double* X = PR + T;           // [slot][v][face point]  outer traces, then lifting terms
+    double* GB = PR + T;          // [slot][v][node]  RK register g (prefetched)
+    double* X = GB + NV * T;      // [slot][v][face point]  outer traces, then lifting terms
     __shared__ long long s_off[S::CNT];
     __shared__ int s_e[S::CNT];
     __shared__ double s_sc[S::CNT][3];
@@ -132,11 +166,11 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS) k_res_t(ResParams P, in
     const int cnt = w.count;
     const int tid = threadIdx.x;
     if (tid < cnt) {
-        const int e = P.elist[w.start + tid];
-        s_e[tid] = e;
-        s_off[tid] = P.off[e];
+        const SlotInfo si = P.slots[w.start + tid];
+        s_e[tid] = si.e;
+        s_off[tid] = si.off;
 #pragma unroll
-        for (int d = 0; d < 3; ++d) s_sc[tid][d] = 2.0 / P.hgeo[3 * e + d];
+        for (int d = 0; d < 3; ++d) s_sc[tid][d] = si.sc[d];
     }
     __syncthreads();
     const double gm1 = P.ph.gm1;
@@ -165,6 +199,22 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS) k_res_t(ResParams P, in
         }
         asm volatile("cp.async.commit_group;\n" ::);
     }
+
+    // ---- RK register g: asynchronous prefetch (needed only in the epilogue)
+    const bool need_g = P.mode == 1 && P.rkA != 0.0;
+    if (need_g) {
+#pragma unroll
+        for (int it = 0; it < NPTT; ++it) {
+            const int t = tid + it * BS;
+            if (t < ntot) {
+                const int slot = t / n, node = t - slot * n;
+                const double* ge = P.g + s_off[slot] + node;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) cp_async8(&GB[(slot * NV + v) * n + node], ge + v * n);
+            }
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
 
     // ---- state into shared memory (coalesced), 1/rho and p once per node -
 #pragma unroll
@@ -232,7 +282,10 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS) k_res_t(ResParams P, in
                 const int slot = t / n, node = t - slot * n;
                 const double sc = s_sc[slot][d];
 #pragma unroll
-                for (int v = 0; v < NV; ++v) acc[it][v] = fma(sc, F[(slot * NV + v) * n + node], acc[it][v]);
+                for (int v = 0; v < NV; ++v) {
+                    acc[it][v] = fma(sc, F[(slot * NV + v) * n + node], acc[it][v]);
+                    if (d == 2) F[(slot * NV + v) * n + node] = acc[it][v];  // park: frees registers
+                }
             }
         }
     }
@@ -281,39 +334,43 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS) k_res_t(ResParams P, in
 
     // ---- epilogue per node --------------------------------------------------
     const double dt = P.mode ? *P.dt : 0.0;
+    if (need_g) asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // own g values only
 #pragma unroll
     for (int it = 0; it < NPTT; ++it) {
         const int t = tid + it * BS;
         if (t >= ntot) continue;
         const int slot = t / n, node = t - slot * n;
+        double accv[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) accv[v] = F[(slot * NV + v) * n + node];
         if (surf) {
             const int i = node % n1, j = (node / n1) % n2, k = node / (n1 * n2);
             const double* Xb = X + slot * NV * FS;
             if (i == 0 || i == N1) {
                 const int r = (i == 0 ? 0 : S::nf0) + j + n2 * k;
 #pragma unroll
-                for (int v = 0; v < NV; ++v) acc[it][v] += Xb[v * FS + r];
+                for (int v = 0; v < NV; ++v) accv[v] += Xb[v * FS + r];
             }
             if (j == 0 || j == N2) {
                 const int r = 2 * S::nf0 + (j == 0 ? 0 : S::nf1) + i + n1 * k;
 #pragma unroll
-                for (int v = 0; v < NV; ++v) acc[it][v] += Xb[v * FS + r];
+                for (int v = 0; v < NV; ++v) accv[v] += Xb[v * FS + r];
             }
             if (k == 0 || k == N3) {
                 const int r = 2 * (S::nf0 + S::nf1) + (k == 0 ? 0 : S::nf2) + i + n1 * j;
 #pragma unroll
-                for (int v = 0; v < NV; ++v) acc[it][v] += Xb[v * FS + r];
+                for (int v = 0; v < NV; ++v) accv[v] += Xb[v * FS + r];
             }
         }
         double* o = P.out + s_off[slot] + node;
         if (P.mode == 0) {
 #pragma unroll
-            for (int v = 0; v < NV; ++v) o[v * n] = -acc[it][v];
+            for (int v = 0; v < NV; ++v) o[v * n] = -accv[v];
         } else {
             double* g = P.g + s_off[slot] + node;
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
-                const double gn = (P.rkA == 0.0 ? 0.0 : P.rkA * g[v * n]) - dt * acc[it][v];
+                const double gn = (need_g ? P.rkA * GB[(slot * NV + v) * n + node] : 0.0) - dt * accv[v];
                 g[v * n] = gn;
                 o[v * n] = Q[(slot * NV + v) * n + node] + P.rkB * gn;
             }
@@ -328,7 +385,26 @@ static inline cudaError_t res_copy_constants(const Tables* host)
 {
     cudaError_t e = cudaMemcpyToSymbol(c_D, host->D, sizeof(c_D));
     if (e != cudaSuccess) return e;
-    return cudaMemcpyToSymbol(c_w, host->w, sizeof(c_w));
+    if ((e = cudaMemcpyToSymbol(c_w, host->w, sizeof(c_w))) != cudaSuccess) return e;
+    double P[NP][16] = {}, Q[NP][16] = {}, Qm[NP][4] = {}, M[NP][4] = {};
+    for (int N = 1; N <= NMAX; ++N) {
+        const int L = N + 1, H = L / 2;
+        const double* D = host->D[N];
+        for (int a = 0; a < H; ++a)
+            for (int m = 0; m < H; ++m) {
+                P[N][a * H + m] = 0.5 * (D[a * L + m] - D[a * L + (N - m)]);
+                Q[N][a * H + m] = 0.5 * (D[a * L + m] + D[a * L + (N - m)]);
+            }
+        if (L & 1)
+            for (int a = 0; a < H; ++a) {
+                Qm[N][a] = D[a * L + H];
+                M[N][a] = D[H * L + a];
+            }
+    }
+    if ((e = cudaMemcpyToSymbol(c_EOP, P, sizeof(P))) != cudaSuccess) return e;
+    if ((e = cudaMemcpyToSymbol(c_EOQ, Q, sizeof(Q))) != cudaSuccess) return e;
+    if ((e = cudaMemcpyToSymbol(c_EOQm, Qm, sizeof(Qm))) != cudaSuccess) return e;
+    return cudaMemcpyToSymbol(c_EOM, M, sizeof(M));
 }
 
 template <int N1, int N2, int N3>
@@ -342,7 +418,11 @@ template <int N1, int N2, int N3>
 cudaError_t attr_res_t()
 {
     using S = Shape<N1, N2, N3>;
-    return cudaFuncSetAttribute(k_res_t<N1, N2, N3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::smem_bytes);
+    cudaError_t e = cudaFuncSetAttribute(k_res_t<N1, N2, N3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)S::smem_bytes);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_res_t<N1, N2, N3>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                (int)cudaSharedmemCarveoutMaxShared);
 }
 
 }  // namespace dgtau
