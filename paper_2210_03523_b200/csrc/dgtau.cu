@@ -19,6 +19,7 @@
 #include "basis.h"
 #include "kernels.cuh"
 #include "residual_t.cuh"
+#include "tau_t.cuh"
 
 using namespace dgtau;
 
@@ -187,12 +188,18 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
                 dg_destroy(ctx);
                 return s;
             }
+        if ((s = cuda_check(ctx, res_copy_constants(&t), "constants")) != DG_OK) {
+            dg_destroy(ctx);
+            return s;
+        }
         const char* g = getenv("DGTAU_GENERIC");
         ctx->generic = g && g[0] == '1';
     }
     // large dynamic shared memory for the element kernels
     cudaFuncSetAttribute(k_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_tau, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_tau2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_tau2, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(k_transfer, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     *out = ctx;
     return DG_OK;
@@ -537,18 +544,32 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
     if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "tau_estimate: orders not set");
     if (o->reference == DG_REF_SOLVER && !qref_dev) return fail(ctx, DG_EINVAL, "tau_estimate: SOLVER needs qdot_ref");
     if (ctx->prm.physics != DG_EULER) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: NS not in this build");
-    TauParams P;
-    P.q = q_dev;
-    P.qref = o->reference == DG_REF_SOLVER ? qref_dev : nullptr;
-    P.tau = tau_dev;
-    P.orders = ctx->d_orders;
-    P.off = ctx->d_off;
-    P.hgeo = ctx->d_h;
-    P.tab = ctx->d_tab;
-    P.formulation = o->formulation;
-    P.ph = phys_dev(ctx->prm);
     const size_t smem = sizeof(double) * 3 * NV * (size_t)ctx->maxn;
-    k_tau<<<ctx->E, BLOCK, smem, (cudaStream_t)stream>>>(P);
+    if (ctx->generic) {
+        TauParams P;
+        P.q = q_dev;
+        P.qref = o->reference == DG_REF_SOLVER ? qref_dev : nullptr;
+        P.tau = tau_dev;
+        P.orders = ctx->d_orders;
+        P.off = ctx->d_off;
+        P.hgeo = ctx->d_h;
+        P.tab = ctx->d_tab;
+        P.formulation = o->formulation;
+        P.ph = phys_dev(ctx->prm);
+        k_tau<<<ctx->E, BLOCK, smem, (cudaStream_t)stream>>>(P);
+    } else {
+        Tau2Params P;
+        P.q = q_dev;
+        P.qref = o->reference == DG_REF_SOLVER ? qref_dev : nullptr;
+        P.tau = tau_dev;
+        P.orders = ctx->d_orders;
+        P.off = ctx->d_off;
+        P.hgeo = ctx->d_h;
+        P.tab = ctx->d_tab;
+        P.formulation = o->formulation;
+        P.gm1 = ctx->prm.gamma - 1.0;
+        k_tau2<<<ctx->E, TAU_BS, smem, (cudaStream_t)stream>>>(P);
+    }
     ctx->launches++;
     return check_stream_error(ctx, "k_tau launch");
 }
