@@ -70,6 +70,11 @@ struct dg_ctx {
     long long* d_moff = nullptr;
     FaceInfo* d_finfo = nullptr;
     SlotInfo* d_slots = nullptr;
+    TauLevel* d_levels = nullptr;
+    int nlevels = 0;
+    int max_level = 0;
+    double* d_ref_scratch = nullptr;  // isolated fine residual for DG_REF_SAME
+    long long ref_len = 0;
     double* d_mortarG = nullptr;
     unsigned long long* d_scratch = nullptr;  // [8]
     int* d_flag = nullptr;                    // [4]
@@ -199,6 +204,8 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
     cudaFuncSetAttribute(k_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_tau, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_tau2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_tau3, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_tau3, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(k_tau2, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(k_transfer, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     *out = ctx;
@@ -219,6 +226,8 @@ void dg_destroy(dg_ctx* ctx)
     dfree(ctx->d_moff);
     dfree(ctx->d_finfo);
     dfree(ctx->d_slots);
+    dfree(ctx->d_levels);
+    dfree(ctx->d_ref_scratch);
     dfree(ctx->d_mortarG);
     dfree(ctx->d_scratch);
     dfree(ctx->d_flag);
@@ -388,6 +397,19 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
         for (int dd = 0; dd < 3; ++dd) slots[i].sc[dd] = 2.0 / ctx->h[3LL * e + dd];
     }
     CK(upload(ctx->d_slots, slots));
+    // tau-estimation levels (e, d, p < N_d), largest first for load balance
+    std::vector<TauLevel> lv;
+    ctx->max_level = 0;
+    for (int e = 0; e < E; ++e)
+        for (int d = 0; d < 3; ++d)
+            for (int p = 1; p < ctx->orders[3 * e + d]; ++p) {
+                lv.push_back(TauLevel{e, d, p, 0});
+                const int* No = &ctx->orders[3 * e];
+                const int nO = npts(No) / (No[d] + 1) * (p + 1);
+                ctx->max_level = std::max(ctx->max_level, nO);
+            }
+    ctx->nlevels = (int)lv.size();
+    CK(upload(ctx->d_levels, lv));
     std::vector<int> ord_i(ctx->orders.begin(), ctx->orders.end());
     CK(upload(ctx->d_orders, ord_i));
     CK(upload(ctx->d_off, ctx->off));
@@ -558,17 +580,34 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
         P.ph = phys_dev(ctx->prm);
         k_tau<<<ctx->E, BLOCK, smem, (cudaStream_t)stream>>>(P);
     } else {
-        Tau2Params P;
-        P.q = q_dev;
-        P.qref = o->reference == DG_REF_SOLVER ? qref_dev : nullptr;
-        P.tau = tau_dev;
-        P.orders = ctx->d_orders;
-        P.off = ctx->d_off;
-        P.hgeo = ctx->d_h;
-        P.tab = ctx->d_tab;
-        P.formulation = o->formulation;
-        P.gm1 = ctx->prm.gamma - 1.0;
-        k_tau2<<<ctx->E, TAU_BS, smem, (cudaStream_t)stream>>>(P);
+        cudaStream_t st = (cudaStream_t)stream;
+        const double* ref = qref_dev;
+        if (o->reference == DG_REF_SAME) {  // isolated fine residual first (reading A4)
+            if (ctx->ref_len < ctx->off[ctx->E]) {
+                dfree(ctx->d_ref_scratch);
+                CK(cudaMalloc(&ctx->d_ref_scratch, sizeof(double) * ctx->off[ctx->E]));
+                ctx->ref_len = ctx->off[ctx->E];
+            }
+            dg_status s = launch_residual(ctx, DG_ISOLATED, q_dev, ctx->d_ref_scratch, nullptr, nullptr, 0.0, 0.0, 0, st);
+            if (s != DG_OK) return s;
+            ref = ctx->d_ref_scratch;
+        }
+        k_tau_norm<<<ctx->E, 128, 0, st>>>(ref, tau_dev, ctx->d_orders, ctx->d_off);
+        ctx->launches++;
+        if (ctx->nlevels > 0) {
+            Tau3Params P;
+            P.q = q_dev;
+            P.qref = ref;
+            P.tau = tau_dev;
+            P.orders = ctx->d_orders;
+            P.off = ctx->d_off;
+            P.hgeo = ctx->d_h;
+            P.levels = ctx->d_levels;
+            P.tab = ctx->d_tab;
+            P.formulation = o->formulation;
+            P.gm1 = ctx->prm.gamma - 1.0;
+            k_tau3<<<ctx->nlevels, TAU3_BS, sizeof(double) * 2 * NV * (size_t)ctx->max_level, st>>>(P);
+        }
     }
     ctx->launches++;
     return check_stream_error(ctx, "k_tau launch");

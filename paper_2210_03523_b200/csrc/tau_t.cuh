@@ -215,3 +215,167 @@ __global__ void __launch_bounds__(TAU_BS, 1) k_tau2(Tau2Params P)
 }
 
 }  // namespace dgtau
+
+namespace dgtau {
+
+// ---------------------------------------------------------------------------
+// tau-estimation v3: one CTA per coarse level (element e, direction d, order
+// p < N_d).  Many small CTAs per SM hide the per-level barrier latency; the
+// element's fine state / reference residual are read through L1 (each level
+// of an element reads the same 2 x 5n values, so they stay cache-resident).
+// ---------------------------------------------------------------------------
+
+struct TauLevel {
+    int e, d, p, pad;
+};
+
+struct Tau3Params {
+    const double* q;
+    const double* qref;  // reference residual (SOLVER: non-isolated; SAME: isolated, computed first)
+    double* tau;         // [E][3][9]
+    const int* orders;
+    const long long* off;
+    const double* hgeo;
+    const TauLevel* levels;
+    const Tables* tab;
+    int formulation;
+    double gm1;
+};
+
+constexpr int TAU3_BS = 256;
+constexpr int TAU3_NPT = 3;  // 256 * 3 >= 648 = max coarse level size (8 x 9 x 9)
+
+__global__ void __launch_bounds__(TAU3_BS, 2) k_tau3(Tau3Params P)
+{
+    extern __shared__ double sm[];
+    __shared__ double red[32];
+    __shared__ double Ts[NP * NP];
+    const TauLevel lv = P.levels[blockIdx.x];
+    const int e = lv.e, d = lv.d, p = lv.p;
+    const int tid = threadIdx.x;
+    const int N1 = P.orders[3 * e], N2 = P.orders[3 * e + 1], N3 = P.orders[3 * e + 2];
+    const int n1 = N1 + 1, n2 = N2 + 1;
+    const int n = n1 * n2 * (N3 + 1);
+    const int Nd = d == 0 ? N1 : (d == 1 ? N2 : N3);
+    const int nd = Nd + 1;
+    const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
+    const int o1 = d == 0 ? p + 1 : n1, o2 = d == 1 ? p + 1 : n2, o3 = d == 2 ? p + 1 : N3 + 1;
+    const int nO = o1 * o2 * o3;
+    const double h0 = P.hgeo[3 * e], h1 = P.hgeo[3 * e + 1], h2 = P.hgeo[3 * e + 2];
+    const double sc[3] = {2.0 / h0, 2.0 / h1, 2.0 / h2};
+    const long long o = P.off[e];
+    const double* qe = P.q + o;
+    const double* re = P.qref + o;
+    double* Qc = sm;            // 5 nO coarse state
+    double* Fb = Qc + NV * nO;  // 5 nO flux / derivative
+    for (int t = tid; t < (p + 1) * nd; t += TAU3_BS) Ts[t] = P.tab->T[Nd][p][t];
+    __syncthreads();
+    // q_c = T^{N_d -> p} q along d  (reading A3: interpolation at the coarse nodes)
+    for (int t = tid; t < nO; t += TAU3_BS) {
+        int i, j, k;
+        node_ijk(t, o1, o2, i, j, k);
+        const int ic = d == 0 ? i : (d == 1 ? j : k);
+        if (d == 0) i = 0; else if (d == 1) j = 0; else k = 0;
+        const int base = i + n1 * (j + n2 * k);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const double* ql = qe + v * n + base;
+            double s = 0.0;
+            for (int a = 0; a < nd; ++a) s = fma(Ts[ic * nd + a], __ldg(ql + a * stride), s);
+            Qc[v * nO + t] = s;
+        }
+    }
+    __syncthreads();
+    // isolated residual at the coarse orders: acc = sum_d' (2/h_d') D^{O_d'} f_d'(q_c)
+    double acc[TAU3_NPT][NV];
+#pragma unroll
+    for (int it = 0; it < TAU3_NPT; ++it)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[it][v] = 0.0;
+#pragma unroll
+    for (int dd = 0; dd < 3; ++dd) {
+        if (dd > 0) __syncthreads();
+#pragma unroll
+        for (int it = 0; it < TAU3_NPT; ++it) {
+            const int t = tid + it * TAU3_BS;
+            if (t < nO) {
+                double qv[NV], f[NV];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) qv[v] = Qc[v * nO + t];
+                const double ir = 1.0 / qv[0];
+                const double pr = P.gm1 * (qv[4] - 0.5 * ir * (qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]));
+                if (dd == 0) flux_axis<0>(qv, ir, pr, f);
+                else if (dd == 1) flux_axis<1>(qv, ir, pr, f);
+                else flux_axis<2>(qv, ir, pr, f);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) Fb[v * nO + t] = f[v];
+            }
+        }
+        __syncthreads();
+        const int L = dd == 0 ? o1 : (dd == 1 ? o2 : o3);
+        const int nlines = nO / L;
+        for (int task = tid; task < NV * nlines; task += TAU3_BS) {
+            const int v = task / nlines, l = task - v * nlines;
+            int base, str;
+            if (dd == 0) { base = l * o1; str = 1; }
+            else if (dd == 1) { base = (l % o1) + o1 * o2 * (l / o1); str = o1; }
+            else { base = l; str = o1 * o2; }
+            dline_dispatch(L, Fb + v * nO + base, str);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int it = 0; it < TAU3_NPT; ++it) {
+            const int t = tid + it * TAU3_BS;
+            if (t < nO)
+#pragma unroll
+                for (int v = 0; v < NV; ++v) acc[it][v] = fma(sc[dd], Fb[v * nO + t], acc[it][v]);
+        }
+    }
+    // tau~ = T R - Qdot_c = T R + acc; traditional: scaled by J w w w
+    const double Jel = h0 * h1 * h2 / 8.0;
+    double tmax = 0.0;
+#pragma unroll
+    for (int it = 0; it < TAU3_NPT; ++it) {
+        const int t = tid + it * TAU3_BS;
+        if (t < nO) {
+            int i, j, k;
+            node_ijk(t, o1, o2, i, j, k);
+            double scale = 1.0;
+            if (P.formulation == 1) scale = Jel * c_w[o1 - 1][i] * c_w[o2 - 1][j] * c_w[o3 - 1][k];
+            const int ic = d == 0 ? i : (d == 1 ? j : k);
+            if (d == 0) i = 0; else if (d == 1) j = 0; else k = 0;
+            const int base = i + n1 * (j + n2 * k);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const double* rl = re + v * n + base;
+                double s = 0.0;
+                for (int a = 0; a < nd; ++a) s = fma(Ts[ic * nd + a], __ldg(rl + a * stride), s);
+                tmax = fmax(tmax, fabs(scale * (s + acc[it][v])));
+            }
+        }
+    }
+    tmax = block_max(tmax, red);
+    if (tid == 0) P.tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV + p] = tmax;
+}
+
+// tau[e][d][0] = ||Qdot_ref,e||_inf and NaN for p >= N_d (one CTA per element)
+__global__ void __launch_bounds__(128) k_tau_norm(const double* qref, double* tau, const int* orders,
+                                                  const long long* off)
+{
+    __shared__ double red[32];
+    const int e = blockIdx.x;
+    const int N1 = orders[3 * e], N2 = orders[3 * e + 1], N3 = orders[3 * e + 2];
+    const int n = (N1 + 1) * (N2 + 1) * (N3 + 1);
+    const double* re = qref + off[e];
+    double rn = 0.0;
+    for (int t = threadIdx.x; t < NV * n; t += blockDim.x) rn = fmax(rn, fabs(re[t]));
+    rn = block_max(rn, red);
+    if (threadIdx.x < 3 * DG_TAU_STRIDE_DEV) {
+        const int d = threadIdx.x / DG_TAU_STRIDE_DEV, p = threadIdx.x % DG_TAU_STRIDE_DEV;
+        const int Nd = d == 0 ? N1 : (d == 1 ? N2 : N3);
+        if (p == 0) tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV] = rn;
+        else if (p >= Nd) tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV + p] = __longlong_as_double(0x7ff8000000000000LL);
+    }
+}
+
+}  // namespace dgtau
