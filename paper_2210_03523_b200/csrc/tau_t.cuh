@@ -245,6 +245,78 @@ struct Tau3Params {
 constexpr int TAU3_BS = 256;
 constexpr int TAU3_NPT = 3;  // 256 * 3 >= 648 = max coarse level size (8 x 9 x 9)
 
+// All lines of one direction of a (5, o1, o2, o3) block, each thread one
+// (variable, line) task at a time; the D^{L-1} constants stay live across the
+// task loop (the switch selects the compile-time line length once).
+template <int L>
+__device__ __forceinline__ void sweep_lines(double* Fb, int nO, int o1, int o2, int dd)
+{
+    const int nlines = nO / L;
+    for (int task = threadIdx.x; task < NV * nlines; task += blockDim.x) {
+        const int v = task / nlines, l = task - v * nlines;
+        int base, str;
+        if (dd == 0) { base = l * L; str = 1; }
+        else if (dd == 1) { base = (l % o1) + o1 * L * (l / o1); str = o1; }
+        else { base = l; str = o1 * o2; }
+        dline_inplace<L>(Fb + v * nO + base, str);
+    }
+}
+
+__device__ __forceinline__ void sweep_dispatch(int L, double* Fb, int nO, int o1, int o2, int dd)
+{
+    switch (L) {
+        case 2: sweep_lines<2>(Fb, nO, o1, o2, dd); break;
+        case 3: sweep_lines<3>(Fb, nO, o1, o2, dd); break;
+        case 4: sweep_lines<4>(Fb, nO, o1, o2, dd); break;
+        case 5: sweep_lines<5>(Fb, nO, o1, o2, dd); break;
+        case 6: sweep_lines<6>(Fb, nO, o1, o2, dd); break;
+        case 7: sweep_lines<7>(Fb, nO, o1, o2, dd); break;
+        case 8: sweep_lines<8>(Fb, nO, o1, o2, dd); break;
+        default: sweep_lines<9>(Fb, nO, o1, o2, dd); break;
+    }
+}
+
+// Interpolation along d of the fine lines of 5 fields (fine line length ND,
+// p+1 coarse points): out[v][coarse node] for src = q or the reference
+// residual.  One (variable, line) task per thread; fine values read once.
+template <int ND>
+__device__ __forceinline__ void interp_lines(const double* __restrict__ src, int n, int stride_f, int n1, int n2,
+                                             double* out, int nO, int o1, int o2, int pc, int d, const double* Ts)
+{
+    const int nl = nO / pc;  // lines of the coarse block along d (= fine lines)
+    const int strc = d == 0 ? 1 : (d == 1 ? o1 : o1 * o2);
+    for (int task = threadIdx.x; task < NV * nl; task += blockDim.x) {
+        const int v = task / nl, l = task - v * nl;
+        int bf, bc;  // base of the line in the fine / coarse layouts
+        if (d == 0) { bf = l * n1; bc = l * pc; }
+        else if (d == 1) { const int i = l % n1, k = l / n1; bf = i + n1 * n2 * k; bc = i + o1 * pc * k; }
+        else { bf = l; bc = l; }
+        double f[ND];
+#pragma unroll
+        for (int a = 0; a < ND; ++a) f[a] = __ldg(src + (long long)v * n + bf + a * stride_f);
+        for (int ic = 0; ic < pc; ++ic) {
+            double s = Ts[ic * ND] * f[0];
+#pragma unroll
+            for (int a = 1; a < ND; ++a) s = fma(Ts[ic * ND + a], f[a], s);
+            out[v * nO + bc + ic * strc] = s;
+        }
+    }
+}
+
+__device__ __forceinline__ void interp_dispatch(int ND, const double* src, int n, int stride_f, int n1, int n2,
+                                                double* out, int nO, int o1, int o2, int pc, int d, const double* Ts)
+{
+    switch (ND) {
+        case 3: interp_lines<3>(src, n, stride_f, n1, n2, out, nO, o1, o2, pc, d, Ts); break;
+        case 4: interp_lines<4>(src, n, stride_f, n1, n2, out, nO, o1, o2, pc, d, Ts); break;
+        case 5: interp_lines<5>(src, n, stride_f, n1, n2, out, nO, o1, o2, pc, d, Ts); break;
+        case 6: interp_lines<6>(src, n, stride_f, n1, n2, out, nO, o1, o2, pc, d, Ts); break;
+        case 7: interp_lines<7>(src, n, stride_f, n1, n2, out, nO, o1, o2, pc, d, Ts); break;
+        case 8: interp_lines<8>(src, n, stride_f, n1, n2, out, nO, o1, o2, pc, d, Ts); break;
+        default: interp_lines<9>(src, n, stride_f, n1, n2, out, nO, o1, o2, pc, d, Ts); break;
+    }
+}
+
 __global__ void __launch_bounds__(TAU3_BS, 2) k_tau3(Tau3Params P)
 {
     extern __shared__ double sm[];
@@ -262,29 +334,16 @@ __global__ void __launch_bounds__(TAU3_BS, 2) k_tau3(Tau3Params P)
     const int o1 = d == 0 ? p + 1 : n1, o2 = d == 1 ? p + 1 : n2, o3 = d == 2 ? p + 1 : N3 + 1;
     const int nO = o1 * o2 * o3;
     const double h0 = P.hgeo[3 * e], h1 = P.hgeo[3 * e + 1], h2 = P.hgeo[3 * e + 2];
-    const double sc[3] = {2.0 / h0, 2.0 / h1, 2.0 / h2};
+    const double sc0 = 2.0 / h0, sc1 = 2.0 / h1, sc2 = 2.0 / h2;
     const long long o = P.off[e];
-    const double* qe = P.q + o;
-    const double* re = P.qref + o;
     double* Qc = sm;            // 5 nO coarse state
-    double* Fb = Qc + NV * nO;  // 5 nO flux / derivative
+    double* Rc = Qc + NV * nO;  // 5 nO interpolated reference residual
+    double* Fb = Rc + NV * nO;  // 5 nO flux / derivative
     for (int t = tid; t < (p + 1) * nd; t += TAU3_BS) Ts[t] = P.tab->T[Nd][p][t];
     __syncthreads();
-    // q_c = T^{N_d -> p} q along d  (reading A3: interpolation at the coarse nodes)
-    for (int t = tid; t < nO; t += TAU3_BS) {
-        int i, j, k;
-        node_ijk(t, o1, o2, i, j, k);
-        const int ic = d == 0 ? i : (d == 1 ? j : k);
-        if (d == 0) i = 0; else if (d == 1) j = 0; else k = 0;
-        const int base = i + n1 * (j + n2 * k);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            const double* ql = qe + v * n + base;
-            double s = 0.0;
-            for (int a = 0; a < nd; ++a) s = fma(Ts[ic * nd + a], __ldg(ql + a * stride), s);
-            Qc[v * nO + t] = s;
-        }
-    }
+    // q_c = T^{N_d -> p} q and T R along d (reading A3: interpolation at the coarse nodes)
+    interp_dispatch(nd, P.q + o, n, stride, n1, n2, Qc, nO, o1, o2, p + 1, d, Ts);
+    interp_dispatch(nd, P.qref + o, n, stride, n1, n2, Rc, nO, o1, o2, p + 1, d, Ts);
     __syncthreads();
     // isolated residual at the coarse orders: acc = sum_d' (2/h_d') D^{O_d'} f_d'(q_c)
     double acc[TAU3_NPT][NV];
@@ -312,23 +371,15 @@ __global__ void __launch_bounds__(TAU3_BS, 2) k_tau3(Tau3Params P)
             }
         }
         __syncthreads();
-        const int L = dd == 0 ? o1 : (dd == 1 ? o2 : o3);
-        const int nlines = nO / L;
-        for (int task = tid; task < NV * nlines; task += TAU3_BS) {
-            const int v = task / nlines, l = task - v * nlines;
-            int base, str;
-            if (dd == 0) { base = l * o1; str = 1; }
-            else if (dd == 1) { base = (l % o1) + o1 * o2 * (l / o1); str = o1; }
-            else { base = l; str = o1 * o2; }
-            dline_dispatch(L, Fb + v * nO + base, str);
-        }
+        sweep_dispatch(dd == 0 ? o1 : (dd == 1 ? o2 : o3), Fb, nO, o1, o2, dd);
         __syncthreads();
+        const double sc = dd == 0 ? sc0 : (dd == 1 ? sc1 : sc2);
 #pragma unroll
         for (int it = 0; it < TAU3_NPT; ++it) {
             const int t = tid + it * TAU3_BS;
             if (t < nO)
 #pragma unroll
-                for (int v = 0; v < NV; ++v) acc[it][v] = fma(sc[dd], Fb[v * nO + t], acc[it][v]);
+                for (int v = 0; v < NV; ++v) acc[it][v] = fma(sc, Fb[v * nO + t], acc[it][v]);
         }
     }
     // tau~ = T R - Qdot_c = T R + acc; traditional: scaled by J w w w
@@ -338,20 +389,14 @@ __global__ void __launch_bounds__(TAU3_BS, 2) k_tau3(Tau3Params P)
     for (int it = 0; it < TAU3_NPT; ++it) {
         const int t = tid + it * TAU3_BS;
         if (t < nO) {
-            int i, j, k;
-            node_ijk(t, o1, o2, i, j, k);
             double scale = 1.0;
-            if (P.formulation == 1) scale = Jel * c_w[o1 - 1][i] * c_w[o2 - 1][j] * c_w[o3 - 1][k];
-            const int ic = d == 0 ? i : (d == 1 ? j : k);
-            if (d == 0) i = 0; else if (d == 1) j = 0; else k = 0;
-            const int base = i + n1 * (j + n2 * k);
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const double* rl = re + v * n + base;
-                double s = 0.0;
-                for (int a = 0; a < nd; ++a) s = fma(Ts[ic * nd + a], __ldg(rl + a * stride), s);
-                tmax = fmax(tmax, fabs(scale * (s + acc[it][v])));
+            if (P.formulation == 1) {
+                int i, j, k;
+                node_ijk(t, o1, o2, i, j, k);
+                scale = Jel * c_w[o1 - 1][i] * c_w[o2 - 1][j] * c_w[o3 - 1][k];
             }
+#pragma unroll
+            for (int v = 0; v < NV; ++v) tmax = fmax(tmax, fabs(scale * (Rc[v * nO + t] + acc[it][v])));
         }
     }
     tmax = block_max(tmax, red);
