@@ -204,7 +204,7 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
     cudaFuncSetAttribute(k_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_tau, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_tau2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_tau3, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    cudaFuncSetAttribute(k_tau3, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
     cudaFuncSetAttribute(k_tau3, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(k_tau2, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(k_transfer, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -606,7 +606,7 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
             P.tab = ctx->d_tab;
             P.formulation = o->formulation;
             P.gm1 = ctx->prm.gamma - 1.0;
-            k_tau3<<<ctx->nlevels, TAU3_BS, sizeof(double) * 3 * NV * (size_t)ctx->max_level, st>>>(P);
+            k_tau3<<<ctx->nlevels, TAU3_BS, sizeof(double) * 5 * NV * (size_t)ctx->max_level, st>>>(P);
         }
     }
     ctx->launches++;

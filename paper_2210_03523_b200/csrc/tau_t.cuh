@@ -317,7 +317,7 @@ __device__ __forceinline__ void interp_dispatch(int ND, const double* src, int n
     }
 }
 
-__global__ void __launch_bounds__(TAU3_BS, 2) k_tau3(Tau3Params P)
+__global__ void __launch_bounds__(TAU3_BS, 4) k_tau3(Tau3Params P)
 {
     extern __shared__ double sm[];
     __shared__ double red[32];
@@ -334,69 +334,57 @@ __global__ void __launch_bounds__(TAU3_BS, 2) k_tau3(Tau3Params P)
     const int o1 = d == 0 ? p + 1 : n1, o2 = d == 1 ? p + 1 : n2, o3 = d == 2 ? p + 1 : N3 + 1;
     const int nO = o1 * o2 * o3;
     const double h0 = P.hgeo[3 * e], h1 = P.hgeo[3 * e + 1], h2 = P.hgeo[3 * e + 2];
-    const double sc0 = 2.0 / h0, sc1 = 2.0 / h1, sc2 = 2.0 / h2;
     const long long o = P.off[e];
-    double* Qc = sm;            // 5 nO coarse state
-    double* Rc = Qc + NV * nO;  // 5 nO interpolated reference residual
-    double* Fb = Rc + NV * nO;  // 5 nO flux / derivative
+    double* Qc = sm;              // 5 nO coarse state
+    double* Rc = Qc + NV * nO;    // 5 nO interpolated reference residual
+    double* F0 = Rc + NV * nO;    // 3 x 5 nO fluxes f_0, f_1, f_2, then their derivatives
+    double* F1 = F0 + NV * nO;
+    double* F2 = F1 + NV * nO;
     for (int t = tid; t < (p + 1) * nd; t += TAU3_BS) Ts[t] = P.tab->T[Nd][p][t];
     __syncthreads();
-    // q_c = T^{N_d -> p} q and T R along d (reading A3: interpolation at the coarse nodes)
+    // (A) q_c = T^{N_d -> p} q and T R along d (reading A3)
     interp_dispatch(nd, P.q + o, n, stride, n1, n2, Qc, nO, o1, o2, p + 1, d, Ts);
     interp_dispatch(nd, P.qref + o, n, stride, n1, n2, Rc, nO, o1, o2, p + 1, d, Ts);
     __syncthreads();
-    // isolated residual at the coarse orders: acc = sum_d' (2/h_d') D^{O_d'} f_d'(q_c)
-    double acc[TAU3_NPT][NV];
+    // (B) the three Cartesian fluxes of the coarse state
+    for (int t = tid; t < nO; t += TAU3_BS) {
+        double qv[NV], f[NV];
 #pragma unroll
-    for (int it = 0; it < TAU3_NPT; ++it)
+        for (int v = 0; v < NV; ++v) qv[v] = Qc[v * nO + t];
+        const double ir = 1.0 / qv[0];
+        const double pr = P.gm1 * (qv[4] - 0.5 * ir * (qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]));
+        flux_axis<0>(qv, ir, pr, f);
 #pragma unroll
-        for (int v = 0; v < NV; ++v) acc[it][v] = 0.0;
+        for (int v = 0; v < NV; ++v) F0[v * nO + t] = f[v];
+        flux_axis<1>(qv, ir, pr, f);
 #pragma unroll
-    for (int dd = 0; dd < 3; ++dd) {
-        if (dd > 0) __syncthreads();
+        for (int v = 0; v < NV; ++v) F1[v * nO + t] = f[v];
+        flux_axis<2>(qv, ir, pr, f);
 #pragma unroll
-        for (int it = 0; it < TAU3_NPT; ++it) {
-            const int t = tid + it * TAU3_BS;
-            if (t < nO) {
-                double qv[NV], f[NV];
-#pragma unroll
-                for (int v = 0; v < NV; ++v) qv[v] = Qc[v * nO + t];
-                const double ir = 1.0 / qv[0];
-                const double pr = P.gm1 * (qv[4] - 0.5 * ir * (qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]));
-                if (dd == 0) flux_axis<0>(qv, ir, pr, f);
-                else if (dd == 1) flux_axis<1>(qv, ir, pr, f);
-                else flux_axis<2>(qv, ir, pr, f);
-#pragma unroll
-                for (int v = 0; v < NV; ++v) Fb[v * nO + t] = f[v];
-            }
-        }
-        __syncthreads();
-        sweep_dispatch(dd == 0 ? o1 : (dd == 1 ? o2 : o3), Fb, nO, o1, o2, dd);
-        __syncthreads();
-        const double sc = dd == 0 ? sc0 : (dd == 1 ? sc1 : sc2);
-#pragma unroll
-        for (int it = 0; it < TAU3_NPT; ++it) {
-            const int t = tid + it * TAU3_BS;
-            if (t < nO)
-#pragma unroll
-                for (int v = 0; v < NV; ++v) acc[it][v] = fma(sc, Fb[v * nO + t], acc[it][v]);
-        }
+        for (int v = 0; v < NV; ++v) F2[v * nO + t] = f[v];
     }
-    // tau~ = T R - Qdot_c = T R + acc; traditional: scaled by J w w w
+    __syncthreads();
+    // (C) D^{O_d'} along each direction d' (independent buffers: no barrier between)
+    sweep_dispatch(o1, F0, nO, o1, o2, 0);
+    sweep_dispatch(o2, F1, nO, o1, o2, 1);
+    sweep_dispatch(o3, F2, nO, o1, o2, 2);
+    __syncthreads();
+    // (D) tau~ = T R - Qdot_c = T R + sum_d' (2/h_d') D f_d'; traditional * J w w w
+    const double sc0 = 2.0 / h0, sc1 = 2.0 / h1, sc2 = 2.0 / h2;
     const double Jel = h0 * h1 * h2 / 8.0;
     double tmax = 0.0;
+    for (int t = tid; t < nO; t += TAU3_BS) {
+        double scale = 1.0;
+        if (P.formulation == 1) {
+            int i, j, k;
+            node_ijk(t, o1, o2, i, j, k);
+            scale = Jel * c_w[o1 - 1][i] * c_w[o2 - 1][j] * c_w[o3 - 1][k];
+        }
 #pragma unroll
-    for (int it = 0; it < TAU3_NPT; ++it) {
-        const int t = tid + it * TAU3_BS;
-        if (t < nO) {
-            double scale = 1.0;
-            if (P.formulation == 1) {
-                int i, j, k;
-                node_ijk(t, o1, o2, i, j, k);
-                scale = Jel * c_w[o1 - 1][i] * c_w[o2 - 1][j] * c_w[o3 - 1][k];
-            }
-#pragma unroll
-            for (int v = 0; v < NV; ++v) tmax = fmax(tmax, fabs(scale * (Rc[v * nO + t] + acc[it][v])));
+        for (int v = 0; v < NV; ++v) {
+            const int ix = v * nO + t;
+            const double acc = fma(sc2, F2[ix], fma(sc1, F1[ix], sc0 * F0[ix]));
+            tmax = fmax(tmax, fabs(scale * (Rc[ix] + acc)));
         }
     }
     tmax = block_max(tmax, red);
