@@ -245,6 +245,18 @@ struct Tau3Params {
 constexpr int TAU3_BS = 256;
 constexpr int TAU3_NPT = 3;  // 256 * 3 >= 648 = max coarse level size (8 x 9 x 9)
 
+// Exact integer quotient a / b for 0 <= a < 4096, 1 <= b < 1024 from the
+// correctly rounded float reciprocal: the float product's absolute error
+// (< 4096 * 2^-23 < 5e-4) is below the distance 0.5/b >= 4.9e-4 of
+// (a + 0.5)/b to the nearest integer.  Avoids ~20-instruction integer division.
+__device__ __forceinline__ int fdiv(int a, float inv_b) { return __float2int_rz(((float)a + 0.5f) * inv_b); }
+
+// variable index of a (v, l) task, 0 <= task < 5 * nl, by comparisons
+__device__ __forceinline__ int var_of(int task, int nl)
+{
+    return (task >= nl) + (task >= 2 * nl) + (task >= 3 * nl) + (task >= 4 * nl);
+}
+
 // All lines of one direction of a (5, o1, o2, o3) block, each thread one
 // (variable, line) task at a time; the D^{L-1} constants stay live across the
 // task loop (the switch selects the compile-time line length once).
@@ -252,11 +264,12 @@ template <int L>
 __device__ __forceinline__ void sweep_lines(double* Fb, int nO, int o1, int o2, int dd)
 {
     const int nlines = nO / L;
+    const float inv_o1 = 1.0f / (float)o1;
     for (int task = threadIdx.x; task < NV * nlines; task += blockDim.x) {
-        const int v = task / nlines, l = task - v * nlines;
+        const int v = var_of(task, nlines), l = task - v * nlines;
         int base, str;
         if (dd == 0) { base = l * L; str = 1; }
-        else if (dd == 1) { base = (l % o1) + o1 * L * (l / o1); str = o1; }
+        else if (dd == 1) { const int kk = fdiv(l, inv_o1); base = (l - kk * o1) + o1 * L * kk; str = o1; }
         else { base = l; str = o1 * o2; }
         dline_inplace<L>(Fb + v * nO + base, str);
     }
@@ -285,11 +298,12 @@ __device__ __forceinline__ void interp_lines(const double* __restrict__ src, int
 {
     const int nl = nO / pc;  // lines of the coarse block along d (= fine lines)
     const int strc = d == 0 ? 1 : (d == 1 ? o1 : o1 * o2);
+    const float inv_n1 = 1.0f / (float)n1;
     for (int task = threadIdx.x; task < NV * nl; task += blockDim.x) {
-        const int v = task / nl, l = task - v * nl;
+        const int v = var_of(task, nl), l = task - v * nl;
         int bf, bc;  // base of the line in the fine / coarse layouts
         if (d == 0) { bf = l * n1; bc = l * pc; }
-        else if (d == 1) { const int i = l % n1, k = l / n1; bf = i + n1 * n2 * k; bc = i + o1 * pc * k; }
+        else if (d == 1) { const int k = fdiv(l, inv_n1), i = l - k * n1; bf = i + n1 * n2 * k; bc = i + o1 * pc * k; }
         else { bf = l; bc = l; }
         double f[ND];
 #pragma unroll
