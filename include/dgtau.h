@@ -131,6 +131,12 @@ dg_status dg_compute_dt(dg_ctx* ctx, const double* q_dev, double cfl, double* dt
 dg_status dg_rk_step(dg_ctx* ctx, double* q_in_dev, double* q_out_dev, double* g_dev, const double* dt_dev,
                      void* stream);
 
+/* As dg_rk_step, and the CFL time step of the NEW state q^{n+1} (P:474-475,
+ * reading A11) is reduced inside the last stage's kernel (no extra pass over
+ * the state) and written to dt_next_dev[0] (device, != dt_dev). */
+dg_status dg_rk_step_dt(dg_ctx* ctx, double* q_in_dev, double* q_out_dev, double* g_dev, const double* dt_dev,
+                        double cfl, double* dt_next_dev, void* stream);
+
 /* Batched tau-estimation over all coarse orders p < N_d of every element and
  * direction, isolated coarse residuals, in one launch.  qdot_ref_dev
  * is required for DG_REF_SOLVER and ignored for DG_REF_SAME.  tau_dev is

@@ -36,7 +36,7 @@ NMAX = 8
 
 EXPORTS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_upload", "dg_set_orders", "dg_state_len", "dg_ndof",
            "dg_node_coords", "dg_rhs_eval", "dg_compute_dt", "dg_rk_step", "dg_tau_estimate", "dg_select_orders",
-           "dg_transfer", "dg_diagnostics", "dg_launch_count"]
+           "dg_transfer", "dg_diagnostics", "dg_launch_count", "dg_rk_step_dt"]
 
 
 def sources():
@@ -234,6 +234,11 @@ class Solver:
     def rk_step(self, q_in, q_out, g, dt, stream=None):
         self._check(self.L.dg_rk_step(self.ctx, _ptr(q_in), _ptr(q_out), _ptr(g), _ptr(dt), _stream(stream)),
                     "dg_rk_step")
+
+    def rk_step_dt(self, q_in, q_out, g, dt, cfl, dt_next, stream=None):
+        """RK3 step; the CFL dt of the new state is reduced inside the last stage."""
+        self._check(self.L.dg_rk_step_dt(self.ctx, _ptr(q_in), _ptr(q_out), _ptr(g), _ptr(dt), C.c_double(cfl),
+                                         _ptr(dt_next), _stream(stream)), "dg_rk_step_dt")
 
     def tau_estimate(self, q, qdot_ref=None, formulation=TAU_NEW, reference=REF_SOLVER, tau=None, stream=None):
         import torch

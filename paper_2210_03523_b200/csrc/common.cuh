@@ -224,6 +224,8 @@ struct ResParams {
     const Tables* tab;
     PhysDev ph;
     int* flag;              // [0] admissibility violations, [1] element id
+    unsigned long long* lam_max;  // if set (last RK stage): max CFL rate of the NEW state (bits of a double >= 0)
+    double gamma;
 };
 
 __device__ __forceinline__ void node_ijk(int node, int n1, int n2, int& i, int& j, int& k)

@@ -74,6 +74,10 @@ struct dg_ctx {
     int nlevels = 0;
     int max_level = 0;
     double* d_ref_scratch = nullptr;  // isolated fine residual for DG_REF_SAME
+    int* d_tr_orders = nullptr;       // transfer scratch
+    long long* d_tr_off = nullptr;
+    std::vector<int> tr_orders_host;
+    std::vector<long long> tr_off_host;
     long long ref_len = 0;
     double* d_mortarG = nullptr;
     unsigned long long* d_scratch = nullptr;  // [8]
@@ -178,6 +182,7 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
     if ((s = cuda_check(ctx, cudaMalloc(&ctx->d_tab, sizeof(Tables)), "cudaMalloc tables")) != DG_OK ||
         (s = cuda_check(ctx, cudaMemcpy(ctx->d_tab, &t, sizeof(Tables), cudaMemcpyHostToDevice), "tables")) != DG_OK ||
         (s = cuda_check(ctx, cudaMalloc(&ctx->d_scratch, 8 * sizeof(unsigned long long)), "scratch")) != DG_OK ||
+        (s = cuda_check(ctx, cudaMemset(ctx->d_scratch, 0, 8 * sizeof(unsigned long long)), "scratch")) != DG_OK ||
         (s = cuda_check(ctx, cudaMalloc(&ctx->d_flag, 4 * sizeof(int)), "flag")) != DG_OK ||
         (s = cuda_check(ctx, cudaMemset(ctx->d_flag, 0, 4 * sizeof(int)), "flag")) != DG_OK ||
         (s = cuda_check(ctx, cudaMalloc(&ctx->d_sums, 8 * sizeof(double)), "sums")) != DG_OK) {
@@ -228,6 +233,8 @@ void dg_destroy(dg_ctx* ctx)
     dfree(ctx->d_slots);
     dfree(ctx->d_levels);
     dfree(ctx->d_ref_scratch);
+    dfree(ctx->d_tr_orders);
+    dfree(ctx->d_tr_off);
     dfree(ctx->d_mortarG);
     dfree(ctx->d_scratch);
     dfree(ctx->d_flag);
@@ -456,7 +463,7 @@ dg_status dg_node_coords(dg_ctx* ctx, double* X)
 }
 
 static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, double* out, double* g, const double* dt,
-                                 double A, double B, int mode, cudaStream_t st)
+                                 double A, double B, int mode, cudaStream_t st, unsigned long long* lam_max = nullptr)
 {
     if (variant == DG_NONISOLATED && ctx->nmortar > 0) {
         MortarParams M;
@@ -493,6 +500,9 @@ static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, doub
     P.tab = ctx->d_tab;
     P.ph = phys_dev(ctx->prm);
     P.flag = ctx->d_flag;
+    P.lam_max = lam_max;
+    P.gamma = ctx->prm.gamma;
+    if (ctx->generic && lam_max) return fail(ctx, DG_EUNSUPPORTED, "fused dt needs the specialised kernels");
     if (ctx->generic) {
         k_residual<<<ctx->nwork, BLOCK, ctx->res_smem, st>>>(P);
         ctx->launches++;
@@ -520,6 +530,7 @@ dg_status dg_compute_dt(dg_ctx* ctx, const double* q_dev, double cfl, double* dt
     if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "compute_dt: orders not set");
     cudaStream_t st = (cudaStream_t)stream;
     CK(cudaMemsetAsync(ctx->d_scratch, 0, sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(ctx->d_scratch + 4, 0, sizeof(unsigned long long), st));  // fused-dt accumulator
     DtParams P;
     P.q = q_dev;
     P.work = ctx->d_work;
@@ -559,6 +570,28 @@ dg_status dg_rk_step(dg_ctx* ctx, double* q_in, double* q_out, double* g, const 
     return DG_OK;
 }
 
+dg_status dg_rk_step_dt(dg_ctx* ctx, double* q_in, double* q_out, double* g, const double* dt_dev, double cfl,
+                        double* dt_next_dev, void* stream)
+{
+    if (!ctx || !q_in || !q_out || !g || !dt_dev || !dt_next_dev || q_in == q_out || dt_next_dev == dt_dev || !(cfl > 0))
+        return DG_EINVAL;
+    if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "rk_step_dt: orders not set");
+    if (ctx->prm.physics != DG_EULER) return fail(ctx, DG_EUNSUPPORTED, "rk_step_dt: NS not in this build");
+    static const double A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
+    static const double B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
+    cudaStream_t st = (cudaStream_t)stream;
+    double* src[3] = {q_in, q_out, q_in};
+    double* dst[3] = {q_out, q_in, q_out};
+    for (int k = 0; k < 3; ++k) {
+        dg_status s = launch_residual(ctx, DG_NONISOLATED, src[k], dst[k], g, dt_dev, A[k], B[k], 1, st,
+                                      k == 2 ? ctx->d_scratch + 4 : nullptr);
+        if (s != DG_OK) return s;
+    }
+    k_dt_final<<<1, 1, 0, st>>>(ctx->d_scratch + 4, cfl, dt_next_dev);
+    ctx->launches++;
+    return check_stream_error(ctx, "k_dt_final launch");
+}
+
 dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev, const double* qref_dev, double* tau_dev,
                           void* stream)
 {
@@ -585,6 +618,8 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
         if (o->reference == DG_REF_SAME) {  // isolated fine residual first (reading A4)
             if (ctx->ref_len < ctx->off[ctx->E]) {
                 dfree(ctx->d_ref_scratch);
+    dfree(ctx->d_tr_orders);
+    dfree(ctx->d_tr_off);
                 CK(cudaMalloc(&ctx->d_ref_scratch, sizeof(double) * ctx->off[ctx->E]));
                 ctx->ref_len = ctx->off[ctx->E];
             }
@@ -666,18 +701,23 @@ dg_status dg_transfer(dg_ctx* ctx, const int32_t* new_orders, const double* q_ol
     if (!ctx || !new_orders || !q_old || !q_new) return DG_EINVAL;
     if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "transfer: orders not set");
     const int E = ctx->E;
-    std::vector<long long> offn(E + 1, 0);
+    std::vector<long long>& offn = ctx->tr_off_host;  // persistent: outlives the async copy
+    offn.assign(E + 1, 0);
     for (int e = 0; e < E; ++e) {
         for (int d = 0; d < 3; ++d)
             if (new_orders[3 * e + d] < 1 || new_orders[3 * e + d] > NMAX) return fail(ctx, DG_EINVAL, "transfer: order");
         offn[e + 1] = offn[e] + (long long)NV * npts(&new_orders[3 * e]);
     }
     cudaStream_t st = (cudaStream_t)stream;
-    int* d_on = nullptr;
-    long long* d_offn = nullptr;
-    std::vector<int> on(new_orders, new_orders + 3LL * E);
-    CK(upload(d_on, on));
-    CK(upload(d_offn, offn));
+    if (!ctx->d_tr_orders) {
+        CK(cudaMalloc(&ctx->d_tr_orders, sizeof(int) * 3LL * E));
+        CK(cudaMalloc(&ctx->d_tr_off, sizeof(long long) * (E + 1)));
+    }
+    int* d_on = ctx->d_tr_orders;
+    long long* d_offn = ctx->d_tr_off;
+    ctx->tr_orders_host.assign(new_orders, new_orders + 3LL * E);
+    CK(cudaMemcpyAsync(d_on, ctx->tr_orders_host.data(), sizeof(int) * 3LL * E, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_offn, offn.data(), sizeof(long long) * (E + 1), cudaMemcpyHostToDevice, st));
     TransferParams P;
     P.qold = q_old;
     P.qnew = q_new;
@@ -688,11 +728,7 @@ dg_status dg_transfer(dg_ctx* ctx, const int32_t* new_orders, const double* q_ol
     P.tab = ctx->d_tab;
     k_transfer<<<E, BLOCK, sizeof(double) * 3 * NV * NP * NP * NP, st>>>(P);
     ctx->launches++;
-    dg_status s = check_stream_error(ctx, "k_transfer launch");
-    CK(cudaStreamSynchronize(st));
-    dfree(d_on);
-    dfree(d_offn);
-    return s;
+    return check_stream_error(ctx, "k_transfer launch");
 }
 
 dg_status dg_diagnostics(dg_ctx* ctx, const double* q_dev, const double* v_dev, double* sums_host, double* minrp_host,

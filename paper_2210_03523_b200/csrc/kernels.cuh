@@ -323,9 +323,10 @@ __global__ void __launch_bounds__(BLOCK) k_dt(DtParams P)
     if (threadIdx.x == 0) atomicMax(P.maxbits, (unsigned long long)__double_as_longlong(lmax));
 }
 
-__global__ void k_dt_final(const unsigned long long* maxbits, double cfl, double* dt)
+__global__ void k_dt_final(unsigned long long* maxbits, double cfl, double* dt)
 {
     dt[0] = cfl / __longlong_as_double((long long)maxbits[0]);
+    maxbits[0] = 0ull;  // ready for the next accumulation
 }
 
 // ---------------------------------------------------------------------------

@@ -334,6 +334,7 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
 
     // ---- epilogue per node --------------------------------------------------
     const double dt = P.mode ? *P.dt : 0.0;
+    double lmax = 0.0;
     if (need_g) asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // own g values only
 #pragma unroll
     for (int it = 0; it < NPTT; ++it) {
@@ -368,13 +369,30 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
             for (int v = 0; v < NV; ++v) o[v * n] = -accv[v];
         } else {
             double* g = P.g + s_off[slot] + node;
+            double qn[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
                 const double gn = (need_g ? P.rkA * GB[(slot * NV + v) * n + node] : 0.0) - dt * accv[v];
                 g[v * n] = gn;
-                o[v * n] = Q[(slot * NV + v) * n + node] + P.rkB * gn;
+                qn[v] = Q[(slot * NV + v) * n + node] + P.rkB * gn;
+                o[v * n] = qn[v];
+            }
+            if (P.lam_max) {  // CFL rate of q^{n+1} (reading A11), fused
+                const double ir = 1.0 / qn[0];
+                const double p = (P.gamma - 1.0) * (qn[4] - 0.5 * ir * (qn[1] * qn[1] + qn[2] * qn[2] + qn[3] * qn[3]));
+                const double c = sqrt(P.gamma * p * ir);
+                constexpr double L1 = (double)n1 * n1, L2 = (double)n2 * n2, L3 = (double)n3 * n3;
+                const double lam = 0.5 * ((fabs(qn[1] * ir) + c) * L1 * s_sc[slot][0] +
+                                          (fabs(qn[2] * ir) + c) * L2 * s_sc[slot][1] +
+                                          (fabs(qn[3] * ir) + c) * L3 * s_sc[slot][2]);
+                lmax = fmax(lmax, lam);
             }
         }
+    }
+    if (P.lam_max) {
+        __shared__ double red[32];
+        lmax = block_max(lmax, red);
+        if (threadIdx.x == 0) atomicMax(P.lam_max, (unsigned long long)__double_as_longlong(lmax));
     }
 }
 

@@ -121,6 +121,27 @@ def test_rk3_cfg1_trajectory(dg, orc):
     assert rel_linf(qa.cpu().numpy(), qo, orders) < RES_TOL
 
 
+def test_rk3_fused_dt(dg, orc):
+    """dg_rk_step_dt: the next step's CFL dt reduced inside the last RK stage
+    equals the oracle's dt of the new state; trajectory as cfg1."""
+    import torch
+
+    mesh, orders, kw = CASES["cfg3_subbox_mixed"]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, **kw)
+    qa, qb, g = qd.clone(), torch.empty_like(qd), torch.empty_like(qd)
+    dts = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in range(2)]
+    S.compute_dt(qa, 0.5, dts[0])
+    qo = q.copy()
+    for step in range(4):
+        dto = P.dt(orders, qo, 0.5)
+        assert abs(dts[step % 2].item() - dto) <= 1e-14 * dto
+        S.rk_step_dt(qa, qb, g, dts[step % 2], 0.5, dts[(step + 1) % 2])
+        qa, qb = qb, qa
+        qo = P.rk3_step(orders, qo, dto)
+    assert rel_linf(qa.cpu().numpy(), qo, orders) < RES_TOL
+    assert abs(dts[0].item() - P.dt(orders, qo, 0.5)) <= 1e-14 * dts[0].item()
+
+
 def test_rk3_mixed_orders(dg, orc):
     import torch
 
