@@ -1,0 +1,800 @@
+// curved.cuh -- generic (runtime-order) sm_100a kernels for curved elements
+// and the compressible Navier-Stokes equations with BR1 (cfg4 / cfg5).
+//
+// PAPER.md: P:106-126 (advection-diffusion split, first-order system with
+// g = grad q), P:129-145 (eqs DGSEMsystem:1-2: weak form of the flux
+// divergence and of the BR1 lifting of the gradient), P:144 (Jacobians of the
+// geometry transformation), P:472 (Roe advective flux, BR1 diffusive flux).
+// Readings A6 (mortars, metric from the L side's geometry), A8 (gradients of
+// the conserved variables), A9 (nondimensionalisation), A10 (wall / far-field
+// states), A11 (CFL / DFL), as in DESIGN.md.
+//
+// Metric terms (cross-product form, exact for the extruded meshes here):
+//   Ja^1 = x_eta x x_zeta, Ja^2 = x_zeta x x_xi, Ja^3 = x_xi x x_eta,
+//   J = x_xi . (x_eta x x_zeta),
+// with x the interpolant at the solution nodes of the geometry polynomial and
+// derivatives by D^N (as the oracle).  Per node 10 doubles: Ja^d_k at
+// 3d+k, J at 9 (offset 2 x the state offset of the element).
+// Gradient field: 15 doubles per node, [k][v] = d q_v / d x_k (offset 3 x).
+//
+// Strong form on the device (equal to the weak form for GL nodes):
+//   J g_k = sum_d D^d (Ja^d_k q) + lifting of (qhat Ja^d_k|_face - q Ja^d_k|_own)/w
+//   J Qdot = -sum_d D^d Ft^d - lifting of (G - Ft^d_own)/w,
+//   Ft^d = Ja^d . (f^a - f^nu),
+//   G = |Ja_f| Roe(q_L, q_R; n) - 1/2 (f^nu_L + f^nu_R) . Ja_f   (BR1 average).
+#pragma once
+
+#include "common.cuh"
+
+namespace dgtau {
+
+constexpr int CBS = 256;  // threads per CTA of the curved kernels
+
+struct CurvedMesh {
+    const double* geo;   // [E][3][ng] geometry nodes
+    int g1, g2, g3, ng;  // geometry orders and node count
+};
+
+// viscous flux along vector a (f^nu . a), A8-A9: stresses from conserved gradients
+__device__ __forceinline__ void visc_dot(const double* q, const double* g /*[15] k*5+v*/, double ax, double ay,
+                                         double az, const PhysDev& ph, double* fv)
+{
+    const double gam = ph.gamma, mu = ph.mu;
+    const double ir = 1.0 / q[0];
+    const double u = q[1] * ir, v = q[2] * ir, w = q[3] * ir;
+    const double p = (gam - 1.0) * (q[4] - 0.5 * q[0] * (u * u + v * v + w * w));
+    const double T = p * ir;
+    double du[3][3], dT[3];  // du[i][j] = d u_i / d x_j
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const double* gj = g + 5 * j;
+        du[0][j] = (gj[1] - u * gj[0]) * ir;
+        du[1][j] = (gj[2] - v * gj[0]) * ir;
+        du[2][j] = (gj[3] - w * gj[0]) * ir;
+        const double dp = (gam - 1.0) * (gj[4] - (u * gj[1] + v * gj[2] + w * gj[3]) + 0.5 * (u * u + v * v + w * w) * gj[0]);
+        dT[j] = (dp - T * gj[0]) * ir;
+    }
+    const double div = du[0][0] + du[1][1] + du[2][2];
+    const double kappa = mu * gam / ((gam - 1.0) * ph.Pr);
+    const double a[3] = {ax, ay, az};
+    double ta[3];  // tau . a
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) s += mu * (du[i][j] + du[j][i] - (i == j ? 2.0 / 3.0 * div : 0.0)) * a[j];
+        ta[i] = s;
+    }
+    fv[0] = 0.0;
+    fv[1] = ta[0];
+    fv[2] = ta[1];
+    fv[3] = ta[2];
+    fv[4] = u * ta[0] + v * ta[1] + w * ta[2] + kappa * (dT[0] * ax + dT[1] * ay + dT[2] * az);
+}
+
+// advective flux along vector a
+__device__ __forceinline__ void adv_dot(const double* q, double ax, double ay, double az, double gm1, double* f)
+{
+    const double ir = 1.0 / q[0];
+    const double p = gm1 * (q[4] - 0.5 * ir * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]));
+    const double ua = (q[1] * ax + q[2] * ay + q[3] * az) * ir;
+    f[0] = q[0] * ua;
+    f[1] = q[1] * ua + p * ax;
+    f[2] = q[2] * ua + p * ay;
+    f[3] = q[3] * ua + p * az;
+    f[4] = (q[4] + p) * ua;
+}
+
+// Ft = a . (f^a - f^nu)
+__device__ __forceinline__ void contra_flux(const double* q, const double* g, double ax, double ay, double az,
+                                            const PhysDev& ph, double* F)
+{
+    adv_dot(q, ax, ay, az, ph.gm1, F);
+    if (ph.physics == 1) {
+        double fv[NV];
+        visc_dot(q, g, ax, ay, az, ph, fv);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) F[v] -= fv[v];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Element geometry at orders (o1,o2,o3): X = T^{g->o} Xgeo (3 x no, smem),
+// then metrics via D^o (written to Mout[c*no + node]).  All CTA threads.
+// ---------------------------------------------------------------------------
+__device__ void element_metrics(const CurvedMesh& cm, int e, int o1, int o2, int o3, const Tables* tab, double* Xs,
+                                double* Mout)
+{
+    const int no = o1 * o2 * o3;
+    const int ga = cm.g1 + 1, gb = cm.g2 + 1;
+    const double* G = cm.geo + (long long)e * 3 * cm.ng;
+    const double* T1 = tab->T[cm.g1][o1 - 1];
+    const double* T2 = tab->T[cm.g2][o2 - 1];
+    const double* T3 = tab->T[cm.g3][o3 - 1];
+    for (int t = threadIdx.x; t < no; t += blockDim.x) {
+        int i, j, k;
+        node_ijk(t, o1, o2, i, j, k);
+        double x[3] = {0.0, 0.0, 0.0};
+        for (int c = 0; c <= cm.g3; ++c)
+            for (int b = 0; b <= cm.g2; ++b)
+                for (int a = 0; a <= cm.g1; ++a) {
+                    const double wgt = T1[i * ga + a] * T2[j * gb + b] * T3[k * (cm.g3 + 1) + c];
+                    const int gi = a + ga * (b + gb * c);
+                    x[0] += wgt * __ldg(G + gi);
+                    x[1] += wgt * __ldg(G + cm.ng + gi);
+                    x[2] += wgt * __ldg(G + 2 * cm.ng + gi);
+                }
+        Xs[t] = x[0];
+        Xs[no + t] = x[1];
+        Xs[2 * no + t] = x[2];
+    }
+    __syncthreads();
+    const double* D1 = tab->D[o1 - 1];
+    const double* D2 = tab->D[o2 - 1];
+    const double* D3 = tab->D[o3 - 1];
+    for (int t = threadIdx.x; t < no; t += blockDim.x) {
+        int i, j, k;
+        node_ijk(t, o1, o2, i, j, k);
+        double dx[3][3];  // dx[dd][c] = d x_c / d xi_dd
+        for (int c = 0; c < 3; ++c) {
+            const double* X = Xs + c * no;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+            for (int m = 0; m < o1; ++m) s0 += D1[i * o1 + m] * X[m + o1 * (j + o2 * k)];
+            for (int m = 0; m < o2; ++m) s1 += D2[j * o2 + m] * X[i + o1 * (m + o2 * k)];
+            for (int m = 0; m < o3; ++m) s2 += D3[k * o3 + m] * X[i + o1 * (j + o2 * m)];
+            dx[0][c] = s0;
+            dx[1][c] = s1;
+            dx[2][c] = s2;
+        }
+        const double* xa = dx[0];
+        const double* xb = dx[1];
+        const double* xc = dx[2];
+        const double c1[3] = {xb[1] * xc[2] - xb[2] * xc[1], xb[2] * xc[0] - xb[0] * xc[2], xb[0] * xc[1] - xb[1] * xc[0]};
+        const double c2[3] = {xc[1] * xa[2] - xc[2] * xa[1], xc[2] * xa[0] - xc[0] * xa[2], xc[0] * xa[1] - xc[1] * xa[0]};
+        const double c3[3] = {xa[1] * xb[2] - xa[2] * xb[1], xa[2] * xb[0] - xa[0] * xb[2], xa[0] * xb[1] - xa[1] * xb[0]};
+        for (int q = 0; q < 3; ++q) {
+            Mout[q * no + t] = c1[q];
+            Mout[(3 + q) * no + t] = c2[q];
+            Mout[(6 + q) * no + t] = c3[q];
+        }
+        Mout[9 * no + t] = xa[0] * c1[0] + xa[1] * c1[1] + xa[2] * c1[2];
+    }
+    __syncthreads();
+}
+
+struct MetParams {
+    CurvedMesh cm;
+    const int* orders;
+    const long long* off;  // state offsets (metrics at 2x)
+    double* met;
+    const Tables* tab;
+};
+
+__global__ void __launch_bounds__(CBS) k_metrics(MetParams P)
+{
+    extern __shared__ double sm[];
+    const int e = blockIdx.x;
+    const int o1 = P.orders[3 * e] + 1, o2 = P.orders[3 * e + 1] + 1, o3 = P.orders[3 * e + 2] + 1;
+    const int no = o1 * o2 * o3;
+    double* Xs = sm;
+    double* Ms = sm + 3 * no;
+    element_metrics(P.cm, e, o1, o2, o3, P.tab, Xs, Ms);
+    double* out = P.met + 2 * P.off[e];
+    for (int t = threadIdx.x; t < 10 * no; t += blockDim.x) out[t] = Ms[t];
+}
+
+// ---------------------------------------------------------------------------
+// generic sweep helpers: acc[c][node] (+)= sum_m D^{o_d}[a][m] F[c][..m..]
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double dsum(const double* Dd, int od, int a, const double* Fl, int stride)
+{
+    double s = 0.0;
+    for (int m = 0; m < od; ++m) s += Dd[a * od + m] * Fl[m * stride];
+    return s;
+}
+
+struct CurvedParams {
+    const double* q;
+    double* out;            // mode 0: qdot / grad (k_grad); mode 1: q' (RK)
+    double* g;              // RK register
+    const double* dt;
+    double rkA, rkB;
+    int mode, variant;
+    const int* orders;
+    const long long* off;
+    const FaceInfo* finfo;
+    const double* met;      // metrics (2x offsets)
+    const double* grad;     // gradients (3x offsets), NS
+    const double* mortarG;  // projected mortar fluxes (5 per point) or gradient terms (15 per point)
+    const Tables* tab;
+    PhysDev ph;
+    int* flag;
+    unsigned long long* lam_max;  // CFL / DFL rates of the new state (2 slots), last RK stage
+};
+
+__device__ __forceinline__ int face_nodes(int d, int n1, int n2, int n3) { return d == 0 ? n2 * n3 : (d == 1 ? n1 * n3 : n1 * n2); }
+
+// own boundary node of face (d, s) at tangential point pt
+__device__ __forceinline__ int face_node(int d, int s, int pt, int n1, int n2, int n3)
+{
+    int i, j, k;
+    if (d == 0) { i = s ? n1 - 1 : 0; j = pt % n2; k = pt / n2; }
+    else if (d == 1) { i = pt % n1; j = s ? n2 - 1 : 0; k = pt / n1; }
+    else { i = pt % n1; j = pt / n1; k = s ? n3 - 1 : 0; }
+    return i + n1 * (j + n2 * k);
+}
+
+// ---------------------------------------------------------------------------
+// BR1 gradient (eq DGSEMsystem:2), non-isolated or isolated, per element.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(CBS) k_grad(CurvedParams P)
+{
+    extern __shared__ double sm[];
+    const int e = blockIdx.x;
+    const int n1 = P.orders[3 * e] + 1, n2 = P.orders[3 * e + 1] + 1, n3 = P.orders[3 * e + 2] + 1;
+    const int n = n1 * n2 * n3;
+    const long long o = P.off[e];
+    const double* M = P.met + 2 * o;
+    double* Q = sm;          // 5n
+    double* F = Q + NV * n;  // 5n
+    double* GA = F + NV * n; // 15n
+    for (int t = threadIdx.x; t < NV * n; t += CBS) Q[t] = P.q[o + t];
+    for (int t = threadIdx.x; t < 15 * n; t += CBS) GA[t] = 0.0;
+    __syncthreads();
+    for (int d = 0; d < 3; ++d) {
+        const int od = d == 0 ? n1 : (d == 1 ? n2 : n3);
+        const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
+        const double* Dd = P.tab->D[od - 1];
+        for (int k = 0; k < 3; ++k) {
+            for (int t = threadIdx.x; t < n; t += CBS) {
+                const double jak = __ldg(M + (3 * d + k) * n + t);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) F[v * n + t] = jak * Q[v * n + t];
+            }
+            __syncthreads();
+            for (int t = threadIdx.x; t < n; t += CBS) {
+                int ijk[3];
+                node_ijk(t, n1, n2, ijk[0], ijk[1], ijk[2]);
+                const int a = d == 0 ? ijk[0] : (d == 1 ? ijk[1] : ijk[2]);
+                const int base = t - a * stride;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) GA[(k * NV + v) * n + t] += dsum(Dd, od, a, F + v * n + base, stride);
+            }
+            __syncthreads();
+        }
+        // lifting on the two faces normal to d: (qhat Ja_f - q_own Ja_own)/w
+        const int nf = face_nodes(d, n1, n2, n3);
+        for (int task = threadIdx.x; task < 2 * nf; task += CBS) {
+            const int s = task >= nf, pt = task - s * nf, f = 2 * d + s;
+            const int node = face_node(d, s, pt, n1, n2, n3);
+            double qo[NV], qh[NV], jo[3], jf[3];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) qo[v] = Q[v * n + node];
+            for (int c = 0; c < 3; ++c) jo[c] = __ldg(M + (3 * d + c) * n + node);
+            const FaceInfo fi = P.finfo[6 * e + f];
+            if (P.variant == 1) {  // isolated: qhat = own trace
+                for (int v = 0; v < NV; ++v) qh[v] = qo[v];
+                for (int c = 0; c < 3; ++c) jf[c] = jo[c];
+            } else if (fi.kind == 1) {  // mortar: projected qhat Ja_f terms
+                const double* src = P.mortarG + 3 * fi.off + pt;
+                const double w = s ? 1.0 : -1.0;
+                const double sc = w / P.tab->w[od - 1][0];
+                for (int c = 0; c < 3; ++c)
+                    for (int v = 0; v < NV; ++v)
+                        GA[(c * NV + v) * n + node] += sc * (src[(long long)(c * NV + v) * fi.n] - qo[v] * jo[c]);
+                continue;
+            } else if (fi.kind >= 2) {
+                for (int c = 0; c < 3; ++c) jf[c] = jo[c];
+                if (fi.kind == 2) {  // wall: zero velocity, keep rho and internal energy
+                    qh[0] = qo[0]; qh[1] = 0.0; qh[2] = 0.0; qh[3] = 0.0;
+                    qh[4] = qo[4] - 0.5 * (qo[1] * qo[1] + qo[2] * qo[2] + qo[3] * qo[3]) / qo[0];
+                } else {
+                    for (int v = 0; v < NV; ++v) qh[v] = 0.5 * (qo[v] + P.ph.qinf[v]);
+                }
+            } else {
+                const long long nb_node = fi.base + (long long)(d == 0 ? pt % n2 : pt % n1) * fi.sa +
+                                          (long long)(d == 0 ? pt / n2 : pt / n1) * fi.sb;
+                const double* qn = P.q + fi.off + nb_node;
+                for (int v = 0; v < NV; ++v) qh[v] = 0.5 * (qo[v] + __ldg(qn + (long long)v * fi.n));
+                if (s) {
+                    for (int c = 0; c < 3; ++c) jf[c] = jo[c];
+                } else {  // face metric from the L side (the neighbour)
+                    const double* Mn = P.met + 2 * fi.off + nb_node;
+                    for (int c = 0; c < 3; ++c) jf[c] = __ldg(Mn + (long long)(3 * d + c) * fi.n);
+                }
+            }
+            const double sc = (s ? 1.0 : -1.0) / P.tab->w[od - 1][0];
+            for (int c = 0; c < 3; ++c)
+                for (int v = 0; v < NV; ++v) GA[(c * NV + v) * n + node] += sc * (qh[v] * jf[c] - qo[v] * jo[c]);
+        }
+        __syncthreads();
+    }
+    double* out = P.out + 3 * o;
+    for (int t = threadIdx.x; t < n; t += CBS) {
+        const double iJ = 1.0 / __ldg(M + 9 * n + t);
+        for (int c = 0; c < 15; ++c) out[c * n + t] = GA[c * n + t] * iJ;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Curved residual / RK stage (Euler or NS), per element.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void load_grad(const double* base, int stride, double* g)
+{
+#pragma unroll
+    for (int c = 0; c < 15; ++c) g[c] = __ldg(base + (long long)c * stride);
+}
+
+__global__ void __launch_bounds__(CBS) k_res_curved(CurvedParams P)
+{
+    extern __shared__ double sm[];
+    __shared__ double red[32];
+    const int e = blockIdx.x;
+    const int n1 = P.orders[3 * e] + 1, n2 = P.orders[3 * e + 1] + 1, n3 = P.orders[3 * e + 2] + 1;
+    const int n = n1 * n2 * n3;
+    const long long o = P.off[e];
+    const double* M = P.met + 2 * o;
+    const bool ns = P.ph.physics == 1;
+    const double* GR = ns ? P.grad + 3 * o : nullptr;
+    double* Q = sm;            // 5n
+    double* F = Q + NV * n;    // 5n
+    double* A = F + NV * n;    // 5n
+    for (int t = threadIdx.x; t < NV * n; t += CBS) {
+        Q[t] = P.q[o + t];
+        A[t] = 0.0;
+    }
+    __syncthreads();
+    for (int d = 0; d < 3; ++d) {
+        const int od = d == 0 ? n1 : (d == 1 ? n2 : n3);
+        const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
+        const double* Dd = P.tab->D[od - 1];
+        for (int t = threadIdx.x; t < n; t += CBS) {
+            double qv[NV], gv[15], Fv[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) qv[v] = Q[v * n + t];
+            if (ns) load_grad(GR + t, n, gv);
+            contra_flux(qv, gv, __ldg(M + (3 * d) * n + t), __ldg(M + (3 * d + 1) * n + t), __ldg(M + (3 * d + 2) * n + t),
+                        P.ph, Fv);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) F[v * n + t] = Fv[v];
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < n; t += CBS) {
+            int ijk[3];
+            node_ijk(t, n1, n2, ijk[0], ijk[1], ijk[2]);
+            const int a = d == 0 ? ijk[0] : (d == 1 ? ijk[1] : ijk[2]);
+            const int base = t - a * stride;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) A[v * n + t] += dsum(Dd, od, a, F + v * n + base, stride);
+        }
+        __syncthreads();
+        if (P.variant == 0) {  // surface terms (isolated: G == Ft_own, no contribution)
+            const int nf = face_nodes(d, n1, n2, n3);
+            for (int task = threadIdx.x; task < 2 * nf; task += CBS) {
+                const int s = task >= nf, pt = task - s * nf, f = 2 * d + s;
+                const int node = face_node(d, s, pt, n1, n2, n3);
+                double qo[NV], go[15], jo[3], Fo[NV], G[NV];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) qo[v] = Q[v * n + node];
+                if (ns) load_grad(GR + node, n, go);
+                for (int c = 0; c < 3; ++c) jo[c] = __ldg(M + (3 * d + c) * n + node);
+                contra_flux(qo, go, jo[0], jo[1], jo[2], P.ph, Fo);
+                const FaceInfo fi = P.finfo[6 * e + f];
+                if (fi.kind == 1) {
+                    const double* src = P.mortarG + fi.off + pt;
+                    for (int v = 0; v < NV; ++v) G[v] = src[(long long)v * fi.n];
+                } else {
+                    double qx[NV], gx[15], jf[3];
+                    if (fi.kind >= 2) {
+                        for (int c = 0; c < 3; ++c) jf[c] = jo[c];
+                        ghost_state(qo, fi.kind == 2 ? -1 : -2, P.ph, qx);
+                    } else {
+                        const long long nb_node = fi.base + (long long)(d == 0 ? pt % n2 : pt % n1) * fi.sa +
+                                                  (long long)(d == 0 ? pt / n2 : pt / n1) * fi.sb;
+                        const double* qn = P.q + fi.off + nb_node;
+                        for (int v = 0; v < NV; ++v) qx[v] = __ldg(qn + (long long)v * fi.n);
+                        if (ns) load_grad(P.grad + 3 * fi.off + nb_node, fi.n, gx);
+                        if (s) {
+                            for (int c = 0; c < 3; ++c) jf[c] = jo[c];
+                        } else {
+                            const double* Mn = P.met + 2 * fi.off + nb_node;
+                            for (int c = 0; c < 3; ++c) jf[c] = __ldg(Mn + (long long)(3 * d + c) * fi.n);
+                        }
+                    }
+                    const double S = sqrt(jf[0] * jf[0] + jf[1] * jf[1] + jf[2] * jf[2]);
+                    const double nrm[3] = {jf[0] / S, jf[1] / S, jf[2] / S};
+                    if (s) riemann(qo, qx, nrm, P.ph, G); else riemann(qx, qo, nrm, P.ph, G);
+                    for (int v = 0; v < NV; ++v) G[v] *= S;
+                    if (ns) {
+                        double fo[NV], fx[NV];
+                        visc_dot(qo, go, jf[0], jf[1], jf[2], P.ph, fo);
+                        if (fi.kind == 2) {  // wall: viscous flux from the inner gradient, u = 0, adiabatic
+                            fo[4] = 0.0;
+                            for (int v = 0; v < NV; ++v) G[v] -= fo[v];
+                        } else if (fi.kind == 3) {  // far field: inner viscous flux
+                            for (int v = 0; v < NV; ++v) G[v] -= fo[v];
+                        } else {  // BR1 average
+                            visc_dot(qx, gx, jf[0], jf[1], jf[2], P.ph, fx);
+                            for (int v = 0; v < NV; ++v) G[v] -= 0.5 * (fo[v] + fx[v]);
+                        }
+                    }
+                }
+                const double sc = (s ? 1.0 : -1.0) / P.tab->w[od - 1][0];
+                for (int v = 0; v < NV; ++v) A[v * n + node] += sc * (G[v] - Fo[v]);
+            }
+            __syncthreads();
+        }
+    }
+    // epilogue: Qdot = -A / J, or the low-storage RK update (+ CFL/DFL rates)
+    const double dt = P.mode ? *P.dt : 0.0;
+    double lmax = 0.0, vmax = 0.0;
+    for (int t = threadIdx.x; t < n; t += CBS) {
+        const double iJ = 1.0 / __ldg(M + 9 * n + t);
+        if (P.mode == 0) {
+            for (int v = 0; v < NV; ++v) P.out[o + (long long)v * n + t] = -A[v * n + t] * iJ;
+        } else {
+            double qn[NV];
+            for (int v = 0; v < NV; ++v) {
+                const long long ix = o + (long long)v * n + t;
+                const double gn = (P.rkA == 0.0 ? 0.0 : P.rkA * P.g[ix]) - dt * A[v * n + t] * iJ;
+                P.g[ix] = gn;
+                qn[v] = Q[v * n + t] + P.rkB * gn;
+                P.out[ix] = qn[v];
+            }
+            if (P.lam_max) {
+                int ijk[3];
+                node_ijk(t, n1, n2, ijk[0], ijk[1], ijk[2]);
+                const double ir = 1.0 / qn[0];
+                const double p = P.ph.gm1 * (qn[4] - 0.5 * ir * (qn[1] * qn[1] + qn[2] * qn[2] + qn[3] * qn[3]));
+                const double c = sqrt(P.ph.gamma * p * ir);
+                double lam = 0.0, nu = 0.0;
+                const double numax = P.ph.mu * ir * fmax(4.0 / 3.0, P.ph.gamma / P.ph.Pr);
+                for (int d = 0; d < 3; ++d) {
+                    const double a0 = __ldg(M + (3 * d) * n + t) * iJ, a1 = __ldg(M + (3 * d + 1) * n + t) * iJ,
+                                 a2 = __ldg(M + (3 * d + 2) * n + t) * iJ;
+                    const double an2 = a0 * a0 + a1 * a1 + a2 * a2;
+                    const double ua = (qn[1] * a0 + qn[2] * a1 + qn[3] * a2) * ir;
+                    const double np1 = d == 0 ? n1 : (d == 1 ? n2 : n3);
+                    lam += (fabs(ua) + c * sqrt(an2)) * np1 * np1 * 0.5;
+                    nu += numax * an2 * np1 * np1 * np1 * np1 * 0.25;
+                }
+                lmax = fmax(lmax, lam);
+                vmax = fmax(vmax, nu);
+            }
+        }
+    }
+    if (P.lam_max) {
+        lmax = block_max(lmax, red);
+        vmax = block_max(vmax, red);
+        if (threadIdx.x == 0) {
+            atomicMax(P.lam_max, (unsigned long long)__double_as_longlong(lmax));
+            if (ns) atomicMax(P.lam_max + 1, (unsigned long long)__double_as_longlong(vmax));
+        }
+    }
+}
+
+// CFL (+DFL) rates of a state, curved metrics (reading A11)
+struct CDtParams {
+    const double* q;
+    const int* orders;
+    const long long* off;
+    const double* met;
+    PhysDev ph;
+    unsigned long long* maxbits;  // [2]
+};
+
+__global__ void __launch_bounds__(CBS) k_dt_curved(CDtParams P)
+{
+    __shared__ double red[32];
+    const int e = blockIdx.x;
+    const int n1 = P.orders[3 * e] + 1, n2 = P.orders[3 * e + 1] + 1, n3 = P.orders[3 * e + 2] + 1;
+    const int n = n1 * n2 * n3;
+    const long long o = P.off[e];
+    const double* M = P.met + 2 * o;
+    double lmax = 0.0, vmax = 0.0;
+    for (int t = threadIdx.x; t < n; t += CBS) {
+        double q[NV];
+        for (int v = 0; v < NV; ++v) q[v] = P.q[o + (long long)v * n + t];
+        const double iJ = 1.0 / M[9 * n + t];
+        const double ir = 1.0 / q[0];
+        const double p = P.ph.gm1 * (q[4] - 0.5 * ir * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]));
+        const double c = sqrt(P.ph.gamma * p * ir);
+        const double numax = P.ph.mu * ir * fmax(4.0 / 3.0, P.ph.gamma / P.ph.Pr);
+        double lam = 0.0, nu = 0.0;
+        for (int d = 0; d < 3; ++d) {
+            const double a0 = M[(3 * d) * n + t] * iJ, a1 = M[(3 * d + 1) * n + t] * iJ, a2 = M[(3 * d + 2) * n + t] * iJ;
+            const double an2 = a0 * a0 + a1 * a1 + a2 * a2;
+            const double ua = (q[1] * a0 + q[2] * a1 + q[3] * a2) * ir;
+            const double np1 = d == 0 ? n1 : (d == 1 ? n2 : n3);
+            lam += (fabs(ua) + c * sqrt(an2)) * np1 * np1 * 0.5;
+            nu += numax * an2 * np1 * np1 * np1 * np1 * 0.25;
+        }
+        lmax = fmax(lmax, lam);
+        vmax = fmax(vmax, nu);
+    }
+    lmax = block_max(lmax, red);
+    vmax = block_max(vmax, red);
+    if (threadIdx.x == 0) {
+        atomicMax(P.maxbits, (unsigned long long)__double_as_longlong(lmax));
+        if (P.ph.physics == 1) atomicMax(P.maxbits + 1, (unsigned long long)__double_as_longlong(vmax));
+    }
+}
+
+// dt = min(CFL / lam_max, DFL / nu_max); resets the accumulators
+__global__ void k_dt_final2(unsigned long long* maxbits, double cfl, double dfl, double* dt)
+{
+    const double lam = __longlong_as_double((long long)maxbits[0]);
+    const double nu = __longlong_as_double((long long)maxbits[1]);
+    double v = cfl / lam;
+    if (nu > 0.0) v = fmin(v, dfl / nu);
+    dt[0] = v;
+    maxbits[0] = 0ull;
+    maxbits[1] = 0ull;
+}
+
+// ---------------------------------------------------------------------------
+// Curved mortar (reading A6): metric from L's geometry at the mortar nodes.
+// mode 0: G = |Ja| Roe - BR1 average viscous (5 per point, projected);
+// mode 1: qhat Ja_k (15 per point, projected).
+// ---------------------------------------------------------------------------
+struct CMortarParams {
+    const double* q;
+    const double* grad;
+    const int* orders;
+    const long long* off;
+    const MortarItem* items;
+    const long long* moff;
+    double* mortarG;  // mode 0: 5 per point at moff; mode 1: 15 per point at 3*moff
+    CurvedMesh cm;
+    const Tables* tab;
+    PhysDev ph;
+    int mode;
+};
+
+__global__ void __launch_bounds__(128) k_mortar_curved(CMortarParams P)
+{
+    __shared__ double Xm[3][NP * NP];
+    __shared__ double Jm[3][NP * NP];
+    __shared__ double GM[15][NP * NP];
+    const MortarItem it = P.items[blockIdx.x];
+    const int d = it.d;
+    const int ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
+    int NL[3], NR[3];
+    for (int k = 0; k < 3; ++k) { NL[k] = P.orders[3 * it.L + k]; NR[k] = P.orders[3 * it.R + k]; }
+    const int M1 = max(NL[ta], NR[ta]), M2 = max(NL[tb], NR[tb]);
+    const int nm = (M1 + 1) * (M2 + 1);
+    const int gd[3] = {P.cm.g1, P.cm.g2, P.cm.g3};
+    // face coordinates of L's +1 face at the mortar nodes (GL geometry nodes: last layer along d)
+    const double* G = P.cm.geo + (long long)it.L * 3 * P.cm.ng;
+    const double* Ta = P.tab->T[gd[ta]][M1];
+    const double* Tb = P.tab->T[gd[tb]][M2];
+    const int ga = gd[0] + 1, gb = gd[1] + 1;
+    for (int t = threadIdx.x; t < nm; t += blockDim.x) {
+        const int m1 = t % (M1 + 1), m2 = t / (M1 + 1);
+        double x[3] = {0.0, 0.0, 0.0};
+        for (int b = 0; b <= gd[tb]; ++b)
+            for (int a = 0; a <= gd[ta]; ++a) {
+                int idx[3];
+                idx[d] = gd[d]; idx[ta] = a; idx[tb] = b;
+                const int gi = idx[0] + ga * (idx[1] + gb * idx[2]);
+                const double wgt = Ta[m1 * (gd[ta] + 1) + a] * Tb[m2 * (gd[tb] + 1) + b];
+                for (int c = 0; c < 3; ++c) x[c] += wgt * G[c * P.cm.ng + gi];
+            }
+        for (int c = 0; c < 3; ++c) Xm[c][t] = x[c];
+    }
+    __syncthreads();
+    const double* D1 = P.tab->D[M1];
+    const double* D2 = P.tab->D[M2];
+    for (int t = threadIdx.x; t < nm; t += blockDim.x) {
+        const int m1 = t % (M1 + 1), m2 = t / (M1 + 1);
+        double u[3], v[3];
+        for (int c = 0; c < 3; ++c) {
+            double s1 = 0.0, s2 = 0.0;
+            for (int m = 0; m <= M1; ++m) s1 += D1[m1 * (M1 + 1) + m] * Xm[c][m + (M1 + 1) * m2];
+            for (int m = 0; m <= M2; ++m) s2 += D2[m2 * (M2 + 1) + m] * Xm[c][m1 + (M1 + 1) * m];
+            u[c] = s1;
+            v[c] = s2;
+        }
+        double w[3];
+        if (d == 1) { w[0] = v[1] * u[2] - v[2] * u[1]; w[1] = v[2] * u[0] - v[0] * u[2]; w[2] = v[0] * u[1] - v[1] * u[0]; }
+        else { w[0] = u[1] * v[2] - u[2] * v[1]; w[1] = u[2] * v[0] - u[0] * v[2]; w[2] = u[0] * v[1] - u[1] * v[0]; }
+        for (int c = 0; c < 3; ++c) Jm[c][t] = w[c];
+    }
+    __syncthreads();
+    const int nL = (NL[0] + 1) * (NL[1] + 1) * (NL[2] + 1), nR = (NR[0] + 1) * (NR[1] + 1) * (NR[2] + 1);
+    const long long oL = P.off[it.L], oR = P.off[it.R];
+    const double* TL1 = P.tab->T[NL[ta]][M1];
+    const double* TL2 = P.tab->T[NL[tb]][M2];
+    const double* TR1 = P.tab->T[NR[ta]][M1];
+    const double* TR2 = P.tab->T[NR[tb]][M2];
+    const bool ns = P.ph.physics == 1;
+    const int ncomp = P.mode == 0 ? NV : 15;
+    for (int t = threadIdx.x; t < nm; t += blockDim.x) {
+        const int m1 = t % (M1 + 1), m2 = t / (M1 + 1);
+        double qL[NV] = {0, 0, 0, 0, 0}, qR[NV] = {0, 0, 0, 0, 0};
+        double gL[15], gR[15];
+        for (int c = 0; c < 15; ++c) { gL[c] = 0.0; gR[c] = 0.0; }
+        const bool wantg = ns && P.mode == 0;
+        for (int b = 0; b <= NL[tb]; ++b)
+            for (int a = 0; a <= NL[ta]; ++a) {
+                int ijk[3];
+                ijk[d] = NL[d]; ijk[ta] = a; ijk[tb] = b;
+                const long long node = ijk[0] + (NL[0] + 1) * (ijk[1] + (NL[1] + 1) * ijk[2]);
+                const double wgt = TL1[m1 * (NL[ta] + 1) + a] * TL2[m2 * (NL[tb] + 1) + b];
+                for (int v = 0; v < NV; ++v) qL[v] += wgt * P.q[oL + node + (long long)v * nL];
+                if (wantg)
+                    for (int c = 0; c < 15; ++c) gL[c] += wgt * P.grad[3 * oL + node + (long long)c * nL];
+            }
+        for (int b = 0; b <= NR[tb]; ++b)
+            for (int a = 0; a <= NR[ta]; ++a) {
+                int ijk[3];
+                ijk[d] = 0; ijk[ta] = a; ijk[tb] = b;
+                const long long node = ijk[0] + (NR[0] + 1) * (ijk[1] + (NR[1] + 1) * ijk[2]);
+                const double wgt = TR1[m1 * (NR[ta] + 1) + a] * TR2[m2 * (NR[tb] + 1) + b];
+                for (int v = 0; v < NV; ++v) qR[v] += wgt * P.q[oR + node + (long long)v * nR];
+                if (wantg)
+                    for (int c = 0; c < 15; ++c) gR[c] += wgt * P.grad[3 * oR + node + (long long)c * nR];
+            }
+        const double jf[3] = {Jm[0][t], Jm[1][t], Jm[2][t]};
+        if (P.mode == 1) {
+            for (int c = 0; c < 3; ++c)
+                for (int v = 0; v < NV; ++v) GM[c * NV + v][t] = 0.5 * (qL[v] + qR[v]) * jf[c];
+        } else {
+            const double S = sqrt(jf[0] * jf[0] + jf[1] * jf[1] + jf[2] * jf[2]);
+            const double nrm[3] = {jf[0] / S, jf[1] / S, jf[2] / S};
+            double F[NV];
+            riemann(qL, qR, nrm, P.ph, F);
+            for (int v = 0; v < NV; ++v) F[v] *= S;
+            if (ns) {
+                double fL[NV], fR[NV];
+                visc_dot(qL, gL, jf[0], jf[1], jf[2], P.ph, fL);
+                visc_dot(qR, gR, jf[0], jf[1], jf[2], P.ph, fR);
+                for (int v = 0; v < NV; ++v) F[v] -= 0.5 * (fL[v] + fR[v]);
+            }
+            for (int v = 0; v < NV; ++v) GM[v][t] = F[v];
+        }
+    }
+    __syncthreads();
+    for (int side = 0; side < 2; ++side) {
+        const int* NS = side == 0 ? NL : NR;
+        const int S1 = NS[ta], S2 = NS[tb];
+        const int nsd = (S1 + 1) * (S2 + 1);
+        const long long mo = P.moff[6 * (side == 0 ? it.L : it.R) + 2 * d + (side == 0 ? 1 : 0)];
+        const double* P1 = P.tab->P[M1][S1];
+        const double* P2 = P.tab->P[M2][S2];
+        double* dst = P.mortarG + (P.mode == 0 ? mo : 3 * mo);
+        for (int t = threadIdx.x; t < nsd; t += blockDim.x) {
+            const int a = t % (S1 + 1), b = t / (S1 + 1);
+            for (int c = 0; c < ncomp; ++c) {
+                double s = 0.0;
+                for (int m2 = 0; m2 <= M2; ++m2)
+                    for (int m1 = 0; m1 <= M1; ++m1)
+                        s += P1[a * (M1 + 1) + m1] * P2[b * (M2 + 1) + m2] * GM[c][m1 + (M1 + 1) * m2];
+                dst[(long long)c * nsd + t] = s;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// tau-estimation on curved elements (Euler or NS), one CTA per level (e,d,p):
+// coarse geometry = geometry polynomial at the coarse nodes, metrics by D^O;
+// isolated BR1 gradient (strong form) and isolated residual at O.
+// ---------------------------------------------------------------------------
+struct CTauParams {
+    const double* q;
+    const double* qref;
+    double* tau;
+    const int* orders;
+    const long long* off;
+    const TauLevel* levels;
+    CurvedMesh cm;
+    const Tables* tab;
+    int formulation;
+    PhysDev ph;
+};
+
+__global__ void __launch_bounds__(CBS) k_tau_curved(CTauParams P)
+{
+    extern __shared__ double sm[];
+    __shared__ double red[32];
+    const TauLevel lv = P.levels[blockIdx.x];
+    const int e = lv.e, d = lv.d, p = lv.p;
+    const int n1 = P.orders[3 * e] + 1, n2 = P.orders[3 * e + 1] + 1, n3 = P.orders[3 * e + 2] + 1;
+    const int n = n1 * n2 * n3;
+    const int nd = d == 0 ? n1 : (d == 1 ? n2 : n3);
+    const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
+    const int o1 = d == 0 ? p + 1 : n1, o2 = d == 1 ? p + 1 : n2, o3 = d == 2 ? p + 1 : n3;
+    const int nO = o1 * o2 * o3;
+    const bool ns = P.ph.physics == 1;
+    double* Mc = sm;              // 10 nO metrics
+    double* Qc = Mc + 10 * nO;    // 5 nO
+    double* Rc = Qc + NV * nO;    // 5 nO
+    double* F = Rc + NV * nO;     // 5 nO (also 3 nO coordinates at first)
+    double* A = F + NV * nO;      // 5 nO
+    double* GA = A + NV * nO;     // 15 nO (NS)
+    element_metrics(P.cm, e, o1, o2, o3, P.tab, F, Mc);
+    const long long o = P.off[e];
+    const double* T = P.tab->T[nd - 1][p];
+    for (int t = threadIdx.x; t < nO; t += CBS) {
+        int i, j, k;
+        node_ijk(t, o1, o2, i, j, k);
+        const int ic = d == 0 ? i : (d == 1 ? j : k);
+        if (d == 0) i = 0; else if (d == 1) j = 0; else k = 0;
+        const int base = i + n1 * (j + n2 * k);
+        for (int v = 0; v < NV; ++v) {
+            double s = 0.0, r = 0.0;
+            for (int a = 0; a < nd; ++a) {
+                const double w = T[ic * nd + a];
+                s += w * __ldg(P.q + o + (long long)v * n + base + a * stride);
+                r += w * __ldg(P.qref + o + (long long)v * n + base + a * stride);
+            }
+            Qc[v * nO + t] = s;
+            Rc[v * nO + t] = r;
+            A[v * nO + t] = 0.0;
+        }
+    }
+    __syncthreads();
+    if (ns) {  // isolated gradient: J g_k = sum_d' D^{d'} (Ja^{d'}_k q)
+        for (int t = threadIdx.x; t < 15 * nO; t += CBS) GA[t] = 0.0;
+        __syncthreads();
+        for (int dd = 0; dd < 3; ++dd) {
+            const int od = dd == 0 ? o1 : (dd == 1 ? o2 : o3);
+            const int str = dd == 0 ? 1 : (dd == 1 ? o1 : o1 * o2);
+            const double* Dd = P.tab->D[od - 1];
+            for (int k = 0; k < 3; ++k) {
+                for (int t = threadIdx.x; t < nO; t += CBS)
+                    for (int v = 0; v < NV; ++v) F[v * nO + t] = Mc[(3 * dd + k) * nO + t] * Qc[v * nO + t];
+                __syncthreads();
+                for (int t = threadIdx.x; t < nO; t += CBS) {
+                    int ijk[3];
+                    node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
+                    const int a = dd == 0 ? ijk[0] : (dd == 1 ? ijk[1] : ijk[2]);
+                    const int base = t - a * str;
+                    for (int v = 0; v < NV; ++v) GA[(k * NV + v) * nO + t] += dsum(Dd, od, a, F + v * nO + base, str);
+                }
+                __syncthreads();
+            }
+        }
+        for (int t = threadIdx.x; t < nO; t += CBS) {
+            const double iJ = 1.0 / Mc[9 * nO + t];
+            for (int c = 0; c < 15; ++c) GA[c * nO + t] *= iJ;
+        }
+        __syncthreads();
+    }
+    for (int dd = 0; dd < 3; ++dd) {
+        const int od = dd == 0 ? o1 : (dd == 1 ? o2 : o3);
+        const int str = dd == 0 ? 1 : (dd == 1 ? o1 : o1 * o2);
+        const double* Dd = P.tab->D[od - 1];
+        for (int t = threadIdx.x; t < nO; t += CBS) {
+            double qv[NV], gv[15], Fv[NV];
+            for (int v = 0; v < NV; ++v) qv[v] = Qc[v * nO + t];
+            if (ns)
+                for (int c = 0; c < 15; ++c) gv[c] = GA[c * nO + t];
+            contra_flux(qv, gv, Mc[(3 * dd) * nO + t], Mc[(3 * dd + 1) * nO + t], Mc[(3 * dd + 2) * nO + t], P.ph, Fv);
+            for (int v = 0; v < NV; ++v) F[v * nO + t] = Fv[v];
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < nO; t += CBS) {
+            int ijk[3];
+            node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
+            const int a = dd == 0 ? ijk[0] : (dd == 1 ? ijk[1] : ijk[2]);
+            const int base = t - a * str;
+            for (int v = 0; v < NV; ++v) A[v * nO + t] += dsum(Dd, od, a, F + v * nO + base, str);
+        }
+        __syncthreads();
+    }
+    double tmax = 0.0;
+    for (int t = threadIdx.x; t < nO; t += CBS) {
+        int i, j, k;
+        node_ijk(t, o1, o2, i, j, k);
+        const double J = Mc[9 * nO + t];
+        double scale = 1.0;
+        if (P.formulation == 1) scale = J * P.tab->w[o1 - 1][i] * P.tab->w[o2 - 1][j] * P.tab->w[o3 - 1][k];
+        for (int v = 0; v < NV; ++v) tmax = fmax(tmax, fabs(scale * (Rc[v * nO + t] + A[v * nO + t] / J)));
+    }
+    tmax = block_max(tmax, red);
+    if (threadIdx.x == 0) P.tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV + p] = tmax;
+}
+
+}  // namespace dgtau

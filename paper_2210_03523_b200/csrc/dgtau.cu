@@ -20,6 +20,7 @@
 #include "kernels.cuh"
 #include "residual_t.cuh"
 #include "tau_t.cuh"
+#include "curved.cuh"
 
 using namespace dgtau;
 
@@ -77,6 +78,13 @@ struct dg_ctx {
     int* d_tr_orders = nullptr;       // transfer scratch
     long long* d_tr_off = nullptr;
     std::vector<int> tr_orders_host;
+    // curved geometry / Navier-Stokes
+    bool curved = false;
+    double* d_geo = nullptr;
+    double* d_met = nullptr;       // 10 per node
+    double* d_grad = nullptr;      // 15 per node (NS)
+    double* d_mortarGq = nullptr;  // 15 per mortar point (NS gradient mortars)
+    long long met_len = 0, grad_len = 0, mq_len = 0;
     std::vector<long long> tr_off_host;
     long long ref_len = 0;
     double* d_mortarG = nullptr;
@@ -161,6 +169,17 @@ const Tables& host_tables()
     return *t;
 }
 
+CurvedMesh curved_mesh(const dg_ctx* ctx)
+{
+    CurvedMesh cm;
+    cm.geo = ctx->d_geo;
+    cm.g1 = ctx->gorder[0];
+    cm.g2 = ctx->gorder[1];
+    cm.g3 = ctx->gorder[2];
+    cm.ng = (cm.g1 + 1) * (cm.g2 + 1) * (cm.g3 + 1);
+    return cm;
+}
+
 }  // namespace
 
 extern "C" {
@@ -213,6 +232,10 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
     cudaFuncSetAttribute(k_tau3, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(k_tau2, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
     cudaFuncSetAttribute(k_transfer, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_metrics, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_res_curved, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(k_tau_curved, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     *out = ctx;
     return DG_OK;
 }
@@ -234,6 +257,10 @@ void dg_destroy(dg_ctx* ctx)
     dfree(ctx->d_levels);
     dfree(ctx->d_ref_scratch);
     dfree(ctx->d_tr_orders);
+    dfree(ctx->d_geo);
+    dfree(ctx->d_met);
+    dfree(ctx->d_grad);
+    dfree(ctx->d_mortarGq);
     dfree(ctx->d_tr_off);
     dfree(ctx->d_mortarG);
     dfree(ctx->d_scratch);
@@ -286,7 +313,11 @@ dg_status dg_mesh_upload(dg_ctx* ctx, int E, const int32_t* nbr_host, const int3
             if (!(hi > lo)) affine = false;
         }
     }
-    if (!affine) return fail(ctx, DG_EUNSUPPORTED, "mesh: curved / non-axis-aligned geometry not in this build");
+    ctx->curved = !affine;
+    if (ctx->curved) {
+        for (long long i = 0; i < 3LL * E; ++i) ctx->h[i] = 1.0;  // unused by the curved kernels
+        CK(upload(ctx->d_geo, ctx->geo));
+    }
     CK(upload(ctx->d_nbr, ctx->nbr));
     CK(upload(ctx->d_h, ctx->h));
     ctx->have_orders = false;
@@ -430,6 +461,34 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     dfree(ctx->d_margin);
     CK(cudaMalloc(&ctx->d_sel, sizeof(int) * 6LL * E));
     CK(cudaMalloc(&ctx->d_margin, sizeof(double) * E));
+    if (ctx->curved) {
+        const long long L = ctx->off[E];
+        if (ctx->met_len < 2 * L) {
+            dfree(ctx->d_met);
+            CK(cudaMalloc(&ctx->d_met, sizeof(double) * 2 * L));
+            ctx->met_len = 2 * L;
+        }
+        if (ctx->prm.physics == DG_NS && ctx->grad_len < 3 * L) {
+            dfree(ctx->d_grad);
+            CK(cudaMalloc(&ctx->d_grad, sizeof(double) * 3 * L));
+            ctx->grad_len = 3 * L;
+        }
+        if (ctx->prm.physics == DG_NS && mlen > 0 && ctx->mq_len < 3 * mlen) {
+            dfree(ctx->d_mortarGq);
+            CK(cudaMalloc(&ctx->d_mortarGq, sizeof(double) * 3 * mlen));
+            ctx->mq_len = 3 * mlen;
+        }
+        MetParams M;
+        M.cm = curved_mesh(ctx);
+        M.orders = ctx->d_orders;
+        M.off = ctx->d_off;
+        M.met = ctx->d_met;
+        M.tab = ctx->d_tab;
+        k_metrics<<<E, CBS, sizeof(double) * 13 * (size_t)ctx->maxn>>>(M);
+        ctx->launches++;
+        CK(cudaGetLastError());
+        CK(cudaDeviceSynchronize());
+    }
     ctx->have_orders = true;
     return DG_OK;
 }
@@ -442,29 +501,97 @@ dg_status dg_node_coords(dg_ctx* ctx, double* X)
     if (!ctx || !X) return DG_EINVAL;
     if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "node_coords: orders not set");
     const Tables& t = host_tables();
+    const int* g = ctx->gorder;
+    const int ng = (g[0] + 1) * (g[1] + 1) * (g[2] + 1);
     long long o = 0;
     for (int e = 0; e < ctx->E; ++e) {
         const int* N = &ctx->orders[3 * e];
         const int n = npts(N);
-        const double* G = &ctx->geo[24LL * e];
-        for (int c = 0; c < 3; ++c) {
-            const double lo = G[c * 8], hh = ctx->h[3LL * e + c];
-            for (int k = 0; k <= N[2]; ++k)
-                for (int j = 0; j <= N[1]; ++j)
-                    for (int i = 0; i <= N[0]; ++i) {
-                        const int ijk[3] = {i, j, k};
-                        const double xi = t.x[N[c]][ijk[c]];
-                        X[o + (long long)c * n + i + (N[0] + 1) * (j + (N[1] + 1) * k)] = lo + 0.5 * (xi + 1.0) * hh;
-                    }
-        }
+        const double* G = &ctx->geo[3LL * ng * e];
+        // x(i,j,k) = sum_abc T^{g1->N1}[i][a] T^{g2->N2}[j][b] T^{g3->N3}[k][c] X_geo[a,b,c]
+        for (int k = 0; k <= N[2]; ++k)
+            for (int j = 0; j <= N[1]; ++j)
+                for (int i = 0; i <= N[0]; ++i) {
+                    double x[3] = {0.0, 0.0, 0.0};
+                    for (int c = 0; c <= g[2]; ++c)
+                        for (int b = 0; b <= g[1]; ++b)
+                            for (int a = 0; a <= g[0]; ++a) {
+                                const double wgt = t.T[g[0]][N[0]][i * (g[0] + 1) + a] * t.T[g[1]][N[1]][j * (g[1] + 1) + b] *
+                                                   t.T[g[2]][N[2]][k * (g[2] + 1) + c];
+                                const int gi = a + (g[0] + 1) * (b + (g[1] + 1) * c);
+                                for (int cc = 0; cc < 3; ++cc) x[cc] += wgt * G[cc * ng + gi];
+                            }
+                    const int node = i + (N[0] + 1) * (j + (N[1] + 1) * k);
+                    for (int cc = 0; cc < 3; ++cc) X[o + (long long)cc * n + node] = x[cc];
+                }
         o += 3LL * n;
     }
     return DG_OK;
 }
 
+static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* q, double* out, double* g,
+                                        const double* dt, double A, double B, int mode, cudaStream_t st,
+                                        unsigned long long* lam_max)
+{
+    const bool ns = ctx->prm.physics == DG_NS;
+    CurvedParams P{};
+    P.q = q;
+    P.g = g;
+    P.dt = dt;
+    P.rkA = A;
+    P.rkB = B;
+    P.variant = variant;
+    P.orders = ctx->d_orders;
+    P.off = ctx->d_off;
+    P.finfo = ctx->d_finfo;
+    P.met = ctx->d_met;
+    P.grad = ctx->d_grad;
+    P.tab = ctx->d_tab;
+    P.ph = phys_dev(ctx->prm);
+    P.flag = ctx->d_flag;
+    CMortarParams M{};
+    M.q = q;
+    M.grad = ctx->d_grad;
+    M.orders = ctx->d_orders;
+    M.off = ctx->d_off;
+    M.items = ctx->d_mortar;
+    M.moff = ctx->d_moff;
+    M.cm = curved_mesh(ctx);
+    M.tab = ctx->d_tab;
+    M.ph = phys_dev(ctx->prm);
+    const bool mort = variant == DG_NONISOLATED && ctx->nmortar > 0;
+    if (ns) {  // BR1 gradient pass (eq DGSEMsystem:2)
+        if (mort) {
+            M.mode = 1;
+            M.mortarG = ctx->d_mortarGq;
+            k_mortar_curved<<<ctx->nmortar, 128, 0, st>>>(M);
+            ctx->launches++;
+        }
+        P.mode = 0;
+        P.out = ctx->d_grad;
+        P.mortarG = ctx->d_mortarGq;
+        k_grad<<<ctx->E, CBS, sizeof(double) * 25 * (size_t)ctx->maxn, st>>>(P);
+        ctx->launches++;
+    }
+    if (mort) {
+        M.mode = 0;
+        M.mortarG = ctx->d_mortarG;
+        k_mortar_curved<<<ctx->nmortar, 128, 0, st>>>(M);
+        ctx->launches++;
+    }
+    P.mode = mode;
+    P.out = out;
+    P.mortarG = ctx->d_mortarG;
+    P.lam_max = lam_max;
+    k_res_curved<<<ctx->E, CBS, sizeof(double) * 15 * (size_t)ctx->maxn, st>>>(P);
+    ctx->launches++;
+    return check_stream_error(ctx, "curved residual launch");
+}
+
 static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, double* out, double* g, const double* dt,
                                  double A, double B, int mode, cudaStream_t st, unsigned long long* lam_max = nullptr)
 {
+    if (ctx->curved) return launch_residual_curved(ctx, variant, q, out, g, dt, A, B, mode, st, lam_max);
     if (variant == DG_NONISOLATED && ctx->nmortar > 0) {
         MortarParams M;
         M.q = q;
@@ -520,7 +647,7 @@ dg_status dg_rhs_eval(dg_ctx* ctx, int variant, const double* q_dev, double* qdo
     if (!ctx || !q_dev || !qdot_dev) return DG_EINVAL;
     if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "rhs_eval: orders not set");
     if (variant != DG_NONISOLATED && variant != DG_ISOLATED) return fail(ctx, DG_EINVAL, "rhs_eval: variant");
-    if (ctx->prm.physics != DG_EULER) return fail(ctx, DG_EUNSUPPORTED, "rhs_eval: NS not in this build");
+    if (ctx->prm.physics == DG_NS && !ctx->curved) return fail(ctx, DG_EUNSUPPORTED, "rhs_eval: NS needs the curved path");
     return launch_residual(ctx, variant, q_dev, qdot_dev, nullptr, nullptr, 0.0, 0.0, 0, (cudaStream_t)stream);
 }
 
@@ -530,7 +657,27 @@ dg_status dg_compute_dt(dg_ctx* ctx, const double* q_dev, double cfl, double* dt
     if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "compute_dt: orders not set");
     cudaStream_t st = (cudaStream_t)stream;
     CK(cudaMemsetAsync(ctx->d_scratch, 0, sizeof(unsigned long long), st));
-    CK(cudaMemsetAsync(ctx->d_scratch + 4, 0, sizeof(unsigned long long), st));  // fused-dt accumulator
+    CK(cudaMemsetAsync(ctx->d_scratch + 4, 0, 2 * sizeof(unsigned long long), st));  // fused-dt accumulators
+    if (ctx->curved) {
+        CK(cudaMemsetAsync(ctx->d_scratch + 1, 0, sizeof(unsigned long long), st));
+        CDtParams C;
+        C.q = q_dev;
+        C.orders = ctx->d_orders;
+        C.off = ctx->d_off;
+        C.met = ctx->d_met;
+        C.ph = phys_dev(ctx->prm);
+        C.maxbits = ctx->d_scratch;
+        k_dt_curved<<<ctx->E, CBS, 0, st>>>(C);
+        k_dt_final2<<<1, 1, 0, st>>>(ctx->d_scratch, cfl, cfl, dt_dev);
+        ctx->launches += 2;
+        dg_status s = check_stream_error(ctx, "k_dt_curved launch");
+        if (s != DG_OK) return s;
+        if (dt_host) {
+            CK(cudaMemcpyAsync(dt_host, dt_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        }
+        return DG_OK;
+    }
     DtParams P;
     P.q = q_dev;
     P.work = ctx->d_work;
@@ -555,7 +702,7 @@ dg_status dg_rk_step(dg_ctx* ctx, double* q_in, double* q_out, double* g, const 
 {
     if (!ctx || !q_in || !q_out || !g || !dt_dev || q_in == q_out) return DG_EINVAL;
     if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "rk_step: orders not set");
-    if (ctx->prm.physics != DG_EULER) return fail(ctx, DG_EUNSUPPORTED, "rk_step: NS not in this build");
+    if (ctx->prm.physics == DG_NS && !ctx->curved) return fail(ctx, DG_EUNSUPPORTED, "rk_step: NS needs the curved path");
     // Williamson (1980) low-storage RK3 coefficients
     static const double A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
     static const double B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
@@ -576,7 +723,7 @@ dg_status dg_rk_step_dt(dg_ctx* ctx, double* q_in, double* q_out, double* g, con
     if (!ctx || !q_in || !q_out || !g || !dt_dev || !dt_next_dev || q_in == q_out || dt_next_dev == dt_dev || !(cfl > 0))
         return DG_EINVAL;
     if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "rk_step_dt: orders not set");
-    if (ctx->prm.physics != DG_EULER) return fail(ctx, DG_EUNSUPPORTED, "rk_step_dt: NS not in this build");
+    if (ctx->prm.physics == DG_NS && !ctx->curved) return fail(ctx, DG_EUNSUPPORTED, "rk_step_dt: NS needs the curved path");
     static const double A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
     static const double B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
     cudaStream_t st = (cudaStream_t)stream;
@@ -587,7 +734,8 @@ dg_status dg_rk_step_dt(dg_ctx* ctx, double* q_in, double* q_out, double* g, con
                                       k == 2 ? ctx->d_scratch + 4 : nullptr);
         if (s != DG_OK) return s;
     }
-    k_dt_final<<<1, 1, 0, st>>>(ctx->d_scratch + 4, cfl, dt_next_dev);
+    if (ctx->curved) k_dt_final2<<<1, 1, 0, st>>>(ctx->d_scratch + 4, cfl, cfl, dt_next_dev);
+    else k_dt_final<<<1, 1, 0, st>>>(ctx->d_scratch + 4, cfl, dt_next_dev);
     ctx->launches++;
     return check_stream_error(ctx, "k_dt_final launch");
 }
@@ -598,7 +746,7 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
     if (!ctx || !o || !q_dev || !tau_dev) return DG_EINVAL;
     if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "tau_estimate: orders not set");
     if (o->reference == DG_REF_SOLVER && !qref_dev) return fail(ctx, DG_EINVAL, "tau_estimate: SOLVER needs qdot_ref");
-    if (ctx->prm.physics != DG_EULER) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: NS not in this build");
+    if (ctx->prm.physics == DG_NS && !ctx->curved) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: NS needs the curved path");
     const size_t smem = sizeof(double) * 3 * NV * (size_t)ctx->maxn;
     if (ctx->generic) {
         TauParams P;
@@ -629,7 +777,22 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
         }
         k_tau_norm<<<ctx->E, 128, 0, st>>>(ref, tau_dev, ctx->d_orders, ctx->d_off);
         ctx->launches++;
-        if (ctx->nlevels > 0) {
+        if (ctx->curved && ctx->nlevels > 0) {
+            const size_t sm = sizeof(double) * (ctx->prm.physics == DG_NS ? 45 : 30) * (size_t)ctx->max_level;
+            if (sm > 227 * 1024) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: coarse level too large for shared memory");
+            CTauParams C;
+            C.q = q_dev;
+            C.qref = ref;
+            C.tau = tau_dev;
+            C.orders = ctx->d_orders;
+            C.off = ctx->d_off;
+            C.levels = ctx->d_levels;
+            C.cm = curved_mesh(ctx);
+            C.tab = ctx->d_tab;
+            C.formulation = o->formulation;
+            C.ph = phys_dev(ctx->prm);
+            k_tau_curved<<<ctx->nlevels, CBS, sm, st>>>(C);
+        } else if (ctx->nlevels > 0) {
             Tau3Params P;
             P.q = q_dev;
             P.qref = ref;
@@ -746,6 +909,7 @@ dg_status dg_diagnostics(dg_ctx* ctx, const double* q_dev, const double* v_dev, 
     P.orders = ctx->d_orders;
     P.off = ctx->d_off;
     P.hgeo = ctx->d_h;
+    P.met = ctx->curved ? ctx->d_met : nullptr;
     P.tab = ctx->d_tab;
     P.gamma = ctx->prm.gamma;
     P.sums = ctx->d_sums;

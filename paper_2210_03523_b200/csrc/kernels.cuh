@@ -684,6 +684,7 @@ struct DiagParams {
     const int* orders;
     const long long* off;
     const double* hgeo;
+    const double* met;             // curved: metric array (J at component 9), else nullptr
     const Tables* tab;
     double gamma;
     double* sums;                  // [5]
@@ -697,10 +698,11 @@ __global__ void __launch_bounds__(BLOCK) k_diag(DiagParams P)
     int N[3] = {P.orders[3 * e], P.orders[3 * e + 1], P.orders[3 * e + 2]};
     const int n1 = N[0] + 1, n2 = N[1] + 1, n = n1 * n2 * (N[2] + 1);
     const long long o = P.off[e];
-    const double J = P.hgeo[3 * e] * P.hgeo[3 * e + 1] * P.hgeo[3 * e + 2] / 8.0;
+    const double Ja = P.met ? 0.0 : P.hgeo[3 * e] * P.hgeo[3 * e + 1] * P.hgeo[3 * e + 2] / 8.0;
     for (int t = threadIdx.x; t < n; t += blockDim.x) {
         int i, j, k;
         node_ijk(t, n1, n2, i, j, k);
+        const double J = P.met ? P.met[2 * o + 9 * n + t] : Ja;
         const double m = J * P.tab->w[N[0]][i] * P.tab->w[N[1]][j] * P.tab->w[N[2]][k];
         if (P.v)
             for (int v = 0; v < NV; ++v) atomicAdd(&P.sums[v], m * P.v[o + (long long)v * n + t]);
