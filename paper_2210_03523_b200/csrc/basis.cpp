@@ -166,4 +166,40 @@ void build_tables(Tables* t)
         }
 }
 
+void build_tables_dd(TablesDD* t)
+{
+    std::memset(t, 0, sizeof(TablesDD));
+    long double X[NMAX + 1][NMAX + 1], Wt[NMAX + 1][NMAX + 1], L[NMAX + 1][NMAX + 1];
+    for (int N = 1; N <= NMAX; ++N) {
+        lobatto(N, X[N], Wt[N]);
+        bary_weights(N, X[N], L[N]);
+        for (int a = 0; a <= N; ++a) {
+            long double diag = 0.0L;
+            long double row[NMAX + 1];
+            for (int b = 0; b <= N; ++b) {
+                if (a == b) continue;
+                row[b] = (L[N][b] / L[N][a]) / (X[N][a] - X[N][b]);
+                diag -= row[b];
+            }
+            row[a] = diag;
+            for (int b = 0; b <= N; ++b) {
+                const double hi = (double)row[b];
+                t->Dhi[N][a * (N + 1) + b] = hi;
+                t->Dlo[N][a * (N + 1) + b] = (double)(row[b] - (long double)hi);
+            }
+        }
+    }
+    for (int Nf = 1; Nf <= NMAX; ++Nf)
+        for (int Nt = 1; Nt <= NMAX; ++Nt)
+            for (int i = 0; i <= Nt; ++i) {
+                long double row[NMAX + 1];
+                bary_row(Nf, X[Nf], L[Nf], X[Nt][i], row);
+                for (int a = 0; a <= Nf; ++a) {
+                    const double hi = (double)row[a];
+                    t->Thi[Nf][Nt][i * (Nf + 1) + a] = hi;
+                    t->Tlo[Nf][Nt][i * (Nf + 1) + a] = (double)(row[a] - (long double)hi);
+                }
+            }
+}
+
 }  // namespace dgtau

@@ -15,6 +15,15 @@ struct Tables {
     double P[NP][NP][NP * NP];  // P[M][s][a*(M+1)+m], exact L2 projection M -> s <= M
 };
 
+// hi + lo (double-double) copies of T and D, exact to the long double value:
+// used only where geometry is differentiated (metric terms), whose rounding
+// errors are amplified by D (reading: DESIGN.md "Metric accuracy").
+struct TablesDD {
+    double Thi[NP][NP][NP * NP], Tlo[NP][NP][NP * NP];
+    double Dhi[NP][NP * NP], Dlo[NP][NP * NP];
+};
+
 void build_tables(Tables* t);
+void build_tables_dd(TablesDD* t);
 
 }  // namespace dgtau

@@ -99,65 +99,109 @@ __device__ __forceinline__ void contra_flux(const double* q, const double* g, do
 }
 
 // ---------------------------------------------------------------------------
-// Element geometry at orders (o1,o2,o3): X = T^{g->o} Xgeo (3 x no, smem),
-// then metrics via D^o (written to Mout[c*no + node]).  All CTA threads.
+// Double-double arithmetic (error-free transformations) for the metric terms:
+// the coordinates are O(20) while elements are O(0.02..2) and D amplifies
+// rounding by O(N^2), so a plain fp64 evaluation loses ~1e-13 relative in
+// Ja; the cfg4 state (free stream + 1e-3 noise) makes the residual sensitive
+// to that.  Evaluated in dd and rounded once, the metrics equal the
+// correctly rounded values (as the long double oracle's).
 // ---------------------------------------------------------------------------
-__device__ void element_metrics(const CurvedMesh& cm, int e, int o1, int o2, int o3, const Tables* tab, double* Xs,
+struct dd {
+    double hi, lo;
+};
+__device__ __forceinline__ dd two_sum(double a, double b)
+{
+    const double s = a + b;
+    const double bb = s - a;
+    return {s, (a - (s - bb)) + (b - bb)};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b)
+{
+    dd s = two_sum(a.hi, b.hi);
+    const double lo = s.lo + a.lo + b.lo;
+    return two_sum(s.hi, lo);
+}
+__device__ __forceinline__ dd dd_mul(dd a, dd b)
+{
+    const double p = a.hi * b.hi;
+    const double e = fma(a.hi, b.hi, -p);
+    const double lo = e + (a.hi * b.lo + a.lo * b.hi);
+    return two_sum(p, lo);
+}
+__device__ __forceinline__ dd dd_neg(dd a) { return {-a.hi, -a.lo}; }
+__device__ __forceinline__ dd mkdd(double a) { return {a, 0.0}; }
+
+// Element geometry at orders (o1,o2,o3): X = T^{g->o} Xgeo (3 x no, dd in
+// smem), then metrics via D^o (cross-product form) rounded to Mout[c*no+node].
+__device__ void element_metrics(const CurvedMesh& cm, int e, int o1, int o2, int o3, const TablesDD* tdd, dd* Xs,
                                 double* Mout)
 {
     const int no = o1 * o2 * o3;
     const int ga = cm.g1 + 1, gb = cm.g2 + 1;
     const double* G = cm.geo + (long long)e * 3 * cm.ng;
-    const double* T1 = tab->T[cm.g1][o1 - 1];
-    const double* T2 = tab->T[cm.g2][o2 - 1];
-    const double* T3 = tab->T[cm.g3][o3 - 1];
     for (int t = threadIdx.x; t < no; t += blockDim.x) {
         int i, j, k;
         node_ijk(t, o1, o2, i, j, k);
-        double x[3] = {0.0, 0.0, 0.0};
+        dd x[3] = {mkdd(0.0), mkdd(0.0), mkdd(0.0)};
         for (int c = 0; c <= cm.g3; ++c)
             for (int b = 0; b <= cm.g2; ++b)
                 for (int a = 0; a <= cm.g1; ++a) {
-                    const double wgt = T1[i * ga + a] * T2[j * gb + b] * T3[k * (cm.g3 + 1) + c];
+                    const int i1 = i * ga + a, i2 = j * gb + b, i3 = k * (cm.g3 + 1) + c;
+                    const dd w1 = {tdd->Thi[cm.g1][o1 - 1][i1], tdd->Tlo[cm.g1][o1 - 1][i1]};
+                    const dd w2 = {tdd->Thi[cm.g2][o2 - 1][i2], tdd->Tlo[cm.g2][o2 - 1][i2]};
+                    const dd w3 = {tdd->Thi[cm.g3][o3 - 1][i3], tdd->Tlo[cm.g3][o3 - 1][i3]};
+                    const dd wgt = dd_mul(dd_mul(w1, w2), w3);
                     const int gi = a + ga * (b + gb * c);
-                    x[0] += wgt * __ldg(G + gi);
-                    x[1] += wgt * __ldg(G + cm.ng + gi);
-                    x[2] += wgt * __ldg(G + 2 * cm.ng + gi);
+                    for (int q = 0; q < 3; ++q) x[q] = dd_add(x[q], dd_mul(wgt, mkdd(__ldg(G + q * cm.ng + gi))));
                 }
         Xs[t] = x[0];
         Xs[no + t] = x[1];
         Xs[2 * no + t] = x[2];
     }
     __syncthreads();
-    const double* D1 = tab->D[o1 - 1];
-    const double* D2 = tab->D[o2 - 1];
-    const double* D3 = tab->D[o3 - 1];
     for (int t = threadIdx.x; t < no; t += blockDim.x) {
         int i, j, k;
         node_ijk(t, o1, o2, i, j, k);
-        double dx[3][3];  // dx[dd][c] = d x_c / d xi_dd
+        dd dx[3][3];  // dx[dd][c] = d x_c / d xi_dd
         for (int c = 0; c < 3; ++c) {
-            const double* X = Xs + c * no;
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-            for (int m = 0; m < o1; ++m) s0 += D1[i * o1 + m] * X[m + o1 * (j + o2 * k)];
-            for (int m = 0; m < o2; ++m) s1 += D2[j * o2 + m] * X[i + o1 * (m + o2 * k)];
-            for (int m = 0; m < o3; ++m) s2 += D3[k * o3 + m] * X[i + o1 * (j + o2 * m)];
+            const dd* X = Xs + c * no;
+            dd s0 = mkdd(0.0), s1 = mkdd(0.0), s2 = mkdd(0.0);
+            for (int m = 0; m < o1; ++m) {
+                const dd Dv = {tdd->Dhi[o1 - 1][i * o1 + m], tdd->Dlo[o1 - 1][i * o1 + m]};
+                s0 = dd_add(s0, dd_mul(Dv, X[m + o1 * (j + o2 * k)]));
+            }
+            for (int m = 0; m < o2; ++m) {
+                const dd Dv = {tdd->Dhi[o2 - 1][j * o2 + m], tdd->Dlo[o2 - 1][j * o2 + m]};
+                s1 = dd_add(s1, dd_mul(Dv, X[i + o1 * (m + o2 * k)]));
+            }
+            for (int m = 0; m < o3; ++m) {
+                const dd Dv = {tdd->Dhi[o3 - 1][k * o3 + m], tdd->Dlo[o3 - 1][k * o3 + m]};
+                s2 = dd_add(s2, dd_mul(Dv, X[i + o1 * (j + o2 * m)]));
+            }
             dx[0][c] = s0;
             dx[1][c] = s1;
             dx[2][c] = s2;
         }
-        const double* xa = dx[0];
-        const double* xb = dx[1];
-        const double* xc = dx[2];
-        const double c1[3] = {xb[1] * xc[2] - xb[2] * xc[1], xb[2] * xc[0] - xb[0] * xc[2], xb[0] * xc[1] - xb[1] * xc[0]};
-        const double c2[3] = {xc[1] * xa[2] - xc[2] * xa[1], xc[2] * xa[0] - xc[0] * xa[2], xc[0] * xa[1] - xc[1] * xa[0]};
-        const double c3[3] = {xa[1] * xb[2] - xa[2] * xb[1], xa[2] * xb[0] - xa[0] * xb[2], xa[0] * xb[1] - xa[1] * xb[0]};
+        const dd* xa = dx[0];
+        const dd* xb = dx[1];
+        const dd* xc = dx[2];
+        // c = a x b in dd
+        auto cross = [](const dd* a, const dd* b, dd* r) {
+            r[0] = dd_add(dd_mul(a[1], b[2]), dd_neg(dd_mul(a[2], b[1])));
+            r[1] = dd_add(dd_mul(a[2], b[0]), dd_neg(dd_mul(a[0], b[2])));
+            r[2] = dd_add(dd_mul(a[0], b[1]), dd_neg(dd_mul(a[1], b[0])));
+        };
+        dd c1[3], c2[3], c3[3];
+        cross(xb, xc, c1);
+        cross(xc, xa, c2);
+        cross(xa, xb, c3);
         for (int q = 0; q < 3; ++q) {
-            Mout[q * no + t] = c1[q];
-            Mout[(3 + q) * no + t] = c2[q];
-            Mout[(6 + q) * no + t] = c3[q];
+            Mout[q * no + t] = c1[q].hi + c1[q].lo;
+            Mout[(3 + q) * no + t] = c2[q].hi + c2[q].lo;
+            Mout[(6 + q) * no + t] = c3[q].hi + c3[q].lo;
         }
-        Mout[9 * no + t] = xa[0] * c1[0] + xa[1] * c1[1] + xa[2] * c1[2];
+        const dd J = dd_add(dd_add(dd_mul(xa[0], c1[0]), dd_mul(xa[1], c1[1])), dd_mul(xa[2], c1[2]));
+        Mout[9 * no + t] = J.hi + J.lo;
     }
     __syncthreads();
 }
@@ -167,7 +211,7 @@ struct MetParams {
     const int* orders;
     const long long* off;  // state offsets (metrics at 2x)
     double* met;
-    const Tables* tab;
+    const TablesDD* tdd;
 };
 
 __global__ void __launch_bounds__(CBS) k_metrics(MetParams P)
@@ -176,9 +220,9 @@ __global__ void __launch_bounds__(CBS) k_metrics(MetParams P)
     const int e = blockIdx.x;
     const int o1 = P.orders[3 * e] + 1, o2 = P.orders[3 * e + 1] + 1, o3 = P.orders[3 * e + 2] + 1;
     const int no = o1 * o2 * o3;
-    double* Xs = sm;
-    double* Ms = sm + 3 * no;
-    element_metrics(P.cm, e, o1, o2, o3, P.tab, Xs, Ms);
+    dd* Xs = reinterpret_cast<dd*>(sm);
+    double* Ms = sm + 6 * no;
+    element_metrics(P.cm, e, o1, o2, o3, P.tdd, Xs, Ms);
     double* out = P.met + 2 * P.off[e];
     for (int t = threadIdx.x; t < 10 * no; t += blockDim.x) out[t] = Ms[t];
 }
@@ -538,6 +582,7 @@ __global__ void k_dt_final2(unsigned long long* maxbits, double cfl, double dfl,
 // mode 1: qhat Ja_k (15 per point, projected).
 // ---------------------------------------------------------------------------
 struct CMortarParams {
+    const TablesDD* tdd;
     const double* q;
     const double* grad;
     const int* orders;
@@ -553,7 +598,7 @@ struct CMortarParams {
 
 __global__ void __launch_bounds__(128) k_mortar_curved(CMortarParams P)
 {
-    __shared__ double Xm[3][NP * NP];
+    __shared__ double Xm[3][NP * NP], Xml[3][NP * NP];
     __shared__ double Jm[3][NP * NP];
     __shared__ double GM[15][NP * NP];
     const MortarItem it = P.items[blockIdx.x];
@@ -564,41 +609,52 @@ __global__ void __launch_bounds__(128) k_mortar_curved(CMortarParams P)
     const int M1 = max(NL[ta], NR[ta]), M2 = max(NL[tb], NR[tb]);
     const int nm = (M1 + 1) * (M2 + 1);
     const int gd[3] = {P.cm.g1, P.cm.g2, P.cm.g3};
-    // face coordinates of L's +1 face at the mortar nodes (GL geometry nodes: last layer along d)
+    // face coordinates of L's +1 face at the mortar nodes (GL geometry nodes:
+    // last layer along d), tangential derivatives, cross product -- in dd
     const double* G = P.cm.geo + (long long)it.L * 3 * P.cm.ng;
-    const double* Ta = P.tab->T[gd[ta]][M1];
-    const double* Tb = P.tab->T[gd[tb]][M2];
     const int ga = gd[0] + 1, gb = gd[1] + 1;
+    const TablesDD* tdd = P.tdd;
     for (int t = threadIdx.x; t < nm; t += blockDim.x) {
         const int m1 = t % (M1 + 1), m2 = t / (M1 + 1);
-        double x[3] = {0.0, 0.0, 0.0};
+        dd x[3] = {mkdd(0.0), mkdd(0.0), mkdd(0.0)};
         for (int b = 0; b <= gd[tb]; ++b)
             for (int a = 0; a <= gd[ta]; ++a) {
                 int idx[3];
                 idx[d] = gd[d]; idx[ta] = a; idx[tb] = b;
                 const int gi = idx[0] + ga * (idx[1] + gb * idx[2]);
-                const double wgt = Ta[m1 * (gd[ta] + 1) + a] * Tb[m2 * (gd[tb] + 1) + b];
-                for (int c = 0; c < 3; ++c) x[c] += wgt * G[c * P.cm.ng + gi];
+                const int ia = m1 * (gd[ta] + 1) + a, ib = m2 * (gd[tb] + 1) + b;
+                const dd wgt = dd_mul(dd{tdd->Thi[gd[ta]][M1][ia], tdd->Tlo[gd[ta]][M1][ia]},
+                                      dd{tdd->Thi[gd[tb]][M2][ib], tdd->Tlo[gd[tb]][M2][ib]});
+                for (int c = 0; c < 3; ++c) x[c] = dd_add(x[c], dd_mul(wgt, mkdd(G[c * P.cm.ng + gi])));
             }
-        for (int c = 0; c < 3; ++c) Xm[c][t] = x[c];
+        for (int c = 0; c < 3; ++c) { Xm[c][t] = x[c].hi; Xml[c][t] = x[c].lo; }
     }
     __syncthreads();
-    const double* D1 = P.tab->D[M1];
-    const double* D2 = P.tab->D[M2];
     for (int t = threadIdx.x; t < nm; t += blockDim.x) {
         const int m1 = t % (M1 + 1), m2 = t / (M1 + 1);
-        double u[3], v[3];
+        dd u[3], v[3];
         for (int c = 0; c < 3; ++c) {
-            double s1 = 0.0, s2 = 0.0;
-            for (int m = 0; m <= M1; ++m) s1 += D1[m1 * (M1 + 1) + m] * Xm[c][m + (M1 + 1) * m2];
-            for (int m = 0; m <= M2; ++m) s2 += D2[m2 * (M2 + 1) + m] * Xm[c][m1 + (M1 + 1) * m];
+            dd s1 = mkdd(0.0), s2 = mkdd(0.0);
+            for (int m = 0; m <= M1; ++m) {
+                const int ix = m + (M1 + 1) * m2;
+                s1 = dd_add(s1, dd_mul(dd{tdd->Dhi[M1][m1 * (M1 + 1) + m], tdd->Dlo[M1][m1 * (M1 + 1) + m]},
+                                       dd{Xm[c][ix], Xml[c][ix]}));
+            }
+            for (int m = 0; m <= M2; ++m) {
+                const int ix = m1 + (M1 + 1) * m;
+                s2 = dd_add(s2, dd_mul(dd{tdd->Dhi[M2][m2 * (M2 + 1) + m], tdd->Dlo[M2][m2 * (M2 + 1) + m]},
+                                       dd{Xm[c][ix], Xml[c][ix]}));
+            }
             u[c] = s1;
             v[c] = s2;
         }
-        double w[3];
-        if (d == 1) { w[0] = v[1] * u[2] - v[2] * u[1]; w[1] = v[2] * u[0] - v[0] * u[2]; w[2] = v[0] * u[1] - v[1] * u[0]; }
-        else { w[0] = u[1] * v[2] - u[2] * v[1]; w[1] = u[2] * v[0] - u[0] * v[2]; w[2] = u[0] * v[1] - u[1] * v[0]; }
-        for (int c = 0; c < 3; ++c) Jm[c][t] = w[c];
+        dd w[3];
+        const dd* A = d == 1 ? v : u;  // Ja^2 = x_zeta x x_xi = x_t2 x x_t1
+        const dd* B = d == 1 ? u : v;
+        w[0] = dd_add(dd_mul(A[1], B[2]), dd_neg(dd_mul(A[2], B[1])));
+        w[1] = dd_add(dd_mul(A[2], B[0]), dd_neg(dd_mul(A[0], B[2])));
+        w[2] = dd_add(dd_mul(A[0], B[1]), dd_neg(dd_mul(A[1], B[0])));
+        for (int c = 0; c < 3; ++c) Jm[c][t] = w[c].hi + w[c].lo;
     }
     __syncthreads();
     const int nL = (NL[0] + 1) * (NL[1] + 1) * (NL[2] + 1), nR = (NR[0] + 1) * (NR[1] + 1) * (NR[2] + 1);
@@ -682,6 +738,7 @@ __global__ void __launch_bounds__(128) k_mortar_curved(CMortarParams P)
 // isolated BR1 gradient (strong form) and isolated residual at O.
 // ---------------------------------------------------------------------------
 struct CTauParams {
+    const TablesDD* tdd;
     const double* q;
     const double* qref;
     double* tau;
@@ -713,7 +770,7 @@ __global__ void __launch_bounds__(CBS) k_tau_curved(CTauParams P)
     double* F = Rc + NV * nO;     // 5 nO (also 3 nO coordinates at first)
     double* A = F + NV * nO;      // 5 nO
     double* GA = A + NV * nO;     // 15 nO (NS)
-    element_metrics(P.cm, e, o1, o2, o3, P.tab, F, Mc);
+    element_metrics(P.cm, e, o1, o2, o3, P.tdd, reinterpret_cast<dd*>(F), Mc);  // F, A: 10 nO >= 6 nO scratch
     const long long o = P.off[e];
     const double* T = P.tab->T[nd - 1][p];
     for (int t = threadIdx.x; t < nO; t += CBS) {

@@ -61,6 +61,7 @@ struct dg_ctx {
     int maxn = 0;
     // device
     Tables* d_tab = nullptr;
+    TablesDD* d_tdd = nullptr;
     int* d_nbr = nullptr;
     double* d_h = nullptr;
     int* d_orders = nullptr;
@@ -80,6 +81,7 @@ struct dg_ctx {
     std::vector<int> tr_orders_host;
     // curved geometry / Navier-Stokes
     bool curved = false;
+    int smem_limit = 0;
     double* d_geo = nullptr;
     double* d_met = nullptr;       // 10 per node
     double* d_grad = nullptr;      // 15 per node (NS)
@@ -180,6 +182,16 @@ CurvedMesh curved_mesh(const dg_ctx* ctx)
     return cm;
 }
 
+const TablesDD& host_tables_dd()
+{
+    static TablesDD* t = nullptr;
+    if (!t) {
+        t = new TablesDD;
+        build_tables_dd(t);
+    }
+    return *t;
+}
+
 }  // namespace
 
 extern "C" {
@@ -204,7 +216,10 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         (s = cuda_check(ctx, cudaMemset(ctx->d_scratch, 0, 8 * sizeof(unsigned long long)), "scratch")) != DG_OK ||
         (s = cuda_check(ctx, cudaMalloc(&ctx->d_flag, 4 * sizeof(int)), "flag")) != DG_OK ||
         (s = cuda_check(ctx, cudaMemset(ctx->d_flag, 0, 4 * sizeof(int)), "flag")) != DG_OK ||
-        (s = cuda_check(ctx, cudaMalloc(&ctx->d_sums, 8 * sizeof(double)), "sums")) != DG_OK) {
+        (s = cuda_check(ctx, cudaMalloc(&ctx->d_sums, 8 * sizeof(double)), "sums")) != DG_OK ||
+        (s = cuda_check(ctx, cudaMalloc(&ctx->d_tdd, sizeof(TablesDD)), "dd tables")) != DG_OK ||
+        (s = cuda_check(ctx, cudaMemcpy(ctx->d_tdd, &host_tables_dd(), sizeof(TablesDD), cudaMemcpyHostToDevice),
+                        "dd tables")) != DG_OK) {
         dg_destroy(ctx);
         return s;
     }
@@ -224,18 +239,30 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         const char* g = getenv("DGTAU_GENERIC");
         ctx->generic = g && g[0] == '1';
     }
-    // large dynamic shared memory for the element kernels
-    cudaFuncSetAttribute(k_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_tau, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_tau2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_tau3, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
-    cudaFuncSetAttribute(k_tau3, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(k_tau2, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
-    cudaFuncSetAttribute(k_transfer, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_metrics, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_res_curved, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_tau_curved, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    // large dynamic shared memory for the element kernels (opt-in limit minus static smem)
+    {
+        int optin = 0;
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+        const int lim = optin - 1024;  // headroom for static shared arrays
+        cudaFuncSetAttribute(k_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
+        cudaFuncSetAttribute(k_tau, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
+        cudaFuncSetAttribute(k_tau2, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
+        cudaFuncSetAttribute(k_tau2, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+        cudaFuncSetAttribute(k_tau3, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(140 * 1024, lim));
+        cudaFuncSetAttribute(k_tau3, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+        cudaFuncSetAttribute(k_transfer, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
+        cudaFuncSetAttribute(k_metrics, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+        cudaFuncSetAttribute(k_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+        cudaFuncSetAttribute(k_res_curved, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+        cudaFuncSetAttribute(k_tau_curved, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+        ctx->smem_limit = lim;
+        cudaError_t e = cudaGetLastError();  // attribute errors are fatal here, not stale later
+        if (e != cudaSuccess) {
+            s = cuda_check(ctx, e, "cudaFuncSetAttribute");
+            dg_destroy(ctx);
+            return s;
+        }
+    }
     *out = ctx;
     return DG_OK;
 }
@@ -244,6 +271,7 @@ void dg_destroy(dg_ctx* ctx)
 {
     if (!ctx) return;
     dfree(ctx->d_tab);
+    dfree(ctx->d_tdd);
     dfree(ctx->d_nbr);
     dfree(ctx->d_h);
     dfree(ctx->d_orders);
@@ -483,8 +511,8 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
         M.orders = ctx->d_orders;
         M.off = ctx->d_off;
         M.met = ctx->d_met;
-        M.tab = ctx->d_tab;
-        k_metrics<<<E, CBS, sizeof(double) * 13 * (size_t)ctx->maxn>>>(M);
+        M.tdd = ctx->d_tdd;
+        k_metrics<<<E, CBS, sizeof(double) * 16 * (size_t)ctx->maxn>>>(M);
         ctx->launches++;
         CK(cudaGetLastError());
         CK(cudaDeviceSynchronize());
@@ -550,6 +578,7 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
     P.ph = phys_dev(ctx->prm);
     P.flag = ctx->d_flag;
     CMortarParams M{};
+    M.tdd = ctx->d_tdd;
     M.q = q;
     M.grad = ctx->d_grad;
     M.orders = ctx->d_orders;
@@ -779,8 +808,9 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
         ctx->launches++;
         if (ctx->curved && ctx->nlevels > 0) {
             const size_t sm = sizeof(double) * (ctx->prm.physics == DG_NS ? 45 : 30) * (size_t)ctx->max_level;
-            if (sm > 227 * 1024) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: coarse level too large for shared memory");
+            if ((long long)sm > ctx->smem_limit) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: coarse level too large for shared memory");
             CTauParams C;
+            C.tdd = ctx->d_tdd;
             C.q = q_dev;
             C.qref = ref;
             C.tau = tau_dev;
