@@ -102,10 +102,19 @@ dg_status dg_mesh_upload(dg_ctx* ctx, int E, const int32_t* nbr_host, const int3
  * (N1,N2,N3) bucket work list and the mortar face plan.  Synchronous. */
 dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host);
 
+/* Multi-rank local meshes: elements [0, n_owned) are owned (computed),
+ * elements [n_owned, E) are halo copies of other ranks' elements whose state
+ * the caller refreshes (one face-trace exchange per residual).
+ * Neighbour code -3 marks "outside the local set" (allowed for halo elements
+ * only).  Call after dg_mesh_upload and before dg_set_orders; default E. */
+dg_status dg_set_owned(dg_ctx* ctx, int n_owned);
+
 /* Number of doubles in a state vector for the current orders (5 * NDOF). */
 int64_t dg_state_len(const dg_ctx* ctx);
-/* NDOF = sum_e prod_d (N_d+1). */
+/* NDOF = sum_e prod_d (N_d+1) over all local elements. */
 int64_t dg_ndof(const dg_ctx* ctx);
+/* Length (doubles) of the owned part of a state vector (owned elements first). */
+int64_t dg_owned_state_len(const dg_ctx* ctx);
 
 /* Node coordinates at the solution nodes, host [e][3][n] (for building
  * initial conditions).  Synchronous. */
@@ -137,6 +146,19 @@ dg_status dg_rk_step(dg_ctx* ctx, double* q_in_dev, double* q_out_dev, double* g
 dg_status dg_rk_step_dt(dg_ctx* ctx, double* q_in_dev, double* q_out_dev, double* g_dev, const double* dt_dev,
                         double cfl, double* dt_next_dev, void* stream);
 
+/* One stage k in {0,1,2} of the Williamson RK3 step, for callers
+ * that refresh halo states between stages: q_out = q_in + B_k g' with
+ * g' = A_k g + dt Qdot(q_in) on owned elements.  If lam_accum_dev != NULL
+ * (2 x uint64, zeroed, device) the CFL (and DFL) rates of q_out are
+ * max-reduced into it (as bits of non-negative doubles, so an integer MAX
+ * all-reduce across ranks is exact). */
+dg_status dg_rk_stage(dg_ctx* ctx, int stage, const double* q_in_dev, double* q_out_dev, double* g_dev,
+                      const double* dt_dev, unsigned long long* lam_accum_dev, void* stream);
+/* Max-reduce the CFL/DFL rates of q (owned elements) into lam_accum_dev. */
+dg_status dg_dt_accumulate(dg_ctx* ctx, const double* q_dev, unsigned long long* lam_accum_dev, void* stream);
+/* dt_dev[0] = min(cfl / lam, cfl / nu) from lam_accum_dev; resets it to 0. */
+dg_status dg_dt_finalize(dg_ctx* ctx, unsigned long long* lam_accum_dev, double cfl, double* dt_dev, void* stream);
+
 /* Batched tau-estimation over all coarse orders p < N_d of every element and
  * direction, isolated coarse residuals, in one launch.  qdot_ref_dev
  * is required for DG_REF_SOLVER and ignored for DG_REF_SAME.  tau_dev is
@@ -156,6 +178,16 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* opts, const double* q_
  * Synchronises the stream. */
 dg_status dg_select_orders(dg_ctx* ctx, const dg_adapt_policy* pol, const double* tau_dev, double* total_map_dev,
                            int32_t* orders_out_host, double* margin_host, void* stream);
+
+/* Multi-rank selection pieces: map / min-NDOF / decrease cap for the owned
+ * elements into orders_out_dev (int32 [E][3] device; halo rows = current
+ * orders), and one Jacobi sweep of the jump fixpoint (eqs N23 / N_1) over
+ * owned elements (halo rows copied through; *changed_dev |= 1 if any owned
+ * order rose).  The caller exchanges halo rows and all-reduces `changed`. */
+dg_status dg_select_local(dg_ctx* ctx, const dg_adapt_policy* pol, const double* tau_dev, double* total_map_dev,
+                          int32_t* orders_out_dev, double* margin_dev, void* stream);
+dg_status dg_jump_sweep(dg_ctx* ctx, const int32_t* orders_in_dev, int32_t* orders_out_dev, int rule, int Nmax,
+                        int32_t* changed_dev, void* stream);
 
 /* Project a state from the current orders to new_orders (P:299-301:
  * "the solution projected in the new polynomial spaces"; per-direction

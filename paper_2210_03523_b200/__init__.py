@@ -36,7 +36,8 @@ NMAX = 8
 
 EXPORTS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_upload", "dg_set_orders", "dg_state_len", "dg_ndof",
            "dg_node_coords", "dg_rhs_eval", "dg_compute_dt", "dg_rk_step", "dg_tau_estimate", "dg_select_orders",
-           "dg_transfer", "dg_diagnostics", "dg_launch_count", "dg_rk_step_dt"]
+           "dg_transfer", "dg_diagnostics", "dg_launch_count", "dg_rk_step_dt", "dg_set_owned", "dg_rk_stage",
+           "dg_dt_accumulate", "dg_dt_finalize", "dg_select_local", "dg_jump_sweep", "dg_owned_state_len"]
 
 
 def sources():
@@ -124,6 +125,7 @@ def lib():
         L.dg_state_len.restype = C.c_int64
         L.dg_ndof.restype = C.c_int64
         L.dg_launch_count.restype = C.c_int64
+        L.dg_owned_state_len.restype = C.c_int64
         for name in EXPORTS:
             getattr(L, name)
         _lib = L
@@ -239,6 +241,33 @@ class Solver:
         """RK3 step; the CFL dt of the new state is reduced inside the last stage."""
         self._check(self.L.dg_rk_step_dt(self.ctx, _ptr(q_in), _ptr(q_out), _ptr(g), _ptr(dt), C.c_double(cfl),
                                          _ptr(dt_next), _stream(stream)), "dg_rk_step_dt")
+
+    # -- multi-rank pieces (see dist.py) ---------------------------------------
+    def set_owned(self, n_owned):
+        self._check(self.L.dg_set_owned(self.ctx, int(n_owned)), "dg_set_owned")
+
+    def owned_len(self):
+        return int(self.L.dg_owned_state_len(self.ctx))
+
+    def rk_stage(self, k, q_in, q_out, g, dt, lam=None, stream=None):
+        self._check(self.L.dg_rk_stage(self.ctx, int(k), _ptr(q_in), _ptr(q_out), _ptr(g), _ptr(dt), _ptr(lam),
+                                       _stream(stream)), "dg_rk_stage")
+
+    def dt_accumulate(self, q, lam, stream=None):
+        self._check(self.L.dg_dt_accumulate(self.ctx, _ptr(q), _ptr(lam), _stream(stream)), "dg_dt_accumulate")
+
+    def dt_finalize(self, lam, cfl, dt, stream=None):
+        self._check(self.L.dg_dt_finalize(self.ctx, _ptr(lam), C.c_double(cfl), _ptr(dt), _stream(stream)),
+                    "dg_dt_finalize")
+
+    def select_local(self, tau, tau_max, Nmin, Nmax, out, mode=SELECT_DYNAMIC, dec_cap=1, total_map=None, stream=None):
+        pol = _Policy(int(mode), float(tau_max), int(Nmin), int(Nmax), JUMP_B, int(dec_cap))
+        self._check(self.L.dg_select_local(self.ctx, C.byref(pol), _ptr(tau), _ptr(total_map), _ptr(out), None,
+                                           _stream(stream)), "dg_select_local")
+
+    def jump_sweep(self, a, b, rule, Nmax, changed, stream=None):
+        self._check(self.L.dg_jump_sweep(self.ctx, _ptr(a), _ptr(b), int(rule), int(Nmax), _ptr(changed),
+                                         _stream(stream)), "dg_jump_sweep")
 
     def tau_estimate(self, q, qdot_ref=None, formulation=TAU_NEW, reference=REF_SOLVER, tau=None, stream=None):
         import torch

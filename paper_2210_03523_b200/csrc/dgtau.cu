@@ -44,7 +44,8 @@ struct dg_ctx {
     dg_params prm{};
     int device = 0;
     // mesh
-    int E = 0;
+    int E = 0;       // local elements: owned [0, n_own) then halo copies
+    int n_own = 0;   // elements whose residual this context computes
     int gorder[3] = {1, 1, 1};
     std::vector<int> nbr;
     std::vector<double> geo;
@@ -310,16 +311,17 @@ dg_status dg_mesh_upload(dg_ctx* ctx, int E, const int32_t* nbr_host, const int3
     for (int d = 0; d < 3; ++d)
         if (gorder_host[d] < 1 || gorder_host[d] > NMAX) return fail(ctx, DG_EINVAL, "mesh: geometry order out of range");
     for (long long i = 0; i < 6LL * E; ++i)
-        if (nbr_host[i] >= E || nbr_host[i] < -2) return fail(ctx, DG_EINVAL, "mesh: neighbour id out of range");
+        if (nbr_host[i] >= E || nbr_host[i] < -3) return fail(ctx, DG_EINVAL, "mesh: neighbour id out of range");
     // aligned-axes check: e's face f neighbour must see e across the opposite face
     for (int e = 0; e < E; ++e)
         for (int f = 0; f < 6; ++f) {
             int nb = nbr_host[6 * e + f];
-            if (nb >= 0 && nbr_host[6 * nb + (f ^ 1)] != e)
+            if (nb >= 0 && nbr_host[6 * nb + (f ^ 1)] != e && nbr_host[6 * nb + (f ^ 1)] != -3)
                 return fail(ctx, DG_EINVAL, "mesh: neighbour local axes not aligned (face " + std::to_string(f) +
                                                 " of element " + std::to_string(e) + ")");
         }
     ctx->E = E;
+    ctx->n_own = E;
     for (int d = 0; d < 3; ++d) ctx->gorder[d] = gorder_host[d];
     const int ng = (gorder_host[0] + 1) * (gorder_host[1] + 1) * (gorder_host[2] + 1);
     ctx->nbr.assign(nbr_host, nbr_host + 6LL * E);
@@ -372,7 +374,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     // (N1,N2,N3) buckets -> work items of up to floor(256/n) elements, ordered
     // by their first element id (spatially coherent sweep, neighbour traces hit L2)
     std::map<int, std::vector<int>> buckets;
-    for (int e = 0; e < E; ++e) {
+    for (int e = 0; e < ctx->n_own; ++e) {
         const int* N = &ctx->orders[3 * e];
         buckets[N[0] | (N[1] << 8) | (N[2] << 16)].push_back(e);
     }
@@ -416,6 +418,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
         for (int d = 0; d < 3; ++d) {
             const int nb = ctx->nbr[6 * e + 2 * d + 1];
             if (nb < 0) continue;
+            if (e >= ctx->n_own && nb >= ctx->n_own) continue;  // halo-halo face: not needed
             const int* NL = &ctx->orders[3 * e];
             const int* NR = &ctx->orders[3 * nb];
             if (NL[TA[d]] == NR[TA[d]] && NL[TB[d]] == NR[TB[d]]) continue;
@@ -437,6 +440,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
             const int* No = &ctx->orders[3 * e];
             if (nb == -1) fi.kind = 2;
             else if (nb == -2) fi.kind = 3;
+            else if (nb == -3) fi.kind = 4;  // outside the local set (halo elements only; never read)
             else if (moff[6LL * e + f] >= 0) {
                 fi.kind = 1;
                 fi.off = moff[6LL * e + f];
@@ -466,7 +470,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     // tau-estimation levels (e, d, p < N_d), largest first for load balance
     std::vector<TauLevel> lv;
     ctx->max_level = 0;
-    for (int e = 0; e < E; ++e)
+    for (int e = 0; e < ctx->n_own; ++e)
         for (int d = 0; d < 3; ++d)
             for (int p = 1; p < ctx->orders[3 * e + d]; ++p) {
                 lv.push_back(TauLevel{e, d, p, 0});
@@ -523,6 +527,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
 
 int64_t dg_state_len(const dg_ctx* ctx) { return ctx && ctx->have_orders ? ctx->off[ctx->E] : 0; }
 int64_t dg_ndof(const dg_ctx* ctx) { return ctx && ctx->have_orders ? ctx->ndof : 0; }
+int64_t dg_owned_state_len(const dg_ctx* ctx) { return ctx && ctx->have_orders ? ctx->off[ctx->n_own] : 0; }
 
 dg_status dg_node_coords(dg_ctx* ctx, double* X)
 {
@@ -599,7 +604,7 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
         P.mode = 0;
         P.out = ctx->d_grad;
         P.mortarG = ctx->d_mortarGq;
-        k_grad<<<ctx->E, CBS, sizeof(double) * 25 * (size_t)ctx->maxn, st>>>(P);
+        k_grad<<<ctx->n_own, CBS, sizeof(double) * 25 * (size_t)ctx->maxn, st>>>(P);
         ctx->launches++;
     }
     if (mort) {
@@ -612,7 +617,7 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
     P.out = out;
     P.mortarG = ctx->d_mortarG;
     P.lam_max = lam_max;
-    k_res_curved<<<ctx->E, CBS, sizeof(double) * 15 * (size_t)ctx->maxn, st>>>(P);
+    k_res_curved<<<ctx->n_own, CBS, sizeof(double) * 15 * (size_t)ctx->maxn, st>>>(P);
     ctx->launches++;
     return check_stream_error(ctx, "curved residual launch");
 }
@@ -696,7 +701,7 @@ dg_status dg_compute_dt(dg_ctx* ctx, const double* q_dev, double cfl, double* dt
         C.met = ctx->d_met;
         C.ph = phys_dev(ctx->prm);
         C.maxbits = ctx->d_scratch;
-        k_dt_curved<<<ctx->E, CBS, 0, st>>>(C);
+        k_dt_curved<<<ctx->n_own, CBS, 0, st>>>(C);
         k_dt_final2<<<1, 1, 0, st>>>(ctx->d_scratch, cfl, cfl, dt_dev);
         ctx->launches += 2;
         dg_status s = check_stream_error(ctx, "k_dt_curved launch");
@@ -769,6 +774,109 @@ dg_status dg_rk_step_dt(dg_ctx* ctx, double* q_in, double* q_out, double* g, con
     return check_stream_error(ctx, "k_dt_final launch");
 }
 
+dg_status dg_set_owned(dg_ctx* ctx, int n_owned)
+{
+    if (!ctx) return DG_EINVAL;
+    if (ctx->E == 0) return fail(ctx, DG_ESTATE, "set_owned: no mesh");
+    if (n_owned < 1 || n_owned > ctx->E) return fail(ctx, DG_EINVAL, "set_owned: 1 <= n_owned <= E");
+    for (long long i = 0; i < 6LL * n_owned; ++i)
+        if (ctx->nbr[i] == -3) return fail(ctx, DG_EINVAL, "set_owned: an owned element has an outside neighbour");
+    ctx->n_own = n_owned;
+    ctx->have_orders = false;
+    return DG_OK;
+}
+
+dg_status dg_rk_stage(dg_ctx* ctx, int stage, const double* q_in, double* q_out, double* g, const double* dt_dev,
+                      unsigned long long* lam_accum_dev, void* stream)
+{
+    if (!ctx || !q_in || !q_out || !g || !dt_dev || q_in == q_out || stage < 0 || stage > 2) return DG_EINVAL;
+    if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "rk_stage: orders not set");
+    if (ctx->prm.physics == DG_NS && !ctx->curved) return fail(ctx, DG_EUNSUPPORTED, "rk_stage: NS needs the curved path");
+    static const double A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
+    static const double B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
+    return launch_residual(ctx, DG_NONISOLATED, q_in, q_out, g, dt_dev, A[stage], B[stage], 1, (cudaStream_t)stream,
+                           lam_accum_dev);
+}
+
+dg_status dg_dt_finalize(dg_ctx* ctx, unsigned long long* lam_accum_dev, double cfl, double* dt_dev, void* stream)
+{
+    if (!ctx || !lam_accum_dev || !dt_dev || !(cfl > 0)) return DG_EINVAL;
+    k_dt_final2<<<1, 1, 0, (cudaStream_t)stream>>>(lam_accum_dev, cfl, cfl, dt_dev);
+    ctx->launches++;
+    return check_stream_error(ctx, "k_dt_final2 launch");
+}
+
+dg_status dg_dt_accumulate(dg_ctx* ctx, const double* q_dev, unsigned long long* lam_accum_dev, void* stream)
+{
+    if (!ctx || !q_dev || !lam_accum_dev) return DG_EINVAL;
+    if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "dt_accumulate: orders not set");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (ctx->curved) {
+        CDtParams C;
+        C.q = q_dev;
+        C.orders = ctx->d_orders;
+        C.off = ctx->d_off;
+        C.met = ctx->d_met;
+        C.ph = phys_dev(ctx->prm);
+        C.maxbits = lam_accum_dev;
+        k_dt_curved<<<ctx->n_own, CBS, 0, st>>>(C);
+    } else {
+        DtParams P;
+        P.q = q_dev;
+        P.work = ctx->d_work;
+        P.elist = ctx->d_elist;
+        P.off = ctx->d_off;
+        P.hgeo = ctx->d_h;
+        P.gamma = ctx->prm.gamma;
+        P.maxbits = lam_accum_dev;
+        k_dt<<<ctx->nwork, BLOCK, 0, st>>>(P);
+    }
+    ctx->launches++;
+    return check_stream_error(ctx, "dt accumulate launch");
+}
+
+dg_status dg_select_local(dg_ctx* ctx, const dg_adapt_policy* pol, const double* tau_dev, double* total_dev,
+                          int32_t* orders_out_dev, double* margin_dev, void* stream)
+{
+    if (!ctx || !pol || !tau_dev || !orders_out_dev) return DG_EINVAL;
+    if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "select_local: orders not set");
+    if (pol->Nmin < 1 || pol->Nmax > NMAX || pol->Nmin > pol->Nmax || !(pol->tau_max > 0) || pol->dec_cap < 0)
+        return fail(ctx, DG_EINVAL, "select_local: bad policy");
+    if (pol->mode != DG_SELECT_DYNAMIC && !total_dev) return fail(ctx, DG_EINVAL, "select_local: static needs total map");
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(cudaMemcpyAsync(orders_out_dev, ctx->d_orders, sizeof(int) * 3LL * ctx->E, cudaMemcpyDeviceToDevice, st));
+    SelParams P;
+    P.tau = tau_dev;
+    P.orders = ctx->d_orders;
+    P.total = total_dev;
+    P.sel = orders_out_dev;
+    P.margin = margin_dev;
+    P.E = ctx->n_own;
+    P.mode = pol->mode;
+    P.tau_max = pol->tau_max;
+    P.Nmin = pol->Nmin;
+    P.Nmax = pol->Nmax;
+    P.dec_cap = pol->dec_cap;
+    k_select<<<(ctx->n_own + 127) / 128, 128, 0, st>>>(P);
+    ctx->launches++;
+    return check_stream_error(ctx, "k_select launch");
+}
+
+dg_status dg_jump_sweep(dg_ctx* ctx, const int32_t* orders_in_dev, int32_t* orders_out_dev, int rule, int Nmax,
+                        int32_t* changed_dev, void* stream)
+{
+    if (!ctx || !orders_in_dev || !orders_out_dev || !changed_dev || orders_in_dev == orders_out_dev) return DG_EINVAL;
+    if (ctx->E == 0) return fail(ctx, DG_ESTATE, "jump_sweep: no mesh");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (ctx->n_own < ctx->E)
+        CK(cudaMemcpyAsync(orders_out_dev + 3LL * ctx->n_own, orders_in_dev + 3LL * ctx->n_own,
+                           sizeof(int) * 3LL * (ctx->E - ctx->n_own), cudaMemcpyDeviceToDevice, st));
+    k_jump<<<(ctx->n_own + 127) / 128, 128, 0, st>>>(ctx->d_nbr, orders_in_dev, orders_out_dev, ctx->n_own,
+                                                      rule == DG_JUMP_A ? 0 : 1, Nmax, changed_dev);
+    ctx->launches++;
+    return check_stream_error(ctx, "k_jump launch");
+}
+
 dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev, const double* qref_dev, double* tau_dev,
                           void* stream)
 {
@@ -788,7 +896,7 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
         P.tab = ctx->d_tab;
         P.formulation = o->formulation;
         P.ph = phys_dev(ctx->prm);
-        k_tau<<<ctx->E, BLOCK, smem, (cudaStream_t)stream>>>(P);
+        k_tau<<<ctx->n_own, BLOCK, smem, (cudaStream_t)stream>>>(P);
     } else {
         cudaStream_t st = (cudaStream_t)stream;
         const double* ref = qref_dev;
@@ -804,7 +912,7 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
             if (s != DG_OK) return s;
             ref = ctx->d_ref_scratch;
         }
-        k_tau_norm<<<ctx->E, 128, 0, st>>>(ref, tau_dev, ctx->d_orders, ctx->d_off);
+        k_tau_norm<<<ctx->n_own, 128, 0, st>>>(ref, tau_dev, ctx->d_orders, ctx->d_off);
         ctx->launches++;
         if (ctx->curved && ctx->nlevels > 0) {
             const size_t sm = sizeof(double) * (ctx->prm.physics == DG_NS ? 45 : 30) * (size_t)ctx->max_level;
@@ -858,13 +966,17 @@ dg_status dg_select_orders(dg_ctx* ctx, const dg_adapt_policy* pol, const double
     P.total = total_dev;
     P.sel = ctx->d_sel;
     P.margin = ctx->d_margin;
-    P.E = E;
+    P.E = ctx->n_own;
     P.mode = pol->mode;
     P.tau_max = pol->tau_max;
     P.Nmin = pol->Nmin;
     P.Nmax = pol->Nmax;
     P.dec_cap = pol->dec_cap;
-    k_select<<<(E + 127) / 128, 128, 0, st>>>(P);
+    // halo rows (multi-rank local meshes) keep their current orders
+    if (ctx->n_own < E)
+        CK(cudaMemcpyAsync(ctx->d_sel + 3LL * ctx->n_own, ctx->d_orders + 3LL * ctx->n_own,
+                           sizeof(int) * 3LL * (E - ctx->n_own), cudaMemcpyDeviceToDevice, st));
+    k_select<<<(ctx->n_own + 127) / 128, 128, 0, st>>>(P);
     ctx->launches++;
     dg_status s = check_stream_error(ctx, "k_select launch");
     if (s != DG_OK) return s;
@@ -874,8 +986,11 @@ dg_status dg_select_orders(dg_ctx* ctx, const dg_adapt_policy* pol, const double
     int* b = ctx->d_sel + 3LL * E;
     for (int sweep = 0; sweep < 64; ++sweep) {
         CK(cudaMemsetAsync(ctx->d_flag + 2, 0, sizeof(int), st));
-        k_jump<<<(E + 127) / 128, 128, 0, st>>>(ctx->d_nbr, a, b, E, pol->jump_rule == DG_JUMP_A ? 0 : 1, pol->Nmax,
-                                                 ctx->d_flag + 2);
+        if (ctx->n_own < E)
+            CK(cudaMemcpyAsync(b + 3LL * ctx->n_own, a + 3LL * ctx->n_own, sizeof(int) * 3LL * (E - ctx->n_own),
+                               cudaMemcpyDeviceToDevice, st));
+        k_jump<<<(ctx->n_own + 127) / 128, 128, 0, st>>>(ctx->d_nbr, a, b, ctx->n_own,
+                                                          pol->jump_rule == DG_JUMP_A ? 0 : 1, pol->Nmax, ctx->d_flag + 2);
         ctx->launches++;
         int changed = 0;
         CK(cudaMemcpyAsync(&changed, ctx->d_flag + 2, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -945,7 +1060,7 @@ dg_status dg_diagnostics(dg_ctx* ctx, const double* q_dev, const double* v_dev, 
     P.sums = ctx->d_sums;
     P.minbits = ctx->d_scratch + 1;
     P.neg = ctx->d_flag + 3;
-    k_diag<<<ctx->E, 128, 0, st>>>(P);
+    k_diag<<<ctx->n_own, 128, 0, st>>>(P);
     ctx->launches++;
     dg_status s = check_stream_error(ctx, "k_diag launch");
     if (s != DG_OK) return s;

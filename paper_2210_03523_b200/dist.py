@@ -1,0 +1,168 @@
+"""Multi-rank driver: one process per GPU, torch.distributed (NCCL over
+NVLink/NVSwitch on GPUs, gloo on CPU for tests) for the halo exchange and
+the global reductions; every numerical step runs in libdgtau's kernels.
+
+Per residual evaluation (RK stage, SOLVER reference) one halo exchange of
+element states with the face-neighbour ranks; per RK step one MAX
+all-reduce of the CFL/DFL rates (dt = CFL / global max, reading A11); per
+jump-fixpoint sweep one exchange of halo orders and one MAX all-reduce of the
+`changed` flag (the fixpoint is monotone, so the result is rank-count
+invariant).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import partition as part
+
+
+def exchange(tensor, plan: "part.HaloPlan", rank: int, group=None):
+    """Refresh halo ranges of `tensor` (1-D) from the owning ranks.  Contiguous
+    runs are sent as views (no packing when a run covers a peer's range)."""
+    import torch
+    import torch.distributed as dist
+
+    ops, bufs = [], []
+    for r in sorted(plan.send):
+        sruns, rruns = plan.send[r], plan.recv[r]
+        if len(sruns) == 1:
+            sbuf = tensor[sruns[0][0]:sruns[0][1]]
+        else:
+            sbuf = torch.cat([tensor[a:b] for a, b in sruns])
+        if len(rruns) == 1:
+            rbuf = tensor[rruns[0][0]:rruns[0][1]]
+        else:
+            rbuf = torch.empty(plan.recv_len[r], dtype=tensor.dtype, device=tensor.device)
+            bufs.append((rbuf, rruns))
+        ops.append(dist.P2POp(dist.isend, sbuf.contiguous(), r, group))
+        ops.append(dist.P2POp(dist.irecv, rbuf, r, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    for rbuf, rruns in bufs:
+        o = 0
+        for a, b in rruns:
+            tensor[a:b].copy_(rbuf[o:o + b - a])
+            o += b - a
+
+
+class DistSolver:
+    """A `Solver` on this rank's local mesh (owned + halo elements) plus the
+    exchanges that make owned results identical to the single-rank ones."""
+
+    def __init__(self, global_mesh, owner: np.ndarray, rank: int, world: int, group=None, **solver_kw):
+        from . import Solver
+
+        self.rank, self.world, self.group = rank, world, group
+        self.lm = part.local_mesh(global_mesh, owner, rank)
+        self.S = Solver(self.lm, **solver_kw)
+        self.S._check(self.S.L.dg_set_owned(self.S.ctx, int(self.lm.n_own)), "dg_set_owned")
+        self.plan = None
+        self.gplan = None
+        import torch
+
+        self._lam = torch.zeros(2, dtype=torch.int64, device="cuda")
+
+    # -- layout ------------------------------------------------------------
+    def set_orders(self, global_orders):
+        lo = np.ascontiguousarray(np.asarray(global_orders)[self.lm.gids], np.int32)
+        self.S.set_orders(lo)
+        self.local_orders = lo
+        self.plan = part.HaloPlan(self.lm, lo, 5)
+        self.gplan = part.HaloPlan(self.lm, lo, 15)
+
+    @property
+    def n_own(self):
+        return self.lm.n_own
+
+    def owned_len(self):
+        return int(self.S.L.dg_owned_state_len(self.S.ctx))
+
+    def new_state(self):
+        return self.S.new_state()
+
+    def halo(self, q):
+        exchange(q, self.plan, self.rank, self.group)
+
+    # -- operators -----------------------------------------------------------
+    def rhs_eval(self, q, qdot=None, variant=0):
+        if variant == 0:
+            self.halo(q)
+        return self.S.rhs_eval(q, qdot, variant=variant)
+
+    def compute_dt(self, q, cfl, dt):
+        import torch.distributed as dist
+
+        self._lam.zero_()
+        self.S._check(self.S.L.dg_dt_accumulate(self.S.ctx, C.c_void_p(q.data_ptr()),
+                                                C.c_void_p(self._lam.data_ptr()), self._stream()), "dg_dt_accumulate")
+        dist.all_reduce(self._lam, op=dist.ReduceOp.MAX, group=self.group)
+        self.S._check(self.S.L.dg_dt_finalize(self.S.ctx, C.c_void_p(self._lam.data_ptr()), C.c_double(cfl),
+                                              C.c_void_p(dt.data_ptr()), self._stream()), "dg_dt_finalize")
+        return dt
+
+    def _stream(self):
+        import torch
+
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def rk_step_dt(self, q_in, q_out, g, dt, cfl, dt_next):
+        """Three stages with a halo refresh before each; the CFL rates of the
+        new state are reduced in the last stage and MAX-all-reduced."""
+        import torch.distributed as dist
+
+        src, dst = [q_in, q_out, q_in], [q_out, q_in, q_out]
+        self._lam.zero_()
+        for k in range(3):
+            self.halo(src[k])
+            lam = C.c_void_p(self._lam.data_ptr()) if k == 2 else None
+            self.S._check(self.S.L.dg_rk_stage(self.S.ctx, k, C.c_void_p(src[k].data_ptr()),
+                                               C.c_void_p(dst[k].data_ptr()), C.c_void_p(g.data_ptr()),
+                                               C.c_void_p(dt.data_ptr()), lam, self._stream()), "dg_rk_stage")
+        dist.all_reduce(self._lam, op=dist.ReduceOp.MAX, group=self.group)
+        self.S._check(self.S.L.dg_dt_finalize(self.S.ctx, C.c_void_p(self._lam.data_ptr()), C.c_double(cfl),
+                                              C.c_void_p(dt_next.data_ptr()), self._stream()), "dg_dt_finalize")
+
+    def tau_estimate(self, q, qdot_ref=None, **kw):
+        return self.S.tau_estimate(q, qdot_ref, **kw)  # isolated levels: element-local
+
+    def select_orders(self, tau, tau_max, Nmin, Nmax, rule=1, dec_cap=1, mode=0, total_map=None):
+        """Map/select/cap on owned elements, then the jump fixpoint with halo
+        order exchanges; returns the global orders array (all ranks)."""
+        import torch
+        import torch.distributed as dist
+
+        from . import _Policy
+
+        pol = _Policy(int(mode), float(tau_max), int(Nmin), int(Nmax), int(rule), int(dec_cap))
+        E = self.lm.E
+        a = torch.empty((E, 3), dtype=torch.int32, device="cuda")
+        b = torch.empty_like(a)
+        S = self.S
+        S._check(S.L.dg_select_local(S.ctx, C.byref(pol), C.c_void_p(tau.data_ptr()),
+                                     C.c_void_p(0 if total_map is None else total_map.data_ptr()),
+                                     C.c_void_p(a.data_ptr()), None, self._stream()), "dg_select_local")
+        oplan = part.HaloPlan(self.lm, np.zeros((E, 3), np.int32), 3)  # 3 ints per element, n = 1 node
+        changed = torch.zeros(1, dtype=torch.int32, device="cuda")
+        for _ in range(64):
+            flat = a.view(-1)
+            exchange(flat, oplan, self.rank, self.group)
+            changed.zero_()
+            S._check(S.L.dg_jump_sweep(S.ctx, C.c_void_p(a.data_ptr()), C.c_void_p(b.data_ptr()), int(rule), int(Nmax),
+                                       C.c_void_p(changed.data_ptr()), self._stream()), "dg_jump_sweep")
+            a, b = b, a
+            dist.all_reduce(changed, op=dist.ReduceOp.MAX, group=self.group)
+            if int(changed.item()) == 0:
+                break
+        own = a[: self.lm.n_own].cpu().numpy()
+        out = [torch.zeros(0)] * self.world
+        gathered = [None] * self.world
+        dist.all_gather_object(gathered, (self.lm.gids[: self.lm.n_own], own), group=self.group)
+        total = sum(len(g[0]) for g in gathered)
+        res = np.zeros((total, 3), np.int32)
+        for gid, o in gathered:
+            res[gid] = o
+        del out
+        return res

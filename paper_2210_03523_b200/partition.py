@@ -1,0 +1,128 @@
+"""Element partitioning and halo plans for multi-rank runs.
+
+Host logic only (O(E) index bookkeeping, no method arithmetic).  Each rank
+holds a *local mesh*: its owned elements first (increasing global id), then
+halo copies of the other ranks' elements that share a face with an owned
+element, grouped by owning rank (increasing rank, then global id).  The
+residual of an owned element needs only its own state and its face
+neighbours' traces, so refreshing the halo states once per residual
+evaluation reproduces the single-rank result exactly (the kernels read the
+same values in the same order).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+OUTSIDE = -3  # neighbour code for faces of halo elements that leave the local set
+
+
+def slab_owner(dims, world: int, axis: int = 2) -> np.ndarray:
+    """Owner rank of every element of a lexicographic (i fastest) structured
+    mesh with dims (n0, n1, n2): contiguous slabs along `axis`, as equal as
+    possible.  axis=2 gives contiguous global-id ranges."""
+    n0, n1, n2 = dims
+    E = n0 * n1 * n2
+    idx = np.arange(E)
+    coord = [idx % n0, (idx // n0) % n1, idx // (n0 * n1)][axis]
+    n = dims[axis]
+    if world > n:
+        raise ValueError(f"cannot split {n} element layers over {world} ranks")
+    bounds = [(r * n) // world for r in range(world + 1)]
+    owner = np.empty(E, np.int32)
+    for r in range(world):
+        owner[(coord >= bounds[r]) & (coord < bounds[r + 1])] = r
+    return owner
+
+
+@dataclass
+class LocalMesh:
+    rank: int
+    world: int
+    gids: np.ndarray          # local id -> global id (owned then halo)
+    n_own: int
+    nbr: np.ndarray           # [E_loc][6] local ids, BC codes, or OUTSIDE
+    gorder: tuple
+    geo: np.ndarray
+    send: dict = field(default_factory=dict)  # rank -> local ids of owned elements to send (ordered)
+    recv: dict = field(default_factory=dict)  # rank -> local ids of halo elements to receive (ordered)
+    kind: str = "affine"
+
+    @property
+    def E(self) -> int:
+        return int(self.gids.shape[0])
+
+
+def local_mesh(mesh, owner: np.ndarray, rank: int) -> LocalMesh:
+    world = int(owner.max()) + 1
+    nbr_g = np.asarray(mesh.nbr)
+    owned = np.flatnonzero(owner == rank)
+    own_set = np.zeros(len(owner), bool)
+    own_set[owned] = True
+    nb = nbr_g[owned].ravel()
+    nb = nb[nb >= 0]
+    halo = np.unique(nb[~own_set[nb]])
+    halo = halo[np.lexsort((halo, owner[halo]))]  # by owning rank, then global id
+    gids = np.concatenate([owned, halo]).astype(np.int64)
+    g2l = -np.ones(len(owner), np.int64)
+    g2l[gids] = np.arange(len(gids))
+    loc = nbr_g[gids].astype(np.int64)
+    mapped = np.where(loc >= 0, g2l[np.maximum(loc, 0)], loc)
+    mapped = np.where((loc >= 0) & (mapped < 0), OUTSIDE, mapped)
+    lm = LocalMesh(rank=rank, world=world, gids=gids, n_own=len(owned), nbr=mapped.astype(np.int32),
+                   gorder=tuple(mesh.gorder), geo=np.ascontiguousarray(np.asarray(mesh.geo)[gids]),
+                   kind=getattr(mesh, "kind", "affine"))
+    # receive lists: halo elements grouped by owner
+    for r in range(world):
+        if r == rank:
+            continue
+        ids = np.flatnonzero(owner[gids[lm.n_own:]] == r) + lm.n_own
+        if len(ids):
+            lm.recv[r] = ids
+    # send lists: owned elements that appear in rank r's halo, increasing global id
+    for r in range(world):
+        if r == rank:
+            continue
+        r_owned = owner == r
+        # elements of mine adjacent to an element of r
+        adj = np.zeros(len(owner), bool)
+        nbr_r = nbr_g[r_owned].ravel()
+        adj[nbr_r[nbr_r >= 0]] = True
+        mine = owned[adj[owned]]
+        if len(mine):
+            lm.send[r] = g2l[mine]
+    return lm
+
+
+def element_offsets(orders: np.ndarray, ncomp: int = 5) -> np.ndarray:
+    n = np.prod(orders.astype(np.int64) + 1, axis=1)
+    off = np.zeros(len(orders) + 1, np.int64)
+    off[1:] = np.cumsum(ncomp * n)
+    return off
+
+
+def ranges(ids: np.ndarray, off: np.ndarray):
+    """Merge the state ranges of element ids (in order) into (start, stop) runs."""
+    runs = []
+    for e in ids:
+        a, b = int(off[e]), int(off[e + 1])
+        if runs and runs[-1][1] == a:
+            runs[-1][1] = b
+        else:
+            runs.append([a, b])
+    return [tuple(r) for r in runs]
+
+
+class HaloPlan:
+    """State-level exchange plan for the current local orders: per peer rank,
+    the (start, stop) ranges of the local state vector to send and to receive
+    (ncomp doubles per node: 5 for q, 15 for gradients)."""
+
+    def __init__(self, lm: LocalMesh, local_orders: np.ndarray, ncomp: int = 5):
+        off = element_offsets(local_orders, ncomp)
+        self.send = {r: ranges(ids, off) for r, ids in lm.send.items()}
+        self.recv = {r: ranges(ids, off) for r, ids in lm.recv.items()}
+        self.send_len = {r: sum(b - a for a, b in rs) for r, rs in self.send.items()}
+        self.recv_len = {r: sum(b - a for a, b in rs) for r, rs in self.recv.items()}
+        assert set(self.send) == set(self.recv), "face adjacency is symmetric"

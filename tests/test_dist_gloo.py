@@ -1,0 +1,171 @@
+"""Multi-rank host logic on CPU: world_size 2, gloo backend, real halo
+exchanges between processes (paper_2210_03523_b200.dist.exchange) over the
+slab partition (partition.py).  The per-rank compute engine here is the CPU
+oracle on the rank's local mesh (owned + halo elements); the product path
+uses the same partition / plans / exchange with NCCL and libdgtau.  Owned
+results must equal the single-rank (global) oracle results exactly."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import workloads as W
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _per_elem(arr, orders, ncomp=5):
+    off = W.offsets(orders, ncomp)
+    return [arr[off[e]:off[e + 1]] for e in range(len(orders))]
+
+
+def _worker(rank, world, port, out_q):
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2210_03523_b200 import partition as part
+    from paper_2210_03523_b200.dist import exchange
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = {}
+        mesh = W.cube_mesh(4, 3, 6)
+        g_orders = W.orders_random(mesh.E, 2, 6, 21)
+        owner = part.slab_owner(mesh.dims, world, axis=2)
+        lm = part.local_mesh(mesh, owner, rank)
+        lo = g_orders[lm.gids]
+        # global reference (every rank can compute it)
+        P = oracle.Problem(mesh)
+        X = P.node_coords(g_orders)
+        q_g = W.pulse_state(X, g_orders, center=(0.4, 0.6, 0.5), sigma=0.2)
+        r_g = P.rhs(g_orders, q_g)
+        # local state: owned part from the global field, halo zero until exchanged
+        blocks = _per_elem(q_g, g_orders)
+        q_l = np.concatenate([blocks[g] if i < lm.n_own else np.zeros_like(blocks[g]) for i, g in enumerate(lm.gids)])
+        plan = part.HaloPlan(lm, lo, 5)
+        t = torch.from_numpy(q_l)
+        exchange(t, plan, rank)
+        q_l = t.numpy()
+        want = np.concatenate([blocks[g] for g in lm.gids])
+        res["halo_exact"] = bool(np.array_equal(q_l, want))
+        # residual on the local mesh: owned part == global residual
+        Pl = oracle.Problem(lm)
+        r_l = Pl.rhs(lo, q_l)
+        rb = _per_elem(r_g, g_orders)
+        owned = np.concatenate([rb[g] for g in lm.gids[: lm.n_own]])
+        res["rhs_owned_exact"] = bool(np.array_equal(r_l[: len(owned)], owned))
+        # one RK3 step stage by stage with a halo refresh before each stage
+        A = [0.0, -5.0 / 9.0, -153.0 / 128.0]
+        B = [1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0]
+        dt = P.dt(g_orders, q_g, 0.5)
+        # distributed dt: local max rate -> MAX all-reduce (here via the oracle's dt of owned+halo)
+        lam_loc = 0.5 / Pl.dt(lo, q_l, 0.5)
+        lam = torch.tensor([lam_loc], dtype=torch.float64)
+        dist.all_reduce(lam, op=dist.ReduceOp.MAX)
+        res["dt_close"] = abs(0.5 / lam.item() - dt) <= 1e-15 * dt
+        g = np.zeros_like(q_l)
+        qs = q_l.copy()
+        for k in range(3):
+            t = torch.from_numpy(qs)
+            exchange(t, plan, rank)
+            qs = t.numpy()
+            rk = Pl.rhs(lo, qs)
+            g = A[k] * g + dt * rk
+            qs = qs + B[k] * g
+        q1 = P.rk3_step(g_orders, q_g, dt)
+        qb = _per_elem(q1, g_orders)
+        owned_q1 = np.concatenate([qb[gid] for gid in lm.gids[: lm.n_own]])
+        res["rk_owned_exact"] = bool(np.array_equal(qs[: len(owned_q1)], owned_q1))
+        # distributed jump fixpoint (Jacobi sweeps on owned + halo order exchange + MAX all-reduce)
+        rng = np.random.default_rng(5)
+        sel_g = rng.integers(1, 9, size=(mesh.E, 3)).astype(np.int32)
+        ref, _ = oracle.jump_fixpoint(mesh.nbr, sel_g, oracle.JUMP_B, 8)
+        a = sel_g[lm.gids].copy()
+        oplan = part.HaloPlan(lm, np.zeros((lm.E, 3), np.int32), 3)
+        for _ in range(64):
+            ta = torch.from_numpy(a.reshape(-1))
+            exchange(ta, oplan, rank)
+            a = ta.numpy().reshape(-1, 3)
+            b = a.copy()
+            ch = 0
+            for e in range(lm.n_own):
+                for d in range(3):
+                    v = a[e, d]
+                    for f in range(6):
+                        j = lm.nbr[e, f]
+                        if j >= 0:
+                            v = max(v, a[j, d] - 1)
+                    v = min(v, 8)
+                    if v != a[e, d]:
+                        b[e, d] = v
+                        ch = 1
+            a = b
+            c = torch.tensor([ch], dtype=torch.int32)
+            dist.all_reduce(c, op=dist.ReduceOp.MAX)
+            if c.item() == 0:
+                break
+        res["jump_exact"] = bool(np.array_equal(a[: lm.n_own], ref[lm.gids[: lm.n_own]]))
+        res["n_own"] = lm.n_own
+        res["n_halo"] = lm.E - lm.n_own
+        out_q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_two_rank_halo_rhs_rk_jump():
+    import torch.multiprocessing as mp
+
+    import oracle
+
+    oracle.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(2):
+        assert res[r]["halo_exact"], res[r]
+        assert res[r]["rhs_owned_exact"], res[r]
+        assert res[r]["dt_close"], res[r]
+        assert res[r]["rk_owned_exact"], res[r]
+        assert res[r]["jump_exact"], res[r]
+        assert res[r]["n_halo"] > 0
+
+
+def test_slab_partition_plans():
+    from paper_2210_03523_b200 import partition as part
+
+    mesh = W.cube_mesh(4, 4, 8)
+    for world in (2, 4, 8):
+        owner = part.slab_owner(mesh.dims, world)
+        assert np.bincount(owner).min() == np.bincount(owner).max()
+        lms = [part.local_mesh(mesh, owner, r) for r in range(world)]
+        for lm in lms:
+            # every owned element's neighbours are local
+            assert np.all(lm.nbr[: lm.n_own] != part.OUTSIDE)
+            # global ids of owned elements are mine
+            assert np.all(owner[lm.gids[: lm.n_own]] == lm.rank)
+            for r, ids in lm.recv.items():
+                peer = lms[r]
+                # what I receive from r is exactly what r sends to me, in order
+                assert np.array_equal(lm.gids[ids], peer.gids[peer.send[lm.rank]])
+    # O-grid: azimuthal slabs (axis 1) keep walls / far field as BCs
+    og = W.ogrid_mesh(4, 8, 2, g_eta=2)
+    owner = part.slab_owner(og.dims, 4, axis=1)
+    lm = part.local_mesh(og, owner, 1)
+    assert (lm.nbr[: lm.n_own] == W.BC_WALL).any() and (lm.nbr[: lm.n_own] == W.BC_FARFIELD).any()
