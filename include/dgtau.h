@@ -153,7 +153,18 @@ dg_status dg_rk_step_dt(dg_ctx* ctx, double* q_in_dev, double* q_out_dev, double
  * max-reduced into it (as bits of non-negative doubles, so an integer MAX
  * all-reduce across ranks is exact). */
 dg_status dg_rk_stage(dg_ctx* ctx, int stage, const double* q_in_dev, double* q_out_dev, double* g_dev,
-                      const double* dt_dev, unsigned long long* lam_accum_dev, void* stream);
+                      const double* dt_dev, unsigned long long* lam_accum_dev, int flags, void* stream);
+/* flags for dg_rk_stage / dg_rhs_eval_flags: */
+#define DG_FLAG_GRADIENT_READY 1 /* NS: skip the BR1 gradient pass; the caller ran dg_gradient
+                                    and refreshed the halo rows of dg_gradient_buffer() */
+/* NS: BR1 gradient of q (eq DGSEMsystem:2) of the owned elements
+ * into the context's gradient buffer (15 doubles per node, [k][v] = d q_v /
+ * d x_k, element e at 3 x its state offset); the buffer's device pointer is
+ * returned by dg_gradient_buffer() for halo exchange (owned by the context). */
+dg_status dg_gradient(dg_ctx* ctx, int variant, const double* q_dev, void* stream);
+double* dg_gradient_buffer(dg_ctx* ctx);
+/* dg_rhs_eval with flags (DG_FLAG_GRADIENT_READY). */
+dg_status dg_rhs_eval_flags(dg_ctx* ctx, int variant, const double* q_dev, double* qdot_dev, int flags, void* stream);
 /* Max-reduce the CFL/DFL rates of q (owned elements) into lam_accum_dev. */
 dg_status dg_dt_accumulate(dg_ctx* ctx, const double* q_dev, unsigned long long* lam_accum_dev, void* stream);
 /* dt_dev[0] = min(cfl / lam, cfl / nu) from lam_accum_dev; resets it to 0. */

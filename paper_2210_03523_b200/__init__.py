@@ -37,7 +37,8 @@ NMAX = 8
 EXPORTS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_upload", "dg_set_orders", "dg_state_len", "dg_ndof",
            "dg_node_coords", "dg_rhs_eval", "dg_compute_dt", "dg_rk_step", "dg_tau_estimate", "dg_select_orders",
            "dg_transfer", "dg_diagnostics", "dg_launch_count", "dg_rk_step_dt", "dg_set_owned", "dg_rk_stage",
-           "dg_dt_accumulate", "dg_dt_finalize", "dg_select_local", "dg_jump_sweep", "dg_owned_state_len"]
+           "dg_dt_accumulate", "dg_dt_finalize", "dg_select_local", "dg_jump_sweep", "dg_owned_state_len", "dg_gradient",
+           "dg_gradient_buffer", "dg_rhs_eval_flags"]
 
 
 def sources():
@@ -126,10 +127,21 @@ def lib():
         L.dg_ndof.restype = C.c_int64
         L.dg_launch_count.restype = C.c_int64
         L.dg_owned_state_len.restype = C.c_int64
+        L.dg_gradient_buffer.restype = C.c_void_p
         for name in EXPORTS:
             getattr(L, name)
         _lib = L
     return _lib
+
+
+def _device_view(ptr, n):
+    """Borrowed fp64 CUDA tensor over context-owned memory (lifetime: the context)."""
+    import torch
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 2}
+
+    return torch.as_tensor(_Arr(), device="cuda")
 
 
 def _ptr(t):
@@ -249,9 +261,22 @@ class Solver:
     def owned_len(self):
         return int(self.L.dg_owned_state_len(self.ctx))
 
-    def rk_stage(self, k, q_in, q_out, g, dt, lam=None, stream=None):
+    def rk_stage(self, k, q_in, q_out, g, dt, lam=None, flags=0, stream=None):
         self._check(self.L.dg_rk_stage(self.ctx, int(k), _ptr(q_in), _ptr(q_out), _ptr(g), _ptr(dt), _ptr(lam),
-                                       _stream(stream)), "dg_rk_stage")
+                                       int(flags), _stream(stream)), "dg_rk_stage")
+
+    def gradient(self, q, variant=NONISOLATED, stream=None):
+        self._check(self.L.dg_gradient(self.ctx, int(variant), _ptr(q), _stream(stream)), "dg_gradient")
+
+    def gradient_buffer(self):
+        """torch view of the context's gradient buffer (15 doubles per node)."""
+        import torch
+
+        n = 3 * self.state_len
+        ptr = self.L.dg_gradient_buffer(self.ctx)
+        if not ptr:
+            raise DGError("no gradient buffer (NS on the curved path only)")
+        return _device_view(ptr, n)
 
     def dt_accumulate(self, q, lam, stream=None):
         self._check(self.L.dg_dt_accumulate(self.ctx, _ptr(q), _ptr(lam), _stream(stream)), "dg_dt_accumulate")

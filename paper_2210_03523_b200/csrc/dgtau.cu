@@ -564,7 +564,7 @@ dg_status dg_node_coords(dg_ctx* ctx, double* X)
 
 static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* q, double* out, double* g,
                                         const double* dt, double A, double B, int mode, cudaStream_t st,
-                                        unsigned long long* lam_max)
+                                        unsigned long long* lam_max, int flags = 0)
 {
     const bool ns = ctx->prm.physics == DG_NS;
     CurvedParams P{};
@@ -594,7 +594,7 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
     M.tab = ctx->d_tab;
     M.ph = phys_dev(ctx->prm);
     const bool mort = variant == DG_NONISOLATED && ctx->nmortar > 0;
-    if (ns) {  // BR1 gradient pass (eq DGSEMsystem:2)
+    if (ns && !(flags & 1)) {  // BR1 gradient pass (eq DGSEMsystem:2); flag 1: caller already did it
         if (mort) {
             M.mode = 1;
             M.mortarG = ctx->d_mortarGq;
@@ -623,9 +623,10 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
 }
 
 static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, double* out, double* g, const double* dt,
-                                 double A, double B, int mode, cudaStream_t st, unsigned long long* lam_max = nullptr)
+                                 double A, double B, int mode, cudaStream_t st, unsigned long long* lam_max = nullptr,
+                                 int flags = 0)
 {
-    if (ctx->curved) return launch_residual_curved(ctx, variant, q, out, g, dt, A, B, mode, st, lam_max);
+    if (ctx->curved) return launch_residual_curved(ctx, variant, q, out, g, dt, A, B, mode, st, lam_max, flags);
     if (variant == DG_NONISOLATED && ctx->nmortar > 0) {
         MortarParams M;
         M.q = q;
@@ -787,7 +788,7 @@ dg_status dg_set_owned(dg_ctx* ctx, int n_owned)
 }
 
 dg_status dg_rk_stage(dg_ctx* ctx, int stage, const double* q_in, double* q_out, double* g, const double* dt_dev,
-                      unsigned long long* lam_accum_dev, void* stream)
+                      unsigned long long* lam_accum_dev, int flags, void* stream)
 {
     if (!ctx || !q_in || !q_out || !g || !dt_dev || q_in == q_out || stage < 0 || stage > 2) return DG_EINVAL;
     if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "rk_stage: orders not set");
@@ -795,7 +796,59 @@ dg_status dg_rk_stage(dg_ctx* ctx, int stage, const double* q_in, double* q_out,
     static const double A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
     static const double B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
     return launch_residual(ctx, DG_NONISOLATED, q_in, q_out, g, dt_dev, A[stage], B[stage], 1, (cudaStream_t)stream,
-                           lam_accum_dev);
+                           lam_accum_dev, flags);
+}
+
+dg_status dg_gradient(dg_ctx* ctx, int variant, const double* q_dev, void* stream)
+{
+    if (!ctx || !q_dev) return DG_EINVAL;
+    if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "gradient: orders not set");
+    if (ctx->prm.physics != DG_NS || !ctx->curved) return fail(ctx, DG_EUNSUPPORTED, "gradient: NS on the curved path only");
+    cudaStream_t st = (cudaStream_t)stream;
+    CurvedParams P{};
+    P.q = q_dev;
+    P.variant = variant;
+    P.orders = ctx->d_orders;
+    P.off = ctx->d_off;
+    P.finfo = ctx->d_finfo;
+    P.met = ctx->d_met;
+    P.grad = ctx->d_grad;
+    P.tab = ctx->d_tab;
+    P.ph = phys_dev(ctx->prm);
+    P.flag = ctx->d_flag;
+    if (variant == DG_NONISOLATED && ctx->nmortar > 0) {
+        CMortarParams M{};
+        M.tdd = ctx->d_tdd;
+        M.q = q_dev;
+        M.grad = ctx->d_grad;
+        M.orders = ctx->d_orders;
+        M.off = ctx->d_off;
+        M.items = ctx->d_mortar;
+        M.moff = ctx->d_moff;
+        M.cm = curved_mesh(ctx);
+        M.tab = ctx->d_tab;
+        M.ph = phys_dev(ctx->prm);
+        M.mode = 1;
+        M.mortarG = ctx->d_mortarGq;
+        k_mortar_curved<<<ctx->nmortar, 128, 0, st>>>(M);
+        ctx->launches++;
+    }
+    P.mode = 0;
+    P.out = ctx->d_grad;
+    P.mortarG = ctx->d_mortarGq;
+    k_grad<<<ctx->n_own, CBS, sizeof(double) * 25 * (size_t)ctx->maxn, st>>>(P);
+    ctx->launches++;
+    return check_stream_error(ctx, "k_grad launch");
+}
+
+double* dg_gradient_buffer(dg_ctx* ctx) { return ctx ? ctx->d_grad : nullptr; }
+
+dg_status dg_rhs_eval_flags(dg_ctx* ctx, int variant, const double* q_dev, double* qdot_dev, int flags, void* stream)
+{
+    if (!ctx || !q_dev || !qdot_dev) return DG_EINVAL;
+    if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "rhs_eval: orders not set");
+    return launch_residual(ctx, variant, q_dev, qdot_dev, nullptr, nullptr, 0.0, 0.0, 0, (cudaStream_t)stream, nullptr,
+                           flags);
 }
 
 dg_status dg_dt_finalize(dg_ctx* ctx, unsigned long long* lam_accum_dev, double cfl, double* dt_dev, void* stream)
