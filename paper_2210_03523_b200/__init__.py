@@ -32,6 +32,7 @@ REF_SOLVER, REF_SAME = 0, 1
 JUMP_A, JUMP_B = 0, 1
 SELECT_DYNAMIC, SELECT_STATIC_ACCUM, SELECT_STATIC_FINAL = 0, 1, 2
 TAU_STRIDE = 9
+FLAG_GRADIENT_READY = 1
 NMAX = 8
 
 EXPORTS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_upload", "dg_set_orders", "dg_state_len", "dg_ndof",

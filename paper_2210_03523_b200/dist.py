@@ -57,6 +57,7 @@ class DistSolver:
 
         self.rank, self.world, self.group = rank, world, group
         self.lm = part.local_mesh(global_mesh, owner, rank)
+        self.physics = solver_kw.get("physics", 0)
         self.S = Solver(self.lm, **solver_kw)
         self.S._check(self.S.L.dg_set_owned(self.S.ctx, int(self.lm.n_own)), "dg_set_owned")
         self.plan = None
@@ -87,10 +88,27 @@ class DistSolver:
         exchange(q, self.plan, self.rank, self.group)
 
     # -- operators -----------------------------------------------------------
+    def _gradient_halo(self, q, variant=0):
+        """NS: BR1 gradients of the owned elements, then their halo refresh
+        (the viscous face flux needs the neighbour's gradient trace)."""
+        from . import FLAG_GRADIENT_READY, NS
+
+        if self.physics != NS:
+            return 0
+        self.S.gradient(q, variant)
+        if variant == 0:
+            exchange(self.S.gradient_buffer(), self.gplan, self.rank, self.group)
+        return FLAG_GRADIENT_READY
+
     def rhs_eval(self, q, qdot=None, variant=0):
         if variant == 0:
             self.halo(q)
-        return self.S.rhs_eval(q, qdot, variant=variant)
+        flags = self._gradient_halo(q, variant)
+        qdot = self.S.new_state() if qdot is None else qdot
+        self.S._check(self.S.L.dg_rhs_eval_flags(self.S.ctx, int(variant), C.c_void_p(q.data_ptr()),
+                                                 C.c_void_p(qdot.data_ptr()), int(flags), self._stream()),
+                      "dg_rhs_eval_flags")
+        return qdot
 
     def compute_dt(self, q, cfl, dt):
         import torch.distributed as dist
@@ -117,10 +135,8 @@ class DistSolver:
         self._lam.zero_()
         for k in range(3):
             self.halo(src[k])
-            lam = C.c_void_p(self._lam.data_ptr()) if k == 2 else None
-            self.S._check(self.S.L.dg_rk_stage(self.S.ctx, k, C.c_void_p(src[k].data_ptr()),
-                                               C.c_void_p(dst[k].data_ptr()), C.c_void_p(g.data_ptr()),
-                                               C.c_void_p(dt.data_ptr()), lam, self._stream()), "dg_rk_stage")
+            flags = self._gradient_halo(src[k])
+            self.S.rk_stage(k, src[k], dst[k], g, dt, self._lam if k == 2 else None, flags)
         dist.all_reduce(self._lam, op=dist.ReduceOp.MAX, group=self.group)
         self.S._check(self.S.L.dg_dt_finalize(self.S.ctx, C.c_void_p(self._lam.data_ptr()), C.c_double(cfl),
                                               C.c_void_p(dt_next.data_ptr()), self._stream()), "dg_dt_finalize")

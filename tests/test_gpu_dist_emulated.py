@@ -69,7 +69,7 @@ def test_two_rank_emulated(dg, orc, case):
         qa0, qb0 = qb0, qa0
     # two local meshes
     lms = [part.local_mesh(mesh, owner, r) for r in range(2)]
-    solvers, plans, qa, qb, gg = [], [], [], [], []
+    solvers, plans, gplans, qa, qb, gg = [], [], [], [], [], []
     blocks = [q_g[a:b] for a, b in zip(W.offsets(g_orders)[:-1], W.offsets(g_orders)[1:])]
     for lm in lms:
         S = dg.Solver(lm, **kw)
@@ -78,6 +78,7 @@ def test_two_rank_emulated(dg, orc, case):
         S.set_orders(lo)
         solvers.append(S)
         plans.append(part.HaloPlan(lm, lo, 5))
+        gplans.append(part.HaloPlan(lm, lo, 15))
         x = torch.from_numpy(np.concatenate([blocks[g] for g in lm.gids])).cuda()
         qa.append(x)
         qb.append(torch.empty_like(x))
@@ -97,8 +98,14 @@ def test_two_rank_emulated(dg, orc, case):
             lam[r].zero_()
         for k in range(3):
             _copy_halos(solvers, plans, src[k])
+            flags = 0
+            if case == "ogrid_ns":  # BR1: gradient pass, gradient halo refresh, then the flux pass
+                for r in range(2):
+                    solvers[r].gradient(src[k][r])
+                _copy_halos(solvers, gplans, [S.gradient_buffer() for S in solvers])
+                flags = dg.FLAG_GRADIENT_READY
             for r in range(2):
-                solvers[r].rk_stage(k, src[k][r], dst[k][r], gg[r], dts[s % 2], lam[r] if k == 2 else None)
+                solvers[r].rk_stage(k, src[k][r], dst[k][r], gg[r], dts[s % 2], lam[r] if k == 2 else None, flags)
         lmax = torch.maximum(lam[0], lam[1])
         solvers[0].dt_finalize(lmax, 0.5, dts[(s + 1) % 2])
         qa, qb = qb, qa
