@@ -183,19 +183,27 @@ def run_gpu(args, rank, world):
         if timers:
             e1.record(stream)
             timers["tau"].append((e0, e1))
+        if timers:
+            e2 = ev()
+            e2.record(stream)
         sel = select(tau)
         qn = core.transfer(local(sel), qa)
+        if timers:
+            e3 = ev()
+            e3.record(stream)
+            timers["adapt"].append((e2, e3))
         return sel, qn
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     # timed region
-    timers = {"rk": [], "tau": []}
+    timers = {"rk": [], "tau": [], "adapt": []}
     launches0 = core.launches
     clocks = ClockSampler(dev.index)
     if rank == 0:
         clocks.start()
+        time.sleep(0.5)  # let nvidia-smi start streaming before the timed region (NVML init stalls)
     if world > 1:
         import torch.distributed as dist
 
@@ -214,6 +222,7 @@ def run_gpu(args, rank, world):
     total_ms = start.elapsed_time(end)
     rk_ms = sum(a.elapsed_time(b) for a, b in timers["rk"])
     tau_ms = sum(a.elapsed_time(b) for a, b in timers["tau"])
+    adapt_ms = sum(a.elapsed_time(b) for a, b in timers["adapt"])
     if world > 1:
         t = torch.tensor([total_ms, rk_ms, tau_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -251,7 +260,7 @@ def run_gpu(args, rank, world):
         e2e = {"value": world * ndof * evals_per_step * args.steps / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s",
                "h2d_bytes_per_step": int(owned_len * 8), "d2h_bytes_per_step": int(d2h // args.steps)}
 
-    return dict(value=value, total_ms=total_ms, rk_ms=rk_ms, tau_ms=tau_ms, ndof=ndof, E=n_elem,
+    return dict(value=value, total_ms=total_ms, rk_ms=rk_ms, tau_ms=tau_ms, adapt_ms=adapt_ms, ndof=ndof, E=n_elem,
                 achieved=achieved, peak=peak, peak_kind=peak_kind, tau_elems=tau_elems, clocks=clk,
                 launches=launches, e2e=e2e, rk_count=rk_count, bytes_rk_step=bytes_rk_step)
 
@@ -362,6 +371,8 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_block(world),
         "tau_elems_per_s": res["tau_elems"] * world,
+        "phase_ms_per_step": {"rk3_x50": res["rk_ms"] / args.steps, "ref_rhs_plus_tau": res["tau_ms"] / args.steps,
+                              "select_plus_transfer": res["adapt_ms"] / args.steps},
         "rhs_rk_gdof_s": world * res["ndof"] * 3 * res["rk_count"] / (res["rk_ms"] * 1e-3) / 1e9,
         "roofline": {"kernel": "k_residual (fused residual + RK stage)", "bound": "hbm", "achieved": res["achieved"],
                      "peak": res["peak"], "unit": "GB/s", "frac": res["achieved"] / res["peak"],

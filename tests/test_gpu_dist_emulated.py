@@ -145,3 +145,45 @@ def test_two_rank_emulated(dg, orc, case):
             break
     for r, lm in enumerate(lms):
         assert np.array_equal(a[r][: lm.n_own].cpu().numpy(), sel0[lm.gids[: lm.n_own]])
+
+
+def test_distsolver_single_rank_matches_solver(dg, orc):
+    """DistSolver composition (exchange calls, all-reduces, distributed
+    selection) on a 1-rank gloo group: identical to the plain Solver."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2210_03523_b200 import partition as part
+    from paper_2210_03523_b200.dist import DistSolver
+
+    if not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    mesh = W.cube_mesh(4, 4, 4)
+    orders = W.orders_random(mesh.E, 2, 6, 41)
+    P = orc.Problem(mesh)
+    q = torch.from_numpy(W.pulse_state(P.node_coords(orders), orders, sigma=0.2)).cuda()
+    S = dg.Solver(mesh)
+    S.set_orders(orders)
+    D = DistSolver(mesh, part.slab_owner(mesh.dims, 1), 0, 1)
+    D.set_orders(orders)
+    r1 = S.rhs_eval(q)
+    r2 = D.rhs_eval(q.clone())
+    assert torch.equal(r1, r2)
+    dt1 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    dt2 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    S.compute_dt(q, 0.5, dt1)
+    D.compute_dt(q, 0.5, dt2)
+    assert torch.equal(dt1, dt2)
+    tau = S.tau_estimate(q, r1)
+    sel1, _ = S.select_orders(tau, 1e-4, 2, 8)
+    sel2 = D.select_orders(tau, 1e-4, 2, 8)
+    assert np.array_equal(sel1, sel2)
