@@ -145,6 +145,79 @@ __device__ __forceinline__ void face_of(int r, int& f, int& pt)
     }
 }
 
+// Roe flux (no entropy fix, reading A7) for the axis normal e_d, with
+// 1/rho and p of both states precomputed (same algebra as roe_flux with n = e_d).
+template <int d>
+__device__ __forceinline__ void roe_axis(const double* qL, double irL, double pL, const double* qR, double irR,
+                                         double pR, double gamma, double* F)
+{
+    const double gm1 = gamma - 1.0;
+    double uL[3], uR[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { uL[k] = qL[1 + k] * irL; uR[k] = qR[1 + k] * irR; }
+    const double HL = (qL[4] + pL) * irL, HR = (qR[4] + pR) * irR;
+    const double sL = sqrt(qL[0]), sR = sqrt(qR[0]);
+    const double is = 1.0 / (sL + sR);
+    const double wl = sL * is, wr = sR * is;
+    double u[3], du[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) { u[k] = wl * uL[k] + wr * uR[k]; du[k] = uR[k] - uL[k]; }
+    const double H = wl * HL + wr * HR;
+    const double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
+    const double c2 = gm1 * (H - 0.5 * uu);
+    const double c = sqrt(c2);
+    const double ic2 = 1.0 / c2;
+    const double un = u[d], dun = du[d];
+    const double rho = sL * sR;
+    const double dp = pR - pL;
+    const double rcd = rho * c * dun;
+    const double a1 = 0.5 * (dp - rcd) * ic2, a5 = 0.5 * (dp + rcd) * ic2;
+    const double a2 = (qR[0] - qL[0]) - dp * ic2;
+    const double w1 = fabs(un - c) * a1, w5 = fabs(un + c) * a5, l2 = fabs(un);
+    const double mL = qL[1 + d], mR = qR[1 + d];
+    F[0] = 0.5 * (mL + mR) - 0.5 * (w1 + l2 * a2 + w5);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        double fk = qL[1 + k] * uL[d] + qR[1 + k] * uR[d];
+        double dk = (w1 + w5) * u[k] + l2 * (a2 * u[k] + rho * du[k]);
+        if (k == d) {
+            fk += pL + pR;
+            dk += c * (w5 - w1) - l2 * rho * dun;
+        }
+        F[1 + k] = 0.5 * fk - 0.5 * dk;
+    }
+    const double udu = u[0] * du[0] + u[1] * du[1] + u[2] * du[2];
+    const double fe = (qL[4] + pL) * uL[d] + (qR[4] + pR) * uR[d];
+    const double de = (w1 + w5) * H + un * c * (w5 - w1) + l2 * (a2 * 0.5 * uu + rho * (udu - un * dun));
+    F[4] = 0.5 * fe - 0.5 * de;
+}
+
+// surface term of one face point for the compile-time axis d: G - f_own
+template <int d>
+__device__ __forceinline__ void face_point(const double* qo, double iro, double po, double* qx, int kind, int s,
+                                           const PhysDev& ph, double* out)
+{
+    double fo[NV], G[NV];
+    flux_axis<d>(qo, iro, po, fo);
+    if (kind == 1) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) G[v] = qx[v];
+    } else {
+        if (kind >= 2) ghost_state(qo, kind == 2 ? -1 : -2, ph, qx);
+        if (ph.flux == 1) {
+            double nrm[3] = {d == 0 ? 1.0 : 0.0, d == 1 ? 1.0 : 0.0, d == 2 ? 1.0 : 0.0};
+            if (s) llf_flux(qo, qx, nrm, ph.gamma, G); else llf_flux(qx, qo, nrm, ph.gamma, G);
+        } else {
+            const double irx = 1.0 / qx[0];
+            const double px = ph.gm1 * (qx[4] - 0.5 * irx * (qx[1] * qx[1] + qx[2] * qx[2] + qx[3] * qx[3]));
+            if (s) roe_axis<d>(qo, iro, po, qx, irx, px, ph.gamma, G);
+            else roe_axis<d>(qx, irx, px, qo, iro, po, ph.gamma, G);
+        }
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) out[v] = G[v] - fo[v];
+}
+
 template <int N1, int N2, int N3>
 __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB) k_res_t(ResParams P, int item0)
 {
@@ -307,27 +380,20 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
             else if (d == 1) { i = ta; j = s ? N2 : 0; k = tb; Nd = N2; }
             else { i = ta; j = tb; k = s ? N3 : 0; Nd = N3; }
             const int node = i + n1 * (j + n2 * k);
-            double qo[NV], fo[NV], G[NV], qx[NV];
+            double qo[NV], qx[NV], out[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
                 qo[v] = Q[(slot * NV + v) * n + node];
                 qx[v] = X[(slot * NV + v) * FS + r];
             }
-            const double nx = d == 0 ? 1.0 : 0.0, ny = d == 1 ? 1.0 : 0.0, nz = d == 2 ? 1.0 : 0.0;
-            flux_normal(qo, nx, ny, nz, gm1, fo);
-            const double nrm[3] = {nx, ny, nz};
+            const double iro = IR[slot * n + node], po = PR[slot * n + node];
             const int kind = P.finfo[6 * s_e[slot] + f].kind;
-            if (kind == 1) {
-#pragma unroll
-                for (int v = 0; v < NV; ++v) G[v] = qx[v];
-            } else {
-                if (kind >= 2) ghost_state(qo, kind == 2 ? -1 : -2, P.ph, qx);
-                if (s) riemann(qo, qx, nrm, P.ph, G);
-                else riemann(qx, qo, nrm, P.ph, G);
-            }
+            if (d == 0) face_point<0>(qo, iro, po, qx, kind, s, P.ph, out);
+            else if (d == 1) face_point<1>(qo, iro, po, qx, kind, s, P.ph, out);
+            else face_point<2>(qo, iro, po, qx, kind, s, P.ph, out);
             const double sc = (s ? 1.0 : -1.0) * s_sc[slot][d] / c_w[Nd][0];
 #pragma unroll
-            for (int v = 0; v < NV; ++v) X[(slot * NV + v) * FS + r] = sc * (G[v] - fo[v]);
+            for (int v = 0; v < NV; ++v) X[(slot * NV + v) * FS + r] = sc * out[v];
         }
         __syncthreads();
     }
