@@ -42,15 +42,18 @@ template <int N1, int N2, int N3>
 struct Shape {
     static constexpr int n1 = N1 + 1, n2 = N2 + 1, n3 = N3 + 1;
     static constexpr int n = n1 * n2 * n3;
-    static constexpr int CNT = cmax(1, cmin(MAXSLOTS, 512 / n));
+    // <= ~384 nodes per CTA so nodes, (line, variable) tasks and face tasks
+    // each take one round of threads (no half-empty second rounds before the
+    // barriers); two node passes only for n > 384.
+    static constexpr int CNT = cmax(1, cmin(MAXSLOTS, 384 / n));
     static constexpr int T = CNT * n;
-    static constexpr int NPT = (T + 255) / 256;
+    static constexpr int NPT = T > 384 ? 2 : 1;
     static constexpr int BS = ((T + NPT - 1) / NPT + 31) / 32 * 32;
     static constexpr int nf0 = n2 * n3, nf1 = n1 * n3, nf2 = n1 * n2;
     static constexpr int FS = 2 * (nf0 + nf1 + nf2);
     // Q (5T) + F (5T) + RK register g (5T) + IR,P (2T) + outer traces / lifting terms (5 FS per element)
     static constexpr size_t smem_bytes = sizeof(double) * (size_t)(17 * T + NV * CNT * FS);
-    static constexpr int MINB = BS <= 128 ? 4 : (BS <= 192 ? 3 : 2);
+    static constexpr int MINB = BS <= 128 ? 4 : (BS <= 192 ? 3 : (BS <= 384 ? 2 : 1));
 };
 
 // f . e_d for the Euler flux, from q with precomputed 1/rho and p
