@@ -221,6 +221,7 @@ struct ResParams {
     const long long* moff;  // [E][6] offset into mortarG or -1
     const FaceInfo* finfo;  // [E][6]
     const SlotInfo* slots;  // [elist length], parallel to elist
+    const FaceInfo* finfo_slot;  // [elist length][6]: finfo of elist[i] (one dependent load less)
     const Tables* tab;
     PhysDev ph;
     int* flag;              // [0] admissibility violations, [1] element id

@@ -25,18 +25,19 @@
 using namespace dgtau;
 
 namespace dgtau {
-cudaError_t res_setup_1(const Tables*, res_launcher (*)[NP][NP]);
-cudaError_t res_setup_2(const Tables*, res_launcher (*)[NP][NP]);
-cudaError_t res_setup_3(const Tables*, res_launcher (*)[NP][NP]);
-cudaError_t res_setup_4(const Tables*, res_launcher (*)[NP][NP]);
-cudaError_t res_setup_5(const Tables*, res_launcher (*)[NP][NP]);
-cudaError_t res_setup_6(const Tables*, res_launcher (*)[NP][NP]);
-cudaError_t res_setup_7(const Tables*, res_launcher (*)[NP][NP]);
-cudaError_t res_setup_8(const Tables*, res_launcher (*)[NP][NP]);
+cudaError_t res_setup_1(const Tables*, res_launcher (*)[NP][NP], res_occupancy (*)[NP][NP]);
+cudaError_t res_setup_2(const Tables*, res_launcher (*)[NP][NP], res_occupancy (*)[NP][NP]);
+cudaError_t res_setup_3(const Tables*, res_launcher (*)[NP][NP], res_occupancy (*)[NP][NP]);
+cudaError_t res_setup_4(const Tables*, res_launcher (*)[NP][NP], res_occupancy (*)[NP][NP]);
+cudaError_t res_setup_5(const Tables*, res_launcher (*)[NP][NP], res_occupancy (*)[NP][NP]);
+cudaError_t res_setup_6(const Tables*, res_launcher (*)[NP][NP], res_occupancy (*)[NP][NP]);
+cudaError_t res_setup_7(const Tables*, res_launcher (*)[NP][NP], res_occupancy (*)[NP][NP]);
+cudaError_t res_setup_8(const Tables*, res_launcher (*)[NP][NP], res_occupancy (*)[NP][NP]);
 }  // namespace dgtau
 
 struct Bucket {
     int ord, item0, nitems;
+    int start0, nelem, grid;  // elist start, element count, persistent grid size
 };
 
 struct dg_ctx {
@@ -99,6 +100,9 @@ struct dg_ctx {
     long long launches = 0;
     std::vector<Bucket> buckets;
     res_launcher rtab[NP][NP][NP] = {};
+    res_occupancy rocc[NP][NP][NP] = {};
+    int nsm = 148;
+    FaceInfo* d_finfo_slot = nullptr;
     bool generic = false;  // DGTAU_GENERIC=1: runtime-order residual kernel (A/B testing)
 };
 
@@ -209,6 +213,7 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
     dg_ctx* ctx = new dg_ctx;
     ctx->prm = *params;
     cudaGetDevice(&ctx->device);
+    cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, ctx->device);
     const Tables& t = host_tables();
     dg_status s;
     if ((s = cuda_check(ctx, cudaMalloc(&ctx->d_tab, sizeof(Tables)), "cudaMalloc tables")) != DG_OK ||
@@ -225,11 +230,11 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         return s;
     }
     {
-        typedef cudaError_t (*setup_fn)(const Tables*, res_launcher (*)[NP][NP]);
+        typedef cudaError_t (*setup_fn)(const Tables*, res_launcher (*)[NP][NP], res_occupancy (*)[NP][NP]);
         const setup_fn fns[8] = {res_setup_1, res_setup_2, res_setup_3, res_setup_4,
                                  res_setup_5, res_setup_6, res_setup_7, res_setup_8};
         for (int i = 0; i < 8; ++i)
-            if ((s = cuda_check(ctx, fns[i](&t, ctx->rtab), "residual setup")) != DG_OK) {
+            if ((s = cuda_check(ctx, fns[i](&t, ctx->rtab, ctx->rocc), "residual setup")) != DG_OK) {
                 dg_destroy(ctx);
                 return s;
             }
@@ -282,6 +287,7 @@ void dg_destroy(dg_ctx* ctx)
     dfree(ctx->d_mortar);
     dfree(ctx->d_moff);
     dfree(ctx->d_finfo);
+    dfree(ctx->d_finfo_slot);
     dfree(ctx->d_slots);
     dfree(ctx->d_levels);
     dfree(ctx->d_ref_scratch);
@@ -404,8 +410,9 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     ctx->buckets.clear();
     for (size_t i = 0; i < work.size(); ++i) {
         if (ctx->buckets.empty() || ctx->buckets.back().ord != work[i].ord)
-            ctx->buckets.push_back(Bucket{work[i].ord, (int)i, 0});
+            ctx->buckets.push_back(Bucket{work[i].ord, (int)i, 0, work[i].start, 0, 0});
         ctx->buckets.back().nitems++;
+        ctx->buckets.back().nelem += work[i].count;
     }
     ctx->nwork = (int)work.size();
     ctx->res_smem = smem;
@@ -467,6 +474,14 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
         for (int dd = 0; dd < 3; ++dd) slots[i].sc[dd] = 2.0 / ctx->h[3LL * e + dd];
     }
     CK(upload(ctx->d_slots, slots));
+    std::vector<FaceInfo> fslot(6 * elist.size());
+    for (size_t i = 0; i < elist.size(); ++i)
+        for (int f = 0; f < 6; ++f) fslot[6 * i + f] = finfo[6LL * elist[i] + f];
+    CK(upload(ctx->d_finfo_slot, fslot));
+    for (Bucket& b : ctx->buckets) {
+        const int occ = ctx->rocc[b.ord & 255][(b.ord >> 8) & 255][(b.ord >> 16) & 255]();
+        b.grid = std::max(1, occ) * ctx->nsm;
+    }
     // tau-estimation levels (e, d, p < N_d), largest first for load balance
     std::vector<TauLevel> lv;
     ctx->max_level = 0;
@@ -659,6 +674,7 @@ static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, doub
     P.moff = ctx->d_moff;
     P.finfo = ctx->d_finfo;
     P.slots = ctx->d_slots;
+    P.finfo_slot = ctx->d_finfo_slot;
     P.tab = ctx->d_tab;
     P.ph = phys_dev(ctx->prm);
     P.flag = ctx->d_flag;
@@ -670,7 +686,7 @@ static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, doub
         ctx->launches++;
     } else {
         for (const Bucket& b : ctx->buckets) {
-            ctx->rtab[b.ord & 255][(b.ord >> 8) & 255][(b.ord >> 16) & 255](P, b.item0, b.nitems, st);
+            ctx->rtab[b.ord & 255][(b.ord >> 8) & 255][(b.ord >> 16) & 255](P, b.start0, b.nelem, b.nitems, b.grid, st);
             ctx->launches++;
         }
     }

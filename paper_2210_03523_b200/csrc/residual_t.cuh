@@ -51,8 +51,10 @@ struct Shape {
     static constexpr int BS = ((T + NPT - 1) / NPT + 31) / 32 * 32;
     static constexpr int nf0 = n2 * n3, nf1 = n1 * n3, nf2 = n1 * n2;
     static constexpr int FS = 2 * (nf0 + nf1 + nf2);
-    // Q (5T) + F (5T) + RK register g (5T) + IR,P (2T) + outer traces / lifting terms (5 FS per element)
-    static constexpr size_t smem_bytes = sizeof(double) * (size_t)(17 * T + NV * CNT * FS);
+    // F (5T) + IR,P (2T) + 2 pipeline stages x {Q (5T), g (5T), outer traces (5 FS per element)}
+    // + 3 meta buffers (slot info + face descriptors)
+    static constexpr size_t smem_bytes =
+        sizeof(double) * (size_t)(7 * T + 2 * (10 * T + NV * CNT * FS) + 3 * CNT * (5 + 24));
     static constexpr int MINB = BS <= 128 ? 4 : (BS <= 192 ? 3 : (BS <= 384 ? 2 : 1));
 };
 
@@ -221,252 +223,282 @@ __device__ __forceinline__ void face_point(const double* qo, double iro, double 
     for (int v = 0; v < NV; ++v) out[v] = G[v] - fo[v];
 }
 
+// Per-item metadata staged in shared memory: slot info (5 doubles) and the 6
+// face descriptors (4 doubles each) of every element of the item.
+constexpr int META_SLOT_W = 5, META_FACE_W = 4;
+
 template <int N1, int N2, int N3>
-__global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB) k_res_t(ResParams P, int item0)
+__global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB)
+    k_res_t(ResParams P, int start0, int nelem, int nitems)
 {
     using S = Shape<N1, N2, N3>;
     constexpr int n = S::n, n1 = S::n1, n2 = S::n2, n3 = S::n3, BS = S::BS, NPTT = S::NPT, FS = S::FS;
-    constexpr int T = S::T;
+    constexpr int T = S::T, CNT = S::CNT;
+    constexpr int MW = CNT * (META_SLOT_W + 6 * META_FACE_W);  // meta words per item
     extern __shared__ double sm[];
-    double* Q = sm;               // [slot][v][node]  state
-    double* F = Q + NV * T;       // [slot][v][node]  flux of one direction, then its derivative
-    double* IR = F + NV * T;      // [slot*n + node]  1/rho
-    double* PR = IR + T;          // [slot*n + node]  pressure
-    double* GB = PR + T;          // [slot][v][node]  RK register g (prefetched)
-    double* X = GB + NV * T;      // [slot][v][face point]  outer traces, then lifting terms
-    __shared__ long long s_off[S::CNT];
-    __shared__ int s_e[S::CNT];
-    __shared__ double s_sc[S::CNT][3];
+    double* F = sm;                   // [slot][v][node]  flux of one direction, then its derivative
+    double* IR = F + NV * T;          // 1/rho
+    double* PR = IR + T;              // pressure
+    double* STG = PR + T;             // 2 pipeline stages of {Q 5T, GB 5T, X 5 CNT FS}
+    constexpr int STAGE = 10 * T + NV * CNT * FS;
+    double* META = STG + 2 * STAGE;   // 3 meta buffers of MW words
+    __shared__ double red[32];
 
-    const WorkItem w = P.work[item0 + blockIdx.x];
-    const int cnt = w.count;
     const int tid = threadIdx.x;
-    if (tid < cnt) {
-        const SlotInfo si = P.slots[w.start + tid];
-        s_e[tid] = si.e;
-        s_off[tid] = si.off;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) s_sc[tid][d] = si.sc[d];
-    }
-    __syncthreads();
-    const double gm1 = P.ph.gm1;
-    const int ntot = cnt * n;
     const bool surf = P.variant == 0;
-
-    // ---- outer traces / mortar fluxes: asynchronous gather into X ---------
-    if (surf) {
-        for (int t = tid; t < cnt * FS; t += BS) {
-            const int slot = t / FS;
-            const int r = t - slot * FS;
-            int f, pt;
-            face_of<S>(r, f, pt);
-            const FaceInfo fi = P.finfo[6 * s_e[slot] + f];
-            const int nta = f < 2 ? n2 : n1;
-            const int ta = pt % nta, tb = pt / nta;
-            if (fi.kind == 0) {
-                const double* src = P.q + fi.off + fi.base + ta * fi.sa + tb * fi.sb;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) cp_async8(&X[(slot * NV + v) * FS + r], src + (long long)v * fi.n);
-            } else if (fi.kind == 1) {
-                const double* src = P.mortarG + fi.off + pt;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) cp_async8(&X[(slot * NV + v) * FS + r], src + (long long)v * fi.n);
-            }
-        }
-        asm volatile("cp.async.commit_group;\n" ::);
-    }
-
-    // ---- RK register g: asynchronous prefetch (needed only in the epilogue)
     const bool need_g = P.mode == 1 && P.rkA != 0.0;
-    if (need_g) {
+    const double gm1 = P.ph.gm1;
+    const int G = gridDim.x;
+
+    auto item_cnt = [&](int item) { return min(CNT, nelem - item * CNT); };
+    // meta (slot info + face descriptors) of `item` into meta buffer mb
+    auto issue_meta = [&](int item, int mb) {
+        double* M = META + mb * MW;
+        const int cnt = item_cnt(item);
+        const int start = start0 + item * CNT;
+        const double* sl = reinterpret_cast<const double*>(P.slots + start);
+        const double* fl = reinterpret_cast<const double*>(P.finfo_slot + 6LL * start);
+        for (int w = tid; w < cnt * META_SLOT_W; w += BS) cp_async8(M + w, sl + w);
+        for (int w = tid; w < cnt * 6 * META_FACE_W; w += BS) cp_async8(M + CNT * META_SLOT_W + w, fl + w);
+    };
+    auto slot_of = [&](const double* M, int s) { return reinterpret_cast<const SlotInfo*>(M + s * META_SLOT_W); };
+    auto face_of_m = [&](const double* M, int s, int f) {
+        return reinterpret_cast<const FaceInfo*>(M + CNT * META_SLOT_W + (s * 6 + f) * META_FACE_W);
+    };
+    // state, RK register and outer traces of `item` into pipeline stage st
+    auto issue_data = [&](int item, const double* M, int st) {
+        double* Q = STG + st * STAGE;
+        double* GB = Q + NV * T;
+        double* X = GB + NV * T;
+        const int cnt = item_cnt(item);
 #pragma unroll
         for (int it = 0; it < NPTT; ++it) {
             const int t = tid + it * BS;
-            if (t < ntot) {
+            if (t < cnt * n) {
                 const int slot = t / n, node = t - slot * n;
-                const double* ge = P.g + s_off[slot] + node;
+                const long long off = slot_of(M, slot)->off;
+                const double* qe = P.q + off + node;
 #pragma unroll
-                for (int v = 0; v < NV; ++v) cp_async8(&GB[(slot * NV + v) * n + node], ge + v * n);
+                for (int v = 0; v < NV; ++v) cp_async8(&Q[(slot * NV + v) * n + node], qe + v * n);
+                if (need_g) {
+                    const double* ge = P.g + off + node;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) cp_async8(&GB[(slot * NV + v) * n + node], ge + v * n);
+                }
             }
         }
-    }
+        if (surf) {
+            for (int t = tid; t < cnt * FS; t += BS) {
+                const int slot = t / FS;
+                const int r = t - slot * FS;
+                int f, pt;
+                face_of<S>(r, f, pt);
+                const FaceInfo* fi = face_of_m(M, slot, f);
+                const int nta = f < 2 ? n2 : n1;
+                const int ta = pt % nta, tb = pt / nta;
+                if (fi->kind == 0) {
+                    const double* src = P.q + fi->off + fi->base + ta * fi->sa + tb * fi->sb;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) cp_async8(&X[(slot * NV + v) * FS + r], src + (long long)v * fi->n);
+                } else if (fi->kind == 1) {
+                    const double* src = P.mortarG + fi->off + pt;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) cp_async8(&X[(slot * NV + v) * FS + r], src + (long long)v * fi->n);
+                }
+            }
+        }
+    };
+
+    const int first = blockIdx.x;
+    if (first >= nitems) return;
+    // prologue: meta of items 0 and 1 of this CTA, then data of item 0
+    issue_meta(first, 0);
+    if (first + G < nitems) issue_meta(first + G, 1);
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    issue_data(first, META, 0);
     asm volatile("cp.async.commit_group;\n" ::);
 
-    // ---- state into shared memory (coalesced), 1/rho and p once per node -
-#pragma unroll
-    for (int it = 0; it < NPTT; ++it) {
-        const int t = tid + it * BS;
-        if (t < ntot) {
-            const int slot = t / n, node = t - slot * n;
-            const double* qe = P.q + s_off[slot] + node;
-            double qv[NV];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                qv[v] = qe[v * n];
-                Q[(slot * NV + v) * n + node] = qv[v];
-            }
-            const double ir = 1.0 / qv[0];
-            const double p = gm1 * (qv[4] - 0.5 * ir * (qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]));
-            IR[t] = ir;
-            PR[t] = p;
-            if (!(qv[0] > 0.0 && p > 0.0)) {
-                if (atomicAdd(P.flag, 1) == 0) P.flag[1] = s_e[slot];
-            }
-        }
-    }
+    const double dt = P.mode ? *P.dt : 0.0;
+    double lmax = 0.0;
+    for (int k = 0;; ++k) {
+        const int item = first + k * G;
+        if (item >= nitems) break;
+        // data of item k (issued one iteration ago) and meta of item k+1 have landed
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncthreads();
+        if (item + 2 * G < nitems) issue_meta(item + 2 * G, (k + 2) % 3);
+        if (item + G < nitems) issue_data(item + G, META + ((k + 1) % 3) * MW, (k + 1) & 1);
+        asm volatile("cp.async.commit_group;\n" ::);
 
-    // ---- volume term, direction by direction ------------------------------
-    double acc[NPTT][NV];
-#pragma unroll
-    for (int it = 0; it < NPTT; ++it)
-#pragma unroll
-        for (int v = 0; v < NV; ++v) acc[it][v] = 0.0;
+        const double* M = META + (k % 3) * MW;
+        double* Q = STG + (k & 1) * STAGE;
+        double* GB = Q + NV * T;
+        double* X = GB + NV * T;
+        const int cnt = item_cnt(item);
+        const int ntot = cnt * n;
 
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        if (d > 0) __syncthreads();  // previous direction's derivatives consumed
+        // ---- 1/rho and p once per node; admissibility (reading A25) ----------
 #pragma unroll
         for (int it = 0; it < NPTT; ++it) {
             const int t = tid + it * BS;
             if (t < ntot) {
                 const int slot = t / n, node = t - slot * n;
-                double qv[NV], f[NV];
-#pragma unroll
-                for (int v = 0; v < NV; ++v) qv[v] = Q[(slot * NV + v) * n + node];
-                if (d == 0) flux_axis<0>(qv, IR[t], PR[t], f);
-                else if (d == 1) flux_axis<1>(qv, IR[t], PR[t], f);
-                else flux_axis<2>(qv, IR[t], PR[t], f);
-#pragma unroll
-                for (int v = 0; v < NV; ++v) F[(slot * NV + v) * n + node] = f[v];
+                const double q0 = Q[(slot * NV) * n + node];
+                const double ir = 1.0 / q0;
+                const double m1 = Q[(slot * NV + 1) * n + node], m2 = Q[(slot * NV + 2) * n + node],
+                             m3 = Q[(slot * NV + 3) * n + node];
+                const double p = gm1 * (Q[(slot * NV + 4) * n + node] - 0.5 * ir * (m1 * m1 + m2 * m2 + m3 * m3));
+                IR[t] = ir;
+                PR[t] = p;
+                if (!(q0 > 0.0 && p > 0.0)) {
+                    if (atomicAdd(P.flag, 1) == 0) P.flag[1] = slot_of(M, slot)->e;
+                }
             }
         }
-        __syncthreads();
-        constexpr int Ld[3] = {n1, n2, n3};
-        const int nlines = n / Ld[d];
-        for (int task = tid; task < cnt * NV * nlines; task += BS) {
-            const int sv = task / nlines;  // slot * NV + v
-            const int l = task - sv * nlines;
-            if (d == 0) dline_inplace<n1>(F + sv * n + l * n1, 1);
-            else if (d == 1) dline_inplace<n2>(F + sv * n + (l % n1) + n1 * n2 * (l / n1), n1);
-            else dline_inplace<n3>(F + sv * n + l, n1 * n2);
-        }
-        __syncthreads();
+
+        // ---- volume term, direction by direction --------------------------------
+        double acc[NPTT][NV];
 #pragma unroll
-        for (int it = 0; it < NPTT; ++it) {
-            const int t = tid + it * BS;
-            if (t < ntot) {
-                const int slot = t / n, node = t - slot * n;
-                const double sc = s_sc[slot][d];
+        for (int it = 0; it < NPTT; ++it)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) acc[it][v] = 0.0;
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            __syncthreads();  // IR/PR ready (d = 0); previous derivatives consumed (d > 0)
+#pragma unroll
+            for (int it = 0; it < NPTT; ++it) {
+                const int t = tid + it * BS;
+                if (t < ntot) {
+                    const int slot = t / n, node = t - slot * n;
+                    double qv[NV], f[NV];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) qv[v] = Q[(slot * NV + v) * n + node];
+                    if (d == 0) flux_axis<0>(qv, IR[t], PR[t], f);
+                    else if (d == 1) flux_axis<1>(qv, IR[t], PR[t], f);
+                    else flux_axis<2>(qv, IR[t], PR[t], f);
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) F[(slot * NV + v) * n + node] = f[v];
+                }
+            }
+            __syncthreads();
+            constexpr int Ld[3] = {n1, n2, n3};
+            const int nlines = n / Ld[d];
+            for (int task = tid; task < cnt * NV * nlines; task += BS) {
+                const int sv = task / nlines;  // slot * NV + v
+                const int l = task - sv * nlines;
+                if (d == 0) dline_inplace<n1>(F + sv * n + l * n1, 1);
+                else if (d == 1) dline_inplace<n2>(F + sv * n + (l % n1) + n1 * n2 * (l / n1), n1);
+                else dline_inplace<n3>(F + sv * n + l, n1 * n2);
+            }
+            __syncthreads();
+#pragma unroll
+            for (int it = 0; it < NPTT; ++it) {
+                const int t = tid + it * BS;
+                if (t < ntot) {
+                    const int slot = t / n, node = t - slot * n;
+                    const double sc = slot_of(M, slot)->sc[d];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) acc[it][v] = fma(sc, F[(slot * NV + v) * n + node], acc[it][v]);
+                }
+            }
+        }
+
+        // ---- surface: lifting terms +-(G - f_own) 2/(h_d w_end) into X -------------
+        if (surf) {
+            for (int t = tid; t < cnt * FS; t += BS) {
+                const int slot = t / FS;
+                const int r = t - slot * FS;
+                int f, pt;
+                face_of<S>(r, f, pt);
+                const int d = f >> 1, s = f & 1;
+                const int nta = d == 0 ? n2 : n1;
+                const int ta = pt % nta, tb = pt / nta;
+                int i, j, kk, Nd;
+                if (d == 0) { i = s ? N1 : 0; j = ta; kk = tb; Nd = N1; }
+                else if (d == 1) { i = ta; j = s ? N2 : 0; kk = tb; Nd = N2; }
+                else { i = ta; j = tb; kk = s ? N3 : 0; Nd = N3; }
+                const int node = i + n1 * (j + n2 * kk);
+                double qo[NV], qx[NV], out[NV];
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
-                    acc[it][v] = fma(sc, F[(slot * NV + v) * n + node], acc[it][v]);
-                    if (d == 2) F[(slot * NV + v) * n + node] = acc[it][v];  // park: frees registers
+                    qo[v] = Q[(slot * NV + v) * n + node];
+                    qx[v] = X[(slot * NV + v) * FS + r];
+                }
+                const double iro = IR[slot * n + node], po = PR[slot * n + node];
+                const int kind = face_of_m(M, slot, f)->kind;
+                if (d == 0) face_point<0>(qo, iro, po, qx, kind, s, P.ph, out);
+                else if (d == 1) face_point<1>(qo, iro, po, qx, kind, s, P.ph, out);
+                else face_point<2>(qo, iro, po, qx, kind, s, P.ph, out);
+                const double sc = (s ? 1.0 : -1.0) * slot_of(M, slot)->sc[d] / c_w[Nd][0];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) X[(slot * NV + v) * FS + r] = sc * out[v];
+            }
+            __syncthreads();
+        }
+
+        // ---- epilogue per node: Qdot, or the low-storage RK update (+ CFL rate) ----
+#pragma unroll
+        for (int it = 0; it < NPTT; ++it) {
+            const int t = tid + it * BS;
+            if (t >= ntot) continue;
+            const int slot = t / n, node = t - slot * n;
+            const SlotInfo* si = slot_of(M, slot);
+            if (surf) {
+                const int i = node % n1, j = (node / n1) % n2, kk = node / (n1 * n2);
+                const double* Xb = X + slot * NV * FS;
+                if (i == 0 || i == N1) {
+                    const int r = (i == 0 ? 0 : S::nf0) + j + n2 * kk;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) acc[it][v] += Xb[v * FS + r];
+                }
+                if (j == 0 || j == N2) {
+                    const int r = 2 * S::nf0 + (j == 0 ? 0 : S::nf1) + i + n1 * kk;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) acc[it][v] += Xb[v * FS + r];
+                }
+                if (kk == 0 || kk == N3) {
+                    const int r = 2 * (S::nf0 + S::nf1) + (kk == 0 ? 0 : S::nf2) + i + n1 * j;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) acc[it][v] += Xb[v * FS + r];
+                }
+            }
+            double* o = P.out + si->off + node;
+            if (P.mode == 0) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v) o[v * n] = -acc[it][v];
+            } else {
+                double* g = P.g + si->off + node;
+                double qn[NV];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    const double gn = (need_g ? P.rkA * GB[(slot * NV + v) * n + node] : 0.0) - dt * acc[it][v];
+                    g[v * n] = gn;
+                    qn[v] = Q[(slot * NV + v) * n + node] + P.rkB * gn;
+                    o[v * n] = qn[v];
+                }
+                if (P.lam_max) {  // CFL rate of q^{n+1} (reading A11), fused
+                    const double ir = 1.0 / qn[0];
+                    const double p = gm1 * (qn[4] - 0.5 * ir * (qn[1] * qn[1] + qn[2] * qn[2] + qn[3] * qn[3]));
+                    const double c = sqrt(P.gamma * p * ir);
+                    constexpr double L1 = (double)n1 * n1, L2 = (double)n2 * n2, L3 = (double)n3 * n3;
+                    const double lam = 0.5 * ((fabs(qn[1] * ir) + c) * L1 * si->sc[0] + (fabs(qn[2] * ir) + c) * L2 * si->sc[1] +
+                                              (fabs(qn[3] * ir) + c) * L3 * si->sc[2]);
+                    lmax = fmax(lmax, lam);
                 }
             }
         }
     }
-
-    // ---- surface: lifting terms +-(G - f_own) 2/(h_d w_end) into X ---------
-    if (surf) {
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-        __syncthreads();
-        for (int t = tid; t < cnt * FS; t += BS) {
-            const int slot = t / FS;
-            const int r = t - slot * FS;
-            int f, pt;
-            face_of<S>(r, f, pt);
-            const int d = f >> 1, s = f & 1;
-            const int nta = d == 0 ? n2 : n1;
-            const int ta = pt % nta, tb = pt / nta;
-            int i, j, k, Nd;
-            if (d == 0) { i = s ? N1 : 0; j = ta; k = tb; Nd = N1; }
-            else if (d == 1) { i = ta; j = s ? N2 : 0; k = tb; Nd = N2; }
-            else { i = ta; j = tb; k = s ? N3 : 0; Nd = N3; }
-            const int node = i + n1 * (j + n2 * k);
-            double qo[NV], qx[NV], out[NV];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                qo[v] = Q[(slot * NV + v) * n + node];
-                qx[v] = X[(slot * NV + v) * FS + r];
-            }
-            const double iro = IR[slot * n + node], po = PR[slot * n + node];
-            const int kind = P.finfo[6 * s_e[slot] + f].kind;
-            if (d == 0) face_point<0>(qo, iro, po, qx, kind, s, P.ph, out);
-            else if (d == 1) face_point<1>(qo, iro, po, qx, kind, s, P.ph, out);
-            else face_point<2>(qo, iro, po, qx, kind, s, P.ph, out);
-            const double sc = (s ? 1.0 : -1.0) * s_sc[slot][d] / c_w[Nd][0];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) X[(slot * NV + v) * FS + r] = sc * out[v];
-        }
-        __syncthreads();
-    }
-
-    // ---- epilogue per node --------------------------------------------------
-    const double dt = P.mode ? *P.dt : 0.0;
-    double lmax = 0.0;
-    if (need_g) asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // own g values only
-#pragma unroll
-    for (int it = 0; it < NPTT; ++it) {
-        const int t = tid + it * BS;
-        if (t >= ntot) continue;
-        const int slot = t / n, node = t - slot * n;
-        double accv[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) accv[v] = F[(slot * NV + v) * n + node];
-        if (surf) {
-            const int i = node % n1, j = (node / n1) % n2, k = node / (n1 * n2);
-            const double* Xb = X + slot * NV * FS;
-            if (i == 0 || i == N1) {
-                const int r = (i == 0 ? 0 : S::nf0) + j + n2 * k;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) accv[v] += Xb[v * FS + r];
-            }
-            if (j == 0 || j == N2) {
-                const int r = 2 * S::nf0 + (j == 0 ? 0 : S::nf1) + i + n1 * k;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) accv[v] += Xb[v * FS + r];
-            }
-            if (k == 0 || k == N3) {
-                const int r = 2 * (S::nf0 + S::nf1) + (k == 0 ? 0 : S::nf2) + i + n1 * j;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) accv[v] += Xb[v * FS + r];
-            }
-        }
-        double* o = P.out + s_off[slot] + node;
-        if (P.mode == 0) {
-#pragma unroll
-            for (int v = 0; v < NV; ++v) o[v * n] = -accv[v];
-        } else {
-            double* g = P.g + s_off[slot] + node;
-            double qn[NV];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const double gn = (need_g ? P.rkA * GB[(slot * NV + v) * n + node] : 0.0) - dt * accv[v];
-                g[v * n] = gn;
-                qn[v] = Q[(slot * NV + v) * n + node] + P.rkB * gn;
-                o[v * n] = qn[v];
-            }
-            if (P.lam_max) {  // CFL rate of q^{n+1} (reading A11), fused
-                const double ir = 1.0 / qn[0];
-                const double p = (P.gamma - 1.0) * (qn[4] - 0.5 * ir * (qn[1] * qn[1] + qn[2] * qn[2] + qn[3] * qn[3]));
-                const double c = sqrt(P.gamma * p * ir);
-                constexpr double L1 = (double)n1 * n1, L2 = (double)n2 * n2, L3 = (double)n3 * n3;
-                const double lam = 0.5 * ((fabs(qn[1] * ir) + c) * L1 * s_sc[slot][0] +
-                                          (fabs(qn[2] * ir) + c) * L2 * s_sc[slot][1] +
-                                          (fabs(qn[3] * ir) + c) * L3 * s_sc[slot][2]);
-                lmax = fmax(lmax, lam);
-            }
-        }
-    }
     if (P.lam_max) {
-        __shared__ double red[32];
         lmax = block_max(lmax, red);
         if (threadIdx.x == 0) atomicMax(P.lam_max, (unsigned long long)__double_as_longlong(lmax));
     }
 }
 
 // host-side: launcher table filled by the instantiation units
-typedef void (*res_launcher)(const ResParams& P, int item0, int nitems, cudaStream_t st);
+typedef void (*res_launcher)(const ResParams& P, int start0, int nelem, int nitems, int grid, cudaStream_t st);
+typedef int (*res_occupancy)();
 
 static inline cudaError_t res_copy_constants(const Tables* host)
 {
@@ -494,11 +526,21 @@ static inline cudaError_t res_copy_constants(const Tables* host)
     return cudaMemcpyToSymbol(c_EOM, M, sizeof(M));
 }
 
+// persistent launch: `grid` CTAs (resident capacity), each walking the bucket's items
 template <int N1, int N2, int N3>
-void launch_res_t(const ResParams& P, int item0, int nitems, cudaStream_t st)
+void launch_res_t(const ResParams& P, int start0, int nelem, int nitems, int grid, cudaStream_t st)
 {
     using S = Shape<N1, N2, N3>;
-    k_res_t<N1, N2, N3><<<nitems, S::BS, S::smem_bytes, st>>>(P, item0);
+    k_res_t<N1, N2, N3><<<grid < nitems ? grid : nitems, S::BS, S::smem_bytes, st>>>(P, start0, nelem, nitems);
+}
+
+template <int N1, int N2, int N3>
+int occ_res_t()
+{
+    using S = Shape<N1, N2, N3>;
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_res_t<N1, N2, N3>, S::BS, S::smem_bytes);
+    return nb;
 }
 
 template <int N1, int N2, int N3>
