@@ -103,6 +103,9 @@ struct dg_ctx {
     res_occupancy rocc[NP][NP][NP] = {};
     int nsm = 148;
     FaceInfo* d_finfo_slot = nullptr;
+    static constexpr int NSTREAMS = 8;  // concurrent bucket launches for mixed-order layouts
+    cudaStream_t side[NSTREAMS] = {};
+    cudaEvent_t ev_fork = nullptr, ev_join[NSTREAMS] = {};
     bool generic = false;  // DGTAU_GENERIC=1: runtime-order residual kernel (A/B testing)
 };
 
@@ -242,6 +245,15 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
             dg_destroy(ctx);
             return s;
         }
+        for (int i = 0; i < dg_ctx::NSTREAMS && s == DG_OK; ++i) {
+            s = cuda_check(ctx, cudaStreamCreateWithFlags(&ctx->side[i], cudaStreamNonBlocking), "side stream");
+            if (s == DG_OK) s = cuda_check(ctx, cudaEventCreateWithFlags(&ctx->ev_join[i], cudaEventDisableTiming), "event");
+        }
+        if (s == DG_OK) s = cuda_check(ctx, cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming), "event");
+        if (s != DG_OK) {
+            dg_destroy(ctx);
+            return s;
+        }
         const char* g = getenv("DGTAU_GENERIC");
         ctx->generic = g && g[0] == '1';
     }
@@ -276,6 +288,11 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
 void dg_destroy(dg_ctx* ctx)
 {
     if (!ctx) return;
+    for (int i = 0; i < dg_ctx::NSTREAMS; ++i) {
+        if (ctx->side[i]) cudaStreamDestroy(ctx->side[i]);
+        if (ctx->ev_join[i]) cudaEventDestroy(ctx->ev_join[i]);
+    }
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     dfree(ctx->d_tab);
     dfree(ctx->d_tdd);
     dfree(ctx->d_nbr);
@@ -652,7 +669,8 @@ static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, doub
         M.mortarG = ctx->d_mortarG;
         M.tab = ctx->d_tab;
         M.ph = phys_dev(ctx->prm);
-        k_mortar<<<ctx->nmortar, 128, 0, st>>>(M);
+        if (ctx->generic) k_mortar<<<ctx->nmortar, 128, 0, st>>>(M);
+        else k_mortar2<<<(ctx->nmortar + MW_FACES - 1) / MW_FACES, 32 * MW_FACES, 0, st>>>(M, ctx->nmortar);
         ctx->launches++;
     }
     ResParams P;
@@ -685,9 +703,24 @@ static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, doub
         k_residual<<<ctx->nwork, BLOCK, ctx->res_smem, st>>>(P);
         ctx->launches++;
     } else {
-        for (const Bucket& b : ctx->buckets) {
+        if (ctx->buckets.size() == 1) {
+            const Bucket& b = ctx->buckets[0];
             ctx->rtab[b.ord & 255][(b.ord >> 8) & 255][(b.ord >> 16) & 255](P, b.start0, b.nelem, b.nitems, b.grid, st);
             ctx->launches++;
+        } else {  // mixed orders: the buckets are independent -> run them concurrently
+            const int ns = std::min<int>(dg_ctx::NSTREAMS, (int)ctx->buckets.size());
+            CK(cudaEventRecord(ctx->ev_fork, st));
+            for (int i = 0; i < ns; ++i) CK(cudaStreamWaitEvent(ctx->side[i], ctx->ev_fork, 0));
+            for (size_t i = 0; i < ctx->buckets.size(); ++i) {
+                const Bucket& b = ctx->buckets[i];
+                ctx->rtab[b.ord & 255][(b.ord >> 8) & 255][(b.ord >> 16) & 255](P, b.start0, b.nelem, b.nitems, b.grid,
+                                                                                ctx->side[i % ns]);
+                ctx->launches++;
+            }
+            for (int i = 0; i < ns; ++i) {
+                CK(cudaEventRecord(ctx->ev_join[i], ctx->side[i]));
+                CK(cudaStreamWaitEvent(st, ctx->ev_join[i], 0));
+            }
         }
     }
     return check_stream_error(ctx, "k_residual launch");
