@@ -39,6 +39,15 @@ TAU_MAX = 1e-4
 NMIN, NMAX = 3, 8
 
 
+def load_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel from the committed ncu --set full capture (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic_k_res_t.json")
+    if os.path.exists(p):
+        return json.load(open(p)).get("dram_bytes_per_launch")
+    return None
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -376,7 +385,7 @@ def main():
         "rhs_rk_gdof_s": world * res["ndof"] * 3 * res["rk_count"] / (res["rk_ms"] * 1e-3) / 1e9,
         "roofline": {"kernel": "k_residual (fused residual + RK stage)", "bound": "hbm", "achieved": res["achieved"],
                      "peak": res["peak"], "unit": "GB/s", "frac": res["achieved"] / res["peak"],
-                     "peak_source": res["peak_kind"], "traffic": None,
+                     "peak_source": res["peak_kind"], "traffic": load_traffic(),
                      "bytes_per_dof": "120 (stage 1) / 160 (stages 2,3)"},
         "cpu_baseline": cpu,
         "e2e": res["e2e"],
