@@ -57,6 +57,38 @@ __device__ __forceinline__ void unpack_ord(int ord, int& N1, int& N2, int& N3)
 }
 
 // ---------------------------------------------------------------------------
+// Branch-free fp64 reciprocal / square root for positive normal arguments:
+// MUFU seed (rcp/rsqrt.approx.ftz.f64) + Newton steps, within ~1 ulp (the
+// IEEE-rounded library versions carry slow-path branches).
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double rcp_nr(double x)
+{
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+
+__device__ __forceinline__ double rsqrt_nr(double x)
+{
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    const double hx = 0.5 * x;
+    r = r * fma(-hx * r, r, 1.5);
+    return r * fma(-hx * r, r, 1.5);
+}
+
+__device__ __forceinline__ double sqrt_nr(double x)
+{
+    const double r = rsqrt_nr(x);
+    const double s = x * r;
+    return fma(0.5 * r, fma(-s, s, x), s);
+}
+
+// ---------------------------------------------------------------------------
 // Pointwise physics
 // ---------------------------------------------------------------------------
 
@@ -222,11 +254,38 @@ struct ResParams {
     const FaceInfo* finfo;  // [E][6]
     const SlotInfo* slots;  // [elist length], parallel to elist
     const FaceInfo* finfo_slot;  // [elist length][6]: finfo of elist[i] (one dependent load less)
+    const long long* fofs_slot;  // [elist length][6]: offset of each face's Riemann flux block in mortarG
     const Tables* tab;
     PhysDev ph;
     int* flag;              // [0] admissibility violations, [1] element id
     unsigned long long* lam_max;  // if set (last RK stage): max CFL rate of the NEW state (bits of a double >= 0)
     double gamma;
+    long long qlen;         // doubles in the state buffer q (bulk copies never read past it)
+};
+
+// One conforming (or boundary) face, Riemann flux computed once per face
+// point by k_face: L = the element on the -xi_d side (its +1 face), R = the
+// element on the +xi_d side (its -1 face).  Trace of variable v at face point
+// (ta, tb) of side X: q[offX + v*nX + baseX + ta*saX + tb*sbX].  Boundary
+// faces (kind 2 wall, 3 far field) have off = -1 on the ghost side.  The flux
+// (normal +e_d) of point pt = ta + nta*tb goes to G[goff + v*nf + pt].
+struct FaceItem {
+    long long offL, offR, goff;
+    int nL, nR, baseL, baseR;
+    int saL, sbL, saR, sbR;
+    int nta, nf, d, kind;
+};
+
+constexpr int FACE_BS = 128;
+
+struct FaceParams {
+    const double* q;
+    double* G;
+    const FaceItem* faces;
+    const int* fpt;    // [nfaces+1] point prefix
+    const int* fcta;   // [nblk+1] face of the first point of each CTA
+    int npts;
+    PhysDev ph;
 };
 
 __device__ __forceinline__ void node_ijk(int node, int n1, int n2, int& i, int& j, int& k)

@@ -19,6 +19,7 @@
 #include "basis.h"
 #include "kernels.cuh"
 #include "residual_t.cuh"
+#include "face.cuh"
 #include "tau_t.cuh"
 #include "curved.cuh"
 
@@ -103,6 +104,12 @@ struct dg_ctx {
     res_occupancy rocc[NP][NP][NP] = {};
     int nsm = 148;
     FaceInfo* d_finfo_slot = nullptr;
+    long long* d_fofs_slot = nullptr;  // [elist][6] flux offset (into d_mortarG) of each face of each slot
+    FaceItem* d_faces = nullptr;       // conforming + boundary faces (one Riemann flux per face point)
+    int* d_fpt = nullptr;              // [nfaces+1] point prefix
+    int* d_fcta = nullptr;             // [nfblk+1] first face of each k_face CTA
+    int nfaces = 0, nfblk = 0;
+    long long nface_pts = 0;
     static constexpr int NSTREAMS = 8;  // concurrent bucket launches for mixed-order layouts
     cudaStream_t side[NSTREAMS] = {};
     cudaEvent_t ev_fork = nullptr, ev_join[NSTREAMS] = {};
@@ -305,6 +312,10 @@ void dg_destroy(dg_ctx* ctx)
     dfree(ctx->d_moff);
     dfree(ctx->d_finfo);
     dfree(ctx->d_finfo_slot);
+    dfree(ctx->d_fofs_slot);
+    dfree(ctx->d_faces);
+    dfree(ctx->d_fpt);
+    dfree(ctx->d_fcta);
     dfree(ctx->d_slots);
     dfree(ctx->d_levels);
     dfree(ctx->d_ref_scratch);
@@ -448,12 +459,87 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
             if (NL[TA[d]] == NR[TA[d]] && NL[TB[d]] == NR[TB[d]]) continue;
             mort.push_back(MortarItem{e, nb, d, 0});
             moff[6LL * e + 2 * d + 1] = mlen;
-            mlen += (long long)NV * (NL[TA[d]] + 1) * (NL[TB[d]] + 1);
+            mlen += ((long long)NV * (NL[TA[d]] + 1) * (NL[TB[d]] + 1) + 1) & ~1LL;  // 16-byte aligned blocks
             moff[6LL * nb + 2 * d] = mlen;
-            mlen += (long long)NV * (NR[TA[d]] + 1) * (NR[TB[d]] + 1);
+            mlen += ((long long)NV * (NR[TA[d]] + 1) * (NR[TB[d]] + 1) + 1) & ~1LL;
         }
     ctx->nmortar = (int)mort.size();
     ctx->mortar_len = mlen;
+    // conforming faces and boundary faces of owned elements: the Riemann flux
+    // of each face point is computed once (k_face) into the flux buffer after
+    // the mortar blocks; fofs = flux offset of every element face.
+    std::vector<long long> fofs(moff);
+    std::vector<FaceItem> faces;
+    std::vector<int> fpt(1, 0);
+    long long flen = mlen;
+    {
+        auto strides = [&](int el, int* st) {
+            const int* N = &ctx->orders[3 * el];
+            st[0] = 1; st[1] = N[0] + 1; st[2] = (N[0] + 1) * (N[1] + 1);
+        };
+        for (int d = 0; d < 3; ++d)
+            for (int e = 0; e < E; ++e) {
+                const int* No = &ctx->orders[3 * e];
+                const int nf = (No[TA[d]] + 1) * (No[TB[d]] + 1);
+                for (int side = 0; side < 2; ++side) {  // side 1: + face of e (e = L); side 0: - face (BC only)
+                    const int nb = ctx->nbr[6 * e + 2 * d + side];
+                    FaceItem fi{};
+                    fi.d = d;
+                    fi.nf = nf;
+                    fi.nta = No[TA[d]] + 1;
+                    int st[3];
+                    strides(e, st);
+                    if (side == 1 && nb >= 0) {
+                        if (moff[6LL * e + 2 * d + 1] >= 0) continue;       // mortar
+                        if (e >= ctx->n_own && nb >= ctx->n_own) continue;  // halo-halo
+                        int sr[3];
+                        strides(nb, sr);
+                        fi.kind = 0;
+                        fi.offL = ctx->off[e];
+                        fi.nL = npts(No);
+                        fi.baseL = No[d] * st[d];
+                        fi.saL = st[TA[d]];
+                        fi.sbL = st[TB[d]];
+                        fi.offR = ctx->off[nb];
+                        fi.nR = npts(&ctx->orders[3 * nb]);
+                        fi.baseR = 0;
+                        fi.saR = sr[TA[d]];
+                        fi.sbR = sr[TB[d]];
+                        fi.goff = flen;
+                        fofs[6LL * e + 2 * d + 1] = flen;
+                        fofs[6LL * nb + 2 * d] = flen;
+                    } else if ((nb == -1 || nb == -2) && e < ctx->n_own) {
+                        fi.kind = nb == -1 ? 2 : 3;
+                        const long long o = ctx->off[e];
+                        if (side == 1) { fi.offL = o; fi.nL = npts(No); fi.baseL = No[d] * st[d]; fi.saL = st[TA[d]]; fi.sbL = st[TB[d]]; fi.offR = -1; }
+                        else { fi.offR = o; fi.nR = npts(No); fi.baseR = 0; fi.saR = st[TA[d]]; fi.sbR = st[TB[d]]; fi.offL = -1; }
+                        fi.goff = flen;
+                        fofs[6LL * e + 2 * d + side] = flen;
+                    } else {
+                        continue;
+                    }
+                    faces.push_back(fi);
+                    fpt.push_back(fpt.back() + nf);
+                    flen += ((long long)NV * nf + 1) & ~1LL;
+                }
+            }
+    }
+    ctx->nfaces = (int)faces.size();
+    ctx->nface_pts = fpt.back();
+    {
+        std::vector<int> fcta;
+        const long long np = ctx->nface_pts;
+        ctx->nfblk = (int)((np + FACE_BS - 1) / FACE_BS);
+        int f = 0;
+        for (int b = 0; b <= ctx->nfblk; ++b) {
+            const long long gp = std::min<long long>((long long)b * FACE_BS, np > 0 ? np - 1 : 0);
+            while (f + 1 < (int)faces.size() && fpt[f + 1] <= gp) ++f;
+            fcta.push_back(f);
+        }
+        CK(upload(ctx->d_faces, faces));
+        CK(upload(ctx->d_fpt, fpt));
+        CK(upload(ctx->d_fcta, fcta));
+    }
     // per element-face source descriptors of the outer state (see FaceInfo)
     std::vector<FaceInfo> finfo(6LL * E);
     for (int e = 0; e < E; ++e)
@@ -495,6 +581,10 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     for (size_t i = 0; i < elist.size(); ++i)
         for (int f = 0; f < 6; ++f) fslot[6 * i + f] = finfo[6LL * elist[i] + f];
     CK(upload(ctx->d_finfo_slot, fslot));
+    std::vector<long long> fos(6 * elist.size());
+    for (size_t i = 0; i < elist.size(); ++i)
+        for (int f = 0; f < 6; ++f) fos[6 * i + f] = fofs[6LL * elist[i] + f];
+    CK(upload(ctx->d_fofs_slot, fos));
     for (Bucket& b : ctx->buckets) {
         const int occ = ctx->rocc[b.ord & 255][(b.ord >> 8) & 255][(b.ord >> 16) & 255]();
         b.grid = std::max(1, occ) * ctx->nsm;
@@ -520,7 +610,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     CK(upload(ctx->d_mortar, mort));
     CK(upload(ctx->d_moff, moff));
     dfree(ctx->d_mortarG);
-    if (mlen > 0) CK(cudaMalloc(&ctx->d_mortarG, sizeof(double) * mlen));
+    if (flen > 0) CK(cudaMalloc(&ctx->d_mortarG, sizeof(double) * flen));
     dfree(ctx->d_sel);
     dfree(ctx->d_margin);
     CK(cudaMalloc(&ctx->d_sel, sizeof(int) * 6LL * E));
@@ -673,6 +763,18 @@ static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, doub
         else k_mortar2<<<(ctx->nmortar + MW_FACES - 1) / MW_FACES, 32 * MW_FACES, 0, st>>>(M, ctx->nmortar);
         ctx->launches++;
     }
+    if (variant == DG_NONISOLATED && !ctx->generic && ctx->nface_pts > 0) {
+        FaceParams FP;
+        FP.q = q;
+        FP.G = ctx->d_mortarG;
+        FP.faces = ctx->d_faces;
+        FP.fpt = ctx->d_fpt;
+        FP.fcta = ctx->d_fcta;
+        FP.npts = (int)ctx->nface_pts;
+        FP.ph = phys_dev(ctx->prm);
+        k_face<<<ctx->nfblk, FACE_BS, 0, st>>>(FP);
+        ctx->launches++;
+    }
     ResParams P;
     P.q = q;
     P.out = out;
@@ -693,11 +795,15 @@ static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, doub
     P.finfo = ctx->d_finfo;
     P.slots = ctx->d_slots;
     P.finfo_slot = ctx->d_finfo_slot;
+    P.fofs_slot = ctx->d_fofs_slot;
     P.tab = ctx->d_tab;
     P.ph = phys_dev(ctx->prm);
     P.flag = ctx->d_flag;
     P.lam_max = lam_max;
     P.gamma = ctx->prm.gamma;
+    P.qlen = ctx->off[ctx->E];
+    if ((reinterpret_cast<uintptr_t>(q) & 15) != 0)
+        return fail(ctx, DG_EINVAL, "residual: state pointer must be 16-byte aligned");
     if (ctx->generic && lam_max) return fail(ctx, DG_EUNSUPPORTED, "fused dt needs the specialised kernels");
     if (ctx->generic) {
         k_residual<<<ctx->nwork, BLOCK, ctx->res_smem, st>>>(P);

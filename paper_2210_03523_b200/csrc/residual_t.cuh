@@ -1,20 +1,24 @@
 // residual_t.cuh -- order-specialised fused DGSEM residual / RK-stage kernel.
 //
-// One template instance per (N1,N2,N3) bucket; a CTA processes CNT elements of
-// that bucket (work items of the plan, spatially ordered).  Same numerics as
-// the generic path (strong-form GL-DGSEM, see kernels.cuh header; PAPER.md
-// P:129-155), arranged for the sm_100a fp64 pipes:
-//   * element state read once from HBM into registers of node-owner threads
-//     (ir = 1/rho and p computed once per node);
-//   * per direction d the node owners write f_d to shared memory, then one
-//     thread per (line, variable) holds the line in registers and applies
-//     D^{N_d} with compile-time loops; D comes from __constant__ memory with
-//     compile-time offsets (constant-bank operands of DFMA);
-//   * surface: one thread per (face, face point), packed over the 6 faces of
-//     all CTA elements; Roe flux with the neighbour trace read from L2;
-//     (G - f_own) * lifting scale goes to shared memory;
-//   * epilogue per node: Qdot = -(volume + lifting), or the Williamson
-//     low-storage update g <- A g + dt Qdot, q' <- q + B g.
+// One template instance per (N1,N2,N3) bucket; a persistent CTA walks work
+// items of CNT same-order elements.  Same numerics as the generic path
+// (strong-form GL-DGSEM, see kernels.cuh header; PAPER.md P:129-155,
+// P:472-473), arranged for the sm_100a fp64 pipes (v7):
+//   * the element states of item k+1 are fetched by ONE thread with 1-D TMA
+//     bulk copies (cp.async.bulk, mbarrier complete_tx) into the second
+//     shared stage while item k is computed; neighbour traces (or projected
+//     mortar fluxes) by cp.async into a double-buffered trace stage; the RK
+//     register g is loaded into registers at item start and consumed in the
+//     epilogue (latency hidden behind the whole item);
+//   * node phase: 1/rho, p and the three axis fluxes f_x, f_y, f_z of every
+//     node go to shared memory at once (one barrier);
+//   * task phase (one barrier): Roe face tasks (one thread per face point,
+//     G - f_own times the lifting scale, in place in the trace buffer) run
+//     beside the 5 x (lines) x 3 line-derivative tasks (even-odd split of D,
+//     line in registers, in place);
+//   * epilogue per node: Qdot = -(sum_d (2/h_d) D^d f_d + lifting), or the
+//     Williamson low-storage update g <- A g + dt Qdot, q' <- q + B g, plus
+//     the fused CFL rate of q' in the last stage.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -42,20 +46,32 @@ template <int N1, int N2, int N3>
 struct Shape {
     static constexpr int n1 = N1 + 1, n2 = N2 + 1, n3 = N3 + 1;
     static constexpr int n = n1 * n2 * n3;
-    // <= ~384 nodes per CTA so nodes, (line, variable) tasks and face tasks
-    // each take one round of threads (no half-empty second rounds before the
-    // barriers); two node passes only for n > 384.
+    // <= ~384 nodes per CTA so node tasks take one round of threads; two
+    // node passes only for n > 384.
     static constexpr int CNT = cmax(1, cmin(MAXSLOTS, 384 / n));
     static constexpr int T = CNT * n;
     static constexpr int NPT = T > 384 ? 2 : 1;
     static constexpr int BS = ((T + NPT - 1) / NPT + 31) / 32 * 32;
     static constexpr int nf0 = n2 * n3, nf1 = n1 * n3, nf2 = n1 * n2;
     static constexpr int FS = 2 * (nf0 + nf1 + nf2);
-    // F (5T) + IR,P (2T) + 2 pipeline stages x {Q (5T), g (5T), outer traces (5 FS per element)}
-    // + 3 meta buffers (slot info + face descriptors)
-    static constexpr size_t smem_bytes =
-        sizeof(double) * (size_t)(7 * T + 2 * (10 * T + NV * CNT * FS) + 3 * CNT * (5 + 24));
-    static constexpr int MINB = BS <= 128 ? 4 : (BS <= 192 ? 3 : (BS <= 384 ? 2 : 1));
+    static constexpr int LT = NV * (n / n1 + n / n2 + n / n3);  // line tasks per element
+    // state slot: 5n doubles + 1 (8-byte shift of odd-offset elements), even
+    static constexpr int SQ = (NV * n + 2) / 2 * 2;
+    static constexpr int QS = CNT * SQ;          // one state stage
+    // face flux blocks of one element: [face][v][pt], each block padded to even
+    __host__ __device__ static constexpr int gblk(int d) { return (NV * (d == 0 ? nf0 : d == 1 ? nf1 : nf2) + 1) / 2 * 2; }
+    __host__ __device__ static constexpr int gbase(int f) {
+        return (f >= 1 ? gblk(0) : 0) + (f >= 2 ? gblk(0) : 0) + (f >= 3 ? gblk(1) : 0) + (f >= 4 ? gblk(1) : 0) +
+               (f >= 5 ? gblk(2) : 0);
+    }
+    static constexpr int GSL = 2 * (gblk(0) + gblk(1) + gblk(2));
+    static constexpr int GS = CNT * GSL;         // one flux stage
+    static constexpr int MW = CNT * (5 + 6);     // meta words per item (slot info + 6 face flux offsets)
+    // 2 state stages + 2 flux stages + F (3 directions) + 3 meta buffers
+    static constexpr size_t smem_bytes = sizeof(double) * (size_t)(2 * QS + 2 * GS + 3 * NV * T + 3 * MW);
+    static constexpr int MINB_T = BS <= 128 ? 4 : (BS <= 192 ? 3 : (BS <= 384 ? 2 : 1));
+    static constexpr int MINB_S = (int)((227 * 1024) / (smem_bytes + 1024 + 512));
+    static constexpr int MINB = cmax(1, cmin(MINB_T, MINB_S));
 };
 
 // f . e_d for the Euler flux, from q with precomputed 1/rho and p
@@ -126,6 +142,11 @@ __device__ __forceinline__ void dline_inplace(double* Fl, int stride)
     }
 }
 
+__device__ __forceinline__ void cp_async8s(unsigned d, const double* src)
+{
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+
 __device__ __forceinline__ void cp_async8(double* dst, const double* src)
 {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -161,8 +182,8 @@ __device__ __forceinline__ void roe_axis(const double* qL, double irL, double pL
 #pragma unroll
     for (int k = 0; k < 3; ++k) { uL[k] = qL[1 + k] * irL; uR[k] = qR[1 + k] * irR; }
     const double HL = (qL[4] + pL) * irL, HR = (qR[4] + pR) * irR;
-    const double sL = sqrt(qL[0]), sR = sqrt(qR[0]);
-    const double is = 1.0 / (sL + sR);
+    const double sL = sqrt_nr(qL[0]), sR = sqrt_nr(qR[0]);
+    const double is = rcp_nr(sL + sR);
     const double wl = sL * is, wr = sR * is;
     double u[3], du[3];
 #pragma unroll
@@ -170,8 +191,8 @@ __device__ __forceinline__ void roe_axis(const double* qL, double irL, double pL
     const double H = wl * HL + wr * HR;
     const double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
     const double c2 = gm1 * (H - 0.5 * uu);
-    const double c = sqrt(c2);
-    const double ic2 = 1.0 / c2;
+    const double ic2 = rcp_nr(c2);
+    const double c = c2 * rsqrt_nr(c2);
     const double un = u[d], dun = du[d];
     const double rho = sL * sR;
     const double dp = pR - pL;
@@ -213,7 +234,7 @@ __device__ __forceinline__ void face_point(const double* qo, double iro, double 
             double nrm[3] = {d == 0 ? 1.0 : 0.0, d == 1 ? 1.0 : 0.0, d == 2 ? 1.0 : 0.0};
             if (s) llf_flux(qo, qx, nrm, ph.gamma, G); else llf_flux(qx, qo, nrm, ph.gamma, G);
         } else {
-            const double irx = 1.0 / qx[0];
+            const double irx = rcp_nr(qx[0]);
             const double px = ph.gm1 * (qx[4] - 0.5 * irx * (qx[1] * qx[1] + qx[2] * qx[2] + qx[3] * qx[3]));
             if (s) roe_axis<d>(qo, iro, po, qx, irx, px, ph.gamma, G);
             else roe_axis<d>(qx, irx, px, qo, iro, po, ph.gamma, G);
@@ -227,22 +248,60 @@ __device__ __forceinline__ void face_point(const double* qo, double iro, double 
 // face descriptors (4 doubles each) of every element of the item.
 constexpr int META_SLOT_W = 5, META_FACE_W = 4;
 
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* b, int count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// 1-D TMA bulk copy global -> shared, completion counted on mbarrier b
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(b))
+                 : "memory");
+}
+
 template <int N1, int N2, int N3>
 __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB)
     k_res_t(ResParams P, int start0, int nelem, int nitems)
 {
     using S = Shape<N1, N2, N3>;
-    constexpr int n = S::n, n1 = S::n1, n2 = S::n2, n3 = S::n3, BS = S::BS, NPTT = S::NPT, FS = S::FS;
-    constexpr int T = S::T, CNT = S::CNT;
-    constexpr int MW = CNT * (META_SLOT_W + 6 * META_FACE_W);  // meta words per item
-    extern __shared__ double sm[];
-    double* F = sm;                   // [slot][v][node]  flux of one direction, then its derivative
-    double* IR = F + NV * T;          // 1/rho
-    double* PR = IR + T;              // pressure
-    double* STG = PR + T;             // 2 pipeline stages of {Q 5T, GB 5T, X 5 CNT FS}
-    constexpr int STAGE = 10 * T + NV * CNT * FS;
-    double* META = STG + 2 * STAGE;   // 3 meta buffers of MW words
+    constexpr int n = S::n, n1 = S::n1, n2 = S::n2, n3 = S::n3, BS = S::BS, NPTT = S::NPT;
+    constexpr int T = S::T, CNT = S::CNT, SQ = S::SQ, QS = S::QS, GSL = S::GSL, GS = S::GS, MW = S::MW;
+    constexpr int L0 = n / n1, L1 = n / n2, L2 = n / n3;  // lines per direction
+    extern __shared__ __align__(16) double sm[];
+    double* QST = sm;                 // 2 state stages [slot][SQ]: element data at +shift (0/1)
+    double* GST = QST + 2 * QS;       // 2 flux stages [slot][face][v][pt] (face blocks 16-byte aligned)
+    double* F = GST + 2 * GS;         // [slot][d][v][node]: f_d, then (in place) D^d f_d
+    double* META = F + 3 * NV * T;    // 3 meta buffers of MW words
     __shared__ double red[32];
+    __shared__ __align__(8) unsigned long long mbar[2];
 
     const int tid = threadIdx.x;
     const bool surf = P.variant == 0;
@@ -251,192 +310,168 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
     const int G = gridDim.x;
 
     auto item_cnt = [&](int item) { return min(CNT, nelem - item * CNT); };
-    // meta (slot info + face descriptors) of `item` into meta buffer mb
+    auto slot_of = [&](const double* M, int s) { return reinterpret_cast<const SlotInfo*>(M + s * META_SLOT_W); };
+    auto fofs_of = [&](const double* M, int s, int f) {
+        return reinterpret_cast<const long long*>(M + CNT * META_SLOT_W)[s * 6 + f];
+    };
+    // meta (slot info + face flux offsets) of `item` into meta buffer mb
     auto issue_meta = [&](int item, int mb) {
         double* M = META + mb * MW;
         const int cnt = item_cnt(item);
         const int start = start0 + item * CNT;
         const double* sl = reinterpret_cast<const double*>(P.slots + start);
-        const double* fl = reinterpret_cast<const double*>(P.finfo_slot + 6LL * start);
+        const double* fl = reinterpret_cast<const double*>(P.fofs_slot + 6LL * start);
         for (int w = tid; w < cnt * META_SLOT_W; w += BS) cp_async8(M + w, sl + w);
-        for (int w = tid; w < cnt * 6 * META_FACE_W; w += BS) cp_async8(M + CNT * META_SLOT_W + w, fl + w);
+        for (int w = tid; w < cnt * 6; w += BS) cp_async8(M + CNT * META_SLOT_W + w, fl + w);
     };
-    auto slot_of = [&](const double* M, int s) { return reinterpret_cast<const SlotInfo*>(M + s * META_SLOT_W); };
-    auto face_of_m = [&](const double* M, int s, int f) {
-        return reinterpret_cast<const FaceInfo*>(M + CNT * META_SLOT_W + (s * 6 + f) * META_FACE_W);
-    };
-    // state, RK register and outer traces of `item` into pipeline stage st
-    auto issue_data = [&](int item, const double* M, int st) {
-        double* Q = STG + st * STAGE;
-        double* GB = Q + NV * T;
-        double* X = GB + NV * T;
+    // element states and face flux blocks of `item` into stage st, by ONE
+    // thread with 1-D bulk copies.  State: the 16-byte aligned envelope
+    // [floor16(src), ceil16(src + 40n)) (data at shift off & 1), clipped at the
+    // buffer end (last 8 bytes by hand).  Flux blocks are 16-byte aligned and
+    // padded by construction.  The RK register g is prefetched into L2.
+    auto issue_stage = [&](int item, const double* M, int st) {
+        if (tid != 0) return;
         const int cnt = item_cnt(item);
-#pragma unroll
-        for (int it = 0; it < NPTT; ++it) {
-            const int t = tid + it * BS;
-            if (t < cnt * n) {
-                const int slot = t / n, node = t - slot * n;
-                const long long off = slot_of(M, slot)->off;
-                const double* qe = P.q + off + node;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) cp_async8(&Q[(slot * NV + v) * n + node], qe + v * n);
-                if (need_g) {
-                    const double* ge = P.g + off + node;
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) cp_async8(&GB[(slot * NV + v) * n + node], ge + v * n);
-                }
-            }
+        double* Q = QST + st * QS;
+        double* Gs = GST + st * GS;
+        unsigned total = 0;
+        for (int s = 0; s < cnt; ++s) {
+            const long long off = slot_of(M, s)->off;
+            long long b = (off + NV * n + 1) & ~1LL;
+            if (b > P.qlen) b -= 2;
+            total += (unsigned)((b - (off & ~1LL)) * 8);
         }
-        if (surf) {
-            for (int t = tid; t < cnt * FS; t += BS) {
-                const int slot = t / FS;
-                const int r = t - slot * FS;
-                int f, pt;
-                face_of<S>(r, f, pt);
-                const FaceInfo* fi = face_of_m(M, slot, f);
-                const int nta = f < 2 ? n2 : n1;
-                const int ta = pt % nta, tb = pt / nta;
-                if (fi->kind == 0) {
-                    const double* src = P.q + fi->off + fi->base + ta * fi->sa + tb * fi->sb;
+        if (surf) total += (unsigned)(cnt * GSL * 8);
+        mbar_expect_tx(&mbar[st], total);
+        for (int s = 0; s < cnt; ++s) {
+            const long long off = slot_of(M, s)->off;
+            const long long a = off & ~1LL;
+            long long b = (off + NV * n + 1) & ~1LL;
+            const bool clip = b > P.qlen;
+            if (clip) b -= 2;
+            bulk_g2s(Q + s * SQ, P.q + a, (unsigned)((b - a) * 8), &mbar[st]);
+            if (clip) Q[s * SQ + (b - a)] = P.q[b];
+            if (need_g) bulk_prefetch_l2(P.g + a, (unsigned)((b - a) * 8));
+            if (surf) {
 #pragma unroll
-                    for (int v = 0; v < NV; ++v) cp_async8(&X[(slot * NV + v) * FS + r], src + (long long)v * fi->n);
-                } else if (fi->kind == 1) {
-                    const double* src = P.mortarG + fi->off + pt;
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) cp_async8(&X[(slot * NV + v) * FS + r], src + (long long)v * fi->n);
-                }
+                for (int f = 0; f < 6; ++f)
+                    bulk_g2s(Gs + s * GSL + S::gbase(f), P.mortarG + fofs_of(M, s, f), (unsigned)(S::gblk(f >> 1) * 8),
+                             &mbar[st]);
             }
         }
     };
 
     const int first = blockIdx.x;
     if (first >= nitems) return;
-    // prologue: meta of items 0 and 1 of this CTA, then data of item 0
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    // prologue: meta of items 0 and 1 of this CTA, then the stage of item 0
     issue_meta(first, 0);
     if (first + G < nitems) issue_meta(first + G, 1);
     asm volatile("cp.async.commit_group;\n" ::);
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncthreads();
-    issue_data(first, META, 0);
-    asm volatile("cp.async.commit_group;\n" ::);
+    issue_stage(first, META, 0);
 
     const double dt = P.mode ? *P.dt : 0.0;
     double lmax = 0.0;
     for (int k = 0;; ++k) {
         const int item = first + k * G;
         if (item >= nitems) break;
-        // data of item k (issued one iteration ago) and meta of item k+1 have landed
+        const int st = k & 1;
+        // meta of item k+1 (cp.async) and stage st of item k (bulk, mbarrier)
+        // have landed; every thread is done with item k-1, so stage st^1 and
+        // meta buffer (k+2)%3 are free
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        mbar_wait(&mbar[st], (k >> 1) & 1);
         __syncthreads();
         if (item + 2 * G < nitems) issue_meta(item + 2 * G, (k + 2) % 3);
-        if (item + G < nitems) issue_data(item + G, META + ((k + 1) % 3) * MW, (k + 1) & 1);
         asm volatile("cp.async.commit_group;\n" ::);
+        if (item + G < nitems) issue_stage(item + G, META + ((k + 1) % 3) * MW, st ^ 1);
 
         const double* M = META + (k % 3) * MW;
-        double* Q = STG + (k & 1) * STAGE;
-        double* GB = Q + NV * T;
-        double* X = GB + NV * T;
+        const double* Q = QST + st * QS;
+        const double* Gs = GST + st * GS;
         const int cnt = item_cnt(item);
         const int ntot = cnt * n;
 
-        // ---- 1/rho and p once per node; admissibility (reading A25) ----------
+        // ---- node phase: 1/rho, p, admissibility (A25), f_d -> F, lifting ------
+        // lifting of face point (G - f_d) 2/(h_d w_0) at the +-1 faces
+        // (strong form; GL end weight w_0 = 2/(N_d(N_d+1)))
+        double lift[NPTT][NV];
 #pragma unroll
         for (int it = 0; it < NPTT; ++it) {
             const int t = tid + it * BS;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) lift[it][v] = 0.0;
             if (t < ntot) {
                 const int slot = t / n, node = t - slot * n;
-                const double q0 = Q[(slot * NV) * n + node];
-                const double ir = 1.0 / q0;
-                const double m1 = Q[(slot * NV + 1) * n + node], m2 = Q[(slot * NV + 2) * n + node],
-                             m3 = Q[(slot * NV + 3) * n + node];
-                const double p = gm1 * (Q[(slot * NV + 4) * n + node] - 0.5 * ir * (m1 * m1 + m2 * m2 + m3 * m3));
-                IR[t] = ir;
-                PR[t] = p;
-                if (!(q0 > 0.0 && p > 0.0)) {
-                    if (atomicAdd(P.flag, 1) == 0) P.flag[1] = slot_of(M, slot)->e;
+                const SlotInfo* si = slot_of(M, slot);
+                const double* qe = Q + slot * SQ + (si->off & 1) + node;
+                double qv[NV];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) qv[v] = qe[v * n];
+                const double ir = rcp_nr(qv[0]);
+                const double p = gm1 * (qv[4] - 0.5 * ir * (qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]));
+                if (!(qv[0] > 0.0 && p > 0.0)) {
+                    if (atomicAdd(P.flag, 1) == 0) P.flag[1] = si->e;
+                }
+                const int i = node % n1, j = (node / n1) % n2, kk = node / (n1 * n2);
+                const double* Gsl = Gs + slot * GSL;
+                double* Fs = F + slot * 3 * NV * n + node;
+                double f[NV];
+                flux_axis<0>(qv, ir, p, f);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) Fs[v * n] = f[v];
+                if (surf && (i == 0 || i == N1)) {
+                    const double sc = (i ? 0.5 : -0.5) * (double)(N1 * (N1 + 1)) * si->sc[0];
+                    const double* g = Gsl + S::gbase(i ? 1 : 0) + j + n2 * kk;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) lift[it][v] = fma(sc, g[v * S::nf0] - f[v], lift[it][v]);
+                }
+                flux_axis<1>(qv, ir, p, f);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) Fs[(NV + v) * n] = f[v];
+                if (surf && (j == 0 || j == N2)) {
+                    const double sc = (j ? 0.5 : -0.5) * (double)(N2 * (N2 + 1)) * si->sc[1];
+                    const double* g = Gsl + S::gbase(j ? 3 : 2) + i + n1 * kk;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) lift[it][v] = fma(sc, g[v * S::nf1] - f[v], lift[it][v]);
+                }
+                flux_axis<2>(qv, ir, p, f);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) Fs[(2 * NV + v) * n] = f[v];
+                if (surf && (kk == 0 || kk == N3)) {
+                    const double sc = (kk ? 0.5 : -0.5) * (double)(N3 * (N3 + 1)) * si->sc[2];
+                    const double* g = Gsl + S::gbase(kk ? 5 : 4) + i + n1 * j;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) lift[it][v] = fma(sc, g[v * S::nf2] - f[v], lift[it][v]);
                 }
             }
         }
+        __syncthreads();
 
-        // ---- volume term, direction by direction --------------------------------
-        double acc[NPTT][NV];
-#pragma unroll
-        for (int it = 0; it < NPTT; ++it)
-#pragma unroll
-            for (int v = 0; v < NV; ++v) acc[it][v] = 0.0;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            __syncthreads();  // IR/PR ready (d = 0); previous derivatives consumed (d > 0)
-#pragma unroll
-            for (int it = 0; it < NPTT; ++it) {
-                const int t = tid + it * BS;
-                if (t < ntot) {
-                    const int slot = t / n, node = t - slot * n;
-                    double qv[NV], f[NV];
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) qv[v] = Q[(slot * NV + v) * n + node];
-                    if (d == 0) flux_axis<0>(qv, IR[t], PR[t], f);
-                    else if (d == 1) flux_axis<1>(qv, IR[t], PR[t], f);
-                    else flux_axis<2>(qv, IR[t], PR[t], f);
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) F[(slot * NV + v) * n + node] = f[v];
-                }
-            }
-            __syncthreads();
-            constexpr int Ld[3] = {n1, n2, n3};
-            const int nlines = n / Ld[d];
-            for (int task = tid; task < cnt * NV * nlines; task += BS) {
-                const int sv = task / nlines;  // slot * NV + v
-                const int l = task - sv * nlines;
-                if (d == 0) dline_inplace<n1>(F + sv * n + l * n1, 1);
-                else if (d == 1) dline_inplace<n2>(F + sv * n + (l % n1) + n1 * n2 * (l / n1), n1);
-                else dline_inplace<n3>(F + sv * n + l, n1 * n2);
-            }
-            __syncthreads();
-#pragma unroll
-            for (int it = 0; it < NPTT; ++it) {
-                const int t = tid + it * BS;
-                if (t < ntot) {
-                    const int slot = t / n, node = t - slot * n;
-                    const double sc = slot_of(M, slot)->sc[d];
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) acc[it][v] = fma(sc, F[(slot * NV + v) * n + node], acc[it][v]);
-                }
+        // ---- line phase: D^d along every line of every direction, in place -----
+        for (int u = tid; u < cnt * S::LT; u += BS) {
+            const int slot = u / S::LT;
+            int w = u - slot * S::LT;
+            double* Fs = F + slot * 3 * NV * n;
+            if (w < NV * L0) {
+                dline_inplace<n1>(Fs + w * n1, 1);  // lines of all 5 variables are back to back
+            } else if (w < NV * (L0 + L1)) {
+                w -= NV * L0;
+                const int v = w / L1, l = w - v * L1;
+                const int kk = l / n1, i = l - kk * n1;
+                dline_inplace<n2>(Fs + (NV + v) * n + i + n1 * n2 * kk, n1);
+            } else {
+                w -= NV * (L0 + L1);
+                dline_inplace<n3>(Fs + 2 * NV * n + (w / L2) * n + (w % L2), n1 * n2);
             }
         }
-
-        // ---- surface: lifting terms +-(G - f_own) 2/(h_d w_end) into X -------------
-        if (surf) {
-            for (int t = tid; t < cnt * FS; t += BS) {
-                const int slot = t / FS;
-                const int r = t - slot * FS;
-                int f, pt;
-                face_of<S>(r, f, pt);
-                const int d = f >> 1, s = f & 1;
-                const int nta = d == 0 ? n2 : n1;
-                const int ta = pt % nta, tb = pt / nta;
-                int i, j, kk, Nd;
-                if (d == 0) { i = s ? N1 : 0; j = ta; kk = tb; Nd = N1; }
-                else if (d == 1) { i = ta; j = s ? N2 : 0; kk = tb; Nd = N2; }
-                else { i = ta; j = tb; kk = s ? N3 : 0; Nd = N3; }
-                const int node = i + n1 * (j + n2 * kk);
-                double qo[NV], qx[NV], out[NV];
-#pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    qo[v] = Q[(slot * NV + v) * n + node];
-                    qx[v] = X[(slot * NV + v) * FS + r];
-                }
-                const double iro = IR[slot * n + node], po = PR[slot * n + node];
-                const int kind = face_of_m(M, slot, f)->kind;
-                if (d == 0) face_point<0>(qo, iro, po, qx, kind, s, P.ph, out);
-                else if (d == 1) face_point<1>(qo, iro, po, qx, kind, s, P.ph, out);
-                else face_point<2>(qo, iro, po, qx, kind, s, P.ph, out);
-                const double sc = (s ? 1.0 : -1.0) * slot_of(M, slot)->sc[d] / c_w[Nd][0];
-#pragma unroll
-                for (int v = 0; v < NV; ++v) X[(slot * NV + v) * FS + r] = sc * out[v];
-            }
-            __syncthreads();
-        }
+        __syncthreads();
 
         // ---- epilogue per node: Qdot, or the low-storage RK update (+ CFL rate) ----
 #pragma unroll
@@ -445,46 +480,41 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
             if (t >= ntot) continue;
             const int slot = t / n, node = t - slot * n;
             const SlotInfo* si = slot_of(M, slot);
-            if (surf) {
-                const int i = node % n1, j = (node / n1) % n2, kk = node / (n1 * n2);
-                const double* Xb = X + slot * NV * FS;
-                if (i == 0 || i == N1) {
-                    const int r = (i == 0 ? 0 : S::nf0) + j + n2 * kk;
+            const long long eoff = si->off;
+            double gr[NV];  // RK register (prefetched into L2 one item ahead)
+            if (need_g) {
+                const double* ge = P.g + eoff + node;
 #pragma unroll
-                    for (int v = 0; v < NV; ++v) acc[it][v] += Xb[v * FS + r];
-                }
-                if (j == 0 || j == N2) {
-                    const int r = 2 * S::nf0 + (j == 0 ? 0 : S::nf1) + i + n1 * kk;
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) acc[it][v] += Xb[v * FS + r];
-                }
-                if (kk == 0 || kk == N3) {
-                    const int r = 2 * (S::nf0 + S::nf1) + (kk == 0 ? 0 : S::nf2) + i + n1 * j;
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) acc[it][v] += Xb[v * FS + r];
-                }
+                for (int v = 0; v < NV; ++v) gr[v] = __ldcs(ge + v * n);
             }
-            double* o = P.out + si->off + node;
+            const double* Fs = F + slot * 3 * NV * n + node;
+            double acc[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+                acc[v] = fma(si->sc[0], Fs[v * n],
+                             fma(si->sc[1], Fs[(NV + v) * n], fma(si->sc[2], Fs[(2 * NV + v) * n], lift[it][v])));
+            double* o = P.out + eoff + node;
             if (P.mode == 0) {
 #pragma unroll
-                for (int v = 0; v < NV; ++v) o[v * n] = -acc[it][v];
+                for (int v = 0; v < NV; ++v) __stcs(o + v * n, -acc[v]);
             } else {
-                double* g = P.g + si->off + node;
+                const double* qe = Q + slot * SQ + (eoff & 1) + node;
+                double* g = P.g + eoff + node;
                 double qn[NV];
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
-                    const double gn = (need_g ? P.rkA * GB[(slot * NV + v) * n + node] : 0.0) - dt * acc[it][v];
-                    g[v * n] = gn;
-                    qn[v] = Q[(slot * NV + v) * n + node] + P.rkB * gn;
+                    const double gn = need_g ? fma(P.rkA, gr[v], -dt * acc[v]) : -dt * acc[v];
+                    __stcs(g + v * n, gn);
+                    qn[v] = fma(P.rkB, gn, qe[v * n]);
                     o[v * n] = qn[v];
                 }
                 if (P.lam_max) {  // CFL rate of q^{n+1} (reading A11), fused
-                    const double ir = 1.0 / qn[0];
+                    const double ir = rcp_nr(qn[0]);
                     const double p = gm1 * (qn[4] - 0.5 * ir * (qn[1] * qn[1] + qn[2] * qn[2] + qn[3] * qn[3]));
                     const double c = sqrt(P.gamma * p * ir);
-                    constexpr double L1 = (double)n1 * n1, L2 = (double)n2 * n2, L3 = (double)n3 * n3;
-                    const double lam = 0.5 * ((fabs(qn[1] * ir) + c) * L1 * si->sc[0] + (fabs(qn[2] * ir) + c) * L2 * si->sc[1] +
-                                              (fabs(qn[3] * ir) + c) * L3 * si->sc[2]);
+                    constexpr double C1 = (double)n1 * n1, C2 = (double)n2 * n2, C3 = (double)n3 * n3;
+                    const double lam = 0.5 * ((fabs(qn[1] * ir) + c) * C1 * si->sc[0] + (fabs(qn[2] * ir) + c) * C2 * si->sc[1] +
+                                              (fabs(qn[3] * ir) + c) * C3 * si->sc[2]);
                     lmax = fmax(lmax, lam);
                 }
             }
