@@ -89,6 +89,39 @@ __device__ __forceinline__ double sqrt_nr(double x)
 }
 
 // ---------------------------------------------------------------------------
+// L2 eviction-priority hints.  Within an RK stage the new state q' is read
+// again by the next stage's face and element kernels (keep: evict_last); the
+// state read by the element kernel and the face flux blocks are dead after it
+// (evict_first).  Pure hints: results do not depend on them.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ unsigned long long l2_policy_first()
+{
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ unsigned long long l2_policy_last()
+{
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ void st_hint(double* a, double v, unsigned long long pol)
+{
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;\n" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+
+__device__ __forceinline__ double ld_hint(const double* a, unsigned long long pol)
+{
+    double v;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;\n" : "=d"(v) : "l"(a), "l"(pol));
+    return v;
+}
+
+// ---------------------------------------------------------------------------
 // Pointwise physics
 // ---------------------------------------------------------------------------
 
@@ -283,7 +316,7 @@ struct FaceParams {
     double* G;
     const FaceItem* faces;
     const int* fpt;    // [nfaces+1] point prefix
-    const int* fcta;   // [nblk+1] face of the first point of each CTA
+    const int4* fcta;  // [npts] {L trace index, R trace index (-1: ghost), flux index, nL | nR<<10 | d<<20 | kind<<22 | (nf-1)<<24}
     int npts;
     PhysDev ph;
 };

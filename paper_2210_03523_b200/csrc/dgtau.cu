@@ -107,7 +107,7 @@ struct dg_ctx {
     long long* d_fofs_slot = nullptr;  // [elist][6] flux offset (into d_mortarG) of each face of each slot
     FaceItem* d_faces = nullptr;       // conforming + boundary faces (one Riemann flux per face point)
     int* d_fpt = nullptr;              // [nfaces+1] point prefix
-    int* d_fcta = nullptr;             // [nfblk+1] first face of each k_face CTA
+    int4* d_fcta = nullptr;            // [nface_pts] per face point: trace indices, flux index, packed sizes
     int nfaces = 0, nfblk = 0;
     long long nface_pts = 0;
     static constexpr int NSTREAMS = 8;  // concurrent bucket launches for mixed-order layouts
@@ -477,8 +477,10 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
             const int* N = &ctx->orders[3 * el];
             st[0] = 1; st[1] = N[0] + 1; st[2] = (N[0] + 1) * (N[1] + 1);
         };
-        for (int d = 0; d < 3; ++d)
-            for (int e = 0; e < E; ++e) {
+        // element-descending order: the faces of the elements the preceding
+        // element kernel wrote last (still in L2) come first
+        for (int e = E - 1; e >= 0; --e)
+            for (int d = 0; d < 3; ++d) {
                 const int* No = &ctx->orders[3 * e];
                 const int nf = (No[TA[d]] + 1) * (No[TB[d]] + 1);
                 for (int side = 0; side < 2; ++side) {  // side 1: + face of e (e = L); side 0: - face (BC only)
@@ -527,18 +529,29 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     ctx->nfaces = (int)faces.size();
     ctx->nface_pts = fpt.back();
     {
-        std::vector<int> fcta;
+        // k_face: one thread per face point with a precomputed record
+        // {L trace index, R trace index, flux index, packed nL | nR | d | kind | nf-1}
         const long long np = ctx->nface_pts;
         ctx->nfblk = (int)((np + FACE_BS - 1) / FACE_BS);
-        int f = 0;
-        for (int b = 0; b <= ctx->nfblk; ++b) {
-            const long long gp = std::min<long long>((long long)b * FACE_BS, np > 0 ? np - 1 : 0);
-            while (f + 1 < (int)faces.size() && fpt[f + 1] <= gp) ++f;
-            fcta.push_back(f);
+        if (ctx->off[E] >= (1LL << 31) || flen >= (1LL << 31))
+            return fail(ctx, DG_EINVAL, "set_orders: state or flux buffer beyond 2^31 doubles");
+        std::vector<int4> fcode((size_t)np);
+        for (size_t f = 0; f < faces.size(); ++f) {
+            const FaceItem& fi = faces[f];
+            for (int p = fpt[f]; p < fpt[f + 1]; ++p) {
+                const int pt = p - fpt[f], ta = pt % fi.nta, tb = pt / fi.nta;
+                int4 r;
+                r.x = fi.offL >= 0 ? (int)(fi.offL + fi.baseL + ta * fi.saL + tb * fi.sbL) : -1;
+                r.y = fi.offR >= 0 ? (int)(fi.offR + fi.baseR + ta * fi.saR + tb * fi.sbR) : -1;
+                r.z = (int)(fi.goff + pt);
+                r.w = (fi.offL >= 0 ? fi.nL : 0) | ((fi.offR >= 0 ? fi.nR : 0) << 10) | (fi.d << 20) | (fi.kind << 22) |
+                      ((fi.nf - 1) << 24);
+                fcode[p] = r;
+            }
         }
         CK(upload(ctx->d_faces, faces));
         CK(upload(ctx->d_fpt, fpt));
-        CK(upload(ctx->d_fcta, fcta));
+        CK(upload(ctx->d_fcta, fcode));
     }
     // per element-face source descriptors of the outer state (see FaceInfo)
     std::vector<FaceInfo> finfo(6LL * E);

@@ -51,10 +51,15 @@ struct Shape {
     static constexpr int CNT = cmax(1, cmin(MAXSLOTS, 384 / n));
     static constexpr int T = CNT * n;
     static constexpr int NPT = T > 384 ? 2 : 1;
-    static constexpr int BS = ((T + NPT - 1) / NPT + 31) / 32 * 32;
+    static constexpr int LT = NV * (n / n1 + n / n2 + n / n3);  // line tasks per element
+    // threads: enough for one round of nodes; raised (up to 384) when that
+    // saves a round of line tasks (N=6: 343 nodes, 735 line tasks -> 384)
+    static constexpr int BS0 = ((T + NPT - 1) / NPT + 31) / 32 * 32;
+    static constexpr int LR = (CNT * LT + BS0 - 1) / BS0;  // line rounds at BS0
+    static constexpr int BS1 = LR > 1 ? ((CNT * LT + LR - 2) / (LR - 1) + 31) / 32 * 32 : BS0;
+    static constexpr int BS = BS1 <= 384 && BS1 > BS0 ? BS1 : BS0;
     static constexpr int nf0 = n2 * n3, nf1 = n1 * n3, nf2 = n1 * n2;
     static constexpr int FS = 2 * (nf0 + nf1 + nf2);
-    static constexpr int LT = NV * (n / n1 + n / n2 + n / n3);  // line tasks per element
     // state slot: 5n doubles + 1 (8-byte shift of odd-offset elements), even
     static constexpr int SQ = (NV * n + 2) / 2 * 2;
     static constexpr int QS = CNT * SQ;          // one state stage
@@ -278,6 +283,17 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
 }
 
+// 1-D TMA bulk copy global -> shared with an L2 cache policy
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, unsigned long long* b,
+                                              unsigned long long pol)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
+        : "memory");
+}
+
 // 1-D TMA bulk copy global -> shared, completion counted on mbarrier b
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* b)
 {
@@ -308,6 +324,7 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
     const bool need_g = P.mode == 1 && P.rkA != 0.0;
     const double gm1 = P.ph.gm1;
     const int G = gridDim.x;
+    const unsigned long long pol_first = l2_policy_first(), pol_last = l2_policy_last();
 
     auto item_cnt = [&](int item) { return min(CNT, nelem - item * CNT); };
     auto slot_of = [&](const double* M, int s) { return reinterpret_cast<const SlotInfo*>(M + s * META_SLOT_W); };
@@ -349,14 +366,14 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
             long long b = (off + NV * n + 1) & ~1LL;
             const bool clip = b > P.qlen;
             if (clip) b -= 2;
-            bulk_g2s(Q + s * SQ, P.q + a, (unsigned)((b - a) * 8), &mbar[st]);
+            bulk_g2s_hint(Q + s * SQ, P.q + a, (unsigned)((b - a) * 8), &mbar[st], pol_first);
             if (clip) Q[s * SQ + (b - a)] = P.q[b];
             if (need_g) bulk_prefetch_l2(P.g + a, (unsigned)((b - a) * 8));
             if (surf) {
 #pragma unroll
                 for (int f = 0; f < 6; ++f)
-                    bulk_g2s(Gs + s * GSL + S::gbase(f), P.mortarG + fofs_of(M, s, f), (unsigned)(S::gblk(f >> 1) * 8),
-                             &mbar[st]);
+                    bulk_g2s_hint(Gs + s * GSL + S::gbase(f), P.mortarG + fofs_of(M, s, f),
+                                  (unsigned)(S::gblk(f >> 1) * 8), &mbar[st], pol_first);
             }
         }
     };
@@ -454,6 +471,20 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
         }
         __syncthreads();
 
+        // RK register g of this thread's nodes (L2-prefetched one item ahead),
+        // loaded here so the line phase hides the latency
+        double gr[NPTT][NV];
+#pragma unroll
+        for (int it = 0; it < NPTT; ++it) {
+            const int t = tid + it * BS;
+            if (need_g && t < ntot) {
+                const int slot = t / n, node = t - slot * n;
+                const double* ge = P.g + slot_of(M, slot)->off + node;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) gr[it][v] = __ldcs(ge + v * n);
+            }
+        }
+
         // ---- line phase: D^d along every line of every direction, in place -----
         for (int u = tid; u < cnt * S::LT; u += BS) {
             const int slot = u / S::LT;
@@ -481,12 +512,6 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
             const int slot = t / n, node = t - slot * n;
             const SlotInfo* si = slot_of(M, slot);
             const long long eoff = si->off;
-            double gr[NV];  // RK register (prefetched into L2 one item ahead)
-            if (need_g) {
-                const double* ge = P.g + eoff + node;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) gr[v] = __ldcs(ge + v * n);
-            }
             const double* Fs = F + slot * 3 * NV * n + node;
             double acc[NV];
 #pragma unroll
@@ -503,10 +528,10 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
                 double qn[NV];
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
-                    const double gn = need_g ? fma(P.rkA, gr[v], -dt * acc[v]) : -dt * acc[v];
+                    const double gn = need_g ? fma(P.rkA, gr[it][v], -dt * acc[v]) : -dt * acc[v];
                     __stcs(g + v * n, gn);
                     qn[v] = fma(P.rkB, gn, qe[v * n]);
-                    o[v * n] = qn[v];
+                    st_hint(o + v * n, qn[v], pol_last);
                 }
                 if (P.lam_max) {  // CFL rate of q^{n+1} (reading A11), fused
                     const double ir = rcp_nr(qn[0]);
