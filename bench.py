@@ -238,7 +238,7 @@ def run_gpu(args, rank, world):
         total_ms, rk_ms, tau_ms = t.tolist()
     evals_per_step = 3 * RK_PER_STEP + 1
     value = world * ndof * evals_per_step * args.steps / (total_ms * 1e-3) / 1e9
-    # roofline of the dominant kernel: fused residual + RK-stage (k_residual)
+    # roofline of the dominant kernel pair: one RK stage = k_face + k_res_t
     # algorithmic bytes per DOF: stage 1 reads q, writes g and q' (A_1 = 0: g
     # not read) = 120 B; stages 2-3 read q, g and write g, q' = 160 B.
     bytes_rk_step = ndof * (120 + 160 + 160)
@@ -383,7 +383,8 @@ def main():
         "phase_ms_per_step": {"rk3_x50": res["rk_ms"] / args.steps, "ref_rhs_plus_tau": res["tau_ms"] / args.steps,
                               "select_plus_transfer": res["adapt_ms"] / args.steps},
         "rhs_rk_gdof_s": world * res["ndof"] * 3 * res["rk_count"] / (res["rk_ms"] * 1e-3) / 1e9,
-        "roofline": {"kernel": "k_residual (fused residual + RK stage)", "bound": "hbm", "achieved": res["achieved"],
+        "roofline": {"kernel": "RK stage = k_face (face Riemann fluxes) + k_res_t (volume, lifting, fused RK update)",
+                     "bound": "hbm", "achieved": res["achieved"],
                      "peak": res["peak"], "unit": "GB/s", "frac": res["achieved"] / res["peak"],
                      "peak_source": res["peak_kind"], "traffic": load_traffic(),
                      "bytes_per_dof": "120 (stage 1) / 160 (stages 2,3)"},
