@@ -309,6 +309,13 @@ struct FaceItem {
     int nta, nf, d, kind;
 };
 
+// One mortar face for k_mortar3: state offsets of L (-xi_d side) and R, the
+// offsets of the two projected flux blocks, packed orders N1 | N2 << 4 | N3 << 8.
+struct MortarFace {
+    long long offL, offR, moL, moR;
+    int ordL, ordR, d, pad;
+};
+
 constexpr int FACE_BS = 128;
 
 struct FaceParams {

@@ -104,6 +104,7 @@ struct dg_ctx {
     res_occupancy rocc[NP][NP][NP] = {};
     int nsm = 148;
     FaceInfo* d_finfo_slot = nullptr;
+    MortarFace* d_mfaces = nullptr;    // mortar faces (k_mortar3)
     long long* d_fofs_slot = nullptr;  // [elist][6] flux offset (into d_mortarG) of each face of each slot
     FaceItem* d_faces = nullptr;       // conforming + boundary faces (one Riemann flux per face point)
     int* d_fpt = nullptr;              // [nfaces+1] point prefix
@@ -248,6 +249,14 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
                 dg_destroy(ctx);
                 return s;
             }
+        {
+            std::vector<double> mop;
+            mortar_build_ops(&t, mop);
+            if ((s = cuda_check(ctx, cudaMemcpyToSymbol(c_mop, mop.data(), sizeof(double) * mop.size()), "mortar operators")) != DG_OK) {
+                dg_destroy(ctx);
+                return s;
+            }
+        }
         if ((s = cuda_check(ctx, res_copy_constants(&t), "constants")) != DG_OK) {
             dg_destroy(ctx);
             return s;
@@ -313,6 +322,7 @@ void dg_destroy(dg_ctx* ctx)
     dfree(ctx->d_finfo);
     dfree(ctx->d_finfo_slot);
     dfree(ctx->d_fofs_slot);
+    dfree(ctx->d_mfaces);
     dfree(ctx->d_faces);
     dfree(ctx->d_fpt);
     dfree(ctx->d_fcta);
@@ -465,6 +475,23 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
         }
     ctx->nmortar = (int)mort.size();
     ctx->mortar_len = mlen;
+    {
+        std::vector<MortarFace> mf(mort.size());
+        for (size_t i = 0; i < mort.size(); ++i) {
+            const MortarItem& m = mort[i];
+            const int* a = &ctx->orders[3 * m.L];
+            const int* b = &ctx->orders[3 * m.R];
+            mf[i].offL = ctx->off[m.L];
+            mf[i].offR = ctx->off[m.R];
+            mf[i].moL = moff[6LL * m.L + 2 * m.d + 1];
+            mf[i].moR = moff[6LL * m.R + 2 * m.d];
+            mf[i].ordL = a[0] | (a[1] << 4) | (a[2] << 8);
+            mf[i].ordR = b[0] | (b[1] << 4) | (b[2] << 8);
+            mf[i].d = m.d;
+            mf[i].pad = 0;
+        }
+        CK(upload(ctx->d_mfaces, mf));
+    }
     // conforming faces and boundary faces of owned elements: the Riemann flux
     // of each face point is computed once (k_face) into the flux buffer after
     // the mortar blocks; fofs = flux offset of every element face.
@@ -773,7 +800,7 @@ static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, doub
         M.tab = ctx->d_tab;
         M.ph = phys_dev(ctx->prm);
         if (ctx->generic) k_mortar<<<ctx->nmortar, 128, 0, st>>>(M);
-        else k_mortar2<<<(ctx->nmortar + MW_FACES - 1) / MW_FACES, 32 * MW_FACES, 0, st>>>(M, ctx->nmortar);
+        else k_mortar3<<<std::min(ctx->nmortar, MT_MINB * ctx->nsm), MT_BS, 0, st>>>(M, ctx->d_mfaces, ctx->nmortar);
         ctx->launches++;
     }
     if (variant == DG_NONISOLATED && !ctx->generic && ctx->nface_pts > 0) {
