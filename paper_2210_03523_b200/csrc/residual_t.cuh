@@ -113,6 +113,51 @@ __device__ __forceinline__ void flux_normal(const double* q, double nx, double n
 //   out_{N-a} = sum_m P_am o_m - (sum_m Q_am e_m + Qm_a v_mid),
 //   out_mid = sum_m M_m o_m.
 template <int L>
+__device__ __forceinline__ void dline_inplace(double* Fl, int stride);
+
+// As dline_inplace, plus the strong-form lifting of the two end points of the
+// line (GL end weight w_0 = 2/(N(N+1))): the face fluxes
+// gm (at xi = -1) and gp (at xi = +1) enter as
+//   out_0 -= (N(N+1)/2) (gm - f_0),   out_N += (N(N+1)/2) (gp - f_N),
+// with f_0, f_N the line's own end values (the element's trace flux).
+template <int L>
+__device__ __forceinline__ void dline_lift(double* Fl, int stride, double gm, double gp)
+{
+    constexpr int N = L - 1, H = L / 2;
+    constexpr bool odd = (L & 1) != 0;
+    constexpr double CL = 0.5 * N * (N + 1);
+    double v[L];
+#pragma unroll
+    for (int m = 0; m < L; ++m) v[m] = Fl[m * stride];
+    const double l0 = -CL * (gm - v[0]), lN = CL * (gp - v[N]);
+    double o[H], ev[H];
+#pragma unroll
+    for (int m = 0; m < H; ++m) {
+        o[m] = v[m] - v[N - m];
+        ev[m] = v[m] + v[N - m];
+    }
+#pragma unroll
+    for (int a = 0; a < H; ++a) {
+        double p = c_EOP[N][a * H] * o[0];
+        double q = c_EOQ[N][a * H] * ev[0];
+#pragma unroll
+        for (int m = 1; m < H; ++m) {
+            p = fma(c_EOP[N][a * H + m], o[m], p);
+            q = fma(c_EOQ[N][a * H + m], ev[m], q);
+        }
+        if (odd) q = fma(c_EOQm[N][a], v[H], q);
+        Fl[a * stride] = a == 0 ? (p + q) + l0 : p + q;
+        Fl[(N - a) * stride] = a == 0 ? (p - q) + lN : p - q;
+    }
+    if (odd) {
+        double s = c_EOM[N][0] * o[0];
+#pragma unroll
+        for (int m = 1; m < H; ++m) s = fma(c_EOM[N][m], o[m], s);
+        Fl[H * stride] = s;
+    }
+}
+
+template <int L>
 __device__ __forceinline__ void dline_inplace(double* Fl, int stride)
 {
     constexpr int N = L - 1, H = L / 2;
@@ -415,15 +460,10 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
         const int cnt = item_cnt(item);
         const int ntot = cnt * n;
 
-        // ---- node phase: 1/rho, p, admissibility (A25), f_d -> F, lifting ------
-        // lifting of face point (G - f_d) 2/(h_d w_0) at the +-1 faces
-        // (strong form; GL end weight w_0 = 2/(N_d(N_d+1)))
-        double lift[NPTT][NV];
+        // ---- node phase: 1/rho, p, admissibility (A25), f_d -> F ---------------
 #pragma unroll
         for (int it = 0; it < NPTT; ++it) {
             const int t = tid + it * BS;
-#pragma unroll
-            for (int v = 0; v < NV; ++v) lift[it][v] = 0.0;
             if (t < ntot) {
                 const int slot = t / n, node = t - slot * n;
                 const SlotInfo* si = slot_of(M, slot);
@@ -436,37 +476,17 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
                 if (!(qv[0] > 0.0 && p > 0.0)) {
                     if (atomicAdd(P.flag, 1) == 0) P.flag[1] = si->e;
                 }
-                const int i = node % n1, j = (node / n1) % n2, kk = node / (n1 * n2);
-                const double* Gsl = Gs + slot * GSL;
                 double* Fs = F + slot * 3 * NV * n + node;
                 double f[NV];
                 flux_axis<0>(qv, ir, p, f);
 #pragma unroll
                 for (int v = 0; v < NV; ++v) Fs[v * n] = f[v];
-                if (surf && (i == 0 || i == N1)) {
-                    const double sc = (i ? 0.5 : -0.5) * (double)(N1 * (N1 + 1)) * si->sc[0];
-                    const double* g = Gsl + S::gbase(i ? 1 : 0) + j + n2 * kk;
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) lift[it][v] = fma(sc, g[v * S::nf0] - f[v], lift[it][v]);
-                }
                 flux_axis<1>(qv, ir, p, f);
 #pragma unroll
                 for (int v = 0; v < NV; ++v) Fs[(NV + v) * n] = f[v];
-                if (surf && (j == 0 || j == N2)) {
-                    const double sc = (j ? 0.5 : -0.5) * (double)(N2 * (N2 + 1)) * si->sc[1];
-                    const double* g = Gsl + S::gbase(j ? 3 : 2) + i + n1 * kk;
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) lift[it][v] = fma(sc, g[v * S::nf1] - f[v], lift[it][v]);
-                }
                 flux_axis<2>(qv, ir, p, f);
 #pragma unroll
                 for (int v = 0; v < NV; ++v) Fs[(2 * NV + v) * n] = f[v];
-                if (surf && (kk == 0 || kk == N3)) {
-                    const double sc = (kk ? 0.5 : -0.5) * (double)(N3 * (N3 + 1)) * si->sc[2];
-                    const double* g = Gsl + S::gbase(kk ? 5 : 4) + i + n1 * j;
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) lift[it][v] = fma(sc, g[v * S::nf2] - f[v], lift[it][v]);
-                }
             }
         }
         __syncthreads();
@@ -485,21 +505,31 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
             }
         }
 
-        // ---- line phase: D^d along every line of every direction, in place -----
+        // ---- line phase: D^d along every line of every direction, in place, ------
+        // with the lifting of the line's two face points (face point index = line index)
         for (int u = tid; u < cnt * S::LT; u += BS) {
             const int slot = u / S::LT;
             int w = u - slot * S::LT;
             double* Fs = F + slot * 3 * NV * n;
+            const double* Gsl = Gs + slot * GSL;
             if (w < NV * L0) {
-                dline_inplace<n1>(Fs + w * n1, 1);  // lines of all 5 variables are back to back
+                const int v = w / L0, l = w - v * L0;
+                double* Fl = Fs + w * n1;  // lines of all 5 variables are back to back
+                if (surf) dline_lift<n1>(Fl, 1, Gsl[S::gbase(0) + v * S::nf0 + l], Gsl[S::gbase(1) + v * S::nf0 + l]);
+                else dline_inplace<n1>(Fl, 1);
             } else if (w < NV * (L0 + L1)) {
                 w -= NV * L0;
                 const int v = w / L1, l = w - v * L1;
                 const int kk = l / n1, i = l - kk * n1;
-                dline_inplace<n2>(Fs + (NV + v) * n + i + n1 * n2 * kk, n1);
+                double* Fl = Fs + (NV + v) * n + i + n1 * n2 * kk;
+                if (surf) dline_lift<n2>(Fl, n1, Gsl[S::gbase(2) + v * S::nf1 + l], Gsl[S::gbase(3) + v * S::nf1 + l]);
+                else dline_inplace<n2>(Fl, n1);
             } else {
                 w -= NV * (L0 + L1);
-                dline_inplace<n3>(Fs + 2 * NV * n + (w / L2) * n + (w % L2), n1 * n2);
+                const int v = w / L2, l = w - v * L2;
+                double* Fl = Fs + (2 * NV + v) * n + l;
+                if (surf) dline_lift<n3>(Fl, n1 * n2, Gsl[S::gbase(4) + v * S::nf2 + l], Gsl[S::gbase(5) + v * S::nf2 + l]);
+                else dline_inplace<n3>(Fl, n1 * n2);
             }
         }
         __syncthreads();
@@ -516,8 +546,7 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
             double acc[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v)
-                acc[v] = fma(si->sc[0], Fs[v * n],
-                             fma(si->sc[1], Fs[(NV + v) * n], fma(si->sc[2], Fs[(2 * NV + v) * n], lift[it][v])));
+                acc[v] = fma(si->sc[0], Fs[v * n], fma(si->sc[1], Fs[(NV + v) * n], si->sc[2] * Fs[(2 * NV + v) * n]));
             double* o = P.out + eoff + node;
             if (P.mode == 0) {
 #pragma unroll
