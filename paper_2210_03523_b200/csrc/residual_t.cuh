@@ -430,37 +430,17 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
         mbar_init(&mbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    // prologue: meta of items 0 and 1 of this CTA, then the stage of item 0
-    issue_meta(first, 0);
-    if (first + G < nitems) issue_meta(first + G, 1);
-    asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    __syncthreads();
-    issue_stage(first, META, 0);
-
     const double dt = P.mode ? *P.dt : 0.0;
     double lmax = 0.0;
-    for (int k = 0;; ++k) {
-        const int item = first + k * G;
-        if (item >= nitems) break;
-        const int st = k & 1;
-        // meta of item k+1 (cp.async) and stage st of item k (bulk, mbarrier)
-        // have landed; every thread is done with item k-1, so stage st^1 and
-        // meta buffer (k+2)%3 are free
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-        mbar_wait(&mbar[st], (k >> 1) & 1);
-        __syncthreads();
-        if (item + 2 * G < nitems) issue_meta(item + 2 * G, (k + 2) % 3);
-        asm volatile("cp.async.commit_group;\n" ::);
-        if (item + G < nitems) issue_stage(item + G, META + ((k + 1) % 3) * MW, st ^ 1);
 
+    // node phase of local item k (state stage k&1, meta k%3): 1/rho, p,
+    // admissibility (A25), f_d -> F.  Thread t owns nodes t + it*BS; their
+    // states stay in registers (qreg) for the item's epilogue.
+    double qreg[NPTT][NV];
+    auto node_phase = [&](int k) {
         const double* M = META + (k % 3) * MW;
-        const double* Q = QST + st * QS;
-        const double* Gs = GST + st * GS;
-        const int cnt = item_cnt(item);
-        const int ntot = cnt * n;
-
-        // ---- node phase: 1/rho, p, admissibility (A25), f_d -> F ---------------
+        const double* Q = QST + (k & 1) * QS;
+        const int ntot = item_cnt(first + k * G) * n;
 #pragma unroll
         for (int it = 0; it < NPTT; ++it) {
             const int t = tid + it * BS;
@@ -468,7 +448,7 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
                 const int slot = t / n, node = t - slot * n;
                 const SlotInfo* si = slot_of(M, slot);
                 const double* qe = Q + slot * SQ + (si->off & 1) + node;
-                double qv[NV];
+                double* qv = qreg[it];
 #pragma unroll
                 for (int v = 0; v < NV; ++v) qv[v] = qe[v * n];
                 const double ir = rcp_nr(qv[0]);
@@ -489,24 +469,13 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
                 for (int v = 0; v < NV; ++v) Fs[(2 * NV + v) * n] = f[v];
             }
         }
-        __syncthreads();
-
-        // RK register g of this thread's nodes (L2-prefetched one item ahead),
-        // loaded here so the line phase hides the latency
-        double gr[NPTT][NV];
-#pragma unroll
-        for (int it = 0; it < NPTT; ++it) {
-            const int t = tid + it * BS;
-            if (need_g && t < ntot) {
-                const int slot = t / n, node = t - slot * n;
-                const double* ge = P.g + slot_of(M, slot)->off + node;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) gr[it][v] = __ldcs(ge + v * n);
-            }
-        }
-
-        // ---- line phase: D^d along every line of every direction, in place, ------
-        // with the lifting of the line's two face points (face point index = line index)
+    };
+    // line phase of local item k: D^d along every line of every direction, in
+    // place, with the lifting of the line's two face points (face point index
+    // = line index)
+    auto line_phase = [&](int k) {
+        const int cnt = item_cnt(first + k * G);
+        const double* Gs = GST + (k & 1) * GS;
         for (int u = tid; u < cnt * S::LT; u += BS) {
             const int slot = u / S::LT;
             int w = u - slot * S::LT;
@@ -532,47 +501,103 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
                 else dline_inplace<n3>(Fl, n1 * n2);
             }
         }
-        __syncthreads();
-
-        // ---- epilogue per node: Qdot, or the low-storage RK update (+ CFL rate) ----
+    };
+    // RK register g of local item k (L2-prefetched with its stage) into registers
+    double gr[NPTT][NV];
+    auto load_g = [&](int k) {
+        if (!need_g) return;
+        const double* M = META + (k % 3) * MW;
+        const int ntot = item_cnt(first + k * G) * n;
 #pragma unroll
         for (int it = 0; it < NPTT; ++it) {
             const int t = tid + it * BS;
-            if (t >= ntot) continue;
-            const int slot = t / n, node = t - slot * n;
-            const SlotInfo* si = slot_of(M, slot);
-            const long long eoff = si->off;
-            const double* Fs = F + slot * 3 * NV * n + node;
-            double acc[NV];
+            if (t < ntot) {
+                const int slot = t / n, node = t - slot * n;
+                const double* ge = P.g + slot_of(M, slot)->off + node;
 #pragma unroll
-            for (int v = 0; v < NV; ++v)
-                acc[v] = fma(si->sc[0], Fs[v * n], fma(si->sc[1], Fs[(NV + v) * n], si->sc[2] * Fs[(2 * NV + v) * n]));
-            double* o = P.out + eoff + node;
-            if (P.mode == 0) {
-#pragma unroll
-                for (int v = 0; v < NV; ++v) __stcs(o + v * n, -acc[v]);
-            } else {
-                const double* qe = Q + slot * SQ + (eoff & 1) + node;
-                double* g = P.g + eoff + node;
-                double qn[NV];
-#pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    const double gn = need_g ? fma(P.rkA, gr[it][v], -dt * acc[v]) : -dt * acc[v];
-                    __stcs(g + v * n, gn);
-                    qn[v] = fma(P.rkB, gn, qe[v * n]);
-                    st_hint(o + v * n, qn[v], pol_last);
-                }
-                if (P.lam_max) {  // CFL rate of q^{n+1} (reading A11), fused
-                    const double ir = rcp_nr(qn[0]);
-                    const double p = gm1 * (qn[4] - 0.5 * ir * (qn[1] * qn[1] + qn[2] * qn[2] + qn[3] * qn[3]));
-                    const double c = sqrt(P.gamma * p * ir);
-                    constexpr double C1 = (double)n1 * n1, C2 = (double)n2 * n2, C3 = (double)n3 * n3;
-                    const double lam = 0.5 * ((fabs(qn[1] * ir) + c) * C1 * si->sc[0] + (fabs(qn[2] * ir) + c) * C2 * si->sc[1] +
-                                              (fabs(qn[3] * ir) + c) * C3 * si->sc[2]);
-                    lmax = fmax(lmax, lam);
-                }
+                for (int v = 0; v < NV; ++v) gr[it][v] = __ldcs(ge + v * n);
             }
         }
+    };
+    // epilogue of local item k for node slot it of this thread: Qdot, or the
+    // low-storage RK update (+ fused CFL rate of the new state)
+    auto epilogue = [&](int k, int it) {
+        const double* M = META + (k % 3) * MW;
+        const int ntot = item_cnt(first + k * G) * n;
+        const int t = tid + it * BS;
+        if (t >= ntot) return;
+        const int slot = t / n, node = t - slot * n;
+        const SlotInfo* si = slot_of(M, slot);
+        const long long eoff = si->off;
+        const double* Fs = F + slot * 3 * NV * n + node;
+        double acc[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+            acc[v] = fma(si->sc[0], Fs[v * n], fma(si->sc[1], Fs[(NV + v) * n], si->sc[2] * Fs[(2 * NV + v) * n]));
+        double* o = P.out + eoff + node;
+        if (P.mode == 0) {
+#pragma unroll
+            for (int v = 0; v < NV; ++v) __stcs(o + v * n, -acc[v]);
+        } else {
+            double* g = P.g + eoff + node;
+            double qn[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const double gn = need_g ? fma(P.rkA, gr[it][v], -dt * acc[v]) : -dt * acc[v];
+                __stcs(g + v * n, gn);
+                qn[v] = fma(P.rkB, gn, qreg[it][v]);
+                st_hint(o + v * n, qn[v], pol_last);
+            }
+            if (P.lam_max) {  // CFL rate of q^{n+1} (reading A11), fused
+                const double ir = rcp_nr(qn[0]);
+                const double p = gm1 * (qn[4] - 0.5 * ir * (qn[1] * qn[1] + qn[2] * qn[2] + qn[3] * qn[3]));
+                const double c = sqrt(P.gamma * p * ir);
+                constexpr double C1 = (double)n1 * n1, C2 = (double)n2 * n2, C3 = (double)n3 * n3;
+                const double lam = 0.5 * ((fabs(qn[1] * ir) + c) * C1 * si->sc[0] + (fabs(qn[2] * ir) + c) * C2 * si->sc[1] +
+                                          (fabs(qn[3] * ir) + c) * C3 * si->sc[2]);
+                lmax = fmax(lmax, lam);
+            }
+        }
+    };
+
+    // Software pipeline over the CTA's items (local index k, item first + kG):
+    //   [epilogue(k) + node(k+1)] | barrier | lines(k+1) | barrier
+    // epilogue(k) and node(k+1) of the same thread touch the same F entries
+    // (read, then overwrite), so one F buffer serves both.  State/flux stage
+    // j&1 and meta buffer j%3 hold item j; the stage of item k+2 is issued as
+    // soon as item k is consumed.
+    issue_meta(first, 0);
+    if (first + G < nitems) issue_meta(first + G, 1);
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    issue_stage(first, META, 0);
+    if (first + G < nitems) issue_stage(first + G, META + MW, 1);
+    if (first + 2 * G < nitems) issue_meta(first + 2 * G, 2);
+    asm volatile("cp.async.commit_group;\n" ::);
+    mbar_wait(&mbar[0], 0);
+    node_phase(0);
+    __syncthreads();
+    load_g(0);
+    line_phase(0);
+    __syncthreads();
+    for (int k = 0;; ++k) {
+        const int item = first + k * G;
+        const bool has_next = item + G < nitems;
+        if (has_next) mbar_wait(&mbar[(k + 1) & 1], ((k + 1) >> 1) & 1);
+#pragma unroll
+        for (int it = 0; it < NPTT; ++it) epilogue(k, it);
+        if (has_next) node_phase(k + 1);
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");  // meta of item k+2
+        __syncthreads();
+        // item k consumed: its stage k&1 takes item k+2, meta buffer k%3 item k+3
+        if (item + 2 * G < nitems) issue_stage(item + 2 * G, META + ((k + 2) % 3) * MW, k & 1);
+        if (item + 3 * G < nitems) issue_meta(item + 3 * G, k % 3);
+        asm volatile("cp.async.commit_group;\n" ::);
+        if (!has_next) break;
+        load_g(k + 1);
+        line_phase(k + 1);
+        __syncthreads();
     }
     if (P.lam_max) {
         lmax = block_max(lmax, red);
