@@ -76,6 +76,9 @@ struct dg_ctx {
     FaceInfo* d_finfo = nullptr;
     SlotInfo* d_slots = nullptr;
     TauLevel* d_levels = nullptr;
+    TauGroup* d_tgroups = nullptr;  // k_tau5 (element, direction, level group) work list
+    int ntgroups = 0;
+    size_t tau5_smem = 0;
     int nlevels = 0;
     int max_level = 0;
     double* d_ref_scratch = nullptr;  // isolated fine residual for DG_REF_SAME
@@ -168,6 +171,12 @@ PhysDev phys_dev(const dg_params& p)
 }
 
 inline int npts(const int* N) { return (N[0] + 1) * (N[1] + 1) * (N[2] + 1); }
+
+inline bool getenv_flag(const char* name)
+{
+    const char* g = getenv(name);
+    return g && g[0] == '1';
+}
 
 dg_status check_stream_error(dg_ctx* ctx, const char* what)
 {
@@ -283,6 +292,8 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         cudaFuncSetAttribute(k_tau2, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
         cudaFuncSetAttribute(k_tau2, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
         cudaFuncSetAttribute(k_tau3, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(140 * 1024, lim));
+        cudaFuncSetAttribute(k_tau5, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 4096);  // 3.1 KB static
+        cudaFuncSetAttribute(k_tau5, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
         cudaFuncSetAttribute(k_tau3, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
         cudaFuncSetAttribute(k_transfer, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
         cudaFuncSetAttribute(k_metrics, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
@@ -328,6 +339,7 @@ void dg_destroy(dg_ctx* ctx)
     dfree(ctx->d_fcta);
     dfree(ctx->d_slots);
     dfree(ctx->d_levels);
+    dfree(ctx->d_tgroups);
     dfree(ctx->d_ref_scratch);
     dfree(ctx->d_tr_orders);
     dfree(ctx->d_geo);
@@ -642,6 +654,34 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
             }
     ctx->nlevels = (int)lv.size();
     CK(upload(ctx->d_levels, lv));
+    {   // k_tau5 work: (element, direction, coarse orders p0..p1) groups of <= TAU5_MAXN
+        // coarse nodes (a single larger level forms its own group), largest first
+        std::vector<TauGroup> tg;
+        std::vector<int> gsz;
+        int gmax = 0;
+        for (int e = 0; e < ctx->n_own; ++e)
+            for (int d = 0; d < 3; ++d) {
+                const int* No = &ctx->orders[3 * e];
+                const int nx = npts(No) / (No[d] + 1);
+                int p = 1;
+                while (p < No[d]) {
+                    int q = p, sz = (p + 1) * nx;
+                    while (q + 1 < No[d] && sz + (q + 2) * nx <= TAU5_MAXN) sz += (++q + 1) * nx;
+                    tg.push_back(TauGroup{e, d, p, q});
+                    gsz.push_back(sz);
+                    gmax = std::max(gmax, sz);
+                    p = q + 1;
+                }
+            }
+        std::vector<int> idx(tg.size());
+        for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int)i;
+        std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return gsz[a] > gsz[b]; });
+        std::vector<TauGroup> sorted(tg.size());
+        for (size_t i = 0; i < idx.size(); ++i) sorted[i] = tg[idx[i]];
+        ctx->ntgroups = (int)sorted.size();
+        ctx->tau5_smem = sizeof(double) * 4 * NV * (size_t)gmax;
+        CK(upload(ctx->d_tgroups, sorted));
+    }
     std::vector<int> ord_i(ctx->orders.begin(), ctx->orders.end());
     CK(upload(ctx->d_orders, ord_i));
     CK(upload(ctx->d_off, ctx->off));
@@ -1178,6 +1218,19 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
             C.formulation = o->formulation;
             C.ph = phys_dev(ctx->prm);
             k_tau_curved<<<ctx->nlevels, CBS, sm, st>>>(C);
+        } else if (ctx->ntgroups > 0 && !getenv_flag("DGTAU_TAU3")) {
+            Tau5Params P;
+            P.q = q_dev;
+            P.qref = ref;
+            P.tau = tau_dev;
+            P.orders = ctx->d_orders;
+            P.off = ctx->d_off;
+            P.hgeo = ctx->d_h;
+            P.groups = ctx->d_tgroups;
+            P.tab = ctx->d_tab;
+            P.formulation = o->formulation;
+            P.gm1 = ctx->prm.gamma - 1.0;
+            k_tau5<<<ctx->ntgroups, TAU5_BS, ctx->tau5_smem, st>>>(P);
         } else if (ctx->nlevels > 0) {
             Tau3Params P;
             P.q = q_dev;

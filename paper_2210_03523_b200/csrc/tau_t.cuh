@@ -426,3 +426,220 @@ __global__ void __launch_bounds__(128) k_tau_norm(const double* qref, double* ta
 }
 
 }  // namespace dgtau
+
+namespace dgtau {
+
+// ---------------------------------------------------------------------------
+// tau-estimation v5: one CTA per (element e, direction d, group of coarse
+// orders p0..p1) (reading A12).  All levels of the group are
+// evaluated at once, their coarse blocks (O_d = p+1) laid out back to back in
+// shared memory, so each of the four phases has a few hundred independent
+// tasks and the CTA needs only four barriers:
+//   (A) q_c = T_d^{N_d->p} q for every level: one (line across d, variable)
+//       task reads the fine line once (L1) and writes all levels' coarse lines;
+//   (B) f_0, f_1, f_2 of q_c at every coarse node (f_0 in place of q_c);
+//   (C) D^{O_d'} along every line of every axis of every level (even-odd,
+//       compile-time line lengths through a switch);
+//   (D) tau~ = T_d R + sum_d' (2/h_d') D f_d' per node and variable (T_d R from
+//       the fine R through L1), traditional * J w w w, max-reduced
+//       per level (shared atomicMax on the bits of non-negative doubles).
+// ---------------------------------------------------------------------------
+
+struct TauGroup {
+    int e, d, p0, p1;
+};
+
+constexpr int TAU5_BS = 256;
+constexpr int TAU5_MAXN = 384;  // coarse nodes per group (unless one level alone is larger)
+
+struct Tau5Params {
+    const double* q;
+    const double* qref;
+    double* tau;
+    const int* orders;
+    const long long* off;
+    const double* hgeo;
+    const TauGroup* groups;
+    const Tables* tab;
+    int formulation;
+    double gm1;
+};
+
+__global__ void __launch_bounds__(TAU5_BS) k_tau5(Tau5Params P)
+{
+    extern __shared__ __align__(16) double sm[];
+    __shared__ double Ts[NP * NP * NP / 2];      // T^{N_d -> p} of the group's levels, back to back
+    __shared__ int lbase[NP + 1], tbase[NP];      // node / table offsets per level of the group
+    __shared__ int abase[3][NP + 1];              // line-task prefix per axis over the levels
+    __shared__ unsigned long long lmaxb[NP];
+    const TauGroup tg = P.groups[blockIdx.x];
+    const int e = tg.e, d = tg.d, p0 = tg.p0, nlev = tg.p1 - tg.p0 + 1;
+    const int tid = threadIdx.x;
+    const int N1 = P.orders[3 * e], N2 = P.orders[3 * e + 1], N3 = P.orders[3 * e + 2];
+    const int n1 = N1 + 1, n2 = N2 + 1, n3 = N3 + 1;
+    const int n = n1 * n2 * n3;
+    const int Nd = d == 0 ? N1 : (d == 1 ? N2 : N3);
+    const int nd = Nd + 1;
+    const int nx = n / nd;  // coarse nodes per unit of O_d (cross-section of d)
+    const long long o = P.off[e];
+    if (tid == 0) {
+        int b = 0, tb = 0, c = 0, Lprev[3] = {1, 1, 1};
+        for (int li = 0; li < nlev; ++li) {
+            const int pc = p0 + li + 1;
+            lbase[li] = b;
+            tbase[li] = tb;
+            b += pc * nx;
+            tb += pc * nd;
+            const int L[3] = {d == 0 ? pc : n1, d == 1 ? pc : n2, d == 2 ? pc : n3};
+            for (int a = 0; a < 3; ++a) abase[a][li] = li == 0 ? 0 : abase[a][li - 1] + NV * ((pc - 1) * nx / Lprev[a]);
+            for (int a = 0; a < 3; ++a) Lprev[a] = L[a];
+        }
+        lbase[nlev] = b;
+        for (int a = 0; a < 3; ++a) abase[a][nlev] = abase[a][nlev - 1] + NV * ((p0 + nlev) * nx / Lprev[a]);
+        (void)c;
+    }
+    if (tid < nlev) lmaxb[tid] = 0ull;
+    __syncthreads();
+    const int ntot = lbase[nlev];
+    for (int t = tid; t < tbase[nlev - 1] + (p0 + nlev) * nd; t += TAU5_BS) {
+        int li = 0;
+        while (li + 1 < nlev && tbase[li + 1] <= t) ++li;
+        Ts[t] = P.tab->T[Nd][p0 + li][t - tbase[li]];
+    }
+    double* F0 = sm;               // coarse state, then f_0 and D^{O_0} f_0
+    double* F1 = F0 + NV * ntot;
+    double* F2 = F1 + NV * ntot;
+    double* RC = F2 + NV * ntot;   // T_d R of every level
+    const int strf = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
+    __syncthreads();
+    // (A) q_c = T_d q and T_d R along d for every level (reading A3); layout per
+    //     level: [v][coarse node of the level's (o1,o2,o3) block] at 5*lbase + v*nO
+    {
+        const float inv_n1 = 1.0f / (float)n1;
+        for (int task2 = tid; task2 < 2 * NV * nx; task2 += TAU5_BS) {
+            const bool isR = task2 >= NV * nx;
+            const int task = isR ? task2 - NV * nx : task2;
+            const double* qe = (isR ? P.qref : P.q) + o;
+            double* dstb = isR ? RC : F0;
+            const int v = var_of(task, nx), l = task - v * nx;
+            int bf, i = 0, k = 0;
+            if (d == 0) bf = l * nd;
+            else if (d == 1) { k = fdiv(l, inv_n1); i = l - k * n1; bf = i + n1 * nd * k; }
+            else bf = l;
+            double f[NP];
+#pragma unroll
+            for (int a = 0; a < NP; ++a) f[a] = a < nd ? __ldg(qe + v * n + bf + a * strf) : 0.0;
+            for (int li = 0; li < nlev; ++li) {
+                const int pc = p0 + li + 1, nO = pc * nx;
+                const int o1 = d == 0 ? pc : n1;
+                int bc, strc;
+                if (d == 0) { bc = l * pc; strc = 1; }
+                else if (d == 1) { bc = i + o1 * pc * k; strc = o1; }
+                else { bc = l; strc = n1 * n2; }
+                const double* T = Ts + tbase[li];
+                double* out = dstb + NV * lbase[li] + v * nO + bc;
+                for (int ic = 0; ic < pc; ++ic) {
+                    double s = 0.0;
+#pragma unroll
+                    for (int a = 0; a < NP; ++a)
+                        if (a < nd) s = fma(T[ic * nd + a], f[a], s);
+                    out[ic * strc] = s;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    // (B) the three Cartesian fluxes of every coarse node (f_0 in place of q_c)
+    for (int t = tid; t < ntot; t += TAU5_BS) {
+        int li = 0;
+        while (li + 1 < nlev && lbase[li + 1] <= t) ++li;
+        const int nO = lbase[li + 1] - lbase[li], r = t - lbase[li];
+        double* b0 = F0 + NV * lbase[li] + r;
+        double* b1 = F1 + NV * lbase[li] + r;
+        double* b2 = F2 + NV * lbase[li] + r;
+        double qv[NV], f[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) qv[v] = b0[v * nO];
+        const double ir = rcp_nr(qv[0]);
+        const double pr = P.gm1 * (qv[4] - 0.5 * ir * (qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]));
+        flux_axis<1>(qv, ir, pr, f);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) b1[v * nO] = f[v];
+        flux_axis<2>(qv, ir, pr, f);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) b2[v * nO] = f[v];
+        flux_axis<0>(qv, ir, pr, f);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) b0[v * nO] = f[v];
+    }
+    __syncthreads();
+    // (C) D^{O_a} along every line of every axis a of every level (one pass per
+    //     axis; a thread's tasks increase, so its level index only moves forward)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        double* Fa = a == 0 ? F0 : (a == 1 ? F1 : F2);
+        int li = 0;
+        for (int task = tid; task < abase[a][nlev]; task += TAU5_BS) {
+            while (abase[a][li + 1] <= task) ++li;
+            const int u = task - abase[a][li];
+            const int pc = p0 + li + 1, nO = pc * nx;
+            const int o1 = d == 0 ? pc : n1, o2 = d == 1 ? pc : n2, o3 = d == 2 ? pc : n3;
+            const int L = a == 0 ? o1 : (a == 1 ? o2 : o3);
+            const int nl = nO / L;
+            const int v = var_of(u, nl), l = u - v * nl;
+            int base, str;
+            if (a == 0) { base = l * L; str = 1; }
+            else if (a == 1) { const int kk = fdiv(l, 1.0f / (float)o1); base = (l - kk * o1) + o1 * L * kk; str = o1; }
+            else { base = l; str = o1 * o2; }
+            double* Fb = Fa + NV * lbase[li] + v * nO + base;
+            switch (L) {
+                case 2: dline_inplace<2>(Fb, str); break;
+                case 3: dline_inplace<3>(Fb, str); break;
+                case 4: dline_inplace<4>(Fb, str); break;
+                case 5: dline_inplace<5>(Fb, str); break;
+                case 6: dline_inplace<6>(Fb, str); break;
+                case 7: dline_inplace<7>(Fb, str); break;
+                case 8: dline_inplace<8>(Fb, str); break;
+                default: dline_inplace<9>(Fb, str); break;
+            }
+        }
+    }
+    __syncthreads();
+    // (D) tau~ = T_d R + sum_a (2/h_a) D f_a; traditional * J w w w
+    {
+        const double h0 = P.hgeo[3 * e], h1 = P.hgeo[3 * e + 1], h2 = P.hgeo[3 * e + 2];
+        const double sc0 = 2.0 / h0, sc1 = 2.0 / h1, sc2 = 2.0 / h2;
+        const double Jel = h0 * h1 * h2 / 8.0;
+        int lcur = -1;
+        double tmax = 0.0;
+        for (int t = tid; t < ntot; t += TAU5_BS) {
+            int li = 0;
+            while (li + 1 < nlev && lbase[li + 1] <= t) ++li;
+            if (li != lcur) {
+                if (lcur >= 0) atomicMax(&lmaxb[lcur], (unsigned long long)__double_as_longlong(tmax));
+                lcur = li;
+                tmax = 0.0;
+            }
+            const int pc = p0 + li + 1, nO = pc * nx, r = t - lbase[li];
+            const int o1 = d == 0 ? pc : n1, o2 = d == 1 ? pc : n2, o3 = d == 2 ? pc : n3;
+            const int kz = fdiv(r, 1.0f / (float)(o1 * o2)), rr = r - kz * o1 * o2, j = fdiv(rr, 1.0f / (float)o1),
+                      i = rr - j * o1;
+            double scale = 1.0;
+            if (P.formulation == 1) scale = Jel * c_w[o1 - 1][i] * c_w[o2 - 1][j] * c_w[o3 - 1][kz];
+            const double* rc = RC + NV * lbase[li] + r;
+            const double* f0 = F0 + NV * lbase[li] + r;
+            const double* f1 = F1 + NV * lbase[li] + r;
+            const double* f2 = F2 + NV * lbase[li] + r;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const double acc = fma(sc2, f2[v * nO], fma(sc1, f1[v * nO], fma(sc0, f0[v * nO], rc[v * nO])));
+                tmax = fmax(tmax, fabs(scale * acc));
+            }
+        }
+        if (lcur >= 0) atomicMax(&lmaxb[lcur], (unsigned long long)__double_as_longlong(tmax));
+    }
+    __syncthreads();
+    if (tid < nlev) P.tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV + p0 + tid] = __longlong_as_double((long long)lmaxb[tid]);
+}
+
+}  // namespace dgtau
