@@ -1285,6 +1285,10 @@ dg_status dg_select_orders(dg_ctx* ctx, const dg_adapt_policy* pol, const double
     // jump-condition fixpoint: Jacobi sweeps until no element changes
     int* a = ctx->d_sel;
     int* b = ctx->d_sel + 3LL * E;
+    if (ctx->n_own == E && E <= (1 << 18)) {  // one launch, no host round trips
+        k_jump_fix<<<1, JUMP_FIX_BS, 0, st>>>(ctx->d_nbr, a, b, E, pol->jump_rule == DG_JUMP_A ? 0 : 1, pol->Nmax, 64);
+        ctx->launches++;
+    } else
     for (int sweep = 0; sweep < 64; ++sweep) {
         CK(cudaMemsetAsync(ctx->d_flag + 2, 0, sizeof(int), st));
         if (ctx->n_own < E)

@@ -618,6 +618,45 @@ __global__ void k_jump(const int* nbr, const int* in, int* out, int E, int rule,
     }
 }
 
+// Jump-condition least fixpoint in ONE launch: a single CTA runs
+// the Jacobi sweeps of k_jump with a block barrier between sweeps until no
+// order changes; the result ends in `a`.  For local meshes without halo rows.
+constexpr int JUMP_FIX_BS = 1024;
+
+__global__ void __launch_bounds__(JUMP_FIX_BS) k_jump_fix(const int* nbr, int* a, int* b, int E, int rule, int Nmax,
+                                                          int maxsweeps)
+{
+    __shared__ int changed;
+    int* in = a;
+    int* out = b;
+    for (int sweep = 0; sweep < maxsweeps; ++sweep) {
+        if (threadIdx.x == 0) changed = 0;
+        __syncthreads();
+        for (int e = threadIdx.x; e < E; e += JUMP_FIX_BS)
+            for (int d = 0; d < 3; ++d) {
+                const int cur = in[3 * e + d];
+                int v = cur;
+                for (int f = 0; f < 6; ++f) {
+                    const int j = nbr[6 * e + f];
+                    if (j < 0) continue;
+                    const int x = in[3 * j + d];
+                    v = max(v, rule == 0 ? (2 * x) / 3 : x - 1);
+                }
+                v = max(cur, min(v, Nmax));
+                out[3 * e + d] = v;
+                if (v != cur) changed = 1;
+            }
+        __syncthreads();  // sweep complete and visible to the block
+        int* t = in;
+        in = out;
+        out = t;
+        if (!changed) break;
+        __syncthreads();  // everyone has read `changed` before it is reset
+    }
+    if (in != a)
+        for (int i = threadIdx.x; i < 3 * E; i += JUMP_FIX_BS) a[i] = in[i];
+}
+
 // ---------------------------------------------------------------------------
 // Transfer: q_new = T_z T_y T_x q_old per element.
 // ---------------------------------------------------------------------------
