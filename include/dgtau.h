@@ -122,7 +122,12 @@ dg_status dg_node_coords(dg_ctx* ctx, double* X_host);
 
 /* Qdot = -(M^N)^-1 F^N(q)  (eq DGMassMatrixRight).  variant
  * DG_NONISOLATED uses the numerical fluxes at faces (mortars between unequal
- * orders, reading A6); DG_ISOLATED uses the inner trace flux. */
+ * orders, reading A6); DG_ISOLATED uses the inner trace flux.
+ * The state pointer of the residual / RK calls must be 16-byte aligned (it is
+ * read with 1-D bulk copies; cudaMalloc and torch allocations are), else
+ * DG_EINVAL.  Non-isolated evaluations run k_mortar3 (mortar faces) and
+ * k_face (conforming and boundary faces: each face point's Riemann flux once)
+ * before the element kernels, all on `stream`. */
 dg_status dg_rhs_eval(dg_ctx* ctx, int variant, const double* q_dev, double* qdot_dev, void* stream);
 
 /* CFL time step (reading A11) from q, written to dt_dev[0]
