@@ -151,6 +151,16 @@ dg_status dg_rk_step(dg_ctx* ctx, double* q_in_dev, double* q_out_dev, double* g
 dg_status dg_rk_step_dt(dg_ctx* ctx, double* q_in_dev, double* q_out_dev, double* g_dev, const double* dt_dev,
                         double cfl, double* dt_next_dev, void* stream);
 
+/* nsteps Williamson RK3 steps with the CFL step of each new state
+ * fused into its last stage (reading A11): step s reads the state
+ * from (s even ? qa : qb) and dt from (s even ? dt_a : dt_b), writes the new
+ * state and the next dt into the other buffer of each pair, so after the call
+ * the state is in (nsteps even ? qa : qb) and the next dt in (nsteps even ?
+ * dt_a : dt_b).  Same kernels as nsteps dg_rk_step_dt calls, one host call.
+ * Stream-ordered, no host sync. */
+dg_status dg_rk_steps(dg_ctx* ctx, int nsteps, double* qa_dev, double* qb_dev, double* g_dev, double* dt_a_dev,
+                      double* dt_b_dev, double cfl, void* stream);
+
 /* One stage k in {0,1,2} of the Williamson RK3 step, for callers
  * that refresh halo states between stages: q_out = q_in + B_k g' with
  * g' = A_k g + dt Qdot(q_in) on owned elements.  If lam_accum_dev != NULL

@@ -39,7 +39,7 @@ EXPORTS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_upload", "dg_set
            "dg_node_coords", "dg_rhs_eval", "dg_compute_dt", "dg_rk_step", "dg_tau_estimate", "dg_select_orders",
            "dg_transfer", "dg_diagnostics", "dg_launch_count", "dg_rk_step_dt", "dg_set_owned", "dg_rk_stage",
            "dg_dt_accumulate", "dg_dt_finalize", "dg_select_local", "dg_jump_sweep", "dg_owned_state_len", "dg_gradient",
-           "dg_gradient_buffer", "dg_rhs_eval_flags"]
+           "dg_gradient_buffer", "dg_rhs_eval_flags", "dg_rk_steps"]
 
 
 def sources():
@@ -255,6 +255,13 @@ class Solver:
         self._check(self.L.dg_rk_step_dt(self.ctx, _ptr(q_in), _ptr(q_out), _ptr(g), _ptr(dt), C.c_double(cfl),
                                          _ptr(dt_next), _stream(stream)), "dg_rk_step_dt")
 
+    def rk_steps(self, nsteps, qa, qb, g, dt_a, dt_b, cfl, stream=None):
+        """nsteps RK3 steps ping-ponging (qa, qb) and (dt_a, dt_b) on the device
+        (dg_rk_steps); returns (state, next dt) tensors after the last step."""
+        self._check(self.L.dg_rk_steps(self.ctx, int(nsteps), _ptr(qa), _ptr(qb), _ptr(g), _ptr(dt_a), _ptr(dt_b),
+                                       C.c_double(cfl), _stream(stream)), "dg_rk_steps")
+        return (qa, dt_a) if nsteps % 2 == 0 else (qb, dt_b)
+
     # -- multi-rank pieces (see dist.py) ---------------------------------------
     def set_owned(self, n_owned):
         self._check(self.L.dg_set_owned(self.ctx, int(n_owned)), "dg_set_owned")
@@ -314,12 +321,19 @@ class Solver:
                                             _stream(stream)), "dg_select_orders")
         return out, margin
 
-    def transfer(self, new_orders, q_old, stream=None):
+    def transfer(self, new_orders, q_old, out=None, stream=None):
+        """State projected onto new_orders.  `out`: optional device
+        buffer of at least the new state length (reused, no allocation)."""
         import torch
 
         no = _np(new_orders, np.int32)
         n = int((5 * np.prod(no.astype(np.int64) + 1, axis=1)).sum())
-        q_new = torch.empty(n, dtype=torch.float64, device="cuda")
+        if out is not None:
+            if out.numel() < n:
+                raise DGError(f"transfer: out has {out.numel()} doubles, needs {n}")
+            q_new = out[:n]
+        else:
+            q_new = torch.empty(n, dtype=torch.float64, device="cuda")
         self._check(self.L.dg_transfer(self.ctx, no.ctypes.data_as(C.c_void_p), _ptr(q_old), _ptr(q_new),
                                        _stream(stream)), "dg_transfer")
         return q_new

@@ -316,7 +316,8 @@ struct MortarFace {
     int ordL, ordR, d, pad;
 };
 
-constexpr int FACE_BS = 128;
+constexpr int FACE_BS = 128;   // k_face threads per CTA
+constexpr int FACE_MINB = 5;   // k_face CTAs per SM (persistent grid)
 
 struct FaceParams {
     const double* q;

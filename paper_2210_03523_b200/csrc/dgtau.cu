@@ -852,7 +852,7 @@ static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, doub
         FP.fcta = ctx->d_fcta;
         FP.npts = (int)ctx->nface_pts;
         FP.ph = phys_dev(ctx->prm);
-        k_face<<<ctx->nfblk, FACE_BS, 0, st>>>(FP);
+        k_face<<<std::min(ctx->nfblk, FACE_MINB * ctx->nsm), FACE_BS, 0, st>>>(FP);
         ctx->launches++;
     }
     ResParams P;
@@ -1010,6 +1010,35 @@ dg_status dg_rk_step_dt(dg_ctx* ctx, double* q_in, double* q_out, double* g, con
     return check_stream_error(ctx, "k_dt_final launch");
 }
 
+dg_status dg_rk_steps(dg_ctx* ctx, int nsteps, double* qa, double* qb, double* g, double* dt_a, double* dt_b,
+                      double cfl, void* stream)
+{
+    if (!ctx || nsteps < 1 || !qa || !qb || !g || !dt_a || !dt_b || qa == qb || dt_a == dt_b || !(cfl > 0))
+        return DG_EINVAL;
+    if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "rk_steps: orders not set");
+    if (ctx->prm.physics == DG_NS && !ctx->curved) return fail(ctx, DG_EUNSUPPORTED, "rk_steps: NS needs the curved path");
+    static const double A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
+    static const double B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int s = 0; s < nsteps; ++s) {
+        double* q_in = (s & 1) ? qb : qa;
+        double* q_out = (s & 1) ? qa : qb;
+        const double* dt = (s & 1) ? dt_b : dt_a;
+        double* dt_next = (s & 1) ? dt_a : dt_b;
+        double* src[3] = {q_in, q_out, q_in};
+        double* dst[3] = {q_out, q_in, q_out};
+        for (int k = 0; k < 3; ++k) {
+            dg_status r = launch_residual(ctx, DG_NONISOLATED, src[k], dst[k], g, dt, A[k], B[k], 1, st,
+                                          k == 2 ? ctx->d_scratch + 4 : nullptr);
+            if (r != DG_OK) return r;
+        }
+        if (ctx->curved) k_dt_final2<<<1, 1, 0, st>>>(ctx->d_scratch + 4, cfl, cfl, dt_next);
+        else k_dt_final<<<1, 1, 0, st>>>(ctx->d_scratch + 4, cfl, dt_next);
+        ctx->launches++;
+    }
+    return check_stream_error(ctx, "k_dt_final launch");
+}
+
 dg_status dg_set_owned(dg_ctx* ctx, int n_owned)
 {
     if (!ctx) return DG_EINVAL;
@@ -1031,7 +1060,7 @@ dg_status dg_rk_stage(dg_ctx* ctx, int stage, const double* q_in, double* q_out,
     static const double A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
     static const double B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
     return launch_residual(ctx, DG_NONISOLATED, q_in, q_out, g, dt_dev, A[stage], B[stage], 1, (cudaStream_t)stream,
-                           lam_accum_dev, flags);
+                           lam_accum_dev, flags & DG_FLAG_GRADIENT_READY);
 }
 
 dg_status dg_gradient(dg_ctx* ctx, int variant, const double* q_dev, void* stream)
@@ -1083,7 +1112,7 @@ dg_status dg_rhs_eval_flags(dg_ctx* ctx, int variant, const double* q_dev, doubl
     if (!ctx || !q_dev || !qdot_dev) return DG_EINVAL;
     if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "rhs_eval: orders not set");
     return launch_residual(ctx, variant, q_dev, qdot_dev, nullptr, nullptr, 0.0, 0.0, 0, (cudaStream_t)stream, nullptr,
-                           flags);
+                           flags & DG_FLAG_GRADIENT_READY);
 }
 
 dg_status dg_dt_finalize(dg_ctx* ctx, unsigned long long* lam_accum_dev, double cfl, double* dt_dev, void* stream)

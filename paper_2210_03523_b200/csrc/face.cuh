@@ -74,37 +74,59 @@ __device__ __forceinline__ void roe_axis_q(int d, const double* qL, const double
 
 // One thread per face point; its record (one 16-byte load) gives the trace
 // positions of both sides in q, the flux position in G and the sizes.
-__global__ void __launch_bounds__(FACE_BS, 8) k_face(FaceParams P)
+// Grid-stride and software-pipelined: a thread computes point gp while the
+// traces of its next point (gp + stride) and the record of the one after are
+// in flight, so the dependent record -> trace loads never sit on the critical
+// path.
+__device__ __forceinline__ void face_load(const FaceParams& P, const int4& r, double* qL, double* qR,
+                                          unsigned long long pol)
 {
-    const int gp = blockIdx.x * FACE_BS + threadIdx.x;
-    if (gp >= P.npts) return;
-    const int4 r = __ldg(P.fcta + gp);
-    const unsigned long long pol_last = l2_policy_last();
-    const int nL = r.w & 1023, nR = (r.w >> 10) & 1023, d = (r.w >> 20) & 3, kind = (r.w >> 22) & 3;
-    const int nf = ((r.w >> 24) & 127) + 1;
-    double qL[NV], qR[NV];
+    const int nL = r.w & 1023, nR = (r.w >> 10) & 1023;
     if (r.x >= 0) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) qL[v] = ld_hint(P.q + r.x + v * nL, pol_last);
+        for (int v = 0; v < NV; ++v) qL[v] = ld_hint(P.q + r.x + v * nL, pol);
     }
     if (r.y >= 0) {
 #pragma unroll
-        for (int v = 0; v < NV; ++v) qR[v] = ld_hint(P.q + r.y + v * nR, pol_last);
+        for (int v = 0; v < NV; ++v) qR[v] = ld_hint(P.q + r.y + v * nR, pol);
     }
-    if (kind >= 2) {
-        if (r.x < 0) ghost_state(qR, kind == 2 ? -1 : -2, P.ph, qL);
-        else ghost_state(qL, kind == 2 ? -1 : -2, P.ph, qR);
-    }
-    double G[NV];
-    if (P.ph.flux == 1) {
-        const double nrm[3] = {d == 0 ? 1.0 : 0.0, d == 1 ? 1.0 : 0.0, d == 2 ? 1.0 : 0.0};
-        llf_flux(qL, qR, nrm, P.ph.gamma, G);
-    } else {
-        roe_axis_q(d, qL, qR, P.ph.gm1, G);
-    }
-    double* o = P.G + r.z;
+}
+
+__global__ void __launch_bounds__(FACE_BS, FACE_MINB) k_face(FaceParams P)
+{
+    const unsigned long long pol_last = l2_policy_last();
+    const int stride = gridDim.x * FACE_BS;
+    int gp = blockIdx.x * FACE_BS + threadIdx.x;
+    const int4 none = make_int4(-1, -1, 0, 0);
+    int4 r = gp < P.npts ? __ldg(P.fcta + gp) : none;
+    int4 rn = gp + stride < P.npts ? __ldg(P.fcta + gp + stride) : none;
+    double qL[NV], qR[NV];
+    face_load(P, r, qL, qR, pol_last);
+    for (; gp < P.npts; gp += stride) {
+        const int4 rnn = gp + 2 * stride < P.npts ? __ldg(P.fcta + gp + 2 * stride) : none;
+        double qLn[NV], qRn[NV];
+        face_load(P, rn, qLn, qRn, pol_last);  // traces of the next point
+        const int d = (r.w >> 20) & 3, kind = (r.w >> 22) & 3;
+        const int nf = ((r.w >> 24) & 127) + 1;
+        if (kind >= 2) {
+            if (r.x < 0) ghost_state(qR, kind == 2 ? -1 : -2, P.ph, qL);
+            else ghost_state(qL, kind == 2 ? -1 : -2, P.ph, qR);
+        }
+        double G[NV];
+        if (P.ph.flux == 1) {
+            const double nrm[3] = {d == 0 ? 1.0 : 0.0, d == 1 ? 1.0 : 0.0, d == 2 ? 1.0 : 0.0};
+            llf_flux(qL, qR, nrm, P.ph.gamma, G);
+        } else {
+            roe_axis_q(d, qL, qR, P.ph.gm1, G);
+        }
+        double* o = P.G + r.z;
 #pragma unroll
-    for (int v = 0; v < NV; ++v) st_hint(o + v * nf, G[v], pol_last);
+        for (int v = 0; v < NV; ++v) st_hint(o + v * nf, G[v], pol_last);
+        r = rn;
+        rn = rnn;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) { qL[v] = qLn[v]; qR[v] = qRn[v]; }
+    }
 }
 
 // ---------------------------------------------------------------------------

@@ -142,6 +142,34 @@ def test_rk3_fused_dt(dg, orc):
     assert abs(dts[0].item() - P.dt(orders, qo, 0.5)) <= 1e-14 * dts[0].item()
 
 
+@pytest.mark.parametrize("case", ["cfg1", "cfg3_subbox_mixed", "ragged_1to8", "single_element", "all_order8"])
+def test_rk_steps(dg, orc, case):
+    """dg_rk_steps (several RK3 steps in one call, dt ping-pong on the device)
+    gives the same states as stepping with dg_rk_step_dt and as the oracle."""
+    import torch
+
+    mesh, orders, kw = CASES[case]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, **kw)
+    nsteps = 3
+    dts = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in range(2)]
+    S.compute_dt(qd, 0.5, dts[0])
+    qa, qb, g = qd.clone(), torch.empty_like(qd), torch.empty_like(qd)
+    qs, dts_out = S.rk_steps(nsteps, qa, qb, g, dts[0], dts[1], 0.5)
+    ref_a, ref_b, g2 = qd.clone(), torch.empty_like(qd), torch.empty_like(qd)
+    rdt = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in range(2)]
+    S.compute_dt(ref_a, 0.5, rdt[0])
+    qo = q.copy()
+    for step in range(nsteps):
+        dto = P.dt(orders, qo, 0.5)
+        S.rk_step_dt(ref_a, ref_b, g2, rdt[step % 2], 0.5, rdt[(step + 1) % 2])
+        ref_a, ref_b = ref_b, ref_a
+        qo = P.rk3_step(orders, qo, dto)
+    a, b = qs.cpu().numpy(), ref_a.cpu().numpy()
+    assert np.abs(a - b).max() <= 1e-14 * np.abs(b).max()
+    assert abs(dts_out.item() - rdt[nsteps % 2].item()) <= 1e-14 * rdt[nsteps % 2].item()
+    assert rel_linf(a, qo, orders) < RES_TOL
+
+
 def test_rk3_mixed_orders(dg, orc):
     import torch
 

@@ -55,6 +55,8 @@ res["rhs_noniso_us"] = timeit(lambda: S.rhs_eval(q, r, variant=0))
 res["rhs_iso_us"] = timeit(lambda: S.rhs_eval(q, r, variant=1))
 res["rk_step_us"] = timeit(lambda: S.rk_step_dt(q, qb, g, dts[0], 0.5, dts[1]))
 res["tau_solver_us"] = timeit(lambda: S.tau_estimate(q, r), reps=max(3, a.reps // 4))
+res["rk_steps10_us"] = timeit(lambda: S.rk_steps(10, q, qb, g, dts[0], dts[1], 0.5), reps=max(3, a.reps // 4))
+res["gdofs_rk_stage_traces"] = 30 * ndof / res["rk_steps10_us"] / 1e3
 res["gdofs_rhs"] = ndof / res["rhs_noniso_us"] / 1e3
 res["gdofs_rk_stage"] = 3 * ndof / res["rk_step_us"] / 1e3
 res["tau_Melem_s"] = mesh.E / res["tau_solver_us"]
