@@ -488,7 +488,18 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
                 else dline_inplace<n1>(Fl, 1);
             } else if (w < NV * (L0 + L1)) {
                 w -= NV * L0;
-                const int v = w / L1, l = w - v * L1;
+                // for n1 >= 6 order (i, variable, k): consecutive threads then hit
+                // distinct shared-memory banks (the (i, k) order collides on
+                // i + k mod 16; bank simulation)
+                int v, l;
+                if (n1 >= 6) {
+                    const int kk = w / (NV * n1), r = w - kk * NV * n1;
+                    v = r / n1;
+                    l = (r - v * n1) + n1 * kk;
+                } else {
+                    v = w / L1;
+                    l = w - v * L1;
+                }
                 const int kk = l / n1, i = l - kk * n1;
                 double* Fl = Fs + (NV + v) * n + i + n1 * n2 * kk;
                 if (surf) dline_lift<n2>(Fl, n1, Gsl[S::gbase(2) + v * S::nf1 + l], Gsl[S::gbase(3) + v * S::nf1 + l]);
