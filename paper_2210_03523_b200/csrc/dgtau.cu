@@ -92,6 +92,8 @@ struct dg_ctx {
     double* d_met = nullptr;       // 10 per node
     double* d_grad = nullptr;      // 15 per node (NS)
     double* d_mortarGq = nullptr;  // 15 per mortar point (NS gradient mortars)
+    double* d_mgeo = nullptr;      // curved mortars: Ja at the mortar nodes (3 per point)
+    long long* d_mgoff = nullptr;  // [nmortar] offsets into d_mgeo
     long long met_len = 0, grad_len = 0, mq_len = 0;
     std::vector<long long> tr_off_host;
     long long ref_len = 0;
@@ -293,6 +295,7 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         cudaFuncSetAttribute(k_tau2, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
         cudaFuncSetAttribute(k_tau3, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(140 * 1024, lim));
         cudaFuncSetAttribute(k_tau5, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 4096);  // 3.1 KB static
+        cudaFuncSetAttribute(k_mortar_curved2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CM_SMEM);
         cudaFuncSetAttribute(k_tau5, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
         cudaFuncSetAttribute(k_tau3, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
         cudaFuncSetAttribute(k_transfer, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
@@ -346,6 +349,8 @@ void dg_destroy(dg_ctx* ctx)
     dfree(ctx->d_met);
     dfree(ctx->d_grad);
     dfree(ctx->d_mortarGq);
+    dfree(ctx->d_mgeo);
+    dfree(ctx->d_mgoff);
     dfree(ctx->d_tr_off);
     dfree(ctx->d_mortarG);
     dfree(ctx->d_scratch);
@@ -721,6 +726,34 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
         k_metrics<<<E, CBS, sizeof(double) * 16 * (size_t)ctx->maxn>>>(M);
         ctx->launches++;
         CK(cudaGetLastError());
+        // mortar metric at the mortar nodes, once per layout (k_mortar_curved2 reads it)
+        dfree(ctx->d_mgeo);
+        dfree(ctx->d_mgoff);
+        if (ctx->nmortar > 0) {
+            static const int TA[3] = {1, 0, 0}, TB[3] = {2, 2, 1};
+            std::vector<long long> mgoff(ctx->nmortar);
+            long long glen = 0;
+            for (int i = 0; i < ctx->nmortar; ++i) {
+                const MortarItem& m = mort[i];
+                const int* a = &ctx->orders[3 * m.L];
+                const int* b = &ctx->orders[3 * m.R];
+                const int M1 = std::max(a[TA[m.d]], b[TA[m.d]]), M2 = std::max(a[TB[m.d]], b[TB[m.d]]);
+                mgoff[i] = glen;
+                glen += 3LL * (M1 + 1) * (M2 + 1);
+            }
+            CK(upload(ctx->d_mgoff, mgoff));
+            CK(cudaMalloc(&ctx->d_mgeo, sizeof(double) * glen));
+            CMortarParams G{};
+            G.tdd = ctx->d_tdd;
+            G.orders = ctx->d_orders;
+            G.off = ctx->d_off;
+            G.items = ctx->d_mortar;
+            G.cm = curved_mesh(ctx);
+            G.tab = ctx->d_tab;
+            k_mortar_geom<<<ctx->nmortar, 128>>>(G, ctx->d_mgeo, ctx->d_mgoff);
+            ctx->launches++;
+            CK(cudaGetLastError());
+        }
         CK(cudaDeviceSynchronize());
     }
     ctx->have_orders = true;
@@ -800,7 +833,7 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
         if (mort) {
             M.mode = 1;
             M.mortarG = ctx->d_mortarGq;
-            k_mortar_curved<<<ctx->nmortar, 128, 0, st>>>(M);
+            k_mortar_curved2<<<ctx->nmortar, CM_BS, CM_SMEM, st>>>(M, ctx->d_mgeo, ctx->d_mgoff);
             ctx->launches++;
         }
         P.mode = 0;
@@ -812,7 +845,7 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
     if (mort) {
         M.mode = 0;
         M.mortarG = ctx->d_mortarG;
-        k_mortar_curved<<<ctx->nmortar, 128, 0, st>>>(M);
+        k_mortar_curved2<<<ctx->nmortar, CM_BS, CM_SMEM, st>>>(M, ctx->d_mgeo, ctx->d_mgoff);
         ctx->launches++;
     }
     P.mode = mode;
@@ -1094,7 +1127,7 @@ dg_status dg_gradient(dg_ctx* ctx, int variant, const double* q_dev, void* strea
         M.ph = phys_dev(ctx->prm);
         M.mode = 1;
         M.mortarG = ctx->d_mortarGq;
-        k_mortar_curved<<<ctx->nmortar, 128, 0, st>>>(M);
+        k_mortar_curved2<<<ctx->nmortar, CM_BS, CM_SMEM, st>>>(M, ctx->d_mgeo, ctx->d_mgoff);
         ctx->launches++;
     }
     P.mode = 0;

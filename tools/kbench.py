@@ -15,7 +15,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", default="cfg2")
 ap.add_argument("--reps", type=int, default=20)
 a = ap.parse_args()
-if a.cfg == "cfg2":
+if a.cfg in ("cfg4", "cfg5", "cfg5u"):
+    pass
+elif a.cfg == "cfg2":
     mesh = W.cube_mesh(16)
     orders = W.orders_uniform(mesh.E, 6)
     kw = dict(center=W.cfg2_center(), sigma=0.08)
@@ -28,9 +30,18 @@ else:
     mesh = W.cube_mesh(32)
     orders = W.orders_random(mesh.E, 2, 7, 3)
     kw = dict(sigma=0.1)
-S = dg.Solver(mesh)
-S.set_orders(orders)
-q = torch.from_numpy(W.pulse_state(S.node_coords(), orders, **kw)).cuda()
+if a.cfg in ("cfg4", "cfg5", "cfg5u"):  # Navier-Stokes on the curved O-grid (B:10-11)
+    spec = W.CONFIGS["cfg5" if a.cfg == "cfg5u" else a.cfg]
+    mesh = W.make_mesh(spec["mesh"])
+    orders = W.orders_uniform(mesh.E, (8, 8, 2)) if a.cfg == "cfg5u" else W.make_orders(spec["orders"], mesh.E)
+    nsp = W.ns_params()
+    S = dg.Solver(mesh, physics=dg.NS, mu=nsp["mu"], Pr=nsp["Pr"], qinf=nsp["qinf"])
+    S.set_orders(orders)
+    q = torch.from_numpy(W.freestream_noise_state(orders, (1.0, 1.0, 0.0, 0.0, nsp["p_inf"]), noise=1e-3, seed=4)).cuda()
+else:
+    S = dg.Solver(mesh)
+    S.set_orders(orders)
+    q = torch.from_numpy(W.pulse_state(S.node_coords(), orders, **kw)).cuda()
 qb, g, r = torch.empty_like(q), torch.empty_like(q), torch.empty_like(q)
 dts = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in range(2)]
 S.compute_dt(q, 0.5, dts[0])
