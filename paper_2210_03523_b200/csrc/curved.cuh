@@ -28,7 +28,7 @@
 
 namespace dgtau {
 
-constexpr int CBS = 256;  // threads per CTA of the curved kernels
+constexpr int CBS = 128;  // threads per CTA of the curved kernels (cfg5 elements: ~108 nodes)
 
 struct CurvedMesh {
     const double* geo;   // [E][3][ng] geometry nodes
@@ -232,9 +232,25 @@ __global__ void __launch_bounds__(CBS) k_metrics(MetParams P)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ double dsum(const double* Dd, int od, int a, const double* Fl, int stride)
 {
-    double s = 0.0;
-    for (int m = 0; m < od; ++m) s += Dd[a * od + m] * Fl[m * stride];
-    return s;
+    // Dd in shared memory (stage_D); independent partial sums for the FMA chain
+    double s0 = 0.0, s1 = 0.0;
+    const double* Dr = Dd + a * od;
+#pragma unroll
+    for (int m = 0; m < NP; m += 2) {
+        if (m < od) s0 = fma(Dr[m], Fl[m * stride], s0);
+        if (m + 1 < od) s1 = fma(Dr[m + 1], Fl[(m + 1) * stride], s1);
+    }
+    return s0 + s1;
+}
+
+// D^{o_d - 1} of the three directions into shared memory (Ds[d][a*o_d + m])
+__device__ __forceinline__ void stage_D(double (*Ds)[NP * NP], const Tables* tab, int o1, int o2, int o3)
+{
+    for (int t = threadIdx.x; t < 3 * NP * NP; t += blockDim.x) {
+        const int d = t / (NP * NP), r = t - d * (NP * NP);
+        const int od = d == 0 ? o1 : (d == 1 ? o2 : o3);
+        if (r < od * od) Ds[d][r] = tab->D[od - 1][r];
+    }
 }
 
 struct CurvedParams {
@@ -274,8 +290,10 @@ __device__ __forceinline__ int face_node(int d, int s, int pt, int n1, int n2, i
 __global__ void __launch_bounds__(CBS) k_grad(CurvedParams P)
 {
     extern __shared__ double sm[];
+    __shared__ double Ds[3][NP * NP];
     const int e = blockIdx.x;
     const int n1 = P.orders[3 * e] + 1, n2 = P.orders[3 * e + 1] + 1, n3 = P.orders[3 * e + 2] + 1;
+    stage_D(Ds, P.tab, n1, n2, n3);
     const int n = n1 * n2 * n3;
     const long long o = P.off[e];
     const double* M = P.met + 2 * o;
@@ -288,7 +306,7 @@ __global__ void __launch_bounds__(CBS) k_grad(CurvedParams P)
     for (int d = 0; d < 3; ++d) {
         const int od = d == 0 ? n1 : (d == 1 ? n2 : n3);
         const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
-        const double* Dd = P.tab->D[od - 1];
+        const double* Dd = Ds[d];
         for (int k = 0; k < 3; ++k) {
             for (int t = threadIdx.x; t < n; t += CBS) {
                 const double jak = __ldg(M + (3 * d + k) * n + t);
@@ -373,8 +391,10 @@ __global__ void __launch_bounds__(CBS) k_res_curved(CurvedParams P)
 {
     extern __shared__ double sm[];
     __shared__ double red[32];
+    __shared__ double Ds[3][NP * NP];
     const int e = blockIdx.x;
     const int n1 = P.orders[3 * e] + 1, n2 = P.orders[3 * e + 1] + 1, n3 = P.orders[3 * e + 2] + 1;
+    stage_D(Ds, P.tab, n1, n2, n3);
     const int n = n1 * n2 * n3;
     const long long o = P.off[e];
     const double* M = P.met + 2 * o;
@@ -391,7 +411,7 @@ __global__ void __launch_bounds__(CBS) k_res_curved(CurvedParams P)
     for (int d = 0; d < 3; ++d) {
         const int od = d == 0 ? n1 : (d == 1 ? n2 : n3);
         const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
-        const double* Dd = P.tab->D[od - 1];
+        const double* Dd = Ds[d];
         for (int t = threadIdx.x; t < n; t += CBS) {
             double qv[NV], gv[15], Fv[NV];
 #pragma unroll
@@ -690,7 +710,8 @@ __device__ __forceinline__ void cm_pass(const double* __restrict__ A, const doub
     }
 }
 
-__global__ void __launch_bounds__(CM_BS) k_mortar_curved2(CMortarParams P, const double* mgeo, const long long* mgoff)
+__global__ void __launch_bounds__(CM_BS, 4) k_mortar_curved2(CMortarParams P, const double* mgeo, const long long* mgoff,
+                                                         int nitems)
 {
     extern __shared__ __align__(16) double cm_sm[];
     // B0: traces, then mortar states, then projection pass A; B1: interpolation
@@ -699,7 +720,12 @@ __global__ void __launch_bounds__(CM_BS) k_mortar_curved2(CMortarParams P, const
     double (*B0)[CM_NC][81] = reinterpret_cast<double (*)[CM_NC][81]>(cm_sm);
     double (*B1)[CM_NC][81] = reinterpret_cast<double (*)[CM_NC][81]>(cm_sm + 2 * CM_NC * 81);
     double (*OP)[81] = reinterpret_cast<double (*)[81]>(cm_sm + 4 * CM_NC * 81);
-    const MortarItem it = P.items[blockIdx.x];
+    const int t = threadIdx.x;
+    // padding values only ever meet zero operator entries: finite once is enough
+    for (int w = t; w < 2 * CM_NC * 81; w += CM_BS) { (&B0[0][0][0])[w] = 0.0; (&B1[0][0][0])[w] = 0.0; }
+    for (int fid = blockIdx.x; fid < nitems; fid += gridDim.x) {
+    __syncthreads();  // previous face fully consumed
+    const MortarItem it = P.items[fid];
     const int d = it.d;
     const int ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
     int NL[3], NR[3];
@@ -710,8 +736,6 @@ __global__ void __launch_bounds__(CM_BS) k_mortar_curved2(CMortarParams P, const
     const bool ns = P.ph.physics == 1;
     const int nin = (P.mode == 0 && ns) ? CM_NC : NV;  // components interpolated per side
     const int nout = P.mode == 0 ? NV : 15;            // components projected back
-    const int t = threadIdx.x;
-    for (int w = t; w < 2 * CM_NC * 81; w += CM_BS) { (&B0[0][0][0])[w] = 0.0; (&B1[0][0][0])[w] = 0.0; }
     for (int w = t; w < 8 * 81; w += CM_BS) {
         const int k = w / 81, r = w - k * 81, row = r / 9, col = r - row * 9;
         const int* NS = (k & 2) ? NR : NL;
@@ -746,16 +770,10 @@ __global__ void __launch_bounds__(CM_BS) k_mortar_curved2(CMortarParams P, const
         cm_pass(OP[2 * side], &B0[side][0][0], &B1[side][0][0], m1, NS[tb] + 1, true, nin, t);
     }
     __syncthreads();
-    for (int side = 0; side < 2; ++side) {
-        for (int w = t; w < nin * 81; w += CM_BS) (&B0[side][0][0])[w] = 0.0;
-    }
-    __syncthreads();
     for (int side = 0; side < 2; ++side) cm_pass(OP[2 * side + 1], &B1[side][0][0], &B0[side][0][0], m2, m1, false, nin, t);
     __syncthreads();
     // flux at the mortar points -> B1[0] (nout components)
-    const double* Jg = mgeo + mgoff[blockIdx.x];
-    for (int w = t; w < nout * 81; w += CM_BS) (&B1[0][0][0])[w] = 0.0;
-    __syncthreads();
+    const double* Jg = mgeo + mgoff[fid];
     if (t < nm) {
         const int i = t % m1, j = t / m1, pidx = j * 9 + i;
         double qL[NV], qR[NV];
@@ -791,12 +809,6 @@ __global__ void __launch_bounds__(CM_BS) k_mortar_curved2(CMortarParams P, const
     // exact L2 projection back: along a (B1[0] -> B0[side]), then along b -> global
     for (int side = 0; side < 2; ++side) {
         const int* NS = side ? NR : NL;
-        for (int w = t; w < nout * 81; w += CM_BS) (&B0[side][0][0])[w] = 0.0;
-        (void)NS;
-    }
-    __syncthreads();
-    for (int side = 0; side < 2; ++side) {
-        const int* NS = side ? NR : NL;
         cm_pass(OP[4 + 2 * side], &B1[0][0][0], &B0[side][0][0], NS[ta] + 1, m2, true, nout, t);
     }
     __syncthreads();
@@ -818,6 +830,7 @@ __global__ void __launch_bounds__(CM_BS) k_mortar_curved2(CMortarParams P, const
                 dst[(long long)c * nsd + a + s1 * bb] = s;
             }
         }
+    }
     }
 }
 
@@ -989,6 +1002,8 @@ __global__ void __launch_bounds__(CBS) k_tau_curved(CTauParams P)
     const int o1 = d == 0 ? p + 1 : n1, o2 = d == 1 ? p + 1 : n2, o3 = d == 2 ? p + 1 : n3;
     const int nO = o1 * o2 * o3;
     const bool ns = P.ph.physics == 1;
+    __shared__ double Ds[3][NP * NP];
+    stage_D(Ds, P.tab, o1, o2, o3);
     double* Mc = sm;              // 10 nO metrics
     double* Qc = Mc + 10 * nO;    // 5 nO
     double* Rc = Qc + NV * nO;    // 5 nO
@@ -1023,7 +1038,7 @@ __global__ void __launch_bounds__(CBS) k_tau_curved(CTauParams P)
         for (int dd = 0; dd < 3; ++dd) {
             const int od = dd == 0 ? o1 : (dd == 1 ? o2 : o3);
             const int str = dd == 0 ? 1 : (dd == 1 ? o1 : o1 * o2);
-            const double* Dd = P.tab->D[od - 1];
+            const double* Dd = Ds[dd];
             for (int k = 0; k < 3; ++k) {
                 for (int t = threadIdx.x; t < nO; t += CBS)
                     for (int v = 0; v < NV; ++v) F[v * nO + t] = Mc[(3 * dd + k) * nO + t] * Qc[v * nO + t];
@@ -1047,7 +1062,7 @@ __global__ void __launch_bounds__(CBS) k_tau_curved(CTauParams P)
     for (int dd = 0; dd < 3; ++dd) {
         const int od = dd == 0 ? o1 : (dd == 1 ? o2 : o3);
         const int str = dd == 0 ? 1 : (dd == 1 ? o1 : o1 * o2);
-        const double* Dd = P.tab->D[od - 1];
+        const double* Dd = Ds[dd];
         for (int t = threadIdx.x; t < nO; t += CBS) {
             double qv[NV], gv[15], Fv[NV];
             for (int v = 0; v < NV; ++v) qv[v] = Qc[v * nO + t];

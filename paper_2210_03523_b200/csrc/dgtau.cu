@@ -299,11 +299,12 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         cudaFuncSetAttribute(k_tau5, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
         cudaFuncSetAttribute(k_tau3, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
         cudaFuncSetAttribute(k_transfer, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
-        cudaFuncSetAttribute(k_metrics, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-        cudaFuncSetAttribute(k_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-        cudaFuncSetAttribute(k_res_curved, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-        cudaFuncSetAttribute(k_tau_curved, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
-        ctx->smem_limit = lim;
+        const int limc = optin - 8192;  // curved kernels: up to ~6 KB static (staged D, reductions)
+        cudaFuncSetAttribute(k_metrics, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
+        cudaFuncSetAttribute(k_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
+        cudaFuncSetAttribute(k_res_curved, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
+        cudaFuncSetAttribute(k_tau_curved, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
+        ctx->smem_limit = limc;
         cudaError_t e = cudaGetLastError();  // attribute errors are fatal here, not stale later
         if (e != cudaSuccess) {
             s = cuda_check(ctx, e, "cudaFuncSetAttribute");
@@ -833,7 +834,7 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
         if (mort) {
             M.mode = 1;
             M.mortarG = ctx->d_mortarGq;
-            k_mortar_curved2<<<ctx->nmortar, CM_BS, CM_SMEM, st>>>(M, ctx->d_mgeo, ctx->d_mgoff);
+            k_mortar_curved2<<<std::min(ctx->nmortar, 4 * ctx->nsm), CM_BS, CM_SMEM, st>>>(M, ctx->d_mgeo, ctx->d_mgoff, ctx->nmortar);
             ctx->launches++;
         }
         P.mode = 0;
@@ -845,7 +846,7 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
     if (mort) {
         M.mode = 0;
         M.mortarG = ctx->d_mortarG;
-        k_mortar_curved2<<<ctx->nmortar, CM_BS, CM_SMEM, st>>>(M, ctx->d_mgeo, ctx->d_mgoff);
+        k_mortar_curved2<<<std::min(ctx->nmortar, 4 * ctx->nsm), CM_BS, CM_SMEM, st>>>(M, ctx->d_mgeo, ctx->d_mgoff, ctx->nmortar);
         ctx->launches++;
     }
     P.mode = mode;
@@ -1127,7 +1128,7 @@ dg_status dg_gradient(dg_ctx* ctx, int variant, const double* q_dev, void* strea
         M.ph = phys_dev(ctx->prm);
         M.mode = 1;
         M.mortarG = ctx->d_mortarGq;
-        k_mortar_curved2<<<ctx->nmortar, CM_BS, CM_SMEM, st>>>(M, ctx->d_mgeo, ctx->d_mgoff);
+        k_mortar_curved2<<<std::min(ctx->nmortar, 4 * ctx->nsm), CM_BS, CM_SMEM, st>>>(M, ctx->d_mgeo, ctx->d_mgoff, ctx->nmortar);
         ctx->launches++;
     }
     P.mode = 0;
