@@ -29,6 +29,9 @@ def ogrid_case(name):
     elif name == "cfg4_adapted":  # after static adaptation: mixed orders in [4,8] (mortars)
         mesh = W.ogrid_mesh(6, 12, 2, ratio=1.1 ** 8, g_eta=4)
         orders = W.orders_random(mesh.E, 4, 7, 41)
+    elif name == "cfg4_full":  # BASELINE cfg4 [B:10] at full size: 48 x 64 x 1, g=4, N=4
+        mesh = W.make_mesh(W.CONFIGS["cfg4"]["mesh"])
+        orders = W.orders_uniform(mesh.E, 4)
     elif name == "cfg5_subbox":  # cfg5 structure: g=2, Nx,Ny ~ U{2..8}, Nz = 2
         mesh = W.ogrid_mesh(6, 16, 4, ratio=1.1 ** 4, g_eta=2)
         orders = W.orders_random(mesh.E, (2, 2, 2), (8, 8, 2), 5)
@@ -55,7 +58,7 @@ def test_node_coords_match(dg, orc):
     assert np.abs(S.node_coords() - P.node_coords(orders)).max() < 1e-13 * 20
 
 
-@pytest.mark.parametrize("name", ["cfg4_small", "cfg4_adapted", "cfg5_subbox"])
+@pytest.mark.parametrize("name", ["cfg4_small", "cfg4_adapted", "cfg5_subbox", "cfg4_full"])
 @pytest.mark.parametrize("physics", ["ns", "euler"])
 @pytest.mark.parametrize("variant", [0, 1])
 def test_curved_rhs_parity(dg, orc, name, physics, variant):
@@ -115,7 +118,7 @@ def test_curved_conservation_periodic_ns(dg, orc):
     assert np.all(np.abs(sums) < 1e-13 * ab)
 
 
-@pytest.mark.parametrize("name", ["cfg4_small", "cfg5_subbox"])
+@pytest.mark.parametrize("name", ["cfg4_small", "cfg5_subbox", "cfg4_full"])
 def test_curved_rk_dt(dg, orc, name):
     import torch
 
@@ -133,7 +136,7 @@ def test_curved_rk_dt(dg, orc, name):
     assert rel_linf(qa.cpu().numpy(), qo, orders) < RES_TOL
 
 
-@pytest.mark.parametrize("name", ["cfg4_small", "cfg5_subbox"])
+@pytest.mark.parametrize("name", ["cfg4_small", "cfg5_subbox", "cfg4_full"])
 @pytest.mark.parametrize("ref", ["solver", "same"])
 @pytest.mark.parametrize("form", [0, 1])
 def test_curved_tau_parity(dg, orc, name, ref, form):

@@ -38,12 +38,23 @@ def per_var(a, orders):
     return [np.concatenate(x) for x in out]
 
 
-def rel_linf(gpu, orc, orders):
-    """max over variables of ||gpu_v - orc_v||_inf / ||orc_v||_inf."""
+# free-stream scales s_v of the SURVEY 8(c) parity criterion for the Euler
+# pulse (rho = 1, p = 1): (rho, rho c x 3, p / (gamma - 1))
+EULER_PULSE_SCALES = (1.0, 1.4 ** 0.5, 1.4 ** 0.5, 1.4 ** 0.5, 2.5)
+
+
+def rel_linf(gpu, orc, orders, floor=None):
+    """max over variables of ||gpu_v - orc_v||_inf / max(||orc_v||_inf, floor_v).
+    floor = free-stream scales s_v (SURVEY 8(c) parity criteria): rounding in
+    the residual scales with the flux magnitudes times (2/h) N^2, not with the
+    residual itself, so on fine meshes a variable whose residual is small
+    against its flux is compared on the flux scale."""
     g, o = per_var(gpu, orders), per_var(orc, orders)
     worst = 0.0
     for v in range(5):
         den = np.abs(o[v]).max()
+        if floor is not None:
+            den = max(den, floor[v])
         num = np.abs(g[v] - o[v]).max()
         worst = max(worst, num / den if den > 0 else num)
     return worst
@@ -301,3 +312,32 @@ def test_dynamic_adaptation_cycle_cfg2_like(dg, orc):
         orders = sel_o
         S.set_orders(orders)
         assert rel_linf(qd.cpu().numpy(), qo, orders) < RES_TOL
+
+
+def test_full_size_cfg3(dg, orc):
+    """BASELINE cfg3 [B:9] at full size (32^3 elements, orders U{2..7}: ~97 %
+    mortar faces): residual, two RK3 steps in the bench's launch configuration
+    (dg_rk_steps, fused dt) and the SOLVER-reference tau-estimate against the
+    oracle, element by element."""
+    import torch
+
+    mesh = W.cube_mesh(32)
+    orders = W.orders_random(mesh.E, 2, 7, 3)
+    P, S, q, qd = setup(dg, orc, mesh, orders, sigma=0.1)
+    r = S.rhs_eval(qd).cpu().numpy()
+    ro = P.rhs(orders, q)
+    # N up to 7 at h = 1/32: corner-node lifting amplifies rounding by
+    # (2/h) N(N+1)/2 ~ 1800 in BOTH implementations (strong vs weak form);
+    # the absolute differences are ~2e-11 against energy fluxes ~3.5
+    assert rel_linf(r, ro, orders, floor=EULER_PULSE_SCALES) < RES_TOL
+    to = P.tau_estimate(orders, q, ro)
+    tg = S.tau_estimate(qd, torch.from_numpy(r).cuda()).cpu().numpy()
+    assert tau_rel(tg, to) < TAU_TOL
+    dts = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in range(2)]
+    S.compute_dt(qd, 0.5, dts[0])
+    qa, qb, g = qd.clone(), torch.empty_like(qd), torch.empty_like(qd)
+    qs, _ = S.rk_steps(2, qa, qb, g, dts[0], dts[1], 0.5)
+    qo = q.copy()
+    for _ in range(2):
+        qo = P.rk3_step(orders, qo, P.dt(orders, qo, 0.5))
+    assert rel_linf(qs.cpu().numpy(), qo, orders, floor=EULER_PULSE_SCALES) < RES_TOL
