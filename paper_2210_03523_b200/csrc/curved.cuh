@@ -387,7 +387,7 @@ __device__ __forceinline__ void load_grad(const double* base, int stride, double
     for (int c = 0; c < 15; ++c) g[c] = __ldg(base + (long long)c * stride);
 }
 
-__global__ void __launch_bounds__(CBS) k_res_curved(CurvedParams P)
+__global__ void __launch_bounds__(CBS, 4) k_res_curved(CurvedParams P)
 {
     extern __shared__ double sm[];
     __shared__ double red[32];
