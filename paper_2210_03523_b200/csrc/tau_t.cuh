@@ -465,7 +465,52 @@ struct Tau5Params {
     double gm1;
 };
 
-__global__ void __launch_bounds__(TAU5_BS) k_tau5(Tau5Params P)
+// (A) of k_tau5 for a compile-time fine line length ND along d: one (field,
+// variable, line) task reads the fine line once and writes the coarse lines of
+// every level of the group.
+template <int ND>
+__device__ __forceinline__ void tau5_interp(const Tau5Params& P, long long o, int n, int n1, int n2, int d, int nx,
+                                            int nlev, int p0, int strf, const int* lbase, const int* tbase,
+                                            const double* Ts, double* F0, double* RC)
+{
+    const float inv_n1 = 1.0f / (float)n1;
+    for (int task2 = threadIdx.x; task2 < 2 * NV * nx; task2 += TAU5_BS) {
+        const bool isR = task2 >= NV * nx;
+        const int task = isR ? task2 - NV * nx : task2;
+        const double* qe = (isR ? P.qref : P.q) + o;
+        double* dstb = isR ? RC : F0;
+        const int v = var_of(task, nx), l = task - v * nx;
+        int bf, i = 0, k = 0;
+        if (d == 0) bf = l * ND;
+        else if (d == 1) { k = fdiv(l, inv_n1); i = l - k * n1; bf = i + n1 * ND * k; }
+        else bf = l;
+        double f[ND];
+#pragma unroll
+        for (int a = 0; a < ND; ++a) f[a] = __ldg(qe + v * n + bf + a * strf);
+        for (int li = 0; li < nlev; ++li) {
+            const int pc = p0 + li + 1, nO = pc * nx;
+            const int o1 = d == 0 ? pc : n1;
+            int bc, strc;
+            if (d == 0) { bc = l * pc; strc = 1; }
+            else if (d == 1) { bc = i + o1 * pc * k; strc = o1; }
+            else { bc = l; strc = n1 * n2; }
+            const double* T = Ts + tbase[li];
+            double* out = dstb + NV * lbase[li] + v * nO + bc;
+            for (int ic = 0; ic < pc; ++ic) {
+                const double* Tr = T + ic * ND;
+                double s0 = Tr[0] * f[0], s1 = 0.0;
+#pragma unroll
+                for (int a = 1; a < ND; ++a) {
+                    if (a & 1) s1 = fma(Tr[a], f[a], s1);
+                    else s0 = fma(Tr[a], f[a], s0);
+                }
+                out[ic * strc] = s0 + s1;
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(TAU5_BS, 3) k_tau5(Tau5Params P)
 {
     extern __shared__ __align__(16) double sm[];
     __shared__ double Ts[NP * NP * NP / 2];      // T^{N_d -> p} of the group's levels, back to back
@@ -514,39 +559,14 @@ __global__ void __launch_bounds__(TAU5_BS) k_tau5(Tau5Params P)
     __syncthreads();
     // (A) q_c = T_d q and T_d R along d for every level (reading A3); layout per
     //     level: [v][coarse node of the level's (o1,o2,o3) block] at 5*lbase + v*nO
-    {
-        const float inv_n1 = 1.0f / (float)n1;
-        for (int task2 = tid; task2 < 2 * NV * nx; task2 += TAU5_BS) {
-            const bool isR = task2 >= NV * nx;
-            const int task = isR ? task2 - NV * nx : task2;
-            const double* qe = (isR ? P.qref : P.q) + o;
-            double* dstb = isR ? RC : F0;
-            const int v = var_of(task, nx), l = task - v * nx;
-            int bf, i = 0, k = 0;
-            if (d == 0) bf = l * nd;
-            else if (d == 1) { k = fdiv(l, inv_n1); i = l - k * n1; bf = i + n1 * nd * k; }
-            else bf = l;
-            double f[NP];
-#pragma unroll
-            for (int a = 0; a < NP; ++a) f[a] = a < nd ? __ldg(qe + v * n + bf + a * strf) : 0.0;
-            for (int li = 0; li < nlev; ++li) {
-                const int pc = p0 + li + 1, nO = pc * nx;
-                const int o1 = d == 0 ? pc : n1;
-                int bc, strc;
-                if (d == 0) { bc = l * pc; strc = 1; }
-                else if (d == 1) { bc = i + o1 * pc * k; strc = o1; }
-                else { bc = l; strc = n1 * n2; }
-                const double* T = Ts + tbase[li];
-                double* out = dstb + NV * lbase[li] + v * nO + bc;
-                for (int ic = 0; ic < pc; ++ic) {
-                    double s = 0.0;
-#pragma unroll
-                    for (int a = 0; a < NP; ++a)
-                        if (a < nd) s = fma(T[ic * nd + a], f[a], s);
-                    out[ic * strc] = s;
-                }
-            }
-        }
+    switch (nd) {
+        case 3: tau5_interp<3>(P, o, n, n1, n2, d, nx, nlev, p0, strf, lbase, tbase, Ts, F0, RC); break;
+        case 4: tau5_interp<4>(P, o, n, n1, n2, d, nx, nlev, p0, strf, lbase, tbase, Ts, F0, RC); break;
+        case 5: tau5_interp<5>(P, o, n, n1, n2, d, nx, nlev, p0, strf, lbase, tbase, Ts, F0, RC); break;
+        case 6: tau5_interp<6>(P, o, n, n1, n2, d, nx, nlev, p0, strf, lbase, tbase, Ts, F0, RC); break;
+        case 7: tau5_interp<7>(P, o, n, n1, n2, d, nx, nlev, p0, strf, lbase, tbase, Ts, F0, RC); break;
+        case 8: tau5_interp<8>(P, o, n, n1, n2, d, nx, nlev, p0, strf, lbase, tbase, Ts, F0, RC); break;
+        default: tau5_interp<9>(P, o, n, n1, n2, d, nx, nlev, p0, strf, lbase, tbase, Ts, F0, RC); break;
     }
     __syncthreads();
     // (B) the three Cartesian fluxes of every coarse node (f_0 in place of q_c)
