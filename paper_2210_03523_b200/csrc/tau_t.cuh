@@ -527,21 +527,13 @@ __global__ void __launch_bounds__(TAU5_BS, 3) k_tau5(Tau5Params P)
     const int nd = Nd + 1;
     const int nx = n / nd;  // coarse nodes per unit of O_d (cross-section of d)
     const long long o = P.off[e];
-    if (tid == 0) {
-        int b = 0, tb = 0, c = 0, Lprev[3] = {1, 1, 1};
-        for (int li = 0; li < nlev; ++li) {
-            const int pc = p0 + li + 1;
-            lbase[li] = b;
-            tbase[li] = tb;
-            b += pc * nx;
-            tb += pc * nd;
-            const int L[3] = {d == 0 ? pc : n1, d == 1 ? pc : n2, d == 2 ? pc : n3};
-            for (int a = 0; a < 3; ++a) abase[a][li] = li == 0 ? 0 : abase[a][li - 1] + NV * ((pc - 1) * nx / Lprev[a]);
-            for (int a = 0; a < 3; ++a) Lprev[a] = L[a];
-        }
-        lbase[nlev] = b;
-        for (int a = 0; a < 3; ++a) abase[a][nlev] = abase[a][nlev - 1] + NV * ((p0 + nlev) * nx / Lprev[a]);
-        (void)c;
+    if (tid <= nlev) {  // closed forms: S(li) = sum_{j<li} (p0 + j + 1)
+        const int li = tid, Sl = li * (p0 + 1) + li * (li - 1) / 2;
+        lbase[li] = nx * Sl;
+        if (li < nlev) tbase[li] = nd * Sl;
+        const int na[3] = {n1, n2, n3};
+#pragma unroll
+        for (int a = 0; a < 3; ++a) abase[a][li] = a == d ? NV * nx * li : NV * (nx / na[a]) * Sl;
     }
     if (tid < nlev) lmaxb[tid] = 0ull;
     __syncthreads();
