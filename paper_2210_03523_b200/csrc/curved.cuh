@@ -298,8 +298,8 @@ __global__ void __launch_bounds__(CBS) k_grad(CurvedParams P)
     const long long o = P.off[e];
     const double* M = P.met + 2 * o;
     double* Q = sm;          // 5n
-    double* F = Q + NV * n;  // 5n
-    double* GA = F + NV * n; // 15n
+    double* F = Q + NV * n;  // 15n: (Ja^d)_k q_v, k = 0..2
+    double* GA = F + 15 * n; // 15n
     for (int t = threadIdx.x; t < NV * n; t += CBS) Q[t] = P.q[o + t];
     for (int t = threadIdx.x; t < 15 * n; t += CBS) GA[t] = 0.0;
     __syncthreads();
@@ -307,23 +307,24 @@ __global__ void __launch_bounds__(CBS) k_grad(CurvedParams P)
         const int od = d == 0 ? n1 : (d == 1 ? n2 : n3);
         const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
         const double* Dd = Ds[d];
-        for (int k = 0; k < 3; ++k) {
-            for (int t = threadIdx.x; t < n; t += CBS) {
+        for (int t = threadIdx.x; t < n; t += CBS) {  // all three k at once (one barrier per direction)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
                 const double jak = __ldg(M + (3 * d + k) * n + t);
 #pragma unroll
-                for (int v = 0; v < NV; ++v) F[v * n + t] = jak * Q[v * n + t];
+                for (int v = 0; v < NV; ++v) F[(k * NV + v) * n + t] = jak * Q[v * n + t];
             }
-            __syncthreads();
-            for (int t = threadIdx.x; t < n; t += CBS) {
-                int ijk[3];
-                node_ijk(t, n1, n2, ijk[0], ijk[1], ijk[2]);
-                const int a = d == 0 ? ijk[0] : (d == 1 ? ijk[1] : ijk[2]);
-                const int base = t - a * stride;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) GA[(k * NV + v) * n + t] += dsum(Dd, od, a, F + v * n + base, stride);
-            }
-            __syncthreads();
         }
+        __syncthreads();
+        for (int t = threadIdx.x; t < n; t += CBS) {
+            int ijk[3];
+            node_ijk(t, n1, n2, ijk[0], ijk[1], ijk[2]);
+            const int a = d == 0 ? ijk[0] : (d == 1 ? ijk[1] : ijk[2]);
+            const int base = t - a * stride;
+#pragma unroll
+            for (int c = 0; c < 15; ++c) GA[c * n + t] += dsum(Dd, od, a, F + c * n + base, stride);
+        }
+        __syncthreads();
         // lifting on the two faces normal to d: (qhat Ja_f - q_own Ja_own)/w
         const int nf = face_nodes(d, n1, n2, n3);
         for (int task = threadIdx.x; task < 2 * nf; task += CBS) {

@@ -840,7 +840,7 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
         P.mode = 0;
         P.out = ctx->d_grad;
         P.mortarG = ctx->d_mortarGq;
-        k_grad<<<ctx->n_own, CBS, sizeof(double) * 25 * (size_t)ctx->maxn, st>>>(P);
+        k_grad<<<ctx->n_own, CBS, sizeof(double) * 35 * (size_t)ctx->maxn, st>>>(P);
         ctx->launches++;
     }
     if (mort) {
@@ -1134,7 +1134,7 @@ dg_status dg_gradient(dg_ctx* ctx, int variant, const double* q_dev, void* strea
     P.mode = 0;
     P.out = ctx->d_grad;
     P.mortarG = ctx->d_mortarGq;
-    k_grad<<<ctx->n_own, CBS, sizeof(double) * 25 * (size_t)ctx->maxn, st>>>(P);
+    k_grad<<<ctx->n_own, CBS, sizeof(double) * 35 * (size_t)ctx->maxn, st>>>(P);
     ctx->launches++;
     return check_stream_error(ctx, "k_grad launch");
 }
