@@ -99,7 +99,7 @@ struct dg_ctx {
     long long ref_len = 0;
     double* d_mortarG = nullptr;
     unsigned long long* d_scratch = nullptr;  // [8]
-    int* d_flag = nullptr;                    // [4]
+    int* d_flag = nullptr;                    // [8]: [0..1] admissibility, [2] jump, [3] diag, [4] mortar queue
     int* d_sel = nullptr;                     // [2][E][3]
     double* d_margin = nullptr;               // [E]
     double* d_sums = nullptr;                 // [5]
@@ -242,8 +242,8 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         (s = cuda_check(ctx, cudaMemcpy(ctx->d_tab, &t, sizeof(Tables), cudaMemcpyHostToDevice), "tables")) != DG_OK ||
         (s = cuda_check(ctx, cudaMalloc(&ctx->d_scratch, 8 * sizeof(unsigned long long)), "scratch")) != DG_OK ||
         (s = cuda_check(ctx, cudaMemset(ctx->d_scratch, 0, 8 * sizeof(unsigned long long)), "scratch")) != DG_OK ||
-        (s = cuda_check(ctx, cudaMalloc(&ctx->d_flag, 4 * sizeof(int)), "flag")) != DG_OK ||
-        (s = cuda_check(ctx, cudaMemset(ctx->d_flag, 0, 4 * sizeof(int)), "flag")) != DG_OK ||
+        (s = cuda_check(ctx, cudaMalloc(&ctx->d_flag, 8 * sizeof(int)), "flag")) != DG_OK ||
+        (s = cuda_check(ctx, cudaMemset(ctx->d_flag, 0, 8 * sizeof(int)), "flag")) != DG_OK ||
         (s = cuda_check(ctx, cudaMalloc(&ctx->d_sums, 8 * sizeof(double)), "sums")) != DG_OK ||
         (s = cuda_check(ctx, cudaMalloc(&ctx->d_tdd, sizeof(TablesDD)), "dd tables")) != DG_OK ||
         (s = cuda_check(ctx, cudaMemcpy(ctx->d_tdd, &host_tables_dd(), sizeof(TablesDD), cudaMemcpyHostToDevice),
@@ -874,7 +874,11 @@ static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, doub
         M.tab = ctx->d_tab;
         M.ph = phys_dev(ctx->prm);
         if (ctx->generic) k_mortar<<<ctx->nmortar, 128, 0, st>>>(M);
-        else k_mortar3<<<std::min(ctx->nmortar, MT_MINB * ctx->nsm), MT_BS, 0, st>>>(M, ctx->d_mfaces, ctx->nmortar);
+        else {
+            CK(cudaMemsetAsync(ctx->d_flag + 4, 0, sizeof(int), st));  // k_mortar3 work counter
+            k_mortar3<<<std::min(ctx->nmortar, MT_MINB * ctx->nsm), MT_BS, 0, st>>>(M, ctx->d_mfaces, ctx->nmortar,
+                                                                                ctx->d_flag + 4);
+        }
         ctx->launches++;
     }
     if (variant == DG_NONISOLATED && !ctx->generic && ctx->nface_pts > 0) {

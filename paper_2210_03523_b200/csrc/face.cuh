@@ -208,7 +208,7 @@ constexpr int MT_MINB = 6;
 
 __device__ __forceinline__ void mt_unpack(int o, int* N) { N[0] = o & 15; N[1] = (o >> 4) & 15; N[2] = (o >> 8) & 15; }
 
-__global__ void __launch_bounds__(MT_BS, MT_MINB) k_mortar3(MortarParams P, const MortarFace* items, int nitems)
+__global__ void __launch_bounds__(MT_BS, MT_MINB) k_mortar3(MortarParams P, const MortarFace* items, int nitems, int* queue)
 {
     __shared__ double TR[2][2][MT_A];  // [stage][side] traces (zero padded)
     __shared__ double TM[2][MT_A];     // pass-A results (interpolation, then projection)
@@ -239,19 +239,24 @@ __global__ void __launch_bounds__(MT_BS, MT_MINB) k_mortar3(MortarParams P, cons
         double* dst = TR[st][me] + v * 81 + b * 9;
         for (int a = 0; a < s1; ++a) cp_async8(dst + a, src + a * sta);
     };
+    // faces: blockIdx.x, blockIdx.x + G, then dynamically from a work counter
+    // (mortar sizes vary: a static round robin leaves a long tail)
+    __shared__ int s_nn[2];
+    int fcur = f0, fnext = f0 + G;
     MortarFace cur = items[f0];
     MortarFace nxt = cur;
-    if (f0 + G < nitems) nxt = items[f0 + G];
+    if (fnext < nitems) nxt = items[fnext];
     issue(cur, 0);
     asm volatile("cp.async.commit_group;\n" ::);
     for (int k = 0;; ++k) {
-        const int fid = f0 + k * G;
-        if (fid >= nitems) break;
-        MortarFace nn = nxt;
-        if (fid + 2 * G < nitems) nn = items[fid + 2 * G];
+        if (fcur >= nitems) break;
+        if (t == 0) s_nn[k & 1] = 2 * G + atomicAdd(queue, 1);
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncthreads();  // traces of face k landed; face k-1 fully consumed
-        if (fid + G < nitems) issue(nxt, (k + 1) & 1);
+        const int fnn = s_nn[k & 1];
+        MortarFace nn = nxt;
+        if (fnn < nitems) nn = items[fnn];
+        if (fnext < nitems) issue(nxt, (k + 1) & 1);
         asm volatile("cp.async.commit_group;\n" ::);
 
         const int d = cur.d;
@@ -309,6 +314,8 @@ __global__ void __launch_bounds__(MT_BS, MT_MINB) k_mortar3(MortarParams P, cons
             const double* src = W + v * 81 + b * 9;
             for (int a = 0; a < sa_me; ++a) dst[a] = src[a];
         }
+        fcur = fnext;
+        fnext = fnn;
         cur = nxt;
         nxt = nn;
     }
