@@ -41,6 +41,29 @@ struct Bucket {
     int start0, nelem, grid;  // elist start, element count, persistent grid size
 };
 
+struct GraphKey {
+    int variant, mode;
+    const void *q, *out, *g, *dt, *lam;
+    double A, B;
+    bool operator<(const GraphKey& o) const
+    {
+        if (variant != o.variant) return variant < o.variant;
+        if (mode != o.mode) return mode < o.mode;
+        if (q != o.q) return q < o.q;
+        if (out != o.out) return out < o.out;
+        if (g != o.g) return g < o.g;
+        if (dt != o.dt) return dt < o.dt;
+        if (lam != o.lam) return lam < o.lam;
+        if (A != o.A) return A < o.A;
+        return B < o.B;
+    }
+};
+
+struct GraphEntry {
+    cudaGraphExec_t exec;
+    long long kernels;  // kernel launches recorded in the graph
+};
+
 struct dg_ctx {
     std::string err;
     dg_params prm{};
@@ -120,6 +143,9 @@ struct dg_ctx {
     cudaStream_t side[NSTREAMS] = {};
     cudaEvent_t ev_fork = nullptr, ev_join[NSTREAMS] = {};
     bool generic = false;  // DGTAU_GENERIC=1: runtime-order residual kernel (A/B testing)
+    bool no_graphs = false;  // DGTAU_NO_GRAPHS=1: launch mixed-order residuals directly
+    cudaStream_t cap_stream = nullptr;  // graph capture stream
+    std::map<GraphKey, GraphEntry> graphs;  // mixed-order residual graphs of the current layout
 };
 
 namespace {
@@ -283,6 +309,12 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         }
         const char* g = getenv("DGTAU_GENERIC");
         ctx->generic = g && g[0] == '1';
+        ctx->no_graphs = getenv_flag("DGTAU_NO_GRAPHS");
+        if ((s = cuda_check(ctx, cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking), "capture stream")) !=
+            DG_OK) {
+            dg_destroy(ctx);
+            return s;
+        }
     }
     // large dynamic shared memory for the element kernels (opt-in limit minus static smem)
     {
@@ -316,9 +348,17 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
     return DG_OK;
 }
 
+static void drop_graphs(dg_ctx* ctx)
+{
+    for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second.exec);
+    ctx->graphs.clear();
+}
+
 void dg_destroy(dg_ctx* ctx)
 {
     if (!ctx) return;
+    drop_graphs(ctx);
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     for (int i = 0; i < dg_ctx::NSTREAMS; ++i) {
         if (ctx->side[i]) cudaStreamDestroy(ctx->side[i]);
         if (ctx->ev_join[i]) cudaEventDestroy(ctx->ev_join[i]);
@@ -420,6 +460,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
 {
     if (!ctx) return DG_EINVAL;
     if (ctx->E == 0) return fail(ctx, DG_ESTATE, "set_orders: no mesh");
+    drop_graphs(ctx);  // captured launches refer to the old plans
     const int E = ctx->E;
     for (long long i = 0; i < 3LL * E; ++i)
         if (orders_host[i] < 1 || orders_host[i] > NMAX) return fail(ctx, DG_EINVAL, "set_orders: order out of 1..8");
@@ -858,11 +899,10 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
     return check_stream_error(ctx, "curved residual launch");
 }
 
-static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, double* out, double* g, const double* dt,
-                                 double A, double B, int mode, cudaStream_t st, unsigned long long* lam_max = nullptr,
-                                 int flags = 0)
+static dg_status launch_residual_direct(dg_ctx* ctx, int variant, const double* q, double* out, double* g,
+                                        const double* dt, double A, double B, int mode, cudaStream_t st,
+                                        unsigned long long* lam_max)
 {
-    if (ctx->curved) return launch_residual_curved(ctx, variant, q, out, g, dt, A, B, mode, st, lam_max, flags);
     if (variant == DG_NONISOLATED && ctx->nmortar > 0) {
         MortarParams M;
         M.q = q;
@@ -948,6 +988,46 @@ static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, doub
         }
     }
     return check_stream_error(ctx, "k_residual launch");
+}
+
+// Mixed-order layouts launch one order-specialised kernel per (N1,N2,N3)
+// bucket (cfg3: 216) plus the mortar and face passes: that sequence is
+// captured once per argument set into a CUDA graph (fork/join over the side
+// streams included) and replayed with a single launch.  Cache per layout.
+static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, double* out, double* g, const double* dt,
+                                 double A, double B, int mode, cudaStream_t st, unsigned long long* lam_max = nullptr,
+                                 int flags = 0)
+{
+    if (ctx->curved) return launch_residual_curved(ctx, variant, q, out, g, dt, A, B, mode, st, lam_max, flags);
+    if (ctx->generic || ctx->buckets.size() <= 1 || ctx->no_graphs)
+        return launch_residual_direct(ctx, variant, q, out, g, dt, A, B, mode, st, lam_max);
+    const GraphKey key{variant, mode, q, out, g, dt, lam_max, A, B};
+    auto itg = ctx->graphs.find(key);
+    if (itg == ctx->graphs.end()) {
+        if (ctx->graphs.size() >= 32) {  // bounded cache: drop everything (layouts rarely need more)
+            for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second.exec);
+            ctx->graphs.clear();
+        }
+        const long long l0 = ctx->launches;
+        CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed));
+        dg_status s = launch_residual_direct(ctx, variant, q, out, g, dt, A, B, mode, ctx->cap_stream, lam_max);
+        cudaGraph_t graph = nullptr;
+        const cudaError_t ec = cudaStreamEndCapture(ctx->cap_stream, &graph);
+        if (s != DG_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return s;
+        }
+        CK(ec);
+        cudaGraphExec_t exec = nullptr;
+        const cudaError_t ei = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        CK(ei);
+        itg = ctx->graphs.emplace(key, GraphEntry{exec, ctx->launches - l0}).first;
+        ctx->launches = l0;
+    }
+    CK(cudaGraphLaunch(itg->second.exec, st));
+    ctx->launches += itg->second.kernels;
+    return check_stream_error(ctx, "residual graph launch");
 }
 
 dg_status dg_rhs_eval(dg_ctx* ctx, int variant, const double* q_dev, double* qdot_dev, void* stream)
@@ -1079,6 +1159,7 @@ dg_status dg_rk_steps(dg_ctx* ctx, int nsteps, double* qa, double* qb, double* g
 
 dg_status dg_set_owned(dg_ctx* ctx, int n_owned)
 {
+    if (ctx) drop_graphs(ctx);
     if (!ctx) return DG_EINVAL;
     if (ctx->E == 0) return fail(ctx, DG_ESTATE, "set_owned: no mesh");
     if (n_owned < 1 || n_owned > ctx->E) return fail(ctx, DG_EINVAL, "set_owned: 1 <= n_owned <= E");
