@@ -489,7 +489,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
         const int ord = kv.first;
         const int N[3] = {ord & 255, (ord >> 8) & 255, (ord >> 16) & 255};
         const int n = npts(N);
-        const int k = std::max(1, std::min(MAXSLOTS, 384 / n));  // = Shape<N>::CNT
+        const int k = res_cnt(N[0] + 1, N[1] + 1, N[2] + 1);  // = Shape<N>::CNT
         const int nfs = 2 * ((N[1] + 1) * (N[2] + 1) + (N[0] + 1) * (N[2] + 1) + (N[0] + 1) * (N[1] + 1));
         for (size_t i = 0; i < kv.second.size(); i += k) {
             WorkItem w;

@@ -42,13 +42,26 @@ static __constant__ double c_EOM[NP][4];
 __host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 
+// Elements per work item of the (n1, n2, n3)-node bucket: <= ~384 nodes per
+// CTA (node tasks in one round of threads), capped so that the CTA's shared
+// memory (2 state + 2 flux stages, 3 flux directions, meta) stays <= 76 KB
+// and 3 CTAs fit an SM (small orders: the face-flux stage dominates).
+// Shared by the host plans (dg_set_orders) and Shape<>.
+__host__ __device__ constexpr int res_cnt(int n1, int n2, int n3)
+{
+    const int n = n1 * n2 * n3;
+    const int sq = (NV * n + 2) / 2 * 2;
+    const int gsl = 2 * ((NV * n2 * n3 + 1) / 2 * 2 + (NV * n1 * n3 + 1) / 2 * 2 + (NV * n1 * n2 + 1) / 2 * 2);
+    const int per = 8 * (2 * sq + 2 * gsl + 3 * NV * n + 33);
+    const int budget = (76 * 1024) / per;
+    return cmax(1, cmin(cmin(MAXSLOTS, 384 / n), budget));
+}
+
 template <int N1, int N2, int N3>
 struct Shape {
     static constexpr int n1 = N1 + 1, n2 = N2 + 1, n3 = N3 + 1;
     static constexpr int n = n1 * n2 * n3;
-    // <= ~384 nodes per CTA so node tasks take one round of threads; two
-    // node passes only for n > 384.
-    static constexpr int CNT = cmax(1, cmin(MAXSLOTS, 384 / n));
+    static constexpr int CNT = res_cnt(n1, n2, n3);
     static constexpr int T = CNT * n;
     static constexpr int NPT = T > 384 ? 2 : 1;
     static constexpr int LT = NV * (n / n1 + n / n2 + n / n3);  // line tasks per element
