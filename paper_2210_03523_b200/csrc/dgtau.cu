@@ -1464,10 +1464,16 @@ dg_status dg_transfer(dg_ctx* ctx, const int32_t* new_orders, const double* q_ol
     const int E = ctx->E;
     std::vector<long long>& offn = ctx->tr_off_host;  // persistent: outlives the async copy
     offn.assign(E + 1, 0);
+    int smax[3] = {1, 1, 1};  // shared memory sized to this transfer's largest element passes
     for (int e = 0; e < E; ++e) {
         for (int d = 0; d < 3; ++d)
             if (new_orders[3 * e + d] < 1 || new_orders[3 * e + d] > NMAX) return fail(ctx, DG_EINVAL, "transfer: order");
         offn[e + 1] = offn[e] + (long long)NV * npts(&new_orders[3 * e]);
+        const int* a = &ctx->orders[3 * e];
+        const int* b = &new_orders[3 * e];
+        smax[0] = std::max(smax[0], npts(a));
+        smax[1] = std::max(smax[1], (b[0] + 1) * (a[1] + 1) * (a[2] + 1));
+        smax[2] = std::max(smax[2], (b[0] + 1) * (b[1] + 1) * (a[2] + 1));
     }
     cudaStream_t st = (cudaStream_t)stream;
     if (!ctx->d_tr_orders) {
@@ -1487,7 +1493,10 @@ dg_status dg_transfer(dg_ctx* ctx, const int32_t* new_orders, const double* q_ol
     P.offold = ctx->d_off;
     P.offnew = d_offn;
     P.tab = ctx->d_tab;
-    k_transfer<<<E, BLOCK, sizeof(double) * 3 * NV * NP * NP * NP, st>>>(P);
+    P.smax0 = smax[0];
+    P.smax1 = smax[1];
+    P.smax2 = smax[2];
+    k_transfer<<<E, BLOCK, sizeof(double) * NV * (size_t)(smax[0] + smax[1] + smax[2]), st>>>(P);
     ctx->launches++;
     return check_stream_error(ctx, "k_transfer launch");
 }

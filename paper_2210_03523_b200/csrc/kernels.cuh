@@ -662,6 +662,7 @@ __global__ void __launch_bounds__(JUMP_FIX_BS) k_jump_fix(const int* nbr, int* a
 // ---------------------------------------------------------------------------
 
 struct TransferParams {
+    int smax0, smax1, smax2;  // max over elements of nA, n1, n2 (shared-memory layout)
     const double* qold;
     double* qnew;
     const int* oold;
@@ -679,9 +680,9 @@ __global__ void __launch_bounds__(BLOCK) k_transfer(TransferParams P)
     for (int d = 0; d < 3; ++d) { A[d] = P.oold[3 * e + d] + 1; B[d] = P.onew[3 * e + d] + 1; }
     const int nA = A[0] * A[1] * A[2];
     const int n1 = B[0] * A[1] * A[2], n2 = B[0] * B[1] * A[2], nB = B[0] * B[1] * B[2];
-    double* s0 = sm;
-    double* s1 = s0 + NV * NP * NP * NP;
-    double* s2 = s1 + NV * NP * NP * NP;
+    double* s0 = sm;                 // 5 nA
+    double* s1 = s0 + NV * P.smax0;  // 5 n1
+    double* s2 = s1 + NV * P.smax1;  // 5 n2 (buffers sized by the host for this transfer)
     const long long oa = P.offold[e], ob = P.offnew[e];
     for (int t = threadIdx.x; t < NV * nA; t += blockDim.x) s0[t] = P.qold[oa + t];
     __syncthreads();
