@@ -57,6 +57,39 @@ def load_peaks():
     return 6650.0, "fallback"
 
 
+def load_fp64_peak():
+    """Measured DFMA peak (tools/fp64_peak.cu on a B200, profiles/r01_fp64_peak.json), TFLOP/s."""
+    p = os.path.join(ROOT, "profiles", "r01_fp64_peak.json")
+    best = None
+    if os.path.exists(p):
+        for line in open(p):
+            d = json.loads(line)
+            if d.get("kernel") == "dfma":
+                best = max(best or 0.0, d["tflops"])
+    return (best, "measured DFMA (profiles/r01_fp64_peak.json)") if best else (37.2, "nominal 148 SM x 64 FMA x 2 x 1.965 GHz")
+
+
+def flops_model(N):
+    """Algorithmic fp64 flops (FMA = 2) of the method steps of SURVEY 8(c).1 on
+    affine hexes with isotropic order N (counted from the definitions, not
+    from kernel code):
+      residual per DOF: primitives + the three axis fluxes (33); D^N along each
+      line of each axis for 5 variables, even-odd form L^2/2 multiply-adds per
+      line plus 2 L adds (15 (L + 2) per node); strong-form lifting at the two
+      line ends (3 flops per end); Roe flux per face point (130) times face
+      points per DOF (3 L^2 / L^3); per-node combination and RK update (50).
+      tau per element: for every level (d, p < N): per coarse node the
+      interpolation of q and R along d (2 x 5 x 2 L), the three fluxes (33),
+      the three axis derivatives (15 (L_d' + 2)) and the combination (30)."""
+    L = N + 1
+    per_dof = 33 + 15 * (L + 2) + 30.0 / L + 130.0 * 3 / L + 50
+    tau = 0.0
+    for p in range(1, N):
+        nodes = (p + 1) * L * L
+        tau += 3 * nodes * (20 * L + 33 + 5 * ((p + 1 + 2) + 2 * (L + 2)) + 30)
+    return per_dof, tau
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
@@ -345,6 +378,20 @@ def oracle_baseline(sample_rk_steps=1, with_tau=True):
                        f"{ndof} DOF)" + (" + 1 SOLVER residual + 1 tau-estimate" if with_tau else ""))
 
 
+def fp64_block(res):
+    """Secondary rooflines: algorithmic fp64 rate (flops_model) of the RK stage
+    and of the tau-estimation against the measured DFMA peak."""
+    peak, src = load_fp64_peak()
+    per_dof, tau_el = flops_model(6)
+    stage_tf = per_dof * res["ndof"] * 3 * res["rk_count"] / (res["rk_ms"] * 1e-3) / 1e12
+    tau_tf = tau_el * res["tau_elems"] / 1e12
+    return {"peak_tflops": peak, "peak_source": src,
+            "rk_stage": {"flops_per_dof": round(per_dof, 1), "achieved_tflops": stage_tf, "frac": stage_tf / peak},
+            "tau": {"flops_per_element": round(tau_el), "achieved_tflops": tau_tf, "frac": tau_tf / peak,
+                    "note": "tau time includes the SOLVER reference residual"},
+            "model": "bench.py flops_model (SURVEY 8(c).1 steps, FMA = 2)"}
+
+
 def config_block(world, extra=None):
     c = {"workload": ("cfg2" if world == 1 else f"cfg2 per rank (weak scaling, global 16x16x{16 * world})") +
                      ": Euler density pulse, periodic 16^3 affine hexes, N=(6,6,6) Gauss-Lobatto, "
@@ -431,6 +478,7 @@ def main():
                      "peak": res["peak"], "unit": "GB/s", "frac": res["achieved"] / res["peak"],
                      "peak_source": res["peak_kind"], "traffic": load_traffic(),
                      "bytes_per_dof": "120 (stage 1) / 160 (stages 2,3)"},
+        "roofline_fp64": fp64_block(res),
         "cpu_baseline": cpu,
         "e2e": res["e2e"],
         "gpu_launches": res["launches"],
