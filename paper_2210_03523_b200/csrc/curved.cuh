@@ -835,141 +835,6 @@ __global__ void __launch_bounds__(CM_BS, 4) k_mortar_curved2(CMortarParams P, co
     }
 }
 
-__global__ void __launch_bounds__(128) k_mortar_curved(CMortarParams P)
-{
-    __shared__ double Xm[3][NP * NP], Xml[3][NP * NP];
-    __shared__ double Jm[3][NP * NP];
-    __shared__ double GM[15][NP * NP];
-    const MortarItem it = P.items[blockIdx.x];
-    const int d = it.d;
-    const int ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
-    int NL[3], NR[3];
-    for (int k = 0; k < 3; ++k) { NL[k] = P.orders[3 * it.L + k]; NR[k] = P.orders[3 * it.R + k]; }
-    const int M1 = max(NL[ta], NR[ta]), M2 = max(NL[tb], NR[tb]);
-    const int nm = (M1 + 1) * (M2 + 1);
-    const int gd[3] = {P.cm.g1, P.cm.g2, P.cm.g3};
-    // face coordinates of L's +1 face at the mortar nodes (GL geometry nodes:
-    // last layer along d), tangential derivatives, cross product -- in dd
-    const double* G = P.cm.geo + (long long)it.L * 3 * P.cm.ng;
-    const int ga = gd[0] + 1, gb = gd[1] + 1;
-    const TablesDD* tdd = P.tdd;
-    for (int t = threadIdx.x; t < nm; t += blockDim.x) {
-        const int m1 = t % (M1 + 1), m2 = t / (M1 + 1);
-        dd x[3] = {mkdd(0.0), mkdd(0.0), mkdd(0.0)};
-        for (int b = 0; b <= gd[tb]; ++b)
-            for (int a = 0; a <= gd[ta]; ++a) {
-                int idx[3];
-                idx[d] = gd[d]; idx[ta] = a; idx[tb] = b;
-                const int gi = idx[0] + ga * (idx[1] + gb * idx[2]);
-                const int ia = m1 * (gd[ta] + 1) + a, ib = m2 * (gd[tb] + 1) + b;
-                const dd wgt = dd_mul(dd{tdd->Thi[gd[ta]][M1][ia], tdd->Tlo[gd[ta]][M1][ia]},
-                                      dd{tdd->Thi[gd[tb]][M2][ib], tdd->Tlo[gd[tb]][M2][ib]});
-                for (int c = 0; c < 3; ++c) x[c] = dd_add(x[c], dd_mul(wgt, mkdd(G[c * P.cm.ng + gi])));
-            }
-        for (int c = 0; c < 3; ++c) { Xm[c][t] = x[c].hi; Xml[c][t] = x[c].lo; }
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < nm; t += blockDim.x) {
-        const int m1 = t % (M1 + 1), m2 = t / (M1 + 1);
-        dd u[3], v[3];
-        for (int c = 0; c < 3; ++c) {
-            dd s1 = mkdd(0.0), s2 = mkdd(0.0);
-            for (int m = 0; m <= M1; ++m) {
-                const int ix = m + (M1 + 1) * m2;
-                s1 = dd_add(s1, dd_mul(dd{tdd->Dhi[M1][m1 * (M1 + 1) + m], tdd->Dlo[M1][m1 * (M1 + 1) + m]},
-                                       dd{Xm[c][ix], Xml[c][ix]}));
-            }
-            for (int m = 0; m <= M2; ++m) {
-                const int ix = m1 + (M1 + 1) * m;
-                s2 = dd_add(s2, dd_mul(dd{tdd->Dhi[M2][m2 * (M2 + 1) + m], tdd->Dlo[M2][m2 * (M2 + 1) + m]},
-                                       dd{Xm[c][ix], Xml[c][ix]}));
-            }
-            u[c] = s1;
-            v[c] = s2;
-        }
-        dd w[3];
-        const dd* A = d == 1 ? v : u;  // Ja^2 = x_zeta x x_xi = x_t2 x x_t1
-        const dd* B = d == 1 ? u : v;
-        w[0] = dd_add(dd_mul(A[1], B[2]), dd_neg(dd_mul(A[2], B[1])));
-        w[1] = dd_add(dd_mul(A[2], B[0]), dd_neg(dd_mul(A[0], B[2])));
-        w[2] = dd_add(dd_mul(A[0], B[1]), dd_neg(dd_mul(A[1], B[0])));
-        for (int c = 0; c < 3; ++c) Jm[c][t] = w[c].hi + w[c].lo;
-    }
-    __syncthreads();
-    const int nL = (NL[0] + 1) * (NL[1] + 1) * (NL[2] + 1), nR = (NR[0] + 1) * (NR[1] + 1) * (NR[2] + 1);
-    const long long oL = P.off[it.L], oR = P.off[it.R];
-    const double* TL1 = P.tab->T[NL[ta]][M1];
-    const double* TL2 = P.tab->T[NL[tb]][M2];
-    const double* TR1 = P.tab->T[NR[ta]][M1];
-    const double* TR2 = P.tab->T[NR[tb]][M2];
-    const bool ns = P.ph.physics == 1;
-    const int ncomp = P.mode == 0 ? NV : 15;
-    for (int t = threadIdx.x; t < nm; t += blockDim.x) {
-        const int m1 = t % (M1 + 1), m2 = t / (M1 + 1);
-        double qL[NV] = {0, 0, 0, 0, 0}, qR[NV] = {0, 0, 0, 0, 0};
-        double gL[15], gR[15];
-        for (int c = 0; c < 15; ++c) { gL[c] = 0.0; gR[c] = 0.0; }
-        const bool wantg = ns && P.mode == 0;
-        for (int b = 0; b <= NL[tb]; ++b)
-            for (int a = 0; a <= NL[ta]; ++a) {
-                int ijk[3];
-                ijk[d] = NL[d]; ijk[ta] = a; ijk[tb] = b;
-                const long long node = ijk[0] + (NL[0] + 1) * (ijk[1] + (NL[1] + 1) * ijk[2]);
-                const double wgt = TL1[m1 * (NL[ta] + 1) + a] * TL2[m2 * (NL[tb] + 1) + b];
-                for (int v = 0; v < NV; ++v) qL[v] += wgt * P.q[oL + node + (long long)v * nL];
-                if (wantg)
-                    for (int c = 0; c < 15; ++c) gL[c] += wgt * P.grad[3 * oL + node + (long long)c * nL];
-            }
-        for (int b = 0; b <= NR[tb]; ++b)
-            for (int a = 0; a <= NR[ta]; ++a) {
-                int ijk[3];
-                ijk[d] = 0; ijk[ta] = a; ijk[tb] = b;
-                const long long node = ijk[0] + (NR[0] + 1) * (ijk[1] + (NR[1] + 1) * ijk[2]);
-                const double wgt = TR1[m1 * (NR[ta] + 1) + a] * TR2[m2 * (NR[tb] + 1) + b];
-                for (int v = 0; v < NV; ++v) qR[v] += wgt * P.q[oR + node + (long long)v * nR];
-                if (wantg)
-                    for (int c = 0; c < 15; ++c) gR[c] += wgt * P.grad[3 * oR + node + (long long)c * nR];
-            }
-        const double jf[3] = {Jm[0][t], Jm[1][t], Jm[2][t]};
-        if (P.mode == 1) {
-            for (int c = 0; c < 3; ++c)
-                for (int v = 0; v < NV; ++v) GM[c * NV + v][t] = 0.5 * (qL[v] + qR[v]) * jf[c];
-        } else {
-            const double S = sqrt(jf[0] * jf[0] + jf[1] * jf[1] + jf[2] * jf[2]);
-            const double nrm[3] = {jf[0] / S, jf[1] / S, jf[2] / S};
-            double F[NV];
-            riemann(qL, qR, nrm, P.ph, F);
-            for (int v = 0; v < NV; ++v) F[v] *= S;
-            if (ns) {
-                double fL[NV], fR[NV];
-                visc_dot(qL, gL, jf[0], jf[1], jf[2], P.ph, fL);
-                visc_dot(qR, gR, jf[0], jf[1], jf[2], P.ph, fR);
-                for (int v = 0; v < NV; ++v) F[v] -= 0.5 * (fL[v] + fR[v]);
-            }
-            for (int v = 0; v < NV; ++v) GM[v][t] = F[v];
-        }
-    }
-    __syncthreads();
-    for (int side = 0; side < 2; ++side) {
-        const int* NS = side == 0 ? NL : NR;
-        const int S1 = NS[ta], S2 = NS[tb];
-        const int nsd = (S1 + 1) * (S2 + 1);
-        const long long mo = P.moff[6 * (side == 0 ? it.L : it.R) + 2 * d + (side == 0 ? 1 : 0)];
-        const double* P1 = P.tab->P[M1][S1];
-        const double* P2 = P.tab->P[M2][S2];
-        double* dst = P.mortarG + (P.mode == 0 ? mo : 3 * mo);
-        for (int t = threadIdx.x; t < nsd; t += blockDim.x) {
-            const int a = t % (S1 + 1), b = t / (S1 + 1);
-            for (int c = 0; c < ncomp; ++c) {
-                double s = 0.0;
-                for (int m2 = 0; m2 <= M2; ++m2)
-                    for (int m1 = 0; m1 <= M1; ++m1)
-                        s += P1[a * (M1 + 1) + m1] * P2[b * (M2 + 1) + m2] * GM[c][m1 + (M1 + 1) * m2];
-                dst[(long long)c * nsd + t] = s;
-            }
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------
 // tau-estimation on curved elements (Euler or NS), one CTA per level (e,d,p):

@@ -323,13 +323,9 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         const int lim = optin - 1024;  // headroom for static shared arrays
         cudaFuncSetAttribute(k_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
         cudaFuncSetAttribute(k_tau, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
-        cudaFuncSetAttribute(k_tau2, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
-        cudaFuncSetAttribute(k_tau2, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
-        cudaFuncSetAttribute(k_tau3, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(140 * 1024, lim));
         cudaFuncSetAttribute(k_tau5, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 4096);  // 3.1 KB static
         cudaFuncSetAttribute(k_mortar_curved2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CM_SMEM);
         cudaFuncSetAttribute(k_tau5, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
-        cudaFuncSetAttribute(k_tau3, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
         cudaFuncSetAttribute(k_transfer, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
         const int limc = optin - 8192;  // curved kernels: up to ~6 KB static (staged D, reductions)
         cudaFuncSetAttribute(k_metrics, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
@@ -1366,7 +1362,7 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
             C.formulation = o->formulation;
             C.ph = phys_dev(ctx->prm);
             k_tau_curved<<<ctx->nlevels, CBS, sm, st>>>(C);
-        } else if (ctx->ntgroups > 0 && !getenv_flag("DGTAU_TAU3")) {
+        } else if (ctx->ntgroups > 0) {
             Tau5Params P;
             P.q = q_dev;
             P.qref = ref;
@@ -1379,19 +1375,6 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
             P.formulation = o->formulation;
             P.gm1 = ctx->prm.gamma - 1.0;
             k_tau5<<<ctx->ntgroups, TAU5_BS, ctx->tau5_smem, st>>>(P);
-        } else if (ctx->nlevels > 0) {
-            Tau3Params P;
-            P.q = q_dev;
-            P.qref = ref;
-            P.tau = tau_dev;
-            P.orders = ctx->d_orders;
-            P.off = ctx->d_off;
-            P.hgeo = ctx->d_h;
-            P.levels = ctx->d_levels;
-            P.tab = ctx->d_tab;
-            P.formulation = o->formulation;
-            P.gm1 = ctx->prm.gamma - 1.0;
-            k_tau3<<<ctx->nlevels, TAU3_BS, sizeof(double) * 5 * NV * (size_t)ctx->max_level, st>>>(P);
         }
     }
     ctx->launches++;

@@ -758,90 +758,3 @@ __global__ void __launch_bounds__(BLOCK) k_diag(DiagParams P)
 }
 
 }  // namespace dgtau
-
-namespace dgtau {
-
-// ---------------------------------------------------------------------------
-// Mortar kernel v2 (reading A6), one warp per face, 3 faces per CTA:
-// tensor-product (two-pass) interpolation of both traces to the mortar,
-// Roe flux at the mortar nodes, two-pass exact L2 projection back to both
-// sides.  Work per face O(n_mortar (N+1)) instead of O(n_mortar n_face).
-// ---------------------------------------------------------------------------
-constexpr int MW_FACES = 3;
-constexpr int MBUF = NV * NP * NP;  // one 5-variable face array
-
-__device__ __forceinline__ void two_pass(const double* in, int na, int nb, const double* A, int ma, const double* B,
-                                         int mb, double* tmp, double* out, int lane)
-{
-    // in[v][a + na b] -> tmp[v][i + ma b] = sum_a A[i][a] in -> out[v][i + ma j] = sum_b B[j][b] tmp
-    for (int t = lane; t < NV * ma * nb; t += 32) {
-        const int v = t / (ma * nb), r = t - v * ma * nb, i = r % ma, b = r / ma;
-        double s = 0.0;
-        for (int a = 0; a < na; ++a) s += A[i * na + a] * in[v * na * nb + a + na * b];
-        tmp[t] = s;
-    }
-    __syncwarp();
-    for (int t = lane; t < NV * ma * mb; t += 32) {
-        const int v = t / (ma * mb), r = t - v * ma * mb, i = r % ma, j = r / ma;
-        double s = 0.0;
-        for (int b = 0; b < nb; ++b) s += B[j * nb + b] * tmp[v * ma * nb + i + ma * b];
-        out[t] = s;
-    }
-    __syncwarp();
-}
-
-__global__ void __launch_bounds__(32 * MW_FACES) k_mortar2(MortarParams P, int nitems)
-{
-    __shared__ double buf[MW_FACES][4][MBUF];  // trace L/R, tmp, mortar
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int fid = blockIdx.x * MW_FACES + w;
-    if (fid >= nitems) return;
-    const MortarItem it = P.items[fid];
-    const int d = it.d;
-    const int ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
-    int NL[3], NR[3];
-    for (int k = 0; k < 3; ++k) { NL[k] = P.orders[3 * it.L + k]; NR[k] = P.orders[3 * it.R + k]; }
-    const int M1 = max(NL[ta], NR[ta]), M2 = max(NL[tb], NR[tb]);
-    const int m1 = M1 + 1, m2 = M2 + 1, nm = m1 * m2;
-    double* trc = buf[w][0];
-    double* tmp = buf[w][1];
-    double* qmL = buf[w][2];
-    double* qmR = buf[w][3];
-    // L's +1 face trace, interpolated to the mortar
-    for (int side = 0; side < 2; ++side) {
-        const int* NS = side == 0 ? NL : NR;
-        const int e = side == 0 ? it.L : it.R;
-        const int s1 = NS[ta] + 1, s2 = NS[tb] + 1;
-        const int n = (NS[0] + 1) * (NS[1] + 1) * (NS[2] + 1);
-        const int st[3] = {1, NS[0] + 1, (NS[0] + 1) * (NS[1] + 1)};
-        const int base = (side == 0 ? NS[d] : 0) * st[d];
-        const double* qe = P.q + P.off[e] + base;
-        for (int t = lane; t < NV * s1 * s2; t += 32) {
-            const int v = t / (s1 * s2), r = t - v * s1 * s2, a = r % s1, b = r / s1;
-            trc[t] = __ldg(qe + (long long)v * n + a * st[ta] + b * st[tb]);
-        }
-        __syncwarp();
-        two_pass(trc, s1, s2, P.tab->T[NS[ta]][M1], m1, P.tab->T[NS[tb]][M2], m2, tmp, side == 0 ? qmL : qmR, lane);
-    }
-    // Roe flux at the mortar nodes -> trc (reused as G_M)
-    double nrm[3] = {0.0, 0.0, 0.0};
-    nrm[d] = 1.0;
-    for (int t = lane; t < nm; t += 32) {
-        double qL[NV], qR[NV], F[NV];
-        for (int v = 0; v < NV; ++v) { qL[v] = qmL[v * nm + t]; qR[v] = qmR[v * nm + t]; }
-        riemann(qL, qR, nrm, P.ph, F);
-        for (int v = 0; v < NV; ++v) trc[v * nm + t] = F[v];
-    }
-    __syncwarp();
-    // project back to both sides (P^{M->s} per tangential direction)
-    for (int side = 0; side < 2; ++side) {
-        const int* NS = side == 0 ? NL : NR;
-        const int s1 = NS[ta] + 1, s2 = NS[tb] + 1;
-        two_pass(trc, m1, m2, P.tab->P[M1][NS[ta]], s1, P.tab->P[M2][NS[tb]], s2, tmp, qmL, lane);
-        const long long mo = P.moff[6 * (side == 0 ? it.L : it.R) + 2 * d + (side == 0 ? 1 : 0)];
-        for (int t = lane; t < NV * s1 * s2; t += 32) P.mortarG[mo + t] = qmL[t];
-        __syncwarp();
-    }
-}
-
-}  // namespace dgtau

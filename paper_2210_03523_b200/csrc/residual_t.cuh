@@ -105,19 +105,6 @@ __device__ __forceinline__ void flux_axis(const double* q, double ir, double p, 
     f[4] = (q[4] + p) * ud;
 }
 
-// Euler flux along a unit normal given as three scalars (no dynamic indexing)
-__device__ __forceinline__ void flux_normal(const double* q, double nx, double ny, double nz, double gm1, double* f)
-{
-    const double ir = 1.0 / q[0];
-    const double p = gm1 * (q[4] - 0.5 * ir * (q[1] * q[1] + q[2] * q[2] + q[3] * q[3]));
-    const double un = (q[1] * nx + q[2] * ny + q[3] * nz) * ir;
-    f[0] = q[0] * un;
-    f[1] = q[1] * un + p * nx;
-    f[2] = q[2] * un + p * ny;
-    f[3] = q[3] * un + p * nz;
-    f[4] = (q[4] + p) * un;
-}
-
 // In-place derivative of one line held in shared memory, F[m*stride] <-
 // sum_m D_am F_m, by the even-odd decomposition of the GL differentiation
 // matrix (about half the multiply-adds of the direct product):
@@ -214,97 +201,6 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src)
 {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
-}
-
-// decode face task r in [0, FS) -> face f and point pt
-template <class S>
-__device__ __forceinline__ void face_of(int r, int& f, int& pt)
-{
-    if (r < 2 * S::nf0) {
-        f = r < S::nf0 ? 0 : 1;
-        pt = r - f * S::nf0;
-    } else if (r < 2 * (S::nf0 + S::nf1)) {
-        const int r1 = r - 2 * S::nf0;
-        f = r1 < S::nf1 ? 2 : 3;
-        pt = r1 - (f - 2) * S::nf1;
-    } else {
-        const int r2 = r - 2 * (S::nf0 + S::nf1);
-        f = r2 < S::nf2 ? 4 : 5;
-        pt = r2 - (f - 4) * S::nf2;
-    }
-}
-
-// Roe flux (no entropy fix, reading A7) for the axis normal e_d, with
-// 1/rho and p of both states precomputed (same algebra as roe_flux with n = e_d).
-template <int d>
-__device__ __forceinline__ void roe_axis(const double* qL, double irL, double pL, const double* qR, double irR,
-                                         double pR, double gamma, double* F)
-{
-    const double gm1 = gamma - 1.0;
-    double uL[3], uR[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) { uL[k] = qL[1 + k] * irL; uR[k] = qR[1 + k] * irR; }
-    const double HL = (qL[4] + pL) * irL, HR = (qR[4] + pR) * irR;
-    const double sL = sqrt_nr(qL[0]), sR = sqrt_nr(qR[0]);
-    const double is = rcp_nr(sL + sR);
-    const double wl = sL * is, wr = sR * is;
-    double u[3], du[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) { u[k] = wl * uL[k] + wr * uR[k]; du[k] = uR[k] - uL[k]; }
-    const double H = wl * HL + wr * HR;
-    const double uu = u[0] * u[0] + u[1] * u[1] + u[2] * u[2];
-    const double c2 = gm1 * (H - 0.5 * uu);
-    const double ic2 = rcp_nr(c2);
-    const double c = c2 * rsqrt_nr(c2);
-    const double un = u[d], dun = du[d];
-    const double rho = sL * sR;
-    const double dp = pR - pL;
-    const double rcd = rho * c * dun;
-    const double a1 = 0.5 * (dp - rcd) * ic2, a5 = 0.5 * (dp + rcd) * ic2;
-    const double a2 = (qR[0] - qL[0]) - dp * ic2;
-    const double w1 = fabs(un - c) * a1, w5 = fabs(un + c) * a5, l2 = fabs(un);
-    const double mL = qL[1 + d], mR = qR[1 + d];
-    F[0] = 0.5 * (mL + mR) - 0.5 * (w1 + l2 * a2 + w5);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        double fk = qL[1 + k] * uL[d] + qR[1 + k] * uR[d];
-        double dk = (w1 + w5) * u[k] + l2 * (a2 * u[k] + rho * du[k]);
-        if (k == d) {
-            fk += pL + pR;
-            dk += c * (w5 - w1) - l2 * rho * dun;
-        }
-        F[1 + k] = 0.5 * fk - 0.5 * dk;
-    }
-    const double udu = u[0] * du[0] + u[1] * du[1] + u[2] * du[2];
-    const double fe = (qL[4] + pL) * uL[d] + (qR[4] + pR) * uR[d];
-    const double de = (w1 + w5) * H + un * c * (w5 - w1) + l2 * (a2 * 0.5 * uu + rho * (udu - un * dun));
-    F[4] = 0.5 * fe - 0.5 * de;
-}
-
-// surface term of one face point for the compile-time axis d: G - f_own
-template <int d>
-__device__ __forceinline__ void face_point(const double* qo, double iro, double po, double* qx, int kind, int s,
-                                           const PhysDev& ph, double* out)
-{
-    double fo[NV], G[NV];
-    flux_axis<d>(qo, iro, po, fo);
-    if (kind == 1) {
-#pragma unroll
-        for (int v = 0; v < NV; ++v) G[v] = qx[v];
-    } else {
-        if (kind >= 2) ghost_state(qo, kind == 2 ? -1 : -2, ph, qx);
-        if (ph.flux == 1) {
-            double nrm[3] = {d == 0 ? 1.0 : 0.0, d == 1 ? 1.0 : 0.0, d == 2 ? 1.0 : 0.0};
-            if (s) llf_flux(qo, qx, nrm, ph.gamma, G); else llf_flux(qx, qo, nrm, ph.gamma, G);
-        } else {
-            const double irx = rcp_nr(qx[0]);
-            const double px = ph.gm1 * (qx[4] - 0.5 * irx * (qx[1] * qx[1] + qx[2] * qx[2] + qx[3] * qx[3]));
-            if (s) roe_axis<d>(qo, iro, po, qx, irx, px, ph.gamma, G);
-            else roe_axis<d>(qx, irx, px, qo, iro, po, ph.gamma, G);
-        }
-    }
-#pragma unroll
-    for (int v = 0; v < NV; ++v) out[v] = G[v] - fo[v];
 }
 
 // Per-item metadata staged in shared memory: slot info (5 doubles) and the 6

@@ -1,249 +1,27 @@
-// tau_t.cuh -- batched tau-estimation kernel (v2), one CTA per element.
+// tau_t.cuh -- batched tau-estimation: tau[e][d][p] for every
+// element e, direction d and coarse order p < N_d.
 //
-// PAPER.md P:225-241 (tau-estimation with the variational DG reference term
-// I F(q) ~ I (M^P)^-1 F^P(q^P)), eqs TEtildedef / TEdef,
-// isolated coarse operators, decoupled directional coarse
-// levels (reading A12): for every direction d and coarse order p < N_d of the
+// tau-estimation with the variational DG reference term I F(q) ~ I (M^P)^-1
+// F^P(q^P), eqs TEtildedef / TEdef, isolated
+// coarse operators, decoupled directional coarse levels
+// (reading A12): for every direction d and coarse order p < N_d of the
 // element, O = N with O_d = p,
 //   q_c = T_d^{N_d->p} q,  Qdot_c = -sum_d' (2/h_d') D^{O_d'} f_d'(q_c)
 //   (strong form == weak form + own-trace lifting for GL),
 //   tau~ = T_d R - Qdot_c,  tau = J w w w tau~ (traditional),
 //   tau[e][d][p] = max |tau| over coarse nodes and variables.
-// All coarse levels of the element are evaluated in this one CTA: the fine
-// state and the reference residual are staged once in shared memory; line
-// sweeps reuse the order-specialised even-odd dline_inplace<L>.
+// k_tau5 (below) evaluates groups of coarse orders of one (element,
+// direction) per CTA; k_tau_norm fills the noise-scale slot (reading R1).
 #pragma once
 
 #include "residual_t.cuh"
 
 namespace dgtau {
 
-constexpr int TAU_BS = 384;
-constexpr int TAU_NPT = 2;  // 384 * 2 >= 729
-
-struct Tau2Params {
-    const double* q;
-    const double* qref;  // SOLVER reference or nullptr (SAME: computed here)
-    double* tau;         // [E][3][9]
-    const int* orders;
-    const long long* off;
-    const double* hgeo;
-    const Tables* tab;
-    int formulation;
-    double gm1;
-};
-
-__device__ __forceinline__ void dline_dispatch(int L, double* Fl, int stride)
-{
-    switch (L) {
-        case 2: dline_inplace<2>(Fl, stride); break;
-        case 3: dline_inplace<3>(Fl, stride); break;
-        case 4: dline_inplace<4>(Fl, stride); break;
-        case 5: dline_inplace<5>(Fl, stride); break;
-        case 6: dline_inplace<6>(Fl, stride); break;
-        case 7: dline_inplace<7>(Fl, stride); break;
-        case 8: dline_inplace<8>(Fl, stride); break;
-        default: dline_inplace<9>(Fl, stride); break;
-    }
-}
-
-// Isolated residual at orders O of the state qc (registers of the owned
-// nodes t = tid + it*TAU_BS < nO):  acc = sum_d (2/h_d) D^{O_d} f_d(qc),
-// i.e. Qdot = -acc.  Fb: shared scratch of 5*nO doubles.
-__device__ __forceinline__ void tau_iso_residual(int o1, int o2, int o3, int nO, const double (&qc)[TAU_NPT][NV],
-                                                 double (&acc)[TAU_NPT][NV], double* Fb, double sc0, double sc1,
-                                                 double sc2, double gm1)
-{
-    const int tid = threadIdx.x;
-    double ir[TAU_NPT], pr[TAU_NPT];
-#pragma unroll
-    for (int it = 0; it < TAU_NPT; ++it) {
-        const int t = tid + it * TAU_BS;
-        ir[it] = 1.0 / qc[it][0];
-        pr[it] = gm1 * (qc[it][4] - 0.5 * ir[it] * (qc[it][1] * qc[it][1] + qc[it][2] * qc[it][2] + qc[it][3] * qc[it][3]));
-#pragma unroll
-        for (int v = 0; v < NV; ++v) acc[it][v] = 0.0;
-        (void)t;
-    }
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-#pragma unroll
-        for (int it = 0; it < TAU_NPT; ++it) {
-            const int t = tid + it * TAU_BS;
-            if (t < nO) {
-                double f[NV];
-                if (d == 0) flux_axis<0>(qc[it], ir[it], pr[it], f);
-                else if (d == 1) flux_axis<1>(qc[it], ir[it], pr[it], f);
-                else flux_axis<2>(qc[it], ir[it], pr[it], f);
-#pragma unroll
-                for (int v = 0; v < NV; ++v) Fb[v * nO + t] = f[v];
-            }
-        }
-        __syncthreads();
-        const int L = d == 0 ? o1 : (d == 1 ? o2 : o3);
-        const int nlines = nO / L;
-        for (int task = tid; task < NV * nlines; task += TAU_BS) {
-            const int v = task / nlines, l = task - v * nlines;
-            int base, stride;
-            if (d == 0) { base = l * o1; stride = 1; }
-            else if (d == 1) { base = (l % o1) + o1 * o2 * (l / o1); stride = o1; }
-            else { base = l; stride = o1 * o2; }
-            dline_dispatch(L, Fb + v * nO + base, stride);
-        }
-        __syncthreads();
-#pragma unroll
-        for (int it = 0; it < TAU_NPT; ++it) {
-            const int t = tid + it * TAU_BS;
-            if (t < nO)
-#pragma unroll
-                for (int v = 0; v < NV; ++v) acc[it][v] = fma(d == 0 ? sc0 : (d == 1 ? sc1 : sc2), Fb[v * nO + t], acc[it][v]);
-        }
-        __syncthreads();  // Fb reused by the next direction
-    }
-}
-
-__global__ void __launch_bounds__(TAU_BS, 1) k_tau2(Tau2Params P)
-{
-    extern __shared__ double sm[];
-    __shared__ double red[32];
-    __shared__ double Ts[NP * NP];
-    const int e = blockIdx.x;
-    const int tid = threadIdx.x;
-    const int N1 = P.orders[3 * e], N2 = P.orders[3 * e + 1], N3 = P.orders[3 * e + 2];
-    const int n1 = N1 + 1, n2 = N2 + 1, n3 = N3 + 1;
-    const int n = n1 * n2 * n3;
-    const double h0 = P.hgeo[3 * e], h1 = P.hgeo[3 * e + 1], h2 = P.hgeo[3 * e + 2];
-    const double sc0 = 2.0 / h0, sc1 = 2.0 / h1, sc2 = 2.0 / h2;
-    const long long o = P.off[e];
-    double* qs = sm;           // 5n fine state
-    double* Rs = qs + NV * n;  // 5n reference residual
-    double* Fb = Rs + NV * n;  // 5n scratch
-    for (int t = tid; t < NV * n; t += TAU_BS) qs[t] = P.q[o + t];
-    if (P.qref)
-        for (int t = tid; t < NV * n; t += TAU_BS) Rs[t] = P.qref[o + t];
-    __syncthreads();
-    double qc[TAU_NPT][NV], acc[TAU_NPT][NV];
-    if (!P.qref) {  // SAME reference: isolated fine residual (reading A4)
-#pragma unroll
-        for (int it = 0; it < TAU_NPT; ++it) {
-            const int t = tid + it * TAU_BS;
-#pragma unroll
-            for (int v = 0; v < NV; ++v) qc[it][v] = t < n ? qs[v * n + t] : (v == 0 ? 1.0 : 0.0);
-        }
-        tau_iso_residual(n1, n2, n3, n, qc, acc, Fb, sc0, sc1, sc2, P.gm1);
-#pragma unroll
-        for (int it = 0; it < TAU_NPT; ++it) {
-            const int t = tid + it * TAU_BS;
-            if (t < n)
-#pragma unroll
-                for (int v = 0; v < NV; ++v) Rs[v * n + t] = -acc[it][v];
-        }
-        __syncthreads();
-    }
-    double rn = 0.0;
-    for (int t = tid; t < NV * n; t += TAU_BS) rn = fmax(rn, fabs(Rs[t]));
-    rn = block_max(rn, red);
-    if (tid == 0)
-        for (int d = 0; d < 3; ++d) {
-            P.tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV + 0] = rn;
-            for (int p = (d == 0 ? N1 : (d == 1 ? N2 : N3)); p < DG_TAU_STRIDE_DEV; ++p)
-                P.tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV + p] = __longlong_as_double(0x7ff8000000000000LL);
-        }
-    const double Jel = h0 * h1 * h2 / 8.0;
-    for (int d = 0; d < 3; ++d) {
-        const int Nd = d == 0 ? N1 : (d == 1 ? N2 : N3);
-        const int nd = Nd + 1;
-        const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
-        for (int p = 1; p < Nd; ++p) {
-            const int o1 = d == 0 ? p + 1 : n1, o2 = d == 1 ? p + 1 : n2, o3 = d == 2 ? p + 1 : n3;
-            const int nO = o1 * o2 * o3;
-            __syncthreads();  // Ts reuse
-            for (int t = tid; t < (p + 1) * nd; t += TAU_BS) Ts[t] = P.tab->T[Nd][p][t];
-            __syncthreads();
-            int base_c[TAU_NPT], ic_c[TAU_NPT];
-#pragma unroll
-            for (int it = 0; it < TAU_NPT; ++it) {
-                const int t = tid + it * TAU_BS;
-                if (t < nO) {
-                    int ijk[3];
-                    node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
-                    const int ic = d == 0 ? ijk[0] : (d == 1 ? ijk[1] : ijk[2]);
-                    int i0 = ijk[0], j0 = ijk[1], k0 = ijk[2];
-                    if (d == 0) i0 = 0; else if (d == 1) j0 = 0; else k0 = 0;
-                    base_c[it] = i0 + n1 * (j0 + n2 * k0);
-                    ic_c[it] = ic;
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) {
-                        const double* ql = qs + v * n + base_c[it];
-                        double s = 0.0;
-                        for (int a = 0; a < nd; ++a) s = fma(Ts[ic * nd + a], ql[a * stride], s);
-                        qc[it][v] = s;
-                    }
-                } else {
-                    base_c[it] = 0;
-                    ic_c[it] = 0;
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) qc[it][v] = v == 0 ? 1.0 : 0.0;
-                }
-            }
-            tau_iso_residual(o1, o2, o3, nO, qc, acc, Fb, sc0, sc1, sc2, P.gm1);
-            double tmax = 0.0;
-#pragma unroll
-            for (int it = 0; it < TAU_NPT; ++it) {
-                const int t = tid + it * TAU_BS;
-                if (t < nO) {
-                    double scale = 1.0;
-                    if (P.formulation == 1) {
-                        int ijk[3];
-                        node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
-                        scale = Jel * c_w[o1 - 1][ijk[0]] * c_w[o2 - 1][ijk[1]] * c_w[o3 - 1][ijk[2]];
-                    }
-                    const int ic = ic_c[it];
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) {
-                        const double* rl = Rs + v * n + base_c[it];
-                        double s = 0.0;
-                        for (int a = 0; a < nd; ++a) s = fma(Ts[ic * nd + a], rl[a * stride], s);
-                        tmax = fmax(tmax, fabs(scale * (s + acc[it][v])));
-                    }
-                }
-            }
-            tmax = block_max(tmax, red);
-            if (tid == 0) P.tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV + p] = tmax;
-        }
-    }
-}
-
-}  // namespace dgtau
-
-namespace dgtau {
-
-// ---------------------------------------------------------------------------
-// tau-estimation v3: one CTA per coarse level (element e, direction d, order
-// p < N_d).  Many small CTAs per SM hide the per-level barrier latency; the
-// element's fine state / reference residual are read through L1 (each level
-// of an element reads the same 2 x 5n values, so they stay cache-resident).
-// ---------------------------------------------------------------------------
-
+// (element, direction, coarse order) of the curved tau kernel (k_tau_curved)
 struct TauLevel {
     int e, d, p, pad;
 };
-
-struct Tau3Params {
-    const double* q;
-    const double* qref;  // reference residual (SOLVER: non-isolated; SAME: isolated, computed first)
-    double* tau;         // [E][3][9]
-    const int* orders;
-    const long long* off;
-    const double* hgeo;
-    const TauLevel* levels;
-    const Tables* tab;
-    int formulation;
-    double gm1;
-};
-
-constexpr int TAU3_BS = 256;
-constexpr int TAU3_NPT = 3;  // 256 * 3 >= 648 = max coarse level size (8 x 9 x 9)
 
 // Exact integer quotient a / b for 0 <= a < 4096, 1 <= b < 1024 from the
 // correctly rounded float reciprocal: the float product's absolute error
@@ -255,154 +33,6 @@ __device__ __forceinline__ int fdiv(int a, float inv_b) { return __float2int_rz(
 __device__ __forceinline__ int var_of(int task, int nl)
 {
     return (task >= nl) + (task >= 2 * nl) + (task >= 3 * nl) + (task >= 4 * nl);
-}
-
-// All lines of one direction of a (5, o1, o2, o3) block, each thread one
-// (variable, line) task at a time; the D^{L-1} constants stay live across the
-// task loop (the switch selects the compile-time line length once).
-template <int L>
-__device__ __forceinline__ void sweep_lines(double* Fb, int nO, int o1, int o2, int dd)
-{
-    const int nlines = nO / L;
-    const float inv_o1 = 1.0f / (float)o1;
-    for (int task = threadIdx.x; task < NV * nlines; task += blockDim.x) {
-        const int v = var_of(task, nlines), l = task - v * nlines;
-        int base, str;
-        if (dd == 0) { base = l * L; str = 1; }
-        else if (dd == 1) { const int kk = fdiv(l, inv_o1); base = (l - kk * o1) + o1 * L * kk; str = o1; }
-        else { base = l; str = o1 * o2; }
-        dline_inplace<L>(Fb + v * nO + base, str);
-    }
-}
-
-__device__ __forceinline__ void sweep_dispatch(int L, double* Fb, int nO, int o1, int o2, int dd)
-{
-    switch (L) {
-        case 2: sweep_lines<2>(Fb, nO, o1, o2, dd); break;
-        case 3: sweep_lines<3>(Fb, nO, o1, o2, dd); break;
-        case 4: sweep_lines<4>(Fb, nO, o1, o2, dd); break;
-        case 5: sweep_lines<5>(Fb, nO, o1, o2, dd); break;
-        case 6: sweep_lines<6>(Fb, nO, o1, o2, dd); break;
-        case 7: sweep_lines<7>(Fb, nO, o1, o2, dd); break;
-        case 8: sweep_lines<8>(Fb, nO, o1, o2, dd); break;
-        default: sweep_lines<9>(Fb, nO, o1, o2, dd); break;
-    }
-}
-
-// Interpolation along d of the fine lines of 5 fields (fine line length ND,
-// p+1 coarse points): out[v][coarse node] for src = q or the reference
-// residual.  One (variable, line) task per thread; fine values read once.
-template <int ND>
-__device__ __forceinline__ void interp_lines(const double* __restrict__ src, int n, int stride_f, int n1, int n2,
-                                             double* out, int nO, int o1, int o2, int pc, int d, const double* Ts)
-{
-    const int nl = nO / pc;  // lines of the coarse block along d (= fine lines)
-    const int strc = d == 0 ? 1 : (d == 1 ? o1 : o1 * o2);
-    const float inv_n1 = 1.0f / (float)n1;
-    for (int task = threadIdx.x; task < NV * nl; task += blockDim.x) {
-        const int v = var_of(task, nl), l = task - v * nl;
-        int bf, bc;  // base of the line in the fine / coarse layouts
-        if (d == 0) { bf = l * n1; bc = l * pc; }
-        else if (d == 1) { const int k = fdiv(l, inv_n1), i = l - k * n1; bf = i + n1 * n2 * k; bc = i + o1 * pc * k; }
-        else { bf = l; bc = l; }
-        double f[ND];
-#pragma unroll
-        for (int a = 0; a < ND; ++a) f[a] = __ldg(src + (long long)v * n + bf + a * stride_f);
-        for (int ic = 0; ic < pc; ++ic) {
-            double s = Ts[ic * ND] * f[0];
-#pragma unroll
-            for (int a = 1; a < ND; ++a) s = fma(Ts[ic * ND + a], f[a], s);
-            out[v * nO + bc + ic * strc] = s;
-        }
-    }
-}
-
-__device__ __forceinline__ void interp_dispatch(int ND, const double* src, int n, int stride_f, int n1, int n2,
-                                                double* out, int nO, int o1, int o2, int pc, int d, const double* Ts)
-{
-    switch (ND) {
-        case 3: interp_lines<3>(src, n, stride_f, n1, n2, out, nO, o1, o2, pc, d, Ts); break;
-        case 4: interp_lines<4>(src, n, stride_f, n1, n2, out, nO, o1, o2, pc, d, Ts); break;
-        case 5: interp_lines<5>(src, n, stride_f, n1, n2, out, nO, o1, o2, pc, d, Ts); break;
-        case 6: interp_lines<6>(src, n, stride_f, n1, n2, out, nO, o1, o2, pc, d, Ts); break;
-        case 7: interp_lines<7>(src, n, stride_f, n1, n2, out, nO, o1, o2, pc, d, Ts); break;
-        case 8: interp_lines<8>(src, n, stride_f, n1, n2, out, nO, o1, o2, pc, d, Ts); break;
-        default: interp_lines<9>(src, n, stride_f, n1, n2, out, nO, o1, o2, pc, d, Ts); break;
-    }
-}
-
-__global__ void __launch_bounds__(TAU3_BS, 4) k_tau3(Tau3Params P)
-{
-    extern __shared__ double sm[];
-    __shared__ double red[32];
-    __shared__ double Ts[NP * NP];
-    const TauLevel lv = P.levels[blockIdx.x];
-    const int e = lv.e, d = lv.d, p = lv.p;
-    const int tid = threadIdx.x;
-    const int N1 = P.orders[3 * e], N2 = P.orders[3 * e + 1], N3 = P.orders[3 * e + 2];
-    const int n1 = N1 + 1, n2 = N2 + 1;
-    const int n = n1 * n2 * (N3 + 1);
-    const int Nd = d == 0 ? N1 : (d == 1 ? N2 : N3);
-    const int nd = Nd + 1;
-    const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
-    const int o1 = d == 0 ? p + 1 : n1, o2 = d == 1 ? p + 1 : n2, o3 = d == 2 ? p + 1 : N3 + 1;
-    const int nO = o1 * o2 * o3;
-    const double h0 = P.hgeo[3 * e], h1 = P.hgeo[3 * e + 1], h2 = P.hgeo[3 * e + 2];
-    const long long o = P.off[e];
-    double* Qc = sm;              // 5 nO coarse state
-    double* Rc = Qc + NV * nO;    // 5 nO interpolated reference residual
-    double* F0 = Rc + NV * nO;    // 3 x 5 nO fluxes f_0, f_1, f_2, then their derivatives
-    double* F1 = F0 + NV * nO;
-    double* F2 = F1 + NV * nO;
-    for (int t = tid; t < (p + 1) * nd; t += TAU3_BS) Ts[t] = P.tab->T[Nd][p][t];
-    __syncthreads();
-    // (A) q_c = T^{N_d -> p} q and T R along d (reading A3)
-    interp_dispatch(nd, P.q + o, n, stride, n1, n2, Qc, nO, o1, o2, p + 1, d, Ts);
-    interp_dispatch(nd, P.qref + o, n, stride, n1, n2, Rc, nO, o1, o2, p + 1, d, Ts);
-    __syncthreads();
-    // (B) the three Cartesian fluxes of the coarse state
-    for (int t = tid; t < nO; t += TAU3_BS) {
-        double qv[NV], f[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) qv[v] = Qc[v * nO + t];
-        const double ir = 1.0 / qv[0];
-        const double pr = P.gm1 * (qv[4] - 0.5 * ir * (qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]));
-        flux_axis<0>(qv, ir, pr, f);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) F0[v * nO + t] = f[v];
-        flux_axis<1>(qv, ir, pr, f);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) F1[v * nO + t] = f[v];
-        flux_axis<2>(qv, ir, pr, f);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) F2[v * nO + t] = f[v];
-    }
-    __syncthreads();
-    // (C) D^{O_d'} along each direction d' (independent buffers: no barrier between)
-    sweep_dispatch(o1, F0, nO, o1, o2, 0);
-    sweep_dispatch(o2, F1, nO, o1, o2, 1);
-    sweep_dispatch(o3, F2, nO, o1, o2, 2);
-    __syncthreads();
-    // (D) tau~ = T R - Qdot_c = T R + sum_d' (2/h_d') D f_d'; traditional * J w w w
-    const double sc0 = 2.0 / h0, sc1 = 2.0 / h1, sc2 = 2.0 / h2;
-    const double Jel = h0 * h1 * h2 / 8.0;
-    double tmax = 0.0;
-    for (int t = tid; t < nO; t += TAU3_BS) {
-        double scale = 1.0;
-        if (P.formulation == 1) {
-            int i, j, k;
-            node_ijk(t, o1, o2, i, j, k);
-            scale = Jel * c_w[o1 - 1][i] * c_w[o2 - 1][j] * c_w[o3 - 1][k];
-        }
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            const int ix = v * nO + t;
-            const double acc = fma(sc2, F2[ix], fma(sc1, F1[ix], sc0 * F0[ix]));
-            tmax = fmax(tmax, fabs(scale * (Rc[ix] + acc)));
-        }
-    }
-    tmax = block_max(tmax, red);
-    if (tid == 0) P.tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV + p] = tmax;
 }
 
 // tau[e][d][0] = ||Qdot_ref,e||_inf and NaN for p >= N_d (one CTA per element)
