@@ -206,6 +206,72 @@ __device__ void element_metrics(const CurvedMesh& cm, int e, int o1, int o2, int
     __syncthreads();
 }
 
+// As element_metrics in plain fp64 (coarse tau levels, reading R6): X = T^{g->o}
+// Xgeo, derivatives by D^o, cross-product form; Xs: 3 no doubles of scratch.
+__device__ void element_metrics_fp64(const CurvedMesh& cm, int e, int o1, int o2, int o3, const Tables* tab,
+                                     double* Xs, double* Mout)
+{
+    const int no = o1 * o2 * o3;
+    const int ga = cm.g1 + 1, gb = cm.g2 + 1;
+    const double* G = cm.geo + (long long)e * 3 * cm.ng;
+    const double* T1 = tab->T[cm.g1][o1 - 1];
+    const double* T2 = tab->T[cm.g2][o2 - 1];
+    const double* T3 = tab->T[cm.g3][o3 - 1];
+    for (int t = threadIdx.x; t < no; t += blockDim.x) {
+        int i, j, k;
+        node_ijk(t, o1, o2, i, j, k);
+        double x[3] = {0.0, 0.0, 0.0};
+        for (int c = 0; c <= cm.g3; ++c) {
+            const double w3 = T3[k * (cm.g3 + 1) + c];
+            for (int b = 0; b <= cm.g2; ++b) {
+                const double w23 = w3 * T2[j * gb + b];
+                for (int a = 0; a <= cm.g1; ++a) {
+                    const double wgt = w23 * T1[i * ga + a];
+                    const int gi = a + ga * (b + gb * c);
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) x[q] = fma(wgt, __ldg(G + q * cm.ng + gi), x[q]);
+                }
+            }
+        }
+        Xs[t] = x[0];
+        Xs[no + t] = x[1];
+        Xs[2 * no + t] = x[2];
+    }
+    __syncthreads();
+    const double* D1 = tab->D[o1 - 1];
+    const double* D2 = tab->D[o2 - 1];
+    const double* D3 = tab->D[o3 - 1];
+    for (int t = threadIdx.x; t < no; t += blockDim.x) {
+        int i, j, k;
+        node_ijk(t, o1, o2, i, j, k);
+        double dx[3][3];
+        for (int c = 0; c < 3; ++c) {
+            const double* X = Xs + c * no;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+            for (int m = 0; m < o1; ++m) s0 = fma(D1[i * o1 + m], X[m + o1 * (j + o2 * k)], s0);
+            for (int m = 0; m < o2; ++m) s1 = fma(D2[j * o2 + m], X[i + o1 * (m + o2 * k)], s1);
+            for (int m = 0; m < o3; ++m) s2 = fma(D3[k * o3 + m], X[i + o1 * (j + o2 * m)], s2);
+            dx[0][c] = s0;
+            dx[1][c] = s1;
+            dx[2][c] = s2;
+        }
+        const double* xa = dx[0];
+        const double* xb = dx[1];
+        const double* xc = dx[2];
+        double c1[3], c2[3], c3[3];
+        c1[0] = xb[1] * xc[2] - xb[2] * xc[1]; c1[1] = xb[2] * xc[0] - xb[0] * xc[2]; c1[2] = xb[0] * xc[1] - xb[1] * xc[0];
+        c2[0] = xc[1] * xa[2] - xc[2] * xa[1]; c2[1] = xc[2] * xa[0] - xc[0] * xa[2]; c2[2] = xc[0] * xa[1] - xc[1] * xa[0];
+        c3[0] = xa[1] * xb[2] - xa[2] * xb[1]; c3[1] = xa[2] * xb[0] - xa[0] * xb[2]; c3[2] = xa[0] * xb[1] - xa[1] * xb[0];
+        for (int q = 0; q < 3; ++q) {
+            Mout[q * no + t] = c1[q];
+            Mout[(3 + q) * no + t] = c2[q];
+            Mout[(6 + q) * no + t] = c3[q];
+        }
+        Mout[9 * no + t] = xa[0] * c1[0] + xa[1] * c1[1] + xa[2] * c1[2];
+    }
+    __syncthreads();
+}
+
 struct MetParams {
     CurvedMesh cm;
     const int* orders;
@@ -876,7 +942,7 @@ __global__ void __launch_bounds__(CBS) k_tau_curved(CTauParams P)
     double* F = Rc + NV * nO;     // 5 nO (also 3 nO coordinates at first)
     double* A = F + NV * nO;      // 5 nO
     double* GA = A + NV * nO;     // 15 nO (NS)
-    element_metrics(P.cm, e, o1, o2, o3, P.tdd, reinterpret_cast<dd*>(F), Mc);  // F, A: 10 nO >= 6 nO scratch
+    element_metrics_fp64(P.cm, e, o1, o2, o3, P.tab, F, Mc);  // F, A: 10 nO >= 3 nO scratch
     const long long o = P.off[e];
     const double* T = P.tab->T[nd - 1][p];
     for (int t = threadIdx.x; t < nO; t += CBS) {
