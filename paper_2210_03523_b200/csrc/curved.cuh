@@ -272,7 +272,14 @@ __device__ void element_metrics_fp64(const CurvedMesh& cm, int e, int o1, int o2
     __syncthreads();
 }
 
+// one launch per size class: CTA b handles element perm[pbase + b]
+struct SizeClass {
+    int base, count, maxn;
+};
+
 struct MetParams {
+    const int* perm;
+    int pbase;
     CurvedMesh cm;
     const int* orders;
     const long long* off;  // state offsets (metrics at 2x)
@@ -283,7 +290,7 @@ struct MetParams {
 __global__ void __launch_bounds__(CBS) k_metrics(MetParams P)
 {
     extern __shared__ double sm[];
-    const int e = blockIdx.x;
+    const int e = P.perm[P.pbase + blockIdx.x];
     const int o1 = P.orders[3 * e] + 1, o2 = P.orders[3 * e + 1] + 1, o3 = P.orders[3 * e + 2] + 1;
     const int no = o1 * o2 * o3;
     dd* Xs = reinterpret_cast<dd*>(sm);
@@ -320,6 +327,8 @@ __device__ __forceinline__ void stage_D(double (*Ds)[NP * NP], const Tables* tab
 }
 
 struct CurvedParams {
+    const int* perm;  // element of CTA b: perm[pbase + b]
+    int pbase;
     const double* q;
     double* out;            // mode 0: qdot / grad (k_grad); mode 1: q' (RK)
     double* g;              // RK register
@@ -357,7 +366,7 @@ __global__ void __launch_bounds__(CBS) k_grad(CurvedParams P)
 {
     extern __shared__ double sm[];
     __shared__ double Ds[3][NP * NP];
-    const int e = blockIdx.x;
+    const int e = P.perm[P.pbase + blockIdx.x];
     const int n1 = P.orders[3 * e] + 1, n2 = P.orders[3 * e + 1] + 1, n3 = P.orders[3 * e + 2] + 1;
     stage_D(Ds, P.tab, n1, n2, n3);
     const int n = n1 * n2 * n3;
@@ -459,7 +468,7 @@ __global__ void __launch_bounds__(CBS, 4) k_res_curved(CurvedParams P)
     extern __shared__ double sm[];
     __shared__ double red[32];
     __shared__ double Ds[3][NP * NP];
-    const int e = blockIdx.x;
+    const int e = P.perm[P.pbase + blockIdx.x];
     const int n1 = P.orders[3 * e] + 1, n2 = P.orders[3 * e + 1] + 1, n3 = P.orders[3 * e + 2] + 1;
     stage_D(Ds, P.tab, n1, n2, n3);
     const int n = n1 * n2 * n3;
@@ -918,6 +927,7 @@ struct CTauParams {
     CurvedMesh cm;
     const Tables* tab;
     int formulation;
+    int lbase;  // size class: CTA b handles level lbase + b
     PhysDev ph;
 };
 
@@ -925,7 +935,7 @@ __global__ void __launch_bounds__(CBS) k_tau_curved(CTauParams P)
 {
     extern __shared__ double sm[];
     __shared__ double red[32];
-    const TauLevel lv = P.levels[blockIdx.x];
+    const TauLevel lv = P.levels[P.lbase + blockIdx.x];
     const int e = lv.e, d = lv.d, p = lv.p;
     const int n1 = P.orders[3 * e] + 1, n2 = P.orders[3 * e + 1] + 1, n3 = P.orders[3 * e + 2] + 1;
     const int n = n1 * n2 * n3;

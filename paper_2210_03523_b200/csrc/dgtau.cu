@@ -99,6 +99,10 @@ struct dg_ctx {
     FaceInfo* d_finfo = nullptr;
     SlotInfo* d_slots = nullptr;
     TauLevel* d_levels = nullptr;
+    // curved kernels run one CTA per element (level): elements sorted by node
+    // count into size classes, each launched with its own dynamic shared memory
+    int* d_eperm = nullptr;
+    std::vector<SizeClass> ecls_own, ecls_all, lcls;
     TauGroup* d_tgroups = nullptr;  // k_tau5 (element, direction, level group) work list
     int ntgroups = 0;
     size_t tau5_smem = 0;
@@ -379,6 +383,7 @@ void dg_destroy(dg_ctx* ctx)
     dfree(ctx->d_fcta);
     dfree(ctx->d_slots);
     dfree(ctx->d_levels);
+    dfree(ctx->d_eperm);
     dfree(ctx->d_tgroups);
     dfree(ctx->d_ref_scratch);
     dfree(ctx->d_tr_orders);
@@ -450,6 +455,23 @@ dg_status dg_mesh_upload(dg_ctx* ctx, int E, const int32_t* nbr_host, const int3
     CK(upload(ctx->d_h, ctx->h));
     ctx->have_orders = false;
     return DG_OK;
+}
+
+// Sort idx[begin,end) by size (largest first) and cut it into classes whose
+// largest member sets the class's shared-memory size (class edges ~ x1.25-1.5).
+static void size_classes(std::vector<int>& idx, const std::vector<int>& sz, int begin, int end,
+                         std::vector<SizeClass>& out)
+{
+    static const int edge[] = {16, 32, 48, 64, 80, 96, 128, 160, 192, 256, 320, 384, 512, 640, 1 << 30};
+    auto cls = [](int n) { int c = 0; while (n > edge[c]) ++c; return c; };
+    std::stable_sort(idx.begin() + begin, idx.begin() + end, [&](int a, int b) { return sz[a] > sz[b]; });
+    for (int i = begin; i < end;) {
+        const int c = cls(sz[idx[i]]);
+        int j = i;
+        while (j < end && cls(sz[idx[j]]) == c) ++j;
+        out.push_back(SizeClass{i, j - i, sz[idx[i]]});
+        i = j;
+    }
 }
 
 dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
@@ -696,7 +718,30 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
                 ctx->max_level = std::max(ctx->max_level, nO);
             }
     ctx->nlevels = (int)lv.size();
+    {
+        std::vector<int> lsz(lv.size()), li(lv.size());
+        for (size_t i = 0; i < lv.size(); ++i) {
+            const int* No = &ctx->orders[3 * lv[i].e];
+            lsz[i] = npts(No) / (No[lv[i].d] + 1) * (lv[i].p + 1);
+            li[i] = (int)i;
+        }
+        ctx->lcls.clear();
+        size_classes(li, lsz, 0, (int)lv.size(), ctx->lcls);
+        std::vector<TauLevel> ls(lv.size());
+        for (size_t i = 0; i < lv.size(); ++i) ls[i] = lv[li[i]];
+        lv.swap(ls);
+    }
     CK(upload(ctx->d_levels, lv));
+    {
+        std::vector<int> esz(E), ei(E);
+        for (int e = 0; e < E; ++e) { esz[e] = npts(&ctx->orders[3 * e]); ei[e] = e; }
+        ctx->ecls_own.clear();
+        ctx->ecls_all.clear();
+        size_classes(ei, esz, 0, ctx->n_own, ctx->ecls_own);
+        ctx->ecls_all = ctx->ecls_own;
+        size_classes(ei, esz, ctx->n_own, E, ctx->ecls_all);
+        CK(upload(ctx->d_eperm, ei));
+    }
     {   // k_tau5 work: (element, direction, coarse orders p0..p1) groups of <= TAU5_MAXN
         // coarse nodes (a single larger level forms its own group), largest first
         std::vector<TauGroup> tg;
@@ -761,8 +806,12 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
         M.off = ctx->d_off;
         M.met = ctx->d_met;
         M.tdd = ctx->d_tdd;
-        k_metrics<<<E, CBS, sizeof(double) * 16 * (size_t)ctx->maxn>>>(M);
-        ctx->launches++;
+        M.perm = ctx->d_eperm;
+        for (const SizeClass& c : ctx->ecls_all) {
+            M.pbase = c.base;
+            k_metrics<<<c.count, CBS, sizeof(double) * 16 * (size_t)c.maxn>>>(M);
+            ctx->launches++;
+        }
         CK(cudaGetLastError());
         // mortar metric at the mortar nodes, once per layout (k_mortar_curved2 reads it)
         dfree(ctx->d_mgeo);
@@ -841,6 +890,7 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
 {
     const bool ns = ctx->prm.physics == DG_NS;
     CurvedParams P{};
+    P.perm = ctx->d_eperm;
     P.q = q;
     P.g = g;
     P.dt = dt;
@@ -877,8 +927,11 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
         P.mode = 0;
         P.out = ctx->d_grad;
         P.mortarG = ctx->d_mortarGq;
-        k_grad<<<ctx->n_own, CBS, sizeof(double) * 35 * (size_t)ctx->maxn, st>>>(P);
-        ctx->launches++;
+        for (const SizeClass& c : ctx->ecls_own) {
+            P.pbase = c.base;
+            k_grad<<<c.count, CBS, sizeof(double) * 35 * (size_t)c.maxn, st>>>(P);
+            ctx->launches++;
+        }
     }
     if (mort) {
         M.mode = 0;
@@ -890,8 +943,11 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
     P.out = out;
     P.mortarG = ctx->d_mortarG;
     P.lam_max = lam_max;
-    k_res_curved<<<ctx->n_own, CBS, sizeof(double) * 15 * (size_t)ctx->maxn, st>>>(P);
-    ctx->launches++;
+    for (const SizeClass& c : ctx->ecls_own) {
+        P.pbase = c.base;
+        k_res_curved<<<c.count, CBS, sizeof(double) * 15 * (size_t)c.maxn, st>>>(P);
+        ctx->launches++;
+    }
     return check_stream_error(ctx, "curved residual launch");
 }
 
@@ -1185,6 +1241,7 @@ dg_status dg_gradient(dg_ctx* ctx, int variant, const double* q_dev, void* strea
     if (ctx->prm.physics != DG_NS || !ctx->curved) return fail(ctx, DG_EUNSUPPORTED, "gradient: NS on the curved path only");
     cudaStream_t st = (cudaStream_t)stream;
     CurvedParams P{};
+    P.perm = ctx->d_eperm;
     P.q = q_dev;
     P.variant = variant;
     P.orders = ctx->d_orders;
@@ -1215,8 +1272,11 @@ dg_status dg_gradient(dg_ctx* ctx, int variant, const double* q_dev, void* strea
     P.mode = 0;
     P.out = ctx->d_grad;
     P.mortarG = ctx->d_mortarGq;
-    k_grad<<<ctx->n_own, CBS, sizeof(double) * 35 * (size_t)ctx->maxn, st>>>(P);
-    ctx->launches++;
+    for (const SizeClass& c : ctx->ecls_own) {
+        P.pbase = c.base;
+        k_grad<<<c.count, CBS, sizeof(double) * 35 * (size_t)c.maxn, st>>>(P);
+        ctx->launches++;
+    }
     return check_stream_error(ctx, "k_grad launch");
 }
 
@@ -1361,7 +1421,11 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
             C.tab = ctx->d_tab;
             C.formulation = o->formulation;
             C.ph = phys_dev(ctx->prm);
-            k_tau_curved<<<ctx->nlevels, CBS, sm, st>>>(C);
+            for (const SizeClass& c : ctx->lcls) {
+                C.lbase = c.base;
+                k_tau_curved<<<c.count, CBS, sizeof(double) * (ctx->prm.physics == DG_NS ? 45 : 30) * (size_t)c.maxn, st>>>(C);
+                ctx->launches++;
+            }
         } else if (ctx->ntgroups > 0) {
             Tau5Params P;
             P.q = q_dev;
