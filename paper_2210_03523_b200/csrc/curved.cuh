@@ -911,6 +911,189 @@ __global__ void __launch_bounds__(CM_BS, 4) k_mortar_curved2(CMortarParams P, co
 }
 
 
+// Curved / NS mortar faces, v3: k_mortar3's pipeline (persistent CTAs, work
+// counter, cp.async prefetch of the next face's traces, constant-memory
+// operators, identity passes skipped) for curved meshes.  NIN components are
+// interpolated per side (5: q; 20: q and the BR1 gradient), NOUT projected
+// back (5: numerical flux; 15: BR1 terms q^ Ja_c).  Threads 0-127 work on
+// side L, 128-255 on side R; at the mortar points threads 0-80 evaluate the
+// Riemann flux (or the BR1 average) and, for NS, threads 128-208 the averaged
+// viscous flux.  Same arithmetic as k_mortar_curved2 (metric Ja of the mortar
+// from L, reading A6).
+constexpr int CM3_BS = 256, CM3_H = 128;
+
+template <int NIN, int NOUT>
+struct CM3 {
+    static constexpr int NC = NIN > NOUT ? NIN : NOUT;
+    static constexpr int ND = 4 * NIN * 81 + 4 * NC * 81 + NOUT * 81 + (NIN == 20 ? NV * 81 : 0);
+    static constexpr size_t smem = sizeof(double) * ND;
+};
+
+__device__ __forceinline__ void bar_half(int side)
+{
+    asm volatile("bar.sync %0, 128;\n" ::"r"(side + 1) : "memory");
+}
+
+// k_mortar3's mt_lines over NC components, line tasks strided by the half CTA
+template <int NC>
+__device__ __forceinline__ void cm3_lines(const double* __restrict__ A, const double* __restrict__ in,
+                                          double* __restrict__ out, int ni, int nl, bool along_a, int l)
+{
+    const int xs = along_a ? 1 : 9;
+    for (int task = l; task < NC * nl; task += CM3_H) {
+        const int c = task / nl, r = task - c * nl;
+        const double* x0 = in + c * 81 + (along_a ? r * 9 : r);
+        double* o = out + c * 81 + (along_a ? r * 9 : r);
+        double x[9];
+#pragma unroll
+        for (int a = 0; a < 9; ++a) x[a] = x0[a * xs];
+        for (int i = 0; i < ni; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int a = 0; a < 9; ++a) s = fma(A[i * 9 + a], x[a], s);
+            o[i * xs] = s;
+        }
+    }
+}
+
+template <int NIN, int NOUT>
+__global__ void __launch_bounds__(CM3_BS, 2) k_mortar_c3(CMortarParams P, const MortarFace* items, int nitems,
+                                                      int* queue, const double* mgeo, const long long* mgoff)
+{
+    using C = CM3<NIN, NOUT>;
+    constexpr int NC = C::NC;
+    extern __shared__ __align__(16) double cm_sm[];
+    double* TR = cm_sm;               // [stage][side][NIN * 81] traces (zero padded)
+    double* TM = TR + 4 * NIN * 81;   // [side][NC * 81] pass-A results
+    double* QM = TM + 2 * NC * 81;    // [side][NC * 81] pass-B results
+    double* GM = QM + 2 * NC * 81;    // [NOUT * 81] flux at the mortar points
+    double* GV = GM + NOUT * 81;      // [NV * 81] averaged viscous flux (NS)
+    const int t = threadIdx.x;
+    const int me = t >= CM3_H, l = t & (CM3_H - 1);
+    const int G = gridDim.x;
+    const int f0 = blockIdx.x;
+    if (f0 >= nitems) return;
+    for (int w = t; w < C::ND; w += CM3_BS) cm_sm[w] = 0.0;  // padding: finite once and for all
+    __syncthreads();
+    auto issue = [&](const MortarFace& it, int st) {
+        int NS[3];
+        mt_unpack(me ? it.ordR : it.ordL, NS);
+        const int d = it.d, ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
+        const int s1 = NS[ta] + 1, s2 = NS[tb] + 1;
+        const int st1 = NS[0] + 1, st2 = st1 * (NS[1] + 1);
+        const int sta = ta == 0 ? 1 : st1, stb = tb == 1 ? st1 : st2, std_ = d == 0 ? 1 : (d == 1 ? st1 : st2);
+        const int n = st2 * (NS[2] + 1);
+        const long long o = me ? it.offR : it.offL;
+        const int base = (me == 0 ? NS[d] * std_ : 0);
+        double* dstb = TR + (st * 2 + me) * NIN * 81;
+        for (int task = l; task < NIN * s2; task += CM3_H) {
+            const int c = task / s2, b = task - c * s2;
+            const double* src = (c < NV ? P.q + o + (long long)c * n : P.grad + 3 * o + (long long)(c - NV) * n) + base + b * stb;
+            double* dst = dstb + c * 81 + b * 9;
+            for (int a = 0; a < s1; ++a) cp_async8(dst + a, src + a * sta);
+        }
+    };
+    __shared__ int s_nn[2];
+    int fcur = f0, fnext = f0 + G;
+    MortarFace cur = items[f0];
+    MortarFace nxt = cur;
+    if (fnext < nitems) nxt = items[fnext];
+    issue(cur, 0);
+    asm volatile("cp.async.commit_group;\n" ::);
+    for (int k = 0;; ++k) {
+        if (fcur >= nitems) break;
+        if (t == 0) s_nn[k & 1] = 2 * G + atomicAdd(queue, 1);
+        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        __syncthreads();  // traces of face k landed; face k-1 fully consumed
+        const int fnn = s_nn[k & 1];
+        MortarFace nn = nxt;
+        if (fnn < nitems) nn = items[fnn];
+        if (fnext < nitems) issue(nxt, (k + 1) & 1);
+        asm volatile("cp.async.commit_group;\n" ::);
+
+        const int d = cur.d;
+        const int ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
+        int NL[3], NR[3];
+        mt_unpack(cur.ordL, NL);
+        mt_unpack(cur.ordR, NR);
+        const int M1 = max(NL[ta], NR[ta]), M2 = max(NL[tb], NR[tb]);
+        const int m1 = M1 + 1, m2 = M2 + 1, nm = m1 * m2;
+        const int sa_me = (me ? NR[ta] : NL[ta]) + 1, sb_me = (me ? NR[tb] : NL[tb]) + 1;
+        const bool ia = sa_me < m1, ib = sb_me < m2;
+        const bool ia0 = NL[ta] < M1, ia1 = NR[ta] < M1, ib0 = NL[tb] < M2, ib1 = NR[tb] < M2;
+        const double* opA = c_mop[ia ? mt_pair(sa_me - 1, M1) : 0];
+        const double* opB = c_mop[ib ? mt_pair(sb_me - 1, M2) : 0];
+        const double* TR0 = TR + (k & 1) * 2 * NIN * 81;
+        const double* TRme = TR0 + me * NIN * 81;
+        double* TMme = TM + me * NC * 81;
+        double* QMme = QM + me * NC * 81;
+        // side traces -> mortar: along a where s_a < m1, then along b where s_b < m2
+        if (ia) cm3_lines<NIN>(opA, TRme, TMme, m1, sb_me, true, l);
+        bar_half(me);
+        const double* Xme = ia ? TMme : TRme;
+        if (ib) cm3_lines<NIN>(opB, Xme, QMme, m2, m1, false, l);
+        __syncthreads();
+        const double* Y0 = ib0 ? QM : (ia0 ? TM : TR0);
+        const double* Y1 = ib1 ? QM + NC * 81 : (ia1 ? TM + NC * 81 : TR0 + NIN * 81);
+        const double* Jg = mgeo + mgoff[fcur];
+        const int tp = t & 127;  // mortar point handled by this thread (t < 81 or 128 <= t < 209)
+        const int pj = tp / 9, pi = tp - pj * 9;
+        if (tp < 81 && pi < m1 && pj < m2 && (me == 0 || NIN == 20)) {
+            const int jp = pj * m1 + pi;
+            const double jf[3] = {__ldg(Jg + jp), __ldg(Jg + nm + jp), __ldg(Jg + 2 * nm + jp)};
+            double qL[NV], qR[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) { qL[v] = Y0[v * 81 + tp]; qR[v] = Y1[v * 81 + tp]; }
+            if (me == 0) {
+                if (NOUT == 15) {  // BR1: q^ = average, times Ja_c
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) GM[(c * NV + v) * 81 + tp] = 0.5 * (qL[v] + qR[v]) * jf[c];
+                } else {
+                    const double S = sqrt(jf[0] * jf[0] + jf[1] * jf[1] + jf[2] * jf[2]);
+                    const double nrm[3] = {jf[0] / S, jf[1] / S, jf[2] / S};
+                    double F[NV];
+                    riemann(qL, qR, nrm, P.ph, F);
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) GM[v * 81 + tp] = F[v] * S;
+                }
+            } else {
+                double gL[15], gR[15], fL[NV], fR[NV];
+#pragma unroll
+                for (int c = 0; c < 15; ++c) { gL[c] = Y0[(NV + c) * 81 + tp]; gR[c] = Y1[(NV + c) * 81 + tp]; }
+                visc_dot(qL, gL, jf[0], jf[1], jf[2], P.ph, fL);
+                visc_dot(qR, gR, jf[0], jf[1], jf[2], P.ph, fR);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) GV[v * 81 + tp] = 0.5 * (fL[v] + fR[v]);
+            }
+        }
+        __syncthreads();
+        if (NIN == 20) {
+            for (int w = t; w < NV * 81; w += CM3_BS) GM[w] -= GV[w];
+            __syncthreads();
+        }
+        // exact L2 projection back to each side (identity passes skipped)
+        if (ia) cm3_lines<NOUT>(opA + 81, GM, TMme, sa_me, m2, true, l);
+        bar_half(me);
+        const double* Zme = ia ? TMme : GM;
+        if (ib) cm3_lines<NOUT>(opB + 81, Zme, QMme, sb_me, sa_me, false, l);
+        bar_half(me);
+        const double* W = ib ? QMme : Zme;
+        double* dstb = P.mortarG + (NOUT == 15 ? 3 : 1) * (me ? cur.moR : cur.moL);
+        for (int task = l; task < NOUT * sb_me; task += CM3_H) {  // one (c, b) row per task
+            const int c = task / sb_me, b = task - c * sb_me;
+            const double* src = W + c * 81 + b * 9;
+            double* dst = dstb + (c * sb_me + b) * sa_me;
+            for (int a = 0; a < sa_me; ++a) dst[a] = src[a];
+        }
+        fcur = fnext;
+        fnext = fnn;
+        cur = nxt;
+        nxt = nn;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // tau-estimation on curved elements (Euler or NS), one CTA per level (e,d,p):
 // coarse geometry = geometry polynomial at the coarse nodes, metrics by D^O;

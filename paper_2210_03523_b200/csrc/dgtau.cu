@@ -135,6 +135,7 @@ struct dg_ctx {
     res_launcher rtab[NP][NP][NP] = {};
     res_occupancy rocc[NP][NP][NP] = {};
     int nsm = 148;
+    int cm3_occ[3] = {1, 1, 1};  // resident k_mortar_c3 CTAs per SM: <5,5>, <20,5>, <5,15>
     FaceInfo* d_finfo_slot = nullptr;
     MortarFace* d_mfaces = nullptr;    // mortar faces (k_mortar3)
     long long* d_fofs_slot = nullptr;  // [elist][6] flux offset (into d_mortarG) of each face of each slot
@@ -329,6 +330,13 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         cudaFuncSetAttribute(k_tau, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
         cudaFuncSetAttribute(k_tau5, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 4096);  // 3.1 KB static
         cudaFuncSetAttribute(k_mortar_curved2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CM_SMEM);
+        cudaFuncSetAttribute(k_mortar_c3<5, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CM3<5, 5>::smem);
+        cudaFuncSetAttribute(k_mortar_c3<20, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CM3<20, 5>::smem);
+        cudaFuncSetAttribute(k_mortar_c3<5, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CM3<5, 15>::smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->cm3_occ[0], k_mortar_c3<5, 5>, CM3_BS, CM3<5, 5>::smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->cm3_occ[1], k_mortar_c3<20, 5>, CM3_BS, CM3<20, 5>::smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->cm3_occ[2], k_mortar_c3<5, 15>, CM3_BS, CM3<5, 15>::smem);
+        for (int& o : ctx->cm3_occ) o = std::max(1, o);
         cudaFuncSetAttribute(k_tau5, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
         cudaFuncSetAttribute(k_transfer, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
         const int limc = optin - 8192;  // curved kernels: up to ~6 KB static (staged D, reductions)
@@ -884,6 +892,25 @@ dg_status dg_node_coords(dg_ctx* ctx, double* X)
     return DG_OK;
 }
 
+// curved mortar faces (k_mortar_c3): mode 1 = BR1 gradient terms, mode 0 = fluxes
+static dg_status launch_mortar_curved(dg_ctx* ctx, const CMortarParams& M, cudaStream_t st)
+{
+    CK(cudaMemsetAsync(ctx->d_flag + 4, 0, sizeof(int), st));  // work counter
+    const bool ns = ctx->prm.physics == DG_NS;
+    int* qc = ctx->d_flag + 4;
+    if (M.mode == 1)
+        k_mortar_c3<5, 15><<<std::min(ctx->nmortar, ctx->cm3_occ[2] * ctx->nsm), CM3_BS, CM3<5, 15>::smem, st>>>(
+            M, ctx->d_mfaces, ctx->nmortar, qc, ctx->d_mgeo, ctx->d_mgoff);
+    else if (ns)
+        k_mortar_c3<20, 5><<<std::min(ctx->nmortar, ctx->cm3_occ[1] * ctx->nsm), CM3_BS, CM3<20, 5>::smem, st>>>(
+            M, ctx->d_mfaces, ctx->nmortar, qc, ctx->d_mgeo, ctx->d_mgoff);
+    else
+        k_mortar_c3<5, 5><<<std::min(ctx->nmortar, ctx->cm3_occ[0] * ctx->nsm), CM3_BS, CM3<5, 5>::smem, st>>>(
+            M, ctx->d_mfaces, ctx->nmortar, qc, ctx->d_mgeo, ctx->d_mgoff);
+    ctx->launches++;
+    return DG_OK;
+}
+
 static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* q, double* out, double* g,
                                         const double* dt, double A, double B, int mode, cudaStream_t st,
                                         unsigned long long* lam_max, int flags = 0)
@@ -921,8 +948,8 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
         if (mort) {
             M.mode = 1;
             M.mortarG = ctx->d_mortarGq;
-            k_mortar_curved2<<<std::min(ctx->nmortar, 4 * ctx->nsm), CM_BS, CM_SMEM, st>>>(M, ctx->d_mgeo, ctx->d_mgoff, ctx->nmortar);
-            ctx->launches++;
+            dg_status s = launch_mortar_curved(ctx, M, st);
+            if (s != DG_OK) return s;
         }
         P.mode = 0;
         P.out = ctx->d_grad;
@@ -936,8 +963,8 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
     if (mort) {
         M.mode = 0;
         M.mortarG = ctx->d_mortarG;
-        k_mortar_curved2<<<std::min(ctx->nmortar, 4 * ctx->nsm), CM_BS, CM_SMEM, st>>>(M, ctx->d_mgeo, ctx->d_mgoff, ctx->nmortar);
-        ctx->launches++;
+        dg_status s = launch_mortar_curved(ctx, M, st);
+        if (s != DG_OK) return s;
     }
     P.mode = mode;
     P.out = out;
@@ -1266,8 +1293,8 @@ dg_status dg_gradient(dg_ctx* ctx, int variant, const double* q_dev, void* strea
         M.ph = phys_dev(ctx->prm);
         M.mode = 1;
         M.mortarG = ctx->d_mortarGq;
-        k_mortar_curved2<<<std::min(ctx->nmortar, 4 * ctx->nsm), CM_BS, CM_SMEM, st>>>(M, ctx->d_mgeo, ctx->d_mgoff, ctx->nmortar);
-        ctx->launches++;
+        dg_status s = launch_mortar_curved(ctx, M, st);
+        if (s != DG_OK) return s;
     }
     P.mode = 0;
     P.out = ctx->d_grad;
