@@ -993,8 +993,10 @@ __global__ void __launch_bounds__(CM3_BS, 2) k_mortar_c3(CMortarParams P, const 
             for (int a = 0; a < s1; ++a) cp_async8(dst + a, src + a * sta);
         }
     };
+    // faces f0, f0 + G, f0 + 2G, then 3G + work counter; thread 0 fetches the
+    // counter one face ahead so the atomic's latency is not exposed
     __shared__ int s_nn[2];
-    int fcur = f0, fnext = f0 + G;
+    int fcur = f0, fnext = f0 + G, pend = f0 + 2 * G;
     MortarFace cur = items[f0];
     MortarFace nxt = cur;
     if (fnext < nitems) nxt = items[fnext];
@@ -1002,7 +1004,10 @@ __global__ void __launch_bounds__(CM3_BS, 2) k_mortar_c3(CMortarParams P, const 
     asm volatile("cp.async.commit_group;\n" ::);
     for (int k = 0;; ++k) {
         if (fcur >= nitems) break;
-        if (t == 0) s_nn[k & 1] = 2 * G + atomicAdd(queue, 1);
+        if (t == 0) {
+            s_nn[k & 1] = pend;
+            pend = 3 * G + atomicAdd(queue, 1);
+        }
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncthreads();  // traces of face k landed; face k-1 fully consumed
         const int fnn = s_nn[k & 1];
@@ -1018,6 +1023,18 @@ __global__ void __launch_bounds__(CM3_BS, 2) k_mortar_c3(CMortarParams P, const 
         mt_unpack(cur.ordR, NR);
         const int M1 = max(NL[ta], NR[ta]), M2 = max(NL[tb], NR[tb]);
         const int m1 = M1 + 1, m2 = M2 + 1, nm = m1 * m2;
+        // mortar metric of this thread's point, loaded now (used after the interpolation)
+        const int tp = t & 127;  // mortar point handled by this thread (t < 81 or 128 <= t < 209)
+        const int pj = tp / 9, pi = tp - pj * 9;
+        const bool pt_on = tp < 81 && pi < m1 && pj < m2 && (me == 0 || NIN == 20);
+        double jf[3] = {0.0, 0.0, 0.0};
+        if (pt_on) {
+            const double* Jg = mgeo + __ldg(mgoff + fcur);
+            const int jp = pj * m1 + pi;
+            jf[0] = __ldg(Jg + jp);
+            jf[1] = __ldg(Jg + nm + jp);
+            jf[2] = __ldg(Jg + 2 * nm + jp);
+        }
         const int sa_me = (me ? NR[ta] : NL[ta]) + 1, sb_me = (me ? NR[tb] : NL[tb]) + 1;
         const bool ia = sa_me < m1, ib = sb_me < m2;
         const bool ia0 = NL[ta] < M1, ia1 = NR[ta] < M1, ib0 = NL[tb] < M2, ib1 = NR[tb] < M2;
@@ -1035,12 +1052,7 @@ __global__ void __launch_bounds__(CM3_BS, 2) k_mortar_c3(CMortarParams P, const 
         __syncthreads();
         const double* Y0 = ib0 ? QM : (ia0 ? TM : TR0);
         const double* Y1 = ib1 ? QM + NC * 81 : (ia1 ? TM + NC * 81 : TR0 + NIN * 81);
-        const double* Jg = mgeo + mgoff[fcur];
-        const int tp = t & 127;  // mortar point handled by this thread (t < 81 or 128 <= t < 209)
-        const int pj = tp / 9, pi = tp - pj * 9;
-        if (tp < 81 && pi < m1 && pj < m2 && (me == 0 || NIN == 20)) {
-            const int jp = pj * m1 + pi;
-            const double jf[3] = {__ldg(Jg + jp), __ldg(Jg + nm + jp), __ldg(Jg + 2 * nm + jp)};
+        if (pt_on) {
             double qL[NV], qR[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) { qL[v] = Y0[v * 81 + tp]; qR[v] = Y1[v * 81 + tp]; }

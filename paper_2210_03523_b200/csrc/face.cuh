@@ -241,8 +241,9 @@ __global__ void __launch_bounds__(MT_BS, MT_MINB) k_mortar3(MortarParams P, cons
     };
     // faces: blockIdx.x, blockIdx.x + G, then dynamically from a work counter
     // (mortar sizes vary: a static round robin leaves a long tail)
+    // (faces f0, f0 + G, f0 + 2G, then 3G + counter fetched one face ahead)
     __shared__ int s_nn[2];
-    int fcur = f0, fnext = f0 + G;
+    int fcur = f0, fnext = f0 + G, pend = f0 + 2 * G;
     MortarFace cur = items[f0];
     MortarFace nxt = cur;
     if (fnext < nitems) nxt = items[fnext];
@@ -250,7 +251,10 @@ __global__ void __launch_bounds__(MT_BS, MT_MINB) k_mortar3(MortarParams P, cons
     asm volatile("cp.async.commit_group;\n" ::);
     for (int k = 0;; ++k) {
         if (fcur >= nitems) break;
-        if (t == 0) s_nn[k & 1] = 2 * G + atomicAdd(queue, 1);
+        if (t == 0) {
+            s_nn[k & 1] = pend;
+            pend = 3 * G + atomicAdd(queue, 1);
+        }
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         __syncthreads();  // traces of face k landed; face k-1 fully consumed
         const int fnn = s_nn[k & 1];
