@@ -957,7 +957,7 @@ __device__ __forceinline__ void cm3_lines(const double* __restrict__ A, const do
 }
 
 template <int NIN, int NOUT>
-__global__ void __launch_bounds__(CM3_BS, 2) k_mortar_c3(CMortarParams P, const MortarFace* items, int nitems,
+__global__ void __launch_bounds__(CM3_BS, NIN == 20 ? 2 : 3) k_mortar_c3(CMortarParams P, const MortarFace* items, int nitems,
                                                       int* queue, const double* mgeo, const long long* mgoff)
 {
     using C = CM3<NIN, NOUT>;
