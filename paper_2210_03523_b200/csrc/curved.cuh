@@ -1126,7 +1126,8 @@ struct CTauParams {
     PhysDev ph;
 };
 
-__global__ void __launch_bounds__(CBS) k_tau_curved(CTauParams P)
+template <int BS>
+__global__ void __launch_bounds__(BS) k_tau_curved(CTauParams P)
 {
     extern __shared__ double sm[];
     __shared__ double red[32];
@@ -1141,16 +1142,16 @@ __global__ void __launch_bounds__(CBS) k_tau_curved(CTauParams P)
     const bool ns = P.ph.physics == 1;
     __shared__ double Ds[3][NP * NP];
     stage_D(Ds, P.tab, o1, o2, o3);
-    double* Mc = sm;              // 10 nO metrics
-    double* Qc = Mc + 10 * nO;    // 5 nO
-    double* Rc = Qc + NV * nO;    // 5 nO
-    double* F = Rc + NV * nO;     // 5 nO (also 3 nO coordinates at first)
-    double* A = F + NV * nO;      // 5 nO
-    double* GA = A + NV * nO;     // 15 nO (NS)
+    double* Mc = sm;                         // 10 nO metrics
+    double* Qc = Mc + 10 * nO;               // 5 nO
+    double* Rc = Qc + NV * nO;               // 5 nO
+    double* GA = Rc + NV * nO;               // 15 nO (NS)
+    double* F = ns ? GA + 15 * nO : GA;      // 5 nO (NS gradient: 15 nO over F, A and 5 more)
+    double* A = F + NV * nO;                 // 5 nO
     element_metrics_fp64(P.cm, e, o1, o2, o3, P.tab, F, Mc);  // F, A: 10 nO >= 3 nO scratch
     const long long o = P.off[e];
     const double* T = P.tab->T[nd - 1][p];
-    for (int t = threadIdx.x; t < nO; t += CBS) {
+    for (int t = threadIdx.x; t < nO; t += BS) {
         int i, j, k;
         node_ijk(t, o1, o2, i, j, k);
         const int ic = d == 0 ? i : (d == 1 ? j : k);
@@ -1165,34 +1166,37 @@ __global__ void __launch_bounds__(CBS) k_tau_curved(CTauParams P)
             }
             Qc[v * nO + t] = s;
             Rc[v * nO + t] = r;
-            A[v * nO + t] = 0.0;
+            if (!ns) A[v * nO + t] = 0.0;
         }
     }
     __syncthreads();
-    if (ns) {  // isolated gradient: J g_k = sum_d' D^{d'} (Ja^{d'}_k q)
-        for (int t = threadIdx.x; t < 15 * nO; t += CBS) GA[t] = 0.0;
-        __syncthreads();
+    if (ns) {  // isolated gradient: J g_k = sum_d' D^{d'} (Ja^{d'}_k q), all k per direction
         for (int dd = 0; dd < 3; ++dd) {
             const int od = dd == 0 ? o1 : (dd == 1 ? o2 : o3);
             const int str = dd == 0 ? 1 : (dd == 1 ? o1 : o1 * o2);
             const double* Dd = Ds[dd];
-            for (int k = 0; k < 3; ++k) {
-                for (int t = threadIdx.x; t < nO; t += CBS)
-                    for (int v = 0; v < NV; ++v) F[v * nO + t] = Mc[(3 * dd + k) * nO + t] * Qc[v * nO + t];
-                __syncthreads();
-                for (int t = threadIdx.x; t < nO; t += CBS) {
-                    int ijk[3];
-                    node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
-                    const int a = dd == 0 ? ijk[0] : (dd == 1 ? ijk[1] : ijk[2]);
-                    const int base = t - a * str;
-                    for (int v = 0; v < NV; ++v) GA[(k * NV + v) * nO + t] += dsum(Dd, od, a, F + v * nO + base, str);
+            for (int t = threadIdx.x; t < nO; t += BS)
+                for (int k = 0; k < 3; ++k) {
+                    const double jak = Mc[(3 * dd + k) * nO + t];
+                    for (int v = 0; v < NV; ++v) F[(k * NV + v) * nO + t] = jak * Qc[v * nO + t];
                 }
-                __syncthreads();
+            __syncthreads();
+            for (int t = threadIdx.x; t < nO; t += BS) {
+                int ijk[3];
+                node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
+                const int a = dd == 0 ? ijk[0] : (dd == 1 ? ijk[1] : ijk[2]);
+                const int base = t - a * str;
+                for (int c = 0; c < 15; ++c) {
+                    const double s = dsum(Dd, od, a, F + c * nO + base, str);
+                    GA[c * nO + t] = dd == 0 ? s : GA[c * nO + t] + s;
+                }
             }
+            __syncthreads();
         }
-        for (int t = threadIdx.x; t < nO; t += CBS) {
+        for (int t = threadIdx.x; t < nO; t += BS) {
             const double iJ = 1.0 / Mc[9 * nO + t];
             for (int c = 0; c < 15; ++c) GA[c * nO + t] *= iJ;
+            for (int v = 0; v < NV; ++v) A[v * nO + t] = 0.0;
         }
         __syncthreads();
     }
@@ -1200,7 +1204,7 @@ __global__ void __launch_bounds__(CBS) k_tau_curved(CTauParams P)
         const int od = dd == 0 ? o1 : (dd == 1 ? o2 : o3);
         const int str = dd == 0 ? 1 : (dd == 1 ? o1 : o1 * o2);
         const double* Dd = Ds[dd];
-        for (int t = threadIdx.x; t < nO; t += CBS) {
+        for (int t = threadIdx.x; t < nO; t += BS) {
             double qv[NV], gv[15], Fv[NV];
             for (int v = 0; v < NV; ++v) qv[v] = Qc[v * nO + t];
             if (ns)
@@ -1209,7 +1213,7 @@ __global__ void __launch_bounds__(CBS) k_tau_curved(CTauParams P)
             for (int v = 0; v < NV; ++v) F[v * nO + t] = Fv[v];
         }
         __syncthreads();
-        for (int t = threadIdx.x; t < nO; t += CBS) {
+        for (int t = threadIdx.x; t < nO; t += BS) {
             int ijk[3];
             node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
             const int a = dd == 0 ? ijk[0] : (dd == 1 ? ijk[1] : ijk[2]);
@@ -1219,7 +1223,7 @@ __global__ void __launch_bounds__(CBS) k_tau_curved(CTauParams P)
         __syncthreads();
     }
     double tmax = 0.0;
-    for (int t = threadIdx.x; t < nO; t += CBS) {
+    for (int t = threadIdx.x; t < nO; t += BS) {
         int i, j, k;
         node_ijk(t, o1, o2, i, j, k);
         const double J = Mc[9 * nO + t];

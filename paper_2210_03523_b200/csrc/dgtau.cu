@@ -343,7 +343,9 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         cudaFuncSetAttribute(k_metrics, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
         cudaFuncSetAttribute(k_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
         cudaFuncSetAttribute(k_res_curved, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
-        cudaFuncSetAttribute(k_tau_curved, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
+        cudaFuncSetAttribute(k_tau_curved<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
+        cudaFuncSetAttribute(k_tau_curved<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
+        cudaFuncSetAttribute(k_tau_curved<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
         ctx->smem_limit = limc;
         cudaError_t e = cudaGetLastError();  // attribute errors are fatal here, not stale later
         if (e != cudaSuccess) {
@@ -1434,7 +1436,7 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
         k_tau_norm<<<ctx->n_own, 128, 0, st>>>(ref, tau_dev, ctx->d_orders, ctx->d_off);
         ctx->launches++;
         if (ctx->curved && ctx->nlevels > 0) {
-            const size_t sm = sizeof(double) * (ctx->prm.physics == DG_NS ? 45 : 30) * (size_t)ctx->max_level;
+            const size_t sm = sizeof(double) * (ctx->prm.physics == DG_NS ? 50 : 30) * (size_t)ctx->max_level;
             if ((long long)sm > ctx->smem_limit) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: coarse level too large for shared memory");
             CTauParams C;
             C.tdd = ctx->d_tdd;
@@ -1450,7 +1452,10 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
             C.ph = phys_dev(ctx->prm);
             for (const SizeClass& c : ctx->lcls) {
                 C.lbase = c.base;
-                k_tau_curved<<<c.count, CBS, sizeof(double) * (ctx->prm.physics == DG_NS ? 45 : 30) * (size_t)c.maxn, st>>>(C);
+                const size_t smc = sizeof(double) * (ctx->prm.physics == DG_NS ? 50 : 30) * (size_t)c.maxn;
+                if (c.maxn <= 64) k_tau_curved<64><<<c.count, 64, smc, st>>>(C);
+                else if (c.maxn <= 160) k_tau_curved<128><<<c.count, 128, smc, st>>>(C);
+                else k_tau_curved<256><<<c.count, 256, smc, st>>>(C);
                 ctx->launches++;
             }
         } else if (ctx->ntgroups > 0) {
