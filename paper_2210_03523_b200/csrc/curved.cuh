@@ -316,6 +316,26 @@ __device__ __forceinline__ double dsum(const double* Dd, int od, int a, const do
     return s0 + s1;
 }
 
+// as dsum, with the D row held in registers (loaded once for all components)
+struct DRow {
+    double r[NP];
+    __device__ __forceinline__ DRow(const double* Dd, int od, int a)
+    {
+#pragma unroll
+        for (int m = 0; m < NP; ++m) r[m] = m < od ? Dd[a * od + m] : 0.0;
+    }
+    __device__ __forceinline__ double sum(int od, const double* Fl, int stride) const
+    {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int m = 0; m < NP; m += 2) {
+            if (m < od) s0 = fma(r[m], Fl[m * stride], s0);
+            if (m + 1 < od) s1 = fma(r[m + 1], Fl[(m + 1) * stride], s1);
+        }
+        return s0 + s1;
+    }
+};
+
 // D^{o_d - 1} of the three directions into shared memory (Ds[d][a*o_d + m])
 __device__ __forceinline__ void stage_D(double (*Ds)[NP * NP], const Tables* tab, int o1, int o2, int o3)
 {
@@ -396,8 +416,9 @@ __global__ void __launch_bounds__(CBS) k_grad(CurvedParams P)
             node_ijk(t, n1, n2, ijk[0], ijk[1], ijk[2]);
             const int a = d == 0 ? ijk[0] : (d == 1 ? ijk[1] : ijk[2]);
             const int base = t - a * stride;
+            const DRow dr(Dd, od, a);
 #pragma unroll
-            for (int c = 0; c < 15; ++c) GA[c * n + t] += dsum(Dd, od, a, F + c * n + base, stride);
+            for (int c = 0; c < 15; ++c) GA[c * n + t] += dr.sum(od, F + c * n + base, stride);
         }
         __syncthreads();
         // lifting on the two faces normal to d: (qhat Ja_f - q_own Ja_own)/w
@@ -504,8 +525,9 @@ __global__ void __launch_bounds__(CBS, 4) k_res_curved(CurvedParams P)
             node_ijk(t, n1, n2, ijk[0], ijk[1], ijk[2]);
             const int a = d == 0 ? ijk[0] : (d == 1 ? ijk[1] : ijk[2]);
             const int base = t - a * stride;
+            const DRow dr(Dd, od, a);
 #pragma unroll
-            for (int v = 0; v < NV; ++v) A[v * n + t] += dsum(Dd, od, a, F + v * n + base, stride);
+            for (int v = 0; v < NV; ++v) A[v * n + t] += dr.sum(od, F + v * n + base, stride);
         }
         __syncthreads();
         if (P.variant == 0) {  // surface terms (isolated: G == Ft_own, no contribution)
@@ -1186,8 +1208,9 @@ __global__ void __launch_bounds__(BS) k_tau_curved(CTauParams P)
                 node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
                 const int a = dd == 0 ? ijk[0] : (dd == 1 ? ijk[1] : ijk[2]);
                 const int base = t - a * str;
+                const DRow dr(Dd, od, a);
                 for (int c = 0; c < 15; ++c) {
-                    const double s = dsum(Dd, od, a, F + c * nO + base, str);
+                    const double s = dr.sum(od, F + c * nO + base, str);
                     GA[c * nO + t] = dd == 0 ? s : GA[c * nO + t] + s;
                 }
             }
@@ -1218,7 +1241,8 @@ __global__ void __launch_bounds__(BS) k_tau_curved(CTauParams P)
             node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
             const int a = dd == 0 ? ijk[0] : (dd == 1 ? ijk[1] : ijk[2]);
             const int base = t - a * str;
-            for (int v = 0; v < NV; ++v) A[v * nO + t] += dsum(Dd, od, a, F + v * nO + base, str);
+            const DRow dr(Dd, od, a);
+            for (int v = 0; v < NV; ++v) A[v * nO + t] += dr.sum(od, F + v * nO + base, str);
         }
         __syncthreads();
     }
