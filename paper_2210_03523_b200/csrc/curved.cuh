@@ -498,38 +498,47 @@ __global__ void __launch_bounds__(CBS, 4) k_res_curved(CurvedParams P)
     const bool ns = P.ph.physics == 1;
     const double* GR = ns ? P.grad + 3 * o : nullptr;
     double* Q = sm;            // 5n
-    double* F = Q + NV * n;    // 5n
-    double* A = F + NV * n;    // 5n
-    for (int t = threadIdx.x; t < NV * n; t += CBS) {
-        Q[t] = P.q[o + t];
-        A[t] = 0.0;
+    double* F = Q + NV * n;    // 15n: contravariant fluxes Ft_d, d = 0..2
+    double* A = F + 15 * n;    // 5n
+    for (int t = threadIdx.x; t < NV * n; t += CBS) Q[t] = P.q[o + t];
+    __syncthreads();
+    // volume fluxes of the three directions from one read of q, grad q, Ja
+    for (int t = threadIdx.x; t < n; t += CBS) {
+        double qv[NV], gv[15];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) qv[v] = Q[v * n + t];
+        if (ns) load_grad(GR + t, n, gv);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            double Fv[NV];
+            contra_flux(qv, gv, __ldg(M + (3 * d) * n + t), __ldg(M + (3 * d + 1) * n + t), __ldg(M + (3 * d + 2) * n + t),
+                        P.ph, Fv);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) F[(d * NV + v) * n + t] = Fv[v];
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < n; t += CBS) {  // sum_d D^d Ft_d at node t
+        int ijk[3];
+        node_ijk(t, n1, n2, ijk[0], ijk[1], ijk[2]);
+        double acc[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+        for (int d = 0; d < 3; ++d) {
+            const int od = d == 0 ? n1 : (d == 1 ? n2 : n3);
+            const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
+            const int a = ijk[d];
+            const int base = t - a * stride;
+            const DRow dr(Ds[d], od, a);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) acc[v] += dr.sum(od, F + (d * NV + v) * n + base, stride);
+        }
+#pragma unroll
+        for (int v = 0; v < NV; ++v) A[v * n + t] = acc[v];
     }
     __syncthreads();
     for (int d = 0; d < 3; ++d) {
         const int od = d == 0 ? n1 : (d == 1 ? n2 : n3);
-        const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
-        const double* Dd = Ds[d];
-        for (int t = threadIdx.x; t < n; t += CBS) {
-            double qv[NV], gv[15], Fv[NV];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) qv[v] = Q[v * n + t];
-            if (ns) load_grad(GR + t, n, gv);
-            contra_flux(qv, gv, __ldg(M + (3 * d) * n + t), __ldg(M + (3 * d + 1) * n + t), __ldg(M + (3 * d + 2) * n + t),
-                        P.ph, Fv);
-#pragma unroll
-            for (int v = 0; v < NV; ++v) F[v * n + t] = Fv[v];
-        }
-        __syncthreads();
-        for (int t = threadIdx.x; t < n; t += CBS) {
-            int ijk[3];
-            node_ijk(t, n1, n2, ijk[0], ijk[1], ijk[2]);
-            const int a = d == 0 ? ijk[0] : (d == 1 ? ijk[1] : ijk[2]);
-            const int base = t - a * stride;
-            const DRow dr(Dd, od, a);
-#pragma unroll
-            for (int v = 0; v < NV; ++v) A[v * n + t] += dr.sum(od, F + v * n + base, stride);
-        }
-        __syncthreads();
         if (P.variant == 0) {  // surface terms (isolated: G == Ft_own, no contribution)
             const int nf = face_nodes(d, n1, n2, n3);
             for (int task = threadIdx.x; task < 2 * nf; task += CBS) {
@@ -537,10 +546,12 @@ __global__ void __launch_bounds__(CBS, 4) k_res_curved(CurvedParams P)
                 const int node = face_node(d, s, pt, n1, n2, n3);
                 double qo[NV], go[15], jo[3], Fo[NV], G[NV];
 #pragma unroll
-                for (int v = 0; v < NV; ++v) qo[v] = Q[v * n + node];
+                for (int v = 0; v < NV; ++v) {
+                    qo[v] = Q[v * n + node];
+                    Fo[v] = F[(d * NV + v) * n + node];
+                }
                 if (ns) load_grad(GR + node, n, go);
                 for (int c = 0; c < 3; ++c) jo[c] = __ldg(M + (3 * d + c) * n + node);
-                contra_flux(qo, go, jo[0], jo[1], jo[2], P.ph, Fo);
                 const FaceInfo fi = P.finfo[6 * e + f];
                 if (fi.kind == 1) {
                     const double* src = P.mortarG + fi.off + pt;

@@ -974,7 +974,7 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
     P.lam_max = lam_max;
     for (const SizeClass& c : ctx->ecls_own) {
         P.pbase = c.base;
-        k_res_curved<<<c.count, CBS, sizeof(double) * 15 * (size_t)c.maxn, st>>>(P);
+        k_res_curved<<<c.count, CBS, sizeof(double) * 25 * (size_t)c.maxn, st>>>(P);
         ctx->launches++;
     }
     return check_stream_error(ctx, "curved residual launch");
