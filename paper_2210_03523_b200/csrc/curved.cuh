@@ -384,6 +384,8 @@ __device__ __forceinline__ int face_node(int d, int s, int pt, int n1, int n2, i
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(CBS) k_grad(CurvedParams P)
 {
+    // one thread per node: the volume sum over the three directions and the
+    // lifting of the faces the node lies on, accumulated in registers
     extern __shared__ double sm[];
     __shared__ double Ds[3][NP * NP];
     const int e = P.perm[P.pbase + blockIdx.x];
@@ -392,86 +394,88 @@ __global__ void __launch_bounds__(CBS) k_grad(CurvedParams P)
     const int n = n1 * n2 * n3;
     const long long o = P.off[e];
     const double* M = P.met + 2 * o;
-    double* Q = sm;          // 5n
-    double* F = Q + NV * n;  // 15n: (Ja^d)_k q_v, k = 0..2
-    double* GA = F + 15 * n; // 15n
+    double* Q = sm;           // 5n
+    double* JA = Q + NV * n;  // 9n: (Ja^d)_k
     for (int t = threadIdx.x; t < NV * n; t += CBS) Q[t] = P.q[o + t];
-    for (int t = threadIdx.x; t < 15 * n; t += CBS) GA[t] = 0.0;
+    for (int t = threadIdx.x; t < 9 * n; t += CBS) JA[t] = __ldg(M + t);
     __syncthreads();
-    for (int d = 0; d < 3; ++d) {
-        const int od = d == 0 ? n1 : (d == 1 ? n2 : n3);
-        const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
-        const double* Dd = Ds[d];
-        for (int t = threadIdx.x; t < n; t += CBS) {  // all three k at once (one barrier per direction)
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const double jak = __ldg(M + (3 * d + k) * n + t);
-#pragma unroll
-                for (int v = 0; v < NV; ++v) F[(k * NV + v) * n + t] = jak * Q[v * n + t];
-            }
-        }
-        __syncthreads();
-        for (int t = threadIdx.x; t < n; t += CBS) {
-            int ijk[3];
-            node_ijk(t, n1, n2, ijk[0], ijk[1], ijk[2]);
-            const int a = d == 0 ? ijk[0] : (d == 1 ? ijk[1] : ijk[2]);
-            const int base = t - a * stride;
-            const DRow dr(Dd, od, a);
-#pragma unroll
-            for (int c = 0; c < 15; ++c) GA[c * n + t] += dr.sum(od, F + c * n + base, stride);
-        }
-        __syncthreads();
-        // lifting on the two faces normal to d: (qhat Ja_f - q_own Ja_own)/w
-        const int nf = face_nodes(d, n1, n2, n3);
-        for (int task = threadIdx.x; task < 2 * nf; task += CBS) {
-            const int s = task >= nf, pt = task - s * nf, f = 2 * d + s;
-            const int node = face_node(d, s, pt, n1, n2, n3);
-            double qo[NV], qh[NV], jo[3], jf[3];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) qo[v] = Q[v * n + node];
-            for (int c = 0; c < 3; ++c) jo[c] = __ldg(M + (3 * d + c) * n + node);
-            const FaceInfo fi = P.finfo[6 * e + f];
-            if (P.variant == 1) {  // isolated: qhat = own trace
-                for (int v = 0; v < NV; ++v) qh[v] = qo[v];
-                for (int c = 0; c < 3; ++c) jf[c] = jo[c];
-            } else if (fi.kind == 1) {  // mortar: projected qhat Ja_f terms
-                const double* src = P.mortarG + 3 * fi.off + pt;
-                const double w = s ? 1.0 : -1.0;
-                const double sc = w / P.tab->w[od - 1][0];
-                for (int c = 0; c < 3; ++c)
-                    for (int v = 0; v < NV; ++v)
-                        GA[(c * NV + v) * n + node] += sc * (src[(long long)(c * NV + v) * fi.n] - qo[v] * jo[c]);
-                continue;
-            } else if (fi.kind >= 2) {
-                for (int c = 0; c < 3; ++c) jf[c] = jo[c];
-                if (fi.kind == 2) {  // wall: zero velocity, keep rho and internal energy
-                    qh[0] = qo[0]; qh[1] = 0.0; qh[2] = 0.0; qh[3] = 0.0;
-                    qh[4] = qo[4] - 0.5 * (qo[1] * qo[1] + qo[2] * qo[2] + qo[3] * qo[3]) / qo[0];
-                } else {
-                    for (int v = 0; v < NV; ++v) qh[v] = 0.5 * (qo[v] + P.ph.qinf[v]);
-                }
-            } else {
-                const long long nb_node = fi.base + (long long)(d == 0 ? pt % n2 : pt % n1) * fi.sa +
-                                          (long long)(d == 0 ? pt / n2 : pt / n1) * fi.sb;
-                const double* qn = P.q + fi.off + nb_node;
-                for (int v = 0; v < NV; ++v) qh[v] = 0.5 * (qo[v] + __ldg(qn + (long long)v * fi.n));
-                if (s) {
-                    for (int c = 0; c < 3; ++c) jf[c] = jo[c];
-                } else {  // face metric from the L side (the neighbour)
-                    const double* Mn = P.met + 2 * fi.off + nb_node;
-                    for (int c = 0; c < 3; ++c) jf[c] = __ldg(Mn + (long long)(3 * d + c) * fi.n);
-                }
-            }
-            const double sc = (s ? 1.0 : -1.0) / P.tab->w[od - 1][0];
-            for (int c = 0; c < 3; ++c)
-                for (int v = 0; v < NV; ++v) GA[(c * NV + v) * n + node] += sc * (qh[v] * jf[c] - qo[v] * jo[c]);
-        }
-        __syncthreads();
-    }
+    const int nn[3] = {n1, n2, n3};
     double* out = P.out + 3 * o;
     for (int t = threadIdx.x; t < n; t += CBS) {
+        int ijk[3];
+        node_ijk(t, n1, n2, ijk[0], ijk[1], ijk[2]);
+        double g[15];
+#pragma unroll
+        for (int c = 0; c < 15; ++c) g[c] = 0.0;
+        // volume: J g_k = sum_d D^d ((Ja^d)_k q)
+        for (int d = 0; d < 3; ++d) {
+            const int od = nn[d];
+            const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
+            const int a = ijk[d];
+            const int base = t - a * stride;
+            const double* Dr = Ds[d] + a * od;
+            for (int m = 0; m < od; ++m) {
+                const int nm = base + m * stride;
+                const double dm = Dr[m];
+                double qv[NV];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) qv[v] = Q[v * n + nm];
+#pragma unroll
+                for (int k = 0; k < 3; ++k) {
+                    const double jk = JA[(3 * d + k) * n + nm];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) g[k * NV + v] = fma(dm, jk * qv[v], g[k * NV + v]);
+                }
+            }
+        }
+        // lifting on the faces through this node: (qhat Ja_f - q_own Ja_own)/w
+        double qo[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) qo[v] = Q[v * n + t];
+        for (int d = 0; d < 3; ++d) {
+            const int od = nn[d];
+            for (int s = 0; s < 2; ++s) {
+                if (ijk[d] != (s ? od - 1 : 0)) continue;
+                const int pt = d == 0 ? ijk[1] + n2 * ijk[2] : (d == 1 ? ijk[0] + n1 * ijk[2] : ijk[0] + n1 * ijk[1]);
+                const int f = 2 * d + s;
+                double qh[NV], jo[3], jf[3];
+                for (int c = 0; c < 3; ++c) jo[c] = JA[(3 * d + c) * n + t];
+                const double sc = (s ? 1.0 : -1.0) / P.tab->w[od - 1][0];
+                if (P.variant == 1) continue;  // isolated: qhat = own trace, no lifting
+                const FaceInfo fi = P.finfo[6 * e + f];
+                if (fi.kind == 1) {  // mortar: projected qhat Ja_f terms
+                    const double* src = P.mortarG + 3 * fi.off + pt;
+                    for (int c = 0; c < 3; ++c)
+                        for (int v = 0; v < NV; ++v)
+                            g[c * NV + v] += sc * (src[(long long)(c * NV + v) * fi.n] - qo[v] * jo[c]);
+                    continue;
+                } else if (fi.kind >= 2) {
+                    for (int c = 0; c < 3; ++c) jf[c] = jo[c];
+                    if (fi.kind == 2) {  // wall: zero velocity, keep rho and internal energy
+                        qh[0] = qo[0]; qh[1] = 0.0; qh[2] = 0.0; qh[3] = 0.0;
+                        qh[4] = qo[4] - 0.5 * (qo[1] * qo[1] + qo[2] * qo[2] + qo[3] * qo[3]) / qo[0];
+                    } else {
+                        for (int v = 0; v < NV; ++v) qh[v] = 0.5 * (qo[v] + P.ph.qinf[v]);
+                    }
+                } else {
+                    const long long nb_node = fi.base + (long long)(d == 0 ? pt % n2 : pt % n1) * fi.sa +
+                                              (long long)(d == 0 ? pt / n2 : pt / n1) * fi.sb;
+                    const double* qn = P.q + fi.off + nb_node;
+                    for (int v = 0; v < NV; ++v) qh[v] = 0.5 * (qo[v] + __ldg(qn + (long long)v * fi.n));
+                    if (s) {
+                        for (int c = 0; c < 3; ++c) jf[c] = jo[c];
+                    } else {  // face metric from the L side (the neighbour)
+                        const double* Mn = P.met + 2 * fi.off + nb_node;
+                        for (int c = 0; c < 3; ++c) jf[c] = __ldg(Mn + (long long)(3 * d + c) * fi.n);
+                    }
+                }
+                for (int c = 0; c < 3; ++c)
+                    for (int v = 0; v < NV; ++v) g[c * NV + v] += sc * (qh[v] * jf[c] - qo[v] * jo[c]);
+            }
+        }
         const double iJ = 1.0 / __ldg(M + 9 * n + t);
-        for (int c = 0; c < 15; ++c) out[c * n + t] = GA[c * n + t] * iJ;
+#pragma unroll
+        for (int c = 0; c < 15; ++c) out[c * n + t] = g[c] * iJ;
     }
 }
 

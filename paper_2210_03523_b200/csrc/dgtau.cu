@@ -958,7 +958,7 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
         P.mortarG = ctx->d_mortarGq;
         for (const SizeClass& c : ctx->ecls_own) {
             P.pbase = c.base;
-            k_grad<<<c.count, CBS, sizeof(double) * 35 * (size_t)c.maxn, st>>>(P);
+            k_grad<<<c.count, CBS, sizeof(double) * 14 * (size_t)c.maxn, st>>>(P);
             ctx->launches++;
         }
     }
@@ -1303,7 +1303,7 @@ dg_status dg_gradient(dg_ctx* ctx, int variant, const double* q_dev, void* strea
     P.mortarG = ctx->d_mortarGq;
     for (const SizeClass& c : ctx->ecls_own) {
         P.pbase = c.base;
-        k_grad<<<c.count, CBS, sizeof(double) * 35 * (size_t)c.maxn, st>>>(P);
+        k_grad<<<c.count, CBS, sizeof(double) * 14 * (size_t)c.maxn, st>>>(P);
         ctx->launches++;
     }
     return check_stream_error(ctx, "k_grad launch");
