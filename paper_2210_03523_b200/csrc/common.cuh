@@ -294,6 +294,13 @@ struct ResParams {
     unsigned long long* lam_max;  // if set (last RK stage): max CFL rate of the NEW state (bits of a double >= 0)
     double gamma;
     long long qlen;         // doubles in the state buffer q (bulk copies never read past it)
+    // fused step size (first stage of RK steps 2..n in dg_rk_steps): dt = cfl / *lam_in
+    // (the CFL rate accumulated by the previous step's last stage, as k_dt_final);
+    // CTA 0 of the launch with dt_out set stores dt there and zeroes *lam_zero
+    const unsigned long long* lam_in;
+    double cfl;
+    double* dt_out;
+    unsigned long long* lam_zero;
 };
 
 // One conforming (or boundary) face, Riemann flux computed once per face

@@ -45,8 +45,13 @@ struct GraphKey {
     int variant, mode;
     const void *q, *out, *g, *dt, *lam;
     double A, B;
+    const void *lam_in, *dt_out;
+    double cfl;
     bool operator<(const GraphKey& o) const
     {
+        if (lam_in != o.lam_in) return lam_in < o.lam_in;
+        if (dt_out != o.dt_out) return dt_out < o.dt_out;
+        if (cfl != o.cfl) return cfl < o.cfl;
         if (variant != o.variant) return variant < o.variant;
         if (mode != o.mode) return mode < o.mode;
         if (q != o.q) return q < o.q;
@@ -980,9 +985,17 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
     return check_stream_error(ctx, "curved residual launch");
 }
 
+// fused step size for the first RK stage (ResParams::lam_in ...), see dg_rk_steps
+struct DtFuse {
+    const unsigned long long* lam_in = nullptr;
+    double cfl = 0.0;
+    double* dt_out = nullptr;
+    unsigned long long* lam_zero = nullptr;
+};
+
 static dg_status launch_residual_direct(dg_ctx* ctx, int variant, const double* q, double* out, double* g,
                                         const double* dt, double A, double B, int mode, cudaStream_t st,
-                                        unsigned long long* lam_max)
+                                        unsigned long long* lam_max, const DtFuse& fz = DtFuse())
 {
     if (variant == DG_NONISOLATED && ctx->nmortar > 0) {
         MortarParams M;
@@ -1041,9 +1054,13 @@ static dg_status launch_residual_direct(dg_ctx* ctx, int variant, const double* 
     P.lam_max = lam_max;
     P.gamma = ctx->prm.gamma;
     P.qlen = ctx->off[ctx->E];
+    P.lam_in = fz.lam_in;
+    P.cfl = fz.cfl;
+    P.dt_out = fz.dt_out;
+    P.lam_zero = fz.lam_zero;
     if ((reinterpret_cast<uintptr_t>(q) & 15) != 0)
         return fail(ctx, DG_EINVAL, "residual: state pointer must be 16-byte aligned");
-    if (ctx->generic && lam_max) return fail(ctx, DG_EUNSUPPORTED, "fused dt needs the specialised kernels");
+    if (ctx->generic && (lam_max || fz.lam_in)) return fail(ctx, DG_EUNSUPPORTED, "fused dt needs the specialised kernels");
     if (ctx->generic) {
         k_residual<<<ctx->nwork, BLOCK, ctx->res_smem, st>>>(P);
         ctx->launches++;
@@ -1058,8 +1075,13 @@ static dg_status launch_residual_direct(dg_ctx* ctx, int variant, const double* 
             for (int i = 0; i < ns; ++i) CK(cudaStreamWaitEvent(ctx->side[i], ctx->ev_fork, 0));
             for (size_t i = 0; i < ctx->buckets.size(); ++i) {
                 const Bucket& b = ctx->buckets[i];
-                ctx->rtab[b.ord & 255][(b.ord >> 8) & 255][(b.ord >> 16) & 255](P, b.start0, b.nelem, b.nitems, b.grid,
-                                                                                ctx->side[i % ns]);
+                ResParams Pb = P;
+                if (i > 0) {  // one writer of the fused dt
+                    Pb.dt_out = nullptr;
+                    Pb.lam_zero = nullptr;
+                }
+                ctx->rtab[b.ord & 255][(b.ord >> 8) & 255][(b.ord >> 16) & 255](Pb, b.start0, b.nelem, b.nitems, b.grid,
+                                                                                    ctx->side[i % ns]);
                 ctx->launches++;
             }
             for (int i = 0; i < ns; ++i) {
@@ -1077,12 +1099,12 @@ static dg_status launch_residual_direct(dg_ctx* ctx, int variant, const double* 
 // streams included) and replayed with a single launch.  Cache per layout.
 static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, double* out, double* g, const double* dt,
                                  double A, double B, int mode, cudaStream_t st, unsigned long long* lam_max = nullptr,
-                                 int flags = 0)
+                                 int flags = 0, const DtFuse& fz = DtFuse())
 {
     if (ctx->curved) return launch_residual_curved(ctx, variant, q, out, g, dt, A, B, mode, st, lam_max, flags);
     if (ctx->generic || ctx->buckets.size() <= 1 || ctx->no_graphs)
-        return launch_residual_direct(ctx, variant, q, out, g, dt, A, B, mode, st, lam_max);
-    const GraphKey key{variant, mode, q, out, g, dt, lam_max, A, B};
+        return launch_residual_direct(ctx, variant, q, out, g, dt, A, B, mode, st, lam_max, fz);
+    const GraphKey key{variant, mode, q, out, g, dt, lam_max, A, B, fz.lam_in, fz.dt_out, fz.cfl};
     auto itg = ctx->graphs.find(key);
     if (itg == ctx->graphs.end()) {
         if (ctx->graphs.size() >= 32) {  // bounded cache: drop everything (layouts rarely need more)
@@ -1091,7 +1113,7 @@ static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, doub
         }
         const long long l0 = ctx->launches;
         CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed));
-        dg_status s = launch_residual_direct(ctx, variant, q, out, g, dt, A, B, mode, ctx->cap_stream, lam_max);
+        dg_status s = launch_residual_direct(ctx, variant, q, out, g, dt, A, B, mode, ctx->cap_stream, lam_max, fz);
         cudaGraph_t graph = nullptr;
         const cudaError_t ec = cudaStreamEndCapture(ctx->cap_stream, &graph);
         if (s != DG_OK) {
@@ -1219,22 +1241,50 @@ dg_status dg_rk_steps(dg_ctx* ctx, int nsteps, double* qa, double* qb, double* g
     static const double A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
     static const double B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
     cudaStream_t st = (cudaStream_t)stream;
+    if (ctx->curved) {
+        for (int s = 0; s < nsteps; ++s) {
+            double* q_in = (s & 1) ? qb : qa;
+            double* q_out = (s & 1) ? qa : qb;
+            const double* dt = (s & 1) ? dt_b : dt_a;
+            double* dt_next = (s & 1) ? dt_a : dt_b;
+            double* src[3] = {q_in, q_out, q_in};
+            double* dst[3] = {q_out, q_in, q_out};
+            for (int k = 0; k < 3; ++k) {
+                dg_status r = launch_residual(ctx, DG_NONISOLATED, src[k], dst[k], g, dt, A[k], B[k], 1, st,
+                                              k == 2 ? ctx->d_scratch + 4 : nullptr);
+                if (r != DG_OK) return r;
+            }
+            k_dt_final2<<<1, 1, 0, st>>>(ctx->d_scratch + 4, cfl, cfl, dt_next);
+            ctx->launches++;
+        }
+        return check_stream_error(ctx, "k_dt_final launch");
+    }
+    // Euler: the step size of step s >= 1 is formed by its first stage from
+    // the CFL rate the previous step's last stage accumulated (accumulators
+    // alternate: acc[s & 1] collects step s); one k_dt_final at the end
+    unsigned long long* acc[2] = {ctx->d_scratch + 4, ctx->d_scratch + 5};
+    CK(cudaMemsetAsync(acc[0], 0, sizeof(unsigned long long), st));
     for (int s = 0; s < nsteps; ++s) {
         double* q_in = (s & 1) ? qb : qa;
         double* q_out = (s & 1) ? qa : qb;
-        const double* dt = (s & 1) ? dt_b : dt_a;
-        double* dt_next = (s & 1) ? dt_a : dt_b;
+        double* dt = (s & 1) ? dt_b : dt_a;
         double* src[3] = {q_in, q_out, q_in};
         double* dst[3] = {q_out, q_in, q_out};
         for (int k = 0; k < 3; ++k) {
+            DtFuse fz;
+            if (k == 0 && s > 0) {
+                fz.lam_in = acc[(s - 1) & 1];
+                fz.cfl = cfl;
+                fz.dt_out = dt;
+                fz.lam_zero = acc[s & 1];
+            }
             dg_status r = launch_residual(ctx, DG_NONISOLATED, src[k], dst[k], g, dt, A[k], B[k], 1, st,
-                                          k == 2 ? ctx->d_scratch + 4 : nullptr);
+                                          k == 2 ? acc[s & 1] : nullptr, 0, fz);
             if (r != DG_OK) return r;
         }
-        if (ctx->curved) k_dt_final2<<<1, 1, 0, st>>>(ctx->d_scratch + 4, cfl, cfl, dt_next);
-        else k_dt_final<<<1, 1, 0, st>>>(ctx->d_scratch + 4, cfl, dt_next);
-        ctx->launches++;
     }
+    k_dt_final<<<1, 1, 0, st>>>(acc[(nsteps - 1) & 1], cfl, ((nsteps - 1) & 1) ? dt_a : dt_b);
+    ctx->launches++;
     return check_stream_error(ctx, "k_dt_final launch");
 }
 

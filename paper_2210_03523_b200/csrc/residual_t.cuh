@@ -339,7 +339,12 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
         mbar_init(&mbar[1], 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    const double dt = P.mode ? *P.dt : 0.0;
+    double dt = 0.0;
+    if (P.mode) dt = P.lam_in ? P.cfl / __longlong_as_double((long long)*P.lam_in) : *P.dt;
+    if (P.dt_out && blockIdx.x == 0 && tid == 0) {
+        *P.dt_out = dt;
+        *P.lam_zero = 0ull;
+    }
     double lmax = 0.0;
 
     // node phase of local item k (state stage k&1, meta k%3): 1/rho, p,
