@@ -1600,9 +1600,9 @@ dg_status dg_transfer(dg_ctx* ctx, const int32_t* new_orders, const double* q_ol
         offn[e + 1] = offn[e] + (long long)NV * npts(&new_orders[3 * e]);
         const int* a = &ctx->orders[3 * e];
         const int* b = &new_orders[3 * e];
-        smax[0] = std::max(smax[0], npts(a));
-        smax[1] = std::max(smax[1], (b[0] + 1) * (a[1] + 1) * (a[2] + 1));
-        smax[2] = std::max(smax[2], (b[0] + 1) * (b[1] + 1) * (a[2] + 1));
+        // every intermediate of the passes fits prod_d max(A_d, B_d) nodes
+        const int m = (std::max(a[0], b[0]) + 1) * (std::max(a[1], b[1]) + 1) * (std::max(a[2], b[2]) + 1);
+        smax[0] = smax[1] = smax[2] = std::max(smax[0], m);
     }
     cudaStream_t st = (cudaStream_t)stream;
     if (!ctx->d_tr_orders) {

@@ -672,46 +672,68 @@ struct TransferParams {
     const Tables* tab;
 };
 
+// one tensor pass along a direction of a [v][c2][c1][c0] block in shared
+// memory: nl lines per variable with input stride st, the m outputs of a line
+// from its a inputs (T zero padded 9 x 9, row i = output i)
+__device__ __forceinline__ void tr_pass(const double* __restrict__ T, const double* __restrict__ in,
+                                        double* __restrict__ out, int nin, int nout, int nl, int lines_per_plane,
+                                        int plane_in, int plane_out, int a, int m, int st)
+{
+    for (int task = threadIdx.x; task < NV * nl; task += blockDim.x) {
+        const int v = task / nl, l = task - v * nl;
+        const int pl = l / lines_per_plane, r = l - pl * lines_per_plane;  // (outer, inner) index of the line
+        const double* x0 = in + v * nin + pl * plane_in + r;
+        double* o = out + v * nout + pl * plane_out + r;
+        double x[NP];
+#pragma unroll
+        for (int b = 0; b < NP; ++b) x[b] = b < a ? x0[b * st] : 0.0;
+        for (int i = 0; i < m; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int b = 0; b < NP; ++b)
+                if (b < a) s += T[i * NP + b] * x[b];
+            o[i * st] = s;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(BLOCK) k_transfer(TransferParams P)
 {
+    // per direction: T^{A_d -> B_d} along lines (identity passes skipped: the
+    // table is exactly the identity then); [v][k][j][i] blocks in shared memory
     extern __shared__ double sm[];
+    __shared__ double Ts[3][NP * NP];
     const int e = blockIdx.x;
     int A[3], B[3];
     for (int d = 0; d < 3; ++d) { A[d] = P.oold[3 * e + d] + 1; B[d] = P.onew[3 * e + d] + 1; }
+    for (int t = threadIdx.x; t < 3 * NP * NP; t += blockDim.x) {
+        const int d = t / (NP * NP), r = t - d * (NP * NP), i = r / NP, b = r - i * NP;
+        Ts[d][r] = (i < B[d] && b < A[d]) ? P.tab->T[A[d] - 1][B[d] - 1][i * A[d] + b] : 0.0;
+    }
     const int nA = A[0] * A[1] * A[2];
-    const int n1 = B[0] * A[1] * A[2], n2 = B[0] * B[1] * A[2], nB = B[0] * B[1] * B[2];
-    double* s0 = sm;                 // 5 nA
-    double* s1 = s0 + NV * P.smax0;  // 5 n1
-    double* s2 = s1 + NV * P.smax1;  // 5 n2 (buffers sized by the host for this transfer)
+    double* buf[2] = {sm, sm + NV * P.smax0};
+    double* s2 = sm + NV * (P.smax0 + P.smax1);
     const long long oa = P.offold[e], ob = P.offnew[e];
-    for (int t = threadIdx.x; t < NV * nA; t += blockDim.x) s0[t] = P.qold[oa + t];
+    for (int t = threadIdx.x; t < NV * nA; t += blockDim.x) buf[0][t] = P.qold[oa + t];
     __syncthreads();
-    const double* Tx = P.tab->T[A[0] - 1][B[0] - 1];
-    for (int t = threadIdx.x; t < NV * n1; t += blockDim.x) {
-        const int v = t / n1, r = t % n1;
-        const int i = r % B[0], jk = r / B[0];
-        double s = 0.0;
-        for (int a = 0; a < A[0]; ++a) s += Tx[i * A[0] + a] * s0[v * nA + a + A[0] * jk];
-        s1[t] = s;
+    int c[3] = {A[0], A[1], A[2]};
+    const double* cur = buf[0];
+    int ncur = nA, nb = 0;
+    for (int d = 0; d < 3; ++d) {
+        if (A[d] == B[d]) continue;
+        double* out = (nb == 0) ? buf[1] : (cur == buf[1] ? s2 : buf[1]);
+        nb = 1;
+        const int st = d == 0 ? 1 : (d == 1 ? c[0] : c[0] * c[1]);
+        const int inner = st;                               // lines per plane (indices below d)
+        const int outer = d == 0 ? c[1] * c[2] : (d == 1 ? c[2] : 1);
+        const int nout = ncur / c[d] * B[d];
+        tr_pass(Ts[d], cur, out, ncur, nout, inner * outer, inner, inner * c[d], inner * B[d], c[d], B[d], st);
+        c[d] = B[d];
+        ncur = nout;
+        cur = out;
+        __syncthreads();
     }
-    __syncthreads();
-    const double* Ty = P.tab->T[A[1] - 1][B[1] - 1];
-    for (int t = threadIdx.x; t < NV * n2; t += blockDim.x) {
-        const int v = t / n2, r = t % n2;
-        const int i = r % B[0], j = (r / B[0]) % B[1], k = r / (B[0] * B[1]);
-        double s = 0.0;
-        for (int b = 0; b < A[1]; ++b) s += Ty[j * A[1] + b] * s1[v * n1 + i + B[0] * (b + A[1] * k)];
-        s2[t] = s;
-    }
-    __syncthreads();
-    const double* Tz = P.tab->T[A[2] - 1][B[2] - 1];
-    for (int t = threadIdx.x; t < NV * nB; t += blockDim.x) {
-        const int v = t / nB, r = t % nB;
-        const int ij = r % (B[0] * B[1]), k = r / (B[0] * B[1]);
-        double s = 0.0;
-        for (int c = 0; c < A[2]; ++c) s += Tz[k * A[2] + c] * s2[v * n2 + ij + B[0] * B[1] * c];
-        P.qnew[ob + t] = s;
-    }
+    for (int t = threadIdx.x; t < NV * ncur; t += blockDim.x) P.qnew[ob + t] = cur[t];
 }
 
 // ---------------------------------------------------------------------------

@@ -501,6 +501,7 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
     if (first + 2 * G < nitems) issue_meta(first + 2 * G, 2);
     asm volatile("cp.async.commit_group;\n" ::);
     mbar_wait(&mbar[0], 0);
+    __syncthreads();  // thread 0's hand copy of a clipped state's last double (issue_stage) is visible
     node_phase(0);
     __syncthreads();
     load_g(0);

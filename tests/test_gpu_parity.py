@@ -95,6 +95,29 @@ def test_rhs_parity(dg, orc, case, variant):
     assert rel_linf(r, ro, orders) < RES_TOL
 
 
+def test_first_launch_clipped_state(dg, orc):
+    """Regression: the last element's state envelope ends past the buffer, its
+    last double is copied by hand; a CTA whose FIRST item is that element must
+    see it (ragged_1to8: one-element buckets, first call of a fresh solver, the
+    isolated SAME reference of the tau-estimate)."""
+    mesh, orders, kw = CASES["ragged_1to8"]()
+    P = orc.Problem(mesh)
+    q = W.pulse_state(P.node_coords(orders), orders, **kw)
+    to = P.tau_estimate(orders, q, P.rhs(orders, q, orc.ISOLATED), 0)
+    ro = P.rhs(orders, q, orc.ISOLATED)
+    import torch
+
+    for _ in range(4):
+        S = dg.Solver(mesh)
+        S.set_orders(orders)
+        qd = torch.from_numpy(q).cuda()
+        tg = S.tau_estimate(qd, None, formulation=0, reference=dg.REF_SAME).cpu().numpy()
+        assert tau_rel(tg, to) < TAU_TOL
+        S2 = dg.Solver(mesh)
+        S2.set_orders(orders)
+        assert rel_linf(S2.rhs_eval(qd, variant=1).cpu().numpy(), ro, orders) < RES_TOL
+
+
 @pytest.mark.parametrize("case", ["cfg3_subbox_mixed", "ragged_1to8"])
 def test_freestream_and_conservation_gpu(dg, orc, case):
     import torch
