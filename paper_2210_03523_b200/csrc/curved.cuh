@@ -316,6 +316,42 @@ __device__ __forceinline__ double dsum(const double* Dd, int od, int a, const do
     return s0 + s1;
 }
 
+// sum_m D[a][m] Fl[c*cs + m*stride] for the NC components c of a line, with
+// the line length OD a compile-time constant (no predicated-off FMAs); the
+// same two partial sums as dsum, so the results are identical
+template <int OD, int NC, typename Op>
+__device__ __forceinline__ void dsum_comps_t(const double* Dr, const double* Fl, int cs, int stride, Op op)
+{
+    double r[OD];
+#pragma unroll
+    for (int m = 0; m < OD; ++m) r[m] = Dr[m];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int m = 0; m < OD; m += 2) {
+            s0 = fma(r[m], Fl[c * cs + m * stride], s0);
+            if (m + 1 < OD) s1 = fma(r[m + 1], Fl[c * cs + (m + 1) * stride], s1);
+        }
+        op(c, s0 + s1);
+    }
+}
+
+template <int NC, typename Op>
+__device__ __forceinline__ void dsum_comps(int od, const double* Dr, const double* Fl, int cs, int stride, Op op)
+{
+    switch (od) {
+        case 2: dsum_comps_t<2, NC>(Dr, Fl, cs, stride, op); break;
+        case 3: dsum_comps_t<3, NC>(Dr, Fl, cs, stride, op); break;
+        case 4: dsum_comps_t<4, NC>(Dr, Fl, cs, stride, op); break;
+        case 5: dsum_comps_t<5, NC>(Dr, Fl, cs, stride, op); break;
+        case 6: dsum_comps_t<6, NC>(Dr, Fl, cs, stride, op); break;
+        case 7: dsum_comps_t<7, NC>(Dr, Fl, cs, stride, op); break;
+        case 8: dsum_comps_t<8, NC>(Dr, Fl, cs, stride, op); break;
+        default: dsum_comps_t<9, NC>(Dr, Fl, cs, stride, op); break;
+    }
+}
+
 // as dsum, with the D row held in registers (loaded once for all components)
 struct DRow {
     double r[NP];
@@ -533,9 +569,8 @@ __global__ void __launch_bounds__(CBS, 4) k_res_curved(CurvedParams P)
             const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
             const int a = ijk[d];
             const int base = t - a * stride;
-            const DRow dr(Ds[d], od, a);
-#pragma unroll
-            for (int v = 0; v < NV; ++v) acc[v] += dr.sum(od, F + (d * NV + v) * n + base, stride);
+            dsum_comps<NV>(od, Ds[d] + a * od, F + d * NV * n + base, n, stride,
+                           [&](int v, double sv) { acc[v] += sv; });
         }
 #pragma unroll
         for (int v = 0; v < NV; ++v) A[v * n + t] = acc[v];
@@ -1223,11 +1258,9 @@ __global__ void __launch_bounds__(BS) k_tau_curved(CTauParams P)
                 node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
                 const int a = dd == 0 ? ijk[0] : (dd == 1 ? ijk[1] : ijk[2]);
                 const int base = t - a * str;
-                const DRow dr(Dd, od, a);
-                for (int c = 0; c < 15; ++c) {
-                    const double s = dr.sum(od, F + c * nO + base, str);
-                    GA[c * nO + t] = dd == 0 ? s : GA[c * nO + t] + s;
-                }
+                dsum_comps<15>(od, Dd + a * od, F + base, nO, str, [&](int c, double sv) {
+                    GA[c * nO + t] = dd == 0 ? sv : GA[c * nO + t] + sv;
+                });
             }
             __syncthreads();
         }
@@ -1256,8 +1289,7 @@ __global__ void __launch_bounds__(BS) k_tau_curved(CTauParams P)
             node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
             const int a = dd == 0 ? ijk[0] : (dd == 1 ? ijk[1] : ijk[2]);
             const int base = t - a * str;
-            const DRow dr(Dd, od, a);
-            for (int v = 0; v < NV; ++v) A[v * nO + t] += dr.sum(od, F + v * nO + base, str);
+            dsum_comps<NV>(od, Dd + a * od, F + base, nO, str, [&](int v, double sv) { A[v * nO + t] += sv; });
         }
         __syncthreads();
     }
