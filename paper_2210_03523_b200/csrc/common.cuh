@@ -296,7 +296,7 @@ struct ResParams {
     long long qlen;         // doubles in the state buffer q (bulk copies never read past it)
     // fused step size (first stage of RK steps 2..n in dg_rk_steps): dt = cfl / *lam_in
     // (the CFL rate accumulated by the previous step's last stage, as k_dt_final);
-    // CTA 0 of the launch with dt_out set stores dt there and zeroes *lam_zero
+    // CTA 0 of the launch stores dt to dt_out and zeroes *lam_zero (each if set)
     const unsigned long long* lam_in;
     double cfl;
     double* dt_out;

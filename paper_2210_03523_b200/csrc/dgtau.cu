@@ -45,12 +45,13 @@ struct GraphKey {
     int variant, mode;
     const void *q, *out, *g, *dt, *lam;
     double A, B;
-    const void *lam_in, *dt_out;
+    const void *lam_in, *dt_out, *lam_zero;
     double cfl;
     bool operator<(const GraphKey& o) const
     {
         if (lam_in != o.lam_in) return lam_in < o.lam_in;
         if (dt_out != o.dt_out) return dt_out < o.dt_out;
+        if (lam_zero != o.lam_zero) return lam_zero < o.lam_zero;
         if (cfl != o.cfl) return cfl < o.cfl;
         if (variant != o.variant) return variant < o.variant;
         if (mode != o.mode) return mode < o.mode;
@@ -1104,7 +1105,7 @@ static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, doub
     if (ctx->curved) return launch_residual_curved(ctx, variant, q, out, g, dt, A, B, mode, st, lam_max, flags);
     if (ctx->generic || ctx->buckets.size() <= 1 || ctx->no_graphs)
         return launch_residual_direct(ctx, variant, q, out, g, dt, A, B, mode, st, lam_max, fz);
-    const GraphKey key{variant, mode, q, out, g, dt, lam_max, A, B, fz.lam_in, fz.dt_out, fz.cfl};
+    const GraphKey key{variant, mode, q, out, g, dt, lam_max, A, B, fz.lam_in, fz.dt_out, fz.lam_zero, fz.cfl};
     auto itg = ctx->graphs.find(key);
     if (itg == ctx->graphs.end()) {
         if (ctx->graphs.size() >= 32) {  // bounded cache: drop everything (layouts rarely need more)
@@ -1262,8 +1263,11 @@ dg_status dg_rk_steps(dg_ctx* ctx, int nsteps, double* qa, double* qb, double* g
     // Euler: the step size of step s >= 1 is formed by its first stage from
     // the CFL rate the previous step's last stage accumulated (accumulators
     // alternate: acc[s & 1] collects step s); one k_dt_final at the end
+    // Both accumulators are zero on entry and on exit: step s >= 1 reads
+    // acc[(s-1)&1] in its first stage and zeroes it in its second; the final
+    // k_dt_final resets the last one (rk_step_dt / compute_dt use acc[0] too).
     unsigned long long* acc[2] = {ctx->d_scratch + 4, ctx->d_scratch + 5};
-    CK(cudaMemsetAsync(acc[0], 0, sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(acc[0], 0, 2 * sizeof(unsigned long long), st));
     for (int s = 0; s < nsteps; ++s) {
         double* q_in = (s & 1) ? qb : qa;
         double* q_out = (s & 1) ? qa : qb;
@@ -1276,7 +1280,8 @@ dg_status dg_rk_steps(dg_ctx* ctx, int nsteps, double* qa, double* qb, double* g
                 fz.lam_in = acc[(s - 1) & 1];
                 fz.cfl = cfl;
                 fz.dt_out = dt;
-                fz.lam_zero = acc[s & 1];
+            } else if (k == 1 && s > 0) {
+                fz.lam_zero = acc[(s - 1) & 1];
             }
             dg_status r = launch_residual(ctx, DG_NONISOLATED, src[k], dst[k], g, dt, A[k], B[k], 1, st,
                                           k == 2 ? acc[s & 1] : nullptr, 0, fz);

@@ -341,9 +341,9 @@ __global__ void __launch_bounds__(Shape<N1, N2, N3>::BS, Shape<N1, N2, N3>::MINB
     }
     double dt = 0.0;
     if (P.mode) dt = P.lam_in ? P.cfl / __longlong_as_double((long long)*P.lam_in) : *P.dt;
-    if (P.dt_out && blockIdx.x == 0 && tid == 0) {
-        *P.dt_out = dt;
-        *P.lam_zero = 0ull;
+    if (blockIdx.x == 0 && tid == 0) {
+        if (P.dt_out) *P.dt_out = dt;
+        if (P.lam_zero) *P.lam_zero = 0ull;
     }
     double lmax = 0.0;
 

@@ -204,6 +204,31 @@ def test_rk_steps(dg, orc, case):
     assert rel_linf(a, qo, orders) < RES_TOL
 
 
+@pytest.mark.parametrize("case", ["cfg1", "ragged_1to8"])
+@pytest.mark.parametrize("nsteps", [1, 2, 4])
+def test_rk_steps_then_step_dt(dg, orc, case, nsteps):
+    """The fused step size of dg_rk_steps leaves its CFL accumulators clean:
+    a following rk_step_dt / compute_dt gives the oracle's dt of the state."""
+    import torch
+
+    mesh, orders, kw = CASES[case]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, **kw)
+    dts = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in range(2)]
+    S.compute_dt(qd, 0.5, dts[0])
+    qa, qb, g = qd.clone(), torch.empty_like(qd), torch.empty_like(qd)
+    qs, dt_next = S.rk_steps(nsteps, qa, qb, g, dts[0], dts[1], 0.5)
+    qo = q.copy()
+    for _ in range(nsteps):
+        qo = P.rk3_step(orders, qo, P.dt(orders, qo, 0.5))
+    assert abs(dt_next.item() - P.dt(orders, qo, 0.5)) <= 1e-14 * dt_next.item()
+    q2, g2 = torch.empty_like(qs), torch.empty_like(qs)
+    dt2 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    S.rk_step_dt(qs.clone(), q2, g2, dt_next.clone(), 0.5, dt2)
+    qo = P.rk3_step(orders, qo, P.dt(orders, qo, 0.5))
+    assert abs(dt2.item() - P.dt(orders, qo, 0.5)) <= 1e-14 * dt2.item()
+    assert rel_linf(q2.cpu().numpy(), qo, orders) < RES_TOL
+
+
 def test_rk3_mixed_orders(dg, orc):
     import torch
 
