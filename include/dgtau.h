@@ -74,6 +74,15 @@ typedef struct {
     int reference;   /* DG_REF_SOLVER: qdot_ref_dev is the non-isolated residual
                         -M^-1 F^N(q); DG_REF_SAME: the isolated
                         fine residual, computed in-kernel (reading A4) */
+    int coarse_faces; /* 0 (default): ISOLATED coarse residuals, element-local
+                        (the paper's choice P:469).  1: NON-ISOLATED
+                        (reading R7): for direction d
+                        and level p the whole mesh is taken at O(e) = N(e) with
+                        O_d = min(p, N_d(e)); q and qdot_ref are interpolated per
+                        direction (A3), the coarse residual couples the elements
+                        through Roe faces / mortars (and BR1 for NS), and
+                        tau[e][d][p] (p < N_d(e)) is the max of |T_d R - Qdot_c|.
+                        Single rank only (DG_EUNSUPPORTED after dg_set_owned). */
 } dg_tau_opts;
 
 /* Order-selection policy (readings A13-A16). */

@@ -152,6 +152,46 @@ class Problem:
         lib().orc_tau_estimate(C.byref(self.m), _p(o), _p(q), _p(r), int(formulation), C.byref(self.ph), _p(tau))
         return tau
 
+    def tau_estimate_noniso(self, orders, q, qdot_ref, formulation=TAU_NEW):
+        """NON-ISOLATED tau-estimation ("uses all terms appearing in
+        the discrete DG variational formulation"; reading R7
+        for the neighbours' orders).  For direction d and level p:
+          O(e) = N(e) with O_d = min(p, N_d(e))        (the whole mesh at level (d, p))
+          q_c = I q, R_c = I Qdot_ref                  (per-direction interpolation, A3)
+          Qdot_c = non-isolated residual of the mesh at O   (Roe faces / mortars, eq DGSEMsystem)
+          tau~ = R_c - Qdot_c (new form); traditional: J w w w tau~
+          tau[e][d][p] = max over nodes, variables of |tau| for p < N_d(e)
+        Slot 0 holds ||Qdot_ref,e||_inf (reading R1).  Composition of the oracle's
+        own residual, transfer and mass operators, one level at a time."""
+        o = self._ord(orders)
+        q = np.ascontiguousarray(q, np.float64)
+        r = np.ascontiguousarray(qdot_ref, np.float64)
+        E = self.E
+        tau = np.full((E, 3, TAU_STRIDE), np.nan)
+        n = np.prod(o.astype(np.int64) + 1, axis=1)
+        off = np.concatenate([[0], np.cumsum(5 * n)])
+        for e in range(E):
+            tau[e, :, 0] = np.abs(r[off[e]:off[e + 1]]).max()
+        for d in range(3):
+            for p in range(1, int(o[:, d].max())):
+                oc = o.copy()
+                oc[:, d] = np.minimum(o[:, d], p)
+                qc = transfer(o, q, oc)
+                rc = transfer(o, r, oc)
+                diff = rc - self.rhs(oc, qc, NONISOLATED)
+                nc = np.prod(oc.astype(np.int64) + 1, axis=1)
+                offc = np.concatenate([[0], np.cumsum(5 * nc)])
+                scale = self.mass(oc) if formulation == TAU_TRADITIONAL else None
+                offm = np.concatenate([[0], np.cumsum(nc)])
+                for e in range(E):
+                    if p >= o[e, d]:
+                        continue
+                    de = diff[offc[e]:offc[e + 1]].reshape(5, nc[e])
+                    if scale is not None:
+                        de = de * scale[offm[e]:offm[e + 1]][None, :]
+                    tau[e, d, p] = np.abs(de).max()
+        return tau
+
     def tau_field(self, orders, q, qdot_ref, e, d, p, formulation=TAU_NEW):
         o = self._ord(orders)
         q = np.ascontiguousarray(q, np.float64)

@@ -115,6 +115,17 @@ struct dg_ctx {
     int nlevels = 0;
     int max_level = 0;
     double* d_ref_scratch = nullptr;  // isolated fine residual for DG_REF_SAME
+    // non-isolated tau-estimation (dg_tau_opts.coarse_faces): one sub-context
+    // per coarse level (d, p) holding the whole mesh at that level's orders
+    struct CoarseLevel {
+        dg_ctx* sub = nullptr;
+        int d = 0, p = 0, smax = 1;
+        int* d_orders = nullptr;
+        long long* d_off = nullptr;
+    };
+    std::vector<CoarseLevel> coarse;
+    double* d_cq = nullptr;  // coarse q, T_d R, Qdot_c (fine length each)
+    long long c_len = 0;
     int* d_tr_orders = nullptr;       // transfer scratch
     long long* d_tr_off = nullptr;
     std::vector<int> tr_orders_host;
@@ -370,9 +381,21 @@ static void drop_graphs(dg_ctx* ctx)
     ctx->graphs.clear();
 }
 
+static void drop_coarse(dg_ctx* ctx)
+{
+    for (auto& L : ctx->coarse) {
+        dg_destroy(L.sub);
+        dfree(L.d_orders);
+        dfree(L.d_off);
+    }
+    ctx->coarse.clear();
+}
+
 void dg_destroy(dg_ctx* ctx)
 {
     if (!ctx) return;
+    drop_coarse(ctx);
+    dfree(ctx->d_cq);
     drop_graphs(ctx);
     if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     for (int i = 0; i < dg_ctx::NSTREAMS; ++i) {
@@ -495,6 +518,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     if (!ctx) return DG_EINVAL;
     if (ctx->E == 0) return fail(ctx, DG_ESTATE, "set_orders: no mesh");
     drop_graphs(ctx);  // captured launches refer to the old plans
+    drop_coarse(ctx);  // non-isolated tau levels of the old layout
     const int E = ctx->E;
     for (long long i = 0; i < 3LL * E; ++i)
         if (orders_host[i] < 1 || orders_host[i] > NMAX) return fail(ctx, DG_EINVAL, "set_orders: order out of 1..8");
@@ -1453,6 +1477,89 @@ dg_status dg_jump_sweep(dg_ctx* ctx, const int32_t* orders_in_dev, int32_t* orde
     return check_stream_error(ctx, "k_jump launch");
 }
 
+// Non-isolated tau-estimation (dg_tau_opts.coarse_faces = 1, reading R7):
+// per coarse level (d, p) the state and the reference residual are
+// interpolated to the level's layout (k_transfer), the level's sub-context
+// evaluates the full (face-coupled) residual there, and k_tau_level takes
+// the per-element maxima.  Sub-contexts are built once per fine layout.
+static dg_status tau_noniso(dg_ctx* ctx, int formulation, const double* q_dev, const double* ref, double* tau_dev,
+                            cudaStream_t st)
+{
+    if (ctx->n_own != ctx->E) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: non-isolated levels need a single rank");
+    const int E = ctx->E;
+    const long long len = ctx->off[E];
+    if (ctx->coarse.empty()) {
+        int nmax[3] = {0, 0, 0};
+        for (int e = 0; e < E; ++e)
+            for (int d = 0; d < 3; ++d) nmax[d] = std::max(nmax[d], ctx->orders[3 * e + d]);
+        for (int d = 0; d < 3; ++d)
+            for (int p = 1; p < nmax[d]; ++p) {
+                dg_ctx::CoarseLevel L;
+                L.d = d;
+                L.p = p;
+                std::vector<int32_t> oc(ctx->orders.begin(), ctx->orders.end());
+                std::vector<long long> offc(E + 1, 0);
+                for (int e = 0; e < E; ++e) {
+                    const int* a = &ctx->orders[3 * e];
+                    oc[3 * e + d] = std::min(p, a[d]);
+                    offc[e + 1] = offc[e] + (long long)NV * npts(&oc[3 * e]);
+                    // every intermediate of the transfer passes fits prod max(old, new) + 1
+                    L.smax = std::max(L.smax, npts(a));
+                }
+                dg_status s = dg_create(&ctx->prm, &L.sub);
+                if (s != DG_OK) {
+                    drop_coarse(ctx);
+                    return fail(ctx, s, "tau_estimate: coarse level context");
+                }
+                ctx->coarse.push_back(L);  // owned from here (drop_coarse frees it)
+                dg_ctx::CoarseLevel& C = ctx->coarse.back();
+                if ((s = dg_mesh_upload(C.sub, E, ctx->nbr.data(), ctx->gorder, ctx->geo.data())) != DG_OK ||
+                    (s = dg_set_orders(C.sub, oc.data())) != DG_OK) {
+                    const std::string why = dg_last_error(C.sub);
+                    drop_coarse(ctx);
+                    return fail(ctx, s, "tau_estimate: coarse level: " + why);
+                }
+                if (upload(C.d_orders, oc) != cudaSuccess || upload(C.d_off, offc) != cudaSuccess) {
+                    drop_coarse(ctx);
+                    return fail(ctx, DG_ECUDA, "tau_estimate: coarse level tables");
+                }
+            }
+        if (ctx->c_len < 3 * len) {
+            dfree(ctx->d_cq);
+            CK(cudaMalloc(&ctx->d_cq, sizeof(double) * 3 * len));
+            ctx->c_len = 3 * len;
+        }
+    }
+    double* qc = ctx->d_cq;
+    double* rc = qc + len;
+    double* dc = rc + len;
+    for (const dg_ctx::CoarseLevel& L : ctx->coarse) {
+        TransferParams T;
+        T.oold = ctx->d_orders;
+        T.onew = L.d_orders;
+        T.offold = ctx->d_off;
+        T.offnew = L.d_off;
+        T.tab = ctx->d_tab;
+        T.smax0 = T.smax1 = T.smax2 = L.smax;
+        const size_t sm = sizeof(double) * NV * 3 * (size_t)L.smax;
+        T.qold = q_dev;
+        T.qnew = qc;
+        k_transfer<<<E, BLOCK, sm, st>>>(T);
+        T.qold = ref;
+        T.qnew = rc;
+        k_transfer<<<E, BLOCK, sm, st>>>(T);
+        ctx->launches += 2;
+        dg_status s = launch_residual(L.sub, DG_NONISOLATED, qc, dc, nullptr, nullptr, 0.0, 0.0, 0, st);
+        if (s != DG_OK) return fail(ctx, s, std::string("tau_estimate: coarse residual: ") + dg_last_error(L.sub));
+        ctx->launches += L.sub->launches;
+        L.sub->launches = 0;
+        k_tau_level<<<E, 128, 0, st>>>(rc, dc, ctx->d_orders, L.d_orders, L.d_off, L.d, L.p, formulation, ctx->d_h,
+                                       ctx->curved ? L.sub->d_met : nullptr, ctx->d_tab, tau_dev);
+        ctx->launches++;
+    }
+    return check_stream_error(ctx, "non-isolated tau launch");
+}
+
 dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev, const double* qref_dev, double* tau_dev,
                           void* stream)
 {
@@ -1460,6 +1567,7 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
     if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "tau_estimate: orders not set");
     if (o->reference == DG_REF_SOLVER && !qref_dev) return fail(ctx, DG_EINVAL, "tau_estimate: SOLVER needs qdot_ref");
     if (ctx->prm.physics == DG_NS && !ctx->curved) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: NS needs the curved path");
+    if (o->coarse_faces && ctx->generic) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: non-isolated levels need the specialised kernels");
     const size_t smem = sizeof(double) * 3 * NV * (size_t)ctx->maxn;
     if (ctx->generic) {
         TauParams P;
@@ -1479,8 +1587,6 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
         if (o->reference == DG_REF_SAME) {  // isolated fine residual first (reading A4)
             if (ctx->ref_len < ctx->off[ctx->E]) {
                 dfree(ctx->d_ref_scratch);
-    dfree(ctx->d_tr_orders);
-    dfree(ctx->d_tr_off);
                 CK(cudaMalloc(&ctx->d_ref_scratch, sizeof(double) * ctx->off[ctx->E]));
                 ctx->ref_len = ctx->off[ctx->E];
             }
@@ -1490,6 +1596,7 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
         }
         k_tau_norm<<<ctx->n_own, 128, 0, st>>>(ref, tau_dev, ctx->d_orders, ctx->d_off);
         ctx->launches++;
+        if (o->coarse_faces) return tau_noniso(ctx, o->formulation, q_dev, ref, tau_dev, st);
         if (ctx->curved && ctx->nlevels > 0) {
             const size_t sm = sizeof(double) * (ctx->prm.physics == DG_NS ? 50 : 30) * (size_t)ctx->max_level;
             if ((long long)sm > ctx->smem_limit) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: coarse level too large for shared memory");

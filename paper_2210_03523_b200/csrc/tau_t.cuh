@@ -36,6 +36,38 @@ __device__ __forceinline__ int var_of(int task, int nl)
 }
 
 // tau[e][d][0] = ||Qdot_ref,e||_inf and NaN for p >= N_d (one CTA per element)
+// Non-isolated tau-estimation, one coarse level (d, p) (reading
+// R7): tau[e][d][p] = max over the coarse nodes and variables of
+// |scale (T_d R - Qdot_c)| for every element with p < N_d(e); rc, dc in the
+// coarse layout (orders oc, offsets offc); scale = J w w w (traditional form,
+// P:186-188; J from hgeo (affine) or the coarse metrics met (curved)), else 1.
+__global__ void __launch_bounds__(128) k_tau_level(const double* rc, const double* dc, const int* ofine, const int* oc,
+                                                   const long long* offc, int d, int p, int formulation,
+                                                   const double* hgeo, const double* met, const Tables* tab,
+                                                   double* tau)
+{
+    __shared__ double red[32];
+    const int e = blockIdx.x;
+    if (p >= ofine[3 * e + d]) return;  // level not defined for e (whole CTA)
+    const int o1 = oc[3 * e] + 1, o2 = oc[3 * e + 1] + 1, o3 = oc[3 * e + 2] + 1;
+    const int n = o1 * o2 * o3;
+    const long long o = offc[e];
+    const double Jel = met ? 0.0 : hgeo[3 * e] * hgeo[3 * e + 1] * hgeo[3 * e + 2] / 8.0;
+    double tmax = 0.0;
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+        double scale = 1.0;
+        if (formulation == 1) {
+            const int k = t / (o1 * o2), r = t - k * o1 * o2, j = r / o1, i = r - j * o1;
+            const double J = met ? met[2 * o + 9LL * n + t] : Jel;
+            scale = J * tab->w[o1 - 1][i] * tab->w[o2 - 1][j] * tab->w[o3 - 1][k];
+        }
+#pragma unroll
+        for (int v = 0; v < NV; ++v) tmax = fmax(tmax, fabs(scale * (rc[o + (long long)v * n + t] - dc[o + (long long)v * n + t])));
+    }
+    tmax = block_max(tmax, red);
+    if (threadIdx.x == 0) tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV + p] = tmax;
+}
+
 __global__ void __launch_bounds__(128) k_tau_norm(const double* qref, double* tau, const int* orders,
                                                   const long long* off)
 {

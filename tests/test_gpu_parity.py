@@ -275,6 +275,43 @@ def test_tau_parity(dg, orc, case, ref, form):
     assert tau_rel(tg, to) < TAU_TOL
 
 
+@pytest.mark.parametrize("case", ["cfg1", "cfg3_subbox_mixed", "ragged_1to8", "single_element", "all_order8"])
+@pytest.mark.parametrize("ref", ["solver", "same"])
+@pytest.mark.parametrize("form", [0, 1])
+def test_tau_noniso_parity(dg, orc, case, ref, form):
+    """Non-isolated tau-estimation (reading R7): coarse levels of
+    the whole mesh on the device vs the oracle's level-by-level composition."""
+    mesh, orders, kw = CASES[case]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, **kw)
+    if ref == "solver":
+        rg = S.rhs_eval(qd)
+        tg = S.tau_estimate(qd, rg, formulation=form, reference=dg.REF_SOLVER, noniso=True).cpu().numpy()
+        to = P.tau_estimate_noniso(orders, q, P.rhs(orders, q), form)
+    else:
+        tg = S.tau_estimate(qd, None, formulation=form, reference=dg.REF_SAME, noniso=True).cpu().numpy()
+        to = P.tau_estimate_noniso(orders, q, P.rhs(orders, q, orc.ISOLATED), form)
+    assert tau_rel(tg, to) < TAU_TOL
+    # the isolated estimate of the same call sequence is unaffected
+    if ref == "solver":
+        ti = S.tau_estimate(qd, rg, formulation=form, reference=dg.REF_SOLVER).cpu().numpy()
+        assert tau_rel(ti, P.tau_estimate(orders, q, P.rhs(orders, q), form)) < TAU_TOL
+
+
+def test_tau_noniso_layout_change(dg, orc):
+    """The coarse-level contexts follow set_orders (rebuilt for a new layout)."""
+    mesh, orders, kw = CASES["cfg3_subbox_mixed"]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, **kw)
+    S.tau_estimate(qd, S.rhs_eval(qd), noniso=True)
+    import torch
+
+    o2 = W.orders_random(mesh.E, 1, 8, 5)
+    S.set_orders(o2)
+    q2 = W.pulse_state(P.node_coords(o2), o2, **kw)
+    qd2 = torch.from_numpy(q2).cuda()
+    tg = S.tau_estimate(qd2, S.rhs_eval(qd2), noniso=True).cpu().numpy()
+    assert tau_rel(tg, P.tau_estimate_noniso(o2, q2, P.rhs(o2, q2))) < TAU_TOL
+
+
 @pytest.mark.parametrize("case", ["cfg2_uniform6", "cfg3_subbox_mixed", "ragged_1to8"])
 @pytest.mark.parametrize("rule", [0, 1])
 def test_select_dynamic_exact(dg, orc, case, rule):

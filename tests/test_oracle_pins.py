@@ -619,3 +619,75 @@ def test_q16_transfer(orc):
         assert np.abs(mo - mh).max() < 1e-13
     qc = W.uniform_state(o)
     assert np.abs(orc.transfer(o, qc, hi) - W.uniform_state(hi)).max() < 1e-13
+
+
+# ----------------------------------------------------------------------------
+# Q17 non-isolated tau-estimation (reading R7)
+# ----------------------------------------------------------------------------
+
+def _entropy_wave(X, orders, slope=0.1, gamma=1.4):
+    """rho = 1 + slope*x, u = (1,0,0), p = 1: the Euler flux is linear in q
+    (f = u q + p e_x-terms with u, p constant), so every DGSEM operator is
+    exact on it wherever the state is continuous; the periodic wrap x=1|0
+    carries the only jump."""
+    off3, off5 = W.offsets(orders, 3), W.offsets(orders, 5)
+    q = np.empty(off5[-1])
+    for e in range(len(orders)):
+        n = (off3[e + 1] - off3[e]) // 3
+        x = X[off3[e]:off3[e] + n]
+        rho = 1.0 + slope * x
+        b = q[off5[e]:off5[e + 1]].reshape(5, n)
+        b[0] = rho
+        b[1] = rho
+        b[2] = 0.0
+        b[3] = 0.0
+        b[4] = 1.0 / (gamma - 1.0) + 0.5 * rho
+    return q
+
+
+def test_q17_noniso_tau_freestream(orc):
+    m = W.cube_mesh(3, 2, 2)
+    P = orc.Problem(m)
+    o = W.orders_random(m.E, 2, 6, 17)
+    q = W.uniform_state(o)
+    R = P.rhs(o, q)
+    for form in (orc.TAU_NEW, orc.TAU_TRADITIONAL):
+        t = P.tau_estimate_noniso(o, q, R, form)
+        lv = t[:, :, 1:]
+        assert np.nanmax(np.abs(lv)) < 1e-11
+        # defined exactly for p < N_d (reading R1), slot 0 = ||R||_inf
+        for e in range(m.E):
+            for d in range(3):
+                assert np.all(np.isfinite(t[e, d, 1:o[e, d]])) and np.all(np.isnan(t[e, d, o[e, d]:]))
+
+
+def test_q17_noniso_tau_jump_pattern(orc):
+    """Entropy wave with one jump (periodic wrap in x, u = +1): the Roe flux of
+    a pure entropy jump is the upwind flux F(q_L) (wave strengths a1 = a5 = 0),
+    so only the downwind element (ix = 0) sees the jump in its lifting.  The
+    non-isolated tau is zero (to rounding) except for direction x at that
+    element; the isolated tau (element-local coarse residual, same SOLVER
+    reference) is nonzero there for EVERY direction (it misses the jump's
+    lifting) -- a dropped face term, a wrong sign, swapped face sides, a
+    misaligned neighbour trace or a transposed interpolation breaks one of
+    these."""
+    nx = 4
+    m = W.cube_mesh(nx, 2, 2)
+    P = orc.Problem(m)
+    o = W.orders_uniform(m.E, 4)
+    q = _entropy_wave(P.node_coords(o), o)
+    R = P.rhs(o, q)
+    scale = np.abs(R).max()
+    tn = P.tau_estimate_noniso(o, q, R)
+    ti = P.tau_estimate(o, q, R)
+    ix = np.arange(m.E) % nx
+    wrap = ix == 0  # downwind of the jump
+    for d in range(3):
+        lv_n, lv_i = tn[:, d, 1:4], ti[:, d, 1:4]
+        assert np.all(lv_i[~wrap] < 1e-10 * scale)
+        assert np.all(lv_i[wrap] > 1e-3 * scale)
+        assert np.all(lv_n[~wrap] < 1e-10 * scale)
+        if d == 0:
+            assert np.all(lv_n[wrap] > 1e-3 * scale)
+        else:
+            assert np.all(lv_n[wrap] < 1e-10 * scale)
