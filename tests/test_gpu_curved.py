@@ -150,6 +150,17 @@ def test_curved_tau_parity(dg, orc, name, ref, form):
     assert tau_rel(tg, to) < TAU_TOL
 
 
+@pytest.mark.parametrize("name", ["cfg4_small", "cfg5_subbox"])
+@pytest.mark.parametrize("form", [0, 1])
+def test_curved_tau_noniso_parity(dg, orc, name, form):
+    """Non-isolated tau (reading R7) on the curved NS meshes: coarse
+    levels with walls, far field, BR1 and (cfg5) mortars."""
+    mesh, orders, P, S, q, qd = setup(dg, orc, name)
+    tg = S.tau_estimate(qd, S.rhs_eval(qd), formulation=form, reference=dg.REF_SOLVER, noniso=True).cpu().numpy()
+    to = P.tau_estimate_noniso(orders, q, P.rhs(orders, q), form)
+    assert tau_rel(tg, to) < TAU_TOL
+
+
 def test_cfg4_static_adaptation_cycle(dg, orc):
     """Static p-adaptation (Fig. 2) on the cfg4 structure at reduced
     size: 3 estimation stages accumulated with approach 2 / F_max, one

@@ -14,6 +14,7 @@ import workloads as W  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", default="cfg2")
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--noniso", action="store_true", help="also time the non-isolated tau-estimation")
 a = ap.parse_args()
 if a.cfg in ("cfg4", "cfg5", "cfg5u"):
     pass
@@ -66,6 +67,9 @@ res["rhs_noniso_us"] = timeit(lambda: S.rhs_eval(q, r, variant=0))
 res["rhs_iso_us"] = timeit(lambda: S.rhs_eval(q, r, variant=1))
 res["rk_step_us"] = timeit(lambda: S.rk_step_dt(q, qb, g, dts[0], 0.5, dts[1]))
 res["tau_solver_us"] = timeit(lambda: S.tau_estimate(q, r), reps=max(3, a.reps // 4))
+if a.noniso:
+    S.tau_estimate(q, r, noniso=True)  # builds the coarse-level contexts once per layout
+    res["tau_noniso_us"] = timeit(lambda: S.tau_estimate(q, r, noniso=True), reps=max(3, a.reps // 4))
 res["rk_steps10_us"] = timeit(lambda: S.rk_steps(10, q, qb, g, dts[0], dts[1], 0.5), reps=max(3, a.reps // 4))
 res["gdofs_rk_stage_traces"] = 30 * ndof / res["rk_steps10_us"] / 1e3
 res["gdofs_rhs"] = ndof / res["rhs_noniso_us"] / 1e3
