@@ -51,7 +51,9 @@ enum { DG_NONISOLATED = 0, DG_ISOLATED = 1 };
 enum { DG_TAU_NEW = 0, DG_TAU_TRADITIONAL = 1 };
 enum { DG_REF_SOLVER = 0, DG_REF_SAME = 1 };
 enum { DG_JUMP_A = 0, DG_JUMP_B = 1 };
-enum { DG_SELECT_DYNAMIC = 0, DG_SELECT_STATIC_ACCUM = 1, DG_SELECT_STATIC_FINAL = 2 };
+enum { DG_SELECT_DYNAMIC = 0, DG_SELECT_STATIC_ACCUM = 1, DG_SELECT_STATIC_FINAL = 2,
+       DG_SELECT_A1_ACCUM = 3, DG_SELECT_A1_FINAL = 4 };
+enum { DG_COMBINE_MAX = 0, DG_COMBINE_AV = 1 };
 
 #define DG_NMAX 8
 #define DG_TAU_STRIDE 9
@@ -92,6 +94,9 @@ typedef struct {
     int Nmin, Nmax;  /* 1 <= Nmin <= Nmax <= 8                              */
     int jump_rule;   /* DG_JUMP_A (eq N23) | DG_JUMP_B (eq N_1)             */
     int dec_cap;     /* dynamic decrease cap per direction, >= 0    */
+    int combine;     /* static stage combination F: DG_COMBINE_MAX (F_max,
+                        the paper's choice) | DG_COMBINE_AV (F_av) */
+    int nstages;     /* n_e, the number of estimation stages (F_av finals only) */
 } dg_adapt_policy;
 
 /* Create a context on the current CUDA device.  Returns DG_EINVAL for bad
@@ -206,8 +211,16 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* opts, const double* q_
  *   STATIC_ACCUM:  total_map_dev <- max(total_map_dev, map)  (approach 2,
  *                  F_max, eq totalTruncMap); orders_out unchanged
  *   STATIC_FINAL:  as STATIC_ACCUM, then select on the total map -> jump
- * total_map_dev: fp64 [E][K][K][K], K = Nmax-Nmin+1, caller-owned, must be
- * zero-filled before the first STATIC_ACCUM (unused for DYNAMIC, may be NULL).
+ *   (combine = F_av: the total map accumulates the sum of the stage maps and
+ *   FINAL selects on sum / nstages)
+ *   A1_ACCUM:      approach 1: select the min-NDOF feasible orders
+ *                  of this stage's map (no decrease cap) and combine them into
+ *                  total_map_dev[e][3]: F_max running max, F_av running sum
+ *   A1_FINAL:      as A1_ACCUM, then orders = F(...) (F_av: the mean rounded
+ *                  half up, reading R8; clamped to [Nmin, Nmax]) -> jump
+ * total_map_dev: fp64 [E][K][K][K], K = Nmax-Nmin+1 (approach 1: [E][3]),
+ * caller-owned, must be zero-filled before the first ACCUM (unused for
+ * DYNAMIC, may be NULL).
  * orders_out_host: int32 [E][3] (written for DYNAMIC / STATIC_FINAL).
  * margin_host: optional fp64 [E], min |map - tau_max| / tau_max (parity aid).
  * Synchronises the stream. */

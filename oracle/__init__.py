@@ -272,6 +272,22 @@ def combine_max(total, mp):
     return total
 
 
+def combine_sum(total, mp):
+    """Approach 2 with F_av: the total map is the mean of the stage
+    maps; this accumulates its numerator (the final selection divides by n_e)."""
+    return np.ascontiguousarray(total, np.float64) + np.ascontiguousarray(mp, np.float64)
+
+
+def combine_degrees(picks, how=0):
+    """Approach 1: N_i^e = F(N_i^{e,1}, ..., N_i^{e,n_e}) per element
+    and direction, F_max (how=0) or F_av (how=1); the F_av mean is
+    rounded half up (reading R8).  picks: [n_e][E][3]."""
+    p = np.asarray(picks, np.float64)
+    if how == 0:
+        return p.max(axis=0).astype(np.int32)
+    return np.floor(p.sum(axis=0) / p.shape[0] + 0.5).astype(np.int32)
+
+
 def select_from_map(mp, Nmin, Nmax, tau_max):
     mp = np.ascontiguousarray(mp, np.float64)
     E = mp.shape[0]

@@ -30,7 +30,8 @@ NONISOLATED, ISOLATED = 0, 1
 TAU_NEW, TAU_TRADITIONAL = 0, 1
 REF_SOLVER, REF_SAME = 0, 1
 JUMP_A, JUMP_B = 0, 1
-SELECT_DYNAMIC, SELECT_STATIC_ACCUM, SELECT_STATIC_FINAL = 0, 1, 2
+SELECT_DYNAMIC, SELECT_STATIC_ACCUM, SELECT_STATIC_FINAL, SELECT_A1_ACCUM, SELECT_A1_FINAL = 0, 1, 2, 3, 4
+COMBINE_MAX, COMBINE_AV = 0, 1
 TAU_STRIDE = 9
 FLAG_GRADIENT_READY = 1
 NMAX = 8
@@ -110,7 +111,7 @@ class _TauOpts(C.Structure):
 
 class _Policy(C.Structure):
     _fields_ = [("mode", C.c_int), ("tau_max", C.c_double), ("Nmin", C.c_int), ("Nmax", C.c_int),
-                ("jump_rule", C.c_int), ("dec_cap", C.c_int)]
+                ("jump_rule", C.c_int), ("dec_cap", C.c_int), ("combine", C.c_int), ("nstages", C.c_int)]
 
 
 _lib = None
@@ -294,7 +295,7 @@ class Solver:
                     "dg_dt_finalize")
 
     def select_local(self, tau, tau_max, Nmin, Nmax, out, mode=SELECT_DYNAMIC, dec_cap=1, total_map=None, stream=None):
-        pol = _Policy(int(mode), float(tau_max), int(Nmin), int(Nmax), JUMP_B, int(dec_cap))
+        pol = _Policy(int(mode), float(tau_max), int(Nmin), int(Nmax), JUMP_B, int(dec_cap), COMBINE_MAX, 0)
         self._check(self.L.dg_select_local(self.ctx, C.byref(pol), _ptr(tau), _ptr(total_map), _ptr(out), None,
                                            _stream(stream)), "dg_select_local")
 
@@ -315,8 +316,12 @@ class Solver:
         return tau
 
     def select_orders(self, tau, tau_max, Nmin, Nmax, mode=SELECT_DYNAMIC, jump_rule=JUMP_B, dec_cap=1,
-                      total_map=None, stream=None):
-        pol = _Policy(int(mode), float(tau_max), int(Nmin), int(Nmax), int(jump_rule), int(dec_cap))
+                      total_map=None, stream=None, combine=COMBINE_MAX, nstages=0):
+        """Orders from tau.  Static approach 2 (SELECT_STATIC_*,
+        total_map [E][K][K][K]) or approach 1 (SELECT_A1_*, total_map [E][3]);
+        combine F_max / F_av (nstages = n_e for the F_av finals)."""
+        pol = _Policy(int(mode), float(tau_max), int(Nmin), int(Nmax), int(jump_rule), int(dec_cap), int(combine),
+                      int(nstages))
         out = np.zeros((self.E, 3), np.int32)
         margin = np.zeros(self.E)
         self._check(self.L.dg_select_orders(self.ctx, C.byref(pol), _ptr(tau), _ptr(total_map),

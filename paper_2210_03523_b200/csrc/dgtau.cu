@@ -1457,6 +1457,8 @@ dg_status dg_select_local(dg_ctx* ctx, const dg_adapt_policy* pol, const double*
     P.Nmin = pol->Nmin;
     P.Nmax = pol->Nmax;
     P.dec_cap = pol->dec_cap;
+    P.combine = pol->combine;
+    P.nstages = pol->nstages;
     k_select<<<(ctx->n_own + 127) / 128, 128, 0, st>>>(P);
     ctx->launches++;
     return check_stream_error(ctx, "k_select launch");
@@ -1646,8 +1648,13 @@ dg_status dg_select_orders(dg_ctx* ctx, const dg_adapt_policy* pol, const double
     if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "select_orders: orders not set");
     if (pol->Nmin < 1 || pol->Nmax > NMAX || pol->Nmin > pol->Nmax || !(pol->tau_max > 0) || pol->dec_cap < 0)
         return fail(ctx, DG_EINVAL, "select_orders: bad policy");
+    if (pol->mode < DG_SELECT_DYNAMIC || pol->mode > DG_SELECT_A1_FINAL || (pol->combine != DG_COMBINE_MAX &&
+        pol->combine != DG_COMBINE_AV) || (pol->combine == DG_COMBINE_AV && pol->nstages < 1 &&
+        (pol->mode == DG_SELECT_STATIC_FINAL || pol->mode == DG_SELECT_A1_FINAL)))
+        return fail(ctx, DG_EINVAL, "select_orders: bad mode / combine / nstages");
     if (pol->mode != DG_SELECT_DYNAMIC && !total_dev) return fail(ctx, DG_EINVAL, "select_orders: static needs total map");
-    if (pol->mode != DG_SELECT_STATIC_ACCUM && !orders_out) return fail(ctx, DG_EINVAL, "select_orders: orders_out");
+    const bool accum_only = pol->mode == DG_SELECT_STATIC_ACCUM || pol->mode == DG_SELECT_A1_ACCUM;
+    if (!accum_only && !orders_out) return fail(ctx, DG_EINVAL, "select_orders: orders_out");
     cudaStream_t st = (cudaStream_t)stream;
     const int E = ctx->E;
     SelParams P;
@@ -1662,6 +1669,8 @@ dg_status dg_select_orders(dg_ctx* ctx, const dg_adapt_policy* pol, const double
     P.Nmin = pol->Nmin;
     P.Nmax = pol->Nmax;
     P.dec_cap = pol->dec_cap;
+    P.combine = pol->combine;
+    P.nstages = pol->nstages;
     // halo rows (multi-rank local meshes) keep their current orders
     if (ctx->n_own < E)
         CK(cudaMemcpyAsync(ctx->d_sel + 3LL * ctx->n_own, ctx->d_orders + 3LL * ctx->n_own,
@@ -1670,7 +1679,7 @@ dg_status dg_select_orders(dg_ctx* ctx, const dg_adapt_policy* pol, const double
     ctx->launches++;
     dg_status s = check_stream_error(ctx, "k_select launch");
     if (s != DG_OK) return s;
-    if (pol->mode == DG_SELECT_STATIC_ACCUM) return DG_OK;
+    if (accum_only) return DG_OK;
     // jump-condition fixpoint: Jacobi sweeps until no element changes
     int* a = ctx->d_sel;
     int* b = ctx->d_sel + 3LL * E;

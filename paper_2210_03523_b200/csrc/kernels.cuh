@@ -515,6 +515,8 @@ struct SelParams {
     int mode;
     double tau_max;
     int Nmin, Nmax, dec_cap;
+    int combine;   // 0 F_max, 1 F_av
+    int nstages;   // n_e for the F_av finals
 };
 
 __device__ void directional_estimate(int Nd, const double* td, double* hat /* [NP+1] indexed by n */)
@@ -565,23 +567,27 @@ __global__ void k_select(SelParams P)
     }
     const int Nmin = P.Nmin, Nmax = P.Nmax, K = Nmax - Nmin + 1;
     double* tot = P.total ? P.total + (long long)e * K * K * K : nullptr;
-    if (P.mode != 0) {  // approach 2, F_max: running max of the maps (eq totalTruncMap)
+    const bool a2 = P.mode == 1 || P.mode == 2, a1 = P.mode == 3 || P.mode == 4;
+    if (a2) {  // approach 2: running F_max (eq totalTruncMap) or running sum (F_av) of the maps
         for (int n3 = Nmin; n3 <= Nmax; ++n3)
             for (int n2 = Nmin; n2 <= Nmax; ++n2)
                 for (int n1 = Nmin; n1 <= Nmax; ++n1) {
                     const int ix = (n1 - Nmin) + K * ((n2 - Nmin) + K * (n3 - Nmin));
-                    tot[ix] = fmax(tot[ix], hat[0][n1] + hat[1][n2] + hat[2][n3]);
+                    const double v = hat[0][n1] + hat[1][n2] + hat[2][n3];
+                    tot[ix] = P.combine == 1 ? tot[ix] + v : fmax(tot[ix], v);
                 }
         if (P.mode == 1) return;
     }
+    const double nst = (P.mode == 2 && P.combine == 1) ? (double)P.nstages : 1.0;  // F_av: total / n_e
     int best[3] = {Nmax, Nmax, Nmax};
     long bestp = -1, bests = 0;
     double mg = INFINITY;
     for (int n1 = Nmin; n1 <= Nmax; ++n1)
         for (int n2 = Nmin; n2 <= Nmax; ++n2)
             for (int n3 = Nmin; n3 <= Nmax; ++n3) {
-                const double v = P.mode == 0 ? hat[0][n1] + hat[1][n2] + hat[2][n3]
-                                             : tot[(n1 - Nmin) + K * ((n2 - Nmin) + K * (n3 - Nmin))];
+                const double v = !a2 ? hat[0][n1] + hat[1][n2] + hat[2][n3]
+                                     : (P.combine == 1 ? tot[(n1 - Nmin) + K * ((n2 - Nmin) + K * (n3 - Nmin))] / nst
+                                                       : tot[(n1 - Nmin) + K * ((n2 - Nmin) + K * (n3 - Nmin))]);
                 mg = fmin(mg, fabs(v - P.tau_max) / P.tau_max);
                 if (!(v < P.tau_max)) continue;
                 const long pr = (long)(n1 + 1) * (n2 + 1) * (n3 + 1), sm = n1 + n2 + n3;
@@ -593,6 +599,15 @@ __global__ void k_select(SelParams P)
             }
     if (P.mode == 0)  // decrease cap
         for (int d = 0; d < 3; ++d) best[d] = max(best[d], Ne[d] - P.dec_cap);
+    if (a1) {  // approach 1: combine this stage's degrees, N_i^e = F(N_i^{e,s})
+        double* acc = P.total + 3LL * e;
+        for (int d = 0; d < 3; ++d) acc[d] = P.combine == 1 ? acc[d] + best[d] : fmax(acc[d], (double)best[d]);
+        if (P.mode == 3) return;
+        for (int d = 0; d < 3; ++d) {  // F_av: mean rounded half up (reading R8)
+            const int Nd = P.combine == 1 ? (int)floor(acc[d] / P.nstages + 0.5) : (int)acc[d];
+            best[d] = min(max(Nd, Nmin), Nmax);
+        }
+    }
     for (int d = 0; d < 3; ++d) P.sel[3 * e + d] = best[d];
     if (P.margin) P.margin[e] = mg;
 }

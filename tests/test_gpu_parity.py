@@ -358,6 +358,44 @@ def test_select_static_exact(dg, orc):
     assert np.array_equal(sel_g, sel_o)
 
 
+@pytest.mark.parametrize("approach", [1, 2])
+@pytest.mark.parametrize("combine", [0, 1])
+def test_select_static_variants_exact(dg, orc, approach, combine):
+    """Static selection variants: approach 1
+    (per-stage picks combined) and approach 2 (combined maps), each with F_max
+    and F_av (reading R8), three stages (ACCUM, ACCUM, FINAL); exact orders."""
+    import torch
+
+    mesh, orders, kw = CASES["cfg3_subbox_mixed"]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, **kw)
+    Nmin, Nmax, tmax, ns = 2, 8, 1e-3, 3
+    K = Nmax - Nmin + 1
+    shape = (mesh.E, 3) if approach == 1 else (mesh.E, K, K, K)
+    total_g = torch.zeros(shape, dtype=torch.float64, device="cuda")
+    total_o = np.zeros((mesh.E, K, K, K))
+    picks = []
+    qo = q.copy()
+    for s in range(ns):
+        to = P.tau_estimate(orders, qo, P.rhs(orders, qo))
+        mp, _ = orc.build_map(orders, to, Nmin, Nmax)
+        picks.append(orc.select_from_map(mp, Nmin, Nmax, tmax)[0])
+        total_o = orc.combine_sum(total_o, mp) if combine == 1 else orc.combine_max(total_o, mp)
+        final = s == ns - 1
+        if approach == 1:
+            mode = dg.SELECT_A1_FINAL if final else dg.SELECT_A1_ACCUM
+        else:
+            mode = dg.SELECT_STATIC_FINAL if final else dg.SELECT_STATIC_ACCUM
+        sel_g, _ = S.select_orders(torch.from_numpy(to).cuda(), tmax, Nmin, Nmax, mode=mode, total_map=total_g,
+                                   combine=combine, nstages=ns)
+        qo = P.rk3_step(orders, qo, 2e-3)
+    if approach == 1:
+        sel_o = orc.combine_degrees(picks, combine)
+    else:
+        sel_o, _ = orc.select_from_map(total_o / ns if combine == 1 else total_o, Nmin, Nmax, tmax)
+    sel_o, _ = orc.jump_fixpoint(mesh.nbr, sel_o, orc.JUMP_B, Nmax)
+    assert np.array_equal(sel_g, sel_o)
+
+
 def test_transfer_parity(dg, orc):
     mesh, orders, kw = CASES["ragged_1to8"]()
     P, S, q, qd = setup(dg, orc, mesh, orders, **kw)

@@ -558,6 +558,33 @@ def test_q14_table1(orc):
     assert list(a2) == g["approach2_Fmax"] and (a2[0] + 1) * (a2[1] + 1) == g["approach2_NDOF"]
 
 
+def test_q14_table1_f_av(orc):
+    """F_av on Table 1: approach 1 averages the
+    stage picks (1,3) and (3,1) to (2,2) -- by hand, NDOF 9 -- and approach 2
+    with the averaged map keeps exactly the combinations feasible in both
+    stages (tau_max/2 stays feasible, (tau_max/2 + 2 tau_max)/2 does not) ->
+    (2,2).  Half-up rounding (reading R8): picks 2 and 3 average to 3."""
+    g = json.load(open(os.path.join(GOLD, "table1.json")))
+    Nmin, Nmax, tmax = g["Nmin"], g["Nmax"], 1.0
+    K = Nmax - Nmin + 1
+
+    def stage_map(feas):
+        mp = np.full((1, K, K, K), 2 * tmax)
+        for n1, n2 in feas:
+            mp[0, 0, n2 - Nmin, n1 - Nmin] = tmax / 2
+        return mp
+
+    maps = [stage_map(f) for f in g["stage_feasible"]]
+    picks = [orc.select_from_map(mp, Nmin, Nmax, tmax)[0] for mp in maps]
+    assert list(orc.combine_degrees(picks, 1)[0][:2]) == [2, 2]
+    assert list(orc.combine_degrees(picks, 0)[0][:2]) == g["approach1_Fmax"]
+    total = np.zeros_like(maps[0])
+    for mp in maps:
+        total = orc.combine_sum(total, mp)
+    assert list(orc.select_from_map(total / len(maps), Nmin, Nmax, tmax)[0][0][:2]) == [2, 2]
+    assert orc.combine_degrees([[[2, 2, 2]], [[3, 2, 1]]], 1).tolist() == [[3, 2, 2]]
+
+
 def test_q15_jump_cones(orc):
     m = W.cube_mesh(15, 1, 1)
     o = np.ones((15, 3), np.int32)
