@@ -85,6 +85,10 @@ typedef struct {
                         through Roe faces / mortars (and BR1 for NS), and
                         tau[e][d][p] (p < N_d(e)) is the max of |T_d R - Qdot_c|.
                         Single rank only (DG_EUNSUPPORTED after dg_set_owned). */
+    int restriction;  /* restriction of q and qdot_ref to the coarse orders along d:
+                        0 (default) interpolation at the coarse nodes (reading A3,
+                        P:165); 1 the exact L2 projection P^{N_d->p} (the A3 flag,
+                        SURVEY 8(f) rank 4).  The coarse geometry is interpolated. */
 } dg_tau_opts;
 
 /* Order-selection policy (readings A13-A16). */

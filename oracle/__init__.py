@@ -144,15 +144,17 @@ class Problem:
             raise ValueError("orc_rk3_step failed")
         return q
 
-    def tau_estimate(self, orders, q, qdot_ref, formulation=TAU_NEW):
+    def tau_estimate(self, orders, q, qdot_ref, formulation=TAU_NEW, restriction=0):
+        """Isolated tau-estimation; restriction 0 = interpolation (A3), 1 = L2 projection."""
         o = self._ord(orders)
         q = np.ascontiguousarray(q, np.float64)
         r = np.ascontiguousarray(qdot_ref, np.float64)
         tau = np.empty((self.E, 3, TAU_STRIDE))
-        lib().orc_tau_estimate(C.byref(self.m), _p(o), _p(q), _p(r), int(formulation), C.byref(self.ph), _p(tau))
+        lib().orc_tau_estimate_r(C.byref(self.m), _p(o), _p(q), _p(r), int(formulation), int(restriction),
+                                 C.byref(self.ph), _p(tau))
         return tau
 
-    def tau_estimate_noniso(self, orders, q, qdot_ref, formulation=TAU_NEW):
+    def tau_estimate_noniso(self, orders, q, qdot_ref, formulation=TAU_NEW, restriction=0):
         """NON-ISOLATED tau-estimation ("uses all terms appearing in
         the discrete DG variational formulation"; reading R7
         for the neighbours' orders).  For direction d and level p:
@@ -176,8 +178,12 @@ class Problem:
             for p in range(1, int(o[:, d].max())):
                 oc = o.copy()
                 oc[:, d] = np.minimum(o[:, d], p)
-                qc = transfer(o, q, oc)
-                rc = transfer(o, r, oc)
+                if restriction:
+                    qc = restrict_l2(o, q, oc, d)
+                    rc = restrict_l2(o, r, oc, d)
+                else:
+                    qc = transfer(o, q, oc)
+                    rc = transfer(o, r, oc)
                 diff = rc - self.rhs(oc, qc, NONISOLATED)
                 nc = np.prod(oc.astype(np.int64) + 1, axis=1)
                 offc = np.concatenate([[0], np.cumsum(5 * nc)])
@@ -313,6 +319,25 @@ def transfer(old_orders, q, new_orders, ncomp=5):
     q = np.ascontiguousarray(q, np.float64)
     out = np.empty(Problem.size(on, ncomp))
     lib().orc_transfer(oo.shape[0], _p(oo), _p(q), _p(on), _p(out), int(ncomp))
+    return out
+
+
+def restrict_l2(old_orders, q, new_orders, d, ncomp=5):
+    """Exact L2 projection along direction d (the A3 flag): every element's
+    [v][k][j][i] block times P^{N_d -> O_d} (projection_matrix) along axis d;
+    elements whose order does not change are copied."""
+    oo = np.asarray(old_orders); on = np.asarray(new_orders)
+    offo = np.concatenate([[0], np.cumsum(ncomp * np.prod(oo.astype(np.int64) + 1, axis=1))])
+    offn = np.concatenate([[0], np.cumsum(ncomp * np.prod(on.astype(np.int64) + 1, axis=1))])
+    out = np.empty(offn[-1])
+    for e in range(len(oo)):
+        a = oo[e] + 1
+        blk = np.asarray(q[offo[e]:offo[e + 1]]).reshape(ncomp, a[2], a[1], a[0])
+        if on[e, d] != oo[e, d]:
+            Pm = projection_matrix(int(oo[e, d]), int(on[e, d]))  # [(s+1), (M+1)]
+            ax = 3 - d  # axis of direction d in [v][k][j][i]
+            blk = np.moveaxis(np.tensordot(Pm, blk, axes=([1], [ax])), 0, ax)
+        out[offn[e]:offn[e + 1]] = blk.ravel()
     return out
 
 

@@ -1105,6 +1105,17 @@ int orc_rk3_step(const orc_mesh* m, const int32_t* orders, double* q, double dt,
 int orc_tau_estimate(const orc_mesh* m, const int32_t* orders, const double* q, const double* qdot_ref,
                      int formulation, const orc_phys* ph, double* tau)
 {
+    return orc_tau_estimate_r(m, orders, q, qdot_ref, formulation, 0, ph, tau);
+}
+
+/* As orc_tau_estimate with the restriction of q and Qdot_ref along d chosen by
+ * `restriction`: 0 = interpolation at the coarse nodes (reading A3, P:165
+ * "simply sampling"), 1 = the exact L2 projection P^{N_d->p} (the A3 flag,
+ * SURVEY 8(f) rank 4; the mortar projection of section 4).  The coarse
+ * geometry is interpolated in both cases. */
+int orc_tau_estimate_r(const orc_mesh* m, const int32_t* orders, const double* q, const double* qdot_ref,
+                       int formulation, int restriction, const orc_phys* ph, double* tau)
+{
     orc_init_basis();
     int E = m->E;
     size_t* off = make_offsets(E, orders, 5);
@@ -1126,7 +1137,7 @@ int orc_tau_estimate(const orc_mesh* m, const int32_t* orders, const double* q, 
                 int O[3] = {N[0], N[1], N[2]};
                 O[d] = p;
                 int nc = npts(O);
-                const double* T = Tm[N[d]][p];
+                const double* T = restriction ? Pm[N[d]][p] : Tm[N[d]][p];
                 double* qc = malloc(sizeof(double) * 5 * nc);
                 double* rc = malloc(sizeof(double) * 5 * nc);
                 long double* Xc = malloc(sizeof(long double) * 3 * nc);

@@ -49,6 +49,8 @@ double orc_compute_dt(const orc_mesh* m, const int32_t* orders, const double* q,
 int orc_rk3_step(const orc_mesh* m, const int32_t* orders, double* q, double dt, const orc_phys* ph);
 int orc_tau_estimate(const orc_mesh* m, const int32_t* orders, const double* q, const double* qdot_ref,
                      int formulation, const orc_phys* ph, double* tau);
+int orc_tau_estimate_r(const orc_mesh* m, const int32_t* orders, const double* q, const double* qdot_ref,
+                       int formulation, int restriction, const orc_phys* ph, double* tau);
 int orc_tau_field(const orc_mesh* m, const int32_t* orders, const double* q, const double* qdot_ref,
                   int e, int d, int p, int formulation, const orc_phys* ph, double* out);
 int orc_build_map(int E, const int32_t* orders, const double* tau, int Nmin, int Nmax, double* map, double* slopes);

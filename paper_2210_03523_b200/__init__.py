@@ -106,7 +106,7 @@ class _Params(C.Structure):
 
 
 class _TauOpts(C.Structure):
-    _fields_ = [("formulation", C.c_int), ("reference", C.c_int), ("coarse_faces", C.c_int)]
+    _fields_ = [("formulation", C.c_int), ("reference", C.c_int), ("coarse_faces", C.c_int), ("restriction", C.c_int)]
 
 
 class _Policy(C.Structure):
@@ -304,12 +304,13 @@ class Solver:
                                          _stream(stream)), "dg_jump_sweep")
 
     def tau_estimate(self, q, qdot_ref=None, formulation=TAU_NEW, reference=REF_SOLVER, tau=None, stream=None,
-                     noniso=False):
+                     noniso=False, restriction=0):
         """tau[e][d][p].  noniso=True: non-isolated coarse residuals
-        (whole mesh at each level's coarse orders; single rank)."""
+        (whole mesh at each level's coarse orders; single rank).
+        restriction: 0 interpolation (A3), 1 exact L2 projection (A3 flag)."""
         import torch
 
-        o = _TauOpts(int(formulation), int(reference), 1 if noniso else 0)
+        o = _TauOpts(int(formulation), int(reference), 1 if noniso else 0, int(restriction))
         tau = torch.empty((self.E, 3, TAU_STRIDE), dtype=torch.float64, device="cuda") if tau is None else tau
         self._check(self.L.dg_tau_estimate(self.ctx, C.byref(o), _ptr(q), _ptr(qdot_ref), _ptr(tau),
                                            _stream(stream)), "dg_tau_estimate")

@@ -1194,6 +1194,7 @@ struct CTauParams {
     CurvedMesh cm;
     const Tables* tab;
     int formulation;
+    int restr;  // 0 interpolation (A3), 1 L2 projection (A3 flag)
     int lbase;  // size class: CTA b handles level lbase + b
     PhysDev ph;
 };
@@ -1222,7 +1223,7 @@ __global__ void __launch_bounds__(BS) k_tau_curved(CTauParams P)
     double* A = F + NV * nO;                 // 5 nO
     element_metrics_fp64(P.cm, e, o1, o2, o3, P.tab, F, Mc);  // F, A: 10 nO >= 3 nO scratch
     const long long o = P.off[e];
-    const double* T = P.tab->T[nd - 1][p];
+    const double* T = P.restr ? P.tab->P[nd - 1][p] : P.tab->T[nd - 1][p];
     for (int t = threadIdx.x; t < nO; t += BS) {
         int i, j, k;
         node_ijk(t, o1, o2, i, j, k);

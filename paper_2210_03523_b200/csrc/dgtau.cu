@@ -1484,8 +1484,8 @@ dg_status dg_jump_sweep(dg_ctx* ctx, const int32_t* orders_in_dev, int32_t* orde
 // interpolated to the level's layout (k_transfer), the level's sub-context
 // evaluates the full (face-coupled) residual there, and k_tau_level takes
 // the per-element maxima.  Sub-contexts are built once per fine layout.
-static dg_status tau_noniso(dg_ctx* ctx, int formulation, const double* q_dev, const double* ref, double* tau_dev,
-                            cudaStream_t st)
+static dg_status tau_noniso(dg_ctx* ctx, int formulation, int restr, const double* q_dev, const double* ref,
+                            double* tau_dev, cudaStream_t st)
 {
     if (ctx->n_own != ctx->E) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: non-isolated levels need a single rank");
     const int E = ctx->E;
@@ -1543,6 +1543,7 @@ static dg_status tau_noniso(dg_ctx* ctx, int formulation, const double* q_dev, c
         T.offnew = L.d_off;
         T.tab = ctx->d_tab;
         T.smax0 = T.smax1 = T.smax2 = L.smax;
+        T.restr = restr;
         const size_t sm = sizeof(double) * NV * 3 * (size_t)L.smax;
         T.qold = q_dev;
         T.qnew = qc;
@@ -1569,7 +1570,9 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
     if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "tau_estimate: orders not set");
     if (o->reference == DG_REF_SOLVER && !qref_dev) return fail(ctx, DG_EINVAL, "tau_estimate: SOLVER needs qdot_ref");
     if (ctx->prm.physics == DG_NS && !ctx->curved) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: NS needs the curved path");
-    if (o->coarse_faces && ctx->generic) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: non-isolated levels need the specialised kernels");
+    if ((o->coarse_faces || o->restriction) && ctx->generic)
+        return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: non-isolated levels / L2 restriction need the specialised kernels");
+    if (o->restriction != 0 && o->restriction != 1) return fail(ctx, DG_EINVAL, "tau_estimate: restriction");
     const size_t smem = sizeof(double) * 3 * NV * (size_t)ctx->maxn;
     if (ctx->generic) {
         TauParams P;
@@ -1598,7 +1601,7 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
         }
         k_tau_norm<<<ctx->n_own, 128, 0, st>>>(ref, tau_dev, ctx->d_orders, ctx->d_off);
         ctx->launches++;
-        if (o->coarse_faces) return tau_noniso(ctx, o->formulation, q_dev, ref, tau_dev, st);
+        if (o->coarse_faces) return tau_noniso(ctx, o->formulation, o->restriction, q_dev, ref, tau_dev, st);
         if (ctx->curved && ctx->nlevels > 0) {
             const size_t sm = sizeof(double) * (ctx->prm.physics == DG_NS ? 50 : 30) * (size_t)ctx->max_level;
             if ((long long)sm > ctx->smem_limit) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: coarse level too large for shared memory");
@@ -1613,6 +1616,7 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
             C.cm = curved_mesh(ctx);
             C.tab = ctx->d_tab;
             C.formulation = o->formulation;
+            C.restr = o->restriction;
             C.ph = phys_dev(ctx->prm);
             for (const SizeClass& c : ctx->lcls) {
                 C.lbase = c.base;
@@ -1633,6 +1637,7 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
             P.groups = ctx->d_tgroups;
             P.tab = ctx->d_tab;
             P.formulation = o->formulation;
+            P.restr = o->restriction;
             P.gm1 = ctx->prm.gamma - 1.0;
             k_tau5<<<ctx->ntgroups, TAU5_BS, ctx->tau5_smem, st>>>(P);
         }
@@ -1746,6 +1751,7 @@ dg_status dg_transfer(dg_ctx* ctx, const int32_t* new_orders, const double* q_ol
     P.smax0 = smax[0];
     P.smax1 = smax[1];
     P.smax2 = smax[2];
+    P.restr = 0;
     k_transfer<<<E, BLOCK, sizeof(double) * NV * (size_t)(smax[0] + smax[1] + smax[2]), st>>>(P);
     ctx->launches++;
     return check_stream_error(ctx, "k_transfer launch");

@@ -678,6 +678,7 @@ __global__ void __launch_bounds__(JUMP_FIX_BS) k_jump_fix(const int* nbr, int* a
 
 struct TransferParams {
     int smax0, smax1, smax2;  // max over elements of nA, n1, n2 (shared-memory layout)
+    int restr;                // decreasing directions by the L2 projection P (A3 flag), else interpolation T
     const double* qold;
     double* qnew;
     const int* oold;
@@ -723,7 +724,9 @@ __global__ void __launch_bounds__(BLOCK) k_transfer(TransferParams P)
     for (int d = 0; d < 3; ++d) { A[d] = P.oold[3 * e + d] + 1; B[d] = P.onew[3 * e + d] + 1; }
     for (int t = threadIdx.x; t < 3 * NP * NP; t += blockDim.x) {
         const int d = t / (NP * NP), r = t - d * (NP * NP), i = r / NP, b = r - i * NP;
-        Ts[d][r] = (i < B[d] && b < A[d]) ? P.tab->T[A[d] - 1][B[d] - 1][i * A[d] + b] : 0.0;
+        Ts[d][r] = (i < B[d] && b < A[d]) ? ((P.restr && B[d] < A[d]) ? P.tab->P[A[d] - 1][B[d] - 1]
+                                                                       : P.tab->T[A[d] - 1][B[d] - 1])[i * A[d] + b]
+                                          : 0.0;
     }
     const int nA = A[0] * A[1] * A[2];
     double* buf[2] = {sm, sm + NV * P.smax0};

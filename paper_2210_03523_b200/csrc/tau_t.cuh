@@ -124,6 +124,7 @@ struct Tau5Params {
     const TauGroup* groups;
     const Tables* tab;
     int formulation;
+    int restr;  // 0 interpolation (A3), 1 L2 projection (A3 flag)
     double gm1;
 };
 
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(TAU5_BS, 3) k_tau5(Tau5Params P)
     for (int t = tid; t < tbase[nlev - 1] + (p0 + nlev) * nd; t += TAU5_BS) {
         int li = 0;
         while (li + 1 < nlev && tbase[li + 1] <= t) ++li;
-        Ts[t] = P.tab->T[Nd][p0 + li][t - tbase[li]];
+        Ts[t] = (P.restr ? P.tab->P[Nd][p0 + li] : P.tab->T[Nd][p0 + li])[t - tbase[li]];
     }
     double* F0 = sm;               // coarse state, then f_0 and D^{O_0} f_0
     double* F1 = F0 + NV * ntot;

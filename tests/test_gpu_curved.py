@@ -161,6 +161,14 @@ def test_curved_tau_noniso_parity(dg, orc, name, form):
     assert tau_rel(tg, to) < TAU_TOL
 
 
+@pytest.mark.parametrize("name", ["cfg4_small", "cfg5_subbox"])
+def test_curved_tau_l2_restriction_parity(dg, orc, name):
+    mesh, orders, P, S, q, qd = setup(dg, orc, name)
+    tg = S.tau_estimate(qd, S.rhs_eval(qd), restriction=1).cpu().numpy()
+    to = P.tau_estimate(orders, q, P.rhs(orders, q), restriction=1)
+    assert tau_rel(tg, to) < TAU_TOL
+
+
 def test_cfg4_static_adaptation_cycle(dg, orc):
     """Static p-adaptation (Fig. 2) on the cfg4 structure at reduced
     size: 3 estimation stages accumulated with approach 2 / F_max, one

@@ -297,6 +297,24 @@ def test_tau_noniso_parity(dg, orc, case, ref, form):
         assert tau_rel(ti, P.tau_estimate(orders, q, P.rhs(orders, q), form)) < TAU_TOL
 
 
+@pytest.mark.parametrize("case", ["cfg1", "cfg3_subbox_mixed", "ragged_1to8", "all_order8"])
+@pytest.mark.parametrize("noniso", [False, True])
+@pytest.mark.parametrize("form", [0, 1])
+def test_tau_l2_restriction_parity(dg, orc, case, noniso, form):
+    """tau-estimate with the exact L2 projection as restriction (the A3 flag,
+    SURVEY 8(f) rank 4), isolated and non-isolated levels."""
+    mesh, orders, kw = CASES[case]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, **kw)
+    rg = S.rhs_eval(qd)
+    tg = S.tau_estimate(qd, rg, formulation=form, noniso=noniso, restriction=1).cpu().numpy()
+    ro = P.rhs(orders, q)
+    if noniso:
+        to = P.tau_estimate_noniso(orders, q, ro, form, restriction=1)
+    else:
+        to = P.tau_estimate(orders, q, ro, form, restriction=1)
+    assert tau_rel(tg, to) < TAU_TOL
+
+
 def test_tau_noniso_layout_change(dg, orc):
     """The coarse-level contexts follow set_orders (rebuilt for a new layout)."""
     mesh, orders, kw = CASES["cfg3_subbox_mixed"]()

@@ -718,3 +718,58 @@ def test_q17_noniso_tau_jump_pattern(orc):
             assert np.all(lv_n[wrap] > 1e-3 * scale)
         else:
             assert np.all(lv_n[wrap] < 1e-10 * scale)
+
+
+# ----------------------------------------------------------------------------
+# Q18 L2-projection restriction for the tau-estimate (the A3 flag, SURVEY 8(f)
+# rank 4): P^{N->p} along one direction
+# ----------------------------------------------------------------------------
+
+def test_q18_restrict_l2_line_integrals(orc):
+    """Along the restricted direction every line keeps its integral (P^{N->p}
+    is the L2 projection onto degree p, which contains the constants; GL with
+    p+1 / N+1 points integrates degree p / N exactly), and data of degree <= p
+    along that direction is reproduced exactly (= interpolation)."""
+    m = W.cube_mesh(1)
+    P = orc.Problem(m)
+    o = np.array([[4, 5, 6]], np.int32)
+    rng = np.random.default_rng(18)
+    q = rng.standard_normal(P.size(o))
+    X = P.node_coords(o)
+    for d in range(3):
+        for p in range(1, int(o[0, d])):
+            oc = o.copy()
+            oc[0, d] = p
+            qc = orc.restrict_l2(o, q, oc, d)
+            # whole-element weighted sums (J w w w), affine element: line integrals summed
+            M, Mc = P.mass(o), P.mass(oc)
+            a = q.reshape(5, -1) @ M
+            b = qc.reshape(5, -1) @ Mc
+            assert np.abs(a - b).max() < 1e-13 * np.abs(q).max()
+            # a state linear in x_d is reproduced: projection == interpolation
+            lin = np.tile(1.0 + 0.3 * X[d * X.size // 3:(d + 1) * X.size // 3], 5)
+            assert np.abs(orc.restrict_l2(o, lin, oc, d) - orc.transfer(o, lin, oc)).max() < 1e-14
+
+
+def test_q18_tau_projection_vs_interpolation(orc):
+    """On the entropy wave of Q17 (linear in x, constant in y, z) the two
+    restrictions agree wherever the restricted data is a polynomial of degree
+    <= p along d (away from the jump's lifting), and they differ on a pulse."""
+    nx = 4
+    m = W.cube_mesh(nx, 2, 2)
+    P = orc.Problem(m)
+    o = W.orders_uniform(m.E, 4)
+    q = _entropy_wave(P.node_coords(o), o)
+    R = P.rhs(o, q)
+    ti, tp = P.tau_estimate(o, q, R), P.tau_estimate(o, q, R, restriction=1)
+    ni, np_ = P.tau_estimate_noniso(o, q, R), P.tau_estimate_noniso(o, q, R, restriction=1)
+    scale = np.abs(R).max()
+    ix = np.arange(m.E) % nx
+    for d in range(3):
+        sel = ix != 0 if d == 0 else slice(None)
+        assert np.abs(ti[sel, d, 1:4] - tp[sel, d, 1:4]).max() < 1e-10 * scale
+        assert np.abs(ni[sel, d, 1:4] - np_[sel, d, 1:4]).max() < 1e-10 * scale
+    qp = W.pulse_state(P.node_coords(o), o, sigma=0.15)
+    Rp = P.rhs(o, qp)
+    a, b = P.tau_estimate(o, qp, Rp), P.tau_estimate(o, qp, Rp, restriction=1)
+    assert np.nanmax(np.abs(a[:, :, 1:] - b[:, :, 1:])) > 1e-6 * np.nanmax(np.abs(a[:, :, 1:]))
