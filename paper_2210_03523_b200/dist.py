@@ -48,6 +48,38 @@ def exchange(tensor, plan: "part.HaloPlan", rank: int, group=None):
             o += b - a
 
 
+def migrate(q_owned, plan: "part.MigrationPlan", group=None):
+    """Move owned element states to their new owners after a repartition
+    (SURVEY 8(f) rank 2): one all_to_all_single (NCCL on GPUs, gloo on CPU).
+    q_owned: 1-D states of plan.old_ids (increasing global id); returns the
+    states of plan.new_ids (increasing global id)."""
+    import torch
+    import torch.distributed as dist
+
+    dev = q_owned.device
+    pos = {int(g): i for i, g in enumerate(plan.old_ids)}
+    chunks = []
+    for ids in plan.send_ids:
+        for g in ids:
+            i = pos[int(g)]
+            chunks.append(q_owned[int(plan.old_off[i]):int(plan.old_off[i + 1])])
+    send = torch.cat(chunks) if chunks else torch.empty(0, dtype=q_owned.dtype, device=dev)
+    recv = torch.empty(sum(plan.recv_len), dtype=q_owned.dtype, device=dev)
+    dist.all_to_all_single(recv, send, plan.recv_len, plan.send_len, group=group)
+    # received blocks come grouped by source rank; order them by global id
+    src = np.concatenate([ids for ids in plan.recv_ids]) if plan.recv_ids else np.zeros(0, np.int64)
+    lens = plan.n[src]
+    starts = np.concatenate([[0], np.cumsum(lens)])
+    order = np.argsort(src, kind="stable")
+    out = torch.empty_like(recv)
+    o = 0
+    for k in order:
+        a, b = int(starts[k]), int(starts[k + 1])
+        out[o:o + b - a].copy_(recv[a:b])
+        o += b - a
+    return out
+
+
 class DistSolver:
     """A `Solver` on this rank's local mesh (owned + halo elements) plus the
     exchanges that make owned results identical to the single-rank ones."""
@@ -56,6 +88,7 @@ class DistSolver:
         from . import Solver
 
         self.rank, self.world, self.group = rank, world, group
+        self.mesh, self.owner, self.solver_kw = global_mesh, np.asarray(owner), dict(solver_kw)
         self.lm = part.local_mesh(global_mesh, owner, rank)
         self.physics = solver_kw.get("physics", 0)
         self.S = Solver(self.lm, **solver_kw)
@@ -182,3 +215,25 @@ class DistSolver:
             res[gid] = o
         del out
         return res
+
+
+def rebalance(ds: DistSolver, global_orders, q_local, axis: int = 2):
+    """Dynamic load rebalancing after an adaptation: a new
+    DOF-balanced slab partition for `global_orders` (partition.dof_owner), the
+    owned element states moved with one all-to-all (migrate), a new DistSolver
+    on the new local mesh, and its halo refreshed.  q_local: this rank's local
+    state (owned + halo) at global_orders under the old partition.  Returns
+    (new DistSolver, new local state)."""
+    import torch
+
+    go = np.asarray(global_orders, np.int32)
+    new_owner = part.dof_owner(ds.mesh.dims, go, ds.world, axis)
+    plan = part.MigrationPlan(ds.owner, new_owner, go, ds.rank, ds.world)
+    q_own = migrate(q_local[: int(plan.old_off[-1])], plan, ds.group)
+    nd = DistSolver(ds.mesh, new_owner, ds.rank, ds.world, ds.group, **ds.solver_kw)
+    nd.set_orders(go)
+    n = part.element_offsets(go[nd.lm.gids])
+    q_new = torch.zeros(int(n[-1]), dtype=q_local.dtype, device=q_local.device)
+    q_new[: q_own.numel()].copy_(q_own)
+    nd.halo(q_new)
+    return nd, q_new

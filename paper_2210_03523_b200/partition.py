@@ -36,6 +36,34 @@ def slab_owner(dims, world: int, axis: int = 2) -> np.ndarray:
     return owner
 
 
+def dof_owner(dims, orders: np.ndarray, world: int, axis: int = 2) -> np.ndarray:
+    """Repartition after a p-adaptation: contiguous slabs
+    of element layers along `axis` whose DOF counts are as equal as the layer
+    granularity allows.  Cut r is placed at the layer boundary whose
+    cumulative DOF is closest to r/world of the total (ties: the earlier
+    boundary), every rank keeps at least one layer."""
+    n0, n1, n2 = dims
+    E = n0 * n1 * n2
+    idx = np.arange(E)
+    coord = [idx % n0, (idx // n0) % n1, idx // (n0 * n1)][axis]
+    n = dims[axis]
+    if world > n:
+        raise ValueError(f"cannot split {n} element layers over {world} ranks")
+    dof = np.prod(np.asarray(orders, np.int64) + 1, axis=1)
+    cum = np.concatenate([[0], np.cumsum(np.bincount(coord, weights=dof, minlength=n))])
+    bounds = [0]
+    for r in range(1, world):
+        lo, hi = bounds[-1] + 1, n - (world - r)  # at least one layer each side
+        target = cum[-1] * r / world
+        b = lo + int(np.argmin(np.abs(cum[lo:hi + 1] - target)))
+        bounds.append(b)
+    bounds.append(n)
+    owner = np.empty(E, np.int32)
+    for r in range(world):
+        owner[(coord >= bounds[r]) & (coord < bounds[r + 1])] = r
+    return owner
+
+
 @dataclass
 class LocalMesh:
     rank: int
@@ -126,3 +154,23 @@ class HaloPlan:
         self.send_len = {r: sum(b - a for a, b in rs) for r, rs in self.send.items()}
         self.recv_len = {r: sum(b - a for a, b in rs) for r, rs in self.recv.items()}
         assert set(self.send) == set(self.recv), "face adjacency is symmetric"
+
+
+class MigrationPlan:
+    """Element moves between two partitions (old_owner -> new_owner) seen from
+    `rank`: per peer, the global ids it sends (its old owned elements that the
+    peer owns now) and receives (its new owned elements the peer owned),
+    increasing global id, with their state lengths (ncomp doubles per node).
+    Owned states are kept in increasing global id order on both sides."""
+
+    def __init__(self, old_owner: np.ndarray, new_owner: np.ndarray, orders: np.ndarray, rank: int, world: int,
+                 ncomp: int = 5):
+        n = ncomp * np.prod(np.asarray(orders, np.int64) + 1, axis=1)
+        self.old_ids = np.flatnonzero(old_owner == rank)
+        self.new_ids = np.flatnonzero(new_owner == rank)
+        self.old_off = np.concatenate([[0], np.cumsum(n[self.old_ids])])
+        self.send_ids = [self.old_ids[new_owner[self.old_ids] == r] for r in range(world)]
+        self.recv_ids = [self.new_ids[old_owner[self.new_ids] == r] for r in range(world)]
+        self.send_len = [int(n[i].sum()) for i in self.send_ids]
+        self.recv_len = [int(n[i].sum()) for i in self.recv_ids]
+        self.n = n

@@ -169,3 +169,96 @@ def test_slab_partition_plans():
     owner = part.slab_owner(og.dims, 4, axis=1)
     lm = part.local_mesh(og, owner, 1)
     assert (lm.nbr[: lm.n_own] == W.BC_WALL).any() and (lm.nbr[: lm.n_own] == W.BC_FARFIELD).any()
+
+
+def _rebalance_worker(rank, world, port, out_q):
+    """Repartition after an adaptation: DOF-balanced slabs,
+    owned states migrated with one all-to-all, halo refreshed; the owned
+    residual on the new local mesh equals the global one."""
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2210_03523_b200 import partition as part
+    from paper_2210_03523_b200.dist import exchange, migrate
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = {}
+        mesh = W.cube_mesh(3, 3, 8)
+        old_owner = part.slab_owner(mesh.dims, world, axis=2)
+        # adapted orders: high orders in the lower z half -> the equal-layer slabs are unbalanced
+        rng = np.random.default_rng(31)
+        orders = rng.integers(2, 4, size=(mesh.E, 3)).astype(np.int32)
+        kz = np.arange(mesh.E) // 9
+        orders[kz < 3] += 4
+        P = oracle.Problem(mesh)
+        q_g = W.pulse_state(P.node_coords(orders), orders, center=(0.5, 0.5, 0.3), sigma=0.2)
+        blocks = _per_elem(q_g, orders)
+        new_owner = part.dof_owner(mesh.dims, orders, world, axis=2)
+        dof = np.prod(orders.astype(np.int64) + 1, axis=1)
+        res["dof_old"] = [int(dof[old_owner == r].sum()) for r in range(world)]
+        res["dof_new"] = [int(dof[new_owner == r].sum()) for r in range(world)]
+        plan = part.MigrationPlan(old_owner, new_owner, orders, rank, world)
+        q_old_own = torch.from_numpy(np.concatenate([blocks[g] for g in plan.old_ids]))
+        q_new_own = migrate(q_old_own, plan).numpy()
+        want = np.concatenate([blocks[g] for g in plan.new_ids])
+        res["migrate_exact"] = bool(np.array_equal(q_new_own, want))
+        lm = part.local_mesh(mesh, new_owner, rank)
+        lo = orders[lm.gids]
+        hplan = part.HaloPlan(lm, lo, 5)
+        n = part.element_offsets(lo)
+        q_l = np.zeros(int(n[-1]))
+        q_l[: len(q_new_own)] = q_new_own
+        t = torch.from_numpy(q_l)
+        exchange(t, hplan, rank)
+        r_l = oracle.Problem(lm).rhs(lo, t.numpy())
+        rb = _per_elem(P.rhs(orders, q_g), orders)
+        owned = np.concatenate([rb[g] for g in lm.gids[: lm.n_own]])
+        res["rhs_owned_exact"] = bool(np.array_equal(r_l[: len(owned)], owned))
+        out_q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_two_rank_rebalance_after_adaptation():
+    import torch.multiprocessing as mp
+
+    import oracle
+
+    oracle.build()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rebalance_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=600) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(2):
+        assert res[r]["migrate_exact"], res[r]
+        assert res[r]["rhs_owned_exact"], res[r]
+    old, new = res[0]["dof_old"], res[0]["dof_new"]
+    assert max(new) - min(new) < max(old) - min(old)
+
+
+def test_dof_owner_two_ranks_optimal():
+    """For two ranks the DOF cut is the best layer boundary (brute force)."""
+    from paper_2210_03523_b200 import partition as part
+
+    rng = np.random.default_rng(7)
+    for trial in range(20):
+        dims = (2, 3, int(rng.integers(2, 12)))
+        E = dims[0] * dims[1] * dims[2]
+        orders = rng.integers(1, 9, size=(E, 3)).astype(np.int32)
+        owner = part.dof_owner(dims, orders, 2)
+        dof = np.prod(orders.astype(np.int64) + 1, axis=1)
+        got = max(dof[owner == 0].sum(), dof[owner == 1].sum())
+        layer = np.arange(E) // (dims[0] * dims[1])
+        best = min(max(dof[layer < b].sum(), dof[layer >= b].sum()) for b in range(1, dims[2]))
+        assert got == best
+        assert np.all(np.diff(owner[np.argsort(layer, kind="stable")]) >= 0)  # contiguous slabs

@@ -35,19 +35,23 @@ def _copy_halos(solvers, plans, states):
                 o += b - a
 
 
-@pytest.mark.parametrize("case", ["cube_mixed", "ogrid_ns"])
+@pytest.mark.parametrize("case", ["cube_mixed", "ogrid_ns", "cube_rebalanced"])
 def test_two_rank_emulated(dg, orc, case):
     import torch
 
     from paper_2210_03523_b200 import partition as part
 
-    if case == "cube_mixed":
+    if case in ("cube_mixed", "cube_rebalanced"):
         mesh = W.cube_mesh(4, 4, 6)
         g_orders = W.orders_random(mesh.E, 2, 6, 31)
         kw = {}
         P = orc.Problem(mesh)
+        if case == "cube_rebalanced":  # adapted orders skewed to low z, DOF-balanced slabs (dist.rebalance)
+            g_orders[np.arange(mesh.E) // 16 < 2] = np.minimum(g_orders[np.arange(mesh.E) // 16 < 2] + 2, 8)
+            owner = part.dof_owner(mesh.dims, g_orders, 2, axis=2)
+        else:
+            owner = part.slab_owner(mesh.dims, 2, axis=2)
         q_g = W.pulse_state(P.node_coords(g_orders), g_orders, sigma=0.2)
-        owner = part.slab_owner(mesh.dims, 2, axis=2)
     else:
         mesh = W.ogrid_mesh(4, 8, 2, ratio=1.1 ** 12, g_eta=2)
         g_orders = W.orders_random(mesh.E, (2, 2, 2), (6, 6, 2), 32)
