@@ -1,0 +1,104 @@
+"""Physics validation run: error vs NDOF of uniform orders
+against dynamic tau-based p-adaptation on the advected density pulse.
+
+The pulse IC (constant u, p; reading A20) is an exact travelling solution of
+the Euler equations (an entropy wave), so the error at time T is measured
+against the translated IC.  Uniform runs: N = Nmin..Nmax.  Dynamic runs
+(Fig. 1): every `--every` RK steps a SOLVER-reference
+tau-estimate, dynamic selection (tau_max, [Nmin, Nmax], jump rule, decrease
+cap 1), transfer of the state and a new layout.  Reported per run: the
+time-averaged NDOF, the final L_inf and RMS density errors, the
+steps and the device time.  Everything runs through libdgtau on one GPU.
+
+usage: python tools/validate_pulse.py [--n 8] [--T 0.25] > profiles/r01_validate_pulse.json
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2210_03523_b200 as dg  # noqa: E402
+import workloads as W  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--n", type=int, default=8, help="elements per direction")
+ap.add_argument("--T", type=float, default=0.25, help="final time")
+ap.add_argument("--cfl", type=float, default=0.5)
+ap.add_argument("--every", type=int, default=10, help="RK steps between adaptations")
+ap.add_argument("--nmin", type=int, default=2)
+ap.add_argument("--nmax", type=int, default=8)
+ap.add_argument("--n0", type=int, default=8, help="initial orders of the dynamic runs (the IC resolved at N_max)")
+ap.add_argument("--sigma", type=float, default=0.08)
+a = ap.parse_args()
+
+VEL = (1.0, 0.5, 0.25)
+C0 = (0.5, 0.5, 0.5)
+mesh = W.cube_mesh(a.n)
+
+
+def exact(S, orders, t):
+    c = tuple((C0[i] + VEL[i] * t) % 1.0 for i in range(3))
+    return W.pulse_state(S.node_coords(), orders, center=c, sigma=a.sigma, vel=VEL)
+
+
+def rho_err(q, qe, orders):
+    off = W.offsets(orders, 5)
+    errs = []
+    for e in range(len(orders)):
+        n = (off[e + 1] - off[e]) // 5
+        errs.append(q[off[e]:off[e] + n] - qe[off[e]:off[e] + n])
+    d = np.concatenate(errs)
+    return float(np.abs(d).max()), float(np.sqrt(np.mean(d * d)))
+
+
+def run(orders, tau_max=None, rule=dg.JUMP_B):
+    S = dg.Solver(mesh)
+    S.set_orders(orders)
+    q = torch.from_numpy(exact(S, orders, 0.0)).cuda()
+    qb, g = torch.empty_like(q), torch.empty_like(q)
+    t, steps, ndof_t, adapts = 0.0, 0, 0.0, 0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    while t < a.T - 1e-14:
+        dt = S.compute_dt(q, a.cfl, sync=True)
+        dt = min(dt, a.T - t)
+        S._dt.fill_(dt)
+        S.rk_step(q, qb, g, S._dt)
+        q, qb = qb, q
+        t += dt
+        steps += 1
+        ndof_t += W.ndof(orders) * dt
+        if tau_max is not None and steps % a.every == 0 and t < a.T - 1e-14:
+            tau = S.tau_estimate(q, S.rhs_eval(q))
+            new, _ = S.select_orders(tau, tau_max, a.nmin, a.nmax, jump_rule=rule, dec_cap=1)
+            if not np.array_equal(new, orders):
+                q = S.transfer(new, q).clone()
+                orders = new
+                S.set_orders(orders)
+                qb, g = torch.empty_like(q), torch.empty_like(q)
+                adapts += 1
+    ev1.record()
+    torch.cuda.synchronize()
+    linf, rms = rho_err(q.cpu().numpy(), exact(S, orders, a.T), orders)
+    return {"ndof_avg": ndof_t / a.T, "ndof_final": W.ndof(orders), "err_linf": linf, "err_rms": rms,
+            "steps": steps, "adaptations": adapts, "device_ms": ev0.elapsed_time(ev1)}
+
+
+out = {"what": "advected density pulse (exact entropy wave), error vs time-averaged NDOF",
+       "mesh": f"{a.n}^3 periodic affine hexes", "T": a.T, "cfl": a.cfl, "sigma": a.sigma,
+       "adapt_every": a.every, "Nmin": a.nmin, "Nmax": a.nmax, "runs": []}
+t0 = time.time()
+for N in range(a.nmin, a.nmax + 1):
+    r = run(W.orders_uniform(mesh.E, N))
+    out["runs"].append({"kind": "uniform", "N": N, **r})
+for rule, name in ((dg.JUMP_B, "b"), (dg.JUMP_A, "a")):
+    for tm in (1e-1, 1e-2, 1e-3, 1e-4):
+        r = run(W.orders_uniform(mesh.E, a.n0), tau_max=tm, rule=rule)
+        out["runs"].append({"kind": "dynamic", "tau_max": tm, "rule": name, **r})
+out["host_s"] = time.time() - t0
+print(json.dumps(out, indent=1))
