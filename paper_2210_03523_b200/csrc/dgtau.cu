@@ -12,6 +12,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -151,6 +153,7 @@ struct dg_ctx {
     std::vector<Bucket> buckets;
     res_launcher rtab[NP][NP][NP] = {};
     res_occupancy rocc[NP][NP][NP] = {};
+    signed char occ_cache[NP][NP][NP];  // resident k_res_t CTAs per SM, -1 = not queried yet
     int nsm = 148;
     int cm3_occ[3] = {1, 1, 1};  // resident k_mortar_c3 CTAs per SM: <5,5>, <20,5>, <5,15>
     FaceInfo* d_finfo_slot = nullptr;
@@ -190,19 +193,66 @@ dg_status cuda_check(dg_ctx* c, cudaError_t e, const char* what)
         if (_s != DG_OK) return _s;                                    \
     } while (0)
 
+inline std::mutex& dcap_mu();
+inline std::unordered_map<const void*, size_t>& dcap();
+
 template <class T>
 void dfree(T*& p)
 {
+    if (p) {
+        {
+            std::lock_guard<std::mutex> lk(dcap_mu());
+            dcap().erase(p);
+        }
+        cudaFree(p);
+    }
+    p = nullptr;
+}
+
+// Grow-only device buffers for the per-layout tables: a layout change
+// (dg_set_orders, every adaptation) reuses the allocations instead of
+// cudaFree (device-synchronising) + cudaMalloc for each of ~25 tables.
+inline std::mutex& dcap_mu()
+{
+    static std::mutex* m = new std::mutex;  // never destroyed: contexts may be freed during process exit
+    return *m;
+}
+inline std::unordered_map<const void*, size_t>& dcap()
+{
+    static auto* m = new std::unordered_map<const void*, size_t>;
+    return *m;
+}
+
+template <class T>
+cudaError_t dalloc(T*& p, size_t count)
+{
+    const size_t bytes = sizeof(T) * count;
+    {
+        std::lock_guard<std::mutex> lk(dcap_mu());
+        auto it = p ? dcap().find(p) : dcap().end();
+        if (it != dcap().end() && it->second >= bytes) return cudaSuccess;
+        if (p) dcap().erase(p);
+    }
     if (p) cudaFree(p);
     p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes ? bytes : 1);
+    if (e != cudaSuccess) {
+        p = nullptr;
+        return e;
+    }
+    std::lock_guard<std::mutex> lk(dcap_mu());
+    dcap()[p] = bytes;
+    return cudaSuccess;
 }
 
 template <class T>
 cudaError_t upload(T*& d, const std::vector<T>& h)
 {
-    dfree(d);
-    if (h.empty()) return cudaSuccess;
-    cudaError_t e = cudaMalloc(&d, sizeof(T) * h.size());
+    if (h.empty()) {
+        dfree(d);
+        return cudaSuccess;
+    }
+    cudaError_t e = dalloc(d, h.size());
     if (e != cudaSuccess) return e;
     return cudaMemcpy(d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice);
 }
@@ -281,6 +331,7 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return DG_ECUDA;
     dg_ctx* ctx = new dg_ctx;
+    std::memset(ctx->occ_cache, -1, sizeof(ctx->occ_cache));
     ctx->prm = *params;
     cudaGetDevice(&ctx->device);
     cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, ctx->device);
@@ -743,13 +794,16 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
         for (int f = 0; f < 6; ++f) fos[6 * i + f] = fofs[6LL * elist[i] + f];
     CK(upload(ctx->d_fofs_slot, fos));
     for (Bucket& b : ctx->buckets) {
-        const int occ = ctx->rocc[b.ord & 255][(b.ord >> 8) & 255][(b.ord >> 16) & 255]();
+        const int o1 = b.ord & 255, o2 = (b.ord >> 8) & 255, o3 = (b.ord >> 16) & 255;
+        if (ctx->occ_cache[o1][o2][o3] < 0) ctx->occ_cache[o1][o2][o3] = (signed char)ctx->rocc[o1][o2][o3]();
+        const int occ = ctx->occ_cache[o1][o2][o3];
         b.grid = std::max(1, occ) * ctx->nsm;
     }
     // tau-estimation levels (e, d, p < N_d), largest first for load balance
+    // (curved kernels only: the affine path batches levels in k_tau5 groups)
     std::vector<TauLevel> lv;
     ctx->max_level = 0;
-    for (int e = 0; e < ctx->n_own; ++e)
+    for (int e = 0; e < (ctx->curved ? ctx->n_own : 0); ++e)
         for (int d = 0; d < 3; ++d)
             for (int p = 1; p < ctx->orders[3 * e + d]; ++p) {
                 lv.push_back(TauLevel{e, d, p, 0});
@@ -772,11 +826,11 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
         lv.swap(ls);
     }
     CK(upload(ctx->d_levels, lv));
-    {
+    ctx->ecls_own.clear();
+    ctx->ecls_all.clear();
+    if (ctx->curved) {  // size classes of the curved element kernels
         std::vector<int> esz(E), ei(E);
         for (int e = 0; e < E; ++e) { esz[e] = npts(&ctx->orders[3 * e]); ei[e] = e; }
-        ctx->ecls_own.clear();
-        ctx->ecls_all.clear();
         size_classes(ei, esz, 0, ctx->n_own, ctx->ecls_own);
         ctx->ecls_all = ctx->ecls_own;
         size_classes(ei, esz, ctx->n_own, E, ctx->ecls_all);
@@ -817,12 +871,9 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     CK(upload(ctx->d_elist, elist));
     CK(upload(ctx->d_mortar, mort));
     CK(upload(ctx->d_moff, moff));
-    dfree(ctx->d_mortarG);
-    if (flen > 0) CK(cudaMalloc(&ctx->d_mortarG, sizeof(double) * flen));
-    dfree(ctx->d_sel);
-    dfree(ctx->d_margin);
-    CK(cudaMalloc(&ctx->d_sel, sizeof(int) * 6LL * E));
-    CK(cudaMalloc(&ctx->d_margin, sizeof(double) * E));
+    if (flen > 0) CK(dalloc(ctx->d_mortarG, (size_t)flen));
+    CK(dalloc(ctx->d_sel, 6 * (size_t)E));
+    CK(dalloc(ctx->d_margin, (size_t)E));
     if (ctx->curved) {
         const long long L = ctx->off[E];
         if (ctx->met_len < 2 * L) {
