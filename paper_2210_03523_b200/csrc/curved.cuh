@@ -397,6 +397,7 @@ struct CurvedParams {
     const double* met;      // metrics (2x offsets)
     const double* grad;     // gradients (3x offsets), NS
     const double* mortarG;  // projected mortar fluxes (5 per point) or gradient terms (15 per point)
+    const long long* fofs;  // [E][6] flux block of each element face in mortarG (k_face_curved), or null
     const Tables* tab;
     PhysDev ph;
     int* flag;
@@ -524,6 +525,59 @@ __device__ __forceinline__ void load_grad(const double* base, int stride, double
     for (int c = 0; c < 15; ++c) g[c] = __ldg(base + (long long)c * stride);
 }
 
+// Conforming interior faces of a curved mesh, numerical flux ONCE per face
+// point (the element kernel used to evaluate it on both sides): Roe flux along
+// the L side's face metric (reading A6) and, for NS, minus the BR1 average of
+// the two viscous fluxes -- the arithmetic of k_res_curved's kind-0 branch, so
+// both elements read bit-identical values.  One CTA per face; boundary faces
+// stay in the element kernel.  G block [v][pt] at the face's flux offset.
+struct CFaceParams {
+    const double* q;
+    const double* grad;
+    const double* met;
+    const FaceItem* faces;
+    double* G;
+    PhysDev ph;
+};
+
+__global__ void __launch_bounds__(128) k_face_curved(CFaceParams P)
+{
+    const FaceItem fi = P.faces[blockIdx.x];
+    if (fi.kind != 0) return;
+    const bool ns = P.ph.physics == 1;
+    const int d = fi.d;
+    for (int pt = threadIdx.x; pt < fi.nf; pt += blockDim.x) {
+        const int ta = pt % fi.nta, tb = pt / fi.nta;
+        const int nodeL = fi.baseL + ta * fi.saL + tb * fi.sbL;
+        const int nodeR = fi.baseR + ta * fi.saR + tb * fi.sbR;
+        double qL[NV], qR[NV], jf[3], G[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            qL[v] = __ldg(P.q + fi.offL + (long long)v * fi.nL + nodeL);
+            qR[v] = __ldg(P.q + fi.offR + (long long)v * fi.nR + nodeR);
+        }
+        const double* Ml = P.met + 2 * fi.offL + nodeL;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) jf[c] = __ldg(Ml + (long long)(3 * d + c) * fi.nL);
+        const double S = sqrt(jf[0] * jf[0] + jf[1] * jf[1] + jf[2] * jf[2]);
+        const double nrm[3] = {jf[0] / S, jf[1] / S, jf[2] / S};
+        riemann(qL, qR, nrm, P.ph, G);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) G[v] *= S;
+        if (ns) {
+            double gL[15], gR[15], fL[NV], fR[NV];
+            load_grad(P.grad + 3 * fi.offL + nodeL, fi.nL, gL);
+            load_grad(P.grad + 3 * fi.offR + nodeR, fi.nR, gR);
+            visc_dot(qL, gL, jf[0], jf[1], jf[2], P.ph, fL);
+            visc_dot(qR, gR, jf[0], jf[1], jf[2], P.ph, fR);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) G[v] -= 0.5 * (fL[v] + fR[v]);
+        }
+#pragma unroll
+        for (int v = 0; v < NV; ++v) P.G[fi.goff + (long long)v * fi.nf + pt] = G[v];
+    }
+}
+
 __global__ void __launch_bounds__(CBS, 4) k_res_curved(CurvedParams P)
 {
     extern __shared__ double sm[];
@@ -589,13 +643,16 @@ __global__ void __launch_bounds__(CBS, 4) k_res_curved(CurvedParams P)
                     qo[v] = Q[v * n + node];
                     Fo[v] = F[(d * NV + v) * n + node];
                 }
-                if (ns) load_grad(GR + node, n, go);
                 for (int c = 0; c < 3; ++c) jo[c] = __ldg(M + (3 * d + c) * n + node);
                 const FaceInfo fi = P.finfo[6 * e + f];
                 if (fi.kind == 1) {
                     const double* src = P.mortarG + fi.off + pt;
                     for (int v = 0; v < NV; ++v) G[v] = src[(long long)v * fi.n];
+                } else if (fi.kind == 0 && P.fofs) {  // conforming: flux once per face point (k_face_curved)
+                    const double* src = P.mortarG + P.fofs[6 * e + f] + pt;
+                    for (int v = 0; v < NV; ++v) G[v] = src[(long long)v * nf];
                 } else {
+                    if (ns) load_grad(GR + node, n, go);  // own gradient: boundary faces / no face kernel
                     double qx[NV], gx[15], jf[3];
                     if (fi.kind >= 2) {
                         for (int c = 0; c < 3; ++c) jf[c] = jo[c];

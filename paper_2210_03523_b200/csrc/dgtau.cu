@@ -158,6 +158,7 @@ struct dg_ctx {
     int cm3_occ[3] = {1, 1, 1};  // resident k_mortar_c3 CTAs per SM: <5,5>, <20,5>, <5,15>
     FaceInfo* d_finfo_slot = nullptr;
     MortarFace* d_mfaces = nullptr;    // mortar faces (k_mortar3)
+    long long* d_fofs_el = nullptr;    // curved: [E][6] flux block of each element face (k_face_curved)
     long long* d_fofs_slot = nullptr;  // [elist][6] flux offset (into d_mortarG) of each face of each slot
     FaceItem* d_faces = nullptr;       // conforming + boundary faces (one Riemann flux per face point)
     int* d_fpt = nullptr;              // [nfaces+1] point prefix
@@ -467,6 +468,7 @@ void dg_destroy(dg_ctx* ctx)
     dfree(ctx->d_finfo);
     dfree(ctx->d_finfo_slot);
     dfree(ctx->d_fofs_slot);
+    dfree(ctx->d_fofs_el);
     dfree(ctx->d_mfaces);
     dfree(ctx->d_faces);
     dfree(ctx->d_fpt);
@@ -793,6 +795,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     for (size_t i = 0; i < elist.size(); ++i)
         for (int f = 0; f < 6; ++f) fos[6 * i + f] = fofs[6LL * elist[i] + f];
     CK(upload(ctx->d_fofs_slot, fos));
+    if (ctx->curved) CK(upload(ctx->d_fofs_el, fofs));
     for (Bucket& b : ctx->buckets) {
         const int o1 = b.ord & 255, o2 = (b.ord >> 8) & 255, o3 = (b.ord >> 16) & 255;
         if (ctx->occ_cache[o1][o2][o3] < 0) ctx->occ_cache[o1][o2][o3] = (signed char)ctx->rocc[o1][o2][o3]();
@@ -1053,6 +1056,19 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
     P.out = out;
     P.mortarG = ctx->d_mortarG;
     P.lam_max = lam_max;
+    P.fofs = nullptr;
+    if (variant == DG_NONISOLATED && ctx->nfaces > 0 && ctx->d_fofs_el) {  // conforming faces once per point
+        CFaceParams FP;
+        FP.q = q;
+        FP.grad = ctx->d_grad;
+        FP.met = ctx->d_met;
+        FP.faces = ctx->d_faces;
+        FP.G = ctx->d_mortarG;
+        FP.ph = phys_dev(ctx->prm);
+        k_face_curved<<<ctx->nfaces, 128, 0, st>>>(FP);
+        ctx->launches++;
+        P.fofs = ctx->d_fofs_el;
+    }
     for (const SizeClass& c : ctx->ecls_own) {
         P.pbase = c.base;
         k_res_curved<<<c.count, CBS, sizeof(double) * 25 * (size_t)c.maxn, st>>>(P);
