@@ -482,3 +482,39 @@ def test_full_size_cfg3(dg, orc):
     for _ in range(2):
         qo = P.rk3_step(orders, qo, P.dt(orders, qo, 0.5))
     assert rel_linf(qs.cpu().numpy(), qo, orders, floor=EULER_PULSE_SCALES) < RES_TOL
+
+
+def test_error_paths(dg, orc):
+    """The ABI refuses, with a status and a message (never a crash), what it
+    does not support: non-isolated levels on a multi-rank local mesh, an
+    unknown restriction, an F_av final without n_e, a layout-free call, a
+    misaligned state."""
+    import torch
+
+    mesh, orders, kw = CASES["cfg1"]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, **kw)
+    r = S.rhs_eval(qd)
+    with pytest.raises(dg.DGError, match="restriction"):
+        S.tau_estimate(qd, r, restriction=2)
+    tau = S.tau_estimate(qd, r)
+    K = 8 - 2 + 1
+    tot = torch.zeros((mesh.E, K, K, K), dtype=torch.float64, device="cuda")
+    with pytest.raises(dg.DGError, match="nstages"):
+        S.select_orders(tau, 1e-3, 2, 8, mode=dg.SELECT_STATIC_FINAL, total_map=tot, combine=dg.COMBINE_AV, nstages=0)
+    with pytest.raises(dg.DGError):
+        S.rhs_eval(torch.empty(qd.numel() + 1, dtype=torch.float64, device="cuda")[1:])  # 8-byte aligned only
+    S2 = dg.Solver(mesh)
+    with pytest.raises(dg.DGError, match="orders"):
+        S2.rhs_eval(qd, torch.empty_like(qd))
+    # a rank-local mesh: non-isolated levels need the whole mesh
+    from paper_2210_03523_b200 import partition as part
+
+    owner = part.slab_owner(mesh.dims, 2, axis=2)
+    lm = part.local_mesh(mesh, owner, 0)
+    S3 = dg.Solver(lm)
+    S3._check(S3.L.dg_set_owned(S3.ctx, int(lm.n_own)), "dg_set_owned")
+    lo = np.ascontiguousarray(orders[lm.gids], np.int32)
+    S3.set_orders(lo)
+    ql = torch.from_numpy(W.uniform_state(lo)).cuda()
+    with pytest.raises(dg.DGError, match="single rank"):
+        S3.tau_estimate(ql, S3.rhs_eval(ql), noniso=True)
