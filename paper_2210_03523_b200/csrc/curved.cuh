@@ -1257,7 +1257,7 @@ struct CTauParams {
 };
 
 template <int BS>
-__global__ void __launch_bounds__(BS) k_tau_curved(CTauParams P)
+__global__ void __launch_bounds__(BS, BS == 256 ? 2 : (BS == 128 ? 5 : 10)) k_tau_curved(CTauParams P)
 {
     extern __shared__ double sm[];
     __shared__ double red[32];
