@@ -419,7 +419,7 @@ __device__ __forceinline__ int face_node(int d, int s, int pt, int n1, int n2, i
 // ---------------------------------------------------------------------------
 // BR1 gradient (eq DGSEMsystem:2), non-isolated or isolated, per element.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(CBS) k_grad(CurvedParams P)
+__global__ void __launch_bounds__(CBS, 5) k_grad(CurvedParams P)
 {
     // one thread per node: the volume sum over the three directions and the
     // lifting of the faces the node lies on, accumulated in registers
