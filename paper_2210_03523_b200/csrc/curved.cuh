@@ -578,7 +578,7 @@ __global__ void __launch_bounds__(128) k_face_curved(CFaceParams P)
     }
 }
 
-__global__ void __launch_bounds__(CBS, 4) k_res_curved(CurvedParams P)
+__global__ void __launch_bounds__(CBS, 5) k_res_curved(CurvedParams P)
 {
     extern __shared__ double sm[];
     __shared__ double red[32];
