@@ -126,6 +126,8 @@ struct dg_ctx {
         long long* d_off = nullptr;
     };
     std::vector<CoarseLevel> coarse;
+    bool coarse_streaming = false;  // levels built / run / freed one at a time (device memory)
+    bool coarse_stream_force = false;  // DGTAU_NONISO_STREAM=1 (tests)
     double* d_cq = nullptr;  // coarse q, T_d R, Qdot_c (fine length each)
     long long c_len = 0;
     int* d_tr_orders = nullptr;       // transfer scratch
@@ -384,6 +386,7 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         const char* g = getenv("DGTAU_GENERIC");
         ctx->generic = g && g[0] == '1';
         ctx->no_graphs = getenv_flag("DGTAU_NO_GRAPHS");
+        ctx->coarse_stream_force = getenv_flag("DGTAU_NONISO_STREAM");
         if ((s = cuda_check(ctx, cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking), "capture stream")) !=
             DG_OK) {
             dg_destroy(ctx);
@@ -437,6 +440,7 @@ static void drop_coarse(dg_ctx* ctx)
 {
     for (auto& L : ctx->coarse) {
         dg_destroy(L.sub);
+        L.sub = nullptr;
         dfree(L.d_orders);
         dfree(L.d_off);
     }
@@ -572,6 +576,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     if (ctx->E == 0) return fail(ctx, DG_ESTATE, "set_orders: no mesh");
     drop_graphs(ctx);  // captured launches refer to the old plans
     drop_coarse(ctx);  // non-isolated tau levels of the old layout
+    ctx->coarse_streaming = false;
     const int E = ctx->E;
     for (long long i = 0; i < 3LL * E; ++i)
         if (orders_host[i] < 1 || orders_host[i] > NMAX) return fail(ctx, DG_EINVAL, "set_orders: order out of 1..8");
@@ -1551,83 +1556,130 @@ dg_status dg_jump_sweep(dg_ctx* ctx, const int32_t* orders_in_dev, int32_t* orde
 // interpolated to the level's layout (k_transfer), the level's sub-context
 // evaluates the full (face-coupled) residual there, and k_tau_level takes
 // the per-element maxima.  Sub-contexts are built once per fine layout.
+// one coarse level (d, p): the whole mesh at O(e) = N(e), O_d = min(p, N_d(e))
+static dg_status build_level(dg_ctx* ctx, int d, int p, dg_ctx::CoarseLevel& L)
+{
+    const int E = ctx->E;
+    L.d = d;
+    L.p = p;
+    std::vector<int32_t> oc(ctx->orders.begin(), ctx->orders.end());
+    std::vector<long long> offc(E + 1, 0);
+    for (int e = 0; e < E; ++e) {
+        const int* a = &ctx->orders[3 * e];
+        oc[3 * e + d] = std::min(p, a[d]);
+        offc[e + 1] = offc[e] + (long long)NV * npts(&oc[3 * e]);
+        L.smax = std::max(L.smax, npts(a));  // every transfer intermediate fits the fine element
+    }
+    dg_status s = dg_create(&ctx->prm, &L.sub);
+    if (s != DG_OK) return fail(ctx, s, "tau_estimate: coarse level context");
+    if ((s = dg_mesh_upload(L.sub, E, ctx->nbr.data(), ctx->gorder, ctx->geo.data())) != DG_OK ||
+        (s = dg_set_orders(L.sub, oc.data())) != DG_OK)
+        return fail(ctx, s, std::string("tau_estimate: coarse level: ") + dg_last_error(L.sub));
+    if (upload(L.d_orders, oc) != cudaSuccess || upload(L.d_off, offc) != cudaSuccess)
+        return fail(ctx, DG_ECUDA, "tau_estimate: coarse level tables");
+    return DG_OK;
+}
+
+static void free_level(dg_ctx::CoarseLevel& L)
+{
+    dg_destroy(L.sub);
+    L.sub = nullptr;
+    dfree(L.d_orders);
+    dfree(L.d_off);
+}
+
+static dg_status run_level(dg_ctx* ctx, const dg_ctx::CoarseLevel& L, int formulation, int restr, const double* q_dev,
+                           const double* ref, double* tau_dev, cudaStream_t st)
+{
+    const int E = ctx->E;
+    const long long len = ctx->off[E];
+    double* qc = ctx->d_cq;
+    double* rc = qc + len;
+    double* dc = rc + len;
+    TransferParams T;
+    T.oold = ctx->d_orders;
+    T.onew = L.d_orders;
+    T.offold = ctx->d_off;
+    T.offnew = L.d_off;
+    T.tab = ctx->d_tab;
+    T.smax0 = T.smax1 = T.smax2 = L.smax;
+    T.restr = restr;
+    const size_t sm = sizeof(double) * NV * 3 * (size_t)L.smax;
+    T.qold = q_dev;
+    T.qnew = qc;
+    k_transfer<<<E, BLOCK, sm, st>>>(T);
+    T.qold = ref;
+    T.qnew = rc;
+    k_transfer<<<E, BLOCK, sm, st>>>(T);
+    ctx->launches += 2;
+    dg_status s = launch_residual(L.sub, DG_NONISOLATED, qc, dc, nullptr, nullptr, 0.0, 0.0, 0, st);
+    if (s != DG_OK) return fail(ctx, s, std::string("tau_estimate: coarse residual: ") + dg_last_error(L.sub));
+    ctx->launches += L.sub->launches;
+    L.sub->launches = 0;
+    k_tau_level<<<E, 128, 0, st>>>(rc, dc, ctx->d_orders, L.d_orders, L.d_off, L.d, L.p, formulation, ctx->d_h,
+                                   ctx->curved ? L.sub->d_met : nullptr, ctx->d_tab, tau_dev);
+    ctx->launches++;
+    return check_stream_error(ctx, "non-isolated tau launch");
+}
+
+// Non-isolated tau-estimation (dg_tau_opts.coarse_faces = 1, reading R7):
+// per coarse level (d, p) the state and the reference residual are
+// interpolated to the level's layout (k_transfer), the level's sub-context
+// evaluates the full (face-coupled) residual there, and k_tau_level takes
+// the per-element maxima.  The sub-contexts stay resident across calls (built
+// once per fine layout); when they do not all fit in device memory (cfg5:
+// 15 levels of a 42.5 M DOF mesh) the levels are built, run and freed one at
+// a time instead.
 static dg_status tau_noniso(dg_ctx* ctx, int formulation, int restr, const double* q_dev, const double* ref,
                             double* tau_dev, cudaStream_t st)
 {
     if (ctx->n_own != ctx->E) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: non-isolated levels need a single rank");
     const int E = ctx->E;
     const long long len = ctx->off[E];
-    if (ctx->coarse.empty()) {
-        int nmax[3] = {0, 0, 0};
-        for (int e = 0; e < E; ++e)
-            for (int d = 0; d < 3; ++d) nmax[d] = std::max(nmax[d], ctx->orders[3 * e + d]);
-        for (int d = 0; d < 3; ++d)
+    if (ctx->c_len < 3 * len) {
+        dfree(ctx->d_cq);
+        CK(cudaMalloc(&ctx->d_cq, sizeof(double) * 3 * len));
+        ctx->c_len = 3 * len;
+    }
+    int nmax[3] = {0, 0, 0};
+    for (int e = 0; e < E; ++e)
+        for (int d = 0; d < 3; ++d) nmax[d] = std::max(nmax[d], ctx->orders[3 * e + d]);
+    if (ctx->coarse_stream_force) ctx->coarse_streaming = true;
+    if (ctx->coarse.empty() && !ctx->coarse_streaming) {
+        for (int d = 0; d < 3 && !ctx->coarse_streaming; ++d)
             for (int p = 1; p < nmax[d]; ++p) {
                 dg_ctx::CoarseLevel L;
-                L.d = d;
-                L.p = p;
-                std::vector<int32_t> oc(ctx->orders.begin(), ctx->orders.end());
-                std::vector<long long> offc(E + 1, 0);
-                for (int e = 0; e < E; ++e) {
-                    const int* a = &ctx->orders[3 * e];
-                    oc[3 * e + d] = std::min(p, a[d]);
-                    offc[e + 1] = offc[e] + (long long)NV * npts(&oc[3 * e]);
-                    // every intermediate of the transfer passes fits prod max(old, new) + 1
-                    L.smax = std::max(L.smax, npts(a));
+                const dg_status s = build_level(ctx, d, p, L);
+                ctx->coarse.push_back(L);  // owned from here (drop_coarse frees it)
+                if (s == DG_ECUDA) {       // out of device memory: stream the levels instead
+                    drop_coarse(ctx);
+                    cudaGetLastError();
+                    ctx->coarse_streaming = true;
+                    break;
                 }
-                dg_status s = dg_create(&ctx->prm, &L.sub);
                 if (s != DG_OK) {
                     drop_coarse(ctx);
-                    return fail(ctx, s, "tau_estimate: coarse level context");
-                }
-                ctx->coarse.push_back(L);  // owned from here (drop_coarse frees it)
-                dg_ctx::CoarseLevel& C = ctx->coarse.back();
-                if ((s = dg_mesh_upload(C.sub, E, ctx->nbr.data(), ctx->gorder, ctx->geo.data())) != DG_OK ||
-                    (s = dg_set_orders(C.sub, oc.data())) != DG_OK) {
-                    const std::string why = dg_last_error(C.sub);
-                    drop_coarse(ctx);
-                    return fail(ctx, s, "tau_estimate: coarse level: " + why);
-                }
-                if (upload(C.d_orders, oc) != cudaSuccess || upload(C.d_off, offc) != cudaSuccess) {
-                    drop_coarse(ctx);
-                    return fail(ctx, DG_ECUDA, "tau_estimate: coarse level tables");
+                    return s;
                 }
             }
-        if (ctx->c_len < 3 * len) {
-            dfree(ctx->d_cq);
-            CK(cudaMalloc(&ctx->d_cq, sizeof(double) * 3 * len));
-            ctx->c_len = 3 * len;
+    }
+    if (!ctx->coarse_streaming) {
+        for (const dg_ctx::CoarseLevel& L : ctx->coarse) {
+            const dg_status s = run_level(ctx, L, formulation, restr, q_dev, ref, tau_dev, st);
+            if (s != DG_OK) return s;
         }
+        return DG_OK;
     }
-    double* qc = ctx->d_cq;
-    double* rc = qc + len;
-    double* dc = rc + len;
-    for (const dg_ctx::CoarseLevel& L : ctx->coarse) {
-        TransferParams T;
-        T.oold = ctx->d_orders;
-        T.onew = L.d_orders;
-        T.offold = ctx->d_off;
-        T.offnew = L.d_off;
-        T.tab = ctx->d_tab;
-        T.smax0 = T.smax1 = T.smax2 = L.smax;
-        T.restr = restr;
-        const size_t sm = sizeof(double) * NV * 3 * (size_t)L.smax;
-        T.qold = q_dev;
-        T.qnew = qc;
-        k_transfer<<<E, BLOCK, sm, st>>>(T);
-        T.qold = ref;
-        T.qnew = rc;
-        k_transfer<<<E, BLOCK, sm, st>>>(T);
-        ctx->launches += 2;
-        dg_status s = launch_residual(L.sub, DG_NONISOLATED, qc, dc, nullptr, nullptr, 0.0, 0.0, 0, st);
-        if (s != DG_OK) return fail(ctx, s, std::string("tau_estimate: coarse residual: ") + dg_last_error(L.sub));
-        ctx->launches += L.sub->launches;
-        L.sub->launches = 0;
-        k_tau_level<<<E, 128, 0, st>>>(rc, dc, ctx->d_orders, L.d_orders, L.d_off, L.d, L.p, formulation, ctx->d_h,
-                                       ctx->curved ? L.sub->d_met : nullptr, ctx->d_tab, tau_dev);
-        ctx->launches++;
-    }
-    return check_stream_error(ctx, "non-isolated tau launch");
+    for (int d = 0; d < 3; ++d)
+        for (int p = 1; p < nmax[d]; ++p) {
+            dg_ctx::CoarseLevel L;
+            dg_status s = build_level(ctx, d, p, L);
+            if (s == DG_OK) s = run_level(ctx, L, formulation, restr, q_dev, ref, tau_dev, st);
+            CK(cudaStreamSynchronize(st));  // the level's buffers are in use until here
+            free_level(L);
+            if (s != DG_OK) return s;
+        }
+    return DG_OK;
 }
 
 dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev, const double* qref_dev, double* tau_dev,

@@ -315,6 +315,16 @@ def test_tau_l2_restriction_parity(dg, orc, case, noniso, form):
     assert tau_rel(tg, to) < TAU_TOL
 
 
+def test_tau_noniso_streaming(dg, orc, monkeypatch):
+    """The levels built / run / freed one at a time (the fallback when the
+    resident sub-contexts do not fit in device memory) give the same tau."""
+    monkeypatch.setenv("DGTAU_NONISO_STREAM", "1")
+    mesh, orders, kw = CASES["ragged_1to8"]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, **kw)
+    tg = S.tau_estimate(qd, S.rhs_eval(qd), noniso=True).cpu().numpy()
+    assert tau_rel(tg, P.tau_estimate_noniso(orders, q, P.rhs(orders, q))) < TAU_TOL
+
+
 def test_tau_noniso_layout_change(dg, orc):
     """The coarse-level contexts follow set_orders (rebuilt for a new layout)."""
     mesh, orders, kw = CASES["cfg3_subbox_mixed"]()
