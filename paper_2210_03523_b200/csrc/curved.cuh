@@ -884,171 +884,19 @@ __global__ void __launch_bounds__(128) k_mortar_geom(CMortarParams P, double* mg
     }
 }
 
-// Curved mortar v2 (reading A6): one CTA per mortar face.  The mortar metric
-// comes precomputed (k_mortar_geom); traces of both sides (5 conserved + 15
-// gradient components for NS) are interpolated to the mortar grid by two
-// tensor passes on zero-padded 9 x 9 arrays, the flux is evaluated per mortar
-// point, and two tensor passes of the exact L2 projection return it to each
-// side.  Same operators as v1 (which used the dense 2-D products).
-constexpr int CM_BS = 128;
-constexpr int CM_NC = 20;  // components per side: 5 conserved + 15 gradient
-constexpr size_t CM_SMEM = sizeof(double) * (4 * CM_NC * 81 + 8 * 81);
-
-__device__ __forceinline__ void cm_pass(const double* __restrict__ A, const double* __restrict__ in,
-                                        double* __restrict__ out, int ni, int nl, bool along_a, int ncomp, int t0)
-{
-    // in/out: [comp][b*9 + a]; one thread per (comp, line r < nl); A zero padded 9 x 9
-    for (int task = t0; task < ncomp * nl; task += CM_BS) {
-        const int c = task / nl, r = task - c * nl;
-        const int xs = along_a ? 1 : 9;
-        const double* x0 = in + c * 81 + (along_a ? r * 9 : r);
-        double* o = out + c * 81 + (along_a ? r * 9 : r);
-        double x[9];
-#pragma unroll
-        for (int a = 0; a < 9; ++a) x[a] = x0[a * xs];
-        for (int i = 0; i < ni; ++i) {
-            double s = 0.0;
-#pragma unroll
-            for (int a = 0; a < 9; ++a) s = fma(A[i * 9 + a], x[a], s);
-            o[i * xs] = s;
-        }
-    }
-}
-
-__global__ void __launch_bounds__(CM_BS, 4) k_mortar_curved2(CMortarParams P, const double* mgeo, const long long* mgoff,
-                                                         int nitems)
-{
-    extern __shared__ __align__(16) double cm_sm[];
-    // B0: traces, then mortar states, then projection pass A; B1: interpolation
-    // pass A, then mortar fluxes (B1[0]); OP: interp TaL TbL TaR TbR, projection
-    // PaL PbL PaR PbR (zero padded)
-    double (*B0)[CM_NC][81] = reinterpret_cast<double (*)[CM_NC][81]>(cm_sm);
-    double (*B1)[CM_NC][81] = reinterpret_cast<double (*)[CM_NC][81]>(cm_sm + 2 * CM_NC * 81);
-    double (*OP)[81] = reinterpret_cast<double (*)[81]>(cm_sm + 4 * CM_NC * 81);
-    const int t = threadIdx.x;
-    // padding values only ever meet zero operator entries: finite once is enough
-    for (int w = t; w < 2 * CM_NC * 81; w += CM_BS) { (&B0[0][0][0])[w] = 0.0; (&B1[0][0][0])[w] = 0.0; }
-    for (int fid = blockIdx.x; fid < nitems; fid += gridDim.x) {
-    __syncthreads();  // previous face fully consumed
-    const MortarItem it = P.items[fid];
-    const int d = it.d;
-    const int ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
-    int NL[3], NR[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) { NL[k] = P.orders[3 * it.L + k]; NR[k] = P.orders[3 * it.R + k]; }
-    const int M1 = max(NL[ta], NR[ta]), M2 = max(NL[tb], NR[tb]);
-    const int m1 = M1 + 1, m2 = M2 + 1, nm = m1 * m2;
-    const bool ns = P.ph.physics == 1;
-    const int nin = (P.mode == 0 && ns) ? CM_NC : NV;  // components interpolated per side
-    const int nout = P.mode == 0 ? NV : 15;            // components projected back
-    for (int w = t; w < 8 * 81; w += CM_BS) {
-        const int k = w / 81, r = w - k * 81, row = r / 9, col = r - row * 9;
-        const int* NS = (k & 2) ? NR : NL;
-        const bool bdir = k & 1;
-        const int ns_ = bdir ? NS[tb] : NS[ta], mm = bdir ? M2 : M1;
-        double val = 0.0;
-        if (k < 4) {
-            if (row <= mm && col <= ns_) val = P.tab->T[ns_][mm][row * (ns_ + 1) + col];
-        } else {
-            if (row <= ns_ && col <= mm) val = P.tab->P[mm][ns_][row * (mm + 1) + col];
-        }
-        OP[k][r] = val;
-    }
-    __syncthreads();
-    // traces: one (side, component, b) row per task
-    for (int task = t; task < 2 * nin * 9; task += CM_BS) {
-        const int side = task / (nin * 9), r = task - side * nin * 9, c = r / 9, b = r - c * 9;
-        const int* NS = side ? NR : NL;
-        if (b > NS[tb]) continue;
-        const int st[3] = {1, NS[0] + 1, (NS[0] + 1) * (NS[1] + 1)};
-        const int n = (NS[0] + 1) * (NS[1] + 1) * (NS[2] + 1);
-        const long long o = P.off[side ? it.R : it.L];
-        const int base = (side == 0 ? NS[d] : 0) * st[d] + b * st[tb];
-        const double* src = c < NV ? P.q + o + (long long)c * n + base : P.grad + 3 * o + (long long)(c - NV) * n + base;
-        double* dst = &B0[side][c][b * 9];
-        for (int a = 0; a <= NS[ta]; ++a) dst[a] = __ldg(src + a * st[ta]);
-    }
-    __syncthreads();
-    // interpolation to the mortar: along a (B0 -> B1), along b (B1 -> B0)
-    for (int side = 0; side < 2; ++side) {
-        const int* NS = side ? NR : NL;
-        cm_pass(OP[2 * side], &B0[side][0][0], &B1[side][0][0], m1, NS[tb] + 1, true, nin, t);
-    }
-    __syncthreads();
-    for (int side = 0; side < 2; ++side) cm_pass(OP[2 * side + 1], &B1[side][0][0], &B0[side][0][0], m2, m1, false, nin, t);
-    __syncthreads();
-    // flux at the mortar points -> B1[0] (nout components)
-    const double* Jg = mgeo + mgoff[fid];
-    if (t < nm) {
-        const int i = t % m1, j = t / m1, pidx = j * 9 + i;
-        double qL[NV], qR[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) { qL[v] = B0[0][v][pidx]; qR[v] = B0[1][v][pidx]; }
-        const double jf[3] = {Jg[t], Jg[nm + t], Jg[2 * nm + t]};
-        if (P.mode == 1) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-#pragma unroll
-                for (int v = 0; v < NV; ++v) B1[0][c * NV + v][pidx] = 0.5 * (qL[v] + qR[v]) * jf[c];
-        } else {
-            const double S = sqrt(jf[0] * jf[0] + jf[1] * jf[1] + jf[2] * jf[2]);
-            const double nrm[3] = {jf[0] / S, jf[1] / S, jf[2] / S};
-            double F[NV];
-            riemann(qL, qR, nrm, P.ph, F);
-#pragma unroll
-            for (int v = 0; v < NV; ++v) F[v] *= S;
-            if (ns) {
-                double gL[15], gR[15], fL[NV], fR[NV];
-#pragma unroll
-                for (int c = 0; c < 15; ++c) { gL[c] = B0[0][NV + c][pidx]; gR[c] = B0[1][NV + c][pidx]; }
-                visc_dot(qL, gL, jf[0], jf[1], jf[2], P.ph, fL);
-                visc_dot(qR, gR, jf[0], jf[1], jf[2], P.ph, fR);
-#pragma unroll
-                for (int v = 0; v < NV; ++v) F[v] -= 0.5 * (fL[v] + fR[v]);
-            }
-#pragma unroll
-            for (int v = 0; v < NV; ++v) B1[0][v][pidx] = F[v];
-        }
-    }
-    __syncthreads();
-    // exact L2 projection back: along a (B1[0] -> B0[side]), then along b -> global
-    for (int side = 0; side < 2; ++side) {
-        const int* NS = side ? NR : NL;
-        cm_pass(OP[4 + 2 * side], &B1[0][0][0], &B0[side][0][0], NS[ta] + 1, m2, true, nout, t);
-    }
-    __syncthreads();
-    for (int side = 0; side < 2; ++side) {
-        const int* NS = side ? NR : NL;
-        const int s1 = NS[ta] + 1, s2 = NS[tb] + 1, nsd = s1 * s2;
-        const double* Pb = OP[5 + 2 * side];
-        const long long mo = P.moff[6 * (side == 0 ? it.L : it.R) + 2 * d + (side == 0 ? 1 : 0)];
-        double* dst = P.mortarG + (P.mode == 0 ? mo : 3 * mo);
-        for (int task = t; task < nout * s1; task += CM_BS) {  // (component, column a): all rows b'
-            const int c = task / s1, a = task - c * s1;
-            double x[9];
-#pragma unroll
-            for (int m = 0; m < 9; ++m) x[m] = B0[side][c][m * 9 + a];
-            for (int bb = 0; bb < s2; ++bb) {
-                double s = 0.0;
-#pragma unroll
-                for (int m = 0; m < 9; ++m) s = fma(Pb[bb * 9 + m], x[m], s);
-                dst[(long long)c * nsd + a + s1 * bb] = s;
-            }
-        }
-    }
-    }
-}
 
 
-// Curved / NS mortar faces, v3: k_mortar3's pipeline (persistent CTAs, work
-// counter, cp.async prefetch of the next face's traces, constant-memory
-// operators, identity passes skipped) for curved meshes.  NIN components are
-// interpolated per side (5: q; 20: q and the BR1 gradient), NOUT projected
-// back (5: numerical flux; 15: BR1 terms q^ Ja_c).  Threads 0-127 work on
-// side L, 128-255 on side R; at the mortar points threads 0-80 evaluate the
-// Riemann flux (or the BR1 average) and, for NS, threads 128-208 the averaged
-// viscous flux.  Same arithmetic as k_mortar_curved2 (metric Ja of the mortar
-// from L, reading A6).
+// Curved / NS mortar faces (reading A6): k_mortar3's pipeline (persistent
+// CTAs, work counter, cp.async prefetch of the next face's traces,
+// constant-memory operators, identity passes skipped) for curved meshes.  The
+// traces of both sides are interpolated to the mortar grid M_t = max(L_t, R_t)
+// by tensor passes, the flux is evaluated per mortar point with the mortar
+// metric Ja of the L side (precomputed by k_mortar_geom), and the exact L2
+// projection returns it to each side.  NIN components are interpolated per
+// side (5: q; 20: q and the BR1 gradient), NOUT projected back (5: numerical
+// flux; 15: BR1 terms q^ Ja_c).  Threads 0-127 work on side L, 128-255 on side
+// R; at the mortar points threads 0-80 evaluate the Riemann flux (or the BR1
+// average) and, for NS, threads 128-208 the averaged viscous flux.
 constexpr int CM3_BS = 256, CM3_H = 128;
 
 template <int NIN, int NOUT>

@@ -401,7 +401,6 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         cudaFuncSetAttribute(k_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
         cudaFuncSetAttribute(k_tau, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
         cudaFuncSetAttribute(k_tau5, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 4096);  // 3.1 KB static
-        cudaFuncSetAttribute(k_mortar_curved2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CM_SMEM);
         cudaFuncSetAttribute(k_mortar_c3<5, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CM3<5, 5>::smem);
         cudaFuncSetAttribute(k_mortar_c3<20, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CM3<20, 5>::smem);
         cudaFuncSetAttribute(k_mortar_c3<5, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CM3<5, 15>::smem);
@@ -912,7 +911,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
             ctx->launches++;
         }
         CK(cudaGetLastError());
-        // mortar metric at the mortar nodes, once per layout (k_mortar_curved2 reads it)
+        // mortar metric at the mortar nodes, once per layout (k_mortar_c3 reads it)
         dfree(ctx->d_mgeo);
         dfree(ctx->d_mgoff);
         if (ctx->nmortar > 0) {
