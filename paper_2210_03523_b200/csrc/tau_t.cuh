@@ -190,6 +190,8 @@ __global__ void __launch_bounds__(TAU5_BS, 3) k_tau5(Tau5Params P)
     const int nd = Nd + 1;
     const int nx = n / nd;  // coarse nodes per unit of O_d (cross-section of d)
     const long long o = P.off[e];
+    // element size (phase D), loaded now so its latency hides behind phases A-C
+    const double h0 = __ldg(P.hgeo + 3 * e), h1 = __ldg(P.hgeo + 3 * e + 1), h2 = __ldg(P.hgeo + 3 * e + 2);
     if (tid <= nlev) {  // closed forms: S(li) = sum_{j<li} (p0 + j + 1)
         const int li = tid, Sl = li * (p0 + 1) + li * (li - 1) / 2;
         lbase[li] = nx * Sl;
@@ -282,7 +284,6 @@ __global__ void __launch_bounds__(TAU5_BS, 3) k_tau5(Tau5Params P)
     __syncthreads();
     // (D) tau~ = T_d R + sum_a (2/h_a) D f_a; traditional * J w w w
     {
-        const double h0 = P.hgeo[3 * e], h1 = P.hgeo[3 * e + 1], h2 = P.hgeo[3 * e + 2];
         const double sc0 = 2.0 / h0, sc1 = 2.0 / h1, sc2 = 2.0 / h2;
         const double Jel = h0 * h1 * h2 / 8.0;
         int lcur = -1;
