@@ -217,6 +217,13 @@ __device__ void element_metrics_fp64(const CurvedMesh& cm, int e, int o1, int o2
     const double* T1 = tab->T[cm.g1][o1 - 1];
     const double* T2 = tab->T[cm.g2][o2 - 1];
     const double* T3 = tab->T[cm.g3][o3 - 1];
+    // the element's geometry coefficients staged in Mout (written only below)
+    const double* Gp = G;
+    if (3 * cm.ng <= 10 * no) {
+        for (int w = threadIdx.x; w < 3 * cm.ng; w += blockDim.x) Mout[w] = __ldg(G + w);
+        __syncthreads();
+        Gp = Mout;
+    }
     for (int t = threadIdx.x; t < no; t += blockDim.x) {
         int i, j, k;
         node_ijk(t, o1, o2, i, j, k);
@@ -229,7 +236,7 @@ __device__ void element_metrics_fp64(const CurvedMesh& cm, int e, int o1, int o2
                     const double wgt = w23 * T1[i * ga + a];
                     const int gi = a + ga * (b + gb * c);
 #pragma unroll
-                    for (int q = 0; q < 3; ++q) x[q] = fma(wgt, __ldg(G + q * cm.ng + gi), x[q]);
+                    for (int q = 0; q < 3; ++q) x[q] = fma(wgt, Gp[q * cm.ng + gi], x[q]);
                 }
             }
         }
