@@ -1111,6 +1111,35 @@ struct CTauParams {
     PhysDev ph;
 };
 
+// q_c = T_d q and T_d R at one coarse node (line length ND at compile time:
+// the loads of a variable's line are issued together)
+template <int ND>
+__device__ __forceinline__ void tau_interp_node(const double* __restrict__ T, int ic, const double* __restrict__ qe,
+                                                const double* __restrict__ re, int n, int base, int stride,
+                                                double* Qc, double* Rc, int nO, int t)
+{
+    double w[ND];
+#pragma unroll
+    for (int a = 0; a < ND; ++a) w[a] = T[ic * ND + a];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+        double xq[ND], xr[ND];
+#pragma unroll
+        for (int a = 0; a < ND; ++a) {
+            xq[a] = __ldg(qe + (long long)v * n + base + a * stride);
+            xr[a] = __ldg(re + (long long)v * n + base + a * stride);
+        }
+        double s = 0.0, r = 0.0;
+#pragma unroll
+        for (int a = 0; a < ND; ++a) {
+            s += w[a] * xq[a];
+            r += w[a] * xr[a];
+        }
+        Qc[v * nO + t] = s;
+        Rc[v * nO + t] = r;
+    }
+}
+
 template <int BS>
 __global__ void __launch_bounds__(BS, BS == 256 ? 2 : (BS == 128 ? 5 : 10)) k_tau_curved(CTauParams P)
 {
@@ -1142,17 +1171,20 @@ __global__ void __launch_bounds__(BS, BS == 256 ? 2 : (BS == 128 ? 5 : 10)) k_ta
         const int ic = d == 0 ? i : (d == 1 ? j : k);
         if (d == 0) i = 0; else if (d == 1) j = 0; else k = 0;
         const int base = i + n1 * (j + n2 * k);
-        for (int v = 0; v < NV; ++v) {
-            double s = 0.0, r = 0.0;
-            for (int a = 0; a < nd; ++a) {
-                const double w = T[ic * nd + a];
-                s += w * __ldg(P.q + o + (long long)v * n + base + a * stride);
-                r += w * __ldg(P.qref + o + (long long)v * n + base + a * stride);
-            }
-            Qc[v * nO + t] = s;
-            Rc[v * nO + t] = r;
-            if (!ns) A[v * nO + t] = 0.0;
+        const double* qe = P.q + o;
+        const double* re = P.qref + o;
+        switch (nd) {
+            case 2: tau_interp_node<2>(T, ic, qe, re, n, base, stride, Qc, Rc, nO, t); break;
+            case 3: tau_interp_node<3>(T, ic, qe, re, n, base, stride, Qc, Rc, nO, t); break;
+            case 4: tau_interp_node<4>(T, ic, qe, re, n, base, stride, Qc, Rc, nO, t); break;
+            case 5: tau_interp_node<5>(T, ic, qe, re, n, base, stride, Qc, Rc, nO, t); break;
+            case 6: tau_interp_node<6>(T, ic, qe, re, n, base, stride, Qc, Rc, nO, t); break;
+            case 7: tau_interp_node<7>(T, ic, qe, re, n, base, stride, Qc, Rc, nO, t); break;
+            case 8: tau_interp_node<8>(T, ic, qe, re, n, base, stride, Qc, Rc, nO, t); break;
+            default: tau_interp_node<9>(T, ic, qe, re, n, base, stride, Qc, Rc, nO, t); break;
         }
+        if (!ns)
+            for (int v = 0; v < NV; ++v) A[v * nO + t] = 0.0;
     }
     __syncthreads();
     if (ns) {  // isolated gradient: J g_k = sum_d' D^{d'} (Ja^{d'}_k q), all k per direction
