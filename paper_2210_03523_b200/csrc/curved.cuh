@@ -206,78 +206,6 @@ __device__ void element_metrics(const CurvedMesh& cm, int e, int o1, int o2, int
     __syncthreads();
 }
 
-// As element_metrics in plain fp64 (coarse tau levels, reading R6): X = T^{g->o}
-// Xgeo, derivatives by D^o, cross-product form; Xs: 3 no doubles of scratch.
-__device__ void element_metrics_fp64(const CurvedMesh& cm, int e, int o1, int o2, int o3, const Tables* tab,
-                                     double* Xs, double* Mout)
-{
-    const int no = o1 * o2 * o3;
-    const int ga = cm.g1 + 1, gb = cm.g2 + 1;
-    const double* G = cm.geo + (long long)e * 3 * cm.ng;
-    const double* T1 = tab->T[cm.g1][o1 - 1];
-    const double* T2 = tab->T[cm.g2][o2 - 1];
-    const double* T3 = tab->T[cm.g3][o3 - 1];
-    // the element's geometry coefficients staged in Mout (written only below)
-    const double* Gp = G;
-    if (3 * cm.ng <= 10 * no) {
-        for (int w = threadIdx.x; w < 3 * cm.ng; w += blockDim.x) Mout[w] = __ldg(G + w);
-        __syncthreads();
-        Gp = Mout;
-    }
-    for (int t = threadIdx.x; t < no; t += blockDim.x) {
-        int i, j, k;
-        node_ijk(t, o1, o2, i, j, k);
-        double x[3] = {0.0, 0.0, 0.0};
-        for (int c = 0; c <= cm.g3; ++c) {
-            const double w3 = T3[k * (cm.g3 + 1) + c];
-            for (int b = 0; b <= cm.g2; ++b) {
-                const double w23 = w3 * T2[j * gb + b];
-                for (int a = 0; a <= cm.g1; ++a) {
-                    const double wgt = w23 * T1[i * ga + a];
-                    const int gi = a + ga * (b + gb * c);
-#pragma unroll
-                    for (int q = 0; q < 3; ++q) x[q] = fma(wgt, Gp[q * cm.ng + gi], x[q]);
-                }
-            }
-        }
-        Xs[t] = x[0];
-        Xs[no + t] = x[1];
-        Xs[2 * no + t] = x[2];
-    }
-    __syncthreads();
-    const double* D1 = tab->D[o1 - 1];
-    const double* D2 = tab->D[o2 - 1];
-    const double* D3 = tab->D[o3 - 1];
-    for (int t = threadIdx.x; t < no; t += blockDim.x) {
-        int i, j, k;
-        node_ijk(t, o1, o2, i, j, k);
-        double dx[3][3];
-        for (int c = 0; c < 3; ++c) {
-            const double* X = Xs + c * no;
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-            for (int m = 0; m < o1; ++m) s0 = fma(D1[i * o1 + m], X[m + o1 * (j + o2 * k)], s0);
-            for (int m = 0; m < o2; ++m) s1 = fma(D2[j * o2 + m], X[i + o1 * (m + o2 * k)], s1);
-            for (int m = 0; m < o3; ++m) s2 = fma(D3[k * o3 + m], X[i + o1 * (j + o2 * m)], s2);
-            dx[0][c] = s0;
-            dx[1][c] = s1;
-            dx[2][c] = s2;
-        }
-        const double* xa = dx[0];
-        const double* xb = dx[1];
-        const double* xc = dx[2];
-        double c1[3], c2[3], c3[3];
-        c1[0] = xb[1] * xc[2] - xb[2] * xc[1]; c1[1] = xb[2] * xc[0] - xb[0] * xc[2]; c1[2] = xb[0] * xc[1] - xb[1] * xc[0];
-        c2[0] = xc[1] * xa[2] - xc[2] * xa[1]; c2[1] = xc[2] * xa[0] - xc[0] * xa[2]; c2[2] = xc[0] * xa[1] - xc[1] * xa[0];
-        c3[0] = xa[1] * xb[2] - xa[2] * xb[1]; c3[1] = xa[2] * xb[0] - xa[0] * xb[2]; c3[2] = xa[0] * xb[1] - xa[1] * xb[0];
-        for (int q = 0; q < 3; ++q) {
-            Mout[q * no + t] = c1[q];
-            Mout[(3 + q) * no + t] = c2[q];
-            Mout[(6 + q) * no + t] = c3[q];
-        }
-        Mout[9 * no + t] = xa[0] * c1[0] + xa[1] * c1[1] + xa[2] * c1[2];
-    }
-    __syncthreads();
-}
 
 // one launch per size class: CTA b handles element perm[pbase + b]
 struct SizeClass {
@@ -359,6 +287,38 @@ __device__ __forceinline__ void dsum_comps(int od, const double* Dr, const doubl
     }
 }
 
+// as dsum_comps with ONE accumulator (sequential fma over m, the order of the
+// coarse metric terms' reference loop)
+template <int OD, int NC, typename Op>
+__device__ __forceinline__ void dchain_comps_t(const double* Dr, const double* Fl, int cs, int stride, Op op)
+{
+    double r[OD];
+#pragma unroll
+    for (int m = 0; m < OD; ++m) r[m] = Dr[m];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        double s = 0.0;
+#pragma unroll
+        for (int m = 0; m < OD; ++m) s = fma(r[m], Fl[c * cs + m * stride], s);
+        op(c, s);
+    }
+}
+
+template <int NC, typename Op>
+__device__ __forceinline__ void dchain_comps(int od, const double* Dr, const double* Fl, int cs, int stride, Op op)
+{
+    switch (od) {
+        case 2: dchain_comps_t<2, NC>(Dr, Fl, cs, stride, op); break;
+        case 3: dchain_comps_t<3, NC>(Dr, Fl, cs, stride, op); break;
+        case 4: dchain_comps_t<4, NC>(Dr, Fl, cs, stride, op); break;
+        case 5: dchain_comps_t<5, NC>(Dr, Fl, cs, stride, op); break;
+        case 6: dchain_comps_t<6, NC>(Dr, Fl, cs, stride, op); break;
+        case 7: dchain_comps_t<7, NC>(Dr, Fl, cs, stride, op); break;
+        case 8: dchain_comps_t<8, NC>(Dr, Fl, cs, stride, op); break;
+        default: dchain_comps_t<9, NC>(Dr, Fl, cs, stride, op); break;
+    }
+}
+
 // as dsum, with the D row held in registers (loaded once for all components)
 struct DRow {
     double r[NP];
@@ -378,6 +338,73 @@ struct DRow {
         return s0 + s1;
     }
 };
+
+// As element_metrics in plain fp64 (coarse tau levels, reading R6): X = T^{g->o}
+// Xgeo, derivatives by D^o, cross-product form; Xs: 3 no doubles of scratch.
+__device__ void element_metrics_fp64(const CurvedMesh& cm, int e, int o1, int o2, int o3, const Tables* tab,
+                                     const double (*Ds)[NP * NP], double* Xs, double* Mout)
+{
+    const int no = o1 * o2 * o3;
+    const int ga = cm.g1 + 1, gb = cm.g2 + 1;
+    const double* G = cm.geo + (long long)e * 3 * cm.ng;
+    const double* T1 = tab->T[cm.g1][o1 - 1];
+    const double* T2 = tab->T[cm.g2][o2 - 1];
+    const double* T3 = tab->T[cm.g3][o3 - 1];
+    // the element's geometry coefficients staged in Mout (written only below)
+    const double* Gp = G;
+    if (3 * cm.ng <= 10 * no) {
+        for (int w = threadIdx.x; w < 3 * cm.ng; w += blockDim.x) Mout[w] = __ldg(G + w);
+        __syncthreads();
+        Gp = Mout;
+    }
+    for (int t = threadIdx.x; t < no; t += blockDim.x) {
+        int i, j, k;
+        node_ijk(t, o1, o2, i, j, k);
+        double x[3] = {0.0, 0.0, 0.0};
+        for (int c = 0; c <= cm.g3; ++c) {
+            const double w3 = T3[k * (cm.g3 + 1) + c];
+            for (int b = 0; b <= cm.g2; ++b) {
+                const double w23 = w3 * T2[j * gb + b];
+                for (int a = 0; a <= cm.g1; ++a) {
+                    const double wgt = w23 * T1[i * ga + a];
+                    const int gi = a + ga * (b + gb * c);
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) x[q] = fma(wgt, Gp[q * cm.ng + gi], x[q]);
+                }
+            }
+        }
+        Xs[t] = x[0];
+        Xs[no + t] = x[1];
+        Xs[2 * no + t] = x[2];
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < no; t += blockDim.x) {
+        int ijk[3];
+        node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
+        double dx[3][3];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const int od = d == 0 ? o1 : (d == 1 ? o2 : o3);
+            const int stride = d == 0 ? 1 : (d == 1 ? o1 : o1 * o2);
+            const int a = ijk[d];
+            dchain_comps<3>(od, Ds[d] + a * od, Xs + (t - a * stride), no, stride, [&](int cc, double s) { dx[d][cc] = s; });
+        }
+        const double* xa = dx[0];
+        const double* xb = dx[1];
+        const double* xc = dx[2];
+        double c1[3], c2[3], c3[3];
+        c1[0] = xb[1] * xc[2] - xb[2] * xc[1]; c1[1] = xb[2] * xc[0] - xb[0] * xc[2]; c1[2] = xb[0] * xc[1] - xb[1] * xc[0];
+        c2[0] = xc[1] * xa[2] - xc[2] * xa[1]; c2[1] = xc[2] * xa[0] - xc[0] * xa[2]; c2[2] = xc[0] * xa[1] - xc[1] * xa[0];
+        c3[0] = xa[1] * xb[2] - xa[2] * xb[1]; c3[1] = xa[2] * xb[0] - xa[0] * xb[2]; c3[2] = xa[0] * xb[1] - xa[1] * xb[0];
+        for (int q = 0; q < 3; ++q) {
+            Mout[q * no + t] = c1[q];
+            Mout[(3 + q) * no + t] = c2[q];
+            Mout[(6 + q) * no + t] = c3[q];
+        }
+        Mout[9 * no + t] = xa[0] * c1[0] + xa[1] * c1[1] + xa[2] * c1[2];
+    }
+    __syncthreads();
+}
 
 // D^{o_d - 1} of the three directions into shared memory (Ds[d][a*o_d + m])
 __device__ __forceinline__ void stage_D(double (*Ds)[NP * NP], const Tables* tab, int o1, int o2, int o3)
@@ -1162,7 +1189,7 @@ __global__ void __launch_bounds__(BS, BS == 256 ? 2 : (BS == 128 ? 5 : 10)) k_ta
     double* GA = Rc + NV * nO;               // 15 nO (NS)
     double* F = ns ? GA + 15 * nO : GA;      // 5 nO (NS gradient: 15 nO over F, A and 5 more)
     double* A = F + NV * nO;                 // 5 nO
-    element_metrics_fp64(P.cm, e, o1, o2, o3, P.tab, F, Mc);  // F, A: 10 nO >= 3 nO scratch
+    element_metrics_fp64(P.cm, e, o1, o2, o3, P.tab, Ds, F, Mc);  // F, A: 10 nO >= 3 nO scratch
     const long long o = P.off[e];
     const double* T = P.restr ? P.tab->P[nd - 1][p] : P.tab->T[nd - 1][p];
     for (int t = threadIdx.x; t < nO; t += BS) {
