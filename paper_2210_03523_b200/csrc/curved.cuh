@@ -1189,12 +1189,19 @@ __global__ void __launch_bounds__(BS, BS == 256 ? 2 : (BS == 128 ? 5 : 10)) k_ta
     double* GA = Rc + NV * nO;               // 15 nO (NS)
     double* F = ns ? GA + 15 * nO : GA;      // 5 nO (NS gradient: 15 nO over F, A and 5 more)
     double* A = F + NV * nO;                 // 5 nO
-    element_metrics_fp64(P.cm, e, o1, o2, o3, P.tab, Ds, F, Mc);  // F, A: 10 nO >= 3 nO scratch
+    // (i, j, k) of every coarse node, packed i | j << 8 | k << 16, computed once
+    int* IJK = reinterpret_cast<int*>(sm + (ns ? 50 : 30) * nO);
+    for (int t = threadIdx.x; t < nO; t += BS) {
+        int ii, jj, kk;
+        node_ijk(t, o1, o2, ii, jj, kk);
+        IJK[t] = ii | (jj << 8) | (kk << 16);
+    }
+    element_metrics_fp64(P.cm, e, o1, o2, o3, P.tab, Ds, F, Mc);  // F, A: 10 nO >= 3 nO scratch (barriers inside)
     const long long o = P.off[e];
     const double* T = P.restr ? P.tab->P[nd - 1][p] : P.tab->T[nd - 1][p];
     for (int t = threadIdx.x; t < nO; t += BS) {
-        int i, j, k;
-        node_ijk(t, o1, o2, i, j, k);
+        const int pk = IJK[t];
+        int i = pk & 255, j = (pk >> 8) & 255, k = pk >> 16;
         const int ic = d == 0 ? i : (d == 1 ? j : k);
         if (d == 0) i = 0; else if (d == 1) j = 0; else k = 0;
         const int base = i + n1 * (j + n2 * k);
@@ -1227,7 +1234,8 @@ __global__ void __launch_bounds__(BS, BS == 256 ? 2 : (BS == 128 ? 5 : 10)) k_ta
             __syncthreads();
             for (int t = threadIdx.x; t < nO; t += BS) {
                 int ijk[3];
-                node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
+                const int pk = IJK[t];
+                ijk[0] = pk & 255; ijk[1] = (pk >> 8) & 255; ijk[2] = pk >> 16;
                 const int a = dd == 0 ? ijk[0] : (dd == 1 ? ijk[1] : ijk[2]);
                 const int base = t - a * str;
                 dsum_comps<15>(od, Dd + a * od, F + base, nO, str, [&](int c, double sv) {
@@ -1258,7 +1266,8 @@ __global__ void __launch_bounds__(BS, BS == 256 ? 2 : (BS == 128 ? 5 : 10)) k_ta
         __syncthreads();
         for (int t = threadIdx.x; t < nO; t += BS) {
             int ijk[3];
-            node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
+            const int pk = IJK[t];
+            ijk[0] = pk & 255; ijk[1] = (pk >> 8) & 255; ijk[2] = pk >> 16;
             const int a = dd == 0 ? ijk[0] : (dd == 1 ? ijk[1] : ijk[2]);
             const int base = t - a * str;
             dsum_comps<NV>(od, Dd + a * od, F + base, nO, str, [&](int v, double sv) { A[v * nO + t] += sv; });
@@ -1267,8 +1276,8 @@ __global__ void __launch_bounds__(BS, BS == 256 ? 2 : (BS == 128 ? 5 : 10)) k_ta
     }
     double tmax = 0.0;
     for (int t = threadIdx.x; t < nO; t += BS) {
-        int i, j, k;
-        node_ijk(t, o1, o2, i, j, k);
+        const int pk = IJK[t];
+        int i = pk & 255, j = (pk >> 8) & 255, k = pk >> 16;
         const double J = Mc[9 * nO + t];
         double scale = 1.0;
         if (P.formulation == 1) scale = J * P.tab->w[o1 - 1][i] * P.tab->w[o2 - 1][j] * P.tab->w[o3 - 1][k];
