@@ -342,7 +342,7 @@ struct DRow {
 // As element_metrics in plain fp64 (coarse tau levels, reading R6): X = T^{g->o}
 // Xgeo, derivatives by D^o, cross-product form; Xs: 3 no doubles of scratch.
 __device__ void element_metrics_fp64(const CurvedMesh& cm, int e, int o1, int o2, int o3, const Tables* tab,
-                                     const double (*Ds)[NP * NP], double* Xs, double* Mout)
+                                     const double (*Ds)[NP * NP], const int* IJK, double* Xs, double* Mout)
 {
     const int no = o1 * o2 * o3;
     const int ga = cm.g1 + 1, gb = cm.g2 + 1;
@@ -358,8 +358,8 @@ __device__ void element_metrics_fp64(const CurvedMesh& cm, int e, int o1, int o2
         Gp = Mout;
     }
     for (int t = threadIdx.x; t < no; t += blockDim.x) {
-        int i, j, k;
-        node_ijk(t, o1, o2, i, j, k);
+        const int pk = IJK[t];  // packed (i, j, k), see k_tau_curved
+        const int i = pk & 255, j = (pk >> 8) & 255, k = pk >> 16;
         double x[3] = {0.0, 0.0, 0.0};
         for (int c = 0; c <= cm.g3; ++c) {
             const double w3 = T3[k * (cm.g3 + 1) + c];
@@ -379,8 +379,8 @@ __device__ void element_metrics_fp64(const CurvedMesh& cm, int e, int o1, int o2
     }
     __syncthreads();
     for (int t = threadIdx.x; t < no; t += blockDim.x) {
-        int ijk[3];
-        node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
+        const int pk = IJK[t];
+        const int ijk[3] = {pk & 255, (pk >> 8) & 255, pk >> 16};
         double dx[3][3];
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
@@ -1196,7 +1196,8 @@ __global__ void __launch_bounds__(BS, BS == 256 ? 2 : (BS == 128 ? 5 : 10)) k_ta
         node_ijk(t, o1, o2, ii, jj, kk);
         IJK[t] = ii | (jj << 8) | (kk << 16);
     }
-    element_metrics_fp64(P.cm, e, o1, o2, o3, P.tab, Ds, F, Mc);  // F, A: 10 nO >= 3 nO scratch (barriers inside)
+    __syncthreads();
+    element_metrics_fp64(P.cm, e, o1, o2, o3, P.tab, Ds, IJK, F, Mc);  // F, A: 10 nO >= 3 nO scratch (barriers inside)
     const long long o = P.off[e];
     const double* T = P.restr ? P.tab->P[nd - 1][p] : P.tab->T[nd - 1][p];
     for (int t = threadIdx.x; t < nO; t += BS) {
