@@ -563,7 +563,7 @@ __device__ __forceinline__ void load_grad(const double* base, int stride, double
 // point (the element kernel used to evaluate it on both sides): Roe flux along
 // the L side's face metric (reading A6) and, for NS, minus the BR1 average of
 // the two viscous fluxes -- the arithmetic of k_res_curved's kind-0 branch, so
-// both elements read bit-identical values.  One CTA per face; boundary faces
+// both elements read bit-identical values.  One warp per face; boundary faces
 // stay in the element kernel.  G block [v][pt] at the face's flux offset.
 struct CFaceParams {
     const double* q;
@@ -574,13 +574,15 @@ struct CFaceParams {
     PhysDev ph;
 };
 
-__global__ void __launch_bounds__(128) k_face_curved(CFaceParams P)
+__global__ void __launch_bounds__(128) k_face_curved(CFaceParams P, int nfaces)
 {
-    const FaceItem fi = P.faces[blockIdx.x];
+    const int f = blockIdx.x * 4 + (threadIdx.x >> 5);  // one warp per face
+    if (f >= nfaces) return;
+    const FaceItem fi = P.faces[f];
     if (fi.kind != 0) return;
     const bool ns = P.ph.physics == 1;
     const int d = fi.d;
-    for (int pt = threadIdx.x; pt < fi.nf; pt += blockDim.x) {
+    for (int pt = threadIdx.x & 31; pt < fi.nf; pt += 32) {
         const int ta = pt % fi.nta, tb = pt / fi.nta;
         const int nodeL = fi.baseL + ta * fi.saL + tb * fi.sbL;
         const int nodeR = fi.baseR + ta * fi.saR + tb * fi.sbR;

@@ -1069,7 +1069,7 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
         FP.faces = ctx->d_faces;
         FP.G = ctx->d_mortarG;
         FP.ph = phys_dev(ctx->prm);
-        k_face_curved<<<ctx->nfaces, 128, 0, st>>>(FP);
+        k_face_curved<<<(ctx->nfaces + 3) / 4, 128, 0, st>>>(FP, ctx->nfaces);
         ctx->launches++;
         P.fofs = ctx->d_fofs_el;
     }
