@@ -207,3 +207,51 @@ def test_cfg4_static_adaptation_cycle(dg, orc):
     assert rel_linf(qd.cpu().numpy(), qo, orders) < RES_TOL
     r = S.rhs_eval(qd).cpu().numpy()
     assert rel_linf(r, P.rhs(orders, qo), orders) < RES_TOL
+
+
+def test_full_size_cfg5_sampled(dg, orc):
+    """BASELINE cfg5 [B:11] at FULL size (96 x 256 x 16 O-grid, 393,216
+    elements, ~42.5 M DOF, orders Nx, Ny ~ U{2..8}, Nz = 2, NS): the device
+    residual and tau-estimate of 48 sampled elements against the oracle on a
+    local mesh around them -- the sampled elements and their face neighbours
+    owned, the next ring as halo, which is everything the BR1 residual of a
+    sampled element reads (the same construction that makes the multi-rank
+    owned results exact, test_dist_gloo)."""
+    import torch
+
+    from paper_2210_03523_b200 import partition as part
+
+    spec = W.CONFIGS["cfg5"]
+    mesh = W.make_mesh(spec["mesh"])
+    orders = W.make_orders(spec["orders"], mesh.E)
+    nsp = W.ns_params()
+    q = W.freestream_noise_state(orders, (1.0, 1.0, 0.0, 0.0, nsp["p_inf"]), noise=1e-3, seed=4)
+    S = dg.Solver(mesh, physics=dg.NS, mu=nsp["mu"], Pr=nsp["Pr"], qinf=nsp["qinf"])
+    S.set_orders(orders)
+    qd = torch.from_numpy(q).cuda()
+    rd = S.rhs_eval(qd)
+    tg = S.tau_estimate(qd, rd).cpu().numpy()
+    r = rd.cpu().numpy()
+    del qd, rd
+    rng = np.random.default_rng(55)
+    samp = np.sort(rng.choice(mesh.E, 48, replace=False))
+    nb = mesh.nbr[samp].ravel()
+    ring = np.unique(nb[nb >= 0])
+    owner = np.ones(mesh.E, np.int32)
+    owner[samp] = 0
+    owner[ring] = 0
+    lm = part.local_mesh(mesh, owner, 0)
+    lo = np.ascontiguousarray(orders[lm.gids], np.int32)
+    off = W.offsets(orders, 5)
+    ql = np.concatenate([q[off[g]:off[g + 1]] for g in lm.gids])
+    ph_o = orc.phys(orc.NS, mu=nsp["mu"], Pr=nsp["Pr"], qinf=nsp["qinf"])
+    Pl = orc.Problem(lm, ph_o)
+    rl = Pl.rhs(lo, ql)
+    tl = Pl.tau_estimate(lo, ql, rl)
+    offl = W.offsets(lo, 5)
+    pos = {int(g): i for i, g in enumerate(lm.gids)}
+    li = np.array([pos[int(e)] for e in samp])
+    r_g = np.concatenate([r[off[e]:off[e + 1]] for e in samp])
+    r_o = np.concatenate([rl[offl[i]:offl[i + 1]] for i in li])
+    assert rel_linf(r_g, r_o, orders[samp]) < RES_TOL
+    assert tau_rel(tg[samp], tl[li]) < TAU_TOL
