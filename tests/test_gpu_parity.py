@@ -465,6 +465,25 @@ def test_dynamic_adaptation_cycle_cfg2_like(dg, orc):
         assert rel_linf(qd.cpu().numpy(), qo, orders) < RES_TOL
 
 
+def test_full_size_cfg2_rk_steps(dg, orc):
+    """The bench's launch configuration at its full size (cfg2, 16^3 elements,
+    N=6, 1.4 M DOF): two RK3 steps in one dg_rk_steps call (the second step's
+    dt formed inside its first stage) against the oracle's trajectory and dt."""
+    import torch
+
+    mesh, orders, kw = CASES["cfg2_uniform6"]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, **kw)
+    dts = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in range(2)]
+    S.compute_dt(qd, 0.5, dts[0])
+    qa, qb, g = qd.clone(), torch.empty_like(qd), torch.empty_like(qd)
+    qs, dt_next = S.rk_steps(2, qa, qb, g, dts[0], dts[1], 0.5)
+    qo = q.copy()
+    for _ in range(2):
+        qo = P.rk3_step(orders, qo, P.dt(orders, qo, 0.5))
+    assert rel_linf(qs.cpu().numpy(), qo, orders) < RES_TOL
+    assert abs(dt_next.item() - P.dt(orders, qo, 0.5)) <= 1e-13 * dt_next.item()
+
+
 def test_full_size_cfg3(dg, orc):
     """BASELINE cfg3 [B:9] at full size (32^3 elements, orders U{2..7}: ~97 %
     mortar faces): residual, two RK3 steps in the bench's launch configuration
