@@ -484,6 +484,15 @@ def test_full_size_cfg2_rk_steps(dg, orc):
     assert abs(dt_next.item() - P.dt(orders, qo, 0.5)) <= 1e-13 * dt_next.item()
 
 
+def test_full_size_cfg2_tau_noniso(dg, orc):
+    """Non-isolated tau (R7) at the bench's full size (cfg2): 15 coarse levels
+    of the whole 16^3 mesh against the oracle's composition."""
+    mesh, orders, kw = CASES["cfg2_uniform6"]()
+    P, S, q, qd = setup(dg, orc, mesh, orders, **kw)
+    tg = S.tau_estimate(qd, S.rhs_eval(qd), noniso=True).cpu().numpy()
+    assert tau_rel(tg, P.tau_estimate_noniso(orders, q, P.rhs(orders, q))) < TAU_TOL
+
+
 def test_full_size_cfg3(dg, orc):
     """BASELINE cfg3 [B:9] at full size (32^3 elements, orders U{2..7}: ~97 %
     mortar faces): residual, two RK3 steps in the bench's launch configuration
