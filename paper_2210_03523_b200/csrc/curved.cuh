@@ -238,22 +238,10 @@ __global__ void __launch_bounds__(CBS) k_metrics(MetParams P)
 // ---------------------------------------------------------------------------
 // generic sweep helpers: acc[c][node] (+)= sum_m D^{o_d}[a][m] F[c][..m..]
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double dsum(const double* Dd, int od, int a, const double* Fl, int stride)
-{
-    // Dd in shared memory (stage_D); independent partial sums for the FMA chain
-    double s0 = 0.0, s1 = 0.0;
-    const double* Dr = Dd + a * od;
-#pragma unroll
-    for (int m = 0; m < NP; m += 2) {
-        if (m < od) s0 = fma(Dr[m], Fl[m * stride], s0);
-        if (m + 1 < od) s1 = fma(Dr[m + 1], Fl[(m + 1) * stride], s1);
-    }
-    return s0 + s1;
-}
 
 // sum_m D[a][m] Fl[c*cs + m*stride] for the NC components c of a line, with
-// the line length OD a compile-time constant (no predicated-off FMAs); the
-// same two partial sums as dsum, so the results are identical
+// the line length OD a compile-time constant (no predicated-off FMAs); two
+// partial sums (even / odd m) for a shorter FMA chain
 template <int OD, int NC, typename Op>
 __device__ __forceinline__ void dsum_comps_t(const double* Dr, const double* Fl, int cs, int stride, Op op)
 {
@@ -319,25 +307,6 @@ __device__ __forceinline__ void dchain_comps(int od, const double* Dr, const dou
     }
 }
 
-// as dsum, with the D row held in registers (loaded once for all components)
-struct DRow {
-    double r[NP];
-    __device__ __forceinline__ DRow(const double* Dd, int od, int a)
-    {
-#pragma unroll
-        for (int m = 0; m < NP; ++m) r[m] = m < od ? Dd[a * od + m] : 0.0;
-    }
-    __device__ __forceinline__ double sum(int od, const double* Fl, int stride) const
-    {
-        double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-        for (int m = 0; m < NP; m += 2) {
-            if (m < od) s0 = fma(r[m], Fl[m * stride], s0);
-            if (m + 1 < od) s1 = fma(r[m + 1], Fl[(m + 1) * stride], s1);
-        }
-        return s0 + s1;
-    }
-};
 
 // As element_metrics in plain fp64 (coarse tau levels, reading R6): X = T^{g->o}
 // Xgeo, derivatives by D^o, cross-product form; Xs: 3 no doubles of scratch.
