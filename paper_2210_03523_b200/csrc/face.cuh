@@ -210,7 +210,7 @@ __device__ __forceinline__ void mt_unpack(int o, int* N) { N[0] = o & 15; N[1] =
 
 __global__ void __launch_bounds__(MT_BS, MT_MINB) k_mortar3(MortarParams P, const MortarFace* items, int nitems, int* queue)
 {
-    __shared__ double TR[2][2][MT_A];  // [stage][side] traces (zero padded)
+    __shared__ double TR[3][2][MT_A];  // [stage][side] traces (zero padded), faces k, k+1, k+2 in flight
     __shared__ double TM[2][MT_A];     // pass-A results (interpolation, then projection)
     __shared__ double QM[2][MT_A];     // pass-B results (mortar states, then projected fluxes)
     __shared__ double GM[MT_A];        // Roe flux on the mortar
@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(MT_BS, MT_MINB) k_mortar3(MortarParams P, cons
     const int f0 = blockIdx.x;
     if (f0 >= nitems) return;
 
-    for (int w = t; w < 4 * MT_A; w += MT_BS) (&TR[0][0][0])[w] = 0.0;  // padding: finite once and for all
+    for (int w = t; w < 6 * MT_A; w += MT_BS) (&TR[0][0][0])[w] = 0.0;  // padding: finite once and for all
     for (int w = t; w < 2 * MT_A; w += MT_BS) { (&TM[0][0])[w] = 0.0; (&QM[0][0])[w] = 0.0; }
     for (int w = t; w < MT_A; w += MT_BS) GM[w] = 0.0;
     __syncthreads();
@@ -239,28 +239,33 @@ __global__ void __launch_bounds__(MT_BS, MT_MINB) k_mortar3(MortarParams P, cons
         double* dst = TR[st][me] + v * 81 + b * 9;
         for (int a = 0; a < s1; ++a) cp_async8(dst + a, src + a * sta);
     };
-    // faces: blockIdx.x, blockIdx.x + G, then dynamically from a work counter
-    // (mortar sizes vary: a static round robin leaves a long tail)
-    // (faces f0, f0 + G, f0 + 2G, then 3G + counter fetched one face ahead)
+    // faces: f0, f0 + G, f0 + 2G, then dynamically from a work counter (mortar
+    // sizes vary: a static round robin leaves a long tail).  Traces run two
+    // faces ahead (3 stages); face records one more; thread 0 fetches the
+    // counter one further, so no latency of the chain is exposed.
     __shared__ int s_nn[2];
-    int fcur = f0, fnext = f0 + G, pend = f0 + 2 * G;
+    int fcur = f0, f1 = f0 + G, f2 = f0 + 2 * G, pend = 3 * G;
+    if (t == 0) pend = 3 * G + atomicAdd(queue, 1);
     MortarFace cur = items[f0];
-    MortarFace nxt = cur;
-    if (fnext < nitems) nxt = items[fnext];
+    MortarFace n1 = cur, n2 = cur;
+    if (f1 < nitems) n1 = items[f1];
+    if (f2 < nitems) n2 = items[f2];
     issue(cur, 0);
+    asm volatile("cp.async.commit_group;\n" ::);
+    if (f1 < nitems) issue(n1, 1);
     asm volatile("cp.async.commit_group;\n" ::);
     for (int k = 0;; ++k) {
         if (fcur >= nitems) break;
         if (t == 0) {
-            s_nn[k & 1] = pend;
+            s_nn[k & 1] = pend;  // face k+3
             pend = 3 * G + atomicAdd(queue, 1);
         }
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-        __syncthreads();  // traces of face k landed; face k-1 fully consumed
-        const int fnn = s_nn[k & 1];
-        MortarFace nn = nxt;
-        if (fnn < nitems) nn = items[fnn];
-        if (fnext < nitems) issue(nxt, (k + 1) & 1);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // face k landed (k+1 may be in flight)
+        __syncthreads();  // ... for every thread; face k-1 fully consumed
+        const int f3 = s_nn[k & 1];
+        MortarFace n3 = n2;
+        if (f3 < nitems) n3 = items[f3];
+        if (f2 < nitems) issue(n2, (k + 2) % 3);
         asm volatile("cp.async.commit_group;\n" ::);
 
         const int d = cur.d;
@@ -275,7 +280,7 @@ __global__ void __launch_bounds__(MT_BS, MT_MINB) k_mortar3(MortarParams P, cons
         const bool ia0 = NL[ta] < M1, ia1 = NR[ta] < M1, ib0 = NL[tb] < M2, ib1 = NR[tb] < M2;
         const double* opA = c_mop[mt_pair(sa_me - 1, M1)];
         const double* opB = c_mop[mt_pair(sb_me - 1, M2)];
-        double* TRs = &TR[k & 1][0][0];
+        double* TRs = &TR[k % 3][0][0];
         // side traces -> mortar: along a where s_a < m1, then along b where s_b < m2
         if (ia) mt_lines(opA, TRs + me * MT_A, TM[me], m1, sb_me, true, l);
         bar_side(me);
@@ -318,10 +323,12 @@ __global__ void __launch_bounds__(MT_BS, MT_MINB) k_mortar3(MortarParams P, cons
             const double* src = W + v * 81 + b * 9;
             for (int a = 0; a < sa_me; ++a) dst[a] = src[a];
         }
-        fcur = fnext;
-        fnext = fnn;
-        cur = nxt;
-        nxt = nn;
+        fcur = f1;
+        f1 = f2;
+        f2 = f3;
+        cur = n1;
+        n1 = n2;
+        n2 = n3;
     }
 }
 
