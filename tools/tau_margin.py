@@ -1,0 +1,19 @@
+import sys, os
+sys.path.insert(0, os.getcwd()); sys.path.insert(0, os.path.join(os.getcwd(), "tests"))
+import numpy as np
+import paper_2210_03523_b200 as dg
+import oracle as orc
+orc.build()
+from test_gpu_curved import setup
+from test_gpu_parity import tau_rel
+for name in ("cfg4_small", "cfg5_subbox", "cfg4_full"):
+    for ref in ("solver", "same"):
+        for form in (0, 1):
+            mesh, orders, P, S, q, qd = setup(dg, orc, name)
+            if ref == "solver":
+                tg = S.tau_estimate(qd, S.rhs_eval(qd), formulation=form, reference=dg.REF_SOLVER).cpu().numpy()
+                to = P.tau_estimate(orders, q, P.rhs(orders, q), form)
+            else:
+                tg = S.tau_estimate(qd, None, formulation=form, reference=dg.REF_SAME).cpu().numpy()
+                to = P.tau_estimate(orders, q, P.rhs(orders, q, orc.ISOLATED), form)
+            print(name, ref, form, "%.2e" % tau_rel(tg, to))
