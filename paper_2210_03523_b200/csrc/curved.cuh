@@ -828,11 +828,17 @@ struct CMortarParams {
 
 // Mortar metric Ja_d at the mortar nodes (L's geometry, reading A6), in
 // double-double, once per layout: mgeo[mgoff[face] + c*nm + t], c = 0..2.
-__global__ void __launch_bounds__(128) k_mortar_geom(CMortarParams P, double* mgeo, const long long* mgoff)
+__global__ void __launch_bounds__(128) k_mortar_geom(CMortarParams P, double* mgeo, const long long* mgoff, int nitems)
 {
-    __shared__ double Xm[3][NP * NP], Xml[3][NP * NP];
-    double* Jg = mgeo + mgoff[blockIdx.x];
-    const MortarItem it = P.items[blockIdx.x];
+    // one warp per mortar face (4 per CTA)
+    __shared__ double Xs[4][2][3][NP * NP];
+    const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int fid = blockIdx.x * 4 + wi;
+    if (fid >= nitems) return;
+    double (*Xm)[NP * NP] = Xs[wi][0];
+    double (*Xml)[NP * NP] = Xs[wi][1];
+    double* Jg = mgeo + mgoff[fid];
+    const MortarItem it = P.items[fid];
     const int d = it.d;
     const int ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
     int NL[3], NR[3];
@@ -845,7 +851,7 @@ __global__ void __launch_bounds__(128) k_mortar_geom(CMortarParams P, double* mg
     const double* G = P.cm.geo + (long long)it.L * 3 * P.cm.ng;
     const int ga = gd[0] + 1, gb = gd[1] + 1;
     const TablesDD* tdd = P.tdd;
-    for (int t = threadIdx.x; t < nm; t += blockDim.x) {
+    for (int t = lane; t < nm; t += 32) {
         const int m1 = t % (M1 + 1), m2 = t / (M1 + 1);
         dd x[3] = {mkdd(0.0), mkdd(0.0), mkdd(0.0)};
         for (int b = 0; b <= gd[tb]; ++b)
@@ -860,8 +866,8 @@ __global__ void __launch_bounds__(128) k_mortar_geom(CMortarParams P, double* mg
             }
         for (int c = 0; c < 3; ++c) { Xm[c][t] = x[c].hi; Xml[c][t] = x[c].lo; }
     }
-    __syncthreads();
-    for (int t = threadIdx.x; t < nm; t += blockDim.x) {
+    __syncwarp();
+    for (int t = lane; t < nm; t += 32) {
         const int m1 = t % (M1 + 1), m2 = t / (M1 + 1);
         dd u[3], v[3];
         for (int c = 0; c < 3; ++c) {

@@ -961,7 +961,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
             G.items = ctx->d_mortar;
             G.cm = curved_mesh(ctx);
             G.tab = ctx->d_tab;
-            k_mortar_geom<<<ctx->nmortar, 128>>>(G, ctx->d_mgeo, ctx->d_mgoff);
+            k_mortar_geom<<<(ctx->nmortar + 3) / 4, 128>>>(G, ctx->d_mgeo, ctx->d_mgoff, ctx->nmortar);
             ctx->launches++;
             CK(cudaGetLastError());
         }
