@@ -461,9 +461,32 @@ static void drop_graphs(dg_ctx* ctx)
     ctx->graphs.clear();
 }
 
+// Coarse-level contexts borrow the fine context's residual scratch (BR1
+// gradient, mortar / face flux buffers): the levels run one after another on
+// the caller's stream and every coarse layout needs no more than the fine one
+// (fewer nodes; mortars only where the fine layout has them, with smaller
+// blocks).  Detach before destroying a level so the scratch stays the parent's.
+static void lend_scratch(dg_ctx* parent, dg_ctx* sub)
+{
+    sub->d_grad = parent->d_grad;
+    sub->grad_len = parent->grad_len;
+    sub->d_mortarGq = parent->d_mortarGq;
+    sub->mq_len = parent->mq_len;
+    sub->d_mortarG = parent->d_mortarG;  // capacity known to dalloc's registry
+}
+
+static void unlend_scratch(dg_ctx* parent, dg_ctx* sub)
+{
+    if (!sub) return;
+    if (sub->d_grad == parent->d_grad) sub->d_grad = nullptr;
+    if (sub->d_mortarGq == parent->d_mortarGq) sub->d_mortarGq = nullptr;
+    if (sub->d_mortarG == parent->d_mortarG) sub->d_mortarG = nullptr;
+}
+
 static void drop_coarse(dg_ctx* ctx)
 {
     for (auto& L : ctx->coarse) {
+        unlend_scratch(ctx, L.sub);
         dg_destroy(L.sub);
         L.sub = nullptr;
         dfree(L.d_orders);
@@ -1647,6 +1670,7 @@ static dg_status build_level(dg_ctx* ctx, int d, int p, dg_ctx::CoarseLevel& L)
     }
     dg_status s = dg_create(&ctx->prm, &L.sub);
     if (s != DG_OK) return fail(ctx, s, "tau_estimate: coarse level context");
+    if (ctx->curved) lend_scratch(ctx, L.sub);
     if ((s = dg_mesh_upload(L.sub, E, ctx->nbr.data(), ctx->gorder, ctx->geo.data())) != DG_OK ||
         (s = dg_set_orders(L.sub, oc.data())) != DG_OK)
         return fail(ctx, s, std::string("tau_estimate: coarse level: ") + dg_last_error(L.sub));
@@ -1655,8 +1679,9 @@ static dg_status build_level(dg_ctx* ctx, int d, int p, dg_ctx::CoarseLevel& L)
     return DG_OK;
 }
 
-static void free_level(dg_ctx::CoarseLevel& L)
+static void free_level(dg_ctx* ctx, dg_ctx::CoarseLevel& L)
 {
+    unlend_scratch(ctx, L.sub);
     dg_destroy(L.sub);
     L.sub = nullptr;
     dfree(L.d_orders);
@@ -1751,7 +1776,7 @@ static dg_status tau_noniso(dg_ctx* ctx, int formulation, int restr, const doubl
             dg_status s = build_level(ctx, d, p, L);
             if (s == DG_OK) s = run_level(ctx, L, formulation, restr, q_dev, ref, tau_dev, st);
             CK(cudaStreamSynchronize(st));  // the level's buffers are in use until here
-            free_level(L);
+            free_level(ctx, L);
             if (s != DG_OK) return s;
         }
     return DG_OK;
