@@ -522,6 +522,32 @@ def test_full_size_cfg3(dg, orc):
     assert rel_linf(qs.cpu().numpy(), qo, orders, floor=EULER_PULSE_SCALES) < RES_TOL
 
 
+def test_graph_repoint_bitwise(dg, orc, monkeypatch):
+    """Mixed-order residuals replay one graph per launch shape, re-pointed to
+    each new buffer pair / RK coefficients: identical bits to direct launches
+    (DGTAU_NO_GRAPHS=1) through RK steps on alternating buffers and residuals
+    into fresh outputs."""
+    import torch
+
+    mesh, orders, kw = CASES["cfg3_subbox_mixed"]()
+    P, Sg, q, qd = setup(dg, orc, mesh, orders, **kw)
+    monkeypatch.setenv("DGTAU_NO_GRAPHS", "1")
+    Sd = dg.Solver(mesh)
+    Sd.set_orders(orders)
+    outs = []
+    for S in (Sg, Sd):
+        dts = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in range(2)]
+        S.compute_dt(qd, 0.5, dts[0])
+        qa, qb, g = qd.clone(), torch.empty_like(qd), torch.empty_like(qd)
+        qs, dt = S.rk_steps(3, qa, qb, g, dts[0], dts[1], 0.5)
+        r1 = S.rhs_eval(qs)
+        r2 = S.rhs_eval(qd)
+        r3 = S.rhs_eval(qs, variant=1)
+        outs.append([x.cpu().numpy().copy() for x in (qs, dt, r1, r2, r3)])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+
+
 def test_error_paths(dg, orc):
     """The ABI refuses, with a status and a message (never a crash), what it
     does not support: non-isolated levels on a multi-rank local mesh, an
