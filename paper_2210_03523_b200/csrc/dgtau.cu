@@ -261,13 +261,15 @@ cudaError_t dalloc(T*& p, size_t count)
     }
     if (p) cudaFree(p);
     p = nullptr;
-    cudaError_t e = cudaMalloc(&p, bytes ? bytes : 1);
+    // 25 % slack: the tables of successive adapted layouts differ a little in size
+    const size_t cap = bytes + bytes / 4;
+    cudaError_t e = cudaMalloc(&p, cap ? cap : 1);
     if (e != cudaSuccess) {
         p = nullptr;
         return e;
     }
     std::lock_guard<std::mutex> lk(dcap_mu());
-    dcap()[p] = bytes;
+    dcap()[p] = cap;
     return cudaSuccess;
 }
 
@@ -911,11 +913,13 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
                     p = q + 1;
                 }
             }
-        std::vector<int> idx(tg.size());
-        for (size_t i = 0; i < idx.size(); ++i) idx[i] = (int)i;
-        std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return gsz[a] > gsz[b]; });
+        // largest first, stable: counting sort on the group size (O(groups))
+        std::vector<int> cnt(gmax + 2, 0);
+        for (int s : gsz) ++cnt[s];
+        std::vector<int> start(gmax + 2, 0);
+        for (int s = gmax - 1; s >= 0; --s) start[s] = start[s + 1] + cnt[s + 1];
         std::vector<TauGroup> sorted(tg.size());
-        for (size_t i = 0; i < idx.size(); ++i) sorted[i] = tg[idx[i]];
+        for (size_t i = 0; i < tg.size(); ++i) sorted[start[gsz[i]]++] = tg[i];
         ctx->ntgroups = (int)sorted.size();
         ctx->tau5_smem = sizeof(double) * 4 * NV * (size_t)gmax;
         CK(upload(ctx->d_tgroups, sorted));
