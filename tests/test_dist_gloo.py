@@ -262,3 +262,26 @@ def test_dof_owner_two_ranks_optimal():
         best = min(max(dof[layer < b].sum(), dof[layer >= b].sum()) for b in range(1, dims[2]))
         assert got == best
         assert np.all(np.diff(owner[np.argsort(layer, kind="stable")]) >= 0)  # contiguous slabs
+
+
+def test_dof_owner_properties():
+    """Any world size: contiguous layer slabs, every rank at least one layer,
+    and no rank above the ideal share by more than the largest layer."""
+    from paper_2210_03523_b200 import partition as part
+
+    rng = np.random.default_rng(11)
+    for trial in range(30):
+        dims = (int(rng.integers(1, 4)), int(rng.integers(1, 4)), int(rng.integers(4, 16)))
+        world = int(rng.integers(2, min(dims[2], 6) + 1))
+        E = dims[0] * dims[1] * dims[2]
+        orders = rng.integers(1, 9, size=(E, 3)).astype(np.int32)
+        owner = part.dof_owner(dims, orders, world)
+        layer = np.arange(E) // (dims[0] * dims[1])
+        per_layer = np.array([owner[layer == l][0] for l in range(dims[2])])
+        assert np.all(np.diff(per_layer) >= 0) and set(per_layer) == set(range(world))
+        for l in range(dims[2]):
+            assert np.all(owner[layer == l] == per_layer[l])
+        dof = np.prod(orders.astype(np.int64) + 1, axis=1)
+        ldof = np.bincount(layer, weights=dof)
+        share = np.array([dof[owner == r].sum() for r in range(world)])
+        assert share.max() <= dof.sum() / world + 2 * ldof.max()
