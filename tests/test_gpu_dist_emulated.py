@@ -191,3 +191,48 @@ def test_distsolver_single_rank_matches_solver(dg, orc):
     sel1, _ = S.select_orders(tau, 1e-4, 2, 8)
     sel2 = D.select_orders(tau, 1e-4, 2, 8)
     assert np.array_equal(sel1, sel2)
+
+
+def test_rebalance_single_rank_nccl(dg, orc):
+    """dist.rebalance end to end on a one-rank NCCL group (the all-to-all,
+    the DistSolver rebuild and the halo refresh run; with one rank every
+    element stays): the rebalanced solver's residual equals the plain
+    solver's, bit for bit."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2210_03523_b200 import partition as part
+    from paper_2210_03523_b200.dist import DistSolver, rebalance
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    created = not dist.is_initialized()
+    if created:
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    assert dist.get_world_size() == 1
+    grp = dist.new_group(ranks=[0], backend="nccl")
+    try:
+        mesh = W.cube_mesh(3, 3, 4)
+        o1 = W.orders_random(mesh.E, 2, 5, 3)
+        o2 = W.orders_random(mesh.E, 2, 7, 4)
+        P = orc.Problem(mesh)
+        ds = DistSolver(mesh, part.slab_owner(mesh.dims, 1), 0, 1, group=grp)
+        ds.set_orders(o1)
+        q2 = torch.from_numpy(W.pulse_state(P.node_coords(o2), o2, sigma=0.2)).cuda()
+        # the state is already at o2 (as after a transfer); o1's solver object is what rebalances
+        nd, q_new = rebalance(ds, o2, q2)
+        r_d = nd.rhs_eval(q_new)
+        S = dg.Solver(mesh)
+        S.set_orders(o2)
+        r_s = S.rhs_eval(q2)
+        assert torch.equal(q_new, q2)
+        assert torch.equal(r_d, r_s)
+    finally:
+        dist.destroy_process_group(grp)
+        if created:
+            dist.destroy_process_group()
