@@ -1059,11 +1059,13 @@ __global__ void __launch_bounds__(CM3_BS, NIN == 20 ? 2 : 3) k_mortar_c3(CMortar
                     for (int v = 0; v < NV; ++v) GM[v * 81 + tp] = F[v] * S;
                 }
             } else {
-                double gL[15], gR[15], fL[NV], fR[NV];
+                double gs[15], fL[NV], fR[NV];  // one side's gradient live at a time
 #pragma unroll
-                for (int c = 0; c < 15; ++c) { gL[c] = Y0[(NV + c) * 81 + tp]; gR[c] = Y1[(NV + c) * 81 + tp]; }
-                visc_dot(qL, gL, jf[0], jf[1], jf[2], P.ph, fL);
-                visc_dot(qR, gR, jf[0], jf[1], jf[2], P.ph, fR);
+                for (int c = 0; c < 15; ++c) gs[c] = Y0[(NV + c) * 81 + tp];
+                visc_dot(qL, gs, jf[0], jf[1], jf[2], P.ph, fL);
+#pragma unroll
+                for (int c = 0; c < 15; ++c) gs[c] = Y1[(NV + c) * 81 + tp];
+                visc_dot(qR, gs, jf[0], jf[1], jf[2], P.ph, fR);
 #pragma unroll
                 for (int v = 0; v < NV; ++v) GV[v * 81 + tp] = 0.5 * (fL[v] + fR[v]);
             }
