@@ -72,6 +72,62 @@ __device__ __forceinline__ void visc_dot(const double* q, const double* g /*[15]
     fv[4] = u * ta[0] + v * ta[1] + w * ta[2] + kappa * (dT[0] * ax + dT[1] * ay + dT[2] * az);
 }
 
+// visc_dot split in two: the node's stress tensor and temperature gradient
+// once (from q and its gradient), then the flux along any vector a with the
+// same operations in the same order (bit-identical to visc_dot)
+struct ViscNode {
+    double T[3][3];   // mu (du_i/dx_j + du_j/dx_i - 2/3 div delta_ij)
+    double dT[3];     // grad T
+    double u[3];
+    double kappa;
+};
+
+__device__ __forceinline__ void visc_node(const double* q, const double* g, const PhysDev& ph, ViscNode& V)
+{
+    const double gam = ph.gamma, mu = ph.mu;
+    const double ir = 1.0 / q[0];
+    const double u = q[1] * ir, v = q[2] * ir, w = q[3] * ir;
+    const double p = (gam - 1.0) * (q[4] - 0.5 * q[0] * (u * u + v * v + w * w));
+    const double Tt = p * ir;
+    double du[3][3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const double* gj = g + 5 * j;
+        du[0][j] = (gj[1] - u * gj[0]) * ir;
+        du[1][j] = (gj[2] - v * gj[0]) * ir;
+        du[2][j] = (gj[3] - w * gj[0]) * ir;
+        const double dp = (gam - 1.0) * (gj[4] - (u * gj[1] + v * gj[2] + w * gj[3]) + 0.5 * (u * u + v * v + w * w) * gj[0]);
+        V.dT[j] = (dp - Tt * gj[0]) * ir;
+    }
+    const double div = du[0][0] + du[1][1] + du[2][2];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) V.T[i][j] = mu * (du[i][j] + du[j][i] - (i == j ? 2.0 / 3.0 * div : 0.0));
+    V.u[0] = u;
+    V.u[1] = v;
+    V.u[2] = w;
+    V.kappa = mu * gam / ((gam - 1.0) * ph.Pr);
+}
+
+__device__ __forceinline__ void visc_along(const ViscNode& V, double ax, double ay, double az, double* fv)
+{
+    const double a[3] = {ax, ay, az};
+    double ta[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        double s = 0.0;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) s += V.T[i][j] * a[j];
+        ta[i] = s;
+    }
+    fv[0] = 0.0;
+    fv[1] = ta[0];
+    fv[2] = ta[1];
+    fv[3] = ta[2];
+    fv[4] = V.u[0] * ta[0] + V.u[1] * ta[1] + V.u[2] * ta[2] + V.kappa * (V.dT[0] * ax + V.dT[1] * ay + V.dT[2] * az);
+}
+
 // advective flux along vector a
 __device__ __forceinline__ void adv_dot(const double* q, double ax, double ay, double az, double gm1, double* f)
 {
@@ -603,15 +659,27 @@ __global__ void __launch_bounds__(CBS, 5) k_res_curved(CurvedParams P)
     __syncthreads();
     // volume fluxes of the three directions from one read of q, grad q, Ja
     for (int t = threadIdx.x; t < n; t += CBS) {
-        double qv[NV], gv[15];
+        double qv[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) qv[v] = Q[v * n + t];
-        if (ns) load_grad(GR + t, n, gv);
+        ViscNode V;
+        if (ns) {
+            double gv[15];
+            load_grad(GR + t, n, gv);
+            visc_node(qv, gv, P.ph, V);
+        }
 #pragma unroll
-        for (int d = 0; d < 3; ++d) {
+        for (int d = 0; d < 3; ++d) {  // = contra_flux: a . f^a - a . f^nu
+            const double ax = __ldg(M + (3 * d) * n + t), ay = __ldg(M + (3 * d + 1) * n + t),
+                         az = __ldg(M + (3 * d + 2) * n + t);
             double Fv[NV];
-            contra_flux(qv, gv, __ldg(M + (3 * d) * n + t), __ldg(M + (3 * d + 1) * n + t), __ldg(M + (3 * d + 2) * n + t),
-                        P.ph, Fv);
+            adv_dot(qv, ax, ay, az, P.ph.gm1, Fv);
+            if (ns) {
+                double fv[NV];
+                visc_along(V, ax, ay, az, fv);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) Fv[v] -= fv[v];
+            }
 #pragma unroll
             for (int v = 0; v < NV; ++v) F[(d * NV + v) * n + t] = Fv[v];
         }
