@@ -1299,28 +1299,58 @@ __global__ void __launch_bounds__(BS, BS == 256 ? 2 : (BS == 128 ? 5 : 10)) k_ta
         }
         __syncthreads();
     }
-    for (int dd = 0; dd < 3; ++dd) {
-        const int od = dd == 0 ? o1 : (dd == 1 ? o2 : o3);
-        const int str = dd == 0 ? 1 : (dd == 1 ? o1 : o1 * o2);
-        const double* Dd = Ds[dd];
+    if (ns) {  // fluxes of the three directions from one viscous evaluation per node, in place of GA
         for (int t = threadIdx.x; t < nO; t += BS) {
-            double qv[NV], gv[15], Fv[NV];
+            double qv[NV], gv[15];
             for (int v = 0; v < NV; ++v) qv[v] = Qc[v * nO + t];
-            if (ns)
-                for (int c = 0; c < 15; ++c) gv[c] = GA[c * nO + t];
-            contra_flux(qv, gv, Mc[(3 * dd) * nO + t], Mc[(3 * dd + 1) * nO + t], Mc[(3 * dd + 2) * nO + t], P.ph, Fv);
-            for (int v = 0; v < NV; ++v) F[v * nO + t] = Fv[v];
+            for (int cc = 0; cc < 15; ++cc) gv[cc] = GA[cc * nO + t];
+            ViscNode V;
+            visc_node(qv, gv, P.ph, V);
+            for (int dd = 0; dd < 3; ++dd) {  // = contra_flux
+                const double ax = Mc[(3 * dd) * nO + t], ay = Mc[(3 * dd + 1) * nO + t], az = Mc[(3 * dd + 2) * nO + t];
+                double Fv[NV], fv[NV];
+                adv_dot(qv, ax, ay, az, P.ph.gm1, Fv);
+                visc_along(V, ax, ay, az, fv);
+                for (int v = 0; v < NV; ++v) GA[(dd * NV + v) * nO + t] = Fv[v] - fv[v];
+            }
         }
         __syncthreads();
         for (int t = threadIdx.x; t < nO; t += BS) {
-            int ijk[3];
             const int pk = IJK[t];
-            ijk[0] = pk & 255; ijk[1] = (pk >> 8) & 255; ijk[2] = pk >> 16;
-            const int a = dd == 0 ? ijk[0] : (dd == 1 ? ijk[1] : ijk[2]);
-            const int base = t - a * str;
-            dsum_comps<NV>(od, Dd + a * od, F + base, nO, str, [&](int v, double sv) { A[v * nO + t] += sv; });
+            const int ijk[3] = {pk & 255, (pk >> 8) & 255, pk >> 16};
+            for (int dd = 0; dd < 3; ++dd) {
+                const int od = dd == 0 ? o1 : (dd == 1 ? o2 : o3);
+                const int str = dd == 0 ? 1 : (dd == 1 ? o1 : o1 * o2);
+                const int a = ijk[dd];
+                dsum_comps<NV>(od, Ds[dd] + a * od, GA + dd * NV * nO + (t - a * str), nO, str,
+                               [&](int v, double sv) { A[v * nO + t] += sv; });
+            }
         }
         __syncthreads();
+    } else {
+        for (int dd = 0; dd < 3; ++dd) {
+            const int od = dd == 0 ? o1 : (dd == 1 ? o2 : o3);
+            const int str = dd == 0 ? 1 : (dd == 1 ? o1 : o1 * o2);
+            const double* Dd = Ds[dd];
+            for (int t = threadIdx.x; t < nO; t += BS) {
+                double qv[NV], gv[15], Fv[NV];
+                for (int v = 0; v < NV; ++v) qv[v] = Qc[v * nO + t];
+                if (ns)
+                    for (int c = 0; c < 15; ++c) gv[c] = GA[c * nO + t];
+                contra_flux(qv, gv, Mc[(3 * dd) * nO + t], Mc[(3 * dd + 1) * nO + t], Mc[(3 * dd + 2) * nO + t], P.ph, Fv);
+                for (int v = 0; v < NV; ++v) F[v * nO + t] = Fv[v];
+            }
+            __syncthreads();
+            for (int t = threadIdx.x; t < nO; t += BS) {
+                int ijk[3];
+                const int pk = IJK[t];
+                ijk[0] = pk & 255; ijk[1] = (pk >> 8) & 255; ijk[2] = pk >> 16;
+                const int a = dd == 0 ? ijk[0] : (dd == 1 ? ijk[1] : ijk[2]);
+                const int base = t - a * str;
+                dsum_comps<NV>(od, Dd + a * od, F + base, nO, str, [&](int v, double sv) { A[v * nO + t] += sv; });
+            }
+            __syncthreads();
+        }
     }
     double tmax = 0.0;
     for (int t = threadIdx.x; t < nO; t += BS) {
