@@ -1269,32 +1269,36 @@ __global__ void __launch_bounds__(BS, BS == 256 ? 2 : (BS == 128 ? 5 : 10)) k_ta
             for (int v = 0; v < NV; ++v) A[v * nO + t] = 0.0;
     }
     __syncthreads();
-    if (ns) {  // isolated gradient: J g_k = sum_d' D^{d'} (Ja^{d'}_k q), all k per direction
-        for (int dd = 0; dd < 3; ++dd) {
-            const int od = dd == 0 ? o1 : (dd == 1 ? o2 : o3);
-            const int str = dd == 0 ? 1 : (dd == 1 ? o1 : o1 * o2);
-            const double* Dd = Ds[dd];
-            for (int t = threadIdx.x; t < nO; t += BS)
-                for (int k = 0; k < 3; ++k) {
-                    const double jak = Mc[(3 * dd + k) * nO + t];
-                    for (int v = 0; v < NV; ++v) F[(k * NV + v) * nO + t] = jak * Qc[v * nO + t];
-                }
-            __syncthreads();
-            for (int t = threadIdx.x; t < nO; t += BS) {
-                int ijk[3];
-                const int pk = IJK[t];
-                ijk[0] = pk & 255; ijk[1] = (pk >> 8) & 255; ijk[2] = pk >> 16;
-                const int a = dd == 0 ? ijk[0] : (dd == 1 ? ijk[1] : ijk[2]);
-                const int base = t - a * str;
-                dsum_comps<15>(od, Dd + a * od, F + base, nO, str, [&](int c, double sv) {
-                    GA[c * nO + t] = dd == 0 ? sv : GA[c * nO + t] + sv;
-                });
-            }
-            __syncthreads();
-        }
+    if (ns) {  // isolated gradient: J g_k = sum_d' D^{d'} (Ja^{d'}_k q), one thread per node in registers
         for (int t = threadIdx.x; t < nO; t += BS) {
+            const int pk = IJK[t];
+            const int ijk[3] = {pk & 255, (pk >> 8) & 255, pk >> 16};
+            double g[15];
+#pragma unroll
+            for (int cc = 0; cc < 15; ++cc) g[cc] = 0.0;
+            for (int dd = 0; dd < 3; ++dd) {
+                const int od = dd == 0 ? o1 : (dd == 1 ? o2 : o3);
+                const int str = dd == 0 ? 1 : (dd == 1 ? o1 : o1 * o2);
+                const int a = ijk[dd];
+                const int base = t - a * str;
+                const double* Dr = Ds[dd] + a * od;
+                for (int m = 0; m < od; ++m) {
+                    const int nm = base + m * str;
+                    const double dm = Dr[m];
+                    double qv[NV];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) qv[v] = Qc[v * nO + nm];
+#pragma unroll
+                    for (int kk = 0; kk < 3; ++kk) {
+                        const double jk = Mc[(3 * dd + kk) * nO + nm];
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) g[kk * NV + v] = fma(dm, jk * qv[v], g[kk * NV + v]);
+                    }
+                }
+            }
             const double iJ = 1.0 / Mc[9 * nO + t];
-            for (int c = 0; c < 15; ++c) GA[c * nO + t] *= iJ;
+#pragma unroll
+            for (int cc = 0; cc < 15; ++cc) GA[cc * nO + t] = g[cc] * iJ;
             for (int v = 0; v < NV; ++v) A[v * nO + t] = 0.0;
         }
         __syncthreads();
