@@ -1234,17 +1234,17 @@ __global__ void __launch_bounds__(BS, BS == 256 ? 2 : (BS == 128 ? 5 : 10)) k_ta
     double* Qc = Mc + 10 * nO;               // 5 nO
     double* Rc = Qc + NV * nO;               // 5 nO
     double* GA = Rc + NV * nO;               // 15 nO (NS)
-    double* F = ns ? GA + 15 * nO : GA;      // 5 nO (NS gradient: 15 nO over F, A and 5 more)
-    double* A = F + NV * nO;                 // 5 nO
+    double* F = ns ? GA + 15 * nO : GA;      // 5 nO (NS: only the metric scratch, shared with A)
+    double* A = ns ? F : F + NV * nO;        // 5 nO
     // (i, j, k) of every coarse node, packed i | j << 8 | k << 16, computed once
-    int* IJK = reinterpret_cast<int*>(sm + (ns ? 50 : 30) * nO);
+    int* IJK = reinterpret_cast<int*>(sm + (ns ? 40 : 30) * nO);
     for (int t = threadIdx.x; t < nO; t += BS) {
         int ii, jj, kk;
         node_ijk(t, o1, o2, ii, jj, kk);
         IJK[t] = ii | (jj << 8) | (kk << 16);
     }
     __syncthreads();
-    element_metrics_fp64(P.cm, e, o1, o2, o3, P.tab, Ds, IJK, F, Mc);  // F, A: 10 nO >= 3 nO scratch (barriers inside)
+    element_metrics_fp64(P.cm, e, o1, o2, o3, P.tab, Ds, IJK, F, Mc);  // F: >= 5 nO >= 3 nO scratch (barriers inside)
     const long long o = P.off[e];
     const double* T = P.restr ? P.tab->P[nd - 1][p] : P.tab->T[nd - 1][p];
     for (int t = threadIdx.x; t < nO; t += BS) {

@@ -1826,7 +1826,7 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
         ctx->launches++;
         if (o->coarse_faces) return tau_noniso(ctx, o->formulation, o->restriction, q_dev, ref, tau_dev, st);
         if (ctx->curved && ctx->nlevels > 0) {
-            const size_t sm = sizeof(double) * ((ctx->prm.physics == DG_NS ? 50 : 30) * (size_t)ctx->max_level + (ctx->max_level + 1) / 2);
+            const size_t sm = sizeof(double) * ((ctx->prm.physics == DG_NS ? 40 : 30) * (size_t)ctx->max_level + (ctx->max_level + 1) / 2);
             if ((long long)sm > ctx->smem_limit) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: coarse level too large for shared memory");
             CTauParams C;
             C.tdd = ctx->d_tdd;
@@ -1843,7 +1843,7 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
             C.ph = phys_dev(ctx->prm);
             for (const SizeClass& c : ctx->lcls) {
                 C.lbase = c.base;
-                const size_t smc = sizeof(double) * ((ctx->prm.physics == DG_NS ? 50 : 30) * (size_t)c.maxn + (c.maxn + 1) / 2);
+                const size_t smc = sizeof(double) * ((ctx->prm.physics == DG_NS ? 40 : 30) * (size_t)c.maxn + (c.maxn + 1) / 2);
                 if (c.maxn <= 64) k_tau_curved<64><<<c.count, 64, smc, st>>>(C);
                 else if (c.maxn <= 160) k_tau_curved<128><<<c.count, 128, smc, st>>>(C);
                 else k_tau_curved<256><<<c.count, 256, smc, st>>>(C);
