@@ -56,11 +56,18 @@ class _Mesh(C.Structure):
 _lib = None
 
 
+def load(path: str):
+    """ctypes handle of an oracle library at ``path`` (the built one by
+    default; tests load mutated copies to show that the pins catch them)."""
+    h = C.CDLL(path)
+    h.orc_compute_dt.restype = C.c_double
+    return h
+
+
 def lib():
     global _lib
     if _lib is None:
-        _lib = C.CDLL(build())
-        _lib.orc_compute_dt.restype = C.c_double
+        _lib = load(build())
     return _lib
 
 
@@ -84,13 +91,17 @@ def phys(physics=EULER, flux=ROE, gamma=1.4, mu=0.0, Pr=0.72, qinf=None):
 class Problem:
     """Holds the mesh arrays alive for the C side."""
 
-    def __init__(self, mesh, ph=None):
+    def __init__(self, mesh, ph=None, handle=None):
         self.nbr = np.ascontiguousarray(mesh.nbr, np.int32)
         self.gorder = np.ascontiguousarray(mesh.gorder, np.int32)
         self.geo = np.ascontiguousarray(mesh.geo, np.float64)
         self.E = int(self.nbr.shape[0])
         self.m = _Mesh(self.E, _p(self.nbr).value, _p(self.gorder).value, _p(self.geo).value)
         self.ph = ph if ph is not None else phys()
+        self._h = handle
+
+    def L(self):
+        return self._h if self._h is not None else lib()
 
     # -- helpers -------------------------------------------------------
     @staticmethod
@@ -105,20 +116,20 @@ class Problem:
     def node_coords(self, orders):
         o = self._ord(orders)
         X = np.empty(self.size(o, 3))
-        lib().orc_node_coords(C.byref(self.m), _p(o), _p(X))
+        self.L().orc_node_coords(C.byref(self.m), _p(o), _p(X))
         return X
 
     def mass(self, orders):
         o = self._ord(orders)
         M = np.empty(self.size(o, 1))
-        lib().orc_mass(C.byref(self.m), _p(o), _p(M))
+        self.L().orc_mass(C.byref(self.m), _p(o), _p(M))
         return M
 
     def rhs(self, orders, q, variant=NONISOLATED):
         o = self._ord(orders)
         q = np.ascontiguousarray(q, np.float64)
         out = np.empty_like(q)
-        rc = lib().orc_rhs(C.byref(self.m), _p(o), _p(q), int(variant), C.byref(self.ph), _p(out))
+        rc = self.L().orc_rhs(C.byref(self.m), _p(o), _p(q), int(variant), C.byref(self.ph), _p(out))
         if rc:
             raise ValueError("orc_rhs failed")
         return out
@@ -127,19 +138,19 @@ class Problem:
         o = self._ord(orders)
         q = np.ascontiguousarray(q, np.float64)
         out = np.empty(self.size(o, 15))
-        lib().orc_gradient(C.byref(self.m), _p(o), _p(q), int(variant), C.byref(self.ph), _p(out))
+        self.L().orc_gradient(C.byref(self.m), _p(o), _p(q), int(variant), C.byref(self.ph), _p(out))
         return out
 
     def dt(self, orders, q, cfl, dfl=None):
         o = self._ord(orders)
         q = np.ascontiguousarray(q, np.float64)
-        return lib().orc_compute_dt(C.byref(self.m), _p(o), _p(q), C.byref(self.ph), C.c_double(cfl),
+        return self.L().orc_compute_dt(C.byref(self.m), _p(o), _p(q), C.byref(self.ph), C.c_double(cfl),
                                     C.c_double(cfl if dfl is None else dfl))
 
     def rk3_step(self, orders, q, dt):
         o = self._ord(orders)
         q = np.array(q, np.float64, copy=True)
-        rc = lib().orc_rk3_step(C.byref(self.m), _p(o), _p(q), C.c_double(dt), C.byref(self.ph))
+        rc = self.L().orc_rk3_step(C.byref(self.m), _p(o), _p(q), C.c_double(dt), C.byref(self.ph))
         if rc:
             raise ValueError("orc_rk3_step failed")
         return q
@@ -150,7 +161,7 @@ class Problem:
         q = np.ascontiguousarray(q, np.float64)
         r = np.ascontiguousarray(qdot_ref, np.float64)
         tau = np.empty((self.E, 3, TAU_STRIDE))
-        lib().orc_tau_estimate_r(C.byref(self.m), _p(o), _p(q), _p(r), int(formulation), int(restriction),
+        self.L().orc_tau_estimate_r(C.byref(self.m), _p(o), _p(q), _p(r), int(formulation), int(restriction),
                                  C.byref(self.ph), _p(tau))
         return tau
 
@@ -203,7 +214,7 @@ class Problem:
         q = np.ascontiguousarray(q, np.float64)
         r = np.ascontiguousarray(qdot_ref, np.float64)
         out = np.empty(5 * 17 ** 3)
-        nc = lib().orc_tau_field(C.byref(self.m), _p(o), _p(q), _p(r), int(e), int(d), int(p), int(formulation),
+        nc = self.L().orc_tau_field(C.byref(self.m), _p(o), _p(q), _p(r), int(e), int(d), int(p), int(formulation),
                                  C.byref(self.ph), _p(out))
         return out[: 5 * nc].reshape(5, nc)
 
@@ -302,9 +313,9 @@ def select_from_map(mp, Nmin, Nmax, tau_max):
     return out, mg
 
 
-def decrease_cap(cur, sel, cap=1):
+def decrease_cap(cur, sel, cap=1, handle=None):
     cur = np.ascontiguousarray(cur, np.int32); sel = np.array(sel, np.int32, copy=True)
-    lib().orc_decrease_cap(cur.shape[0], _p(cur), int(cap), _p(sel))
+    (handle or lib()).orc_decrease_cap(cur.shape[0], _p(cur), int(cap), _p(sel))
     return sel
 
 

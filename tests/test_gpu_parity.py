@@ -148,7 +148,10 @@ def test_rk3_cfg1_trajectory(dg, orc):
     for step in range(10):
         dto = P.dt(orders, qo, 0.5)
         dtg = S.compute_dt(qa, 0.5, sync=True)
-        assert abs(dtg - dto) <= 1e-14 * dto  # a few ulp (different reduction order)
+        # a few ulp: the MAX over nodes is order-independent, but each node's CFL
+        # rate differs in its last bits (FMA contraction, Newton-refined MUFU
+        # reciprocal / sqrt on the device vs IEEE division / sqrt in the oracle)
+        assert abs(dtg - dto) <= 1e-14 * dto
         S.rk_step(qa, qb, g, S._dt)
         qa, qb = qb, qa
         qo = P.rk3_step(orders, qo, dto)
