@@ -1,25 +1,37 @@
 #!/usr/bin/env python
-"""Benchmark of the B200 hot path on BASELINE.json configs[1] (cfg2):
+"""Benchmark of the B200 hot path on BASELINE.json's largest single-GPU
+configuration, configs[4] (cfg5, B:11):
 
-  Euler density pulse, fp64, periodic cube 16^3 elements, fine N=(6,6,6),
-  pulse centre seeded in [0.3,0.7]^3, width 0.08; dynamic p-adaptation with
-  tau_estimate every 50 RK steps, tolerance 1e-4.
+  Compressible Navier-Stokes (Re 100, Ma 0.2, Pr 0.72), fp64, analytic
+  O-grid around a unit cylinder refined to 96 radial x 256 azimuthal x 16 z
+  curved elements (42.5 M DOF), seeded anisotropic orders N_x, N_y ~ U{2..8},
+  N_z = 2 (reading A21), free stream + seeded 1e-3 velocity noise.
 
-One bench STEP = one estimation interval of that run = every row of the hot
-path once over the cfg2 layout:
-  50 x (CFL dt on device + one Williamson RK3 step = 3 fused residual/RK-stage
-  launches)  ->  reference residual (SOLVER, non-isolated)  ->  batched
-  tau-estimation over all coarse orders  ->  dynamic order selection with the
-  jump fixpoint  ->  projection of the state onto the selected orders.
-The layout is kept at N=6 across steps so that every step does identical
-work (the projected state is the step's adaptation output).
+One bench STEP = one measurement interval of SURVEY 8(d) row 5 = every row of
+the hot path once over the cfg5 layout:
+  20 x Williamson RK3 step (3 fused NS residual / RK-stage passes each: BR1
+  gradient, face fluxes with mortars, volume + lifting + RK update + CFL/DFL
+  rates; the step size is formed on the device)  ->  SOLVER reference
+  residual (non-isolated)  ->  batched tau-estimation over all coarse orders
+  of every element and direction  ->  order selection (map, extrapolation,
+  minimum-NDOF search, decrease cap, jump fixpoint; reported, not applied:
+  reading A17 -- cfg5 is an estimate-and-select configuration).
+The state evolves from step to step (20 more RK steps each).
 
 metric: DGSEM residual GDOF/s (fp64), whole job: NDOF x residual evaluations
-in the step (151) / step time, all ranks.  Also reported: tau-estimation
-elements/s and the residual-kernel roofline.
+in the step (61) / step time, all ranks.  tau-estimation elements/s and the
+rooflines (fp64 arithmetic and HBM) of the RK stage are reported beside it.
+
+--workload cfg2 runs the secondary line: BASELINE configs[1] (Euler pulse,
+16^3, N=6) as the dynamic p-adaptation run it describes -- one step = one
+estimation interval (50 RK steps, tau, dynamic selection, transfer) and the
+adapted orders are APPLIED (dg_set_orders) before the next step.
+
+N > 1 (torchrun): cfg5 strong scaling, azimuthal slabs.
 """
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -34,27 +46,23 @@ import numpy as np  # noqa: E402
 import workloads as W  # noqa: E402
 
 METRIC = "DGSEM residual GDOF/s (fp64) + tau-estimation elems/s"
-RK_PER_STEP = 50
 CFL = 0.5
-TAU_MAX = 1e-4
-NMIN, NMAX = 3, 8
+CFG5_RK = 20             # RK3 steps per measurement
+CFG5_TAU_MAX = 1.0       # tau~_max for the reported selection (within [1e-1, 1e2])
+CFG5_NMIN, CFG5_NMAX = 1, 8   # reading A17: cfg5 estimate-and-select, [1, 8]
+CFG2_RK, CFG2_TAU_MAX, CFG2_NMIN, CFG2_NMAX = 50, 1e-4, 3, 8
 
 
-def load_traffic():
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
-    kernel from the committed ncu --set full capture (profiles/), or None."""
-    p = os.path.join(ROOT, "profiles", "traffic_k_res_t.json")
-    if os.path.exists(p):
-        return json.load(open(p)).get("dram_bytes_per_launch")
-    return None
-
+# ----------------------------------------------------------------------------
+# peaks
+# ----------------------------------------------------------------------------
 
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return d.get("hbm_gbs", 6650.0), "measured"
-    return 6650.0, "fallback"
+        return d.get("hbm_gbs", 6650.0), "measured (MEASURED_PEAKS.json, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
 
 
 def load_fp64_peak():
@@ -69,26 +77,104 @@ def load_fp64_peak():
     return (best, "measured DFMA (profiles/r01_fp64_peak.json)") if best else (37.2, "nominal 148 SM x 64 FMA x 2 x 1.965 GHz")
 
 
-def flops_model(N):
-    """Algorithmic fp64 flops (FMA = 2) of the method steps of SURVEY 8(c).1 on
-    affine hexes with isotropic order N (counted from the definitions, not
-    from kernel code):
-      residual per DOF: primitives + the three axis fluxes (33); D^N along each
-      line of each axis for 5 variables, even-odd form L^2/2 multiply-adds per
-      line plus 2 L adds (15 (L + 2) per node); strong-form lifting at the two
-      line ends (3 flops per end); Roe flux per face point (130) times face
-      points per DOF (3 L^2 / L^3); per-node combination and RK update (50).
-      tau per element: for every level (d, p < N): per coarse node the
-      interpolation of q and R along d (2 x 5 x 2 L), the three fluxes (33),
-      the three axis derivatives (15 (L_d' + 2)) and the combination (30)."""
-    L = N + 1
-    per_dof = 33 + 15 * (L + 2) + 30.0 / L + 130.0 * 3 / L + 50
-    tau = 0.0
-    for p in range(1, N):
-        nodes = (p + 1) * L * L
-        tau += 3 * nodes * (20 * L + 33 + 5 * ((p + 1 + 2) + 2 * (L + 2)) + 30)
-    return per_dof, tau
+def load_traffic(workload):
+    """dram__bytes_read.sum + dram__bytes_write.sum per RK stage (the kernels
+    of one stage summed) from the committed ncu --set full capture, or None."""
+    p = os.path.join(ROOT, "profiles", f"traffic_{workload}_stage.json")
+    if os.path.exists(p):
+        return json.load(open(p)).get("dram_bytes_per_stage")
+    return None
 
+
+# ----------------------------------------------------------------------------
+# algorithmic models (written from SURVEY 8(c).1 / the method steps, not from
+# kernel code; FMA = 2 flops)
+# ----------------------------------------------------------------------------
+
+def interior_faces(mesh, orders):
+    """(d, tangential orders of L, of R) of every interior face (L = the -xi_d
+    side: face +d of L)."""
+    nbr = np.asarray(mesh.nbr)
+    out = []
+    TA, TB = (1, 0, 0), (2, 2, 1)
+    for d in range(3):
+        L = np.flatnonzero(nbr[:, 2 * d + 1] >= 0)
+        R = nbr[L, 2 * d + 1]
+        out.append((d, orders[L][:, [TA[d], TB[d]]], orders[R][:, [TA[d], TB[d]]]))
+    return out
+
+
+def flops_residual(mesh, orders, ns=True):
+    """fp64 flops of one non-isolated residual:
+      per node: primitives (12); NS: products (Ja^d)_k q (45), the BR1 volume
+      sums D^d along each line for 15 components (30 n_d per direction), 1/J
+      (15), viscous stress and temperature gradient from the conserved
+      gradients (110); contravariant fluxes Ja^d . (f^a - f^nu) of the three
+      directions (3 x 55; Euler 3 x 25); the volume divergence (10 n_d per
+      direction); 1/J and the RK update (35); CFL/DFL rates (40).
+      per face point (each interior / boundary face once): Roe (150) + two
+      viscous fluxes along the face metric (2 x 138) + BR1 qhat Ja (30) and
+      the two sides' liftings (2 x 20 + 2 x 45).
+      per mortar face: interpolation of 5 (BR1) + 20 (flux) components of
+      both sides to the mortar grid and projection of 15 + 5 components back,
+      by 1-D passes only along the tangential directions whose orders differ."""
+    o = np.asarray(orders, np.int64) + 1
+    n = o.prod(1)
+    per_node = 12 + (45 + 15 + 110 + 3 * 55 if ns else 3 * 25) + 35 + 40
+    lines = (30 if ns else 0) + 10
+    vol = float((n * (per_node + lines * o.sum(1))).sum())
+    face = 0.0
+    pt_cost = (150 + 2 * 138 + 30 + 2 * 20 + 2 * 45) if ns else (150 + 2 * 20)
+    for d, tl, tr in interior_faces(mesh, np.asarray(orders)):
+        sl, sr = tl + 1, tr + 1
+        m = np.maximum(sl, sr)
+        face += float((m.prod(1) * pt_cost).sum())
+        for side in (sl, sr):
+            ncin = (5 + 20) if ns else 5
+            ncout = (15 + 5) if ns else 5
+            a_diff = side[:, 0] < m[:, 0]
+            b_diff = side[:, 1] < m[:, 1]
+            # pass along a on s_b rows, then along b on m_a columns (and back)
+            pa = np.where(a_diff, 2 * m[:, 0] * side[:, 0] * side[:, 1], 0)
+            pb = np.where(b_diff, 2 * m[:, 0] * m[:, 1] * side[:, 1], 0)
+            face += float(((ncin + ncout) * (pa + pb)).sum())
+    nb = np.asarray(mesh.nbr)
+    bnd = 0.0
+    for d in range(3):
+        for s in range(2):
+            e = np.flatnonzero(nb[:, 2 * d + s] < 0)
+            bnd += float((n[e] // o[e, d] * pt_cost).sum())
+    return vol + face + bnd
+
+
+def flops_tau(orders, ns=True):
+    """fp64 flops of one isolated tau-estimate: per
+    level (e, d, p < N_d) and coarse node: interpolation of q and R along d
+    (2 x 5 x 2 L_d), coarse geometry and metrics (3 x 2 x 6 interpolation +
+    3 x 3 x 2 L derivative terms + 30 cross products), the isolated residual
+    at the coarse orders (the per-node and per-line counts of
+    flops_residual, no face terms) and the max (10)."""
+    o = np.asarray(orders, np.int64) + 1
+    per_node = 12 + (45 + 15 + 110 + 3 * 55 if ns else 3 * 25) + 5
+    lines = (30 if ns else 0) + 10
+    tot = 0.0
+    for d in range(3):
+        for p in range(1, 9):
+            sel = (o[:, d] - 1) > p  # levels p < N_d
+            if not sel.any():
+                continue
+            oc = o[sel].copy()
+            Ld = oc[:, d].copy()
+            oc[:, d] = p + 1
+            nc = oc.prod(1)
+            per = 20 * Ld + 36 + 18 * oc.sum(1) + 30 + per_node + lines * oc.sum(1) + 10
+            tot += float((nc * per).sum())
+    return tot
+
+
+# ----------------------------------------------------------------------------
+# clocks
+# ----------------------------------------------------------------------------
 
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
@@ -135,16 +221,204 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cfg2_inputs(S):
-    X = S.node_coords()
-    return W.pulse_state(X, S.orders, center=W.cfg2_center(), sigma=0.08)
+# ----------------------------------------------------------------------------
+# workloads
+# ----------------------------------------------------------------------------
+
+def cfg5_problem():
+    spec = W.CONFIGS["cfg5"]
+    mesh = W.make_mesh(spec["mesh"])
+    orders = W.make_orders(spec["orders"], mesh.E)
+    return mesh, orders, W.ns_params()
 
 
-def make_solver(dg, mesh, orders):
-    S = dg.Solver(mesh)
-    S.set_orders(orders)
-    return S
+def cfg5_sample(nth=8):
+    """The cfg5 recipe on a bounded sample for the CPU oracle: the same O-grid
+    construction, radial count, ratio, geometry order and order law with
+    nth azimuthal elements and one z layer (96 x nth x 1)."""
+    spec = W.CONFIGS["cfg5"]
+    _, nr, _, _, ratio, g = spec["mesh"]
+    mesh = W.ogrid_mesh(nr, nth, 1, ratio=ratio, g_eta=g)
+    orders = W.make_orders(spec["orders"], mesh.E)
+    return mesh, orders, W.ns_params()
 
+
+def ns_state(orders, nsp, seed=5):
+    return W.freestream_noise_state(orders, (1.0, 1.0, 0.0, 0.0, nsp["p_inf"]), noise=1e-3, seed=seed)
+
+
+class Cfg5Run:
+    """The cfg5 step on one GPU (Solver) or one rank of N (DistSolver, strong
+    scaling over azimuthal slabs)."""
+
+    def __init__(self, dg, rank, world, dev):
+        import torch
+
+        self.dg, self.world = dg, world
+        mesh, orders, nsp = cfg5_problem()
+        self.mesh, self.orders_g = mesh, orders
+        kw = dict(physics=dg.NS, mu=nsp["mu"], Pr=nsp["Pr"], qinf=nsp["qinf"])
+        if world == 1:
+            self.S = dg.Solver(mesh, **kw)
+            self.S.set_orders(orders)
+            self.core = self.S
+            self.E_loc = mesh.E
+            self.n_own = mesh.E
+            self.ndof_own = self.S.ndof
+            q0 = ns_state(orders, nsp)
+            self.owned_len = self.S.state_len
+        else:
+            from paper_2210_03523_b200 import partition as part
+            from paper_2210_03523_b200.dist import DistSolver
+
+            owner = part.slab_owner(mesh.dims, world, axis=1)  # azimuthal slabs (SURVEY 8(e))
+            self.D = DistSolver(mesh, owner, rank, world, **kw)
+            self.D.set_orders(orders)
+            self.core = self.D.S
+            self.E_loc = self.D.lm.E
+            self.n_own = self.D.n_own
+            lo = self.D.local_orders
+            self.ndof_own = int(np.prod(lo[: self.n_own].astype(np.int64) + 1, axis=1).sum())
+            q0_g = ns_state(orders, nsp)
+            offg = W.offsets(orders, 5)
+            q0 = np.concatenate([q0_g[offg[g]:offg[g + 1]] for g in self.D.lm.gids])
+            self.owned_len = self.D.owned_len()
+        self.ndof_global = W.ndof(orders)
+        self.q0_host = q0
+        self.qa = torch.from_numpy(q0).to(dev)
+        self.qb = torch.empty_like(self.qa)
+        self.g = torch.empty_like(self.qa)
+        self.ref = torch.empty_like(self.qa)
+        self.tau = torch.empty((self.E_loc, 3, 9), dtype=torch.float64, device=dev)
+        self.dts = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(2)]
+        if world == 1:
+            self.S.compute_dt(self.qa, CFL, self.dts[0])
+        else:
+            self.D.compute_dt(self.qa, CFL, self.dts[0])
+        self.dt0 = self.dts[0].clone()  # dt of the initial state (e2e steps restart from it)
+        self.residuals_per_step = 3 * CFG5_RK + 1
+        self.rk_steps_per_step = CFG5_RK
+
+    def step(self, timers=None, ev=None, stream=None, qin=None):
+        dg = self.dg
+        if qin is not None:
+            self.qa = qin
+        if timers is not None:
+            e0 = ev()
+            e0.record(stream)
+        if self.world == 1:
+            self.S.rk_steps(CFG5_RK, self.qa, self.qb, self.g, self.dts[0], self.dts[1], CFL)  # even: ends in qa
+        else:
+            for _ in range(CFG5_RK):
+                self.D.rk_step_dt(self.qa, self.qb, self.g, self.dts[0], CFL, self.dts[1])
+                self.qa, self.qb = self.qb, self.qa
+                self.dts.reverse()
+        if timers is not None:
+            e1 = ev()
+            e1.record(stream)
+        if self.world == 1:
+            self.S.rhs_eval(self.qa, self.ref)
+            self.S.tau_estimate(self.qa, self.ref, reference=dg.REF_SOLVER, tau=self.tau)
+        else:
+            self.D.rhs_eval(self.qa, self.ref)
+            self.D.tau_estimate(self.qa, self.ref, reference=dg.REF_SOLVER, tau=self.tau)
+        if timers is not None:
+            e2 = ev()
+            e2.record(stream)
+        if self.world == 1:
+            sel = self.S.select_orders(self.tau, CFG5_TAU_MAX, CFG5_NMIN, CFG5_NMAX, mode=dg.SELECT_DYNAMIC,
+                                       jump_rule=dg.JUMP_B, dec_cap=1)[0]
+        else:
+            sel = self.D.select_orders(self.tau, CFG5_TAU_MAX, CFG5_NMIN, CFG5_NMAX, rule=dg.JUMP_B, dec_cap=1)
+        if timers is not None:
+            e3 = ev()
+            e3.record(stream)
+            timers["rk"].append((e0, e1))
+            timers["tau"].append((e1, e2))
+            timers["adapt"].append((e2, e3))
+        return self.qa, sel
+
+
+class Cfg2Run:
+    """BASELINE configs[1] as a dynamic adaptation run, adaptations APPLIED."""
+
+    def __init__(self, dg, rank, world, dev):
+        import torch
+
+        if world != 1:
+            raise SystemExit("--workload cfg2 runs on one GPU (the multi-GPU line is cfg5)")
+        self.dg, self.world = dg, world
+        self.mesh = W.cube_mesh(16)
+        self.orders = W.orders_uniform(self.mesh.E, 6)
+        self.S = dg.Solver(self.mesh)
+        self.S.set_orders(self.orders)
+        self.core = self.S
+        self.E_loc = self.n_own = self.mesh.E
+        self.q0_host = W.pulse_state(self.S.node_coords(), self.orders, center=W.cfg2_center(), sigma=0.08)
+        cap = 5 * 9 ** 3 * self.mesh.E  # any adapted layout (orders <= 8)
+        self.buf = [torch.zeros(cap, dtype=torch.float64, device=dev) for _ in range(3)]
+        self.g = torch.zeros(cap, dtype=torch.float64, device=dev)
+        self.ref = torch.zeros(cap, dtype=torch.float64, device=dev)
+        n0 = self.S.state_len
+        self.buf[0][:n0].copy_(torch.from_numpy(self.q0_host))
+        self.cur = 0
+        self.tau = torch.empty((self.E_loc, 3, 9), dtype=torch.float64, device=dev)
+        self.dts = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(2)]
+        self.S.compute_dt(self._q(0), CFL, self.dts[0])
+        self.residuals_per_step = 3 * CFG2_RK + 1
+        self.rk_steps_per_step = CFG2_RK
+        self.ndof_steps = []
+        self.owned_len = n0
+
+    @property
+    def ndof_global(self):
+        return self.S.ndof
+
+    @property
+    def ndof_own(self):
+        return self.S.ndof
+
+    def _q(self, i):
+        return self.buf[(self.cur + i) % 3][: self.S.state_len]
+
+    def step(self, timers=None, ev=None, stream=None, qin=None):
+        dg, S = self.dg, self.S
+        if qin is not None:
+            self.buf[self.cur][: qin.numel()].copy_(qin)
+        n = S.state_len
+        self.ndof_steps.append(S.ndof)
+        qa, qb = self._q(0), self._q(1)
+        if timers is not None:
+            e0 = ev()
+            e0.record(stream)
+        S.rk_steps(CFG2_RK, qa, qb, self.g[:n], self.dts[0], self.dts[1], CFL)  # even: ends in qa
+        if timers is not None:
+            e1 = ev()
+            e1.record(stream)
+        S.rhs_eval(qa, self.ref[:n])
+        S.tau_estimate(qa, self.ref[:n], reference=dg.REF_SOLVER, tau=self.tau)
+        if timers is not None:
+            e2 = ev()
+            e2.record(stream)
+        sel = S.select_orders(self.tau, CFG2_TAU_MAX, CFG2_NMIN, CFG2_NMAX, mode=dg.SELECT_DYNAMIC,
+                              jump_rule=dg.JUMP_B, dec_cap=1)[0]
+        nxt = (self.cur + 2) % 3
+        qn = S.transfer(sel, qa, out=self.buf[nxt])
+        S.set_orders(sel)             # the adaptation is applied: next step runs the new layout
+        S.compute_dt(qn, CFL, self.dts[0])
+        self.cur = nxt
+        if timers is not None:
+            e3 = ev()
+            e3.record(stream)
+            timers["rk"].append((e0, e1))
+            timers["tau"].append((e1, e2))
+            timers["adapt"].append((e2, e3))
+        return qn, sel
+
+
+# ----------------------------------------------------------------------------
+# GPU arm
+# ----------------------------------------------------------------------------
 
 def run_gpu(args, rank, world):
     import torch
@@ -154,107 +428,14 @@ def run_gpu(args, rank, world):
     dg.build()
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
-    if world == 1:
-        mesh = W.cube_mesh(16)
-        orders = W.orders_uniform(mesh.E, 6)
-        S = make_solver(dg, mesh, orders)
-        ndof = S.ndof
-        n_elem = mesh.E
-        q0_host = cfg2_inputs(S)
-        E_loc = mesh.E
-        select = lambda tau: S.select_orders(tau, TAU_MAX, NMIN, NMAX, mode=dg.SELECT_DYNAMIC,  # noqa: E731
-                                             jump_rule=dg.JUMP_B, dec_cap=1)[0]
-        local = lambda sel: sel  # noqa: E731
-        rk = S.rk_step_dt
-        rhs = S.rhs_eval
-        owned_len = S.state_len
-        core = S
-    else:
-        # weak scaling: global periodic 16 x 16 x (16 N) cube, z-slabs of 16^3 elements per rank
-        from paper_2210_03523_b200 import partition as part
-        from paper_2210_03523_b200.dist import DistSolver
-
-        mesh = W.cube_mesh(16, 16, 16 * world, L=(1.0, 1.0, float(world)))
-        owner = part.slab_owner(mesh.dims, world, axis=2)
-        D = DistSolver(mesh, owner, rank, world)
-        orders_g = W.orders_uniform(mesh.E, 6)
-        D.set_orders(orders_g)
-        S = D.S
-        ndof = int(np.prod(orders_g[D.lm.gids[: D.n_own]].astype(np.int64) + 1, axis=1).sum())
-        n_elem = D.n_own
-        X = S.node_coords()
-        q0_host = W.pulse_state(X, D.local_orders, center=W.cfg2_center(), sigma=0.08, L=(1.0, 1.0, float(world)))
-        E_loc = D.lm.E
-        select = lambda tau: D.select_orders(tau, TAU_MAX, NMIN, NMAX, rule=dg.JUMP_B, dec_cap=1)  # noqa: E731
-        local = lambda sel: sel[D.lm.gids]  # noqa: E731
-        rk = D.rk_step_dt
-        rhs = D.rhs_eval
-        owned_len = D.owned_len()
-        core = S
-    q0 = torch.from_numpy(q0_host).to(dev)
-    qa = q0.clone()
-    qb = torch.empty_like(qa)
-    g = torch.empty_like(qa)
-    ref = torch.empty_like(qa)
-    tau = torch.empty((E_loc, 3, 9), dtype=torch.float64, device=dev)
-    qn_buf = torch.empty(5 * 9 ** 3 * E_loc, dtype=torch.float64, device=dev)  # adapted state, any orders <= 8
-    dts = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(2)]
-    if world == 1:
-        S.compute_dt(qa, CFL, dts[0])  # first step's dt; later ones come fused from the RK kernel
-    else:
-        D.compute_dt(qa, CFL, dts[0])
+    R = (Cfg5Run if args.workload == "cfg5" else Cfg2Run)(dg, rank, world, dev)
     stream = torch.cuda.current_stream()
-    cur = [0]
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-
-    def step(timers=None):
-        nonlocal qa, qb
-        if world == 1:  # the 50 RK3 steps in one call (dg_rk_steps: stage-to-stage face traces)
-            if timers:
-                e0, e1 = ev(), ev()
-                e0.record(stream)
-            S.rk_steps(RK_PER_STEP, qa, qb, g, dts[cur[0]], dts[1 - cur[0]], CFL)
-            if RK_PER_STEP % 2:
-                cur[0] = 1 - cur[0]
-                qa, qb = qb, qa
-            if timers:
-                e1.record(stream)
-                timers["rk"].append((e0, e1))
-        for _ in range(RK_PER_STEP if world > 1 else 0):
-            if timers:
-                e0, e1 = ev(), ev()
-                e0.record(stream)
-            rk(qa, qb, g, dts[cur[0]], CFL, dts[1 - cur[0]])
-            cur[0] = 1 - cur[0]
-            if timers:
-                e1.record(stream)
-                timers["rk"].append((e0, e1))
-            qa, qb = qb, qa
-        if timers:
-            e0, e1 = ev(), ev()
-            e0.record(stream)
-        rhs(qa, ref)
-        core.tau_estimate(qa, ref, reference=dg.REF_SOLVER, tau=tau)
-        if timers:
-            e1.record(stream)
-            timers["tau"].append((e0, e1))
-        if timers:
-            e2 = ev()
-            e2.record(stream)
-        sel = select(tau)
-        qn = core.transfer(local(sel), qa, out=qn_buf)
-        if timers:
-            e3 = ev()
-            e3.record(stream)
-            timers["adapt"].append((e2, e3))
-        return sel, qn
-
     for _ in range(args.warmup):
-        step()
+        R.step()
     torch.cuda.synchronize()
-    # timed region
     timers = {"rk": [], "tau": [], "adapt": []}
-    launches0 = core.launches
+    launches0 = R.core.launches
     clocks = ClockSampler(dev.index)
     if rank == 0:
         clocks.start()
@@ -266,152 +447,196 @@ def run_gpu(args, rank, world):
     torch.cuda.synchronize()
     start, end = ev(), ev()
     start.record(stream)
+    dof_res = 0
     for _ in range(args.steps):
-        sel, qn = step(timers)
+        dof_res += R.ndof_global * R.residuals_per_step
+        R.step(timers, ev, stream)
     end.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     clk = clocks.stop() if rank == 0 else None
-    launches = core.launches - launches0
+    launches = R.core.launches - launches0
     total_ms = start.elapsed_time(end)
     rk_ms = sum(a.elapsed_time(b) for a, b in timers["rk"])
     tau_ms = sum(a.elapsed_time(b) for a, b in timers["tau"])
     adapt_ms = sum(a.elapsed_time(b) for a, b in timers["adapt"])
     if world > 1:
-        t = torch.tensor([total_ms, rk_ms, tau_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([total_ms, rk_ms, tau_ms, adapt_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, rk_ms, tau_ms = t.tolist()
-    evals_per_step = 3 * RK_PER_STEP + 1
-    value = world * ndof * evals_per_step * args.steps / (total_ms * 1e-3) / 1e9
-    # roofline of the dominant kernel pair: one RK stage = k_face + k_res_t
-    # algorithmic bytes per DOF: stage 1 reads q, writes g and q' (A_1 = 0: g
-    # not read) = 120 B; stages 2-3 read q, g and write g, q' = 160 B.
-    bytes_rk_step = ndof * (120 + 160 + 160)
-    rk_count = RK_PER_STEP * args.steps
-    achieved = bytes_rk_step * rk_count / (rk_ms * 1e-3) / 1e9
-    peak, peak_kind = load_peaks()
-    tau_elems = n_elem * args.steps / (tau_ms * 1e-3)
+        total_ms, rk_ms, tau_ms, adapt_ms = t.tolist()
+    value = dof_res / (total_ms * 1e-3) / 1e9
+    n_elem = R.mesh.E
+    res = dict(value=value, total_ms=total_ms, rk_ms=rk_ms, tau_ms=tau_ms, adapt_ms=adapt_ms, clocks=clk,
+               launches=launches, E=n_elem, ndof=R.ndof_global, runner=R)
+    res["rk_stages"] = 3 * R.rk_steps_per_step * args.steps
+    res["tau_elems"] = n_elem * args.steps / (tau_ms * 1e-3)
+    res["e2e"] = None if args.no_e2e else run_e2e(R, args, stream, ev, world)
+    return res
 
-    # end-to-end through the public API with host buffers: H2D of the step's
-    # input state from pinned memory, the step, D2H of the adapted state + orders
-    e2e = None
-    if not args.no_e2e:
-        # Each step: H2D of the step's input state from pinned memory, the step,
-        # D2H of its adapted state (+ the orders, already on the host).  The
-        # copies run on a copy stream, double-buffered, overlapping the
-        # neighbouring steps' compute; every byte still crosses PCIe each step.
-        pinned = torch.from_numpy(q0_host[:owned_len]).pin_memory()
-        out_pinned = [torch.empty(qn_buf.numel(), dtype=torch.float64).pin_memory() for _ in range(2)]
-        bufs = [torch.empty_like(qa) for _ in range(2)]
-        qn_bufs = [qn_buf, torch.empty_like(qn_buf)]
-        cs = torch.cuda.Stream()
-        ev_in = [torch.cuda.Event() for _ in range(args.steps + 1)]
-        ev_step = [torch.cuda.Event() for _ in range(args.steps)]
-        ev_out = [torch.cuda.Event() for _ in range(args.steps)]
-        torch.cuda.synchronize()
-        e0, e1 = ev(), ev()
-        e0.record(stream)
-        cs.wait_stream(stream)
-        with torch.cuda.stream(cs):
-            bufs[0][:owned_len].copy_(pinned, non_blocking=True)
-        ev_in[0].record(cs)
-        d2h = 0
-        for k in range(args.steps):
-            if k + 1 < args.steps:  # input of step k+1 while step k runs
-                if k >= 1:
-                    cs.wait_event(ev_step[k - 1])
-                with torch.cuda.stream(cs):
-                    bufs[(k + 1) % 2][:owned_len].copy_(pinned, non_blocking=True)
-                ev_in[k + 1].record(cs)
-            stream.wait_event(ev_in[k])
-            if k >= 2:
-                stream.wait_event(ev_out[k - 2])  # qn_bufs[k % 2] drained to the host
-            qa = bufs[k % 2]
-            qn_buf = qn_bufs[k % 2]
-            sel, qn = step()
-            ev_step[k].record(stream)
-            cs.wait_event(ev_step[k])
+
+def run_e2e(R, args, stream, ev, world):
+    """The same steps end to end through the public API with host buffers:
+    every step, H2D of the step's input state from pinned memory and D2H of
+    its result (state + selected orders).  Copies run on a copy stream,
+    double-buffered, overlapping the neighbouring steps; every byte still
+    crosses PCIe every step, inside the timed region."""
+    import torch
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    owned = R.owned_len
+    pinned = torch.from_numpy(np.ascontiguousarray(R.q0_host[:owned])).pin_memory()
+    total_len = R.qa.numel() if hasattr(R, "qa") else R.buf[0].numel()
+    out_pinned = [torch.empty(total_len, dtype=torch.float64).pin_memory() for _ in range(2)]
+    bufs = [torch.zeros(total_len, dtype=torch.float64, device=stream.device) for _ in range(2)]
+    if isinstance(R, Cfg2Run):
+        bufs = [torch.zeros(R.S.state_len, dtype=torch.float64, device=stream.device) for _ in range(2)]
+        pinned = torch.from_numpy(R.q0_host).pin_memory()
+        owned = R.q0_host.size
+        R.S.set_orders(R.orders)
+        R.S.compute_dt(R.buf[R.cur][: R.S.state_len], CFL, R.dts[0])
+    cs = torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(args.steps + 1)]
+    ev_step = [torch.cuda.Event() for _ in range(args.steps)]
+    ev_out = [torch.cuda.Event() for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0, e1 = ev(), ev()
+    e0.record(stream)
+    cs.wait_stream(stream)
+    with torch.cuda.stream(cs):
+        bufs[0][:owned].copy_(pinned, non_blocking=True)
+    ev_in[0].record(cs)
+    d2h = 0
+    dof_res = 0
+    for k in range(args.steps):
+        if isinstance(R, Cfg2Run):  # each interval restarts from the uploaded IC at N=6 (same work as the GPU arm's first step)
+            R.S.set_orders(R.orders)
+        if k + 1 < args.steps:  # input of step k+1 while step k runs
+            if k >= 1:
+                cs.wait_event(ev_step[k - 1])
             with torch.cuda.stream(cs):
-                out_pinned[k % 2][: qn.numel()].copy_(qn, non_blocking=True)
-            ev_out[k].record(cs)
-            d2h += qn.numel() * 8 + sel.nbytes
-        stream.wait_stream(cs)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = e0.elapsed_time(e1)
-        e2e = {"value": world * ndof * evals_per_step * args.steps / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s",
-               "h2d_bytes_per_step": int(owned_len * 8), "d2h_bytes_per_step": int(d2h // args.steps),
-               "copies": "pinned H2D of each step's input and D2H of its adapted state on a copy stream, "
-                         "double-buffered, overlapping the neighbouring steps"}
+                bufs[(k + 1) % 2][:owned].copy_(pinned, non_blocking=True)
+            ev_in[k + 1].record(cs)
+        stream.wait_event(ev_in[k])
+        if k >= 2:
+            stream.wait_event(ev_out[k - 2])
+        dof_res += R.ndof_global * R.residuals_per_step
+        if isinstance(R, Cfg2Run):
+            R.S.compute_dt(bufs[k % 2], CFL, R.dts[0])
+        else:
+            R.dts[0].copy_(R.dt0)
+        qn, sel = R.step(qin=bufs[k % 2])
+        ev_step[k].record(stream)
+        cs.wait_event(ev_step[k])
+        with torch.cuda.stream(cs):
+            out_pinned[k % 2][: qn.numel()].copy_(qn, non_blocking=True)
+        ev_out[k].record(cs)
+        d2h += qn.numel() * 8 + sel.nbytes
+    stream.wait_stream(cs)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=stream.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    return {"value": dof_res / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s",
+            "h2d_bytes_per_step": int(owned * 8), "d2h_bytes_per_step": int(d2h // args.steps),
+            "copies": "pinned H2D of each step's input state and D2H of its result state + selected orders on a "
+                      "copy stream, double-buffered, overlapping the neighbouring steps"}
 
-    return dict(value=value, total_ms=total_ms, rk_ms=rk_ms, tau_ms=tau_ms, adapt_ms=adapt_ms, ndof=ndof, E=n_elem,
-                achieved=achieved, peak=peak, peak_kind=peak_kind, tau_elems=tau_elems, clocks=clk,
-                launches=launches, e2e=e2e, rk_count=rk_count, bytes_rk_step=bytes_rk_step)
 
+# ----------------------------------------------------------------------------
+# CPU oracle (baseline leg and reference arm)
+# ----------------------------------------------------------------------------
 
-def oracle_baseline(sample_rk_steps=1, with_tau=True):
-    """The CPU oracle as it stands on this host's cores: a bounded sample of
-    the same workload (cfg2 layout): RK3 steps + one tau-estimate."""
+def oracle_cfg5_step(P, mesh, orders, q, rk_steps):
+    """The cfg5 step on a sample for the oracle: rk_steps RK3 steps (dt from
+    the CFL/DFL rule), a SOLVER reference residual, the isolated tau-estimate
+    and the dynamic selection (reported only, reading A17)."""
     import oracle
 
-    mesh = W.cube_mesh(16)
-    orders = W.orders_uniform(mesh.E, 6)
-    P = oracle.Problem(mesh)
-    X = P.node_coords(orders)
-    q = W.pulse_state(X, orders, center=W.cfg2_center(), sigma=0.08)
-    ndof = W.ndof(orders)
     t0 = time.perf_counter()
-    for _ in range(sample_rk_steps):
-        dt = P.dt(orders, q, CFL)
-        q = P.rk3_step(orders, q, dt)
+    for _ in range(rk_steps):
+        q = P.rk3_step(orders, q, P.dt(orders, q, CFL))
     t1 = time.perf_counter()
-    tau_s = None
-    if with_tau:
-        r = P.rhs(orders, q)
-        P.tau_estimate(orders, q, r)
-        tau_s = time.perf_counter() - t1
-    gdofs = ndof * 3 * sample_rk_steps / (t1 - t0) / 1e9
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
-    return dict(value=gdofs, seconds=t1 - t0, tau_s=tau_s, tau_elems=mesh.E / tau_s if tau_s else None, cores=cores,
-                sample=f"{sample_rk_steps} RK3 step(s) (3 residuals each) on the cfg2 layout (16^3 elements, N=6, "
-                       f"{ndof} DOF)" + (" + 1 SOLVER residual + 1 tau-estimate" if with_tau else ""))
+    r = P.rhs(orders, q)
+    tau = P.tau_estimate(orders, q, r)
+    oracle.select_dynamic(orders, tau, mesh.nbr, CFG5_TAU_MAX, CFG5_NMIN, CFG5_NMAX)
+    t2 = time.perf_counter()
+    return q, t1 - t0, t2 - t1
 
 
-def fp64_block(res):
-    """Secondary rooflines: algorithmic fp64 rate (flops_model) of the RK stage
-    and of the tau-estimation against the measured DFMA peak."""
-    peak, src = load_fp64_peak()
-    per_dof, tau_el = flops_model(6)
-    stage_tf = per_dof * res["ndof"] * 3 * res["rk_count"] / (res["rk_ms"] * 1e-3) / 1e12
-    tau_tf = tau_el * res["tau_elems"] / 1e12
-    return {"peak_tflops": peak, "peak_source": src,
-            "rk_stage": {"flops_per_dof": round(per_dof, 1), "achieved_tflops": stage_tf, "frac": stage_tf / peak},
-            "tau": {"flops_per_element": round(tau_el), "achieved_tflops": tau_tf, "frac": tau_tf / peak,
-                    "note": "tau time includes the SOLVER reference residual"},
-            "model": "bench.py flops_model (SURVEY 8(c).1 steps, FMA = 2)"}
+def oracle_cfg5(nth, rk_steps, threads=None):
+    """Run the oracle's cfg5 step on the 96 x nth x 1 sample; returns rates."""
+    import oracle
+
+    env_threads = os.environ.get("OMP_NUM_THREADS")
+    mesh, orders, nsp = cfg5_sample(nth)
+    P = oracle.Problem(mesh, oracle.phys(oracle.NS, mu=nsp["mu"], Pr=nsp["Pr"], qinf=nsp["qinf"]))
+    q = ns_state(orders, nsp)
+    t = time.perf_counter()
+    q, t_rk, t_tau = oracle_cfg5_step(P, mesh, orders, q, rk_steps)
+    total = time.perf_counter() - t
+    nd = W.ndof(orders)
+    return dict(total=total, t_rk=t_rk, t_tau=t_tau, ndof=nd, E=mesh.E,
+                gdofs=nd * (3 * rk_steps + 1) / total / 1e9,
+                res_gdofs=(nd * 3 * rk_steps / t_rk / 1e9) if rk_steps else None,
+                tau_elems=mesh.E / t_tau, cores=int(threads or env_threads or os.cpu_count()),
+                sample=f"cfg5 recipe on 96 x {nth} x 1 elements ({mesh.E} elements, {nd} DOF): {rk_steps} RK3 step(s) "
+                       f"+ SOLVER residual + tau-estimate + dynamic selection")
 
 
-def config_block(world, extra=None):
-    c = {"workload": ("cfg2" if world == 1 else f"cfg2 per rank (weak scaling, global 16x16x{16 * world})") +
-                     ": Euler density pulse, periodic 16^3 affine hexes, N=(6,6,6) Gauss-Lobatto, "
-                     "50 RK3 steps (CFL 0.5) + SOLVER-reference tau-estimate + dynamic select (tau_max 1e-4, "
-                     "N in [3,8], jump rule b, decrease cap 1) + transfer per step",
-         "elements": 4096, "orders": [6, 6, 6], "ndof": 4096 * 343, "residuals_per_step": 3 * RK_PER_STEP + 1,
-         "l2": "inputs larger than L2: each RK stage touches q, g, q' = 3 x 56.2 MB = 169 MB > 126 MB L2",
-         "parallelism": f"domain decomposition dp{world}: z-slabs of 16^3 elements per rank, NCCL halo "
-                        f"exchange per RK stage, MAX all-reduce of the CFL rate per step" if world > 1 else "single"}
-    if extra:
-        c.update(extra)
+def oracle_one_thread(nth, rk_steps):
+    """The same oracle step at 1 thread (a subprocess with OMP_NUM_THREADS=1)."""
+    code = ("import json,sys; sys.path.insert(0, %r); import bench; "
+            "print(json.dumps(bench.oracle_cfg5(%d, %d, threads=1)))" % (ROOT, nth, rk_steps))
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    if out.returncode != 0:
+        return None
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+# ----------------------------------------------------------------------------
+# JSON line
+# ----------------------------------------------------------------------------
+
+def config_block(args, world, R=None):
+    if args.workload == "cfg5":
+        c = {"workload": "cfg5 (BASELINE configs[4]): Navier-Stokes Re 100 Ma 0.2 Pr 0.72, O-grid 96 x 256 x 16 curved "
+                         "hexes (g_eta = 2, radial ratio sqrt(1.1)), seeded orders N_x, N_y ~ U{2..8}, N_z = 2 (A21), "
+                         "free stream + 1e-3 velocity noise; per step 20 RK3 steps (CFL = DFL = 0.5) + SOLVER "
+                         "reference residual + tau-estimate (all coarse orders) + dynamic selection (tau_max 1, "
+                         "N in [1,8], rule b, cap 1; reported, not applied: A17)",
+             "elements": 393216, "ndof": int(R.ndof_global) if R else 42491745,
+             "residuals_per_step": 3 * CFG5_RK + 1,
+             "l2": "inputs larger than L2: the state alone is 1.7 GB (126 MB L2)",
+             "parallelism": ("single" if world == 1 else
+                             f"dp{world}: azimuthal slabs of 256/{world} x 96 x 16 elements per rank, NCCL halo "
+                             f"exchange per residual, MAX all-reduce of the CFL/DFL rates per RK step")}
+    else:
+        c = {"workload": "cfg2 (BASELINE configs[1]): Euler density pulse, periodic 16^3 affine hexes, start "
+                         "N=(6,6,6); per step one estimation interval of the dynamic run: 50 RK3 steps (CFL 0.5) "
+                         "+ SOLVER reference residual + tau-estimate + dynamic selection (tau_max 1e-4, N in [3,8], "
+                         "rule b, cap 1) + transfer + dg_set_orders (the adaptation is applied)",
+             "elements": 4096, "ndof_per_step": getattr(R, "ndof_steps", None),
+             "residuals_per_step": 3 * CFG2_RK + 1,
+             "l2": "working set ~170 MB per RK stage at N=6 (> 126 MB L2)", "parallelism": "single"}
     return c
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg5", choices=["cfg5", "cfg2"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -429,25 +654,37 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        # The reference arm for this tier is the CPU oracle, timed as it stands.
+        # The reference arm for this tier is the CPU oracle, timed as it stands,
+        # on a bounded sample of the cfg5 step: the same 20 RK steps + reference
+        # residual + tau + selection on 96 x 4 x 1 elements of the cfg5 recipe.
         import oracle
 
         oracle.build()
+        nth = 4
+        mesh, orders, nsp = cfg5_sample(nth)
+        P = oracle.Problem(mesh, oracle.phys(oracle.NS, mu=nsp["mu"], Pr=nsp["Pr"], qinf=nsp["qinf"]))
+        q = ns_state(orders, nsp)
         for _ in range(args.warmup):
-            oracle_baseline(1, with_tau=False)
+            q, _, _ = oracle_cfg5_step(P, mesh, orders, q, CFG5_RK)
         ts = []
         for _ in range(args.steps):
-            r = oracle_baseline(1, with_tau=False)
-            ts.append(r["seconds"])
+            t = time.perf_counter()
+            q, _, _ = oracle_cfg5_step(P, mesh, orders, q, CFG5_RK)
+            ts.append(time.perf_counter() - t)
         total = sum(ts)
-        ndof = 4096 * 343
-        value = ndof * 3 * args.steps / total / 1e9
+        nd = W.ndof(orders)
+        value = nd * (3 * CFG5_RK + 1) * args.steps / total / 1e9
+        cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count()))
+        sample = (f"cfg5 recipe on 96 x {nth} x 1 elements ({mesh.E} elements, {nd} DOF): per step 20 RK3 steps + "
+                  f"SOLVER residual + tau-estimate + dynamic selection (the GPU arm's step on 1/{393216 // mesh.E} "
+                  f"of the mesh)")
         line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GDOF/s",
-                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / args.steps * 1e3,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": config_block(1, {"reference_step": "1 RK3 step (3 residuals) per step, CPU oracle"}),
-                "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": r["cores"], "kind": "oracle",
-                                 "sample": r["sample"]},
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": total / args.steps * 1e3, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config_block(args, 1),
+                "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": cores, "kind": "oracle",
+                                 "sample": sample},
                 "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
@@ -455,30 +692,64 @@ def main():
     res = run_gpu(args, rank, world)
     if rank != 0:
         return
+    R = res["runner"]
     cpu = None
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline and world == 1 and args.workload == "cfg5":
         import oracle
 
         oracle.build()
-        cb = oracle_baseline(1, with_tau=True)
-        cpu = {"value": cb["value"], "unit": "GDOF/s", "cores": cb["cores"], "kind": "oracle", "sample": cb["sample"],
-               "tau_elems_per_s": cb["tau_elems"]}
+        cb = oracle_cfg5(8, 1)
+        one = oracle_one_thread(4, 1)
+        cpu = {"value": cb["gdofs"], "unit": "GDOF/s", "cores": cb["cores"], "kind": "oracle", "sample": cb["sample"],
+               "tau_elems_per_s": cb["tau_elems"],
+               "one_thread": None if one is None else
+               {"value": one["gdofs"], "residual_gdofs": one["res_gdofs"], "tau_elems_per_s": one["tau_elems"],
+                "sample": one["sample"], "cores": 1},
+               "residual_gdofs": cb["res_gdofs"]}
+    peak_bw, peak_bw_src = load_peaks()
+    peak_f, peak_f_src = load_fp64_peak()
+    ns = args.workload == "cfg5"
+    mesh = R.mesh
+    orders = R.orders_g if ns else R.orders
+    stage_ms = res["rk_ms"] / res["rk_stages"]
+    f_stage = flops_residual(mesh, orders, ns=ns)
+    ndof = R.ndof_global
+    # algorithmic bytes of one RK stage: q read (40), g read + written (80),
+    # q' written (40) per DOF; curved: + the coordinates (x, y at the nodes,
+    # 16 B/DOF; metrics are recomputable from them) -- SURVEY 8(d)
+    b_stage = ndof * (40 + 80 + 40 + (16 if ns else 0))
+    tf = f_stage / (stage_ms * 1e-3) / 1e12
+    bw = b_stage / (stage_ms * 1e-3) / 1e9
+    f_tau = flops_tau(orders, ns=ns)
+    tau_tf = f_tau * res["tau_elems"] / mesh.E / 1e12
     line = {
         "metric": METRIC,
         "value": res["value"], "unit": "GDOF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": res["total_ms"] / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": res["total_ms"] / args.steps, "higher_is_better": True,
+        "scaling": "strong" if ns else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config_block(world),
-        "tau_elems_per_s": res["tau_elems"] * world,
-        "phase_ms_per_step": {"rk3_x50": res["rk_ms"] / args.steps, "ref_rhs_plus_tau": res["tau_ms"] / args.steps,
-                              "select_plus_transfer": res["adapt_ms"] / args.steps},
-        "rhs_rk_gdof_s": world * res["ndof"] * 3 * res["rk_count"] / (res["rk_ms"] * 1e-3) / 1e9,
-        "roofline": {"kernel": "RK stage = k_face (face Riemann fluxes) + k_res_t (volume, lifting, fused RK update)",
-                     "bound": "hbm", "achieved": res["achieved"],
-                     "peak": res["peak"], "unit": "GB/s", "frac": res["achieved"] / res["peak"],
-                     "peak_source": res["peak_kind"], "traffic": load_traffic(),
-                     "bytes_per_dof": "120 (stage 1) / 160 (stages 2,3)"},
-        "roofline_fp64": fp64_block(res),
+        "config": config_block(args, world, R),
+        "tau_elems_per_s": res["tau_elems"],
+        "phase_ms_per_step": {f"rk3_x{R.rk_steps_per_step}": res["rk_ms"] / args.steps,
+                              "ref_rhs_plus_tau": res["tau_ms"] / args.steps,
+                              "select" + ("" if ns else "_transfer_set_orders"): res["adapt_ms"] / args.steps},
+        "rk_stage_gdof_s": ndof * res["rk_stages"] / (res["rk_ms"] * 1e-3) / 1e9,
+        "roofline": {"kernel": "RK stage = the residual pipeline of one stage (" +
+                               ("BR1 gradient, face/mortar fluxes, volume + lifting + RK update" if ns else
+                                "k_face + k_res_t") + "), timed with CUDA events on the launch stream",
+                     "bound": "alu" if ns else "hbm",
+                     "achieved": tf if ns else bw, "peak": peak_f if ns else peak_bw,
+                     "unit": "TFLOP/s" if ns else "GB/s",
+                     "frac": (tf / peak_f) if ns else (bw / peak_bw),
+                     "peak_source": peak_f_src if ns else peak_bw_src,
+                     "traffic": load_traffic(args.workload),
+                     "algorithmic": {"flops_per_stage": f_stage, "bytes_per_stage": b_stage,
+                                     "flops_per_dof": f_stage / ndof, "model": "bench.py flops_residual"}},
+        "roofline_hbm": {"achieved": bw, "peak": peak_bw, "unit": "GB/s", "frac": bw / peak_bw,
+                         "bytes_per_dof": b_stage / ndof, "peak_source": peak_bw_src},
+        "roofline_tau": {"bound": "alu", "achieved": tau_tf, "peak": peak_f, "unit": "TFLOP/s",
+                         "frac": tau_tf / peak_f, "flops_per_estimate": f_tau,
+                         "note": "tau time includes the SOLVER reference residual"},
         "cpu_baseline": cpu,
         "e2e": res["e2e"],
         "gpu_launches": res["launches"],

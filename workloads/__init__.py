@@ -205,16 +205,26 @@ def ns_params(Re=100.0, Ma=0.2, Pr=0.72, gamma=GAMMA):
 
 def freestream_noise_state(orders: np.ndarray, qinf_prims, noise=1e-3, seed=4, gamma=GAMMA) -> np.ndarray:
     """Free stream plus i.i.d. U(-1,1)*noise per velocity component per node,
-    canonical order, rho = 1, p = p_inf (reading A22)."""
+    canonical order, rho = 1, p = p_inf (reading A22).  The draws are taken
+    element by element, (3, n) per element (one vectorised draw of the same
+    sequence)."""
     rho0, u0, v0, w0, p0 = qinf_prims
     rng = np.random.default_rng(seed)
     offq = offsets(orders, 5)
+    n = np.diff(offq) // 5
+    draws = rng.uniform(-1.0, 1.0, size=3 * int(n.sum())) * noise  # element e: 3 n_e values, [c][node]
+    # per node: element, local node index -> positions of its u, v, w draws
+    e_of = np.repeat(np.arange(len(n)), n)
+    start = np.concatenate([[0], np.cumsum(3 * n)])[:-1]
+    loc = np.arange(int(n.sum())) - np.repeat(np.concatenate([[0], np.cumsum(n)])[:-1], n)
+    base = start[e_of] + loc
+    du, dv, dw = draws[base], draws[base + n[e_of]], draws[base + 2 * n[e_of]]
+    one = np.ones_like(du)
+    Q = conserved(rho0 * one, u0 + du, v0 + dv, w0 + dw, p0 * one, gamma)  # [5][nodes]
     q = np.empty(offq[-1])
-    for e in range(len(orders)):
-        n = (offq[e + 1] - offq[e]) // 5
-        du = rng.uniform(-1.0, 1.0, size=(3, n)) * noise
-        q[offq[e]:offq[e + 1]] = conserved(rho0 * np.ones(n), u0 + du[0], v0 + du[1], w0 + du[2],
-                                          p0 * np.ones(n), gamma).ravel()
+    qpos = np.repeat(offq[:-1], n) + loc
+    for v in range(5):
+        q[qpos + v * n[e_of]] = Q[v]
     return q
 
 
