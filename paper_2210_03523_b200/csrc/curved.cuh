@@ -441,140 +441,6 @@ __device__ __forceinline__ void stage_D(double (*Ds)[NP * NP], const Tables* tab
     }
 }
 
-struct CurvedParams {
-    const int* perm;  // element of CTA b: perm[pbase + b]
-    int pbase;
-    const double* q;
-    double* out;            // mode 0: qdot / grad (k_grad); mode 1: q' (RK)
-    double* g;              // RK register
-    const double* dt;
-    double rkA, rkB;
-    int mode, variant;
-    const int* orders;
-    const long long* off;
-    const FaceInfo* finfo;
-    const double* met;      // metrics (2x offsets)
-    const double* grad;     // gradients (3x offsets), NS
-    const double* mortarG;  // projected mortar fluxes (5 per point) or gradient terms (15 per point)
-    const long long* fofs;  // [E][6] flux block of each element face in mortarG (k_face_curved), or null
-    const Tables* tab;
-    PhysDev ph;
-    int* flag;
-    unsigned long long* lam_max;  // CFL / DFL rates of the new state (2 slots), last RK stage
-};
-
-__device__ __forceinline__ int face_nodes(int d, int n1, int n2, int n3) { return d == 0 ? n2 * n3 : (d == 1 ? n1 * n3 : n1 * n2); }
-
-// own boundary node of face (d, s) at tangential point pt
-__device__ __forceinline__ int face_node(int d, int s, int pt, int n1, int n2, int n3)
-{
-    int i, j, k;
-    if (d == 0) { i = s ? n1 - 1 : 0; j = pt % n2; k = pt / n2; }
-    else if (d == 1) { i = pt % n1; j = s ? n2 - 1 : 0; k = pt / n1; }
-    else { i = pt % n1; j = pt / n1; k = s ? n3 - 1 : 0; }
-    return i + n1 * (j + n2 * k);
-}
-
-// ---------------------------------------------------------------------------
-// BR1 gradient (eq DGSEMsystem:2), non-isolated or isolated, per element.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(CBS, 5) k_grad(CurvedParams P)
-{
-    // one thread per node: the volume sum over the three directions and the
-    // lifting of the faces the node lies on, accumulated in registers
-    extern __shared__ double sm[];
-    __shared__ double Ds[3][NP * NP];
-    const int e = P.perm[P.pbase + blockIdx.x];
-    const int n1 = P.orders[3 * e] + 1, n2 = P.orders[3 * e + 1] + 1, n3 = P.orders[3 * e + 2] + 1;
-    stage_D(Ds, P.tab, n1, n2, n3);
-    const int n = n1 * n2 * n3;
-    const long long o = P.off[e];
-    const double* M = P.met + 2 * o;
-    double* Q = sm;           // 5n
-    double* JA = Q + NV * n;  // 9n: (Ja^d)_k
-    for (int t = threadIdx.x; t < NV * n; t += CBS) Q[t] = P.q[o + t];
-    for (int t = threadIdx.x; t < 9 * n; t += CBS) JA[t] = __ldg(M + t);
-    __syncthreads();
-    const int nn[3] = {n1, n2, n3};
-    double* out = P.out + 3 * o;
-    for (int t = threadIdx.x; t < n; t += CBS) {
-        int ijk[3];
-        node_ijk(t, n1, n2, ijk[0], ijk[1], ijk[2]);
-        double g[15];
-#pragma unroll
-        for (int c = 0; c < 15; ++c) g[c] = 0.0;
-        // volume: J g_k = sum_d D^d ((Ja^d)_k q)
-        for (int d = 0; d < 3; ++d) {
-            const int od = nn[d];
-            const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
-            const int a = ijk[d];
-            const int base = t - a * stride;
-            const double* Dr = Ds[d] + a * od;
-            for (int m = 0; m < od; ++m) {
-                const int nm = base + m * stride;
-                const double dm = Dr[m];
-                double qv[NV];
-#pragma unroll
-                for (int v = 0; v < NV; ++v) qv[v] = Q[v * n + nm];
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    const double jk = JA[(3 * d + k) * n + nm];
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) g[k * NV + v] = fma(dm, jk * qv[v], g[k * NV + v]);
-                }
-            }
-        }
-        // lifting on the faces through this node: (qhat Ja_f - q_own Ja_own)/w
-        double qo[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) qo[v] = Q[v * n + t];
-        for (int d = 0; d < 3; ++d) {
-            const int od = nn[d];
-            for (int s = 0; s < 2; ++s) {
-                if (ijk[d] != (s ? od - 1 : 0)) continue;
-                const int pt = d == 0 ? ijk[1] + n2 * ijk[2] : (d == 1 ? ijk[0] + n1 * ijk[2] : ijk[0] + n1 * ijk[1]);
-                const int f = 2 * d + s;
-                double qh[NV], jo[3], jf[3];
-                for (int c = 0; c < 3; ++c) jo[c] = JA[(3 * d + c) * n + t];
-                const double sc = (s ? 1.0 : -1.0) / P.tab->w[od - 1][0];
-                if (P.variant == 1) continue;  // isolated: qhat = own trace, no lifting
-                const FaceInfo fi = P.finfo[6 * e + f];
-                if (fi.kind == 1) {  // mortar: projected qhat Ja_f terms
-                    const double* src = P.mortarG + 3 * fi.off + pt;
-                    for (int c = 0; c < 3; ++c)
-                        for (int v = 0; v < NV; ++v)
-                            g[c * NV + v] += sc * (src[(long long)(c * NV + v) * fi.n] - qo[v] * jo[c]);
-                    continue;
-                } else if (fi.kind >= 2) {
-                    for (int c = 0; c < 3; ++c) jf[c] = jo[c];
-                    if (fi.kind == 2) {  // wall: zero velocity, keep rho and internal energy
-                        qh[0] = qo[0]; qh[1] = 0.0; qh[2] = 0.0; qh[3] = 0.0;
-                        qh[4] = qo[4] - 0.5 * (qo[1] * qo[1] + qo[2] * qo[2] + qo[3] * qo[3]) / qo[0];
-                    } else {
-                        for (int v = 0; v < NV; ++v) qh[v] = 0.5 * (qo[v] + P.ph.qinf[v]);
-                    }
-                } else {
-                    const long long nb_node = fi.base + (long long)(d == 0 ? pt % n2 : pt % n1) * fi.sa +
-                                              (long long)(d == 0 ? pt / n2 : pt / n1) * fi.sb;
-                    const double* qn = P.q + fi.off + nb_node;
-                    for (int v = 0; v < NV; ++v) qh[v] = 0.5 * (qo[v] + __ldg(qn + (long long)v * fi.n));
-                    if (s) {
-                        for (int c = 0; c < 3; ++c) jf[c] = jo[c];
-                    } else {  // face metric from the L side (the neighbour)
-                        const double* Mn = P.met + 2 * fi.off + nb_node;
-                        for (int c = 0; c < 3; ++c) jf[c] = __ldg(Mn + (long long)(3 * d + c) * fi.n);
-                    }
-                }
-                for (int c = 0; c < 3; ++c)
-                    for (int v = 0; v < NV; ++v) g[c * NV + v] += sc * (qh[v] * jf[c] - qo[v] * jo[c]);
-            }
-        }
-        const double iJ = 1.0 / __ldg(M + 9 * n + t);
-#pragma unroll
-        for (int c = 0; c < 15; ++c) out[c * n + t] = g[c] * iJ;
-    }
-}
-
 // ---------------------------------------------------------------------------
 // Curved residual / RK stage (Euler or NS), per element.
 // ---------------------------------------------------------------------------
@@ -582,237 +448,6 @@ __device__ __forceinline__ void load_grad(const double* base, int stride, double
 {
 #pragma unroll
     for (int c = 0; c < 15; ++c) g[c] = __ldg(base + (long long)c * stride);
-}
-
-// Conforming interior faces of a curved mesh, numerical flux ONCE per face
-// point (the element kernel used to evaluate it on both sides): Roe flux along
-// the L side's face metric (reading A6) and, for NS, minus the BR1 average of
-// the two viscous fluxes -- the arithmetic of k_res_curved's kind-0 branch, so
-// both elements read bit-identical values.  One warp per face; boundary faces
-// stay in the element kernel.  G block [v][pt] at the face's flux offset.
-struct CFaceParams {
-    const double* q;
-    const double* grad;
-    const double* met;
-    const FaceItem* faces;
-    double* G;
-    PhysDev ph;
-};
-
-__global__ void __launch_bounds__(128) k_face_curved(CFaceParams P, int nfaces)
-{
-    const int f = blockIdx.x * 4 + (threadIdx.x >> 5);  // one warp per face
-    if (f >= nfaces) return;
-    const FaceItem fi = P.faces[f];
-    if (fi.kind != 0) return;
-    const bool ns = P.ph.physics == 1;
-    const int d = fi.d;
-    for (int pt = threadIdx.x & 31; pt < fi.nf; pt += 32) {
-        const int ta = pt % fi.nta, tb = pt / fi.nta;
-        const int nodeL = fi.baseL + ta * fi.saL + tb * fi.sbL;
-        const int nodeR = fi.baseR + ta * fi.saR + tb * fi.sbR;
-        double qL[NV], qR[NV], jf[3], G[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            qL[v] = __ldg(P.q + fi.offL + (long long)v * fi.nL + nodeL);
-            qR[v] = __ldg(P.q + fi.offR + (long long)v * fi.nR + nodeR);
-        }
-        const double* Ml = P.met + 2 * fi.offL + nodeL;
-#pragma unroll
-        for (int c = 0; c < 3; ++c) jf[c] = __ldg(Ml + (long long)(3 * d + c) * fi.nL);
-        const double S = sqrt(jf[0] * jf[0] + jf[1] * jf[1] + jf[2] * jf[2]);
-        const double nrm[3] = {jf[0] / S, jf[1] / S, jf[2] / S};
-        riemann(qL, qR, nrm, P.ph, G);
-#pragma unroll
-        for (int v = 0; v < NV; ++v) G[v] *= S;
-        if (ns) {
-            double gL[15], gR[15], fL[NV], fR[NV];
-            load_grad(P.grad + 3 * fi.offL + nodeL, fi.nL, gL);
-            load_grad(P.grad + 3 * fi.offR + nodeR, fi.nR, gR);
-            visc_dot(qL, gL, jf[0], jf[1], jf[2], P.ph, fL);
-            visc_dot(qR, gR, jf[0], jf[1], jf[2], P.ph, fR);
-#pragma unroll
-            for (int v = 0; v < NV; ++v) G[v] -= 0.5 * (fL[v] + fR[v]);
-        }
-#pragma unroll
-        for (int v = 0; v < NV; ++v) P.G[fi.goff + (long long)v * fi.nf + pt] = G[v];
-    }
-}
-
-__global__ void __launch_bounds__(CBS, 5) k_res_curved(CurvedParams P)
-{
-    extern __shared__ double sm[];
-    __shared__ double red[32];
-    __shared__ double Ds[3][NP * NP];
-    const int e = P.perm[P.pbase + blockIdx.x];
-    const int n1 = P.orders[3 * e] + 1, n2 = P.orders[3 * e + 1] + 1, n3 = P.orders[3 * e + 2] + 1;
-    stage_D(Ds, P.tab, n1, n2, n3);
-    const int n = n1 * n2 * n3;
-    const long long o = P.off[e];
-    const double* M = P.met + 2 * o;
-    const bool ns = P.ph.physics == 1;
-    const double* GR = ns ? P.grad + 3 * o : nullptr;
-    double* Q = sm;            // 5n
-    double* F = Q + NV * n;    // 15n: contravariant fluxes Ft_d, d = 0..2
-    double* A = F + 15 * n;    // 5n
-    for (int t = threadIdx.x; t < NV * n; t += CBS) Q[t] = P.q[o + t];
-    __syncthreads();
-    // volume fluxes of the three directions from one read of q, grad q, Ja
-    for (int t = threadIdx.x; t < n; t += CBS) {
-        double qv[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) qv[v] = Q[v * n + t];
-        ViscNode V;
-        if (ns) {
-            double gv[15];
-            load_grad(GR + t, n, gv);
-            visc_node(qv, gv, P.ph, V);
-        }
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {  // = contra_flux: a . f^a - a . f^nu
-            const double ax = __ldg(M + (3 * d) * n + t), ay = __ldg(M + (3 * d + 1) * n + t),
-                         az = __ldg(M + (3 * d + 2) * n + t);
-            double Fv[NV];
-            adv_dot(qv, ax, ay, az, P.ph.gm1, Fv);
-            if (ns) {
-                double fv[NV];
-                visc_along(V, ax, ay, az, fv);
-#pragma unroll
-                for (int v = 0; v < NV; ++v) Fv[v] -= fv[v];
-            }
-#pragma unroll
-            for (int v = 0; v < NV; ++v) F[(d * NV + v) * n + t] = Fv[v];
-        }
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < n; t += CBS) {  // sum_d D^d Ft_d at node t
-        int ijk[3];
-        node_ijk(t, n1, n2, ijk[0], ijk[1], ijk[2]);
-        double acc[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) acc[v] = 0.0;
-        for (int d = 0; d < 3; ++d) {
-            const int od = d == 0 ? n1 : (d == 1 ? n2 : n3);
-            const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
-            const int a = ijk[d];
-            const int base = t - a * stride;
-            dsum_comps<NV>(od, Ds[d] + a * od, F + d * NV * n + base, n, stride,
-                           [&](int v, double sv) { acc[v] += sv; });
-        }
-#pragma unroll
-        for (int v = 0; v < NV; ++v) A[v * n + t] = acc[v];
-    }
-    __syncthreads();
-    for (int d = 0; d < 3; ++d) {
-        const int od = d == 0 ? n1 : (d == 1 ? n2 : n3);
-        if (P.variant == 0) {  // surface terms (isolated: G == Ft_own, no contribution)
-            const int nf = face_nodes(d, n1, n2, n3);
-            for (int task = threadIdx.x; task < 2 * nf; task += CBS) {
-                const int s = task >= nf, pt = task - s * nf, f = 2 * d + s;
-                const int node = face_node(d, s, pt, n1, n2, n3);
-                double qo[NV], go[15], jo[3], Fo[NV], G[NV];
-#pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    qo[v] = Q[v * n + node];
-                    Fo[v] = F[(d * NV + v) * n + node];
-                }
-                for (int c = 0; c < 3; ++c) jo[c] = __ldg(M + (3 * d + c) * n + node);
-                const FaceInfo fi = P.finfo[6 * e + f];
-                if (fi.kind == 1) {
-                    const double* src = P.mortarG + fi.off + pt;
-                    for (int v = 0; v < NV; ++v) G[v] = src[(long long)v * fi.n];
-                } else if (fi.kind == 0 && P.fofs) {  // conforming: flux once per face point (k_face_curved)
-                    const double* src = P.mortarG + P.fofs[6 * e + f] + pt;
-                    for (int v = 0; v < NV; ++v) G[v] = src[(long long)v * nf];
-                } else {
-                    if (ns) load_grad(GR + node, n, go);  // own gradient: boundary faces / no face kernel
-                    double qx[NV], gx[15], jf[3];
-                    if (fi.kind >= 2) {
-                        for (int c = 0; c < 3; ++c) jf[c] = jo[c];
-                        ghost_state(qo, fi.kind == 2 ? -1 : -2, P.ph, qx);
-                    } else {
-                        const long long nb_node = fi.base + (long long)(d == 0 ? pt % n2 : pt % n1) * fi.sa +
-                                                  (long long)(d == 0 ? pt / n2 : pt / n1) * fi.sb;
-                        const double* qn = P.q + fi.off + nb_node;
-                        for (int v = 0; v < NV; ++v) qx[v] = __ldg(qn + (long long)v * fi.n);
-                        if (ns) load_grad(P.grad + 3 * fi.off + nb_node, fi.n, gx);
-                        if (s) {
-                            for (int c = 0; c < 3; ++c) jf[c] = jo[c];
-                        } else {
-                            const double* Mn = P.met + 2 * fi.off + nb_node;
-                            for (int c = 0; c < 3; ++c) jf[c] = __ldg(Mn + (long long)(3 * d + c) * fi.n);
-                        }
-                    }
-                    const double S = sqrt(jf[0] * jf[0] + jf[1] * jf[1] + jf[2] * jf[2]);
-                    const double nrm[3] = {jf[0] / S, jf[1] / S, jf[2] / S};
-                    if (s) riemann(qo, qx, nrm, P.ph, G); else riemann(qx, qo, nrm, P.ph, G);
-                    for (int v = 0; v < NV; ++v) G[v] *= S;
-                    if (ns) {
-                        double fo[NV], fx[NV];
-                        visc_dot(qo, go, jf[0], jf[1], jf[2], P.ph, fo);
-                        if (fi.kind == 2) {  // wall: viscous flux from the inner gradient, u = 0, adiabatic
-                            fo[4] = 0.0;
-                            for (int v = 0; v < NV; ++v) G[v] -= fo[v];
-                        } else if (fi.kind == 3) {  // far field: inner viscous flux
-                            for (int v = 0; v < NV; ++v) G[v] -= fo[v];
-                        } else {  // BR1 average
-                            visc_dot(qx, gx, jf[0], jf[1], jf[2], P.ph, fx);
-                            for (int v = 0; v < NV; ++v) G[v] -= 0.5 * (fo[v] + fx[v]);
-                        }
-                    }
-                }
-                const double sc = (s ? 1.0 : -1.0) / P.tab->w[od - 1][0];
-                for (int v = 0; v < NV; ++v) A[v * n + node] += sc * (G[v] - Fo[v]);
-            }
-            __syncthreads();
-        }
-    }
-    // epilogue: Qdot = -A / J, or the low-storage RK update (+ CFL/DFL rates)
-    const double dt = P.mode ? *P.dt : 0.0;
-    double lmax = 0.0, vmax = 0.0;
-    for (int t = threadIdx.x; t < n; t += CBS) {
-        const double iJ = 1.0 / __ldg(M + 9 * n + t);
-        if (P.mode == 0) {
-            for (int v = 0; v < NV; ++v) P.out[o + (long long)v * n + t] = -A[v * n + t] * iJ;
-        } else {
-            double qn[NV];
-            for (int v = 0; v < NV; ++v) {
-                const long long ix = o + (long long)v * n + t;
-                const double gn = (P.rkA == 0.0 ? 0.0 : P.rkA * P.g[ix]) - dt * A[v * n + t] * iJ;
-                P.g[ix] = gn;
-                qn[v] = Q[v * n + t] + P.rkB * gn;
-                P.out[ix] = qn[v];
-            }
-            if (P.lam_max) {
-                int ijk[3];
-                node_ijk(t, n1, n2, ijk[0], ijk[1], ijk[2]);
-                const double ir = 1.0 / qn[0];
-                const double p = P.ph.gm1 * (qn[4] - 0.5 * ir * (qn[1] * qn[1] + qn[2] * qn[2] + qn[3] * qn[3]));
-                const double c = sqrt(P.ph.gamma * p * ir);
-                double lam = 0.0, nu = 0.0;
-                const double numax = P.ph.mu * ir * fmax(4.0 / 3.0, P.ph.gamma / P.ph.Pr);
-                for (int d = 0; d < 3; ++d) {
-                    const double a0 = __ldg(M + (3 * d) * n + t) * iJ, a1 = __ldg(M + (3 * d + 1) * n + t) * iJ,
-                                 a2 = __ldg(M + (3 * d + 2) * n + t) * iJ;
-                    const double an2 = a0 * a0 + a1 * a1 + a2 * a2;
-                    const double ua = (qn[1] * a0 + qn[2] * a1 + qn[3] * a2) * ir;
-                    const double np1 = d == 0 ? n1 : (d == 1 ? n2 : n3);
-                    lam += (fabs(ua) + c * sqrt(an2)) * np1 * np1 * 0.5;
-                    nu += numax * an2 * np1 * np1 * np1 * np1 * 0.25;
-                }
-                lmax = fmax(lmax, lam);
-                vmax = fmax(vmax, nu);
-            }
-        }
-    }
-    if (P.lam_max) {
-        lmax = block_max(lmax, red);
-        vmax = block_max(vmax, red);
-        if (threadIdx.x == 0) {
-            atomicMax(P.lam_max, (unsigned long long)__double_as_longlong(lmax));
-            if (ns) atomicMax(P.lam_max + 1, (unsigned long long)__double_as_longlong(vmax));
-        }
-    }
 }
 
 // CFL (+DFL) rates of a state, curved metrics (reading A11)
@@ -872,296 +507,6 @@ __global__ void k_dt_final2(unsigned long long* maxbits, double cfl, double dfl,
     dt[0] = v;
     maxbits[0] = 0ull;
     maxbits[1] = 0ull;
-}
-
-// ---------------------------------------------------------------------------
-// Curved mortar (reading A6): metric from L's geometry at the mortar nodes.
-// mode 0: G = |Ja| Roe - BR1 average viscous (5 per point, projected);
-// mode 1: qhat Ja_k (15 per point, projected).
-// ---------------------------------------------------------------------------
-struct CMortarParams {
-    const TablesDD* tdd;
-    const double* q;
-    const double* grad;
-    const int* orders;
-    const long long* off;
-    const MortarItem* items;
-    const long long* moff;
-    double* mortarG;  // mode 0: 5 per point at moff; mode 1: 15 per point at 3*moff
-    CurvedMesh cm;
-    const Tables* tab;
-    PhysDev ph;
-    int mode;
-};
-
-// Mortar metric Ja_d at the mortar nodes (L's geometry, reading A6), in
-// double-double, once per layout: mgeo[mgoff[face] + c*nm + t], c = 0..2.
-__global__ void __launch_bounds__(128) k_mortar_geom(CMortarParams P, double* mgeo, const long long* mgoff, int nitems)
-{
-    // one warp per mortar face (4 per CTA)
-    __shared__ double Xs[4][2][3][NP * NP];
-    const int wi = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int fid = blockIdx.x * 4 + wi;
-    if (fid >= nitems) return;
-    double (*Xm)[NP * NP] = Xs[wi][0];
-    double (*Xml)[NP * NP] = Xs[wi][1];
-    double* Jg = mgeo + mgoff[fid];
-    const MortarItem it = P.items[fid];
-    const int d = it.d;
-    const int ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
-    int NL[3], NR[3];
-    for (int k = 0; k < 3; ++k) { NL[k] = P.orders[3 * it.L + k]; NR[k] = P.orders[3 * it.R + k]; }
-    const int M1 = max(NL[ta], NR[ta]), M2 = max(NL[tb], NR[tb]);
-    const int nm = (M1 + 1) * (M2 + 1);
-    const int gd[3] = {P.cm.g1, P.cm.g2, P.cm.g3};
-    // face coordinates of L's +1 face at the mortar nodes (GL geometry nodes:
-    // last layer along d), tangential derivatives, cross product -- in dd
-    const double* G = P.cm.geo + (long long)it.L * 3 * P.cm.ng;
-    const int ga = gd[0] + 1, gb = gd[1] + 1;
-    const TablesDD* tdd = P.tdd;
-    for (int t = lane; t < nm; t += 32) {
-        const int m1 = t % (M1 + 1), m2 = t / (M1 + 1);
-        dd x[3] = {mkdd(0.0), mkdd(0.0), mkdd(0.0)};
-        for (int b = 0; b <= gd[tb]; ++b)
-            for (int a = 0; a <= gd[ta]; ++a) {
-                int idx[3];
-                idx[d] = gd[d]; idx[ta] = a; idx[tb] = b;
-                const int gi = idx[0] + ga * (idx[1] + gb * idx[2]);
-                const int ia = m1 * (gd[ta] + 1) + a, ib = m2 * (gd[tb] + 1) + b;
-                const dd wgt = dd_mul(dd{tdd->Thi[gd[ta]][M1][ia], tdd->Tlo[gd[ta]][M1][ia]},
-                                      dd{tdd->Thi[gd[tb]][M2][ib], tdd->Tlo[gd[tb]][M2][ib]});
-                for (int c = 0; c < 3; ++c) x[c] = dd_add(x[c], dd_mul(wgt, mkdd(G[c * P.cm.ng + gi])));
-            }
-        for (int c = 0; c < 3; ++c) { Xm[c][t] = x[c].hi; Xml[c][t] = x[c].lo; }
-    }
-    __syncwarp();
-    for (int t = lane; t < nm; t += 32) {
-        const int m1 = t % (M1 + 1), m2 = t / (M1 + 1);
-        dd u[3], v[3];
-        for (int c = 0; c < 3; ++c) {
-            dd s1 = mkdd(0.0), s2 = mkdd(0.0);
-            for (int m = 0; m <= M1; ++m) {
-                const int ix = m + (M1 + 1) * m2;
-                s1 = dd_add(s1, dd_mul(dd{tdd->Dhi[M1][m1 * (M1 + 1) + m], tdd->Dlo[M1][m1 * (M1 + 1) + m]},
-                                       dd{Xm[c][ix], Xml[c][ix]}));
-            }
-            for (int m = 0; m <= M2; ++m) {
-                const int ix = m1 + (M1 + 1) * m;
-                s2 = dd_add(s2, dd_mul(dd{tdd->Dhi[M2][m2 * (M2 + 1) + m], tdd->Dlo[M2][m2 * (M2 + 1) + m]},
-                                       dd{Xm[c][ix], Xml[c][ix]}));
-            }
-            u[c] = s1;
-            v[c] = s2;
-        }
-        dd w[3];
-        const dd* A = d == 1 ? v : u;  // Ja^2 = x_zeta x x_xi = x_t2 x x_t1
-        const dd* B = d == 1 ? u : v;
-        w[0] = dd_add(dd_mul(A[1], B[2]), dd_neg(dd_mul(A[2], B[1])));
-        w[1] = dd_add(dd_mul(A[2], B[0]), dd_neg(dd_mul(A[0], B[2])));
-        w[2] = dd_add(dd_mul(A[0], B[1]), dd_neg(dd_mul(A[1], B[0])));
-        for (int c = 0; c < 3; ++c) Jg[c * nm + t] = w[c].hi + w[c].lo;
-    }
-}
-
-
-
-// Curved / NS mortar faces (reading A6): k_mortar3's pipeline (persistent
-// CTAs, work counter, cp.async prefetch of the next face's traces,
-// constant-memory operators, identity passes skipped) for curved meshes.  The
-// traces of both sides are interpolated to the mortar grid M_t = max(L_t, R_t)
-// by tensor passes, the flux is evaluated per mortar point with the mortar
-// metric Ja of the L side (precomputed by k_mortar_geom), and the exact L2
-// projection returns it to each side.  NIN components are interpolated per
-// side (5: q; 20: q and the BR1 gradient), NOUT projected back (5: numerical
-// flux; 15: BR1 terms q^ Ja_c).  Threads 0-127 work on side L, 128-255 on side
-// R; at the mortar points threads 0-80 evaluate the Riemann flux (or the BR1
-// average) and, for NS, threads 128-208 the averaged viscous flux.
-constexpr int CM3_BS = 256, CM3_H = 128;
-
-template <int NIN, int NOUT>
-struct CM3 {
-    static constexpr int NC = NIN > NOUT ? NIN : NOUT;
-    static constexpr int ND = 4 * NIN * 81 + 4 * NC * 81 + NOUT * 81 + (NIN == 20 ? NV * 81 : 0);
-    static constexpr size_t smem = sizeof(double) * ND;
-};
-
-__device__ __forceinline__ void bar_half(int side)
-{
-    asm volatile("bar.sync %0, 128;\n" ::"r"(side + 1) : "memory");
-}
-
-// k_mortar3's mt_lines over NC components, line tasks strided by the half CTA
-template <int NC>
-__device__ __forceinline__ void cm3_lines(const double* __restrict__ A, const double* __restrict__ in,
-                                          double* __restrict__ out, int ni, int nl, bool along_a, int l)
-{
-    const int xs = along_a ? 1 : 9;
-    for (int task = l; task < NC * nl; task += CM3_H) {
-        const int c = task / nl, r = task - c * nl;
-        const double* x0 = in + c * 81 + (along_a ? r * 9 : r);
-        double* o = out + c * 81 + (along_a ? r * 9 : r);
-        double x[9];
-#pragma unroll
-        for (int a = 0; a < 9; ++a) x[a] = x0[a * xs];
-        for (int i = 0; i < ni; ++i) {
-            double s = 0.0;
-#pragma unroll
-            for (int a = 0; a < 9; ++a) s = fma(A[i * 9 + a], x[a], s);
-            o[i * xs] = s;
-        }
-    }
-}
-
-template <int NIN, int NOUT>
-__global__ void __launch_bounds__(CM3_BS, NIN == 20 ? 2 : 3) k_mortar_c3(CMortarParams P, const MortarFace* items, int nitems,
-                                                      int* queue, const double* mgeo, const long long* mgoff)
-{
-    using C = CM3<NIN, NOUT>;
-    constexpr int NC = C::NC;
-    extern __shared__ __align__(16) double cm_sm[];
-    double* TR = cm_sm;               // [stage][side][NIN * 81] traces (zero padded)
-    double* TM = TR + 4 * NIN * 81;   // [side][NC * 81] pass-A results
-    double* QM = TM + 2 * NC * 81;    // [side][NC * 81] pass-B results
-    double* GM = QM + 2 * NC * 81;    // [NOUT * 81] flux at the mortar points
-    double* GV = GM + NOUT * 81;      // [NV * 81] averaged viscous flux (NS)
-    const int t = threadIdx.x;
-    const int me = t >= CM3_H, l = t & (CM3_H - 1);
-    const int G = gridDim.x;
-    const int f0 = blockIdx.x;
-    if (f0 >= nitems) return;
-    for (int w = t; w < C::ND; w += CM3_BS) cm_sm[w] = 0.0;  // padding: finite once and for all
-    __syncthreads();
-    auto issue = [&](const MortarFace& it, int st) {
-        int NS[3];
-        mt_unpack(me ? it.ordR : it.ordL, NS);
-        const int d = it.d, ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
-        const int s1 = NS[ta] + 1, s2 = NS[tb] + 1;
-        const int st1 = NS[0] + 1, st2 = st1 * (NS[1] + 1);
-        const int sta = ta == 0 ? 1 : st1, stb = tb == 1 ? st1 : st2, std_ = d == 0 ? 1 : (d == 1 ? st1 : st2);
-        const int n = st2 * (NS[2] + 1);
-        const long long o = me ? it.offR : it.offL;
-        const int base = (me == 0 ? NS[d] * std_ : 0);
-        double* dstb = TR + (st * 2 + me) * NIN * 81;
-        for (int task = l; task < NIN * s2; task += CM3_H) {
-            const int c = task / s2, b = task - c * s2;
-            const double* src = (c < NV ? P.q + o + (long long)c * n : P.grad + 3 * o + (long long)(c - NV) * n) + base + b * stb;
-            double* dst = dstb + c * 81 + b * 9;
-            for (int a = 0; a < s1; ++a) cp_async8(dst + a, src + a * sta);
-        }
-    };
-    // faces f0, f0 + G, f0 + 2G, then 3G + work counter; thread 0 fetches the
-    // counter one face ahead so the atomic's latency is not exposed
-    __shared__ int s_nn[2];
-    int fcur = f0, fnext = f0 + G, pend = f0 + 2 * G;
-    MortarFace cur = items[f0];
-    MortarFace nxt = cur;
-    if (fnext < nitems) nxt = items[fnext];
-    issue(cur, 0);
-    asm volatile("cp.async.commit_group;\n" ::);
-    for (int k = 0;; ++k) {
-        if (fcur >= nitems) break;
-        if (t == 0) {
-            s_nn[k & 1] = pend;
-            pend = 3 * G + atomicAdd(queue, 1);
-        }
-        asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-        __syncthreads();  // traces of face k landed; face k-1 fully consumed
-        const int fnn = s_nn[k & 1];
-        MortarFace nn = nxt;
-        if (fnn < nitems) nn = items[fnn];
-        if (fnext < nitems) issue(nxt, (k + 1) & 1);
-        asm volatile("cp.async.commit_group;\n" ::);
-
-        const int d = cur.d;
-        const int ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
-        int NL[3], NR[3];
-        mt_unpack(cur.ordL, NL);
-        mt_unpack(cur.ordR, NR);
-        const int M1 = max(NL[ta], NR[ta]), M2 = max(NL[tb], NR[tb]);
-        const int m1 = M1 + 1, m2 = M2 + 1, nm = m1 * m2;
-        // mortar metric of this thread's point, loaded now (used after the interpolation)
-        const int tp = t & 127;  // mortar point handled by this thread (t < 81 or 128 <= t < 209)
-        const int pj = tp / 9, pi = tp - pj * 9;
-        const bool pt_on = tp < 81 && pi < m1 && pj < m2 && (me == 0 || NIN == 20);
-        double jf[3] = {0.0, 0.0, 0.0};
-        if (pt_on) {
-            const double* Jg = mgeo + __ldg(mgoff + fcur);
-            const int jp = pj * m1 + pi;
-            jf[0] = __ldg(Jg + jp);
-            jf[1] = __ldg(Jg + nm + jp);
-            jf[2] = __ldg(Jg + 2 * nm + jp);
-        }
-        const int sa_me = (me ? NR[ta] : NL[ta]) + 1, sb_me = (me ? NR[tb] : NL[tb]) + 1;
-        const bool ia = sa_me < m1, ib = sb_me < m2;
-        const bool ia0 = NL[ta] < M1, ia1 = NR[ta] < M1, ib0 = NL[tb] < M2, ib1 = NR[tb] < M2;
-        const double* opA = c_mop[ia ? mt_pair(sa_me - 1, M1) : 0];
-        const double* opB = c_mop[ib ? mt_pair(sb_me - 1, M2) : 0];
-        const double* TR0 = TR + (k & 1) * 2 * NIN * 81;
-        const double* TRme = TR0 + me * NIN * 81;
-        double* TMme = TM + me * NC * 81;
-        double* QMme = QM + me * NC * 81;
-        // side traces -> mortar: along a where s_a < m1, then along b where s_b < m2
-        if (ia) cm3_lines<NIN>(opA, TRme, TMme, m1, sb_me, true, l);
-        bar_half(me);
-        const double* Xme = ia ? TMme : TRme;
-        if (ib) cm3_lines<NIN>(opB, Xme, QMme, m2, m1, false, l);
-        __syncthreads();
-        const double* Y0 = ib0 ? QM : (ia0 ? TM : TR0);
-        const double* Y1 = ib1 ? QM + NC * 81 : (ia1 ? TM + NC * 81 : TR0 + NIN * 81);
-        if (pt_on) {
-            double qL[NV], qR[NV];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) { qL[v] = Y0[v * 81 + tp]; qR[v] = Y1[v * 81 + tp]; }
-            if (me == 0) {
-                if (NOUT == 15) {  // BR1: q^ = average, times Ja_c
-#pragma unroll
-                    for (int c = 0; c < 3; ++c)
-#pragma unroll
-                        for (int v = 0; v < NV; ++v) GM[(c * NV + v) * 81 + tp] = 0.5 * (qL[v] + qR[v]) * jf[c];
-                } else {
-                    const double S = sqrt(jf[0] * jf[0] + jf[1] * jf[1] + jf[2] * jf[2]);
-                    const double nrm[3] = {jf[0] / S, jf[1] / S, jf[2] / S};
-                    double F[NV];
-                    riemann(qL, qR, nrm, P.ph, F);
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) GM[v * 81 + tp] = F[v] * S;
-                }
-            } else {
-                double gs[15], fL[NV], fR[NV];  // one side's gradient live at a time
-#pragma unroll
-                for (int c = 0; c < 15; ++c) gs[c] = Y0[(NV + c) * 81 + tp];
-                visc_dot(qL, gs, jf[0], jf[1], jf[2], P.ph, fL);
-#pragma unroll
-                for (int c = 0; c < 15; ++c) gs[c] = Y1[(NV + c) * 81 + tp];
-                visc_dot(qR, gs, jf[0], jf[1], jf[2], P.ph, fR);
-#pragma unroll
-                for (int v = 0; v < NV; ++v) GV[v * 81 + tp] = 0.5 * (fL[v] + fR[v]);
-            }
-        }
-        __syncthreads();
-        if (NIN == 20) {
-            for (int w = t; w < NV * 81; w += CM3_BS) GM[w] -= GV[w];
-            __syncthreads();
-        }
-        // exact L2 projection back to each side (identity passes skipped)
-        if (ia) cm3_lines<NOUT>(opA + 81, GM, TMme, sa_me, m2, true, l);
-        bar_half(me);
-        const double* Zme = ia ? TMme : GM;
-        if (ib) cm3_lines<NOUT>(opB + 81, Zme, QMme, sb_me, sa_me, false, l);
-        bar_half(me);
-        const double* W = ib ? QMme : Zme;
-        double* dstb = P.mortarG + (NOUT == 15 ? 3 : 1) * (me ? cur.moR : cur.moL);
-        for (int task = l; task < NOUT * sb_me; task += CM3_H) {  // one (c, b) row per task
-            const int c = task / sb_me, b = task - c * sb_me;
-            const double* src = W + c * 81 + b * 9;
-            double* dst = dstb + (c * sb_me + b) * sa_me;
-            for (int a = 0; a < sa_me; ++a) dst[a] = src[a];
-        }
-        fcur = fnext;
-        fnext = fnn;
-        cur = nxt;
-        nxt = nn;
-    }
 }
 
 // ---------------------------------------------------------------------------

@@ -24,6 +24,7 @@
 #include "face.cuh"
 #include "tau_t.cuh"
 #include "curved.cuh"
+#include "ns.cuh"
 
 using namespace dgtau;
 
@@ -162,10 +163,7 @@ struct dg_ctx {
     double* d_geo = nullptr;
     double* d_met = nullptr;       // 10 per node
     double* d_grad = nullptr;      // 15 per node (NS)
-    double* d_mortarGq = nullptr;  // 15 per mortar point (NS gradient mortars)
-    double* d_mgeo = nullptr;      // curved mortars: Ja at the mortar nodes (3 per point)
-    long long* d_mgoff = nullptr;  // [nmortar] offsets into d_mgeo
-    long long met_len = 0, grad_len = 0, mq_len = 0;
+    long long met_len = 0, grad_len = 0;
     std::vector<long long> tr_off_host;
     long long ref_len = 0;
     double* d_mortarG = nullptr;
@@ -180,10 +178,8 @@ struct dg_ctx {
     res_occupancy rocc[NP][NP][NP] = {};
     signed char occ_cache[NP][NP][NP];  // resident k_res_t CTAs per SM, -1 = not queried yet
     int nsm = 148;
-    int cm3_occ[3] = {1, 1, 1};  // resident k_mortar_c3 CTAs per SM: <5,5>, <20,5>, <5,15>
     FaceInfo* d_finfo_slot = nullptr;
     MortarFace* d_mfaces = nullptr;    // mortar faces (k_mortar3)
-    long long* d_fofs_el = nullptr;    // curved: [E][6] flux block of each element face (k_face_curved)
     long long* d_fofs_slot = nullptr;  // [elist][6] flux offset (into d_mortarG) of each face of each slot
     FaceItem* d_faces = nullptr;       // conforming + boundary faces (one Riemann flux per face point)
     int* d_fpt = nullptr;              // [nfaces+1] point prefix
@@ -197,6 +193,22 @@ struct dg_ctx {
     bool no_graphs = false;  // DGTAU_NO_GRAPHS=1: launch mixed-order residuals directly
     cudaStream_t cap_stream = nullptr;  // graph capture stream
     std::map<ShapeKey, GraphEntry> graphs;  // mixed-order residual graphs of the current layout
+    // curved residual path (ns.cuh): element items, face list, face blocks
+    bool extruded = false;     // extruded mesh (compact metrics, structural zeros), see ns.cuh
+    bool borrowed = false;     // coarse-level sub-context: scratch lent by the parent, never reallocated
+    double* d_metc = nullptr;  // EXT: 6 per (i, j) column
+    long long* d_coff = nullptr;
+    NsItem* d_nsitems = nullptr;
+    int* d_nselist = nullptr;
+    std::vector<SizeClass> nscls;  // item classes by node count: [base, base + count), max nodes
+    NsFace* d_nsfaces = nullptr;
+    int nsf_cls[4] = {0, 0, 0, 0};  // faces of W = 1..3 warps: [nsf_cls[W-1], nsf_cls[W])
+    double* d_fg = nullptr;         // face metrics at the mortar points
+    double* d_nsG = nullptr;        // numerical-flux blocks (scratch per residual)
+    double* d_nsH = nullptr;        // BR1 face-term blocks (scratch per residual)
+    long long nsG_cap = 0, nsH_cap = 0;
+    long long* d_fofsG = nullptr;   // [E][6] flux block of each element face
+    long long* d_fofsH = nullptr;   // [E][6] BR1 block of each element face
 };
 
 namespace {
@@ -426,23 +438,31 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         cudaFuncSetAttribute(k_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
         cudaFuncSetAttribute(k_tau, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
         cudaFuncSetAttribute(k_tau5, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 4096);  // 3.1 KB static
-        cudaFuncSetAttribute(k_mortar_c3<5, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CM3<5, 5>::smem);
-        cudaFuncSetAttribute(k_mortar_c3<20, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CM3<20, 5>::smem);
-        cudaFuncSetAttribute(k_mortar_c3<5, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CM3<5, 15>::smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->cm3_occ[0], k_mortar_c3<5, 5>, CM3_BS, CM3<5, 5>::smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->cm3_occ[1], k_mortar_c3<20, 5>, CM3_BS, CM3<20, 5>::smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctx->cm3_occ[2], k_mortar_c3<5, 15>, CM3_BS, CM3<5, 15>::smem);
-        for (int& o : ctx->cm3_occ) o = std::max(1, o);
         cudaFuncSetAttribute(k_tau5, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
         cudaFuncSetAttribute(k_transfer, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
         const int limc = optin - 8192;  // curved kernels: up to ~6 KB static (staged D, reductions)
         cudaFuncSetAttribute(k_metrics, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
-        cudaFuncSetAttribute(k_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
-        cudaFuncSetAttribute(k_res_curved, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
         cudaFuncSetAttribute(k_tau_curved<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
         cudaFuncSetAttribute(k_tau_curved<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
         cudaFuncSetAttribute(k_tau_curved<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
         ctx->smem_limit = limc;
+        // curved residual path (ns.cuh): element kernels up to 20 x 729 doubles, face kernels per W
+        const int lns = std::min(limc, 20 * 729 * 8);
+        cudaFuncSetAttribute(k_ns_grad<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
+        cudaFuncSetAttribute(k_ns_grad<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
+        cudaFuncSetAttribute(k_ns_res<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
+        cudaFuncSetAttribute(k_ns_res<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
+        cudaFuncSetAttribute(k_ns_res<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
+        cudaFuncSetAttribute(k_ns_res<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
+#define NSF_ATTR(W)                                                                                                   \
+    cudaFuncSetAttribute(k_ns_face<W, MODE_QHAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FaceCfg<W>::smem);  \
+    cudaFuncSetAttribute(k_ns_face<W, MODE_FLUX_EULER>, cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
+                         (int)FaceCfg<W>::smem);                                                                        \
+    cudaFuncSetAttribute(k_ns_face<W, MODE_FLUX_NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FaceCfg<W>::smem);
+        NSF_ATTR(1)
+        NSF_ATTR(2)
+        NSF_ATTR(3)
+#undef NSF_ATTR
         cudaError_t e = cudaGetLastError();  // attribute errors are fatal here, not stale later
         if (e != cudaSuccess) {
             s = cuda_check(ctx, e, "cudaFuncSetAttribute");
@@ -468,21 +488,27 @@ static void drop_graphs(dg_ctx* ctx)
 // the caller's stream and every coarse layout needs no more than the fine one
 // (fewer nodes; mortars only where the fine layout has them, with smaller
 // blocks).  Detach before destroying a level so the scratch stays the parent's.
+// Coarse-level sub-contexts (non-isolated tau) borrow the parent's per-residual
+// scratch: the gradient and the face blocks.  A borrowing context never
+// reallocates them (dg_set_orders fails loudly if a coarse layout needed more
+// than the fine one lent -- it cannot: every coarse order is <= the fine one).
 static void lend_scratch(dg_ctx* parent, dg_ctx* sub)
 {
+    sub->borrowed = true;
     sub->d_grad = parent->d_grad;
     sub->grad_len = parent->grad_len;
-    sub->d_mortarGq = parent->d_mortarGq;
-    sub->mq_len = parent->mq_len;
-    sub->d_mortarG = parent->d_mortarG;  // capacity known to dalloc's registry
+    sub->d_nsG = parent->d_nsG;
+    sub->nsG_cap = parent->nsG_cap;
+    sub->d_nsH = parent->d_nsH;
+    sub->nsH_cap = parent->nsH_cap;
 }
 
 static void unlend_scratch(dg_ctx* parent, dg_ctx* sub)
 {
     if (!sub) return;
     if (sub->d_grad == parent->d_grad) sub->d_grad = nullptr;
-    if (sub->d_mortarGq == parent->d_mortarGq) sub->d_mortarGq = nullptr;
-    if (sub->d_mortarG == parent->d_mortarG) sub->d_mortarG = nullptr;
+    if (sub->d_nsG == parent->d_nsG) sub->d_nsG = nullptr;
+    if (sub->d_nsH == parent->d_nsH) sub->d_nsH = nullptr;
 }
 
 static void drop_coarse(dg_ctx* ctx)
@@ -522,7 +548,6 @@ void dg_destroy(dg_ctx* ctx)
     dfree(ctx->d_finfo);
     dfree(ctx->d_finfo_slot);
     dfree(ctx->d_fofs_slot);
-    dfree(ctx->d_fofs_el);
     dfree(ctx->d_mfaces);
     dfree(ctx->d_faces);
     dfree(ctx->d_fpt);
@@ -536,11 +561,18 @@ void dg_destroy(dg_ctx* ctx)
     dfree(ctx->d_geo);
     dfree(ctx->d_met);
     dfree(ctx->d_grad);
-    dfree(ctx->d_mortarGq);
-    dfree(ctx->d_mgeo);
-    dfree(ctx->d_mgoff);
     dfree(ctx->d_tr_off);
     dfree(ctx->d_mortarG);
+    dfree(ctx->d_metc);
+    dfree(ctx->d_coff);
+    dfree(ctx->d_nsitems);
+    dfree(ctx->d_nselist);
+    dfree(ctx->d_nsfaces);
+    dfree(ctx->d_fg);
+    dfree(ctx->d_nsG);
+    dfree(ctx->d_nsH);
+    dfree(ctx->d_fofsG);
+    dfree(ctx->d_fofsH);
     dfree(ctx->d_scratch);
     dfree(ctx->d_flag);
     dfree(ctx->d_sel);
@@ -593,6 +625,21 @@ dg_status dg_mesh_upload(dg_ctx* ctx, int E, const int32_t* nbr_host, const int3
         }
     }
     ctx->curved = !affine;
+    // extruded mesh (ns.cuh): linear in zeta, x and y independent of zeta, z
+    // independent of xi and eta and increasing with zeta
+    bool ext = ctx->curved && gorder_host[2] == 1 && !getenv_flag("DGTAU_NO_EXT");
+    {
+        const int L2 = (gorder_host[0] + 1) * (gorder_host[1] + 1);
+        for (int e = 0; e < E && ext; ++e) {
+            const double* G = geo_host + 3LL * ng * e;
+            for (int ab = 0; ab < L2 && ext; ++ab) {
+                if (G[ab] != G[ab + L2] || G[ng + ab] != G[ng + ab + L2]) ext = false;
+                if (G[2 * ng + ab] != G[2 * ng] || G[2 * ng + L2 + ab] != G[2 * ng + L2]) ext = false;
+            }
+            if (!(G[2 * ng + L2] > G[2 * ng])) ext = false;
+        }
+    }
+    ctx->extruded = ext;
     if (ctx->curved) {
         for (long long i = 0; i < 3LL * E; ++i) ctx->h[i] = 1.0;  // unused by the curved kernels
         CK(upload(ctx->d_geo, ctx->geo));
@@ -618,6 +665,221 @@ static void size_classes(std::vector<int>& idx, const std::vector<int>& sz, int 
         out.push_back(SizeClass{i, j - i, sz[idx[i]]});
         i = j;
     }
+}
+
+// Scratch that a borrowing (coarse-level) context must not reallocate.
+static dg_status scratch_need(dg_ctx* ctx, double*& p, long long& cap, long long need, const char* what)
+{
+    if (need <= cap && p) return DG_OK;
+    if (need == 0) return DG_OK;
+    if (ctx->borrowed)
+        return fail(ctx, DG_EINVAL, std::string("set_orders: borrowed ") + what + " scratch too small (coarse layout larger than the fine one)");
+    dfree(p);
+    CK(cudaMalloc(&p, sizeof(double) * need));
+    cap = need;
+    return DG_OK;
+}
+
+// Plans of the curved residual path (ns.cuh): element items, the face list
+// (every interior face once, boundary faces of owned elements), face-block
+// offsets, face metrics and (extruded meshes) compact volume metrics.
+static dg_status build_ns_plans(dg_ctx* ctx)
+{
+    static const int TA[3] = {1, 0, 0}, TB[3] = {2, 2, 1};
+    const int E = ctx->E;
+    const bool ns = ctx->prm.physics == DG_NS;
+    const bool ext = ctx->extruded;
+    const long long L = ctx->off[E];
+    // ---- element items: same-order owned elements, <= NS_ITEM_NODES nodes ----
+    {
+        std::map<int, std::vector<int>> bk;
+        for (int e = 0; e < ctx->n_own; ++e) {
+            const int* N = &ctx->orders[3 * e];
+            bk[N[0] | (N[1] << 8) | (N[2] << 16)].push_back(e);
+        }
+        std::vector<NsItem> items;
+        std::vector<int> el;
+        el.reserve(ctx->n_own);
+        for (auto& kv : bk) {
+            const int N[3] = {kv.first & 255, (kv.first >> 8) & 255, (kv.first >> 16) & 255};
+            const int n = npts(N);
+            const int k = std::max(1, std::min(NS_MAXSLOTS, NS_ITEM_NODES / n));
+            for (size_t i = 0; i < kv.second.size(); i += k) {
+                NsItem it;
+                it.start = (int)el.size();
+                it.count = (int)std::min<size_t>(k, kv.second.size() - i);
+                it.ord = kv.first;
+                it.nodes = it.count * n;
+                for (int j = 0; j < it.count; ++j) el.push_back(kv.second[i + j]);
+                items.push_back(it);
+            }
+        }
+        // classes by node count (shared memory of the launch): <= 256, <= 512, larger
+        static const int edge[3] = {256, 512, 1 << 30};
+        std::vector<NsItem> sorted;
+        sorted.reserve(items.size());
+        ctx->nscls.clear();
+        for (int c = 0; c < 3; ++c) {
+            const int lo = c ? edge[c - 1] : 0;
+            SizeClass cl{(int)sorted.size(), 0, 0};
+            for (const NsItem& it : items)
+                if (it.nodes > lo && it.nodes <= edge[c]) {
+                    sorted.push_back(it);
+                    cl.count++;
+                    cl.maxn = std::max(cl.maxn, it.nodes);
+                }
+            if (cl.count) ctx->nscls.push_back(cl);
+        }
+        CK(upload(ctx->d_nsitems, sorted));
+        CK(upload(ctx->d_nselist, el));
+    }
+    // ---- faces ----
+    std::vector<NsFace> fl;
+    std::vector<int> fw;  // warps per face
+    std::vector<long long> fofsG(6LL * E, -1), fofsH(6LL * E, -1);
+    long long gl = 0, hl = 0, mgl = 0;
+    auto pack = [&](int e) { const int* a = &ctx->orders[3 * e]; return a[0] | (a[1] << 4) | (a[2] << 8); };
+    auto nkH = [&](int d) { return ext ? ext_nk(d) : 3; };
+    for (int e = 0; e < E; ++e)
+        for (int d = 0; d < 3; ++d) {
+            const int* No = &ctx->orders[3 * e];
+            const int so = (No[TA[d]] + 1) * (No[TB[d]] + 1);
+            // interior face: e is L (its +d face)
+            const int nb = ctx->nbr[6 * e + 2 * d + 1];
+            if (nb >= 0 && !(e >= ctx->n_own && nb >= ctx->n_own)) {
+                const int* Nn = &ctx->orders[3 * nb];
+                const int sr = (Nn[TA[d]] + 1) * (Nn[TB[d]] + 1);
+                const bool conf = No[TA[d]] == Nn[TA[d]] && No[TB[d]] == Nn[TB[d]];
+                const int nm = (std::max(No[TA[d]], Nn[TA[d]]) + 1) * (std::max(No[TB[d]], Nn[TB[d]]) + 1);
+                NsFace F{};
+                F.offL = ctx->off[e];
+                F.offR = ctx->off[nb];
+                F.eL = e;
+                F.eR = nb;
+                F.ordL = pack(e);
+                F.ordR = pack(nb);
+                F.d = d;
+                F.kind = conf ? 0 : 1;
+                F.mg = mgl;
+                mgl += 3LL * nm;
+                F.outL = gl;
+                fofsG[6LL * e + 2 * d + 1] = gl;
+                gl += (long long)NV * so;
+                F.outR = conf ? F.outL : gl;
+                fofsG[6LL * nb + 2 * d] = F.outR;
+                if (!conf) gl += (long long)NV * sr;
+                if (ns) {
+                    F.hL = hl;
+                    fofsH[6LL * e + 2 * d + 1] = hl;
+                    hl += (long long)NV * nkH(d) * so;
+                    F.hR = conf ? F.hL : hl;
+                    fofsH[6LL * nb + 2 * d] = F.hR;
+                    if (!conf) hl += (long long)NV * nkH(d) * sr;
+                }
+                fl.push_back(F);
+                fw.push_back((nm + 31) / 32);
+            }
+            // boundary faces of owned elements
+            if (e >= ctx->n_own) continue;
+            for (int s = 0; s < 2; ++s) {
+                const int b = ctx->nbr[6 * e + 2 * d + s];
+                if (b != -1 && b != -2) continue;
+                NsFace F{};
+                F.offL = s ? ctx->off[e] : -1;
+                F.offR = s ? -1 : ctx->off[e];
+                F.eL = s ? e : -1;
+                F.eR = s ? -1 : e;
+                F.ordL = F.ordR = pack(e);
+                F.d = d;
+                F.kind = b == -1 ? 2 : 3;
+                F.mg = mgl;
+                mgl += 3LL * so;
+                F.outL = F.outR = gl;
+                fofsG[6LL * e + 2 * d + s] = gl;
+                gl += (long long)NV * so;
+                if (ns) {
+                    F.hL = F.hR = hl;
+                    fofsH[6LL * e + 2 * d + s] = hl;
+                    hl += (long long)NV * nkH(d) * so;
+                }
+                fl.push_back(F);
+                fw.push_back((so + 31) / 32);
+            }
+        }
+    {
+        std::vector<NsFace> sorted;
+        sorted.reserve(fl.size());
+        ctx->nsf_cls[0] = 0;
+        for (int w = 1; w <= 3; ++w) {
+            for (size_t i = 0; i < fl.size(); ++i)
+                if (fw[i] == w) sorted.push_back(fl[i]);
+            ctx->nsf_cls[w] = (int)sorted.size();
+        }
+        if (sorted.size() != fl.size()) return fail(ctx, DG_EINVAL, "set_orders: face with more than 96 mortar points");
+        fl.swap(sorted);
+    }
+    CK(upload(ctx->d_nsfaces, fl));
+    CK(upload(ctx->d_fofsG, fofsG));
+    CK(upload(ctx->d_fofsH, fofsH));
+    dg_status s;
+    if ((s = scratch_need(ctx, ctx->d_nsG, ctx->nsG_cap, gl, "flux-block")) != DG_OK) return s;
+    if (ns && (s = scratch_need(ctx, ctx->d_nsH, ctx->nsH_cap, hl, "BR1-block")) != DG_OK) return s;
+    if (ns && (s = scratch_need(ctx, ctx->d_grad, ctx->grad_len, 3 * L, "gradient")) != DG_OK) return s;
+    dfree(ctx->d_fg);
+    if (mgl > 0) {
+        CK(cudaMalloc(&ctx->d_fg, sizeof(double) * mgl));
+        FaceGeomParams G;
+        G.faces = ctx->d_nsfaces;
+        G.nfaces = (int)fl.size();
+        G.cm = curved_mesh(ctx);
+        G.tdd = ctx->d_tdd;
+        G.fg = ctx->d_fg;
+        G.ext = ext ? 1 : 0;
+        k_face_geom<<<(G.nfaces + 3) / 4, 128>>>(G);
+        ctx->launches++;
+        CK(cudaGetLastError());
+    }
+    // ---- volume metrics: full (10 per node, the dt / tau kernels) and compact (EXT) ----
+    if (ctx->met_len < 2 * L) {
+        dfree(ctx->d_met);
+        CK(cudaMalloc(&ctx->d_met, sizeof(double) * 2 * L));
+        ctx->met_len = 2 * L;
+    }
+    MetParams M;
+    M.cm = curved_mesh(ctx);
+    M.orders = ctx->d_orders;
+    M.off = ctx->d_off;
+    M.met = ctx->d_met;
+    M.tdd = ctx->d_tdd;
+    M.perm = ctx->d_eperm;
+    for (const SizeClass& c : ctx->ecls_all) {
+        M.pbase = c.base;
+        k_metrics<<<c.count, CBS, sizeof(double) * 16 * (size_t)c.maxn>>>(M);
+        ctx->launches++;
+    }
+    CK(cudaGetLastError());
+    if (ext) {
+        std::vector<long long> coff(E + 1, 0);
+        for (int e = 0; e < E; ++e) {
+            const int* N = &ctx->orders[3 * e];
+            coff[e + 1] = coff[e] + 6LL * (N[0] + 1) * (N[1] + 1);
+        }
+        CK(upload(ctx->d_coff, coff));
+        dfree(ctx->d_metc);
+        CK(cudaMalloc(&ctx->d_metc, sizeof(double) * coff[E]));
+        MetExtParams X;
+        X.cm = curved_mesh(ctx);
+        X.orders = ctx->d_orders;
+        X.coff = ctx->d_coff;
+        X.metc = ctx->d_metc;
+        X.tdd = ctx->d_tdd;
+        X.E = E;
+        k_metrics_ext<<<E, 128>>>(X);
+        ctx->launches++;
+        CK(cudaGetLastError());
+    }
+    CK(cudaDeviceSynchronize());
+    return DG_OK;
 }
 
 dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
@@ -850,7 +1112,6 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     for (size_t i = 0; i < elist.size(); ++i)
         for (int f = 0; f < 6; ++f) fos[6 * i + f] = fofs[6LL * elist[i] + f];
     CK(upload(ctx->d_fofs_slot, fos));
-    if (ctx->curved) CK(upload(ctx->d_fofs_el, fofs));
     for (Bucket& b : ctx->buckets) {
         const int o1 = b.ord & 255, o2 = (b.ord >> 8) & 255, o3 = (b.ord >> 16) & 255;
         if (ctx->occ_cache[o1][o2][o3] < 0) ctx->occ_cache[o1][o2][o3] = (signed char)ctx->rocc[o1][o2][o3]();
@@ -931,68 +1192,12 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     CK(upload(ctx->d_elist, elist));
     CK(upload(ctx->d_mortar, mort));
     CK(upload(ctx->d_moff, moff));
-    if (flen > 0) CK(dalloc(ctx->d_mortarG, (size_t)flen));
+    if (flen > 0 && !ctx->curved) CK(dalloc(ctx->d_mortarG, (size_t)flen));
     CK(dalloc(ctx->d_sel, 6 * (size_t)E));
     CK(dalloc(ctx->d_margin, (size_t)E));
     if (ctx->curved) {
-        const long long L = ctx->off[E];
-        if (ctx->met_len < 2 * L) {
-            dfree(ctx->d_met);
-            CK(cudaMalloc(&ctx->d_met, sizeof(double) * 2 * L));
-            ctx->met_len = 2 * L;
-        }
-        if (ctx->prm.physics == DG_NS && ctx->grad_len < 3 * L) {
-            dfree(ctx->d_grad);
-            CK(cudaMalloc(&ctx->d_grad, sizeof(double) * 3 * L));
-            ctx->grad_len = 3 * L;
-        }
-        if (ctx->prm.physics == DG_NS && mlen > 0 && ctx->mq_len < 3 * mlen) {
-            dfree(ctx->d_mortarGq);
-            CK(cudaMalloc(&ctx->d_mortarGq, sizeof(double) * 3 * mlen));
-            ctx->mq_len = 3 * mlen;
-        }
-        MetParams M;
-        M.cm = curved_mesh(ctx);
-        M.orders = ctx->d_orders;
-        M.off = ctx->d_off;
-        M.met = ctx->d_met;
-        M.tdd = ctx->d_tdd;
-        M.perm = ctx->d_eperm;
-        for (const SizeClass& c : ctx->ecls_all) {
-            M.pbase = c.base;
-            k_metrics<<<c.count, CBS, sizeof(double) * 16 * (size_t)c.maxn>>>(M);
-            ctx->launches++;
-        }
-        CK(cudaGetLastError());
-        // mortar metric at the mortar nodes, once per layout (k_mortar_c3 reads it)
-        dfree(ctx->d_mgeo);
-        dfree(ctx->d_mgoff);
-        if (ctx->nmortar > 0) {
-            static const int TA[3] = {1, 0, 0}, TB[3] = {2, 2, 1};
-            std::vector<long long> mgoff(ctx->nmortar);
-            long long glen = 0;
-            for (int i = 0; i < ctx->nmortar; ++i) {
-                const MortarItem& m = mort[i];
-                const int* a = &ctx->orders[3 * m.L];
-                const int* b = &ctx->orders[3 * m.R];
-                const int M1 = std::max(a[TA[m.d]], b[TA[m.d]]), M2 = std::max(a[TB[m.d]], b[TB[m.d]]);
-                mgoff[i] = glen;
-                glen += 3LL * (M1 + 1) * (M2 + 1);
-            }
-            CK(upload(ctx->d_mgoff, mgoff));
-            CK(cudaMalloc(&ctx->d_mgeo, sizeof(double) * glen));
-            CMortarParams G{};
-            G.tdd = ctx->d_tdd;
-            G.orders = ctx->d_orders;
-            G.off = ctx->d_off;
-            G.items = ctx->d_mortar;
-            G.cm = curved_mesh(ctx);
-            G.tab = ctx->d_tab;
-            k_mortar_geom<<<(ctx->nmortar + 3) / 4, 128>>>(G, ctx->d_mgeo, ctx->d_mgoff, ctx->nmortar);
-            ctx->launches++;
-            CK(cudaGetLastError());
-        }
-        CK(cudaDeviceSynchronize());
+        dg_status s = build_ns_plans(ctx);
+        if (s != DG_OK) return s;
     }
     ctx->have_orders = true;
     return DG_OK;
@@ -1035,23 +1240,74 @@ dg_status dg_node_coords(dg_ctx* ctx, double* X)
     return DG_OK;
 }
 
-// curved mortar faces (k_mortar_c3): mode 1 = BR1 gradient terms, mode 0 = fluxes
-static dg_status launch_mortar_curved(dg_ctx* ctx, const CMortarParams& M, cudaStream_t st)
+}  // extern "C"
+template <int MODE>
+static void launch_ns_faces(dg_ctx* ctx, const NsFaceParams& base, cudaStream_t st)
 {
-    CK(cudaMemsetAsync(ctx->d_flag + 4, 0, sizeof(int), st));  // work counter
-    const bool ns = ctx->prm.physics == DG_NS;
-    int* qc = ctx->d_flag + 4;
-    if (M.mode == 1)
-        k_mortar_c3<5, 15><<<std::min(ctx->nmortar, ctx->cm3_occ[2] * ctx->nsm), CM3_BS, CM3<5, 15>::smem, st>>>(
-            M, ctx->d_mfaces, ctx->nmortar, qc, ctx->d_mgeo, ctx->d_mgoff);
-    else if (ns)
-        k_mortar_c3<20, 5><<<std::min(ctx->nmortar, ctx->cm3_occ[1] * ctx->nsm), CM3_BS, CM3<20, 5>::smem, st>>>(
-            M, ctx->d_mfaces, ctx->nmortar, qc, ctx->d_mgeo, ctx->d_mgoff);
-    else
-        k_mortar_c3<5, 5><<<std::min(ctx->nmortar, ctx->cm3_occ[0] * ctx->nsm), CM3_BS, CM3<5, 5>::smem, st>>>(
-            M, ctx->d_mfaces, ctx->nmortar, qc, ctx->d_mgeo, ctx->d_mgoff);
-    ctx->launches++;
-    return DG_OK;
+    for (int w = 1; w <= 3; ++w) {
+        NsFaceParams P = base;
+        P.fbase = ctx->nsf_cls[w - 1];
+        P.fend = ctx->nsf_cls[w];
+        const int nf = P.fend - P.fbase;
+        if (nf <= 0) continue;
+        if (w == 1) k_ns_face<1, MODE><<<(nf + FaceCfg<1>::G - 1) / FaceCfg<1>::G, FaceCfg<1>::BS, FaceCfg<1>::smem, st>>>(P);
+        else if (w == 2) k_ns_face<2, MODE><<<(nf + FaceCfg<2>::G - 1) / FaceCfg<2>::G, FaceCfg<2>::BS, FaceCfg<2>::smem, st>>>(P);
+        else k_ns_face<3, MODE><<<(nf + FaceCfg<3>::G - 1) / FaceCfg<3>::G, FaceCfg<3>::BS, FaceCfg<3>::smem, st>>>(P);
+        ctx->launches++;
+    }
+}
+
+extern "C" {
+static NsElemParams ns_elem_params(dg_ctx* ctx, const double* q)
+{
+    NsElemParams P{};
+    P.items = ctx->d_nsitems;
+    P.elist = ctx->d_nselist;
+    P.orders = ctx->d_orders;
+    P.off = ctx->d_off;
+    P.met = ctx->d_met;
+    P.metc = ctx->d_metc;
+    P.coff = ctx->d_coff;
+    P.q = q;
+    P.ph = phys_dev(ctx->prm);
+    return P;
+}
+
+static NsFaceParams ns_face_params(dg_ctx* ctx, const double* q)
+{
+    NsFaceParams F{};
+    F.faces = ctx->d_nsfaces;
+    F.q = q;
+    F.grad = ctx->d_grad;
+    F.fg = ctx->d_fg;
+    F.tab = ctx->d_tab;
+    F.ph = phys_dev(ctx->prm);
+    F.ext = ctx->extruded ? 1 : 0;
+    return F;
+}
+
+// BR1 gradient of the owned elements into d_grad (eq DGSEMsystem:2):
+// face terms H (non-isolated), then the element kernel.
+static dg_status launch_ns_gradient(dg_ctx* ctx, int variant, const double* q, cudaStream_t st)
+{
+    const bool noniso = variant == DG_NONISOLATED;
+    if (noniso) {
+        NsFaceParams F = ns_face_params(ctx, q);
+        F.out = ctx->d_nsH;
+        launch_ns_faces<MODE_QHAT>(ctx, F, st);
+    }
+    NsElemParams P = ns_elem_params(ctx, q);
+    P.gout = ctx->d_grad;
+    P.blk = ctx->d_nsH;
+    P.fofs = noniso ? ctx->d_fofsH : nullptr;
+    for (const SizeClass& c : ctx->nscls) {
+        P.ibase = c.base;
+        const size_t sm = sizeof(double) * 20 * (size_t)c.maxn;
+        if (ctx->extruded) k_ns_grad<true><<<c.count, NS_BS, sm, st>>>(P);
+        else k_ns_grad<false><<<c.count, NS_BS, sm, st>>>(P);
+        ctx->launches++;
+    }
+    return check_stream_error(ctx, "k_ns_grad launch");
 }
 
 static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* q, double* out, double* g,
@@ -1059,76 +1315,38 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
                                         unsigned long long* lam_max, int flags = 0)
 {
     const bool ns = ctx->prm.physics == DG_NS;
-    CurvedParams P{};
-    P.perm = ctx->d_eperm;
-    P.q = q;
+    const bool noniso = variant == DG_NONISOLATED;
+    if (ns && !(flags & 1)) {  // flag 1: the caller already formed the gradient (multi-rank halo)
+        dg_status s = launch_ns_gradient(ctx, variant, q, st);
+        if (s != DG_OK) return s;
+    }
+    if (noniso) {
+        NsFaceParams F = ns_face_params(ctx, q);
+        F.out = ctx->d_nsG;
+        if (ns) launch_ns_faces<MODE_FLUX_NS>(ctx, F, st);
+        else launch_ns_faces<MODE_FLUX_EULER>(ctx, F, st);
+    }
+    NsElemParams P = ns_elem_params(ctx, q);
+    P.grad = ctx->d_grad;
+    P.blk = ctx->d_nsG;
+    P.fofs = noniso ? ctx->d_fofsG : nullptr;
+    P.out = out;
     P.g = g;
     P.dt = dt;
     P.rkA = A;
     P.rkB = B;
-    P.variant = variant;
-    P.orders = ctx->d_orders;
-    P.off = ctx->d_off;
-    P.finfo = ctx->d_finfo;
-    P.met = ctx->d_met;
-    P.grad = ctx->d_grad;
-    P.tab = ctx->d_tab;
-    P.ph = phys_dev(ctx->prm);
-    P.flag = ctx->d_flag;
-    CMortarParams M{};
-    M.tdd = ctx->d_tdd;
-    M.q = q;
-    M.grad = ctx->d_grad;
-    M.orders = ctx->d_orders;
-    M.off = ctx->d_off;
-    M.items = ctx->d_mortar;
-    M.moff = ctx->d_moff;
-    M.cm = curved_mesh(ctx);
-    M.tab = ctx->d_tab;
-    M.ph = phys_dev(ctx->prm);
-    const bool mort = variant == DG_NONISOLATED && ctx->nmortar > 0;
-    if (ns && !(flags & 1)) {  // BR1 gradient pass (eq DGSEMsystem:2); flag 1: caller already did it
-        if (mort) {
-            M.mode = 1;
-            M.mortarG = ctx->d_mortarGq;
-            dg_status s = launch_mortar_curved(ctx, M, st);
-            if (s != DG_OK) return s;
-        }
-        P.mode = 0;
-        P.out = ctx->d_grad;
-        P.mortarG = ctx->d_mortarGq;
-        for (const SizeClass& c : ctx->ecls_own) {
-            P.pbase = c.base;
-            k_grad<<<c.count, CBS, sizeof(double) * 14 * (size_t)c.maxn, st>>>(P);
-            ctx->launches++;
-        }
-    }
-    if (mort) {
-        M.mode = 0;
-        M.mortarG = ctx->d_mortarG;
-        dg_status s = launch_mortar_curved(ctx, M, st);
-        if (s != DG_OK) return s;
-    }
     P.mode = mode;
-    P.out = out;
-    P.mortarG = ctx->d_mortarG;
     P.lam_max = lam_max;
-    P.fofs = nullptr;
-    if (variant == DG_NONISOLATED && ctx->nfaces > 0 && ctx->d_fofs_el) {  // conforming faces once per point
-        CFaceParams FP;
-        FP.q = q;
-        FP.grad = ctx->d_grad;
-        FP.met = ctx->d_met;
-        FP.faces = ctx->d_faces;
-        FP.G = ctx->d_mortarG;
-        FP.ph = phys_dev(ctx->prm);
-        k_face_curved<<<(ctx->nfaces + 3) / 4, 128, 0, st>>>(FP, ctx->nfaces);
-        ctx->launches++;
-        P.fofs = ctx->d_fofs_el;
-    }
-    for (const SizeClass& c : ctx->ecls_own) {
-        P.pbase = c.base;
-        k_res_curved<<<c.count, CBS, sizeof(double) * 25 * (size_t)c.maxn, st>>>(P);
+    for (const SizeClass& c : ctx->nscls) {
+        P.ibase = c.base;
+        const size_t sm = sizeof(double) * 20 * (size_t)c.maxn;
+        if (ctx->extruded) {
+            if (ns) k_ns_res<true, true><<<c.count, NS_BS, sm, st>>>(P);
+            else k_ns_res<true, false><<<c.count, NS_BS, sm, st>>>(P);
+        } else {
+            if (ns) k_ns_res<false, true><<<c.count, NS_BS, sm, st>>>(P);
+            else k_ns_res<false, false><<<c.count, NS_BS, sm, st>>>(P);
+        }
         ctx->launches++;
     }
     return check_stream_error(ctx, "curved residual launch");
@@ -1521,45 +1739,7 @@ dg_status dg_gradient(dg_ctx* ctx, int variant, const double* q_dev, void* strea
     if (!ctx || !q_dev) return DG_EINVAL;
     if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "gradient: orders not set");
     if (ctx->prm.physics != DG_NS || !ctx->curved) return fail(ctx, DG_EUNSUPPORTED, "gradient: NS on the curved path only");
-    cudaStream_t st = (cudaStream_t)stream;
-    CurvedParams P{};
-    P.perm = ctx->d_eperm;
-    P.q = q_dev;
-    P.variant = variant;
-    P.orders = ctx->d_orders;
-    P.off = ctx->d_off;
-    P.finfo = ctx->d_finfo;
-    P.met = ctx->d_met;
-    P.grad = ctx->d_grad;
-    P.tab = ctx->d_tab;
-    P.ph = phys_dev(ctx->prm);
-    P.flag = ctx->d_flag;
-    if (variant == DG_NONISOLATED && ctx->nmortar > 0) {
-        CMortarParams M{};
-        M.tdd = ctx->d_tdd;
-        M.q = q_dev;
-        M.grad = ctx->d_grad;
-        M.orders = ctx->d_orders;
-        M.off = ctx->d_off;
-        M.items = ctx->d_mortar;
-        M.moff = ctx->d_moff;
-        M.cm = curved_mesh(ctx);
-        M.tab = ctx->d_tab;
-        M.ph = phys_dev(ctx->prm);
-        M.mode = 1;
-        M.mortarG = ctx->d_mortarGq;
-        dg_status s = launch_mortar_curved(ctx, M, st);
-        if (s != DG_OK) return s;
-    }
-    P.mode = 0;
-    P.out = ctx->d_grad;
-    P.mortarG = ctx->d_mortarGq;
-    for (const SizeClass& c : ctx->ecls_own) {
-        P.pbase = c.base;
-        k_grad<<<c.count, CBS, sizeof(double) * 14 * (size_t)c.maxn, st>>>(P);
-        ctx->launches++;
-    }
-    return check_stream_error(ctx, "k_grad launch");
+    return launch_ns_gradient(ctx, variant, q_dev, (cudaStream_t)stream);
 }
 
 double* dg_gradient_buffer(dg_ctx* ctx) { return ctx ? ctx->d_grad : nullptr; }
