@@ -201,6 +201,7 @@ struct dg_ctx {
     NsItem* d_nsitems = nullptr;
     int* d_nselist = nullptr;
     std::vector<SizeClass> nscls;  // item classes by node count: [base, base + count), max nodes
+    std::vector<int> nscls_hw;     // per class: max H face-block words of an item
     NsFace* d_nsfaces = nullptr;
     int nsf_cls[4] = {0, 0, 0, 0};  // faces of W = 1..3 warps: [nsf_cls[W-1], nsf_cls[W])
     double* d_fg = nullptr;         // face metrics at the mortar points
@@ -407,7 +408,8 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
                 return s;
             }
         }
-        if ((s = cuda_check(ctx, res_copy_constants(&t), "constants")) != DG_OK) {
+        if ((s = cuda_check(ctx, res_copy_constants(&t), "constants")) != DG_OK ||
+            (s = cuda_check(ctx, ns_copy_constants(), "constants")) != DG_OK) {
             dg_destroy(ctx);
             return s;
         }
@@ -447,9 +449,11 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         cudaFuncSetAttribute(k_tau_curved<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
         ctx->smem_limit = limc;
         // curved residual path (ns.cuh): element kernels up to 20 x 729 doubles, face kernels per W
-        const int lns = std::min(limc, 20 * 729 * 8);
-        cudaFuncSetAttribute(k_ns_grad<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
-        cudaFuncSetAttribute(k_ns_grad<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
+        const int lns = limc;
+        cudaFuncSetAttribute(k_ns_grad<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
+        cudaFuncSetAttribute(k_ns_grad<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
+        cudaFuncSetAttribute(k_ns_grad<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
+        cudaFuncSetAttribute(k_ns_grad<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
         cudaFuncSetAttribute(k_ns_res<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
         cudaFuncSetAttribute(k_ns_res<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
         cudaFuncSetAttribute(k_ns_res<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
@@ -719,16 +723,29 @@ static dg_status build_ns_plans(dg_ctx* ctx)
         std::vector<NsItem> sorted;
         sorted.reserve(items.size());
         ctx->nscls.clear();
+        ctx->nscls_hw.clear();
+        auto hwords = [&](const NsItem& it) {  // H face-block words of the item (ns.cuh hblk_words)
+            const int N[3] = {it.ord & 255, (it.ord >> 8) & 255, (it.ord >> 16) & 255};
+            const int nl[3] = {(N[1] + 1) * (N[2] + 1), (N[0] + 1) * (N[2] + 1), (N[0] + 1) * (N[1] + 1)};
+            int w = 0;
+            for (int d = 0; d < 3; ++d) w += 2 * NV * (ext ? ext_nk(d) : 3) * nl[d];
+            return it.count * w;
+        };
         for (int c = 0; c < 3; ++c) {
             const int lo = c ? edge[c - 1] : 0;
             SizeClass cl{(int)sorted.size(), 0, 0};
+            int hw = 0;
             for (const NsItem& it : items)
                 if (it.nodes > lo && it.nodes <= edge[c]) {
                     sorted.push_back(it);
                     cl.count++;
                     cl.maxn = std::max(cl.maxn, it.nodes);
+                    hw = std::max(hw, hwords(it));
                 }
-            if (cl.count) ctx->nscls.push_back(cl);
+            if (cl.count) {
+                ctx->nscls.push_back(cl);
+                ctx->nscls_hw.push_back(ns ? hw : 0);
+            }
         }
         CK(upload(ctx->d_nsitems, sorted));
         CK(upload(ctx->d_nselist, el));
@@ -1302,9 +1319,17 @@ static dg_status launch_ns_gradient(dg_ctx* ctx, int variant, const double* q, c
     P.fofs = noniso ? ctx->d_fofsH : nullptr;
     for (const SizeClass& c : ctx->nscls) {
         P.ibase = c.base;
-        const size_t sm = sizeof(double) * 20 * (size_t)c.maxn;
-        if (ctx->extruded) k_ns_grad<true><<<c.count, NS_BS, sm, st>>>(P);
-        else k_ns_grad<false><<<c.count, NS_BS, sm, st>>>(P);
+        const int hw = ctx->nscls_hw[&c - &ctx->nscls[0]];
+        size_t sm = sizeof(double) * ns_grad_smem_doubles(ctx->extruded, c.maxn, hw, 2);
+        const bool two = sm <= (size_t)ctx->smem_limit;
+        if (!two) sm = sizeof(double) * ns_grad_smem_doubles(ctx->extruded, c.maxn, hw, 1);
+        if (sm > (size_t)ctx->smem_limit) return fail(ctx, DG_EINVAL, "k_ns_grad: element item exceeds shared memory");
+        int occ = 1;
+        auto kern = ctx->extruded ? (two ? k_ns_grad<true, true> : k_ns_grad<true, false>)
+                                  : (two ? k_ns_grad<false, true> : k_ns_grad<false, false>);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NS_BS, sm);
+        const int grid = std::min(c.count, std::max(1, occ) * ctx->nsm);
+        kern<<<grid, NS_BS, sm, st>>>(P, c.count, c.maxn, hw);
         ctx->launches++;
     }
     return check_stream_error(ctx, "k_ns_grad launch");

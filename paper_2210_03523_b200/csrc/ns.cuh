@@ -271,34 +271,54 @@ __global__ void __launch_bounds__(128) k_metrics_ext(MetExtParams P)
 }
 
 // ---------------------------------------------------------------------------
-// metric access in the element kernels
+// small helpers
 // ---------------------------------------------------------------------------
+
+// x / d for 0 <= x < 2^20, 1 <= d < 4096: umulhi(x, ceil(2^32 / d)) (error
+// < x 2^-32 < 1/d, so the floor is exact); d = 1 is passed through.  The
+// multipliers of d < NS_FDIV come from a constant table (no division at all).
+constexpr int NS_FDIV = 1024;
+static __constant__ unsigned c_fdiv[NS_FDIV];
+struct FDiv {
+    unsigned m;
+    bool one;
+    __device__ __forceinline__ void init(unsigned d)
+    {
+        one = d == 1;
+        m = d < NS_FDIV ? c_fdiv[d] : (one ? 0u : 0xffffffffu / d + 1u);
+    }
+    __device__ __forceinline__ int div(int x) const { return one ? x : (int)__umulhi((unsigned)x, m); }
+};
+
+static inline cudaError_t ns_copy_constants()
+{
+    static unsigned h[NS_FDIV];
+    for (unsigned d = 2; d < NS_FDIV; ++d) h[d] = 0xffffffffu / d + 1u;
+    h[0] = h[1] = 0;
+    return cudaMemcpyToSymbol(c_fdiv, h, sizeof(h));
+}
+
+// metric terms of one element: EXT 6 per (i, j) column, else 10 per node
 template <bool EXT>
 struct Met {
-    const double* p;  // EXT: the element's 6 x nc block; else its 10 x n block
-    int n, nc, n12;
-    __device__ __forceinline__ void init(const NsElemParams& P, int e, long long o, int n_, int n1, int n2)
+    const double* p;
+    int n, n12;
+    __device__ __forceinline__ void init(const NsElemParams& P, int e, long long o, int n_, int n12_)
     {
         n = n_;
-        n12 = n1 * n2;
-        if (EXT) p = P.metc + P.coff[e];
-        else p = P.met + 2 * o;
+        n12 = n12_;
+        p = EXT ? P.metc + P.coff[e] : P.met + 2 * o;
     }
-    // (Ja^d)_k at node t
-    __device__ __forceinline__ double ja(int d, int k, int t) const
+    // (Ja^d)_k at node t (column c = t mod n1 n2, EXT)
+    __device__ __forceinline__ double ja(int d, int k, int t, int c) const
     {
         if (EXT) {
-            const int c = t % n12;
             if (d < 2) return k == 2 ? 0.0 : __ldg(p + (2 * d + k) * n12 + c);
             return k == 2 ? __ldg(p + 4 * n12 + c) : 0.0;
         }
         return __ldg(p + (3 * d + k) * n + t);
     }
-    __device__ __forceinline__ double J(int t) const
-    {
-        if (EXT) return __ldg(p + 5 * n12 + t % n12);
-        return __ldg(p + 9 * n + t);
-    }
+    __device__ __forceinline__ double J(int t, int c) const { return EXT ? __ldg(p + 5 * n12 + c) : __ldg(p + 9 * n + t); }
 };
 
 // ---------------------------------------------------------------------------
@@ -343,113 +363,383 @@ __device__ __forceinline__ void dline_reg(const double (&v)[L], double (&out)[L]
     }
 }
 
-__device__ __forceinline__ void line_geom(int d, int line, int n1, int n2, int& base, int& stride)
+// per-item constants of the element kernels (scalars: no local-memory arrays)
+struct ItemGeo {
+    int n1, n2, n3, n, n12, cnt, NN;
+    int nl0, nl1, nl2;
+    FDiv dn, dn1, dn2, dn12, dnl0, dnl1, dnl2;
+    __device__ __forceinline__ void init(int ord, int count)
+    {
+        int N1, N2, N3;
+        unpack_ord(ord, N1, N2, N3);
+        n1 = N1 + 1;
+        n2 = N2 + 1;
+        n3 = N3 + 1;
+        n12 = n1 * n2;
+        n = n12 * n3;
+        cnt = count;
+        NN = cnt * n;
+        nl0 = n2 * n3;
+        nl1 = n1 * n3;
+        nl2 = n12;
+        dn.init(n);
+        dn1.init(n1);
+        dn2.init(n2);
+        dn12.init(n12);
+        dnl0.init(nl0);
+        dnl1.init(nl1);
+        dnl2.init(nl2);
+    }
+    __device__ __forceinline__ int nl(int d) const { return d == 0 ? nl0 : (d == 1 ? nl1 : nl2); }
+    __device__ __forceinline__ int nd(int d) const { return d == 0 ? n1 : (d == 1 ? n2 : n3); }
+    __device__ __forceinline__ int div_nl(int d, int x) const { return d == 0 ? dnl0.div(x) : (d == 1 ? dnl1.div(x) : dnl2.div(x)); }
+    // line `line` of direction d: first node, node stride, first column, column stride
+    __device__ __forceinline__ void line(int d, int line, int& base, int& stride, int& cb, int& cs) const
+    {
+        if (d == 0) {  // line = j + n2 k
+            base = n1 * line;
+            stride = 1;
+            const int k = dn2.div(line);
+            cb = n1 * (line - n2 * k);
+            cs = 1;
+        } else if (d == 1) {  // line = i + n1 k
+            const int k = dn1.div(line);
+            const int i = line - n1 * k;
+            base = i + n12 * k;
+            stride = n1;
+            cb = i;
+            cs = n1;
+        } else {  // line = i + n1 j
+            base = line;
+            stride = n12;
+            cb = line;
+            cs = 0;
+        }
+    }
+};
+
+__device__ __forceinline__ int nk_of(bool ext, int d) { return ext ? ext_nk(d) : 3; }
+
+// split (kk, rest) = (r mod nk, r / nk) for nk in {1, 2, 3}
+__device__ __forceinline__ void split_nk(int nk, int r, int& kk, int& rest)
 {
-    if (d == 0) { base = n1 * line; stride = 1; }                                    // line = j + n2 k
-    else if (d == 1) { base = line % n1 + n1 * n2 * (line / n1); stride = n1; }      // line = i + n1 k
-    else { base = line; stride = n1 * n2; }                                           // line = i + n1 j
+    if (nk == 1) { kk = 0; rest = r; }
+    else if (nk == 2) { kk = r & 1; rest = r >> 1; }
+    else { rest = r / 3; kk = r - 3 * rest; }
 }
 
 // ---------------------------------------------------------------------------
-// k_ns_grad: BR1 gradient, one CTA per item
+// k_ns_grad: BR1 gradient, one CTA per item, one thread per node.
+//   J g_k = sum_d [ sum_m D^d_{a m} (Ja^d_k q)_m  + lifting at a = 0 / N_d ],
+// the three directions' sums accumulated in registers; the item's states,
+// metric terms and D rows are staged in shared memory once.
 // ---------------------------------------------------------------------------
-template <int L, bool EXT>
-__device__ __forceinline__ void grad_line(const NsElemParams& P, const Met<EXT>& M, const double* Qs, double* GA, int n,
-                                          int d, int k, int kk, int nk, int line, int base, int stride, bool first,
-                                          long long fm, long long fp, int nf)
+
+// shared-memory words of the gradient kernel for an item class: two stages of
+// Q (5 per node) + metrics (EXT: <= 6 per node; else 10 per node) + D rows
+// (3 x 81), and one buffer of the item's H face blocks (maxHW words)
+__host__ __device__ inline size_t ns_grad_smem_doubles(bool ext, int maxnodes, int maxHW, int stages = 2)
 {
-    double ja[L];
+    return stages * ((size_t)maxnodes * (5 + (ext ? 6 : 10)) + 3 * NP * NP) + (size_t)maxHW;
+}
+
+// One direction's volume sum at node t for the NK metric components of that
+// direction: acc[kk][v] += sum_m D_{a m} Ja_k(m) q_v(m) (line length L).
+template <int L, int NK>
+__device__ __forceinline__ void grad_dir(const double* __restrict__ Dr, const double* __restrict__ Qs, int n, int tb,
+                                         int stride, const double* const* ja, int cb, int cs, double (&acc)[NK][NV])
+{
+    double w[L];
 #pragma unroll
-    for (int m = 0; m < L; ++m) ja[m] = M.ja(d, k, base + m * stride);
-    const bool lift = fm >= 0;
-#pragma unroll 1
-    for (int v = 0; v < NV; ++v) {
-        double pv[L], out[L];
+    for (int m = 0; m < L; ++m) w[m] = Dr[m];
 #pragma unroll
-        for (int m = 0; m < L; ++m) pv[m] = ja[m] * Qs[v * n + base + m * stride];
-        double gm = 0.0, gp = 0.0;
-        if (lift) {
-            gm = __ldg(P.blk + fm + (long long)(kk * NV + v) * nf + line);
-            gp = __ldg(P.blk + fp + (long long)(kk * NV + v) * nf + line);
-        }
-        dline_reg<L>(pv, out, lift, gm, gp);
-        double* acc = GA + (k * NV + v) * n + base;
-        if (first) {
+    for (int m = 0; m < L; ++m) {
+        const int tm = tb + m * stride;
+        double qv[NV];
 #pragma unroll
-            for (int m = 0; m < L; ++m) acc[m * stride] = out[m];
-        } else {
+        for (int v = 0; v < NV; ++v) qv[v] = Qs[v * n + tm];
 #pragma unroll
-            for (int m = 0; m < L; ++m) acc[m * stride] += out[m];
+        for (int kk = 0; kk < NK; ++kk) {
+            const double wj = w[m] * ja[kk][cb + m * cs];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) acc[kk][v] = fma(wj, qv[v], acc[kk][v]);
         }
     }
 }
+
+template <int NK>
+__device__ __forceinline__ void grad_dir_sw(int L, const double* Dr, const double* Qs, int n, int tb, int stride,
+                                            const double* const* ja, int cb, int cs, double (&acc)[NK][NV])
+{
+    switch (L) {
+        case 2: grad_dir<2, NK>(Dr, Qs, n, tb, stride, ja, cb, cs, acc); break;
+        case 3: grad_dir<3, NK>(Dr, Qs, n, tb, stride, ja, cb, cs, acc); break;
+        case 4: grad_dir<4, NK>(Dr, Qs, n, tb, stride, ja, cb, cs, acc); break;
+        case 5: grad_dir<5, NK>(Dr, Qs, n, tb, stride, ja, cb, cs, acc); break;
+        case 6: grad_dir<6, NK>(Dr, Qs, n, tb, stride, ja, cb, cs, acc); break;
+        case 7: grad_dir<7, NK>(Dr, Qs, n, tb, stride, ja, cb, cs, acc); break;
+        case 8: grad_dir<8, NK>(Dr, Qs, n, tb, stride, ja, cb, cs, acc); break;
+        default: grad_dir<9, NK>(Dr, Qs, n, tb, stride, ja, cb, cs, acc); break;
+    }
+}
+
+// Per-item metadata of the persistent element kernels (one copy per stage).
+struct NsMeta {
+    int cnt, ord;
+    int hw;                         // H words per slot (face blocks back to back)
+    int e[NS_MAXSLOTS];
+    long long off[NS_MAXSLOTS];
+    long long mo[NS_MAXSLOTS];     // metric block: EXT coff[e], else 2 x off
+    long long fo[NS_MAXSLOTS][6];  // face blocks (-1: isolated)
+};
+
+// volume part of J g at node idx of the item (stage Q | metrics | D rows)
+template <bool EXT>
+__device__ __forceinline__ void grad_node_volume(const ItemGeo& I, const double* Q, int maxNN, int idx, double (&g)[3][NV])
+{
+    const int n = I.n, n1 = I.n1, n2 = I.n2, n3 = I.n3, n12 = I.n12;
+    const int MW = EXT ? 6 * n12 : 10 * n;
+    const double* Ms = Q + NV * maxNN;
+    const double* Ds = Ms + (EXT ? 6 : 10) * maxNN;
+    const int slot = I.dn.div(idx), t = idx - slot * n;
+    const int k3 = I.dn12.div(t), c = t - n12 * k3;
+    const int j = I.dn1.div(c), i = c - n1 * j;
+    const double* Qs = Q + slot * NV * n;
+    const double* Me = Ms + slot * MW;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) g[k][v] = 0.0;
+    if (EXT) {
+        // d = 0: Ja^1 = (M0, M1, 0) at column m + n1 j; d = 1: Ja^2 = (M2, M3, 0)
+        // at i + n1 m; d = 2: Ja^3 = (0, 0, M4) at column c
+        {
+            const double* ja[2] = {Me, Me + n12};
+            double acc[2][NV] = {};
+            grad_dir_sw<2>(n1, Ds + i * n1, Qs, n, t - i, 1, ja, n1 * j, 1, acc);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) { g[0][v] += acc[0][v]; g[1][v] += acc[1][v]; }
+        }
+        {
+            const double* ja[2] = {Me + 2 * n12, Me + 3 * n12};
+            double acc[2][NV] = {};
+            grad_dir_sw<2>(n2, Ds + NP * NP + j * n2, Qs, n, t - n1 * j, n1, ja, i, n1, acc);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) { g[0][v] += acc[0][v]; g[1][v] += acc[1][v]; }
+        }
+        {
+            const double* ja[1] = {Me + 4 * n12};
+            double acc[1][NV] = {};
+            grad_dir_sw<1>(n3, Ds + 2 * NP * NP + k3 * n3, Qs, n, c, n12, ja, c, 0, acc);
+#pragma unroll
+            for (int v = 0; v < NV; ++v) g[2][v] += acc[0][v];
+        }
+    } else {
+        const int tb[3] = {t - i, t - n1 * j, c};
+        const int ai[3] = {i, j, k3};
+        const int stv[3] = {1, n1, n12};
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const double* ja[3] = {Me + (3 * d) * n, Me + (3 * d + 1) * n, Me + (3 * d + 2) * n};
+            double acc[3][NV] = {};
+            const int L = d == 0 ? n1 : (d == 1 ? n2 : n3);
+            grad_dir_sw<3>(L, Ds + d * NP * NP + ai[d] * L, Qs, n, tb[d], stv[d], ja, tb[d], stv[d], acc);
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+#pragma unroll
+                for (int v = 0; v < NV; ++v) g[k][v] += acc[k][v];
+        }
+    }
+}
+
+// lifting (H - q Ja^d_k)/w of the faces through node idx (H staged in Hs),
+// then g = (J g)/J written [k][v][node] at 3 x offset
+template <bool EXT>
+__device__ __forceinline__ void grad_node_finish(const NsElemParams& P, const NsMeta& M, const ItemGeo& I, const double* Q,
+                                                 int maxNN, const double* Hs, int idx, double (&g)[3][NV])
+{
+    const int n = I.n, n1 = I.n1, n2 = I.n2, n3 = I.n3, n12 = I.n12;
+    const int MW = EXT ? 6 * n12 : 10 * n;
+    const double* Me = Q + NV * maxNN + I.dn.div(idx) * MW;
+    const int slot = I.dn.div(idx), t = idx - slot * n;
+    const int k3 = I.dn12.div(t), c = t - n12 * k3;
+    const int j = I.dn1.div(c), i = c - n1 * j;
+    const double* Qs = Q + slot * NV * n;
+    if (P.fofs) {
+        const int ai[3] = {i, j, k3};
+        const int pt[3] = {j + n2 * k3, i + n1 * k3, c};
+        const double* Hsl = Hs + slot * M.hw;
+        int fb = 0;  // offset of face (d, s) in the slot's H area
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const int L = d == 0 ? n1 : (d == 1 ? n2 : n3);
+            const int nk = EXT ? ext_nk(d) : 3;
+            const int nf = d == 0 ? I.nl0 : (d == 1 ? I.nl1 : I.nl2);
+            const int hb = NV * nk * nf;
+#pragma unroll
+            for (int sd = 0; sd < 2; ++sd) {
+                if (ai[d] == (sd ? L - 1 : 0)) {
+                    const double CL = (sd ? 0.5 : -0.5) * (L - 1) * L;  // +-1/w_0
+                    const double* H = Hsl + fb + sd * hb + pt[d];
+                    for (int kk = 0; kk < nk; ++kk) {
+                        const int k = EXT ? ext_k(d, kk) : kk;
+                        double jo;
+                        if (EXT) jo = d < 2 ? Me[(2 * d + k) * n12 + c] : Me[4 * n12 + c];
+                        else jo = Me[(3 * d + k) * n + t];
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) g[k][v] += CL * (H[(kk * NV + v) * nf] - jo * Qs[v * n + t]);
+                    }
+                }
+            }
+            fb += 2 * hb;
+        }
+    }
+    const double iJ = 1.0 / (EXT ? Me[5 * n12 + c] : Me[9 * n + t]);
+    double* o = P.gout + 3 * M.off[slot] + t;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+        for (int v = 0; v < NV; ++v) o[(long long)(k * NV + v) * n] = g[k][v] * iJ;
+}
+
+
+// face-block words of face (d, s) of an element (nk metric components of
+// direction d), and the offset of face f inside the slot's H area
+__device__ __forceinline__ int hblk_words(bool ext, int d, int nl) { return NV * (ext ? ext_nk(d) : 3) * nl; }
 
 template <bool EXT>
-__global__ void __launch_bounds__(NS_BS) k_ns_grad(NsElemParams P)
+__device__ __forceinline__ void ns_load_meta(const NsElemParams& P, int item, NsMeta& M)
+{
+    const NsItem it = P.items[P.ibase + item];
+    if (threadIdx.x == 0) {
+        M.cnt = it.count;
+        M.ord = it.ord;
+        int N1, N2, N3;
+        unpack_ord(it.ord, N1, N2, N3);
+        const int n1 = N1 + 1, n2 = N2 + 1, n3 = N3 + 1;
+        M.hw = 2 * (hblk_words(EXT, 0, n2 * n3) + hblk_words(EXT, 1, n1 * n3) + hblk_words(EXT, 2, n1 * n2));
+    }
+    if (threadIdx.x < it.count) {
+        const int e = P.elist[it.start + threadIdx.x];
+        const long long o = P.off[e];
+        M.e[threadIdx.x] = e;
+        M.off[threadIdx.x] = o;
+        M.mo[threadIdx.x] = EXT ? P.coff[e] : 2 * o;
+#pragma unroll
+        for (int f = 0; f < 6; ++f) M.fo[threadIdx.x][f] = P.fofs ? P.fofs[6LL * e + f] : -1;
+    }
+}
+
+// stage layout of the gradient kernel: Q [slot][v][node] | metrics [slot][MW] | D rows [3][81]
+template <bool EXT>
+__device__ __forceinline__ void grad_issue(const NsElemParams& P, const NsMeta& M, double* st, int maxNN)
+{
+    ItemGeo I;
+    I.init(M.ord, M.cnt);
+    const int n = I.n;
+    const int MW = EXT ? 6 * I.n12 : 10 * n;
+    double* Q = st;
+    double* Ms = st + NV * maxNN;
+    double* Ds = Ms + (EXT ? 6 : 10) * maxNN;
+    FDiv d5n, dmw;
+    d5n.init(NV * n);
+    dmw.init(MW);
+    for (int idx = threadIdx.x; idx < NV * I.NN; idx += NS_BS) {
+        const int slot = d5n.div(idx);
+        cp_async8(Q + idx, P.q + M.off[slot] + (idx - slot * NV * n));
+    }
+    const double* msrc = EXT ? P.metc : P.met;
+    for (int idx = threadIdx.x; idx < I.cnt * MW; idx += NS_BS) {
+        const int slot = dmw.div(idx);
+        cp_async8(Ms + idx, msrc + M.mo[slot] + (idx - slot * MW));
+    }
+    for (int w = threadIdx.x; w < 3 * NP * NP; w += NS_BS) {
+        const int d = w / (NP * NP), r = w - d * NP * NP;
+        const int L = d == 0 ? I.n1 : (d == 1 ? I.n2 : I.n3);
+        if (r < L * L) Ds[w] = c_D[(L - 1) * NP * NP + r];
+    }
+}
+
+// the H face blocks of the item's elements into Hs: [slot][f][kk][v][pt]
+template <bool EXT>
+__device__ __forceinline__ void grad_issue_h(const NsElemParams& P, const NsMeta& M, double* Hs)
+{
+    int N1, N2, N3;
+    unpack_ord(M.ord, N1, N2, N3);
+    const int nl[3] = {(N2 + 1) * (N3 + 1), (N1 + 1) * (N3 + 1), (N1 + 1) * (N2 + 1)};
+    const int hb0 = hblk_words(EXT, 0, nl[0]), hb1 = hblk_words(EXT, 1, nl[1]), hb2 = hblk_words(EXT, 2, nl[2]);
+    const int fb[7] = {0, hb0, 2 * hb0, 2 * hb0 + hb1, 2 * hb0 + 2 * hb1, 2 * hb0 + 2 * hb1 + hb2, M.hw};
+    FDiv dhw;
+    dhw.init(M.hw);
+    for (int idx = threadIdx.x; idx < M.cnt * M.hw; idx += NS_BS) {
+        const int slot = dhw.div(idx), r = idx - slot * M.hw;
+        int f = 0;
+#pragma unroll
+        for (int q = 1; q < 6; ++q) f += r >= fb[q];
+        cp_async8(Hs + idx, P.blk + M.fo[slot][f] + (r - fb[f]));
+    }
+}
+
+// Persistent: CTA b takes items b, b + grid, ...; the states and metric terms
+// of the next item are copied (cp.async) into the other shared stage while
+// the current one is computed.
+// The item's H face blocks are copied into one buffer at the start of its
+// compute and waited for only before the lifting (overlapping the volume sums).
+// TWO = false (large items whose two stages do not fit): one stage, no prefetch.
+template <bool EXT, bool TWO>
+__global__ void __launch_bounds__(NS_BS, 2) k_ns_grad(NsElemParams P, int nitems, int maxNN, int maxHW)
 {
     extern __shared__ __align__(16) double sm[];
-    __shared__ long long s_off[NS_MAXSLOTS];
-    __shared__ int s_e[NS_MAXSLOTS];
-    const NsItem it = P.items[P.ibase + blockIdx.x];
-    int N1, N2, N3;
-    unpack_ord(it.ord, N1, N2, N3);
-    const int n1 = N1 + 1, n2 = N2 + 1, n3 = N3 + 1, n = n1 * n2 * n3;
-    const int cnt = it.count, NN = cnt * n;
-    if (threadIdx.x < cnt) {
-        const int e = P.elist[it.start + threadIdx.x];
-        s_e[threadIdx.x] = e;
-        s_off[threadIdx.x] = P.off[e];
-    }
+    __shared__ NsMeta meta[2];
+    const int SW = (NV + (EXT ? 6 : 10)) * maxNN + 3 * NP * NP;  // stage words
+    double* Hs = sm + (TWO ? 2 : 1) * SW;
+    int item = blockIdx.x;
+    if (item >= nitems) return;
+    ns_load_meta<EXT>(P, item, meta[0]);
     __syncthreads();
-    double* Q = sm;               // [slot][v][node]
-    double* GA = Q + NV * NN;     // [slot][k][v][node] = J g
-    for (int idx = threadIdx.x; idx < NV * NN; idx += NS_BS) {
-        const int slot = idx / (NV * n);
-        Q[idx] = __ldg(P.q + s_off[slot] + (idx - slot * NV * n));
-    }
-    __syncthreads();
-    const int nn[3] = {n1, n2, n3};
-    for (int d = 0; d < 3; ++d) {
-        const int nd = nn[d], nl = n / nd;
-        const int nk = EXT ? ext_nk(d) : 3;
-        const int ntask = cnt * nl * nk;
-        for (int task = threadIdx.x; task < ntask; task += NS_BS) {
-            const int kk = task % nk;
-            const int rest = task / nk;
-            const int line = rest % nl, slot = rest / nl;
-            const int k = EXT ? ext_k(d, kk) : kk;
-            const bool first = EXT ? (d == 0 || d == 2) : d == 0;
-            int base, stride;
-            line_geom(d, line, n1, n2, base, stride);
-            const int e = s_e[slot];
-            Met<EXT> M;
-            M.init(P, e, s_off[slot], n, n1, n2);
-            const long long fm = P.fofs ? P.fofs[6LL * e + 2 * d] : -1, fp = P.fofs ? P.fofs[6LL * e + 2 * d + 1] : -1;
-            const double* Qs = Q + slot * NV * n;
-            double* G = GA + slot * 15 * n;
-            switch (nd) {
-                case 2: grad_line<2, EXT>(P, M, Qs, G, n, d, k, kk, nk, line, base, stride, first, fm, fp, nl); break;
-                case 3: grad_line<3, EXT>(P, M, Qs, G, n, d, k, kk, nk, line, base, stride, first, fm, fp, nl); break;
-                case 4: grad_line<4, EXT>(P, M, Qs, G, n, d, k, kk, nk, line, base, stride, first, fm, fp, nl); break;
-                case 5: grad_line<5, EXT>(P, M, Qs, G, n, d, k, kk, nk, line, base, stride, first, fm, fp, nl); break;
-                case 6: grad_line<6, EXT>(P, M, Qs, G, n, d, k, kk, nk, line, base, stride, first, fm, fp, nl); break;
-                case 7: grad_line<7, EXT>(P, M, Qs, G, n, d, k, kk, nk, line, base, stride, first, fm, fp, nl); break;
-                case 8: grad_line<8, EXT>(P, M, Qs, G, n, d, k, kk, nk, line, base, stride, first, fm, fp, nl); break;
-                default: grad_line<9, EXT>(P, M, Qs, G, n, d, k, kk, nk, line, base, stride, first, fm, fp, nl); break;
+    grad_issue<EXT>(P, meta[0], sm, maxNN);
+    asm volatile("cp.async.commit_group;\n" ::);
+    for (int s = 0;; s = TWO ? s ^ 1 : 0) {
+        const int nxt = item + gridDim.x;
+        const bool more = nxt < nitems;
+        if (TWO && more) ns_load_meta<EXT>(P, nxt, meta[s ^ 1]);
+        __syncthreads();
+        if (P.fofs) grad_issue_h<EXT>(P, meta[s], Hs);  // group H_k
+        asm volatile("cp.async.commit_group;\n" ::);
+        if (TWO && more) grad_issue<EXT>(P, meta[s ^ 1], sm + (s ^ 1) * SW, maxNN);  // group A_{k+1}
+        asm volatile("cp.async.commit_group;\n" ::);
+        const NsMeta& M = meta[s];
+        ItemGeo I;
+        I.init(M.ord, M.cnt);
+        const double* Q = sm + s * SW;
+        const bool one = I.NN <= NS_BS;  // one node per thread: volume sums kept in registers across the H wait
+        if (one) {
+            asm volatile("cp.async.wait_group 2;\n" ::: "memory");  // A_k landed
+            __syncthreads();
+            const int idx = threadIdx.x;
+            double g[3][NV];
+            if (idx < I.NN) grad_node_volume<EXT>(I, Q, maxNN, idx, g);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // H_k landed
+            __syncthreads();
+            if (idx < I.NN) grad_node_finish<EXT>(P, M, I, Q, maxNN, Hs, idx, g);
+        } else {
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // A_k and H_k landed
+            __syncthreads();
+            for (int idx = threadIdx.x; idx < I.NN; idx += NS_BS) {
+                double g[3][NV];
+                grad_node_volume<EXT>(I, Q, maxNN, idx, g);
+                grad_node_finish<EXT>(P, M, I, Q, maxNN, Hs, idx, g);
             }
         }
-        __syncthreads();
-    }
-    // g = (J g) / J, written [k][v][node] at 3 x offset (coalesced per slot)
-    for (int idx = threadIdx.x; idx < NN; idx += NS_BS) {
-        const int slot = idx / n, t = idx - slot * n;
-        Met<EXT> M;
-        M.init(P, s_e[slot], s_off[slot], n, n1, n2);
-        const double iJ = 1.0 / M.J(t);
-        const double* G = GA + slot * 15 * n + t;
-        double* o = P.gout + 3 * s_off[slot] + t;
-#pragma unroll
-        for (int c = 0; c < 15; ++c) o[(long long)c * n] = G[c * n] * iJ;
+        __syncthreads();  // stage s and meta[s] free
+        if (!more) break;
+        item = nxt;
+        if (!TWO) {
+            ns_load_meta<EXT>(P, item, meta[0]);
+            __syncthreads();
+            grad_issue<EXT>(P, meta[0], sm, maxNN);
+            asm volatile("cp.async.commit_group;\n" ::);
+        }
     }
 }
 
@@ -457,18 +747,17 @@ __global__ void __launch_bounds__(NS_BS) k_ns_grad(NsElemParams P)
 // k_ns_res: residual / RK stage, one CTA per item
 // ---------------------------------------------------------------------------
 template <bool EXT, bool NSF>
-__global__ void __launch_bounds__(NS_BS) k_ns_res(NsElemParams P)
+__global__ void __launch_bounds__(NS_BS, 2) k_ns_res(NsElemParams P)
 {
     extern __shared__ __align__(16) double sm[];
     __shared__ long long s_off[NS_MAXSLOTS];
     __shared__ int s_e[NS_MAXSLOTS];
     __shared__ double red[32];
     const NsItem it = P.items[P.ibase + blockIdx.x];
-    int N1, N2, N3;
-    unpack_ord(it.ord, N1, N2, N3);
-    const int n1 = N1 + 1, n2 = N2 + 1, n3 = N3 + 1, n = n1 * n2 * n3;
-    const int cnt = it.count, NN = cnt * n;
-    if (threadIdx.x < cnt) {
+    ItemGeo I;
+    I.init(it.ord, it.count);
+    const int n = I.n, NN = I.NN;
+    if (threadIdx.x < I.cnt) {
         const int e = P.elist[it.start + threadIdx.x];
         s_e[threadIdx.x] = e;
         s_off[threadIdx.x] = P.off[e];
@@ -478,10 +767,11 @@ __global__ void __launch_bounds__(NS_BS) k_ns_res(NsElemParams P)
     double* F = Q + NV * NN;     // [d][slot][v][node]
     // node phase: q, grad q, metrics -> contravariant fluxes of the three directions
     for (int idx = threadIdx.x; idx < NN; idx += NS_BS) {
-        const int slot = idx / n, t = idx - slot * n;
+        const int slot = I.dn.div(idx), t = idx - slot * n;
+        const int c = t - I.n12 * I.dn12.div(t);
         const long long o = s_off[slot];
         Met<EXT> M;
-        M.init(P, s_e[slot], o, n, n1, n2);
+        M.init(P, s_e[slot], o, n, I.n12);
         double qv[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
@@ -496,7 +786,7 @@ __global__ void __launch_bounds__(NS_BS) k_ns_res(NsElemParams P)
         }
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            const double ax = M.ja(d, 0, t), ay = M.ja(d, 1, t), az = M.ja(d, 2, t);
+            const double ax = M.ja(d, 0, t, c), ay = M.ja(d, 1, t, c), az = M.ja(d, 2, t, c);
             double Fv[NV];
             adv_dot(qv, ax, ay, az, P.ph.gm1, Fv);
             if (NSF) {
@@ -512,23 +802,21 @@ __global__ void __launch_bounds__(NS_BS) k_ns_res(NsElemParams P)
     }
     __syncthreads();
     // line phase: every line of every direction, one variable per task, in place
-    const int nl0 = n / n1, nl1 = n / n2, nl2 = n / n3;
-    const int t0 = cnt * NV * nl0, t1 = t0 + cnt * NV * nl1, ntask = t1 + cnt * NV * nl2;
+    const int c1 = I.cnt * NV * I.nl0, c2 = c1 + I.cnt * NV * I.nl1, ntask = c2 + I.cnt * NV * I.nl2;
     for (int task = threadIdx.x; task < ntask; task += NS_BS) {
-        int d, r, nl, nd;
-        if (task < t0) { d = 0; r = task; nl = nl0; nd = n1; }
-        else if (task < t1) { d = 1; r = task - t0; nl = nl1; nd = n2; }
-        else { d = 2; r = task - t1; nl = nl2; nd = n3; }
-        const int v = r % NV;
-        const int rest = r / NV;
-        const int line = rest % nl, slot = rest / nl;
-        int base, stride;
-        line_geom(d, line, n1, n2, base, stride);
+        const int d = task < c1 ? 0 : (task < c2 ? 1 : 2);
+        const int r = task - (d == 0 ? 0 : (d == 1 ? c1 : c2));
+        const int q5 = r / NV, v = r - NV * q5;
+        const int slot = I.div_nl(d, q5);
+        const int line = q5 - slot * I.nl(d);
+        int base, stride, cb, cs;
+        I.line(d, line, base, stride, cb, cs);
         double* Fl = F + d * NV * NN + slot * NV * n + v * n + base;
+        const int nd = I.nd(d);
         if (P.fofs) {
             const long long e6 = 6LL * s_e[slot] + 2 * d;
-            const double gm = __ldg(P.blk + P.fofs[e6] + (long long)v * nl + line);
-            const double gp = __ldg(P.blk + P.fofs[e6 + 1] + (long long)v * nl + line);
+            const double gm = __ldg(P.blk + P.fofs[e6] + (long long)v * I.nl(d) + line);
+            const double gp = __ldg(P.blk + P.fofs[e6 + 1] + (long long)v * I.nl(d) + line);
             switch (nd) {
                 case 2: dline_lift<2>(Fl, stride, gm, gp); break;
                 case 3: dline_lift<3>(Fl, stride, gm, gp); break;
@@ -557,11 +845,12 @@ __global__ void __launch_bounds__(NS_BS) k_ns_res(NsElemParams P)
     const double dt = P.mode ? *P.dt : 0.0;
     double lmax = 0.0, vmax = 0.0;
     for (int idx = threadIdx.x; idx < NN; idx += NS_BS) {
-        const int slot = idx / n, t = idx - slot * n;
+        const int slot = I.dn.div(idx), t = idx - slot * n;
+        const int c = t - I.n12 * I.dn12.div(t);
         const long long o = s_off[slot];
         Met<EXT> M;
-        M.init(P, s_e[slot], o, n, n1, n2);
-        const double iJ = 1.0 / M.J(t);
+        M.init(P, s_e[slot], o, n, I.n12);
+        const double iJ = 1.0 / M.J(t, c);
         const int si = slot * NV * n + t;
         double A[NV];
 #pragma unroll
@@ -580,21 +869,18 @@ __global__ void __launch_bounds__(NS_BS) k_ns_res(NsElemParams P)
                 P.out[ix] = qn[v];
             }
             if (P.lam_max) {
-                int ijk[3];
-                node_ijk(t, n1, n2, ijk[0], ijk[1], ijk[2]);
                 const double ir = 1.0 / qn[0];
                 const double p = P.ph.gm1 * (qn[4] - 0.5 * ir * (qn[1] * qn[1] + qn[2] * qn[2] + qn[3] * qn[3]));
-                const double c = sqrt(P.ph.gamma * p * ir);
+                const double cs = sqrt(P.ph.gamma * p * ir);
                 double lam = 0.0, nu = 0.0;
                 const double numax = P.ph.mu * ir * fmax(4.0 / 3.0, P.ph.gamma / P.ph.Pr);
-                const int np1[3] = {n1, n2, n3};
 #pragma unroll
                 for (int d = 0; d < 3; ++d) {
-                    const double a0 = M.ja(d, 0, t) * iJ, a1 = M.ja(d, 1, t) * iJ, a2 = M.ja(d, 2, t) * iJ;
+                    const double a0 = M.ja(d, 0, t, c) * iJ, a1 = M.ja(d, 1, t, c) * iJ, a2 = M.ja(d, 2, t, c) * iJ;
                     const double an2 = a0 * a0 + a1 * a1 + a2 * a2;
                     const double ua = (qn[1] * a0 + qn[2] * a1 + qn[3] * a2) * ir;
-                    const double np = np1[d];
-                    lam += (fabs(ua) + c * sqrt(an2)) * np * np * 0.5;
+                    const double np = I.nd(d);
+                    lam += (fabs(ua) + cs * sqrt(an2)) * np * np * 0.5;
                     nu += numax * an2 * np * np * np * np * 0.25;
                 }
                 lmax = fmax(lmax, lam);
@@ -625,17 +911,17 @@ __device__ __forceinline__ void grp_sync(int gid)
     }
 }
 
-// groups per CTA and buffer sizes
+// groups per CTA and buffer sizes: a buffer holds 20 component slots of CAP points
 template <int W>
 struct FaceCfg {
     static constexpr int G = W == 1 ? 4 : 2;      // groups per CTA
     static constexpr int BS = G * 32 * W;
-    static constexpr int CAP = 32 * W;            // points per component slot
-    static constexpr int BUF = 15 * CAP;          // one buffer: 15 component slots
+    static constexpr int CAP = 32 * W;
+    static constexpr int BUF = 20 * CAP;
     static constexpr size_t smem = sizeof(double) * (size_t)G * 2 * BUF;
+    static constexpr int MINB = W == 1 ? 4 : (W == 2 ? 4 : 2);
 };
 
-// side descriptor inside a face
 struct FSide {
     long long off;  // state offset (-1: ghost)
     int n, sa, sb, base, sta, stb;
@@ -658,33 +944,46 @@ __device__ __forceinline__ FSide face_side(long long off, int ord, int d, bool i
     return s;
 }
 
-// Interpolate `nc` components of a side trace to the mortar grid: gather
-// (src + c * cstride + node) into X, pass A (along a) into Y where s_a < m_a;
-// then each point owner (p < ma mb) reads its values through pass B (along b)
-// into val[c].  Buffers hold CAP points per component.
+// Interpolate nc components of a side trace to the mortar grid.  Component c
+// is read from (c < 5 ? q : g) + (c mod 5 ...) : qsrc[c n + node] for c < 5,
+// gsrc[(c - 5) n + node] for c >= 5.  Gather (one thread per trace point),
+// pass A along a into Y where s_a < m_a (one thread per (b, i)), then each
+// point owner p < m_a m_b applies pass B along b into val[c].
 template <int W, int NCM>
-__device__ __forceinline__ void side_to_mortar(const double* __restrict__ src, long long cstride, const FSide& s, int nc,
-                                               int ma, int mb, const Tables* tab, double* X, double* Y, int l, int gid,
-                                               int p, double* val)
+__device__ __forceinline__ void side_to_mortar(const double* __restrict__ qsrc, const double* __restrict__ gsrc,
+                                               const FSide& s, int nc, int ma, int mb, const Tables* tab, double* X,
+                                               double* Y, int l, int gid, int p, double* val)
 {
     constexpr int CAP = 32 * W;
     const int sa = s.sa, sb = s.sb, ns = sa * sb;
-    for (int idx = l; idx < nc * ns; idx += 32 * W) {
-        const int c = idx / ns, r = idx - c * ns;
-        const int b = r / sa, a = r - b * sa;
-        X[c * CAP + r] = __ldg(src + c * cstride + s.base + a * s.sta + b * s.stb);
+    if (l < ns) {
+        const int b = l / sa, a = l - b * sa;
+        const long long node = s.base + a * s.sta + b * s.stb;
+#pragma unroll
+        for (int c = 0; c < NCM; ++c) {
+            if (c >= nc) break;
+            X[c * CAP + l] = c < NV ? __ldg(qsrc + (long long)c * s.n + node) : __ldg(gsrc + (long long)(c - NV) * s.n + node);
+        }
     }
     grp_sync<W>(gid);
     const double* Z = X;
     if (sa < ma) {
-        const double* Ta = tab->T[sa - 1][ma - 1];  // [i * sa + a]
-        for (int idx = l; idx < nc * sb * ma; idx += 32 * W) {
-            const int c = idx / (sb * ma), r = idx - c * (sb * ma);
-            const int b = r / ma, i = r - b * ma;
-            const double* x = X + c * CAP + b * sa;
-            double acc = 0.0;
-            for (int a = 0; a < sa; ++a) acc = fma(__ldg(Ta + i * sa + a), x[a], acc);
-            Y[c * CAP + b * ma + i] = acc;
+        if (l < sb * ma) {
+            const double* Ta = tab->T[sa - 1][ma - 1] + 0;  // [i * sa + a]
+            const int b = l / ma, i = l - b * ma;
+            double t[NP];
+#pragma unroll
+            for (int a = 0; a < NP; ++a) t[a] = a < sa ? __ldg(Ta + i * sa + a) : 0.0;
+#pragma unroll
+            for (int c = 0; c < NCM; ++c) {
+                if (c >= nc) break;
+                const double* x = X + c * CAP + b * sa;
+                double acc = 0.0;
+#pragma unroll
+                for (int a = 0; a < NP; ++a)
+                    if (a < sa) acc = fma(t[a], x[a], acc);
+                Y[c * CAP + l] = acc;  // [c][b][i]
+            }
         }
         grp_sync<W>(gid);
         Z = Y;
@@ -693,68 +992,82 @@ __device__ __forceinline__ void side_to_mortar(const double* __restrict__ src, l
         const int j = p / ma, i = p - j * ma;
         if (sb < mb) {
             const double* Tb = tab->T[sb - 1][mb - 1];
+            double t[NP];
+#pragma unroll
+            for (int b = 0; b < NP; ++b) t[b] = b < sb ? __ldg(Tb + j * sb + b) : 0.0;
 #pragma unroll
             for (int c = 0; c < NCM; ++c) {
                 if (c >= nc) break;
                 double acc = 0.0;
-                for (int b = 0; b < sb; ++b) acc = fma(__ldg(Tb + j * sb + b), Z[c * CAP + b * ma + i], acc);
+#pragma unroll
+                for (int b = 0; b < NP; ++b)
+                    if (b < sb) acc = fma(t[b], Z[c * CAP + b * ma + i], acc);
                 val[c] = acc;
             }
         } else {
 #pragma unroll
             for (int c = 0; c < NCM; ++c) {
                 if (c >= nc) break;
-                val[c] = Z[c * CAP + j * ma + i];
+                val[c] = Z[c * CAP + p];
             }
         }
     }
     grp_sync<W>(gid);  // X / Y free for the next call
 }
 
-// Project nc components held at the mortar points (Fm[c * CAP + p]) onto a
-// side's own face nodes and store them to out[c * (sa sb) + a + sa b].
+// Project nc components held at the mortar points (Fm[c CAP + p]) onto a
+// side's own face nodes, stored to out[c (sa sb) + a + sa b].
 template <int W>
 __device__ __forceinline__ void mortar_to_side(const double* Fm, int nc, int ma, int mb, int sa, int sb, const Tables* tab,
                                                double* Y, double* __restrict__ out, int l, int gid)
 {
     constexpr int CAP = 32 * W;
     const double* Z = Fm;
-    int zrow = ma;  // row length of Z (points along a)
+    int zrow = ma;
     if (sa < ma) {
-        const double* Pa = tab->P[ma - 1][sa - 1];  // [i * ma + k]
-        for (int idx = l; idx < nc * mb * sa; idx += 32 * W) {
-            const int c = idx / (mb * sa), r = idx - c * (mb * sa);
-            const int b = r / sa, i = r - b * sa;
-            const double* f = Fm + c * CAP + b * ma;
-            double acc = 0.0;
-            for (int k = 0; k < ma; ++k) acc = fma(__ldg(Pa + i * ma + k), f[k], acc);
-            Y[c * CAP + b * sa + i] = acc;
+        if (l < mb * sa) {
+            const double* Pa = tab->P[ma - 1][sa - 1];  // [i * ma + k]
+            const int b = l / sa, i = l - b * sa;
+            double t[NP];
+#pragma unroll
+            for (int k = 0; k < NP; ++k) t[k] = k < ma ? __ldg(Pa + i * ma + k) : 0.0;
+            for (int c = 0; c < nc; ++c) {
+                const double* f = Fm + c * CAP + b * ma;
+                double acc = 0.0;
+#pragma unroll
+                for (int k = 0; k < NP; ++k)
+                    if (k < ma) acc = fma(t[k], f[k], acc);
+                Y[c * CAP + l] = acc;  // [c][b][i], row length sa
+            }
         }
         grp_sync<W>(gid);
         Z = Y;
         zrow = sa;
     }
     const int ns = sa * sb;
-    if (sb < mb) {
-        const double* Pb = tab->P[mb - 1][sb - 1];  // [j * mb + b]
-        for (int idx = l; idx < nc * ns; idx += 32 * W) {
-            const int c = idx / ns, r = idx - c * ns;
-            const int j = r / sa, i = r - j * sa;
-            double acc = 0.0;
-            for (int b = 0; b < mb; ++b) acc = fma(__ldg(Pb + j * mb + b), Z[c * CAP + b * zrow + i], acc);
-            out[(long long)c * ns + r] = acc;
-        }
-    } else {
-        for (int idx = l; idx < nc * ns; idx += 32 * W) {
-            const int c = idx / ns, r = idx - c * ns;
-            out[(long long)c * ns + r] = Z[c * CAP + r];
+    if (l < ns) {
+        const int j = l / sa, i = l - j * sa;
+        if (sb < mb) {
+            const double* Pb = tab->P[mb - 1][sb - 1];  // [j * mb + b]
+            double t[NP];
+#pragma unroll
+            for (int b = 0; b < NP; ++b) t[b] = b < mb ? __ldg(Pb + j * mb + b) : 0.0;
+            for (int c = 0; c < nc; ++c) {
+                double acc = 0.0;
+#pragma unroll
+                for (int b = 0; b < NP; ++b)
+                    if (b < mb) acc = fma(t[b], Z[c * CAP + b * zrow + i], acc);
+                out[(long long)c * ns + l] = acc;
+            }
+        } else {
+            for (int c = 0; c < nc; ++c) out[(long long)c * ns + l] = Z[c * CAP + l];
         }
     }
     grp_sync<W>(gid);
 }
 
 template <int W, int MODE>
-__global__ void __launch_bounds__(FaceCfg<W>::BS) k_ns_face(NsFaceParams P)
+__global__ void __launch_bounds__(FaceCfg<W>::BS, FaceCfg<W>::MINB) k_ns_face(NsFaceParams P)
 {
     using C = FaceCfg<W>;
     constexpr int CAP = C::CAP;
@@ -779,13 +1092,12 @@ __global__ void __launch_bounds__(FaceCfg<W>::BS) k_ns_face(NsFaceParams P)
         jf[1] = __ldg(fg + nm + p);
         jf[2] = __ldg(fg + 2 * nm + p);
     }
-    // ---- q of both sides at the mortar points ----
-    double qL[NV] = {0, 0, 0, 0, 0}, qR[NV] = {0, 0, 0, 0, 0};
-    if (hasL) side_to_mortar<W, NV>(P.q + SL.off, SL.n, SL, NV, ma, mb, P.tab, X, Y, l, gid, p, qL);
-    if (hasR) side_to_mortar<W, NV>(P.q + SR.off, SR.n, SR, NV, ma, mb, P.tab, X, Y, l, gid, p, qR);
     const int kind = F.kind;
+    double qL[NV] = {0, 0, 0, 0, 0}, qR[NV] = {0, 0, 0, 0, 0};
     int nout;
     if (MODE == MODE_QHAT) {
+        if (hasL) side_to_mortar<W, NV>(P.q + SL.off, nullptr, SL, NV, ma, mb, P.tab, X, Y, l, gid, p, qL);
+        if (hasR) side_to_mortar<W, NV>(P.q + SR.off, nullptr, SR, NV, ma, mb, P.tab, X, Y, l, gid, p, qR);
         const int nk = P.ext ? ext_nk(d) : 3;
         nout = NV * nk;
         if (pon) {
@@ -812,8 +1124,31 @@ __global__ void __launch_bounds__(FaceCfg<W>::BS) k_ns_face(NsFaceParams P)
         }
     } else {
         nout = NV;
-        double G[NV] = {0, 0, 0, 0, 0};
+        // each side: q and (NS) its gradient interpolated in one pass; the
+        // viscous flux along Ja_f formed at once (one side's gradient live)
+        double fsum[NV] = {0, 0, 0, 0, 0};
+        constexpr int NCI = MODE == MODE_FLUX_NS ? 20 : NV;
+        for (int side = 0; side < 2; ++side) {
+            const bool has = side ? hasR : hasL;
+            if (!has) continue;
+            const FSide& S = side ? SR : SL;
+            double val[NCI];
+            side_to_mortar<W, NCI>(P.q + S.off, MODE == MODE_FLUX_NS ? P.grad + 3 * S.off : nullptr, S, NCI, ma, mb, P.tab,
+                                   X, Y, l, gid, p, val);
+            if (pon) {
+                double* qs = side ? qR : qL;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) qs[v] = val[v];
+                if (MODE == MODE_FLUX_NS) {
+                    double fs[NV];
+                    visc_dot(qs, val + NV, jf[0], jf[1], jf[2], P.ph, fs);
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) fsum[v] += fs[v];
+                }
+            }
+        }
         if (pon) {
+            double G[NV];
             const double S = sqrt(jf[0] * jf[0] + jf[1] * jf[1] + jf[2] * jf[2]);
             const double nrm[3] = {jf[0] / S, jf[1] / S, jf[2] / S};
             if (kind >= 2) {
@@ -826,24 +1161,7 @@ __global__ void __launch_bounds__(FaceCfg<W>::BS) k_ns_face(NsFaceParams P)
             }
 #pragma unroll
             for (int v = 0; v < NV; ++v) G[v] *= S;
-        }
-        if (MODE == MODE_FLUX_NS) {
-            // viscous fluxes along Ja_f: one side's interpolated gradient live at a time
-            double fs[NV];
-            double fsum[NV] = {0, 0, 0, 0, 0};
-            for (int side = 0; side < 2; ++side) {
-                const bool has = side ? hasR : hasL;
-                if (!has) continue;
-                const FSide& S = side ? SR : SL;
-                double gv[15];
-                side_to_mortar<W, 15>(P.grad + 3 * S.off, S.n, S, 15, ma, mb, P.tab, X, Y, l, gid, p, gv);
-                if (pon) {
-                    visc_dot(side ? qR : qL, gv, jf[0], jf[1], jf[2], P.ph, fs);
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) fsum[v] += fs[v];
-                }
-            }
-            if (pon) {
+            if (MODE == MODE_FLUX_NS) {
                 if (kind == 2) {  // wall: inner viscous flux, u = 0 and adiabatic (A10)
                     fsum[4] = 0.0;
 #pragma unroll
@@ -856,8 +1174,6 @@ __global__ void __launch_bounds__(FaceCfg<W>::BS) k_ns_face(NsFaceParams P)
                     for (int v = 0; v < NV; ++v) G[v] -= 0.5 * fsum[v];
                 }
             }
-        }
-        if (pon) {
 #pragma unroll
             for (int v = 0; v < NV; ++v) X[v * CAP + p] = G[v];
         }
@@ -866,10 +1182,9 @@ __global__ void __launch_bounds__(FaceCfg<W>::BS) k_ns_face(NsFaceParams P)
     // ---- back to the sides' own face nodes ----
     const long long oL = MODE == MODE_QHAT ? F.hL : F.outL, oR = MODE == MODE_QHAT ? F.hR : F.outR;
     if (kind == 0) {  // conforming: the mortar is the face, one shared block
-        double* out = P.out + oL;
-        for (int idx = l; idx < nout * nm; idx += 32 * W) {
-            const int c = idx / nm, r = idx - c * nm;
-            out[idx] = X[c * CAP + r];
+        if (pon) {
+            double* out = P.out + oL;
+            for (int c = 0; c < nout; ++c) out[(long long)c * nm + p] = X[c * CAP + p];
         }
         return;
     }
