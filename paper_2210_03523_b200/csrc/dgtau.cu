@@ -201,7 +201,7 @@ struct dg_ctx {
     NsItem* d_nsitems = nullptr;
     int* d_nselist = nullptr;
     std::vector<SizeClass> nscls;  // item classes by node count: [base, base + count), max nodes
-    std::vector<int> nscls_hw;     // per class: max H face-block words of an item
+    std::vector<int> nscls_swH, nscls_swG;  // per class: max stage words of an item (gradient / residual kernel)
     NsFace* d_nsfaces = nullptr;
     int nsf_cls[4] = {0, 0, 0, 0};  // faces of W = 1..3 warps: [nsf_cls[W-1], nsf_cls[W])
     double* d_fg = nullptr;         // face metrics at the mortar points
@@ -450,10 +450,8 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         ctx->smem_limit = limc;
         // curved residual path (ns.cuh): element kernels up to 20 x 729 doubles, face kernels per W
         const int lns = limc;
-        cudaFuncSetAttribute(k_ns_grad<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
-        cudaFuncSetAttribute(k_ns_grad<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
-        cudaFuncSetAttribute(k_ns_grad<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
-        cudaFuncSetAttribute(k_ns_grad<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
+        cudaFuncSetAttribute(k_ns_grad<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
+        cudaFuncSetAttribute(k_ns_grad<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
         cudaFuncSetAttribute(k_ns_res<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
         cudaFuncSetAttribute(k_ns_res<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
         cudaFuncSetAttribute(k_ns_res<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
@@ -684,6 +682,10 @@ static dg_status scratch_need(dg_ctx* ctx, double*& p, long long& cap, long long
     return DG_OK;
 }
 
+// 16-byte (even double) padding of the face / metric blocks: element kernels
+// stage them with 1-D TMA bulk copies
+static inline long long EVEN(long long x) { return (x + 1) & ~1LL; }
+
 // Plans of the curved residual path (ns.cuh): element items, the face list
 // (every interior face once, boundary faces of owned elements), face-block
 // offsets, face metrics and (extruded meshes) compact volume metrics.
@@ -723,28 +725,24 @@ static dg_status build_ns_plans(dg_ctx* ctx)
         std::vector<NsItem> sorted;
         sorted.reserve(items.size());
         ctx->nscls.clear();
-        ctx->nscls_hw.clear();
-        auto hwords = [&](const NsItem& it) {  // H face-block words of the item (ns.cuh hblk_words)
-            const int N[3] = {it.ord & 255, (it.ord >> 8) & 255, (it.ord >> 16) & 255};
-            const int nl[3] = {(N[1] + 1) * (N[2] + 1), (N[0] + 1) * (N[2] + 1), (N[0] + 1) * (N[1] + 1)};
-            int w = 0;
-            for (int d = 0; d < 3; ++d) w += 2 * NV * (ext ? ext_nk(d) : 3) * nl[d];
-            return it.count * w;
-        };
+        ctx->nscls_swH.clear();
+        ctx->nscls_swG.clear();
         for (int c = 0; c < 3; ++c) {
             const int lo = c ? edge[c - 1] : 0;
             SizeClass cl{(int)sorted.size(), 0, 0};
-            int hw = 0;
+            int swh = 0, swg = 0;
             for (const NsItem& it : items)
                 if (it.nodes > lo && it.nodes <= edge[c]) {
                     sorted.push_back(it);
                     cl.count++;
                     cl.maxn = std::max(cl.maxn, it.nodes);
-                    hw = std::max(hw, hwords(it));
+                    swh = std::max(swh, ns_stage_words(ext, true, true, it.ord, it.count));
+                    swg = std::max(swg, ns_stage_words(ext, false, true, it.ord, it.count));
                 }
             if (cl.count) {
                 ctx->nscls.push_back(cl);
-                ctx->nscls_hw.push_back(ns ? hw : 0);
+                ctx->nscls_swH.push_back(swh);
+                ctx->nscls_swG.push_back(swg);
             }
         }
         CK(upload(ctx->d_nsitems, sorted));
@@ -781,17 +779,17 @@ static dg_status build_ns_plans(dg_ctx* ctx)
                 mgl += 3LL * nm;
                 F.outL = gl;
                 fofsG[6LL * e + 2 * d + 1] = gl;
-                gl += (long long)NV * so;
+                gl += EVEN((long long)NV * so);
                 F.outR = conf ? F.outL : gl;
                 fofsG[6LL * nb + 2 * d] = F.outR;
-                if (!conf) gl += (long long)NV * sr;
+                if (!conf) gl += EVEN((long long)NV * sr);
                 if (ns) {
                     F.hL = hl;
                     fofsH[6LL * e + 2 * d + 1] = hl;
-                    hl += (long long)NV * nkH(d) * so;
+                    hl += EVEN((long long)NV * nkH(d) * so);
                     F.hR = conf ? F.hL : hl;
                     fofsH[6LL * nb + 2 * d] = F.hR;
-                    if (!conf) hl += (long long)NV * nkH(d) * sr;
+                    if (!conf) hl += EVEN((long long)NV * nkH(d) * sr);
                 }
                 fl.push_back(F);
                 fw.push_back((nm + 31) / 32);
@@ -813,11 +811,11 @@ static dg_status build_ns_plans(dg_ctx* ctx)
                 mgl += 3LL * so;
                 F.outL = F.outR = gl;
                 fofsG[6LL * e + 2 * d + s] = gl;
-                gl += (long long)NV * so;
+                gl += EVEN((long long)NV * so);
                 if (ns) {
                     F.hL = F.hR = hl;
                     fofsH[6LL * e + 2 * d + s] = hl;
-                    hl += (long long)NV * nkH(d) * so;
+                    hl += EVEN((long long)NV * nkH(d) * so);
                 }
                 fl.push_back(F);
                 fw.push_back((so + 31) / 32);
@@ -841,7 +839,7 @@ static dg_status build_ns_plans(dg_ctx* ctx)
     dg_status s;
     if ((s = scratch_need(ctx, ctx->d_nsG, ctx->nsG_cap, gl, "flux-block")) != DG_OK) return s;
     if (ns && (s = scratch_need(ctx, ctx->d_nsH, ctx->nsH_cap, hl, "BR1-block")) != DG_OK) return s;
-    if (ns && (s = scratch_need(ctx, ctx->d_grad, ctx->grad_len, 3 * L, "gradient")) != DG_OK) return s;
+    if (ns && (s = scratch_need(ctx, ctx->d_grad, ctx->grad_len, 3 * L + 2, "gradient")) != DG_OK) return s;
     dfree(ctx->d_fg);
     if (mgl > 0) {
         CK(cudaMalloc(&ctx->d_fg, sizeof(double) * mgl));
@@ -879,7 +877,7 @@ static dg_status build_ns_plans(dg_ctx* ctx)
         std::vector<long long> coff(E + 1, 0);
         for (int e = 0; e < E; ++e) {
             const int* N = &ctx->orders[3 * e];
-            coff[e + 1] = coff[e] + 6LL * (N[0] + 1) * (N[1] + 1);
+            coff[e + 1] = coff[e] + EVEN(6LL * (N[0] + 1) * (N[1] + 1));
         }
         CK(upload(ctx->d_coff, coff));
         dfree(ctx->d_metc);
@@ -1319,17 +1317,16 @@ static dg_status launch_ns_gradient(dg_ctx* ctx, int variant, const double* q, c
     P.fofs = noniso ? ctx->d_fofsH : nullptr;
     for (const SizeClass& c : ctx->nscls) {
         P.ibase = c.base;
-        const int hw = ctx->nscls_hw[&c - &ctx->nscls[0]];
-        size_t sm = sizeof(double) * ns_grad_smem_doubles(ctx->extruded, c.maxn, hw, 2);
-        const bool two = sm <= (size_t)ctx->smem_limit;
-        if (!two) sm = sizeof(double) * ns_grad_smem_doubles(ctx->extruded, c.maxn, hw, 1);
+        const int sw = ctx->nscls_swH[&c - &ctx->nscls[0]];
+        int nst = 2;
+        if (sizeof(double) * 2 * (size_t)sw > (size_t)ctx->smem_limit) nst = 1;
+        const size_t sm = sizeof(double) * nst * (size_t)sw;
         if (sm > (size_t)ctx->smem_limit) return fail(ctx, DG_EINVAL, "k_ns_grad: element item exceeds shared memory");
+        auto kern = ctx->extruded ? k_ns_grad<true> : k_ns_grad<false>;
         int occ = 1;
-        auto kern = ctx->extruded ? (two ? k_ns_grad<true, true> : k_ns_grad<true, false>)
-                                  : (two ? k_ns_grad<false, true> : k_ns_grad<false, false>);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NS_BS, sm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NS_THREADS, sm);
         const int grid = std::min(c.count, std::max(1, occ) * ctx->nsm);
-        kern<<<grid, NS_BS, sm, st>>>(P, c.count, c.maxn, hw);
+        kern<<<grid, NS_THREADS, sm, st>>>(P, c.count, nst, sw, ctx->off[ctx->E]);
         ctx->launches++;
     }
     return check_stream_error(ctx, "k_ns_grad launch");
@@ -1364,14 +1361,18 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
     P.lam_max = lam_max;
     for (const SizeClass& c : ctx->nscls) {
         P.ibase = c.base;
-        const size_t sm = sizeof(double) * 20 * (size_t)c.maxn;
-        if (ctx->extruded) {
-            if (ns) k_ns_res<true, true><<<c.count, NS_BS, sm, st>>>(P);
-            else k_ns_res<true, false><<<c.count, NS_BS, sm, st>>>(P);
-        } else {
-            if (ns) k_ns_res<false, true><<<c.count, NS_BS, sm, st>>>(P);
-            else k_ns_res<false, false><<<c.count, NS_BS, sm, st>>>(P);
-        }
+        const int sw = ctx->nscls_swG[&c - &ctx->nscls[0]];
+        const size_t fw = (size_t)15 * c.maxn;  // F work area
+        int nst = 2;
+        if (sizeof(double) * (2 * (size_t)sw + fw) > (size_t)ctx->smem_limit) nst = 1;
+        const size_t sm = sizeof(double) * (nst * (size_t)sw + fw);
+        if (sm > (size_t)ctx->smem_limit) return fail(ctx, DG_EINVAL, "k_ns_res: element item exceeds shared memory");
+        auto kern = ctx->extruded ? (ns ? k_ns_res<true, true> : k_ns_res<true, false>)
+                                  : (ns ? k_ns_res<false, true> : k_ns_res<false, false>);
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, NS_THREADS, sm);
+        const int grid = std::min(c.count, std::max(1, occ) * ctx->nsm);
+        kern<<<grid, NS_THREADS, sm, st>>>(P, c.count, nst, sw, c.maxn, ctx->off[ctx->E]);
         ctx->launches++;
     }
     return check_stream_error(ctx, "curved residual launch");

@@ -428,20 +428,135 @@ __device__ __forceinline__ void split_nk(int nk, int r, int& kk, int& rest)
     else { rest = r / 3; kk = r - 3 * rest; }
 }
 
-// ---------------------------------------------------------------------------
-// k_ns_grad: BR1 gradient, one CTA per item, one thread per node.
-//   J g_k = sum_d [ sum_m D^d_{a m} (Ja^d_k q)_m  + lifting at a = 0 / N_d ],
-// the three directions' sums accumulated in registers; the item's states,
-// metric terms and D rows are staged in shared memory once.
-// ---------------------------------------------------------------------------
+// ===========================================================================
+// Element kernels (BR1 gradient, residual / RK stage): warp-specialised
+// producer / consumer pipeline over items of same-order elements.
+//   * producer warp (the CTA's last warp): fetches item k+1's element ids and
+//     offsets and issues the 1-D TMA bulk copies (cp.async.bulk, mbarrier
+//     complete_tx) of every element block the item needs -- state q (16-byte
+//     envelope of [off, off + 5n), data at +off&1), metric terms, the six
+//     face blocks -- into stage (k+1) mod NST;
+//   * NS_BS consumer threads: one thread per node, compute item k from stage
+//     k mod NST (named barrier 1 between phases), then release the stage.
+// ===========================================================================
+constexpr int NS_PROD = 32;           // producer warp
+constexpr int NS_THREADS = NS_BS + NS_PROD;
 
-// shared-memory words of the gradient kernel for an item class: two stages of
-// Q (5 per node) + metrics (EXT: <= 6 per node; else 10 per node) + D rows
-// (3 x 81), and one buffer of the item's H face blocks (maxHW words)
-__host__ __device__ inline size_t ns_grad_smem_doubles(bool ext, int maxnodes, int maxHW, int stages = 2)
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b)
 {
-    return stages * ((size_t)maxnodes * (5 + (ext ? 6 : 10)) + 3 * NP * NP) + (size_t)maxHW;
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
 }
+__device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;\n" ::"r"(NS_BS) : "memory"); }
+
+// per-stage metadata (written by the producer before its arrive)
+struct NsStageMeta {
+    int cnt, ord;
+    int qsh[NS_MAXSLOTS];
+    long long off[NS_MAXSLOTS];
+};
+
+// words of the face block of direction d: H (BR1 terms, nk components) or G (flux)
+__host__ __device__ __forceinline__ int ns_fblk(bool hblk, bool ext, int d, int nl)
+{
+    return (NV * (hblk ? (ext ? ext_nk(d) : 3) : 1) * nl + 1) & ~1;
+}
+
+// stage layout of an item: per slot [q: EVEN(5n) + 2][metrics: EVEN(MW)][faces: 6 blocks]
+struct StageLayout {
+    int qs, ms, fs;   // per-slot strides of the three regions
+    int b0, b1, b2;   // face block words of the three directions
+    int q0, m0, f0;   // region bases
+    __host__ __device__ void init(bool ext, bool hblk, int n1, int n2, int n3, int cnt, bool faces)
+    {
+        const int n12 = n1 * n2, n = n12 * n3;
+        qs = ((NV * n + 1) & ~1) + 2;
+        ms = ext ? ((6 * n12 + 1) & ~1) : 10 * n;
+        b0 = faces ? ns_fblk(hblk, ext, 0, n2 * n3) : 0;
+        b1 = faces ? ns_fblk(hblk, ext, 1, n1 * n3) : 0;
+        b2 = faces ? ns_fblk(hblk, ext, 2, n12) : 0;
+        fs = 2 * (b0 + b1 + b2);
+        q0 = 0;
+        m0 = cnt * qs;
+        f0 = m0 + cnt * ms;
+    }
+    // offset of face f = 2d + s inside the slot's face region
+    __host__ __device__ __forceinline__ int fb(int f) const
+    {
+        return (f >= 1 ? b0 : 0) + (f >= 2 ? b0 : 0) + (f >= 3 ? b1 : 0) + (f >= 4 ? b1 : 0) + (f >= 5 ? b2 : 0);
+    }
+    __host__ __device__ int words(int cnt) const { return cnt * (qs + ms + fs); }
+};
+
+// Producer: item `item` into stage `st` (full barrier fb).  hblk: face blocks
+// are H (gradient kernel) else G (residual kernel).
+template <bool EXT>
+__device__ __forceinline__ void ns_produce(const NsElemParams& P, int item, double* st, NsStageMeta& M,
+                                           unsigned long long* full, bool hblk, long long qlen)
+{
+    const int lane = threadIdx.x & 31;
+    const NsItem it = P.items[P.ibase + item];
+    int N1, N2, N3;
+    unpack_ord(it.ord, N1, N2, N3);
+    const int n1 = N1 + 1, n2 = N2 + 1, n3 = N3 + 1, n12 = n1 * n2, n = n12 * n3;
+    const bool faces = P.fofs != nullptr;
+    StageLayout Lo;
+    Lo.init(EXT, hblk, n1, n2, n3, it.count, faces);
+    const int nl[3] = {n2 * n3, n1 * n3, n12};
+    unsigned bytes = 0;
+    long long a = 0, b = 0, mo = 0, fo[6];
+    bool clip = false;
+    if (lane < it.count) {
+        const int e = P.elist[it.start + lane];
+        const long long off = P.off[e];
+        a = off & ~1LL;
+        b = (off + NV * n + 1) & ~1LL;
+        clip = b > qlen;
+        if (clip) b -= 2;
+        bytes += (unsigned)((b - a) * 8);
+        mo = EXT ? P.coff[e] : 2 * off;
+        bytes += (unsigned)(Lo.ms * 8);
+#pragma unroll
+        for (int f = 0; f < 6; ++f) {
+            fo[f] = faces ? P.fofs[6LL * e + f] : 0;
+            if (faces) bytes += (unsigned)(ns_fblk(hblk, EXT, f >> 1, nl[f >> 1]) * 8);
+        }
+        M.qsh[lane] = (int)(off & 1);
+        M.off[lane] = off;
+        if (clip) st[Lo.q0 + lane * Lo.qs + (b - a)] = P.q[b];  // last 8 bytes by hand (buffer end)
+    }
+    if (lane == 0) {
+        M.cnt = it.count;
+        M.ord = it.ord;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, o);
+    __syncwarp();
+    if (lane == 0) mbar_expect_tx(full, bytes);
+    __syncwarp();
+    if (lane < it.count) {
+        bulk_g2s(st + Lo.q0 + lane * Lo.qs, P.q + a, (unsigned)((b - a) * 8), full);
+        bulk_g2s(st + Lo.m0 + lane * Lo.ms, (EXT ? P.metc : P.met) + mo, (unsigned)(Lo.ms * 8), full);
+        if (faces) {
+#pragma unroll
+            for (int f = 0; f < 6; ++f)
+                bulk_g2s(st + Lo.f0 + lane * Lo.fs + Lo.fb(f), P.blk + fo[f],
+                         (unsigned)(ns_fblk(hblk, EXT, f >> 1, nl[f >> 1]) * 8), full);
+        }
+    }
+}
+
+// stage words needed by an item (host: class sizing)
+__host__ __device__ inline int ns_stage_words(bool ext, bool hblk, bool faces, int ord, int cnt)
+{
+    StageLayout Lo;
+    Lo.init(ext, hblk, (ord & 255) + 1, ((ord >> 8) & 255) + 1, ((ord >> 16) & 255) + 1, cnt, faces);
+    return Lo.words(cnt);
+}
+
+// ---------------------------------------------------------------------------
+// BR1 gradient: J g_k = sum_d [ sum_m D^d_{a m} (Ja^d_k q)_m + lifting ], one
+// consumer thread per node, the three directions' sums in registers.
+// ---------------------------------------------------------------------------
 
 // One direction's volume sum at node t for the NK metric components of that
 // direction: acc[kk][v] += sum_m D_{a m} Ja_k(m) q_v(m) (line length L).
@@ -483,29 +598,16 @@ __device__ __forceinline__ void grad_dir_sw(int L, const double* Dr, const doubl
     }
 }
 
-// Per-item metadata of the persistent element kernels (one copy per stage).
-struct NsMeta {
-    int cnt, ord;
-    int hw;                         // H words per slot (face blocks back to back)
-    int e[NS_MAXSLOTS];
-    long long off[NS_MAXSLOTS];
-    long long mo[NS_MAXSLOTS];     // metric block: EXT coff[e], else 2 x off
-    long long fo[NS_MAXSLOTS][6];  // face blocks (-1: isolated)
-};
-
-// volume part of J g at node idx of the item (stage Q | metrics | D rows)
+// J g at node t of an element (Qs: its state [v][node], Me: its metric block,
+// Hs: its face blocks or null, Ds: D rows [3][81]), then g written to gout
 template <bool EXT>
-__device__ __forceinline__ void grad_node_volume(const ItemGeo& I, const double* Q, int maxNN, int idx, double (&g)[3][NV])
+__device__ __forceinline__ void grad_node(const ItemGeo& I, const StageLayout& Lo, const double* Qs, const double* Me,
+                                          const double* Hs, const double* Ds, int t, double* __restrict__ gout)
 {
     const int n = I.n, n1 = I.n1, n2 = I.n2, n3 = I.n3, n12 = I.n12;
-    const int MW = EXT ? 6 * n12 : 10 * n;
-    const double* Ms = Q + NV * maxNN;
-    const double* Ds = Ms + (EXT ? 6 : 10) * maxNN;
-    const int slot = I.dn.div(idx), t = idx - slot * n;
     const int k3 = I.dn12.div(t), c = t - n12 * k3;
     const int j = I.dn1.div(c), i = c - n1 * j;
-    const double* Qs = Q + slot * NV * n;
-    const double* Me = Ms + slot * MW;
+    double g[3][NV];
 #pragma unroll
     for (int k = 0; k < 3; ++k)
 #pragma unroll
@@ -518,7 +620,7 @@ __device__ __forceinline__ void grad_node_volume(const ItemGeo& I, const double*
             double acc[2][NV] = {};
             grad_dir_sw<2>(n1, Ds + i * n1, Qs, n, t - i, 1, ja, n1 * j, 1, acc);
 #pragma unroll
-            for (int v = 0; v < NV; ++v) { g[0][v] += acc[0][v]; g[1][v] += acc[1][v]; }
+            for (int v = 0; v < NV; ++v) { g[0][v] = acc[0][v]; g[1][v] = acc[1][v]; }
         }
         {
             const double* ja[2] = {Me + 2 * n12, Me + 3 * n12};
@@ -532,7 +634,7 @@ __device__ __forceinline__ void grad_node_volume(const ItemGeo& I, const double*
             double acc[1][NV] = {};
             grad_dir_sw<1>(n3, Ds + 2 * NP * NP + k3 * n3, Qs, n, c, n12, ja, c, 0, acc);
 #pragma unroll
-            for (int v = 0; v < NV; ++v) g[2][v] += acc[0][v];
+            for (int v = 0; v < NV; ++v) g[2][v] = acc[0][v];
         }
     } else {
         const int tb[3] = {t - i, t - n1 * j, c};
@@ -550,37 +652,20 @@ __device__ __forceinline__ void grad_node_volume(const ItemGeo& I, const double*
                 for (int v = 0; v < NV; ++v) g[k][v] += acc[k][v];
         }
     }
-}
-
-// lifting (H - q Ja^d_k)/w of the faces through node idx (H staged in Hs),
-// then g = (J g)/J written [k][v][node] at 3 x offset
-template <bool EXT>
-__device__ __forceinline__ void grad_node_finish(const NsElemParams& P, const NsMeta& M, const ItemGeo& I, const double* Q,
-                                                 int maxNN, const double* Hs, int idx, double (&g)[3][NV])
-{
-    const int n = I.n, n1 = I.n1, n2 = I.n2, n3 = I.n3, n12 = I.n12;
-    const int MW = EXT ? 6 * n12 : 10 * n;
-    const double* Me = Q + NV * maxNN + I.dn.div(idx) * MW;
-    const int slot = I.dn.div(idx), t = idx - slot * n;
-    const int k3 = I.dn12.div(t), c = t - n12 * k3;
-    const int j = I.dn1.div(c), i = c - n1 * j;
-    const double* Qs = Q + slot * NV * n;
-    if (P.fofs) {
+    // lifting (H - q Ja^d_k)/w at the faces through this node (strong form)
+    if (Hs) {
         const int ai[3] = {i, j, k3};
         const int pt[3] = {j + n2 * k3, i + n1 * k3, c};
-        const double* Hsl = Hs + slot * M.hw;
-        int fb = 0;  // offset of face (d, s) in the slot's H area
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
             const int L = d == 0 ? n1 : (d == 1 ? n2 : n3);
             const int nk = EXT ? ext_nk(d) : 3;
             const int nf = d == 0 ? I.nl0 : (d == 1 ? I.nl1 : I.nl2);
-            const int hb = NV * nk * nf;
 #pragma unroll
             for (int sd = 0; sd < 2; ++sd) {
                 if (ai[d] == (sd ? L - 1 : 0)) {
                     const double CL = (sd ? 0.5 : -0.5) * (L - 1) * L;  // +-1/w_0
-                    const double* H = Hsl + fb + sd * hb + pt[d];
+                    const double* H = Hs + Lo.fb(2 * d + sd) + pt[d];
                     for (int kk = 0; kk < nk; ++kk) {
                         const int k = EXT ? ext_k(d, kk) : kk;
                         double jo;
@@ -591,309 +676,270 @@ __device__ __forceinline__ void grad_node_finish(const NsElemParams& P, const Ns
                     }
                 }
             }
-            fb += 2 * hb;
         }
     }
     const double iJ = 1.0 / (EXT ? Me[5 * n12 + c] : Me[9 * n + t]);
-    double* o = P.gout + 3 * M.off[slot] + t;
 #pragma unroll
     for (int k = 0; k < 3; ++k)
 #pragma unroll
-        for (int v = 0; v < NV; ++v) o[(long long)(k * NV + v) * n] = g[k][v] * iJ;
+        for (int v = 0; v < NV; ++v) gout[(long long)(k * NV + v) * n + t] = g[k][v] * iJ;
 }
-
-
-// face-block words of face (d, s) of an element (nk metric components of
-// direction d), and the offset of face f inside the slot's H area
-__device__ __forceinline__ int hblk_words(bool ext, int d, int nl) { return NV * (ext ? ext_nk(d) : 3) * nl; }
 
 template <bool EXT>
-__device__ __forceinline__ void ns_load_meta(const NsElemParams& P, int item, NsMeta& M)
-{
-    const NsItem it = P.items[P.ibase + item];
-    if (threadIdx.x == 0) {
-        M.cnt = it.count;
-        M.ord = it.ord;
-        int N1, N2, N3;
-        unpack_ord(it.ord, N1, N2, N3);
-        const int n1 = N1 + 1, n2 = N2 + 1, n3 = N3 + 1;
-        M.hw = 2 * (hblk_words(EXT, 0, n2 * n3) + hblk_words(EXT, 1, n1 * n3) + hblk_words(EXT, 2, n1 * n2));
-    }
-    if (threadIdx.x < it.count) {
-        const int e = P.elist[it.start + threadIdx.x];
-        const long long o = P.off[e];
-        M.e[threadIdx.x] = e;
-        M.off[threadIdx.x] = o;
-        M.mo[threadIdx.x] = EXT ? P.coff[e] : 2 * o;
-#pragma unroll
-        for (int f = 0; f < 6; ++f) M.fo[threadIdx.x][f] = P.fofs ? P.fofs[6LL * e + f] : -1;
-    }
-}
-
-// stage layout of the gradient kernel: Q [slot][v][node] | metrics [slot][MW] | D rows [3][81]
-template <bool EXT>
-__device__ __forceinline__ void grad_issue(const NsElemParams& P, const NsMeta& M, double* st, int maxNN)
-{
-    ItemGeo I;
-    I.init(M.ord, M.cnt);
-    const int n = I.n;
-    const int MW = EXT ? 6 * I.n12 : 10 * n;
-    double* Q = st;
-    double* Ms = st + NV * maxNN;
-    double* Ds = Ms + (EXT ? 6 : 10) * maxNN;
-    FDiv d5n, dmw;
-    d5n.init(NV * n);
-    dmw.init(MW);
-    for (int idx = threadIdx.x; idx < NV * I.NN; idx += NS_BS) {
-        const int slot = d5n.div(idx);
-        cp_async8(Q + idx, P.q + M.off[slot] + (idx - slot * NV * n));
-    }
-    const double* msrc = EXT ? P.metc : P.met;
-    for (int idx = threadIdx.x; idx < I.cnt * MW; idx += NS_BS) {
-        const int slot = dmw.div(idx);
-        cp_async8(Ms + idx, msrc + M.mo[slot] + (idx - slot * MW));
-    }
-    for (int w = threadIdx.x; w < 3 * NP * NP; w += NS_BS) {
-        const int d = w / (NP * NP), r = w - d * NP * NP;
-        const int L = d == 0 ? I.n1 : (d == 1 ? I.n2 : I.n3);
-        if (r < L * L) Ds[w] = c_D[(L - 1) * NP * NP + r];
-    }
-}
-
-// the H face blocks of the item's elements into Hs: [slot][f][kk][v][pt]
-template <bool EXT>
-__device__ __forceinline__ void grad_issue_h(const NsElemParams& P, const NsMeta& M, double* Hs)
-{
-    int N1, N2, N3;
-    unpack_ord(M.ord, N1, N2, N3);
-    const int nl[3] = {(N2 + 1) * (N3 + 1), (N1 + 1) * (N3 + 1), (N1 + 1) * (N2 + 1)};
-    const int hb0 = hblk_words(EXT, 0, nl[0]), hb1 = hblk_words(EXT, 1, nl[1]), hb2 = hblk_words(EXT, 2, nl[2]);
-    const int fb[7] = {0, hb0, 2 * hb0, 2 * hb0 + hb1, 2 * hb0 + 2 * hb1, 2 * hb0 + 2 * hb1 + hb2, M.hw};
-    FDiv dhw;
-    dhw.init(M.hw);
-    for (int idx = threadIdx.x; idx < M.cnt * M.hw; idx += NS_BS) {
-        const int slot = dhw.div(idx), r = idx - slot * M.hw;
-        int f = 0;
-#pragma unroll
-        for (int q = 1; q < 6; ++q) f += r >= fb[q];
-        cp_async8(Hs + idx, P.blk + M.fo[slot][f] + (r - fb[f]));
-    }
-}
-
-// Persistent: CTA b takes items b, b + grid, ...; the states and metric terms
-// of the next item are copied (cp.async) into the other shared stage while
-// the current one is computed.
-// The item's H face blocks are copied into one buffer at the start of its
-// compute and waited for only before the lifting (overlapping the volume sums).
-// TWO = false (large items whose two stages do not fit): one stage, no prefetch.
-template <bool EXT, bool TWO>
-__global__ void __launch_bounds__(NS_BS, 2) k_ns_grad(NsElemParams P, int nitems, int maxNN, int maxHW)
+__global__ void __launch_bounds__(NS_THREADS, 2) k_ns_grad(NsElemParams P, int nitems, int NST, int SW, long long qlen)
 {
     extern __shared__ __align__(16) double sm[];
-    __shared__ NsMeta meta[2];
-    const int SW = (NV + (EXT ? 6 : 10)) * maxNN + 3 * NP * NP;  // stage words
-    double* Hs = sm + (TWO ? 2 : 1) * SW;
-    int item = blockIdx.x;
-    if (item >= nitems) return;
-    ns_load_meta<EXT>(P, item, meta[0]);
+    __shared__ NsStageMeta meta[2];
+    __shared__ __align__(8) unsigned long long full[2], empty[2];
+    __shared__ double Ds[3 * NP * NP];
+    if (blockIdx.x >= nitems) return;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NS_BS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
     __syncthreads();
-    grad_issue<EXT>(P, meta[0], sm, maxNN);
-    asm volatile("cp.async.commit_group;\n" ::);
-    for (int s = 0;; s = TWO ? s ^ 1 : 0) {
-        const int nxt = item + gridDim.x;
-        const bool more = nxt < nitems;
-        if (TWO && more) ns_load_meta<EXT>(P, nxt, meta[s ^ 1]);
-        __syncthreads();
-        if (P.fofs) grad_issue_h<EXT>(P, meta[s], Hs);  // group H_k
-        asm volatile("cp.async.commit_group;\n" ::);
-        if (TWO && more) grad_issue<EXT>(P, meta[s ^ 1], sm + (s ^ 1) * SW, maxNN);  // group A_{k+1}
-        asm volatile("cp.async.commit_group;\n" ::);
-        const NsMeta& M = meta[s];
+    if (threadIdx.x >= NS_BS) {  // producer warp
+        int k = 0;
+        for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++k) {
+            const int s = k % NST;
+            if (k >= NST) mbar_wait(&empty[s], ((k / NST) - 1) & 1);
+            ns_produce<EXT>(P, item, sm + s * SW, meta[s], &full[s], true, qlen);
+        }
+        return;
+    }
+    int k = 0;
+    int ordD = -1;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++k) {
+        const int s = k % NST;
+        mbar_wait(&full[s], (k / NST) & 1);
+        const NsStageMeta& M = meta[s];
         ItemGeo I;
         I.init(M.ord, M.cnt);
-        const double* Q = sm + s * SW;
-        const bool one = I.NN <= NS_BS;  // one node per thread: volume sums kept in registers across the H wait
-        if (one) {
-            asm volatile("cp.async.wait_group 2;\n" ::: "memory");  // A_k landed
-            __syncthreads();
-            const int idx = threadIdx.x;
-            double g[3][NV];
-            if (idx < I.NN) grad_node_volume<EXT>(I, Q, maxNN, idx, g);
-            asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // H_k landed
-            __syncthreads();
-            if (idx < I.NN) grad_node_finish<EXT>(P, M, I, Q, maxNN, Hs, idx, g);
-        } else {
-            asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // A_k and H_k landed
-            __syncthreads();
-            for (int idx = threadIdx.x; idx < I.NN; idx += NS_BS) {
-                double g[3][NV];
-                grad_node_volume<EXT>(I, Q, maxNN, idx, g);
-                grad_node_finish<EXT>(P, M, I, Q, maxNN, Hs, idx, g);
+        if (M.ord != ordD) {  // D rows of the item's orders (uniform branch)
+            cons_sync();
+            for (int w = threadIdx.x; w < 3 * NP * NP; w += NS_BS) {
+                const int d = w / (NP * NP), r = w - d * NP * NP;
+                const int L = I.nd(d);
+                if (r < L * L) Ds[w] = c_D[(L - 1) * NP * NP + r];
             }
+            cons_sync();
+            ordD = M.ord;
         }
-        __syncthreads();  // stage s and meta[s] free
-        if (!more) break;
-        item = nxt;
-        if (!TWO) {
-            ns_load_meta<EXT>(P, item, meta[0]);
-            __syncthreads();
-            grad_issue<EXT>(P, meta[0], sm, maxNN);
-            asm volatile("cp.async.commit_group;\n" ::);
+        StageLayout Lo;
+        Lo.init(EXT, true, I.n1, I.n2, I.n3, I.cnt, P.fofs != nullptr);
+        const double* st = sm + s * SW;
+        for (int idx = threadIdx.x; idx < I.NN; idx += NS_BS) {
+            const int slot = I.dn.div(idx), t = idx - slot * I.n;
+            grad_node<EXT>(I, Lo, st + Lo.q0 + slot * Lo.qs + M.qsh[slot], st + Lo.m0 + slot * Lo.ms,
+                           P.fofs ? st + Lo.f0 + slot * Lo.fs : nullptr, Ds, t, P.gout + 3 * M.off[slot]);
         }
+        mbar_arrive(&empty[s]);
     }
 }
 
 // ---------------------------------------------------------------------------
-// k_ns_res: residual / RK stage, one CTA per item
+// residual / RK stage: node phase (contravariant fluxes of the three
+// directions into F), line phase (in-place derivative + lifting of (G - Ft)/w),
+// epilogue (Qdot = -(sum_d)/J, or the RK update + CFL / DFL rates).
 // ---------------------------------------------------------------------------
 template <bool EXT, bool NSF>
-__global__ void __launch_bounds__(NS_BS, 2) k_ns_res(NsElemParams P)
+__global__ void __launch_bounds__(NS_THREADS, 2) k_ns_res(NsElemParams P, int nitems, int NST, int SW, int maxNN,
+                                                          long long qlen)
 {
     extern __shared__ __align__(16) double sm[];
-    __shared__ long long s_off[NS_MAXSLOTS];
-    __shared__ int s_e[NS_MAXSLOTS];
+    __shared__ NsStageMeta meta[2];
+    __shared__ __align__(8) unsigned long long full[2], empty[2];
     __shared__ double red[32];
-    const NsItem it = P.items[P.ibase + blockIdx.x];
-    ItemGeo I;
-    I.init(it.ord, it.count);
-    const int n = I.n, NN = I.NN;
-    if (threadIdx.x < I.cnt) {
-        const int e = P.elist[it.start + threadIdx.x];
-        s_e[threadIdx.x] = e;
-        s_off[threadIdx.x] = P.off[e];
+    if (blockIdx.x >= nitems) return;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NS_BS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     __syncthreads();
-    double* Q = sm;              // [slot][v][node]
-    double* F = Q + NV * NN;     // [d][slot][v][node]
-    // node phase: q, grad q, metrics -> contravariant fluxes of the three directions
-    for (int idx = threadIdx.x; idx < NN; idx += NS_BS) {
-        const int slot = I.dn.div(idx), t = idx - slot * n;
-        const int c = t - I.n12 * I.dn12.div(t);
-        const long long o = s_off[slot];
-        Met<EXT> M;
-        M.init(P, s_e[slot], o, n, I.n12);
-        double qv[NV];
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            qv[v] = __ldg(P.q + o + (long long)v * n + t);
-            Q[slot * NV * n + v * n + t] = qv[v];
+    if (threadIdx.x >= NS_BS) {  // producer warp
+        int k = 0;
+        for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++k) {
+            const int s = k % NST;
+            if (k >= NST) mbar_wait(&empty[s], ((k / NST) - 1) & 1);
+            ns_produce<EXT>(P, item, sm + s * SW, meta[s], &full[s], false, qlen);
         }
-        ViscNode V;
-        if (NSF) {
-            double gv[15];
-            load_grad(P.grad + 3 * o + t, n, gv);
-            visc_node(qv, gv, P.ph, V);
-        }
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            const double ax = M.ja(d, 0, t, c), ay = M.ja(d, 1, t, c), az = M.ja(d, 2, t, c);
-            double Fv[NV];
-            adv_dot(qv, ax, ay, az, P.ph.gm1, Fv);
-            if (NSF) {
-                double fv[NV];
-                visc_along(V, ax, ay, az, fv);
-#pragma unroll
-                for (int v = 0; v < NV; ++v) Fv[v] -= fv[v];
-            }
-            double* Fd = F + d * NV * NN + slot * NV * n + t;
-#pragma unroll
-            for (int v = 0; v < NV; ++v) Fd[v * n] = Fv[v];
-        }
+        return;
     }
-    __syncthreads();
-    // line phase: every line of every direction, one variable per task, in place
-    const int c1 = I.cnt * NV * I.nl0, c2 = c1 + I.cnt * NV * I.nl1, ntask = c2 + I.cnt * NV * I.nl2;
-    for (int task = threadIdx.x; task < ntask; task += NS_BS) {
-        const int d = task < c1 ? 0 : (task < c2 ? 1 : 2);
-        const int r = task - (d == 0 ? 0 : (d == 1 ? c1 : c2));
-        const int q5 = r / NV, v = r - NV * q5;
-        const int slot = I.div_nl(d, q5);
-        const int line = q5 - slot * I.nl(d);
-        int base, stride, cb, cs;
-        I.line(d, line, base, stride, cb, cs);
-        double* Fl = F + d * NV * NN + slot * NV * n + v * n + base;
-        const int nd = I.nd(d);
-        if (P.fofs) {
-            const long long e6 = 6LL * s_e[slot] + 2 * d;
-            const double gm = __ldg(P.blk + P.fofs[e6] + (long long)v * I.nl(d) + line);
-            const double gp = __ldg(P.blk + P.fofs[e6 + 1] + (long long)v * I.nl(d) + line);
-            switch (nd) {
-                case 2: dline_lift<2>(Fl, stride, gm, gp); break;
-                case 3: dline_lift<3>(Fl, stride, gm, gp); break;
-                case 4: dline_lift<4>(Fl, stride, gm, gp); break;
-                case 5: dline_lift<5>(Fl, stride, gm, gp); break;
-                case 6: dline_lift<6>(Fl, stride, gm, gp); break;
-                case 7: dline_lift<7>(Fl, stride, gm, gp); break;
-                case 8: dline_lift<8>(Fl, stride, gm, gp); break;
-                default: dline_lift<9>(Fl, stride, gm, gp); break;
-            }
-        } else {
-            switch (nd) {
-                case 2: dline_inplace<2>(Fl, stride); break;
-                case 3: dline_inplace<3>(Fl, stride); break;
-                case 4: dline_inplace<4>(Fl, stride); break;
-                case 5: dline_inplace<5>(Fl, stride); break;
-                case 6: dline_inplace<6>(Fl, stride); break;
-                case 7: dline_inplace<7>(Fl, stride); break;
-                case 8: dline_inplace<8>(Fl, stride); break;
-                default: dline_inplace<9>(Fl, stride); break;
-            }
-        }
-    }
-    __syncthreads();
-    // epilogue: Qdot = -(sum_d)/J, or the low-storage RK update (+ CFL / DFL rates)
+    double* F = sm + NST * SW;  // [d][slot][v][node]
     const double dt = P.mode ? *P.dt : 0.0;
     double lmax = 0.0, vmax = 0.0;
-    for (int idx = threadIdx.x; idx < NN; idx += NS_BS) {
-        const int slot = I.dn.div(idx), t = idx - slot * n;
-        const int c = t - I.n12 * I.dn12.div(t);
-        const long long o = s_off[slot];
-        Met<EXT> M;
-        M.init(P, s_e[slot], o, n, I.n12);
-        const double iJ = 1.0 / M.J(t, c);
-        const int si = slot * NV * n + t;
-        double A[NV];
+    int k = 0;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++k) {
+        const int s = k % NST;
+        mbar_wait(&full[s], (k / NST) & 1);
+        const NsStageMeta& M = meta[s];
+        ItemGeo I;
+        I.init(M.ord, M.cnt);
+        const int n = I.n, NN = I.NN;
+        StageLayout Lo;
+        Lo.init(EXT, false, I.n1, I.n2, I.n3, I.cnt, P.fofs != nullptr);
+        const double* st = sm + s * SW;
+        // node phase
+        for (int idx = threadIdx.x; idx < NN; idx += NS_BS) {
+            const int slot = I.dn.div(idx), t = idx - slot * n;
+            const int c = t - I.n12 * I.dn12.div(t);
+            const double* Qs = st + Lo.q0 + slot * Lo.qs + M.qsh[slot];
+            const double* Me = st + Lo.m0 + slot * Lo.ms;
+            double qv[NV];
 #pragma unroll
-        for (int v = 0; v < NV; ++v) A[v] = (F[si + v * n] + F[NV * NN + si + v * n]) + F[2 * NV * NN + si + v * n];
-        if (P.mode == 0) {
-#pragma unroll
-            for (int v = 0; v < NV; ++v) P.out[o + (long long)v * n + t] = -A[v] * iJ;
-        } else {
-            double qn[NV];
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const long long ix = o + (long long)v * n + t;
-                const double gn = (P.rkA == 0.0 ? 0.0 : P.rkA * P.g[ix]) - dt * A[v] * iJ;
-                P.g[ix] = gn;
-                qn[v] = Q[si + v * n] + P.rkB * gn;
-                P.out[ix] = qn[v];
+            for (int v = 0; v < NV; ++v) qv[v] = Qs[v * n + t];
+            ViscNode V;
+            if (NSF) {
+                double gv[15];
+                load_grad(P.grad + 3 * M.off[slot] + t, n, gv);
+                visc_node(qv, gv, P.ph, V);
             }
-            if (P.lam_max) {
-                const double ir = 1.0 / qn[0];
-                const double p = P.ph.gm1 * (qn[4] - 0.5 * ir * (qn[1] * qn[1] + qn[2] * qn[2] + qn[3] * qn[3]));
-                const double cs = sqrt(P.ph.gamma * p * ir);
-                double lam = 0.0, nu = 0.0;
-                const double numax = P.ph.mu * ir * fmax(4.0 / 3.0, P.ph.gamma / P.ph.Pr);
 #pragma unroll
-                for (int d = 0; d < 3; ++d) {
-                    const double a0 = M.ja(d, 0, t, c) * iJ, a1 = M.ja(d, 1, t, c) * iJ, a2 = M.ja(d, 2, t, c) * iJ;
-                    const double an2 = a0 * a0 + a1 * a1 + a2 * a2;
-                    const double ua = (qn[1] * a0 + qn[2] * a1 + qn[3] * a2) * ir;
-                    const double np = I.nd(d);
-                    lam += (fabs(ua) + cs * sqrt(an2)) * np * np * 0.5;
-                    nu += numax * an2 * np * np * np * np * 0.25;
+            for (int d = 0; d < 3; ++d) {
+                double ax, ay, az;
+                if (EXT) {
+                    ax = d < 2 ? Me[(2 * d) * I.n12 + c] : 0.0;
+                    ay = d < 2 ? Me[(2 * d + 1) * I.n12 + c] : 0.0;
+                    az = d < 2 ? 0.0 : Me[4 * I.n12 + c];
+                } else {
+                    ax = Me[(3 * d) * n + t];
+                    ay = Me[(3 * d + 1) * n + t];
+                    az = Me[(3 * d + 2) * n + t];
                 }
-                lmax = fmax(lmax, lam);
-                vmax = fmax(vmax, nu);
+                double Fv[NV];
+                adv_dot(qv, ax, ay, az, P.ph.gm1, Fv);
+                if (NSF) {
+                    double fv[NV];
+                    visc_along(V, ax, ay, az, fv);
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) Fv[v] -= fv[v];
+                }
+                double* Fd = F + d * NV * NN + slot * NV * n + t;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) Fd[v * n] = Fv[v];
             }
         }
+        cons_sync();
+        // line phase: every line of every direction, one variable per task, in place
+        const int c1 = I.cnt * NV * I.nl0, c2 = c1 + I.cnt * NV * I.nl1, ntask = c2 + I.cnt * NV * I.nl2;
+        for (int task = threadIdx.x; task < ntask; task += NS_BS) {
+            const int d = task < c1 ? 0 : (task < c2 ? 1 : 2);
+            const int r = task - (d == 0 ? 0 : (d == 1 ? c1 : c2));
+            const int q5 = r / NV, v = r - NV * q5;
+            const int slot = I.div_nl(d, q5);
+            const int line = q5 - slot * I.nl(d);
+            int base, stride, cb, cs;
+            I.line(d, line, base, stride, cb, cs);
+            double* Fl = F + d * NV * NN + slot * NV * n + v * n + base;
+            const int nd = I.nd(d);
+            if (P.fofs) {
+                const double* Gs = st + Lo.f0 + slot * Lo.fs + v * I.nl(d) + line;
+                const double gm = Gs[Lo.fb(2 * d)], gp = Gs[Lo.fb(2 * d + 1)];
+                switch (nd) {
+                    case 2: dline_lift<2>(Fl, stride, gm, gp); break;
+                    case 3: dline_lift<3>(Fl, stride, gm, gp); break;
+                    case 4: dline_lift<4>(Fl, stride, gm, gp); break;
+                    case 5: dline_lift<5>(Fl, stride, gm, gp); break;
+                    case 6: dline_lift<6>(Fl, stride, gm, gp); break;
+                    case 7: dline_lift<7>(Fl, stride, gm, gp); break;
+                    case 8: dline_lift<8>(Fl, stride, gm, gp); break;
+                    default: dline_lift<9>(Fl, stride, gm, gp); break;
+                }
+            } else {
+                switch (nd) {
+                    case 2: dline_inplace<2>(Fl, stride); break;
+                    case 3: dline_inplace<3>(Fl, stride); break;
+                    case 4: dline_inplace<4>(Fl, stride); break;
+                    case 5: dline_inplace<5>(Fl, stride); break;
+                    case 6: dline_inplace<6>(Fl, stride); break;
+                    case 7: dline_inplace<7>(Fl, stride); break;
+                    case 8: dline_inplace<8>(Fl, stride); break;
+                    default: dline_inplace<9>(Fl, stride); break;
+                }
+            }
+        }
+        cons_sync();
+        // epilogue
+        for (int idx = threadIdx.x; idx < NN; idx += NS_BS) {
+            const int slot = I.dn.div(idx), t = idx - slot * n;
+            const int c = t - I.n12 * I.dn12.div(t);
+            const long long o = M.off[slot];
+            const double* Qs = st + Lo.q0 + slot * Lo.qs + M.qsh[slot];
+            const double* Me = st + Lo.m0 + slot * Lo.ms;
+            const double J = EXT ? Me[5 * I.n12 + c] : Me[9 * n + t];
+            const double iJ = 1.0 / J;
+            const int si = slot * NV * n + t;
+            double A[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) A[v] = (F[si + v * n] + F[NV * NN + si + v * n]) + F[2 * NV * NN + si + v * n];
+            if (P.mode == 0) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v) P.out[o + (long long)v * n + t] = -A[v] * iJ;
+            } else {
+                double qn[NV];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    const long long ix = o + (long long)v * n + t;
+                    const double gn = (P.rkA == 0.0 ? 0.0 : P.rkA * P.g[ix]) - dt * A[v] * iJ;
+                    P.g[ix] = gn;
+                    qn[v] = Qs[v * n + t] + P.rkB * gn;
+                    P.out[ix] = qn[v];
+                }
+                if (P.lam_max) {
+                    const double ir = 1.0 / qn[0];
+                    const double p = P.ph.gm1 * (qn[4] - 0.5 * ir * (qn[1] * qn[1] + qn[2] * qn[2] + qn[3] * qn[3]));
+                    const double csnd = sqrt(P.ph.gamma * p * ir);
+                    double lam = 0.0, nu = 0.0;
+                    const double numax = P.ph.mu * ir * fmax(4.0 / 3.0, P.ph.gamma / P.ph.Pr);
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        double a0, a1, a2;
+                        if (EXT) {
+                            a0 = (d < 2 ? Me[(2 * d) * I.n12 + c] : 0.0) * iJ;
+                            a1 = (d < 2 ? Me[(2 * d + 1) * I.n12 + c] : 0.0) * iJ;
+                            a2 = (d < 2 ? 0.0 : Me[4 * I.n12 + c]) * iJ;
+                        } else {
+                            a0 = Me[(3 * d) * n + t] * iJ;
+                            a1 = Me[(3 * d + 1) * n + t] * iJ;
+                            a2 = Me[(3 * d + 2) * n + t] * iJ;
+                        }
+                        const double an2 = a0 * a0 + a1 * a1 + a2 * a2;
+                        const double ua = (qn[1] * a0 + qn[2] * a1 + qn[3] * a2) * ir;
+                        const double np = I.nd(d);
+                        lam += (fabs(ua) + csnd * sqrt(an2)) * np * np * 0.5;
+                        nu += numax * an2 * np * np * np * np * 0.25;
+                    }
+                    lmax = fmax(lmax, lam);
+                    vmax = fmax(vmax, nu);
+                }
+            }
+        }
+        mbar_arrive(&empty[s]);  // stage s read for the last time above
+        cons_sync();             // F free for the next item
     }
     if (P.lam_max) {
-        lmax = block_max(lmax, red);
-        vmax = block_max(vmax, red);
+        // block max over the consumer threads (named barrier; the producer warp has left)
+        double v1 = warp_max(lmax), v2 = warp_max(vmax);
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        if (lane == 0) {
+            red[wid] = v1;
+            red[16 + wid] = v2;
+        }
+        cons_sync();
         if (threadIdx.x == 0) {
-            atomicMax(P.lam_max, (unsigned long long)__double_as_longlong(lmax));
-            if (NSF) atomicMax(P.lam_max + 1, (unsigned long long)__double_as_longlong(vmax));
+            double a1 = 0.0, a2 = 0.0;
+            for (int w = 0; w < NS_BS / 32; ++w) {
+                a1 = fmax(a1, red[w]);
+                a2 = fmax(a2, red[16 + w]);
+            }
+            atomicMax(P.lam_max, (unsigned long long)__double_as_longlong(a1));
+            if (NSF) atomicMax(P.lam_max + 1, (unsigned long long)__double_as_longlong(a2));
         }
     }
 }
