@@ -40,7 +40,12 @@ typedef enum {
     DG_EINVAL = -1,       /* bad argument / size / order out of range           */
     DG_ENOMEM = -2,       /* device or host allocation failed                  */
     DG_ECUDA = -3,        /* CUDA runtime error (message has the CUDA text)    */
-    DG_EADMISSIBLE = -5,  /* rho <= 0 or p <= 0 met (reading A25)              */
+    DG_EADMISSIBLE = -5,  /* rho <= 0 or p <= 0 met (reading A25): the residual
+                             kernels flag such nodes on the device; every call
+                             that synchronises the stream (dg_compute_dt with a
+                             host dt, dg_select_orders, dg_diagnostics) returns
+                             this code with the first flagged element in
+                             dg_last_error and clears the flag                */
     DG_ESTATE = -7,       /* call made before mesh / orders were set           */
     DG_EUNSUPPORTED = -8  /* geometry or physics not available in this build   */
 } dg_status;
@@ -193,7 +198,9 @@ dg_status dg_rk_stage(dg_ctx* ctx, int stage, const double* q_in_dev, double* q_
 /* NS: BR1 gradient of q (eq DGSEMsystem:2) of the owned elements
  * into the context's gradient buffer (15 doubles per node, [k][v] = d q_v /
  * d x_k, element e at 3 x its state offset); the buffer's device pointer is
- * returned by dg_gradient_buffer() for halo exchange (owned by the context). */
+ * returned by dg_gradient_buffer() for halo exchange (owned by the context).
+ * Every non-isolated residual, RK stage and tau-estimate (non-isolated coarse
+ * levels included: their contexts borrow this buffer) overwrites it. */
 dg_status dg_gradient(dg_ctx* ctx, int variant, const double* q_dev, void* stream);
 double* dg_gradient_buffer(dg_ctx* ctx);
 /* dg_rhs_eval with flags (DG_FLAG_GRADIENT_READY). */

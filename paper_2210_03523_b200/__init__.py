@@ -74,20 +74,27 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 def _compile(srcs, verbose=False, force_all=False):
-    """Objects in parallel (the 8 order-specialised units dominate), then link."""
+    """Objects in parallel (res_inst.cu once per N1 = 1..8: the 512
+    order-specialised residual kernels dominate), then link."""
     from concurrent.futures import ThreadPoolExecutor
 
     objdir = os.path.join(_HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    units = [s for s in srcs if s.endswith((".cu", ".cpp"))]
+    units = []
+    for s in srcs:
+        if os.path.basename(s) == "res_inst.cu":
+            units += [(s, [f"-DRES_N1={k}"], f"res_inst_{k}.cu.o") for k in range(1, 9)]
+        elif s.endswith((".cu", ".cpp")):
+            units.append((s, [], os.path.basename(s) + ".o"))
     hdr_t = max(os.path.getmtime(s) for s in srcs if s.endswith((".cuh", ".h")))
     cflags = [f for f in NVCC_FLAGS if f != "-shared"]
 
-    def one(src):
-        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+    def one(u):
+        src, defs, name = u
+        obj = os.path.join(objdir, name)
         if not force_all and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(src), hdr_t):
             return obj
-        cmd = ["nvcc", *cflags, "-c", src, "-o", obj] + (["-Xptxas=-v"] if verbose else [])
+        cmd = ["nvcc", *cflags, *defs, "-c", src, "-o", obj] + (["-Xptxas=-v"] if verbose else [])
         subprocess.check_call(cmd)
         return obj
 
@@ -147,8 +154,33 @@ def _device_view(ptr, n):
 
 
 def _ptr(t):
-    """device pointer of a torch tensor (or None)."""
+    """device pointer of a torch tensor (or None), unchecked (context-owned views)."""
     return C.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _dptr(t, n, what, dtype=None, optional=False):
+    """Checked device pointer for the C ABI: a contiguous CUDA tensor of the
+    expected dtype (float64 by default) with at least n elements.  The kernels
+    trust the pointer and the layout, so a wrong tensor is rejected here
+    instead of being read out of bounds on the GPU."""
+    import torch
+
+    if t is None:
+        if optional:
+            return C.c_void_p(0)
+        raise DGError(f"{what}: tensor required")
+    dt = torch.float64 if dtype is None else dtype
+    if not isinstance(t, torch.Tensor):
+        raise DGError(f"{what}: expected a torch tensor, got {type(t).__name__}")
+    if t.dtype != dt:
+        raise DGError(f"{what}: dtype {t.dtype}, expected {dt}")
+    if not t.is_cuda:
+        raise DGError(f"{what}: tensor must live on the CUDA device")
+    if not t.is_contiguous():
+        raise DGError(f"{what}: tensor must be contiguous")
+    if t.numel() < n:
+        raise DGError(f"{what}: {t.numel()} elements, needs at least {n}")
+    return C.c_void_p(t.data_ptr())
 
 
 def _np(a, dtype):
@@ -237,30 +269,39 @@ class Solver:
     # -- operators --------------------------------------------------------
     def rhs_eval(self, q, qdot=None, variant=NONISOLATED, stream=None):
         qdot = self.new_state() if qdot is None else qdot
-        self._check(self.L.dg_rhs_eval(self.ctx, int(variant), _ptr(q), _ptr(qdot), _stream(stream)), "dg_rhs_eval")
+        n = self.state_len
+        self._check(self.L.dg_rhs_eval(self.ctx, int(variant), _dptr(q, n, "rhs_eval q"), _dptr(qdot, n, "rhs_eval qdot"),
+                                       _stream(stream)), "dg_rhs_eval")
         return qdot
 
     def compute_dt(self, q, cfl, dt=None, sync=False, stream=None):
         dt = self._dt if dt is None else dt
         host = C.c_double(0.0)
-        self._check(self.L.dg_compute_dt(self.ctx, _ptr(q), C.c_double(cfl), _ptr(dt),
+        self._check(self.L.dg_compute_dt(self.ctx, _dptr(q, self.state_len, "compute_dt q"), C.c_double(cfl),
+                                         _dptr(dt, 1, "compute_dt dt"),
                                          C.byref(host) if sync else None, _stream(stream)), "dg_compute_dt")
         return host.value if sync else dt
 
     def rk_step(self, q_in, q_out, g, dt, stream=None):
-        self._check(self.L.dg_rk_step(self.ctx, _ptr(q_in), _ptr(q_out), _ptr(g), _ptr(dt), _stream(stream)),
+        n = self.state_len
+        self._check(self.L.dg_rk_step(self.ctx, _dptr(q_in, n, "rk_step q_in"), _dptr(q_out, n, "rk_step q_out"),
+                                      _dptr(g, n, "rk_step g"), _dptr(dt, 1, "rk_step dt"), _stream(stream)),
                     "dg_rk_step")
 
     def rk_step_dt(self, q_in, q_out, g, dt, cfl, dt_next, stream=None):
         """RK3 step; the CFL dt of the new state is reduced inside the last stage."""
-        self._check(self.L.dg_rk_step_dt(self.ctx, _ptr(q_in), _ptr(q_out), _ptr(g), _ptr(dt), C.c_double(cfl),
-                                         _ptr(dt_next), _stream(stream)), "dg_rk_step_dt")
+        n = self.state_len
+        self._check(self.L.dg_rk_step_dt(self.ctx, _dptr(q_in, n, "rk_step_dt q_in"), _dptr(q_out, n, "rk_step_dt q_out"),
+                                         _dptr(g, n, "rk_step_dt g"), _dptr(dt, 1, "rk_step_dt dt"), C.c_double(cfl),
+                                         _dptr(dt_next, 1, "rk_step_dt dt_next"), _stream(stream)), "dg_rk_step_dt")
 
     def rk_steps(self, nsteps, qa, qb, g, dt_a, dt_b, cfl, stream=None):
         """nsteps RK3 steps ping-ponging (qa, qb) and (dt_a, dt_b) on the device
         (dg_rk_steps); returns (state, next dt) tensors after the last step."""
-        self._check(self.L.dg_rk_steps(self.ctx, int(nsteps), _ptr(qa), _ptr(qb), _ptr(g), _ptr(dt_a), _ptr(dt_b),
-                                       C.c_double(cfl), _stream(stream)), "dg_rk_steps")
+        n = self.state_len
+        self._check(self.L.dg_rk_steps(self.ctx, int(nsteps), _dptr(qa, n, "rk_steps qa"), _dptr(qb, n, "rk_steps qb"),
+                                       _dptr(g, n, "rk_steps g"), _dptr(dt_a, 1, "rk_steps dt_a"),
+                                       _dptr(dt_b, 1, "rk_steps dt_b"), C.c_double(cfl), _stream(stream)), "dg_rk_steps")
         return (qa, dt_a) if nsteps % 2 == 0 else (qb, dt_b)
 
     # -- multi-rank pieces (see dist.py) ---------------------------------------
@@ -271,11 +312,17 @@ class Solver:
         return int(self.L.dg_owned_state_len(self.ctx))
 
     def rk_stage(self, k, q_in, q_out, g, dt, lam=None, flags=0, stream=None):
-        self._check(self.L.dg_rk_stage(self.ctx, int(k), _ptr(q_in), _ptr(q_out), _ptr(g), _ptr(dt), _ptr(lam),
-                                       int(flags), _stream(stream)), "dg_rk_stage")
+        import torch
+
+        n = self.state_len
+        self._check(self.L.dg_rk_stage(self.ctx, int(k), _dptr(q_in, n, "rk_stage q_in"), _dptr(q_out, n, "rk_stage q_out"),
+                                       _dptr(g, n, "rk_stage g"), _dptr(dt, 1, "rk_stage dt"),
+                                       _dptr(lam, 2, "rk_stage lam", torch.int64, optional=True), int(flags),
+                                       _stream(stream)), "dg_rk_stage")
 
     def gradient(self, q, variant=NONISOLATED, stream=None):
-        self._check(self.L.dg_gradient(self.ctx, int(variant), _ptr(q), _stream(stream)), "dg_gradient")
+        self._check(self.L.dg_gradient(self.ctx, int(variant), _dptr(q, self.state_len, "gradient q"), _stream(stream)),
+                    "dg_gradient")
 
     def gradient_buffer(self):
         """torch view of the context's gradient buffer (15 doubles per node)."""
@@ -312,8 +359,11 @@ class Solver:
 
         o = _TauOpts(int(formulation), int(reference), 1 if noniso else 0, int(restriction))
         tau = torch.empty((self.E, 3, TAU_STRIDE), dtype=torch.float64, device="cuda") if tau is None else tau
-        self._check(self.L.dg_tau_estimate(self.ctx, C.byref(o), _ptr(q), _ptr(qdot_ref), _ptr(tau),
-                                           _stream(stream)), "dg_tau_estimate")
+        n = self.state_len
+        self._check(self.L.dg_tau_estimate(self.ctx, C.byref(o), _dptr(q, n, "tau_estimate q"),
+                                           _dptr(qdot_ref, n, "tau_estimate qdot_ref", optional=reference == REF_SAME),
+                                           _dptr(tau, self.E * 3 * TAU_STRIDE, "tau_estimate tau"), _stream(stream)),
+                    "dg_tau_estimate")
         return tau
 
     def select_orders(self, tau, tau_max, Nmin, Nmax, mode=SELECT_DYNAMIC, jump_rule=JUMP_B, dec_cap=1,
@@ -325,7 +375,8 @@ class Solver:
                       int(nstages))
         out = np.zeros((self.E, 3), np.int32)
         margin = np.zeros(self.E)
-        self._check(self.L.dg_select_orders(self.ctx, C.byref(pol), _ptr(tau), _ptr(total_map),
+        self._check(self.L.dg_select_orders(self.ctx, C.byref(pol), _dptr(tau, self.E * 3 * TAU_STRIDE, "select tau"),
+                                            _ptr(total_map),
                                             out.ctypes.data_as(C.c_void_p), margin.ctypes.data_as(C.c_void_p),
                                             _stream(stream)), "dg_select_orders")
         return out, margin
@@ -343,13 +394,16 @@ class Solver:
             q_new = out[:n]
         else:
             q_new = torch.empty(n, dtype=torch.float64, device="cuda")
-        self._check(self.L.dg_transfer(self.ctx, no.ctypes.data_as(C.c_void_p), _ptr(q_old), _ptr(q_new),
+        self._check(self.L.dg_transfer(self.ctx, no.ctypes.data_as(C.c_void_p), _dptr(q_old, self.state_len, "transfer q_old"),
+                                       _dptr(q_new, n, "transfer q_new"),
                                        _stream(stream)), "dg_transfer")
         return q_new
 
     def diagnostics(self, q, v=None, stream=None):
         sums = np.zeros(5)
         mn = np.zeros(2)
-        self._check(self.L.dg_diagnostics(self.ctx, _ptr(q), _ptr(v), sums.ctypes.data_as(C.c_void_p),
+        self._check(self.L.dg_diagnostics(self.ctx, _dptr(q, self.state_len, "diagnostics q"),
+                                          _dptr(v, self.state_len, "diagnostics v", optional=True),
+                                          sums.ctypes.data_as(C.c_void_p),
                                           mn.ctypes.data_as(C.c_void_p), _stream(stream)), "dg_diagnostics")
         return sums, mn

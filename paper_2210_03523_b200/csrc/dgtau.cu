@@ -189,7 +189,6 @@ struct dg_ctx {
     static constexpr int NSTREAMS = 8;  // concurrent bucket launches for mixed-order layouts
     cudaStream_t side[NSTREAMS] = {};
     cudaEvent_t ev_fork = nullptr, ev_join[NSTREAMS] = {};
-    bool generic = false;  // DGTAU_GENERIC=1: runtime-order residual kernel (A/B testing)
     bool no_graphs = false;  // DGTAU_NO_GRAPHS=1: launch mixed-order residuals directly
     cudaStream_t cap_stream = nullptr;  // graph capture stream
     std::map<ShapeKey, GraphEntry> graphs;  // mixed-order residual graphs of the current layout
@@ -326,6 +325,25 @@ dg_status check_stream_error(dg_ctx* ctx, const char* what)
     return DG_OK;
 }
 
+// Admissibility (reading A25): the residual kernels count nodes with rho <= 0
+// or p <= 0 in d_flag[0] (first flagged element in d_flag[1]).  Every call
+// that synchronises the stream reads it and fails with DG_EADMISSIBLE (the
+// flag is reset so the caller can recover).
+dg_status admissibility(dg_ctx* ctx, cudaStream_t st)
+{
+    int flag[2] = {0, 0};
+    cudaError_t e = cudaMemcpyAsync(flag, ctx->d_flag, sizeof(flag), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return fail(ctx, DG_ECUDA, std::string("admissibility flag: ") + cudaGetErrorString(e));
+    if (flag[0] > 0) {
+        cudaMemsetAsync(ctx->d_flag, 0, 2 * sizeof(int), st);
+        return fail(ctx, DG_EADMISSIBLE, "inadmissible state (rho <= 0 or p <= 0) at " + std::to_string(flag[0]) +
+                                             " node evaluations since the last check; first flagged element " +
+                                             std::to_string(flag[1]));
+    }
+    return DG_OK;
+}
+
 // Gauss-Lobatto nodes of the geometry orders, for evaluating node coordinates.
 const Tables& host_tables()
 {
@@ -422,8 +440,6 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
             dg_destroy(ctx);
             return s;
         }
-        const char* g = getenv("DGTAU_GENERIC");
-        ctx->generic = g && g[0] == '1';
         ctx->no_graphs = getenv_flag("DGTAU_NO_GRAPHS");
         ctx->coarse_stream_force = getenv_flag("DGTAU_NONISO_STREAM");
         if ((s = cuda_check(ctx, cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking), "capture stream")) !=
@@ -437,8 +453,6 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         int optin = 0;
         cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
         const int lim = optin - 1024;  // headroom for static shared arrays
-        cudaFuncSetAttribute(k_residual, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
-        cudaFuncSetAttribute(k_tau, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
         cudaFuncSetAttribute(k_tau5, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 4096);  // 3.1 KB static
         cudaFuncSetAttribute(k_tau5, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
         cudaFuncSetAttribute(k_transfer, cudaFuncAttributeMaxDynamicSharedMemorySize, std::min(200 * 1024, lim));
@@ -1285,6 +1299,7 @@ static NsElemParams ns_elem_params(dg_ctx* ctx, const double* q)
     P.coff = ctx->d_coff;
     P.q = q;
     P.ph = phys_dev(ctx->prm);
+    P.flag = ctx->d_flag;
     return P;
 }
 
@@ -1400,15 +1415,12 @@ static dg_status launch_residual_direct(dg_ctx* ctx, int variant, const double* 
         M.mortarG = ctx->d_mortarG;
         M.tab = ctx->d_tab;
         M.ph = phys_dev(ctx->prm);
-        if (ctx->generic) k_mortar<<<ctx->nmortar, 128, 0, st>>>(M);
-        else {
-            CK(cudaMemsetAsync(ctx->d_flag + 4, 0, sizeof(int), st));  // k_mortar3 work counter
-            k_mortar3<<<std::min(ctx->nmortar, MT_MINB * ctx->nsm), MT_BS, 0, st>>>(M, ctx->d_mfaces, ctx->nmortar,
-                                                                                ctx->d_flag + 4);
-        }
+        CK(cudaMemsetAsync(ctx->d_flag + 4, 0, sizeof(int), st));  // k_mortar3 work counter
+        k_mortar3<<<std::min(ctx->nmortar, MT_MINB * ctx->nsm), MT_BS, 0, st>>>(M, ctx->d_mfaces, ctx->nmortar,
+                                                                            ctx->d_flag + 4);
         ctx->launches++;
     }
-    if (variant == DG_NONISOLATED && !ctx->generic && ctx->nface_pts > 0) {
+    if (variant == DG_NONISOLATED && ctx->nface_pts > 0) {
         FaceParams FP;
         FP.q = q;
         FP.G = ctx->d_mortarG;
@@ -1453,11 +1465,7 @@ static dg_status launch_residual_direct(dg_ctx* ctx, int variant, const double* 
     P.lam_zero = fz.lam_zero;
     if ((reinterpret_cast<uintptr_t>(q) & 15) != 0)
         return fail(ctx, DG_EINVAL, "residual: state pointer must be 16-byte aligned");
-    if (ctx->generic && (lam_max || fz.lam_in)) return fail(ctx, DG_EUNSUPPORTED, "fused dt needs the specialised kernels");
-    if (ctx->generic) {
-        k_residual<<<ctx->nwork, BLOCK, ctx->res_smem, st>>>(P);
-        ctx->launches++;
-    } else {
+    {
         if (ctx->buckets.size() == 1) {
             const Bucket& b = ctx->buckets[0];
             ctx->rtab[b.ord & 255][(b.ord >> 8) & 255][(b.ord >> 16) & 255](P, b.start0, b.nelem, b.nitems, b.grid, st);
@@ -1495,7 +1503,7 @@ static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, doub
                                  int flags = 0, const DtFuse& fz = DtFuse())
 {
     if (ctx->curved) return launch_residual_curved(ctx, variant, q, out, g, dt, A, B, mode, st, lam_max, flags);
-    if (ctx->generic || ctx->buckets.size() <= 1 || ctx->no_graphs)
+    if (ctx->buckets.size() <= 1 || ctx->no_graphs)
         return launch_residual_direct(ctx, variant, q, out, g, dt, A, B, mode, st, lam_max, fz);
     const GraphKey key{variant, mode, q, out, g, dt, lam_max, A, B, fz.lam_in, fz.dt_out, fz.lam_zero, fz.cfl};
     const ShapeKey shape{variant, mode, lam_max != nullptr, fz.lam_in != nullptr, fz.dt_out != nullptr,
@@ -1608,7 +1616,7 @@ dg_status dg_compute_dt(dg_ctx* ctx, const double* q_dev, double cfl, double* dt
         if (s != DG_OK) return s;
         if (dt_host) {
             CK(cudaMemcpyAsync(dt_host, dt_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
+            return admissibility(ctx, st);
         }
         return DG_OK;
     }
@@ -1627,7 +1635,7 @@ dg_status dg_compute_dt(dg_ctx* ctx, const double* q_dev, double cfl, double* dt
     if (s != DG_OK) return s;
     if (dt_host) {
         CK(cudaMemcpyAsync(dt_host, dt_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        return admissibility(ctx, st);
     }
     return DG_OK;
 }
@@ -1999,23 +2007,8 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
     if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "tau_estimate: orders not set");
     if (o->reference == DG_REF_SOLVER && !qref_dev) return fail(ctx, DG_EINVAL, "tau_estimate: SOLVER needs qdot_ref");
     if (ctx->prm.physics == DG_NS && !ctx->curved) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: NS needs the curved path");
-    if ((o->coarse_faces || o->restriction) && ctx->generic)
-        return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: non-isolated levels / L2 restriction need the specialised kernels");
     if (o->restriction != 0 && o->restriction != 1) return fail(ctx, DG_EINVAL, "tau_estimate: restriction");
-    const size_t smem = sizeof(double) * 3 * NV * (size_t)ctx->maxn;
-    if (ctx->generic) {
-        TauParams P;
-        P.q = q_dev;
-        P.qref = o->reference == DG_REF_SOLVER ? qref_dev : nullptr;
-        P.tau = tau_dev;
-        P.orders = ctx->d_orders;
-        P.off = ctx->d_off;
-        P.hgeo = ctx->d_h;
-        P.tab = ctx->d_tab;
-        P.formulation = o->formulation;
-        P.ph = phys_dev(ctx->prm);
-        k_tau<<<ctx->n_own, BLOCK, smem, (cudaStream_t)stream>>>(P);
-    } else {
+    {
         cudaStream_t st = (cudaStream_t)stream;
         const double* ref = qref_dev;
         if (o->reference == DG_REF_SAME) {  // isolated fine residual first (reading A4)
@@ -2137,8 +2130,7 @@ dg_status dg_select_orders(dg_ctx* ctx, const dg_adapt_policy* pol, const double
     }
     CK(cudaMemcpyAsync(orders_out, a, sizeof(int) * 3LL * E, cudaMemcpyDeviceToHost, st));
     if (margin_host) CK(cudaMemcpyAsync(margin_host, ctx->d_margin, sizeof(double) * E, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    return DG_OK;
+    return admissibility(ctx, st);
 }
 
 dg_status dg_transfer(dg_ctx* ctx, const int32_t* new_orders, const double* q_old, double* q_new, void* stream)

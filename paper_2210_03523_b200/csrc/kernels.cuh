@@ -1,210 +1,14 @@
-// kernels.cuh -- generic (runtime-order) sm_100a kernels of the DGSEM /
-// tau-estimation hot path; included by dgtau.cu only.  Numerics: see
-// common.cuh.
+// kernels.cuh -- sm_100a kernels of the host-light steps of the hot path
+// (CFL step size, order selection and the jump fixpoint, solution transfer,
+// diagnostics) and the mortar parameter block of face.cuh; included by
+// dgtau.cu only.  Numerics: see common.cuh.
 #pragma once
 
 #include "common.cuh"
 
 namespace dgtau {
 
-// ---------------------------------------------------------------------------
-// Residual / RK-stage kernel: one CTA per work item (1..32 elements of the
-// same orders, from one (N1,N2,N3) bucket).
-// ---------------------------------------------------------------------------
-
-__global__ void __launch_bounds__(BLOCK) k_residual(ResParams P)
-{
-    extern __shared__ double sm[];
-    __shared__ long long s_off[MAXSLOTS];
-    __shared__ int s_e[MAXSLOTS];
-    __shared__ double s_h[MAXSLOTS][3];
-
-    const WorkItem w = P.work[blockIdx.x];
-    int N[3];
-    unpack_ord(w.ord, N[0], N[1], N[2]);
-    const int n1 = N[0] + 1, n2 = N[1] + 1, n3 = N[2] + 1;
-    const int n = n1 * n2 * n3;
-    const int cnt = w.count;
-    const int nf[3] = {n2 * n3, n1 * n3, n1 * n2};
-    const int fsz = 2 * (nf[0] + nf[1] + nf[2]);  // face points per element (6 faces)
-    int foff[6];
-    {
-        int acc = 0;
-        for (int f = 0; f < 6; ++f) { foff[f] = acc; acc += NV * nf[f >> 1]; }
-    }
-    double* Dsm = sm;                  // 3 x 81
-    double* qs = Dsm + 3 * NP * NP;    // cnt x 5 x n
-    double* Fs = qs + cnt * NV * n;    // cnt x 5 x n
-    double* Gs = Fs + cnt * NV * n;    // cnt x 5 x fsz
-
-    const int tid = threadIdx.x;
-    if (tid < cnt) {
-        const int e = P.elist[w.start + tid];
-        s_e[tid] = e;
-        s_off[tid] = P.off[e];
-        for (int d = 0; d < 3; ++d) s_h[tid][d] = P.hgeo[3 * e + d];
-    }
-    for (int t = tid; t < 3 * NP * NP; t += BLOCK) {
-        const int d = t / (NP * NP), r = t % (NP * NP);
-        const int nd = N[d] + 1;
-        if (r < nd * nd) Dsm[d * NP * NP + r] = P.tab->D[N[d]][r];
-    }
-    __syncthreads();
-    for (int t = tid; t < cnt * NV * n; t += BLOCK) {
-        const int slot = t / (NV * n), r = t - slot * NV * n;
-        qs[t] = P.q[s_off[slot] + r];
-    }
-    __syncthreads();
-
-    const double gm1 = P.ph.gm1;
-    double acc[NPT][NV];
-#pragma unroll
-    for (int it = 0; it < NPT; ++it)
-#pragma unroll
-        for (int v = 0; v < NV; ++v) acc[it][v] = 0.0;
-
-    // ---- volume term: sum_d (2/h_d) D^{N_d} f_d -------------------------
-    for (int d = 0; d < 3; ++d) {
-        for (int t = tid; t < cnt * n; t += BLOCK) {
-            const int slot = t / n, node = t - slot * n;
-            double qv[NV], f[NV], p;
-            for (int v = 0; v < NV; ++v) qv[v] = qs[(slot * NV + v) * n + node];
-            flux_dir(qv, gm1, d, f, &p);
-            if (d == 0 && !(qv[0] > 0.0 && p > 0.0)) {
-                if (atomicAdd(P.flag, 1) == 0) P.flag[1] = s_e[slot];
-            }
-            for (int v = 0; v < NV; ++v) Fs[(slot * NV + v) * n + node] = f[v];
-        }
-        __syncthreads();
-        const int nd = N[d] + 1;
-        const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
-        const double* Dd = Dsm + d * NP * NP;
-#pragma unroll
-        for (int it = 0; it < NPT; ++it) {
-            const int t = tid + it * BLOCK;
-            if (t < cnt * n) {
-                const int slot = t / n, node = t - slot * n;
-                int ijk[3];
-                node_ijk(node, n1, n2, ijk[0], ijk[1], ijk[2]);
-                const int a = ijk[d];
-                const int base = node - a * stride;
-                const double sc = 2.0 / s_h[slot][d];
-                for (int v = 0; v < NV; ++v) {
-                    const double* Fl = Fs + (slot * NV + v) * n + base;
-                    double s = 0.0;
-                    for (int m = 0; m < nd; ++m) s += Dd[a * nd + m] * Fl[m * stride];
-                    acc[it][v] += sc * s;
-                }
-            }
-        }
-        __syncthreads();
-    }
-
-    // ---- surface: Gs = G - f_own (strong form) on the 6 faces ----------
-    if (P.variant == 0) {
-        for (int t = tid; t < cnt * fsz; t += BLOCK) {
-            const int slot = t / fsz;
-            int r = t - slot * fsz;
-            int f = 0;
-            while (r >= nf[f >> 1]) { r -= nf[f >> 1]; ++f; }
-            const int d = f >> 1, s = f & 1, pt = r;
-            const int e = s_e[slot];
-            // own boundary node
-            int ijk[3];
-            const int ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
-            const int nta = N[ta] + 1;
-            ijk[ta] = pt % nta;
-            ijk[tb] = pt / nta;
-            ijk[d] = s ? N[d] : 0;
-            const int node = ijk[0] + n1 * (ijk[1] + n2 * ijk[2]);
-            double qo[NV], fo[NV], p;
-            for (int v = 0; v < NV; ++v) qo[v] = qs[(slot * NV + v) * n + node];
-            flux_dir(qo, gm1, d, fo, &p);
-            double Gv[NV];
-            const int nb = P.nbr[6 * e + f];
-            double nrm[3] = {0.0, 0.0, 0.0};
-            nrm[d] = 1.0;
-            if (nb < 0) {
-                double qg[NV];
-                ghost_state(qo, nb, P.ph, qg);
-                if (s) riemann(qo, qg, nrm, P.ph, Gv); else riemann(qg, qo, nrm, P.ph, Gv);
-            } else {
-                const long long mo = P.moff[6 * e + f];
-                if (mo >= 0) {
-                    for (int v = 0; v < NV; ++v) Gv[v] = P.mortarG[mo + (long long)v * nf[d] + pt];
-                } else {
-                    const int B1 = P.orders[3 * nb] + 1, B2 = P.orders[3 * nb + 1] + 1, B3 = P.orders[3 * nb + 2] + 1;
-                    int jb[3] = {ijk[0], ijk[1], ijk[2]};
-                    const int Bd = d == 0 ? B1 : (d == 1 ? B2 : B3);
-                    jb[d] = s ? 0 : Bd - 1;
-                    const int nbn = B1 * B2 * B3;
-                    const long long ob = P.off[nb] + jb[0] + B1 * (jb[1] + B2 * jb[2]);
-                    double qn[NV];
-                    for (int v = 0; v < NV; ++v) qn[v] = P.q[ob + (long long)v * nbn];
-                    if (s) riemann(qo, qn, nrm, P.ph, Gv); else riemann(qn, qo, nrm, P.ph, Gv);
-                }
-            }
-            double* Gd = Gs + slot * NV * fsz + foff[f];
-            for (int v = 0; v < NV; ++v) Gd[v * nf[d] + pt] = Gv[v] - fo[v];
-        }
-        __syncthreads();
-        // lifting onto the boundary nodes
-#pragma unroll
-        for (int it = 0; it < NPT; ++it) {
-            const int t = tid + it * BLOCK;
-            if (t < cnt * n) {
-                const int slot = t / n, node = t - slot * n;
-                int ijk[3];
-                node_ijk(node, n1, n2, ijk[0], ijk[1], ijk[2]);
-                for (int d = 0; d < 3; ++d) {
-                    const int a = ijk[d];
-                    if (a != 0 && a != N[d]) continue;
-                    const int ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
-                    const int pt = ijk[ta] + (N[ta] + 1) * ijk[tb];
-                    const int f = 2 * d + (a == N[d] ? 1 : 0);
-                    const double sgn = a == N[d] ? 1.0 : -1.0;
-                    const double sc = sgn * 2.0 / (s_h[slot][d] * P.tab->w[N[d]][a]);
-                    const double* Gd = Gs + slot * NV * fsz + foff[f];
-                    for (int v = 0; v < NV; ++v) acc[it][v] += sc * Gd[v * nf[d] + pt];
-                }
-            }
-        }
-    }
-
-    // ---- output: Qdot = -acc, or the fused low-storage RK update -------
-    if (P.mode == 0) {
-#pragma unroll
-        for (int it = 0; it < NPT; ++it) {
-            const int t = tid + it * BLOCK;
-            if (t < cnt * n) {
-                const int slot = t / n, node = t - slot * n;
-                for (int v = 0; v < NV; ++v) P.out[s_off[slot] + (long long)v * n + node] = -acc[it][v];
-            }
-        }
-    } else {
-        const double dt = *P.dt;
-#pragma unroll
-        for (int it = 0; it < NPT; ++it) {
-            const int t = tid + it * BLOCK;
-            if (t < cnt * n) {
-                const int slot = t / n, node = t - slot * n;
-                for (int v = 0; v < NV; ++v) {
-                    const long long ix = s_off[slot] + (long long)v * n + node;
-                    const double gn = (P.rkA == 0.0 ? 0.0 : P.rkA * P.g[ix]) - dt * acc[it][v];
-                    P.g[ix] = gn;
-                    P.out[ix] = qs[(slot * NV + v) * n + node] + P.rkB * gn;
-                }
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Mortar kernel (reading A6): one CTA per face whose tangential orders differ.
-// Traces interpolated to the mortar (orders max per tangential direction),
-// Riemann flux there, exact L2 projection back to both sides.
-// ---------------------------------------------------------------------------
-
+// Parameters of the affine mortar kernel k_mortar3 (face.cuh, reading A6).
 struct MortarParams {
     const double* q;
     const int* orders;
@@ -215,70 +19,6 @@ struct MortarParams {
     const Tables* tab;
     PhysDev ph;
 };
-
-__global__ void __launch_bounds__(128) k_mortar(MortarParams P)
-{
-    __shared__ double GM[NV][NP * NP];
-    const MortarItem it = P.items[blockIdx.x];
-    const int d = it.d;
-    const int ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
-    int NL[3], NR[3];
-    for (int k = 0; k < 3; ++k) { NL[k] = P.orders[3 * it.L + k]; NR[k] = P.orders[3 * it.R + k]; }
-    const int M1 = max(NL[ta], NR[ta]), M2 = max(NL[tb], NR[tb]);
-    const int nm = (M1 + 1) * (M2 + 1);
-    const int nL = (NL[0] + 1) * (NL[1] + 1) * (NL[2] + 1), nR = (NR[0] + 1) * (NR[1] + 1) * (NR[2] + 1);
-    const long long oL = P.off[it.L], oR = P.off[it.R];
-    const double* TL1 = P.tab->T[NL[ta]][M1];
-    const double* TL2 = P.tab->T[NL[tb]][M2];
-    const double* TR1 = P.tab->T[NR[ta]][M1];
-    const double* TR2 = P.tab->T[NR[tb]][M2];
-    double nrm[3] = {0.0, 0.0, 0.0};
-    nrm[d] = 1.0;
-    for (int t = threadIdx.x; t < nm; t += blockDim.x) {
-        const int m1 = t % (M1 + 1), m2 = t / (M1 + 1);
-        double qL[NV] = {0, 0, 0, 0, 0}, qR[NV] = {0, 0, 0, 0, 0};
-        // L's +1 face and R's -1 face, interpolated along both tangential directions
-        for (int b = 0; b <= NL[tb]; ++b)
-            for (int a = 0; a <= NL[ta]; ++a) {
-                int ijk[3];
-                ijk[d] = NL[d]; ijk[ta] = a; ijk[tb] = b;
-                const long long ix = oL + ijk[0] + (NL[0] + 1) * (ijk[1] + (NL[1] + 1) * ijk[2]);
-                const double wgt = TL1[m1 * (NL[ta] + 1) + a] * TL2[m2 * (NL[tb] + 1) + b];
-                for (int v = 0; v < NV; ++v) qL[v] += wgt * P.q[ix + (long long)v * nL];
-            }
-        for (int b = 0; b <= NR[tb]; ++b)
-            for (int a = 0; a <= NR[ta]; ++a) {
-                int ijk[3];
-                ijk[d] = 0; ijk[ta] = a; ijk[tb] = b;
-                const long long ix = oR + ijk[0] + (NR[0] + 1) * (ijk[1] + (NR[1] + 1) * ijk[2]);
-                const double wgt = TR1[m1 * (NR[ta] + 1) + a] * TR2[m2 * (NR[tb] + 1) + b];
-                for (int v = 0; v < NV; ++v) qR[v] += wgt * P.q[ix + (long long)v * nR];
-            }
-        double F[NV];
-        riemann(qL, qR, nrm, P.ph, F);
-        for (int v = 0; v < NV; ++v) GM[v][t] = F[v];
-    }
-    __syncthreads();
-    // project back: side X with tangential orders (S1, S2)
-    for (int side = 0; side < 2; ++side) {
-        const int* NS = side == 0 ? NL : NR;
-        const int S1 = NS[ta], S2 = NS[tb];
-        const int ns = (S1 + 1) * (S2 + 1);
-        const long long mo = P.moff[6 * (side == 0 ? it.L : it.R) + 2 * d + (side == 0 ? 1 : 0)];
-        const double* P1 = P.tab->P[M1][S1];
-        const double* P2 = P.tab->P[M2][S2];
-        for (int t = threadIdx.x; t < ns; t += blockDim.x) {
-            const int a = t % (S1 + 1), b = t / (S1 + 1);
-            double s[NV] = {0, 0, 0, 0, 0};
-            for (int m2 = 0; m2 <= M2; ++m2)
-                for (int m1 = 0; m1 <= M1; ++m1) {
-                    const double wgt = P1[a * (M1 + 1) + m1] * P2[b * (M2 + 1) + m2];
-                    for (int v = 0; v < NV; ++v) s[v] += wgt * GM[v][m1 + (M1 + 1) * m2];
-                }
-            for (int v = 0; v < NV; ++v) P.mortarG[mo + (long long)v * ns + t] = s[v];
-        }
-    }
-}
 
 // ---------------------------------------------------------------------------
 // CFL time step (reading A11): affine
@@ -327,177 +67,6 @@ __global__ void k_dt_final(unsigned long long* maxbits, double cfl, double* dt)
 {
     dt[0] = cfl / __longlong_as_double((long long)maxbits[0]);
     maxbits[0] = 0ull;  // ready for the next accumulation
-}
-
-// ---------------------------------------------------------------------------
-// tau-estimation (eqs TEtildedef / TEdef; isolated coarse
-// residuals P:469; decoupled directional levels, reading A12).  One CTA per
-// element: for each direction d and coarse order p < N_d, the fine state is
-// interpolated along d (I, reading A3), the isolated residual at the coarse
-// orders is formed on chip, and
-//   tau~ = I(Qdot_ref) - Qdot_c,   tau = J w w w tau~ (traditional),
-//   tau[e][d][p] = max over coarse nodes and variables |tau|.
-// ---------------------------------------------------------------------------
-
-struct TauParams {
-    const double* q;
-    const double* qref;   // SOLVER reference or nullptr (SAME)
-    double* tau;          // [E][3][9]
-    const int* orders;
-    const long long* off;
-    const double* hgeo;
-    const Tables* tab;
-    int formulation;
-    PhysDev ph;
-};
-
-// Isolated strong-form residual at orders O of a state held in registers for
-// the CTA's owned nodes (t = tid + it*BLOCK < nO):  acc = sum_d (2/h_d) D f_d,
-// i.e. Qdot = -acc.  Fs is scratch of 5*nO doubles.
-__device__ __forceinline__ void iso_residual_regs(const int O[3], int nO, const double (&qc)[NPT][NV],
-                                                  double (&acc)[NPT][NV], double* Fs, const double* h,
-                                                  const Tables* tab, double gm1)
-{
-    const int tid = threadIdx.x;
-    const int o1 = O[0] + 1, o2 = O[1] + 1;
-#pragma unroll
-    for (int it = 0; it < NPT; ++it)
-#pragma unroll
-        for (int v = 0; v < NV; ++v) acc[it][v] = 0.0;
-    for (int d = 0; d < 3; ++d) {
-#pragma unroll
-        for (int it = 0; it < NPT; ++it) {
-            const int t = tid + it * BLOCK;
-            if (t < nO) {
-                double f[NV], p;
-                flux_dir(qc[it], gm1, d, f, &p);
-                for (int v = 0; v < NV; ++v) Fs[v * nO + t] = f[v];
-            }
-        }
-        __syncthreads();
-        const int nd = O[d] + 1;
-        const int stride = d == 0 ? 1 : (d == 1 ? o1 : o1 * o2);
-        const double* Dd = tab->D[O[d]];
-        const double sc = 2.0 / h[d];
-#pragma unroll
-        for (int it = 0; it < NPT; ++it) {
-            const int t = tid + it * BLOCK;
-            if (t < nO) {
-                int ijk[3];
-                node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
-                const int a = ijk[d];
-                const int base = t - a * stride;
-                for (int v = 0; v < NV; ++v) {
-                    double s = 0.0;
-                    for (int m = 0; m < nd; ++m) s += __ldg(&Dd[a * nd + m]) * Fs[v * nO + base + m * stride];
-                    acc[it][v] += sc * s;
-                }
-            }
-        }
-        __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(BLOCK) k_tau(TauParams P)
-{
-    extern __shared__ double sm[];
-    __shared__ double red[32];
-    const int e = blockIdx.x;
-    const int tid = threadIdx.x;
-    int N[3] = {P.orders[3 * e], P.orders[3 * e + 1], P.orders[3 * e + 2]};
-    const int n1 = N[0] + 1, n2 = N[1] + 1, n3 = N[2] + 1;
-    const int n = n1 * n2 * n3;
-    double h[3] = {P.hgeo[3 * e], P.hgeo[3 * e + 1], P.hgeo[3 * e + 2]};
-    const long long o = P.off[e];
-    double* qs = sm;           // 5n
-    double* Rs = qs + NV * n;  // 5n
-    double* Fs = Rs + NV * n;  // 5n
-    for (int t = tid; t < NV * n; t += BLOCK) qs[t] = P.q[o + t];
-    const double gm1 = P.ph.gm1;
-    double qc[NPT][NV], acc[NPT][NV];
-    if (P.qref) {
-        for (int t = tid; t < NV * n; t += BLOCK) Rs[t] = P.qref[o + t];
-        __syncthreads();
-    } else {  // SAME reference: isolated fine residual (reading A4)
-        __syncthreads();
-#pragma unroll
-        for (int it = 0; it < NPT; ++it) {
-            const int t = tid + it * BLOCK;
-#pragma unroll
-            for (int v = 0; v < NV; ++v) qc[it][v] = t < n ? qs[v * n + t] : 1.0;
-        }
-        iso_residual_regs(N, n, qc, acc, Fs, h, P.tab, gm1);
-#pragma unroll
-        for (int it = 0; it < NPT; ++it) {
-            const int t = tid + it * BLOCK;
-            if (t < n)
-                for (int v = 0; v < NV; ++v) Rs[v * n + t] = -acc[it][v];
-        }
-        __syncthreads();
-    }
-    double rn = 0.0;
-    for (int t = tid; t < NV * n; t += BLOCK) rn = fmax(rn, fabs(Rs[t]));
-    rn = block_max(rn, red);
-    if (tid == 0)
-        for (int d = 0; d < 3; ++d) {
-            P.tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV + 0] = rn;
-            for (int p = N[d]; p < DG_TAU_STRIDE_DEV; ++p)
-                P.tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV + p] = __longlong_as_double(0x7ff8000000000000LL);
-        }
-    const double Jel = h[0] * h[1] * h[2] / 8.0;
-    for (int d = 0; d < 3; ++d) {
-        const int nd = N[d] + 1;
-        const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
-        for (int p = 1; p < N[d]; ++p) {
-            int O[3] = {N[0], N[1], N[2]};
-            O[d] = p;
-            const int o1 = O[0] + 1, o2 = O[1] + 1;
-            const int nO = o1 * o2 * (O[2] + 1);
-            const double* T = P.tab->T[N[d]][p];
-            // q_c = T^{N_d -> p} q along d
-#pragma unroll
-            for (int it = 0; it < NPT; ++it) {
-                const int t = tid + it * BLOCK;
-                if (t < nO) {
-                    int ijk[3];
-                    node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
-                    const int ic = ijk[d];
-                    ijk[d] = 0;
-                    const int base = ijk[0] + n1 * (ijk[1] + n2 * ijk[2]);
-                    for (int v = 0; v < NV; ++v) {
-                        double s = 0.0;
-                        for (int a = 0; a < nd; ++a) s += __ldg(&T[ic * nd + a]) * qs[v * n + base + a * stride];
-                        qc[it][v] = s;
-                    }
-                } else {
-                    for (int v = 0; v < NV; ++v) qc[it][v] = 1.0;
-                }
-            }
-            iso_residual_regs(O, nO, qc, acc, Fs, h, P.tab, gm1);
-            double tmax = 0.0;
-#pragma unroll
-            for (int it = 0; it < NPT; ++it) {
-                const int t = tid + it * BLOCK;
-                if (t < nO) {
-                    int ijk[3];
-                    node_ijk(t, o1, o2, ijk[0], ijk[1], ijk[2]);
-                    const int ic = ijk[d];
-                    double scale = 1.0;
-                    if (P.formulation == 1)
-                        scale = Jel * P.tab->w[O[0]][ijk[0]] * P.tab->w[O[1]][ijk[1]] * P.tab->w[O[2]][ijk[2]];
-                    ijk[d] = 0;
-                    const int base = ijk[0] + n1 * (ijk[1] + n2 * ijk[2]);
-                    for (int v = 0; v < NV; ++v) {
-                        double s = 0.0;
-                        for (int a = 0; a < nd; ++a) s += __ldg(&T[ic * nd + a]) * Rs[v * n + base + a * stride];
-                        tmax = fmax(tmax, fabs(scale * (s + acc[it][v])));
-                    }
-                }
-            }
-            tmax = block_max(tmax, red);
-            if (tid == 0) P.tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV + p] = tmax;
-        }
-    }
 }
 
 // ---------------------------------------------------------------------------

@@ -107,6 +107,7 @@ struct NsElemParams {
     int mode;
     unsigned long long* lam_max;  // CFL / DFL rates of q' (2 slots), last RK stage
     PhysDev ph;
+    int* flag;                    // admissibility: [0] violations, [1] first element (reading A25)
 };
 
 // ---------------------------------------------------------------------------
@@ -452,6 +453,7 @@ __device__ __forceinline__ void cons_sync() { asm volatile("bar.sync 1, %0;\n" :
 struct NsStageMeta {
     int cnt, ord;
     int qsh[NS_MAXSLOTS];
+    int e[NS_MAXSLOTS];
     long long off[NS_MAXSLOTS];
 };
 
@@ -521,6 +523,7 @@ __device__ __forceinline__ void ns_produce(const NsElemParams& P, int item, doub
             if (faces) bytes += (unsigned)(ns_fblk(hblk, EXT, f >> 1, nl[f >> 1]) * 8);
         }
         M.qsh[lane] = (int)(off & 1);
+        M.e[lane] = e;
         M.off[lane] = off;
         if (clip) st[Lo.q0 + lane * Lo.qs + (b - a)] = P.q[b];  // last 8 bytes by hand (buffer end)
     }
@@ -794,6 +797,10 @@ __global__ void __launch_bounds__(NS_THREADS, 2) k_ns_res(NsElemParams P, int ni
             double qv[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) qv[v] = Qs[v * n + t];
+            {  // admissibility (reading A25)
+                const double pr = P.ph.gm1 * (qv[4] - 0.5 * (qv[1] * qv[1] + qv[2] * qv[2] + qv[3] * qv[3]) / qv[0]);
+                if (!(qv[0] > 0.0 && pr > 0.0) && atomicAdd(P.flag, 1) == 0) P.flag[1] = M.e[slot];
+            }
             ViscNode V;
             if (NSF) {
                 double gv[15];
