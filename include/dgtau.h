@@ -203,6 +203,19 @@ dg_status dg_rk_stage(dg_ctx* ctx, int stage, const double* q_in_dev, double* q_
  * levels included: their contexts borrow this buffer) overwrites it. */
 dg_status dg_gradient(dg_ctx* ctx, int variant, const double* q_dev, void* stream);
 double* dg_gradient_buffer(dg_ctx* ctx);
+/* Face-trace halo copies (north_star "face-trace halos"): the
+ * face kernels read only the nodes of a neighbour's face toward an owned
+ * element, so a rank exchanges partition-boundary face TRACES, not element
+ * states.  entries_dev: int64 [n][2] device array, entry i = (offset into
+ * buf_dev, 8 * local element id + face f), f = 2 d + s (s = 1: the +xi_d
+ * face); field_dev: the state (ncomp = 5, element e at its state offset) or
+ * the gradient buffer (ncomp = 15, at 3 x the offset); the trace of component
+ * c at face point pt = ta + n_a tb is buf[offset + c * nf + pt] (nf = face
+ * points).  direction 0 packs field -> buf, 1 unpacks buf -> the face nodes of
+ * field.  Stream-ordered, no synchronisation; the caller owns every buffer
+ * (partition.TracePlan builds the entries; dist.py posts the NCCL send/recv). */
+dg_status dg_trace_copy(dg_ctx* ctx, const int64_t* entries_dev, int n, double* field_dev, int ncomp, double* buf_dev,
+                        int direction, void* stream);
 /* dg_rhs_eval with flags (DG_FLAG_GRADIENT_READY). */
 dg_status dg_rhs_eval_flags(dg_ctx* ctx, int variant, const double* q_dev, double* qdot_dev, int flags, void* stream);
 /* Max-reduce the CFL/DFL rates of q (owned elements) into lam_accum_dev. */

@@ -40,7 +40,7 @@ EXPORTS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_upload", "dg_set
            "dg_node_coords", "dg_rhs_eval", "dg_compute_dt", "dg_rk_step", "dg_tau_estimate", "dg_select_orders",
            "dg_transfer", "dg_diagnostics", "dg_launch_count", "dg_rk_step_dt", "dg_set_owned", "dg_rk_stage",
            "dg_dt_accumulate", "dg_dt_finalize", "dg_select_local", "dg_jump_sweep", "dg_owned_state_len", "dg_gradient",
-           "dg_gradient_buffer", "dg_rhs_eval_flags", "dg_rk_steps"]
+           "dg_gradient_buffer", "dg_rhs_eval_flags", "dg_rk_steps", "dg_trace_copy"]
 
 
 def sources():
@@ -345,6 +345,18 @@ class Solver:
         pol = _Policy(int(mode), float(tau_max), int(Nmin), int(Nmax), JUMP_B, int(dec_cap), COMBINE_MAX, 0)
         self._check(self.L.dg_select_local(self.ctx, C.byref(pol), _ptr(tau), _ptr(total_map), _ptr(out), None,
                                            _stream(stream)), "dg_select_local")
+
+    def trace_copy(self, entries, field, ncomp, buf, direction, stream=None):
+        """Pack (direction 0: field -> buf) or unpack (1: buf -> face nodes of
+        field) partition-boundary face traces (partition.TracePlan entries,
+        int64 [n][2] on the device)."""
+        import torch
+
+        n = int(entries.shape[0])
+        self._check(self.L.dg_trace_copy(self.ctx, _dptr(entries, 2 * n, "trace entries", torch.int64), n,
+                                         _dptr(field, (ncomp // 5) * self.state_len, "trace field"), int(ncomp),
+                                         _dptr(buf, 0, "trace buffer"), int(direction), _stream(stream)),
+                    "dg_trace_copy")
 
     def jump_sweep(self, a, b, rule, Nmax, changed, stream=None):
         self._check(self.L.dg_jump_sweep(self.ctx, _ptr(a), _ptr(b), int(rule), int(Nmax), _ptr(changed),

@@ -1778,6 +1778,21 @@ dg_status dg_gradient(dg_ctx* ctx, int variant, const double* q_dev, void* strea
 
 double* dg_gradient_buffer(dg_ctx* ctx) { return ctx ? ctx->d_grad : nullptr; }
 
+dg_status dg_trace_copy(dg_ctx* ctx, const int64_t* entries_dev, int n, double* field_dev, int ncomp, double* buf_dev,
+                        int direction, void* stream)
+{
+    if (!ctx || n < 0 || (n > 0 && (!entries_dev || !field_dev || !buf_dev))) return DG_EINVAL;
+    if (ncomp != NV && ncomp != 3 * NV) return fail(ctx, DG_EINVAL, "trace_copy: ncomp must be 5 (state) or 15 (gradient)");
+    if (direction != 0 && direction != 1) return fail(ctx, DG_EINVAL, "trace_copy: direction 0 (pack) or 1 (unpack)");
+    if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "trace_copy: orders not set");
+    if (n == 0) return DG_OK;
+    k_trace_copy<<<(n + 3) / 4, 128, 0, (cudaStream_t)stream>>>(reinterpret_cast<const long long*>(entries_dev), n,
+                                                                 ctx->d_orders, ctx->d_off, field_dev, ncomp, buf_dev,
+                                                                 direction);
+    ctx->launches++;
+    return check_stream_error(ctx, "k_trace_copy launch");
+}
+
 dg_status dg_rhs_eval_flags(dg_ctx* ctx, int variant, const double* q_dev, double* qdot_dev, int flags, void* stream)
 {
     if (!ctx || !q_dev || !qdot_dev) return DG_EINVAL;

@@ -366,4 +366,35 @@ __global__ void __launch_bounds__(BLOCK) k_diag(DiagParams P)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Face-trace halo copies (partition.TracePlan): entry i =
+// (buffer offset, 8 e + f); the trace of field component c (ncomp per node,
+// element block at (ncomp / 5) x off[e]) on face f of element e at face point
+// pt = ta + n_a tb is buf[offset + c nf + pt].  dir 0: field -> buf (pack),
+// 1: buf -> field (unpack into the halo element's face nodes).  One warp per
+// entry.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_trace_copy(const long long* ent, int n, const int* orders, const long long* off,
+                                                    double* field, int ncomp, double* buf, int dir)
+{
+    const int i = blockIdx.x * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const long long boff = ent[2 * i];
+    const int e = (int)(ent[2 * i + 1] >> 3), f = (int)(ent[2 * i + 1] & 7);
+    const int d = f >> 1, s = f & 1;
+    const int N[3] = {orders[3 * e] + 1, orders[3 * e + 1] + 1, orders[3 * e + 2] + 1};
+    const int st[3] = {1, N[0], N[0] * N[1]};
+    const int ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
+    const int na = N[ta], nf = na * N[tb], nn = st[2] * N[2];
+    const int base = s ? (N[d] - 1) * st[d] : 0;
+    double* blk = field + (long long)(ncomp / NV) * off[e];
+    for (int idx = lane; idx < ncomp * nf; idx += 32) {
+        const int c = idx / nf, pt = idx - c * nf;
+        const int b = pt / na, a = pt - b * na;
+        double* x = blk + (long long)c * nn + base + a * st[ta] + b * st[tb];
+        if (dir == 0) buf[boff + idx] = *x;
+        else *x = buf[boff + idx];
+    }
+}
+
 }  // namespace dgtau

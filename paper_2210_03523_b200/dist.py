@@ -3,7 +3,11 @@ NVLink/NVSwitch on GPUs, gloo on CPU for tests) for the halo exchange and
 the global reductions; every numerical step runs in libdgtau's kernels.
 
 Per residual evaluation (RK stage, SOLVER reference) one halo exchange of
-element states with the face-neighbour ranks; per RK step one MAX
+partition-boundary FACE TRACES of the state with the face-neighbour ranks
+(NS: a second one of the gradient's face traces after the BR1 pass) --
+packed and unpacked on the device by dg_trace_copy, sent with NCCL P2P
+(partition.TracePlan; a rank's halo elements only ever have their faces
+toward owned elements read); per RK step one MAX
 all-reduce of the CFL/DFL rates (dt = CFL / global max, reading A11); per
 jump-fixpoint sweep one exchange of halo orders and one MAX all-reduce of the
 `changed` flag (the fixpoint is monotone, so the result is rank-count
@@ -46,6 +50,41 @@ def exchange(tensor, plan: "part.HaloPlan", rank: int, group=None):
         for a, b in rruns:
             tensor[a:b].copy_(rbuf[o:o + b - a])
             o += b - a
+
+
+class TraceExchange:
+    """Device-side face-trace exchange of one field (state: ncomp 5, or the
+    BR1 gradient: ncomp 15) for a DistSolver's current layout: per peer rank
+    the entry tables (partition.TracePlan) on the device and persistent
+    send / receive buffers."""
+
+    def __init__(self, S, plan: "part.TracePlan"):
+        import torch
+
+        self.S, self.plan = S, plan
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.send = {r: torch.from_numpy(t).to(dev) for r, t in plan.send.items()}
+        self.recv = {r: torch.from_numpy(t).to(dev) for r, t in plan.recv.items()}
+        self.sbuf = {r: torch.empty(max(1, plan.send_len[r]), dtype=torch.float64, device=dev) for r in plan.send}
+        self.rbuf = {r: torch.empty(max(1, plan.recv_len[r]), dtype=torch.float64, device=dev) for r in plan.recv}
+
+    def bytes_per_exchange(self):
+        return 8 * sum(self.plan.send_len.values())
+
+    def __call__(self, field, group=None):
+        import torch.distributed as dist
+
+        nc = self.plan.ncomp
+        ops = []
+        for r in sorted(self.send):
+            self.S.trace_copy(self.send[r], field, nc, self.sbuf[r], 0)
+            ops.append(dist.P2POp(dist.isend, self.sbuf[r][: max(1, self.plan.send_len[r])], r, group))
+            ops.append(dist.P2POp(dist.irecv, self.rbuf[r][: max(1, self.plan.recv_len[r])], r, group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        for r in sorted(self.recv):
+            self.S.trace_copy(self.recv[r], field, nc, self.rbuf[r], 1)
 
 
 def migrate(q_owned, plan: "part.MigrationPlan", group=None):
@@ -104,8 +143,9 @@ class DistSolver:
         lo = np.ascontiguousarray(np.asarray(global_orders)[self.lm.gids], np.int32)
         self.S.set_orders(lo)
         self.local_orders = lo
-        self.plan = part.HaloPlan(self.lm, lo, 5)
-        self.gplan = part.HaloPlan(self.lm, lo, 15)
+        self.plan = part.HaloPlan(self.lm, lo, 5)  # whole element states (rebalancing refresh)
+        self.tq = TraceExchange(self.S, part.TracePlan(self.lm, lo, 5))
+        self.tg = TraceExchange(self.S, part.TracePlan(self.lm, lo, 15)) if self.physics == 1 else None
 
     @property
     def n_own(self):
@@ -118,6 +158,11 @@ class DistSolver:
         return self.S.new_state()
 
     def halo(self, q):
+        """face traces of the state toward owned elements (what the residual reads)"""
+        self.tq(q, self.group)
+
+    def halo_states(self, q):
+        """whole element states of the halo (after a repartition)"""
         exchange(q, self.plan, self.rank, self.group)
 
     # -- operators -----------------------------------------------------------
@@ -130,7 +175,7 @@ class DistSolver:
             return 0
         self.S.gradient(q, variant)
         if variant == 0:
-            exchange(self.S.gradient_buffer(), self.gplan, self.rank, self.group)
+            self.tg(self.S.gradient_buffer(), self.group)
         return FLAG_GRADIENT_READY
 
     def rhs_eval(self, q, qdot=None, variant=0):
@@ -235,5 +280,5 @@ def rebalance(ds: DistSolver, global_orders, q_local, axis: int = 2):
     n = part.element_offsets(go[nd.lm.gids])
     q_new = torch.zeros(int(n[-1]), dtype=q_local.dtype, device=q_local.device)
     q_new[: q_own.numel()].copy_(q_own)
-    nd.halo(q_new)
+    nd.halo_states(q_new)
     return nd, q_new

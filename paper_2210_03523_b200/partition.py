@@ -156,6 +156,70 @@ class HaloPlan:
         assert set(self.send) == set(self.recv), "face adjacency is symmetric"
 
 
+# face f = 2 d + s of an element: tangential directions (a, b) of d
+_TAN = ((1, 2), (0, 2), (0, 1))
+
+
+def face_points(orders_e, f: int) -> int:
+    """Nodes of face f of an element of orders (N1, N2, N3)."""
+    a, b = _TAN[f >> 1]
+    return int((orders_e[a] + 1) * (orders_e[b] + 1))
+
+
+class TracePlan:
+    """Face-trace halo plan (one exchange of partition-boundary
+    face traces per residual, two for NS): the face kernels read only the
+    nodes of a neighbour element's face toward the owned element, so instead
+    of whole element states a rank sends, for every face between one of its
+    owned elements A and an element owned by rank r, the trace of A on that
+    face (ncomp components x face points, [comp][pt] with pt = ta + n_a tb),
+    and receives the traces of r's elements into the same face nodes of its
+    halo copies.  Entries are ordered by (global id, face) on both sides, so
+    rank r's send list and this rank's receive list from r match one to one.
+    Per peer: `send[r]` / `recv[r]` int64 arrays [n][2] = (buffer offset,
+    8 local_id + face) for dg_trace_copy, and the buffer lengths."""
+
+    def __init__(self, lm: LocalMesh, local_orders: np.ndarray, ncomp: int = 5):
+        orders = np.asarray(local_orders)
+        owner_local = np.full(lm.E, lm.rank, np.int64)
+        for r, ids in lm.recv.items():
+            owner_local[ids] = r
+        gids = lm.gids
+        owned = np.arange(lm.n_own)
+        self.ncomp = ncomp
+        self.send, self.recv, self.send_len, self.recv_len = {}, {}, {}, {}
+        peers = sorted(set(lm.send) | set(lm.recv))
+        for r in peers:
+            # send: faces of owned elements whose neighbour is a halo element of rank r
+            ent = []
+            for e in owned:
+                for f in range(6):
+                    nb = lm.nbr[e, f]
+                    if nb >= lm.n_own and owner_local[nb] == r:
+                        ent.append((int(gids[e]), f, int(e)))
+            # receive: faces of rank r's halo elements toward an owned element
+            rec = []
+            for h in range(lm.n_own, lm.E):
+                if owner_local[h] != r:
+                    continue
+                for f in range(6):
+                    nb = lm.nbr[h, f]
+                    if 0 <= nb < lm.n_own:
+                        rec.append((int(gids[h]), f, int(h)))
+            self.send[r], self.send_len[r] = self._table(sorted(ent), orders, ncomp)
+            self.recv[r], self.recv_len[r] = self._table(sorted(rec), orders, ncomp)
+
+    @staticmethod
+    def _table(entries, orders, ncomp):
+        t = np.zeros((len(entries), 2), np.int64)
+        o = 0
+        for i, (_, f, e) in enumerate(entries):
+            t[i, 0] = o
+            t[i, 1] = 8 * e + f
+            o += ncomp * face_points(orders[e], f)
+        return t, o
+
+
 class MigrationPlan:
     """Element moves between two partitions (old_owner -> new_owner) seen from
     `rank`: per peer, the global ids it sends (its old owned elements that the

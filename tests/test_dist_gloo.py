@@ -147,6 +147,96 @@ def test_two_rank_halo_rhs_rk_jump():
         assert res[r]["n_halo"] > 0
 
 
+def _np_trace(entries, field, orders, ncomp, buf, direction):
+    """numpy stand-in for dg_trace_copy (test side): entry (offset, 8 e + f)."""
+    from paper_2210_03523_b200.partition import _TAN
+
+    off = W.offsets(orders, ncomp)
+    for boff, code in entries:
+        e, f = int(code) >> 3, int(code) & 7
+        d, s = f >> 1, f & 1
+        N = orders[e] + 1
+        blk = field[off[e]:off[e + 1]].reshape(ncomp, N[2], N[1], N[0])  # [c][k][j][i]
+        sl = [slice(None)] * 3
+        sl[2 - d] = N[d] - 1 if s else 0
+        ta, tb = _TAN[d]
+        tr = blk[(slice(None),) + tuple(sl)]  # [c][..][..] over the two tangential axes, slowest first
+        # face point pt = ta + n_a tb: the array's last axis is the faster of (ta, tb)
+        nf = N[ta] * N[tb]
+        if direction == 0:
+            buf[boff:boff + ncomp * nf] = tr.reshape(ncomp, nf).ravel()
+        else:
+            tr[...] = buf[boff:boff + ncomp * nf].reshape(tr.shape)
+
+
+def _trace_worker(rank, world, port, out_q):
+    """Face-trace halos on gloo: only the traces a rank's residual reads are
+    exchanged; every other halo node holds a poison value; the owned residual
+    still equals the global one bit for bit (Euler, mixed orders, mortars)."""
+    import torch
+    import torch.distributed as dist
+
+    import oracle
+    from paper_2210_03523_b200 import partition as part
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        res = {}
+        mesh = W.cube_mesh(4, 3, 6)
+        g_orders = W.orders_random(mesh.E, 2, 6, 21)
+        owner = part.slab_owner(mesh.dims, world, axis=2)
+        lm = part.local_mesh(mesh, owner, rank)
+        lo = g_orders[lm.gids]
+        P = oracle.Problem(mesh)
+        q_g = W.pulse_state(P.node_coords(g_orders), g_orders, center=(0.4, 0.6, 0.5), sigma=0.2)
+        r_g = P.rhs(g_orders, q_g)
+        blocks = _per_elem(q_g, g_orders)
+        q_l = np.concatenate([blocks[g] if i < lm.n_own else np.full_like(blocks[g], 123.456)
+                              for i, g in enumerate(lm.gids)])
+        tp = part.TracePlan(lm, lo, 5)
+        hp = part.HaloPlan(lm, lo, 5)
+        ops, rbufs = [], {}
+        for r in sorted(tp.send):
+            sb = np.zeros(tp.send_len[r])
+            _np_trace(tp.send[r], q_l, lo, 5, sb, 0)
+            rbufs[r] = torch.zeros(tp.recv_len[r], dtype=torch.float64)
+            ops.append(dist.P2POp(dist.isend, torch.from_numpy(sb), r))
+            ops.append(dist.P2POp(dist.irecv, rbufs[r], r))
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+        for r in sorted(tp.recv):
+            _np_trace(tp.recv[r], q_l, lo, 5, rbufs[r].numpy(), 1)
+        r_l = oracle.Problem(lm).rhs(lo, q_l)
+        rb = _per_elem(r_g, g_orders)
+        owned = np.concatenate([rb[g] for g in lm.gids[: lm.n_own]])
+        res["rhs_owned_exact"] = bool(np.array_equal(r_l[: len(owned)], owned))
+        res["trace_doubles"] = int(sum(tp.send_len.values()))
+        res["state_doubles"] = int(sum(hp.send_len.values()))
+        out_q.put((rank, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(600)
+def test_two_rank_face_trace_halo():
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_trace_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=500) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    for r in range(2):
+        assert out[r]["rhs_owned_exact"], (r, out[r])
+        assert out[r]["trace_doubles"] < out[r]["state_doubles"]
+
+
 def test_slab_partition_plans():
     from paper_2210_03523_b200 import partition as part
 

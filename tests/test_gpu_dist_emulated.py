@@ -35,8 +35,27 @@ def _copy_halos(solvers, plans, states):
                 o += b - a
 
 
+def _copy_traces(solvers, tplans, states, ncomp):
+    """Face-trace halo exchange (partition.TracePlan, dg_trace_copy): every
+    rank packs the traces its peers read, each peer unpacks them into the face
+    nodes of its halo copies (the device copy stands in for the NCCL send)."""
+    import torch
+
+    for r, pl in enumerate(tplans):
+        for peer in sorted(pl.send):
+            buf = torch.empty(max(1, pl.send_len[peer]), dtype=torch.float64, device="cuda")
+            solvers[r].trace_copy(torch.from_numpy(pl.send[peer]).cuda(), states[r], ncomp, buf, 0)
+            rp = tplans[peer]
+            assert rp.recv_len[r] == pl.send_len[peer]
+            solvers[peer].trace_copy(torch.from_numpy(rp.recv[r]).cuda(), states[peer], ncomp, buf, 1)
+
+
+@pytest.mark.parametrize("halo", ["states", "traces"])
 @pytest.mark.parametrize("case", ["cube_mixed", "ogrid_ns", "cube_rebalanced"])
-def test_two_rank_emulated(dg, orc, case):
+def test_two_rank_emulated(dg, orc, case, halo):
+    """halo = "traces": only partition-boundary face traces are exchanged and
+    every other node of the halo copies is NaN -- the owned results are still
+    bit-identical, so nothing reads beyond the traces."""
     import torch
 
     from paper_2210_03523_b200 import partition as part
@@ -81,9 +100,14 @@ def test_two_rank_emulated(dg, orc, case):
         lo = g_orders[lm.gids]
         S.set_orders(lo)
         solvers.append(S)
-        plans.append(part.HaloPlan(lm, lo, 5))
-        gplans.append(part.HaloPlan(lm, lo, 15))
-        x = torch.from_numpy(np.concatenate([blocks[g] for g in lm.gids])).cuda()
+        if halo == "states":
+            plans.append(part.HaloPlan(lm, lo, 5))
+            gplans.append(part.HaloPlan(lm, lo, 15))
+        else:
+            plans.append(part.TracePlan(lm, lo, 5))
+            gplans.append(part.TracePlan(lm, lo, 15))
+        x = torch.from_numpy(np.concatenate([blocks[g] if i < lm.n_own else np.full_like(blocks[g], np.nan)
+                                             for i, g in enumerate(lm.gids)])).cuda()
         qa.append(x)
         qb.append(torch.empty_like(x))
         gg.append(torch.empty_like(x))
@@ -101,12 +125,18 @@ def test_two_rank_emulated(dg, orc, case):
         for r in range(2):
             lam[r].zero_()
         for k in range(3):
-            _copy_halos(solvers, plans, src[k])
+            if halo == "states":
+                _copy_halos(solvers, plans, src[k])
+            else:
+                _copy_traces(solvers, plans, src[k], 5)
             flags = 0
             if case == "ogrid_ns":  # BR1: gradient pass, gradient halo refresh, then the flux pass
                 for r in range(2):
                     solvers[r].gradient(src[k][r])
-                _copy_halos(solvers, gplans, [S.gradient_buffer() for S in solvers])
+                if halo == "states":
+                    _copy_halos(solvers, gplans, [S.gradient_buffer() for S in solvers])
+                else:
+                    _copy_traces(solvers, gplans, [S.gradient_buffer() for S in solvers], 15)
                 flags = dg.FLAG_GRADIENT_READY
             for r in range(2):
                 solvers[r].rk_stage(k, src[k][r], dst[k][r], gg[r], dts[s % 2], lam[r] if k == 2 else None, flags)
