@@ -1119,8 +1119,15 @@ __device__ __forceinline__ void mortar_to_side(const double* Fm, int nc, int ma,
     grp_sync<W>(gid);
 }
 
+// resident CTAs per SM the register budget targets: the BR1 qhat pass fits in
+// 80 registers without spills (more faces in flight), the NS flux needs 128
+__host__ __device__ constexpr int face_minb(int W, int MODE)
+{
+    return MODE == MODE_QHAT ? (W == 1 ? 6 : 4) : (W == 3 ? 2 : 4);
+}
+
 template <int W, int MODE>
-__global__ void __launch_bounds__(FaceCfg<W>::BS, FaceCfg<W>::MINB) k_ns_face(NsFaceParams P)
+__global__ void __launch_bounds__(FaceCfg<W>::BS, face_minb(W, MODE)) k_ns_face(NsFaceParams P)
 {
     using C = FaceCfg<W>;
     constexpr int CAP = C::CAP;
