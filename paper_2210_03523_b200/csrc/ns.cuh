@@ -537,6 +537,8 @@ __device__ __forceinline__ void ns_produce(const NsElemParams& P, int item, doub
     if (lane == 0) mbar_expect_tx(full, bytes);
     __syncwarp();
     if (lane < it.count) {
+        // residual kernel, RK stages 2-3: the register g is read in the epilogue -> into L2 now
+        if (!hblk && P.mode == 1 && P.rkA != 0.0) bulk_prefetch_l2(P.g + a, (unsigned)((b - a) * 8));
         bulk_g2s(st + Lo.q0 + lane * Lo.qs, P.q + a, (unsigned)((b - a) * 8), full);
         bulk_g2s(st + Lo.m0 + lane * Lo.ms, (EXT ? P.metc : P.met) + mo, (unsigned)(Lo.ms * 8), full);
         if (faces) {
