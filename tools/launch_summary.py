@@ -16,9 +16,10 @@ for r in rows:
     if d.get("Metric Name") != "gpu__time_duration.sum":
         continue
     v = float(d["Metric Value"].replace(",", ""))
-    if d.get("Metric Unit") == "nsecond":
+    unit = d.get("Metric Unit")
+    if unit in ("nsecond", "ns"):
         v /= 1e3
-    elif d.get("Metric Unit") == "msecond":
+    elif unit in ("msecond", "ms"):
         v *= 1e3
     k = d["Kernel Name"]
     c = tot.setdefault(k, [0, 0.0])
