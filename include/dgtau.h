@@ -203,6 +203,20 @@ dg_status dg_rk_stage(dg_ctx* ctx, int stage, const double* q_in_dev, double* q_
  * levels included: their contexts borrow this buffer) overwrites it. */
 dg_status dg_gradient(dg_ctx* ctx, int variant, const double* q_dev, void* stream);
 double* dg_gradient_buffer(dg_ctx* ctx);
+/* Non-isolated tau-estimation of ONE coarse level (d, p) on a rank-local mesh
+ * (reading R7), in two phases.  phase 0:
+ * builds the level's context (the local mesh at orders O = N with O_d =
+ * min(p, N_d), owned count kept; once per layout, owned by ctx, returned in
+ * *level_out), interpolates q_dev and qref_dev (the SOLVER reference) to it
+ * and (NS) forms its BR1 gradient of the owned elements.  The caller then
+ * refreshes the halo face traces of that gradient (dg_trace_copy on
+ * *level_out, field = dg_gradient_buffer(*level_out), ncomp 15) -- the halo's
+ * coarse STATE traces need no exchange (GL interpolation maps a face trace to
+ * the coarse face trace alone).  phase 1: the level's face-coupled residual,
+ * then tau[e][d][p] of the owned elements (tau_dev [E][3][9], o->formulation
+ * and o->restriction as dg_tau_estimate).  Stream-ordered. */
+dg_status dg_tau_level(dg_ctx* ctx, int d, int p, int phase, const dg_tau_opts* o, const double* q_dev,
+                       const double* qref_dev, double* tau_dev, dg_ctx** level_out, void* stream);
 /* Face-trace halo copies (north_star "face-trace halos"): the
  * face kernels read only the nodes of a neighbour's face toward an owned
  * element, so a rank exchanges partition-boundary face TRACES, not element

@@ -40,7 +40,7 @@ EXPORTS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_upload", "dg_set
            "dg_node_coords", "dg_rhs_eval", "dg_compute_dt", "dg_rk_step", "dg_tau_estimate", "dg_select_orders",
            "dg_transfer", "dg_diagnostics", "dg_launch_count", "dg_rk_step_dt", "dg_set_owned", "dg_rk_stage",
            "dg_dt_accumulate", "dg_dt_finalize", "dg_select_local", "dg_jump_sweep", "dg_owned_state_len", "dg_gradient",
-           "dg_gradient_buffer", "dg_rhs_eval_flags", "dg_rk_steps", "dg_trace_copy"]
+           "dg_gradient_buffer", "dg_rhs_eval_flags", "dg_rk_steps", "dg_trace_copy", "dg_tau_level"]
 
 
 def sources():
@@ -192,6 +192,33 @@ def _stream(stream):
 
     s = torch.cuda.current_stream() if stream is None else stream
     return C.c_void_p(s.cuda_stream)
+
+
+class Level:
+    """Borrowed handle of a non-isolated tau level's context (owned by its
+    parent Solver's context; valid until the parent's next set_orders)."""
+
+    def __init__(self, L, ctx, state_len):
+        self.L, self.ctx, self.state_len = L, ctx, state_len
+
+    def _check(self, rc, what):
+        if rc != 0:
+            raise DGError(f"{what} failed ({rc}): {self.L.dg_last_error(self.ctx).decode()}")
+
+    def gradient_buffer(self):
+        ptr = self.L.dg_gradient_buffer(self.ctx)
+        if not ptr:
+            raise DGError("level: no gradient buffer")
+        return _device_view(ptr, 3 * self.state_len)
+
+    def trace_copy(self, entries, field, ncomp, buf, direction, stream=None):
+        import torch
+
+        n = int(entries.shape[0])
+        self._check(self.L.dg_trace_copy(self.ctx, _dptr(entries, 2 * n, "trace entries", torch.int64), n,
+                                         _dptr(field, (ncomp // 5) * self.state_len, "trace field"), int(ncomp),
+                                         _dptr(buf, 0, "trace buffer"), int(direction), _stream(stream)),
+                    "dg_trace_copy")
 
 
 class Solver:
@@ -377,6 +404,20 @@ class Solver:
                                            _dptr(tau, self.E * 3 * TAU_STRIDE, "tau_estimate tau"), _stream(stream)),
                     "dg_tau_estimate")
         return tau
+
+    def tau_level(self, d, p, phase, q=None, qdot_ref=None, tau=None, formulation=TAU_NEW, restriction=0, stream=None):
+        """One non-isolated tau level (d, p) in two phases (dg_tau_level, for
+        rank-local meshes): phase 0 -> Level handle (its BR1 gradient formed;
+        refresh its halo face traces), phase 1 writes tau[e][d][p]."""
+        o = _TauOpts(int(formulation), REF_SOLVER, 1, int(restriction))
+        lev = C.c_void_p()
+        n = self.state_len
+        self._check(self.L.dg_tau_level(self.ctx, int(d), int(p), int(phase), C.byref(o),
+                                        _dptr(q, n, "tau_level q", optional=phase == 1),
+                                        _dptr(qdot_ref, n, "tau_level qdot_ref", optional=phase == 1),
+                                        _dptr(tau, self.E * 3 * TAU_STRIDE, "tau_level tau", optional=phase == 0),
+                                        C.byref(lev), _stream(stream)), "dg_tau_level")
+        return Level(self.L, lev, int(self.L.dg_state_len(lev)))
 
     def select_orders(self, tau, tau_max, Nmin, Nmax, mode=SELECT_DYNAMIC, jump_rule=JUMP_B, dec_cap=1,
                       total_map=None, stream=None, combine=COMBINE_MAX, nstages=0):

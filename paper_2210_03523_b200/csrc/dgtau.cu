@@ -1905,6 +1905,7 @@ static dg_status build_level(dg_ctx* ctx, int d, int p, dg_ctx::CoarseLevel& L)
     if (s != DG_OK) return fail(ctx, s, "tau_estimate: coarse level context");
     if (ctx->curved) lend_scratch(ctx, L.sub);
     if ((s = dg_mesh_upload(L.sub, E, ctx->nbr.data(), ctx->gorder, ctx->geo.data())) != DG_OK ||
+        (ctx->n_own < E && (s = dg_set_owned(L.sub, ctx->n_own)) != DG_OK) ||
         (s = dg_set_orders(L.sub, oc.data())) != DG_OK)
         return fail(ctx, s, std::string("tau_estimate: coarse level: ") + dg_last_error(L.sub));
     if (upload(L.d_orders, oc) != cudaSuccess || upload(L.d_off, offc) != cudaSuccess)
@@ -1921,14 +1922,15 @@ static void free_level(dg_ctx* ctx, dg_ctx::CoarseLevel& L)
     dfree(L.d_off);
 }
 
-static dg_status run_level(dg_ctx* ctx, const dg_ctx::CoarseLevel& L, int formulation, int restr, const double* q_dev,
-                           const double* ref, double* tau_dev, cudaStream_t st)
+// phase 0: the state and the reference residual interpolated to the level's
+// layout (k_transfer); NS: the level's BR1 gradient of the owned elements.
+static dg_status level_phase0(dg_ctx* ctx, const dg_ctx::CoarseLevel& L, int restr, const double* q_dev, const double* ref,
+                              cudaStream_t st)
 {
     const int E = ctx->E;
     const long long len = ctx->off[E];
     double* qc = ctx->d_cq;
     double* rc = qc + len;
-    double* dc = rc + len;
     TransferParams T;
     T.oold = ctx->d_orders;
     T.onew = L.d_orders;
@@ -1945,14 +1947,51 @@ static dg_status run_level(dg_ctx* ctx, const dg_ctx::CoarseLevel& L, int formul
     T.qnew = rc;
     k_transfer<<<E, BLOCK, sm, st>>>(T);
     ctx->launches += 2;
-    dg_status s = launch_residual(L.sub, DG_NONISOLATED, qc, dc, nullptr, nullptr, 0.0, 0.0, 0, st);
+    if (ctx->prm.physics == DG_NS && L.sub->curved) {
+        dg_status s = dg_gradient(L.sub, DG_NONISOLATED, qc, st);
+        if (s != DG_OK) return fail(ctx, s, std::string("tau_estimate: coarse gradient: ") + dg_last_error(L.sub));
+        ctx->launches += L.sub->launches;
+        L.sub->launches = 0;
+    }
+    return check_stream_error(ctx, "non-isolated tau launch");
+}
+
+// phase 1: the level's face-coupled residual (its gradient ready) and the
+// per-element maxima |T R - Qdot_c| of the owned elements (k_tau_level).
+static dg_status level_phase1(dg_ctx* ctx, const dg_ctx::CoarseLevel& L, int formulation, double* tau_dev, cudaStream_t st)
+{
+    const long long len = ctx->off[ctx->E];
+    double* qc = ctx->d_cq;
+    double* rc = qc + len;
+    double* dc = rc + len;
+    const int flags = (ctx->prm.physics == DG_NS && L.sub->curved) ? DG_FLAG_GRADIENT_READY : 0;
+    dg_status s = launch_residual(L.sub, DG_NONISOLATED, qc, dc, nullptr, nullptr, 0.0, 0.0, 0, st, nullptr, flags);
     if (s != DG_OK) return fail(ctx, s, std::string("tau_estimate: coarse residual: ") + dg_last_error(L.sub));
     ctx->launches += L.sub->launches;
     L.sub->launches = 0;
-    k_tau_level<<<E, 128, 0, st>>>(rc, dc, ctx->d_orders, L.d_orders, L.d_off, L.d, L.p, formulation, ctx->d_h,
-                                   ctx->curved ? L.sub->d_met : nullptr, ctx->d_tab, tau_dev);
+    k_tau_level<<<ctx->n_own, 128, 0, st>>>(rc, dc, ctx->d_orders, L.d_orders, L.d_off, L.d, L.p, formulation, ctx->d_h,
+                                            ctx->curved ? L.sub->d_met : nullptr, ctx->d_tab, tau_dev);
     ctx->launches++;
     return check_stream_error(ctx, "non-isolated tau launch");
+}
+
+static dg_status run_level(dg_ctx* ctx, const dg_ctx::CoarseLevel& L, int formulation, int restr, const double* q_dev,
+                           const double* ref, double* tau_dev, cudaStream_t st)
+{
+    dg_status s = level_phase0(ctx, L, restr, q_dev, ref, st);
+    if (s != DG_OK) return s;
+    return level_phase1(ctx, L, formulation, tau_dev, st);
+}
+
+static dg_status ensure_cq(dg_ctx* ctx)
+{
+    const long long len = ctx->off[ctx->E];
+    if (ctx->c_len < 3 * len) {
+        dfree(ctx->d_cq);
+        CK(cudaMalloc(&ctx->d_cq, sizeof(double) * 3 * len));
+        ctx->c_len = 3 * len;
+    }
+    return DG_OK;
 }
 
 // Non-isolated tau-estimation (dg_tau_opts.coarse_faces = 1, reading R7):
@@ -1966,14 +2005,11 @@ static dg_status run_level(dg_ctx* ctx, const dg_ctx::CoarseLevel& L, int formul
 static dg_status tau_noniso(dg_ctx* ctx, int formulation, int restr, const double* q_dev, const double* ref,
                             double* tau_dev, cudaStream_t st)
 {
-    if (ctx->n_own != ctx->E) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: non-isolated levels need a single rank");
+    if (ctx->n_own != ctx->E)
+        return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: non-isolated levels on a rank-local mesh: use dg_tau_level "
+                                          "(the coarse gradient traces are exchanged between its two phases)");
     const int E = ctx->E;
-    const long long len = ctx->off[E];
-    if (ctx->c_len < 3 * len) {
-        dfree(ctx->d_cq);
-        CK(cudaMalloc(&ctx->d_cq, sizeof(double) * 3 * len));
-        ctx->c_len = 3 * len;
-    }
+    if (ensure_cq(ctx) != DG_OK) return DG_ECUDA;
     int nmax[3] = {0, 0, 0};
     for (int e = 0; e < E; ++e)
         for (int d = 0; d < 3; ++d) nmax[d] = std::max(nmax[d], ctx->orders[3 * e + d]);
@@ -2081,6 +2117,38 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
     }
     ctx->launches++;
     return check_stream_error(ctx, "k_tau launch");
+}
+
+// Non-isolated tau level (d, p) in two phases for rank-local meshes (SURVEY
+// 8(f) rank 1, include/dgtau.h): phase 0 builds the level's context once per
+// layout (the rank's local mesh at the level's orders, owned count kept),
+// moves q and R to the level's layout and (NS) forms the level's BR1
+// gradient of the owned elements; the caller refreshes the halo face traces
+// of that gradient; phase 1 evaluates the level's residual and writes
+// tau[e][d][p] of the owned elements.
+dg_status dg_tau_level(dg_ctx* ctx, int d, int p, int phase, const dg_tau_opts* o, const double* q_dev,
+                       const double* qref_dev, double* tau_dev, dg_ctx** level_out, void* stream)
+{
+    if (!ctx || !o || d < 0 || d > 2 || p < 1 || (phase != 0 && phase != 1)) return DG_EINVAL;
+    if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "tau_level: orders not set");
+    if (phase == 0 && (!q_dev || !qref_dev)) return fail(ctx, DG_EINVAL, "tau_level: q and the SOLVER reference needed");
+    if (phase == 1 && !tau_dev) return fail(ctx, DG_EINVAL, "tau_level: tau needed");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (ensure_cq(ctx) != DG_OK) return DG_ECUDA;
+    dg_ctx::CoarseLevel* L = nullptr;
+    for (auto& c : ctx->coarse)
+        if (c.d == d && c.p == p) L = &c;
+    if (!L) {
+        if (phase == 1) return fail(ctx, DG_ESTATE, "tau_level: phase 1 before phase 0");
+        dg_ctx::CoarseLevel nl;
+        const dg_status s = build_level(ctx, d, p, nl);
+        ctx->coarse.push_back(nl);  // owned from here (drop_coarse frees it)
+        if (s != DG_OK) return s;
+        L = &ctx->coarse.back();
+    }
+    if (level_out) *level_out = L->sub;
+    if (phase == 0) return level_phase0(ctx, *L, o->restriction, q_dev, qref_dev, st);
+    return level_phase1(ctx, *L, o->formulation, tau_dev, st);
 }
 
 dg_status dg_select_orders(dg_ctx* ctx, const dg_adapt_policy* pol, const double* tau_dev, double* total_dev,

@@ -145,6 +145,7 @@ class DistSolver:
         self.local_orders = lo
         self.plan = part.HaloPlan(self.lm, lo, 5)  # whole element states (rebalancing refresh)
         self.tq = TraceExchange(self.S, part.TracePlan(self.lm, lo, 5))
+        self._level_tx = {}  # non-isolated tau levels: gradient trace exchanges of the coarse layouts
         self.tg = TraceExchange(self.S, part.TracePlan(self.lm, lo, 15)) if self.physics == 1 else None
 
     @property
@@ -219,8 +220,40 @@ class DistSolver:
         self.S._check(self.S.L.dg_dt_finalize(self.S.ctx, C.c_void_p(self._lam.data_ptr()), C.c_double(cfl),
                                               C.c_void_p(dt_next.data_ptr()), self._stream()), "dg_dt_finalize")
 
-    def tau_estimate(self, q, qdot_ref=None, **kw):
-        return self.S.tau_estimate(q, qdot_ref, **kw)  # isolated levels: element-local
+    def tau_estimate(self, q, qdot_ref=None, noniso=False, **kw):
+        """Isolated levels: element-local.  noniso (SURVEY 8(f) rank 1,
+        P:217-219): every coarse level (d, p) of the global loop (MAX
+        all-reduce of the orders) in two phases, the level's BR1 gradient face
+        traces exchanged between them (NS); the halo's coarse state traces
+        follow from the fine ones already exchanged."""
+        if noniso and kw.get("restriction", 0) != 0:
+            raise NotImplementedError("non-isolated tau across ranks: the L2-projection restriction reads halo "
+                                      "interiors; use the interpolation restriction (reading A3)")
+        tau = self.S.tau_estimate(q, qdot_ref, **kw)  # slot 0 and the undefined entries; levels overwrite the rest
+        if not noniso:
+            return tau
+        import torch
+        import torch.distributed as dist
+
+        n_own = self.lm.n_own
+        nmax = torch.tensor(self.local_orders[:n_own].max(axis=0), dtype=torch.int64, device="cuda")
+        dist.all_reduce(nmax, op=dist.ReduceOp.MAX, group=self.group)
+        form = kw.get("formulation", 0)
+        restr = kw.get("restriction", 0)
+        for d in range(3):
+            for p in range(1, int(nmax[d].item())):
+                lev = self.S.tau_level(d, p, 0, q, qdot_ref, formulation=form, restriction=restr)
+                if self.physics == 1:
+                    key = (d, p)
+                    if key not in self._level_tx:
+                        oc = self.local_orders.copy()
+                        oc[:, d] = np.minimum(oc[:, d], p)
+                        self._level_tx[key] = TraceExchange(lev, part.TracePlan(self.lm, oc, 15))
+                    tx = self._level_tx[key]
+                    tx.S = lev
+                    tx(lev.gradient_buffer(), self.group)
+                self.S.tau_level(d, p, 1, tau=tau, formulation=form, restriction=restr)
+        return tau
 
     def select_orders(self, tau, tau_max, Nmin, Nmax, rule=1, dec_cap=1, mode=0, total_map=None):
         """Map/select/cap on owned elements, then the jump fixpoint with halo

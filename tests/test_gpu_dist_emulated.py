@@ -266,3 +266,71 @@ def test_rebalance_single_rank_nccl(dg, orc):
         dist.destroy_process_group(grp)
         if created:
             dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", ["cube_mixed", "ogrid_ns"])
+def test_two_rank_noniso_tau(dg, orc, case):
+    """Non-isolated tau across ranks through
+    dg_tau_level: per coarse level (d, p), phase 0 on both ranks, the level's
+    BR1 gradient face traces exchanged (NS), phase 1.  Only face traces of the
+    fine state cross the partition (the halo interiors hold a finite poison),
+    and the owned tau equal the single-rank non-isolated tau bit for bit."""
+    import torch
+
+    from paper_2210_03523_b200 import partition as part
+
+    if case == "cube_mixed":
+        mesh = W.cube_mesh(4, 4, 6)
+        g_orders = W.orders_random(mesh.E, 2, 6, 31)
+        kw = {}
+        P = orc.Problem(mesh)
+        q_g = W.pulse_state(P.node_coords(g_orders), g_orders, sigma=0.2)
+        owner = part.slab_owner(mesh.dims, 2, axis=2)
+    else:
+        mesh = W.ogrid_mesh(4, 8, 2, ratio=1.1 ** 12, g_eta=2)
+        g_orders = W.orders_random(mesh.E, (2, 2, 2), (6, 6, 2), 32)
+        nsp = W.ns_params()
+        kw = dict(physics=dg.NS, mu=nsp["mu"], Pr=nsp["Pr"], qinf=nsp["qinf"])
+        q_g = W.freestream_noise_state(g_orders, (1.0, 1.0, 0.0, 0.0, nsp["p_inf"]))
+        owner = part.slab_owner(mesh.dims, 2, axis=1)
+    S0 = dg.Solver(mesh, **kw)
+    S0.set_orders(g_orders)
+    q0 = torch.from_numpy(q_g).cuda()
+    r0 = S0.rhs_eval(q0)
+    t0 = S0.tau_estimate(q0, r0, noniso=True).cpu().numpy()
+    off = W.offsets(g_orders)
+    qb = [q_g[a:b] for a, b in zip(off[:-1], off[1:])]
+    rr = r0.cpu().numpy()
+    rb = [rr[a:b] for a, b in zip(off[:-1], off[1:])]
+    lms = [part.local_mesh(mesh, owner, r) for r in range(2)]
+    solvers, qs, rs, taus = [], [], [], []
+    for lm in lms:
+        S = dg.Solver(lm, **kw)
+        S.set_owned(lm.n_own)
+        lo = g_orders[lm.gids]
+        S.set_orders(lo)
+        solvers.append(S)
+        qs.append(torch.from_numpy(np.concatenate([qb[g] if i < lm.n_own else np.full_like(qb[g], 7.25)
+                                                   for i, g in enumerate(lm.gids)])).cuda())
+        rs.append(torch.from_numpy(np.concatenate([rb[g] if i < lm.n_own else np.full_like(rb[g], -3.5)
+                                                   for i, g in enumerate(lm.gids)])).cuda())
+    _copy_traces(solvers, [part.TracePlan(lm, g_orders[lm.gids], 5) for lm in lms], qs, 5)
+    for r in range(2):
+        taus.append(solvers[r].tau_estimate(qs[r], rs[r]))  # isolated prefill (slot 0, undefined entries)
+    nmax = g_orders.max(axis=0)
+    for d in range(3):
+        for p in range(1, int(nmax[d])):
+            levs = [solvers[r].tau_level(d, p, 0, qs[r], rs[r]) for r in range(2)]
+            if case == "ogrid_ns":
+                tplans = []
+                for lm in lms:
+                    oc = g_orders[lm.gids].copy()
+                    oc[:, d] = np.minimum(oc[:, d], p)
+                    tplans.append(part.TracePlan(lm, oc, 15))
+                _copy_traces(levs, tplans, [lv.gradient_buffer() for lv in levs], 15)
+            for r in range(2):
+                solvers[r].tau_level(d, p, 1, tau=taus[r])
+    for r, lm in enumerate(lms):
+        got = taus[r][: lm.n_own].cpu().numpy()
+        want = t0[lm.gids[: lm.n_own]]
+        assert np.array_equal(got, want, equal_nan=True), np.nanmax(np.abs(got - want))
