@@ -583,5 +583,5 @@ def test_error_paths(dg, orc):
     lo = np.ascontiguousarray(orders[lm.gids], np.int32)
     S3.set_orders(lo)
     ql = torch.from_numpy(W.uniform_state(lo)).cuda()
-    with pytest.raises(dg.DGError, match="single rank"):
+    with pytest.raises(dg.DGError, match="rank-local"):
         S3.tau_estimate(ql, S3.rhs_eval(ql), noniso=True)

@@ -10,6 +10,12 @@ cap 1), transfer of the state and a new layout.  Reported per run: the
 time-averaged NDOF, the final L_inf and RMS density errors, the
 steps and the device time.  Everything runs through libdgtau on one GPU.
 
+Static runs (Fig. 2, approach 2 / F_max): an estimation run from
+N0 over [0, T] accumulates the total truncation-error map every `--every`
+steps, one selection per tau_max gives the static layout, and the pulse is
+then run over [0, T] on that fixed layout (the paper compares the NDOF of
+the static and dynamic layouts).
+
 usage: python tools/validate_pulse.py [--n 8] [--T 0.25] > profiles/r01_validate_pulse.json
 """
 import argparse
@@ -89,6 +95,36 @@ def run(orders, tau_max=None, rule=dg.JUMP_B):
             "steps": steps, "adaptations": adapts, "device_ms": ev0.elapsed_time(ev1)}
 
 
+def static_maps():
+    """estimation run from N0 over [0, T]: the static total map (approach 2,
+    F_max) accumulated every `every` steps"""
+    orders = W.orders_uniform(mesh.E, a.n0)
+    S = dg.Solver(mesh)
+    S.set_orders(orders)
+    q = torch.from_numpy(exact(S, orders, 0.0)).cuda()
+    qb, g = torch.empty_like(q), torch.empty_like(q)
+    K = a.nmax - a.nmin + 1
+    tot = torch.zeros((mesh.E, K, K, K), dtype=torch.float64, device="cuda")
+    t, steps, stages = 0.0, 0, 0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    while t < a.T - 1e-14:
+        dt = S.compute_dt(q, a.cfl, sync=True)
+        dt = min(dt, a.T - t)
+        S._dt.fill_(dt)
+        S.rk_step(q, qb, g, S._dt)
+        q, qb = qb, q
+        t += dt
+        steps += 1
+        if steps % a.every == 0:
+            tau = S.tau_estimate(q, S.rhs_eval(q))
+            S.select_orders(tau, 1.0, a.nmin, a.nmax, mode=dg.SELECT_STATIC_ACCUM, total_map=tot)
+            stages += 1
+    ev1.record()
+    torch.cuda.synchronize()
+    return S, tot, stages, ev0.elapsed_time(ev1)
+
+
 out = {"what": "advected density pulse (exact entropy wave), error vs time-averaged NDOF",
        "mesh": f"{a.n}^3 periodic affine hexes", "T": a.T, "cfl": a.cfl, "sigma": a.sigma,
        "adapt_every": a.every, "Nmin": a.nmin, "Nmax": a.nmax, "runs": []}
@@ -100,5 +136,15 @@ for rule, name in ((dg.JUMP_B, "b"), (dg.JUMP_A, "a")):
     for tm in (1e-1, 1e-2, 1e-3, 1e-4):
         r = run(W.orders_uniform(mesh.E, a.n0), tau_max=tm, rule=rule)
         out["runs"].append({"kind": "dynamic", "tau_max": tm, "rule": name, **r})
+S0, tot, stages, est_ms = static_maps()
+dummy = torch.zeros((mesh.E, 3, 9), dtype=torch.float64, device="cuda")
+dummy[:, :, 0] = 1.0
+for tm in (1e-1, 1e-2, 1e-3, 1e-4):
+    sel, _ = S0.select_orders(dummy, tm, a.nmin, a.nmax, mode=dg.SELECT_STATIC_FINAL, total_map=tot.clone(),
+                              jump_rule=dg.JUMP_B)
+    r = run(sel)
+    dyn = [x for x in out["runs"] if x["kind"] == "dynamic" and x["rule"] == "b" and x["tau_max"] == tm][0]
+    out["runs"].append({"kind": "static", "tau_max": tm, "rule": "b", "estimation_stages": stages,
+                        "estimation_ms": est_ms, "ndof_static_over_dynamic": r["ndof_avg"] / dyn["ndof_avg"], **r})
 out["host_s"] = time.time() - t0
 print(json.dumps(out, indent=1))
