@@ -28,6 +28,7 @@ EULER, NS = 0, 1
 ROE, LLF = 0, 1
 NONISOLATED, ISOLATED = 0, 1
 TAU_NEW, TAU_TRADITIONAL = 0, 1
+PATH_AUTO, PATH_RUNTIME = 0, 1
 REF_SOLVER, REF_SAME = 0, 1
 JUMP_A, JUMP_B = 0, 1
 SELECT_DYNAMIC, SELECT_STATIC_ACCUM, SELECT_STATIC_FINAL, SELECT_A1_ACCUM, SELECT_A1_FINAL = 0, 1, 2, 3, 4
@@ -40,7 +41,7 @@ EXPORTS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_upload", "dg_set
            "dg_node_coords", "dg_rhs_eval", "dg_compute_dt", "dg_rk_step", "dg_tau_estimate", "dg_select_orders",
            "dg_transfer", "dg_diagnostics", "dg_launch_count", "dg_rk_step_dt", "dg_set_owned", "dg_rk_stage",
            "dg_dt_accumulate", "dg_dt_finalize", "dg_select_local", "dg_jump_sweep", "dg_owned_state_len", "dg_gradient",
-           "dg_gradient_buffer", "dg_rhs_eval_flags", "dg_rk_steps", "dg_trace_copy", "dg_tau_level"]
+           "dg_gradient_buffer", "dg_rhs_eval_flags", "dg_rk_steps", "dg_trace_copy", "dg_tau_level", "dg_set_path"]
 
 
 def sources():
@@ -229,7 +230,9 @@ class Solver:
     canonical layout of include/dgtau.h.
     """
 
-    def __init__(self, mesh, physics=EULER, flux=ROE, gamma=1.4, mu=0.0, Pr=0.72, qinf=None):
+    def __init__(self, mesh, physics=EULER, flux=ROE, gamma=1.4, mu=0.0, Pr=0.72, qinf=None, path=PATH_AUTO):
+        """path: PATH_AUTO, or PATH_RUNTIME (runtime-order kernels on affine
+        meshes too: many-bucket layouts under dynamic adaptation; dg_set_path)."""
         import torch
 
         if not torch.cuda.is_available():
@@ -243,6 +246,8 @@ class Solver:
         self.ctx = C.c_void_p()
         torch.cuda.current_device()
         self._check(self.L.dg_create(C.byref(p), C.byref(self.ctx)), "dg_create")
+        if path != PATH_AUTO:
+            self._check(self.L.dg_set_path(self.ctx, int(path)), "dg_set_path")
         self.nbr = _np(mesh.nbr, np.int32)
         self.E = int(self.nbr.shape[0])
         gord = _np(mesh.gorder, np.int32)

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -192,9 +193,13 @@ struct dg_ctx {
     bool no_graphs = false;  // DGTAU_NO_GRAPHS=1: launch mixed-order residuals directly
     cudaStream_t cap_stream = nullptr;  // graph capture stream
     std::map<ShapeKey, GraphEntry> graphs;  // mixed-order residual graphs of the current layout
+    std::map<ShapeKey, int> direct_uses;    // direct launches per shape since the layout was set
     // curved residual path (ns.cuh): element items, face list, face blocks
     bool extruded = false;     // extruded mesh (compact metrics, structural zeros), see ns.cuh
     bool borrowed = false;     // coarse-level sub-context: scratch lent by the parent, never reallocated
+    int path = DG_PATH_AUTO;   // dg_set_path
+    bool affine_geo = false;   // axis-aligned box elements (h per element is exact)
+    bool tau_curved = false;   // tau levels by k_tau_curved (else k_tau5, affine Euler)
     double* d_metc = nullptr;  // EXT: 6 per (i, j) column
     long long* d_coff = nullptr;
     NsItem* d_nsitems = nullptr;
@@ -317,6 +322,22 @@ inline bool getenv_flag(const char* name)
     const char* g = getenv(name);
     return g && g[0] == '1';
 }
+
+// DGTAU_TIMING=1: host-side section times of dg_set_orders on stderr (device
+// work synchronised at each mark)
+struct PlanTimer {
+    bool on;
+    std::chrono::steady_clock::time_point t;
+    PlanTimer() : on(getenv_flag("DGTAU_TIMING")), t(std::chrono::steady_clock::now()) {}
+    void mark(const char* what)
+    {
+        if (!on) return;
+        cudaDeviceSynchronize();
+        const auto n = std::chrono::steady_clock::now();
+        fprintf(stderr, "[set_orders] %-28s %8.3f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+        t = n;
+    }
+};
 
 dg_status check_stream_error(dg_ctx* ctx, const char* what)
 {
@@ -497,6 +518,7 @@ static void drop_graphs(dg_ctx* ctx)
         cudaGraphDestroy(kv.second.graph);
     }
     ctx->graphs.clear();
+    ctx->direct_uses.clear();
 }
 
 // Coarse-level contexts borrow the fine context's residual scratch (BR1
@@ -601,6 +623,15 @@ const char* dg_last_error(const dg_ctx* ctx) { return ctx ? ctx->err.c_str() : "
 
 int64_t dg_launch_count(const dg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+dg_status dg_set_path(dg_ctx* ctx, int path)
+{
+    if (!ctx) return DG_EINVAL;
+    if (path != DG_PATH_AUTO && path != DG_PATH_RUNTIME) return fail(ctx, DG_EINVAL, "set_path: unknown path");
+    if (ctx->E != 0) return fail(ctx, DG_ESTATE, "set_path: call before dg_mesh_upload");
+    ctx->path = path;
+    return DG_OK;
+}
+
 dg_status dg_mesh_upload(dg_ctx* ctx, int E, const int32_t* nbr_host, const int32_t* gorder_host, const double* geo_host)
 {
     if (!ctx) return DG_EINVAL;
@@ -640,7 +671,11 @@ dg_status dg_mesh_upload(dg_ctx* ctx, int E, const int32_t* nbr_host, const int3
             if (!(hi > lo)) affine = false;
         }
     }
-    ctx->curved = !affine;
+    // DG_PATH_RUNTIME (dg_set_path): affine meshes take the runtime-order
+    // (class-batched) kernels of the curved path too
+    ctx->affine_geo = affine;
+    ctx->curved = !affine || ctx->path == DG_PATH_RUNTIME;
+    ctx->tau_curved = ctx->curved && !(affine && ctx->prm.physics == DG_EULER);
     // extruded mesh (ns.cuh): linear in zeta, x and y independent of zeta, z
     // independent of xi and eta and increasing with zeta
     bool ext = ctx->curved && gorder_host[2] == 1 && !getenv_flag("DGTAU_NO_EXT");
@@ -657,7 +692,8 @@ dg_status dg_mesh_upload(dg_ctx* ctx, int E, const int32_t* nbr_host, const int3
     }
     ctx->extruded = ext;
     if (ctx->curved) {
-        for (long long i = 0; i < 3LL * E; ++i) ctx->h[i] = 1.0;  // unused by the curved kernels
+        if (!affine)
+            for (long long i = 0; i < 3LL * E; ++i) ctx->h[i] = 1.0;  // unused by the curved kernels
         CK(upload(ctx->d_geo, ctx->geo));
     }
     CK(upload(ctx->d_nbr, ctx->nbr));
@@ -673,7 +709,16 @@ static void size_classes(std::vector<int>& idx, const std::vector<int>& sz, int 
 {
     static const int edge[] = {16, 32, 48, 64, 80, 96, 128, 160, 192, 256, 320, 384, 512, 640, 1 << 30};
     auto cls = [](int n) { int c = 0; while (n > edge[c]) ++c; return c; };
-    std::stable_sort(idx.begin() + begin, idx.begin() + end, [&](int a, int b) { return sz[a] > sz[b]; });
+    {  // stable sort by decreasing size: counting sort, O(n + max size)
+        int smax = 0;
+        for (int i = begin; i < end; ++i) smax = std::max(smax, sz[idx[i]]);
+        std::vector<int> cnt(smax + 2, 0);
+        for (int i = begin; i < end; ++i) ++cnt[smax - sz[idx[i]] + 1];
+        for (int k = 0; k <= smax; ++k) cnt[k + 1] += cnt[k];
+        std::vector<int> tmp(end - begin);
+        for (int i = begin; i < end; ++i) tmp[cnt[smax - sz[idx[i]]]++] = idx[i];
+        std::copy(tmp.begin(), tmp.end(), idx.begin() + begin);
+    }
     for (int i = begin; i < end;) {
         const int c = cls(sz[idx[i]]);
         int j = i;
@@ -681,6 +726,32 @@ static void size_classes(std::vector<int>& idx, const std::vector<int>& sz, int 
         out.push_back(SizeClass{i, j - i, sz[idx[i]]});
         i = j;
     }
+}
+
+// Elements [begin, end) grouped by their order triple, groups in increasing
+// (N3, N2, N1) and element ids increasing inside (counting sort, O(E)).
+static void order_buckets(const std::vector<int>& orders, int begin, int end, std::vector<int>& keys,
+                          std::vector<int>& start, std::vector<int>& elems)
+{
+    constexpr int NK = NMAX * NMAX * NMAX;
+    std::vector<int> cnt(NK + 1, 0);
+    auto key = [&](int e) {
+        const int* N = &orders[3 * e];
+        return (N[0] - 1) + NMAX * ((N[1] - 1) + NMAX * (N[2] - 1));
+    };
+    for (int e = begin; e < end; ++e) ++cnt[key(e) + 1];
+    for (int k = 0; k < NK; ++k) cnt[k + 1] += cnt[k];
+    elems.resize(end - begin);
+    std::vector<int> pos(cnt.begin(), cnt.end() - 1);
+    for (int e = begin; e < end; ++e) elems[pos[key(e)]++] = e;
+    keys.clear();
+    start.clear();
+    for (int k = 0; k < NK; ++k)
+        if (cnt[k + 1] > cnt[k]) {
+            keys.push_back(((k % NMAX) + 1) | (((k / NMAX) % NMAX + 1) << 8) | ((k / (NMAX * NMAX) + 1) << 16));
+            start.push_back(cnt[k]);
+        }
+    start.push_back(end - begin);
 }
 
 // Scratch that a borrowing (coarse-level) context must not reallocate.
@@ -691,8 +762,9 @@ static dg_status scratch_need(dg_ctx* ctx, double*& p, long long& cap, long long
     if (ctx->borrowed)
         return fail(ctx, DG_EINVAL, std::string("set_orders: borrowed ") + what + " scratch too small (coarse layout larger than the fine one)");
     dfree(p);
-    CK(cudaMalloc(&p, sizeof(double) * need));
-    cap = need;
+    const long long c = need + need / 4;  // slack: successive adapted layouts differ a little
+    CK(cudaMalloc(&p, sizeof(double) * c));
+    cap = c;
     return DG_OK;
 }
 
@@ -703,7 +775,7 @@ static inline long long EVEN(long long x) { return (x + 1) & ~1LL; }
 // Plans of the curved residual path (ns.cuh): element items, the face list
 // (every interior face once, boundary faces of owned elements), face-block
 // offsets, face metrics and (extruded meshes) compact volume metrics.
-static dg_status build_ns_plans(dg_ctx* ctx)
+static dg_status build_ns_plans(dg_ctx* ctx, PlanTimer& tm)
 {
     static const int TA[3] = {1, 0, 0}, TB[3] = {2, 2, 1};
     const int E = ctx->E;
@@ -712,25 +784,25 @@ static dg_status build_ns_plans(dg_ctx* ctx)
     const long long L = ctx->off[E];
     // ---- element items: same-order owned elements, <= NS_ITEM_NODES nodes ----
     {
-        std::map<int, std::vector<int>> bk;
-        for (int e = 0; e < ctx->n_own; ++e) {
-            const int* N = &ctx->orders[3 * e];
-            bk[N[0] | (N[1] << 8) | (N[2] << 16)].push_back(e);
-        }
+        std::vector<int> bkey, bstart, belem;
+        order_buckets(ctx->orders, 0, ctx->n_own, bkey, bstart, belem);
         std::vector<NsItem> items;
         std::vector<int> el;
         el.reserve(ctx->n_own);
-        for (auto& kv : bk) {
-            const int N[3] = {kv.first & 255, (kv.first >> 8) & 255, (kv.first >> 16) & 255};
+        for (size_t b = 0; b < bkey.size(); ++b) {
+            const int ord = bkey[b];
+            const int* be = belem.data() + bstart[b];
+            const size_t bn = (size_t)(bstart[b + 1] - bstart[b]);
+            const int N[3] = {ord & 255, (ord >> 8) & 255, (ord >> 16) & 255};
             const int n = npts(N);
             const int k = std::max(1, std::min(NS_MAXSLOTS, NS_ITEM_NODES / n));
-            for (size_t i = 0; i < kv.second.size(); i += k) {
+            for (size_t i = 0; i < bn; i += k) {
                 NsItem it;
                 it.start = (int)el.size();
-                it.count = (int)std::min<size_t>(k, kv.second.size() - i);
-                it.ord = kv.first;
+                it.count = (int)std::min<size_t>(k, bn - i);
+                it.ord = ord;
                 it.nodes = it.count * n;
-                for (int j = 0; j < it.count; ++j) el.push_back(kv.second[i + j]);
+                for (int j = 0; j < it.count; ++j) el.push_back(be[i + j]);
                 items.push_back(it);
             }
         }
@@ -762,9 +834,12 @@ static dg_status build_ns_plans(dg_ctx* ctx)
         CK(upload(ctx->d_nsitems, sorted));
         CK(upload(ctx->d_nselist, el));
     }
+    tm.mark("ns items");
     // ---- faces ----
     std::vector<NsFace> fl;
     std::vector<int> fw;  // warps per face
+    fl.reserve(3LL * E + 16);
+    fw.reserve(3LL * E + 16);
     std::vector<long long> fofsG(6LL * E, -1), fofsH(6LL * E, -1);
     long long gl = 0, hl = 0, mgl = 0;
     auto pack = [&](int e) { const int* a = &ctx->orders[3 * e]; return a[0] | (a[1] << 4) | (a[2] << 8); };
@@ -835,6 +910,7 @@ static dg_status build_ns_plans(dg_ctx* ctx)
                 fw.push_back((so + 31) / 32);
             }
         }
+    tm.mark("ns face loop");
     {
         std::vector<NsFace> sorted;
         sorted.reserve(fl.size());
@@ -847,16 +923,17 @@ static dg_status build_ns_plans(dg_ctx* ctx)
         if (sorted.size() != fl.size()) return fail(ctx, DG_EINVAL, "set_orders: face with more than 96 mortar points");
         fl.swap(sorted);
     }
+    tm.mark("ns face list");
     CK(upload(ctx->d_nsfaces, fl));
     CK(upload(ctx->d_fofsG, fofsG));
     CK(upload(ctx->d_fofsH, fofsH));
     dg_status s;
+    tm.mark("ns face uploads");
     if ((s = scratch_need(ctx, ctx->d_nsG, ctx->nsG_cap, gl, "flux-block")) != DG_OK) return s;
     if (ns && (s = scratch_need(ctx, ctx->d_nsH, ctx->nsH_cap, hl, "BR1-block")) != DG_OK) return s;
     if (ns && (s = scratch_need(ctx, ctx->d_grad, ctx->grad_len, 3 * L + 2, "gradient")) != DG_OK) return s;
-    dfree(ctx->d_fg);
     if (mgl > 0) {
-        CK(cudaMalloc(&ctx->d_fg, sizeof(double) * mgl));
+        CK(dalloc(ctx->d_fg, (size_t)mgl));
         FaceGeomParams G;
         G.faces = ctx->d_nsfaces;
         G.nfaces = (int)fl.size();
@@ -871,9 +948,10 @@ static dg_status build_ns_plans(dg_ctx* ctx)
     // ---- volume metrics: full (10 per node, the dt / tau kernels) and compact (EXT) ----
     if (ctx->met_len < 2 * L) {
         dfree(ctx->d_met);
-        CK(cudaMalloc(&ctx->d_met, sizeof(double) * 2 * L));
-        ctx->met_len = 2 * L;
+        CK(cudaMalloc(&ctx->d_met, sizeof(double) * (2 * L + L / 2)));
+        ctx->met_len = 2 * L + L / 2;
     }
+    tm.mark("ns uploads, face geometry");
     MetParams M;
     M.cm = curved_mesh(ctx);
     M.orders = ctx->d_orders;
@@ -894,8 +972,7 @@ static dg_status build_ns_plans(dg_ctx* ctx)
             coff[e + 1] = coff[e] + EVEN(6LL * (N[0] + 1) * (N[1] + 1));
         }
         CK(upload(ctx->d_coff, coff));
-        dfree(ctx->d_metc);
-        CK(cudaMalloc(&ctx->d_metc, sizeof(double) * coff[E]));
+        CK(dalloc(ctx->d_metc, (size_t)coff[E]));
         MetExtParams X;
         X.cm = curved_mesh(ctx);
         X.orders = ctx->d_orders;
@@ -907,6 +984,7 @@ static dg_status build_ns_plans(dg_ctx* ctx)
         ctx->launches++;
         CK(cudaGetLastError());
     }
+    tm.mark("metrics");
     CK(cudaDeviceSynchronize());
     return DG_OK;
 }
@@ -915,8 +993,10 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
 {
     if (!ctx) return DG_EINVAL;
     if (ctx->E == 0) return fail(ctx, DG_ESTATE, "set_orders: no mesh");
+    PlanTimer tm;
     drop_graphs(ctx);  // captured launches refer to the old plans
     drop_coarse(ctx);  // non-isolated tau levels of the old layout
+    tm.mark("drop graphs / levels");
     ctx->coarse_streaming = false;
     const int E = ctx->E;
     for (long long i = 0; i < 3LL * E; ++i)
@@ -933,28 +1013,27 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     }
     // (N1,N2,N3) buckets -> work items of up to floor(256/n) elements, ordered
     // by their first element id (spatially coherent sweep, neighbour traces hit L2)
-    std::map<int, std::vector<int>> buckets;
-    for (int e = 0; e < ctx->n_own; ++e) {
-        const int* N = &ctx->orders[3 * e];
-        buckets[N[0] | (N[1] << 8) | (N[2] << 16)].push_back(e);
-    }
+    std::vector<int> bkey, bstart, belem;
+    order_buckets(ctx->orders, 0, ctx->curved ? 0 : ctx->n_own, bkey, bstart, belem);  // affine kernels only
     std::vector<int> elist;
     elist.reserve(E);
     std::vector<WorkItem> work;
     size_t smem = 0;
-    for (auto& kv : buckets) {
-        const int ord = kv.first;
+    for (size_t b = 0; b < bkey.size(); ++b) {
+        const int ord = bkey[b];
+        const int* be = belem.data() + bstart[b];
+        const size_t bn = (size_t)(bstart[b + 1] - bstart[b]);
         const int N[3] = {ord & 255, (ord >> 8) & 255, (ord >> 16) & 255};
         const int n = npts(N);
         const int k = res_cnt(N[0] + 1, N[1] + 1, N[2] + 1);  // = Shape<N>::CNT
         const int nfs = 2 * ((N[1] + 1) * (N[2] + 1) + (N[0] + 1) * (N[2] + 1) + (N[0] + 1) * (N[1] + 1));
-        for (size_t i = 0; i < kv.second.size(); i += k) {
+        for (size_t i = 0; i < bn; i += k) {
             WorkItem w;
             w.start = (int)elist.size();
-            w.count = (int)std::min<size_t>(k, kv.second.size() - i);
+            w.count = (int)std::min<size_t>(k, bn - i);
             w.ord = ord;
-            w.pad = kv.second[i];
-            for (int j = 0; j < w.count; ++j) elist.push_back(kv.second[i + j]);
+            w.pad = be[i];
+            for (int j = 0; j < w.count; ++j) elist.push_back(be[i + j]);
             work.push_back(w);
             const size_t bytes = sizeof(double) * (3 * NP * NP + (size_t)w.count * NV * (2 * n + nfs));
             smem = std::max(smem, bytes);
@@ -970,9 +1049,12 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     }
     ctx->nwork = (int)work.size();
     ctx->res_smem = smem;
-    // mortar faces: + side of L against - side of R, tangential orders differ
     std::vector<MortarItem> mort;
-    std::vector<long long> moff(6LL * E, -1);
+    std::vector<long long> moff;
+    long long flen = 0;
+    if (!ctx->curved) {  // ---- plans of the order-specialised (affine) kernels ----
+    // mortar faces: + side of L against - side of R, tangential orders differ
+    moff.assign(6LL * E, -1);
     long long mlen = 0;
     static const int TA[3] = {1, 0, 0}, TB[3] = {2, 2, 1};
     for (int e = 0; e < E; ++e)
@@ -991,6 +1073,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
         }
     ctx->nmortar = (int)mort.size();
     ctx->mortar_len = mlen;
+    tm.mark("buckets, mortar list");
     {
         std::vector<MortarFace> mf(mort.size());
         for (size_t i = 0; i < mort.size(); ++i) {
@@ -1014,7 +1097,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     std::vector<long long> fofs(moff);
     std::vector<FaceItem> faces;
     std::vector<int> fpt(1, 0);
-    long long flen = mlen;
+    flen = mlen;
     {
         auto strides = [&](int el, int* st) {
             const int* N = &ctx->orders[3 * el];
@@ -1096,6 +1179,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
         CK(upload(ctx->d_fpt, fpt));
         CK(upload(ctx->d_fcta, fcode));
     }
+    tm.mark("face lists + upload");
     // per element-face source descriptors of the outer state (see FaceInfo)
     std::vector<FaceInfo> finfo(6LL * E);
     for (int e = 0; e < E; ++e)
@@ -1141,17 +1225,19 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     for (size_t i = 0; i < elist.size(); ++i)
         for (int f = 0; f < 6; ++f) fos[6 * i + f] = fofs[6LL * elist[i] + f];
     CK(upload(ctx->d_fofs_slot, fos));
+    tm.mark("face info, slots");
     for (Bucket& b : ctx->buckets) {
         const int o1 = b.ord & 255, o2 = (b.ord >> 8) & 255, o3 = (b.ord >> 16) & 255;
         if (ctx->occ_cache[o1][o2][o3] < 0) ctx->occ_cache[o1][o2][o3] = (signed char)ctx->rocc[o1][o2][o3]();
         const int occ = ctx->occ_cache[o1][o2][o3];
         b.grid = std::max(1, occ) * ctx->nsm;
     }
+    }  // affine plans
     // tau-estimation levels (e, d, p < N_d), largest first for load balance
     // (curved kernels only: the affine path batches levels in k_tau5 groups)
     std::vector<TauLevel> lv;
     ctx->max_level = 0;
-    for (int e = 0; e < (ctx->curved ? ctx->n_own : 0); ++e)
+    for (int e = 0; e < (ctx->tau_curved ? ctx->n_own : 0); ++e)
         for (int d = 0; d < 3; ++d)
             for (int p = 1; p < ctx->orders[3 * e + d]; ++p) {
                 lv.push_back(TauLevel{e, d, p, 0});
@@ -1174,6 +1260,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
         lv.swap(ls);
     }
     CK(upload(ctx->d_levels, lv));
+    tm.mark("tau levels");
     ctx->ecls_own.clear();
     ctx->ecls_all.clear();
     if (ctx->curved) {  // size classes of the curved element kernels
@@ -1189,7 +1276,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
         std::vector<TauGroup> tg;
         std::vector<int> gsz;
         int gmax = 0;
-        for (int e = 0; e < ctx->n_own; ++e)
+        for (int e = 0; e < (ctx->tau_curved ? 0 : ctx->n_own); ++e)
             for (int d = 0; d < 3; ++d) {
                 const int* No = &ctx->orders[3 * e];
                 const int nx = npts(No) / (No[d] + 1);
@@ -1214,6 +1301,7 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
         ctx->tau5_smem = sizeof(double) * 4 * NV * (size_t)gmax;
         CK(upload(ctx->d_tgroups, sorted));
     }
+    tm.mark("tau5 groups");
     std::vector<int> ord_i(ctx->orders.begin(), ctx->orders.end());
     CK(upload(ctx->d_orders, ord_i));
     CK(upload(ctx->d_off, ctx->off));
@@ -1224,8 +1312,9 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     if (flen > 0 && !ctx->curved) CK(dalloc(ctx->d_mortarG, (size_t)flen));
     CK(dalloc(ctx->d_sel, 6 * (size_t)E));
     CK(dalloc(ctx->d_margin, (size_t)E));
+    tm.mark("tau5 groups, uploads");
     if (ctx->curved) {
-        dg_status s = build_ns_plans(ctx);
+        dg_status s = build_ns_plans(ctx, tm);
         if (s != DG_OK) return s;
     }
     ctx->have_orders = true;
@@ -1498,6 +1587,8 @@ static dg_status launch_residual_direct(dg_ctx* ctx, int variant, const double* 
 // bucket (cfg3: 216) plus the mortar and face passes: that sequence is
 // captured once per argument set into a CUDA graph (fork/join over the side
 // streams included) and replayed with a single launch.  Cache per layout.
+constexpr int GRAPH_AFTER = 8;  // direct launches of a shape before its graph is captured
+
 static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, double* out, double* g, const double* dt,
                                  double A, double B, int mode, cudaStream_t st, unsigned long long* lam_max = nullptr,
                                  int flags = 0, const DtFuse& fz = DtFuse())
@@ -1511,6 +1602,11 @@ static dg_status launch_residual(dg_ctx* ctx, int variant, const double* q, doub
     if ((reinterpret_cast<uintptr_t>(q) & 15) != 0)
         return fail(ctx, DG_EINVAL, "residual: state pointer must be 16-byte aligned");
     auto itg = ctx->graphs.find(shape);
+    // a fresh layout (dynamic adaptation every few steps) launches directly at
+    // first: capture + instantiate costs ~ a few residuals of launches, so a
+    // graph is only built for a shape that keeps recurring
+    if (itg == ctx->graphs.end() && ++ctx->direct_uses[shape] <= GRAPH_AFTER)
+        return launch_residual_direct(ctx, variant, q, out, g, dt, A, B, mode, st, lam_max, fz);
     if (itg == ctx->graphs.end()) {
         const long long l0 = ctx->launches;
         CK(cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed));
@@ -1903,6 +1999,7 @@ static dg_status build_level(dg_ctx* ctx, int d, int p, dg_ctx::CoarseLevel& L)
     }
     dg_status s = dg_create(&ctx->prm, &L.sub);
     if (s != DG_OK) return fail(ctx, s, "tau_estimate: coarse level context");
+    L.sub->path = ctx->path;
     if (ctx->curved) lend_scratch(ctx, L.sub);
     if ((s = dg_mesh_upload(L.sub, E, ctx->nbr.data(), ctx->gorder, ctx->geo.data())) != DG_OK ||
         (ctx->n_own < E && (s = dg_set_owned(L.sub, ctx->n_own)) != DG_OK) ||
@@ -2075,7 +2172,7 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
         k_tau_norm<<<ctx->n_own, 128, 0, st>>>(ref, tau_dev, ctx->d_orders, ctx->d_off);
         ctx->launches++;
         if (o->coarse_faces) return tau_noniso(ctx, o->formulation, o->restriction, q_dev, ref, tau_dev, st);
-        if (ctx->curved && ctx->nlevels > 0) {
+        if (ctx->tau_curved && ctx->nlevels > 0) {
             const size_t sm = sizeof(double) * ((ctx->prm.physics == DG_NS ? 40 : 30) * (size_t)ctx->max_level + (ctx->max_level + 1) / 2);
             if ((long long)sm > ctx->smem_limit) return fail(ctx, DG_EUNSUPPORTED, "tau_estimate: coarse level too large for shared memory");
             CTauParams C;

@@ -542,9 +542,12 @@ def test_graph_repoint_bitwise(dg, orc, monkeypatch):
         dts = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in range(2)]
         S.compute_dt(qd, 0.5, dts[0])
         qa, qb, g = qd.clone(), torch.empty_like(qd), torch.empty_like(qd)
-        qs, dt = S.rk_steps(3, qa, qb, g, dts[0], dts[1], 0.5)
-        r1 = S.rhs_eval(qs)
-        r2 = S.rhs_eval(qd)
+        # a shape is captured after 8 direct launches (GRAPH_AFTER): 12 steps
+        # and 10 residual pairs cross it, then replay re-pointed graphs
+        qs, dt = S.rk_steps(12, qa, qb, g, dts[0], dts[1], 0.5)
+        for _ in range(10):
+            r1 = S.rhs_eval(qs)
+            r2 = S.rhs_eval(qd)
         r3 = S.rhs_eval(qs, variant=1)
         outs.append([x.cpu().numpy().copy() for x in (qs, dt, r1, r2, r3)])
     for a, b in zip(*outs):
