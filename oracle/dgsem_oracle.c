@@ -1246,8 +1246,7 @@ int orc_tau_field(const orc_mesh* m, const int32_t* orders, const double* q, con
 /* ------------------------------------------------------------------------- */
 
 /* Directional estimate tauhat_d(n), n = 1..ORC_NMAX, for one element. */
-/* tall = the element's largest estimate over all directions (reading R11). */
-static void directional_hat(int Nd, const double* td /* tau[e][d][0..] */, double tall, double* hat /* [ORC_NMAX+1] */,
+static void directional_hat(int Nd, const double* td /* tau[e][d][0..] */, double* hat /* [ORC_NMAX+1] */,
                             double* slope_out)
 {
     double eps = 1e-13 * fmax(1.0, td[0]);
@@ -1258,10 +1257,7 @@ static void directional_hat(int Nd, const double* td /* tau[e][d][0..] */, doubl
         for (int n = 1; n <= ORC_NMAX; ++n) hat[n] = n == Nd ? 0.0 : ORC_SENTINEL;
         return;
     }
-    /* resolved direction: at the rounding floor (A14), or rounding against the
-     * element's other directions (R11: 1e-8 of its largest estimate, e.g. the
-     * span direction of a two-dimensional flow) */
-    if (tmax <= eps || tmax <= 1e-8 * tall) {
+    if (tmax <= eps) { /* resolved direction (A14) */
         for (int n = 1; n <= ORC_NMAX; ++n) hat[n] = 0.0;
         return;
     }
@@ -1293,13 +1289,9 @@ int orc_build_map(int E, const int32_t* orders, const double* tau, int Nmin, int
     if (Nmin < 1 || Nmax > ORC_NMAX || K < 1) return -1;
     for (int e = 0; e < E; ++e) {
         double hat[3][ORC_NMAX + 1];
-        double tall = 0.0;
-        for (int d = 0; d < 3; ++d)
-            for (int p = 1; p < orders[3 * e + d]; ++p)
-                tall = fmax(tall, tau[((size_t)e * 3 + d) * ORC_TAU_STRIDE + p]);
         for (int d = 0; d < 3; ++d) {
             double s;
-            directional_hat(orders[3 * e + d], tau + ((size_t)e * 3 + d) * ORC_TAU_STRIDE, tall, hat[d], &s);
+            directional_hat(orders[3 * e + d], tau + ((size_t)e * 3 + d) * ORC_TAU_STRIDE, hat[d], &s);
             if (slopes) slopes[3 * e + d] = s;
         }
         for (int n3 = Nmin; n3 <= Nmax; ++n3)

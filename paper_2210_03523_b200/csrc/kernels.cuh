@@ -88,8 +88,7 @@ struct SelParams {
     int nstages;   // n_e for the F_av finals
 };
 
-// tall: the element's largest estimate over its three directions (reading R11)
-__device__ void directional_estimate(int Nd, const double* td, double tall, double* hat /* [NP+1] indexed by n */)
+__device__ void directional_estimate(int Nd, const double* td, double* hat /* [NP+1] indexed by n */)
 {
     const double SENT = 1e30;
     const double eps = 1e-13 * fmax(1.0, td[0]);
@@ -99,7 +98,7 @@ __device__ void directional_estimate(int Nd, const double* td, double tall, doub
         for (int m = 1; m <= NMAX; ++m) hat[m] = (m == Nd) ? 0.0 : SENT;
         return;
     }
-    if (tmax <= eps || tmax <= 1e-8 * tall) {  // resolved direction (A14), or rounding next to the others (R11)
+    if (tmax <= eps) {  // resolved direction (A14)
         for (int m = 1; m <= NMAX; ++m) hat[m] = 0.0;
         return;
     }
@@ -131,13 +130,9 @@ __global__ void k_select(SelParams P)
     if (e >= P.E) return;
     double hat[3][NP + 1];
     int Ne[3];
-    double tall = 0.0;
     for (int d = 0; d < 3; ++d) {
         Ne[d] = P.orders[3 * e + d];
-        for (int p = 1; p < Ne[d]; ++p) tall = fmax(tall, P.tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV + p]);
-    }
-    for (int d = 0; d < 3; ++d) {
-        directional_estimate(Ne[d], P.tau + (3 * (long long)e + d) * DG_TAU_STRIDE_DEV, tall, hat[d]);
+        directional_estimate(Ne[d], P.tau + (3 * (long long)e + d) * DG_TAU_STRIDE_DEV, hat[d]);
     }
     const int Nmin = P.Nmin, Nmax = P.Nmax, K = Nmax - Nmin + 1;
     double* tot = P.total ? P.total + (long long)e * K * K * K : nullptr;

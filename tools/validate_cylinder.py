@@ -29,6 +29,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--Te", type=float, default=12.0)
 ap.add_argument("--cfl", type=float, default=0.5)
 ap.add_argument("--stages", type=int, default=10)
+ap.add_argument("--ref", choices=("solver", "same"), default="solver",
+                help="tau reference: the solver's non-isolated residual (A4 default) or the isolated fine residual")
 ap.add_argument("--noise", type=float, default=1e-3, help="IC noise amplitude (reading A22: 1e-3; 0 = smooth impulsive start)")
 a = ap.parse_args()
 
@@ -60,7 +62,10 @@ while stage < a.stages:
     if t >= next_est:
         r = S.rhs_eval(q)
         for f in tot:
-            tau = S.tau_estimate(q, r, formulation=f)
+            if a.ref == "same":
+                tau = S.tau_estimate(q, None, formulation=f, reference=dg.REF_SAME)
+            else:
+                tau = S.tau_estimate(q, r, formulation=f)
             S.select_orders(tau, 1.0, Nmin, Nmax, mode=dg.SELECT_STATIC_ACCUM, total_map=tot[f])
         sums, mn = S.diagnostics(q, r)
         log.append({"stage": stage + 1, "t": t, "steps": steps, "dt": dt_last, "min_rho": mn[0], "min_p": mn[1]})
@@ -73,7 +78,7 @@ dummy[:, :, 0] = 1.0
 sel = {}
 res = {"what": "cfg4 cylinder (Re 100, Ma 0.2): static tau-estimation, traditional vs new (Fig. 9)",
        "Te": a.Te, "stages": a.stages, "steps": steps, "device_ms": ev0.elapsed_time(ev1), "uniform_N4_ndof": S.ndof,
-       "noise": a.noise, "log": log, "thresholds": []}
+       "noise": a.noise, "reference": a.ref, "log": log, "thresholds": []}
 nr = W.CONFIGS["cfg4"]["mesh"][1]
 ring = np.arange(mesh.E) % nr  # element (i, j, k): radial index fastest
 bands = [(0, nr // 3), (nr // 3, 2 * nr // 3), (2 * nr // 3, nr)]
