@@ -88,7 +88,8 @@ struct SelParams {
     int nstages;   // n_e for the F_av finals
 };
 
-__device__ void directional_estimate(int Nd, const double* td, double* hat /* [NP+1] indexed by n */)
+// tall: the element's largest estimate over its three directions (reading R11)
+__device__ void directional_estimate(int Nd, const double* td, double tall, double* hat /* [NP+1] indexed by n */)
 {
     const double SENT = 1e30;
     const double eps = 1e-13 * fmax(1.0, td[0]);
@@ -98,7 +99,7 @@ __device__ void directional_estimate(int Nd, const double* td, double* hat /* [N
         for (int m = 1; m <= NMAX; ++m) hat[m] = (m == Nd) ? 0.0 : SENT;
         return;
     }
-    if (tmax <= eps) {  // resolved direction (A14)
+    if (tmax <= eps || tmax <= 1e-8 * tall) {  // resolved direction (A14), or rounding next to the others (R11)
         for (int m = 1; m <= NMAX; ++m) hat[m] = 0.0;
         return;
     }
@@ -120,6 +121,7 @@ __device__ void directional_estimate(int Nd, const double* td, double* hat /* [N
     }
     for (int m = 1; m <= NMAX; ++m) {
         if (m < Nd) hat[m] = td[m];
+        else if (Nd == 2) hat[m] = m == Nd ? 0.0 : SENT;  // no extrapolation possible: keep the order (R12)
         else hat[m] = asym ? pow(10.0, a + b * m) : SENT;
     }
 }
@@ -130,9 +132,13 @@ __global__ void k_select(SelParams P)
     if (e >= P.E) return;
     double hat[3][NP + 1];
     int Ne[3];
+    double tall = 0.0;
     for (int d = 0; d < 3; ++d) {
         Ne[d] = P.orders[3 * e + d];
-        directional_estimate(Ne[d], P.tau + (3 * (long long)e + d) * DG_TAU_STRIDE_DEV, hat[d]);
+        for (int p = 1; p < Ne[d]; ++p) tall = fmax(tall, P.tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV + p]);
+    }
+    for (int d = 0; d < 3; ++d) {
+        directional_estimate(Ne[d], P.tau + (3 * (long long)e + d) * DG_TAU_STRIDE_DEV, tall, hat[d]);
     }
     const int Nmin = P.Nmin, Nmax = P.Nmax, K = Nmax - Nmin + 1;
     double* tot = P.total ? P.total + (long long)e * K * K * K : nullptr;

@@ -491,14 +491,17 @@ def test_q13_extrapolation(orc):
     tau[0, :, 0] = 1.0
     tau[0, 0, 1:5] = 10.0 ** -np.arange(1, 5)  # exact exponential: a = 0, b = -1
     tau[0, 1, 1:4] = [1e-2, 2e-2, 5e-3]        # non-monotone, slope > 0? fit decides
-    tau[0, 2, 1] = 1e-3                        # N = 2: a single point, never asymptotic
+    tau[0, 2, 1] = 1e-3                        # N = 2: a single point, no extrapolation
     mp, sl = orc.build_map(o, tau, 1, 8)
     assert abs(sl[0, 0] + 1.0) < 1e-12
     # hat_x(n) = 10^-n for all n; y, z at n = 1 are the measured values
     for n1 in range(1, 9):
         assert abs(mp[0, 0, 0, n1 - 1] - (10.0 ** -n1 + 1e-2 + 1e-3)) < 1e-12 * (10.0 ** -n1 + 1.1e-2)
     assert mp[0, 0, 0, 0] < 1.0
-    assert mp[0, 1, 0, 0] >= 1e30  # z at n = 2 = N_z: not asymptotic => sentinel
+    # z at N_z = 2: no extrapolation possible, the order is kept (P:592,
+    # reading R12): hat_z(2) = 0, hat_z(n > 2) = sentinel
+    assert abs(mp[0, 1, 0, 0] - (0.1 + 1e-2)) < 1e-14
+    assert mp[0, 2, 0, 0] >= 1e30
     # y: log10 fit over (1e-2, 2e-2, 5e-3): slope = (log10(5e-3) - log10(1e-2)) / 2 < 0 => asymptotic
     b = (math.log10(5e-3) - math.log10(1e-2)) / 2
     a = np.mean(np.log10([1e-2, 2e-2, 5e-3])) - 2 * b
@@ -508,6 +511,21 @@ def test_q13_extrapolation(orc):
     tau2 = tau.copy(); tau2[0, 0, 1:5] = 1e-15
     mp2, _ = orc.build_map(o, tau2, 1, 8)
     assert mp2[0, 0, 0, 7] == mp2[0, 0, 0, 0]
+    # R11: a direction at rounding level next to the element's others (here z,
+    # 1e-12 against x's 1e-1: above the A14 floor, growing with p, so
+    # non-asymptotic) is resolved, not a sentinel; at 1e-7 of the others it
+    # is estimated (sentinel for n_z >= N_z)
+    o4 = np.array([[5, 5, 5]], np.int32)
+    tau4 = np.full((1, 3, 9), np.nan)
+    tau4[0, :, 0] = 1e-3
+    tau4[0, 0, 1:5] = [1e-1, 1e-2, 1e-3, 1e-4]
+    tau4[0, 1, 1:5] = [1e-2, 1e-3, 1e-4, 1e-5]
+    tau4[0, 2, 1:5] = [1e-12, 2e-12, 3e-12, 4e-12]
+    mp4, _ = orc.build_map(o4, tau4, 5, 8)
+    assert np.all(mp4 < 1e30) and np.all(mp4[1:] == mp4[0])  # independent of n_z
+    tau4[0, 2, 1:5] = [1e-8, 2e-8, 3e-8, 4e-8]
+    mp5, _ = orc.build_map(o4, tau4, 5, 8)
+    assert np.all(mp5 >= 1e30)
     # N_d = 1: keep the order
     o3 = np.array([[1, 4, 2]], np.int32)
     mp3, _ = orc.build_map(o3, tau, 1, 8)

@@ -16,6 +16,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--noise", type=float, default=0.0)
 ap.add_argument("--steps", type=int, nargs="+", default=[80000])
 ap.add_argument("--out", default="gpurun_out/cyl_tau.npz")
+ap.add_argument("--ref", choices=("solver", "same"), default="solver")
 a = ap.parse_args()
 nsp = W.ns_params()
 mesh = W.make_mesh(W.CONFIGS["cfg4"]["mesh"])
@@ -30,8 +31,9 @@ out, done = {}, 0
 for n in sorted(a.steps):
     S.rk_steps(n - done, q, qb, g, dts[0], dts[1], 0.5) if (n - done) % 2 == 0 else None
     done = n
-    r = S.rhs_eval(q)
-    out[f"s{n}_new"] = S.tau_estimate(q, r, formulation=dg.TAU_NEW).cpu().numpy()
-    out[f"s{n}_trad"] = S.tau_estimate(q, r, formulation=dg.TAU_TRADITIONAL).cpu().numpy()
+    r = S.rhs_eval(q) if a.ref == "solver" else None
+    refk = dg.REF_SOLVER if a.ref == "solver" else dg.REF_SAME
+    out[f"s{n}_new"] = S.tau_estimate(q, r, formulation=dg.TAU_NEW, reference=refk).cpu().numpy()
+    out[f"s{n}_trad"] = S.tau_estimate(q, r, formulation=dg.TAU_TRADITIONAL, reference=refk).cpu().numpy()
 np.savez_compressed(a.out, **out)
 print("ok", list(out))
