@@ -272,7 +272,7 @@ class Cfg5Run:
             from paper_2210_03523_b200.dist import DistSolver
 
             owner = part.slab_owner(mesh.dims, world, axis=1)  # azimuthal slabs
-            self.D = DistSolver(mesh, owner, rank, world, **kw)
+            self.D = DistSolver(mesh, owner, rank, world, overlap=True, **kw)  # trace exchange overlapped
             self.D.set_orders(orders)
             self.core = self.D.S
             self.E_loc = self.D.lm.E

@@ -208,6 +208,15 @@ dg_status dg_rk_stage(dg_ctx* ctx, int stage, const double* q_in_dev, double* q_
 /* flags for dg_rk_stage / dg_rhs_eval_flags: */
 #define DG_FLAG_GRADIENT_READY 1 /* NS: skip the BR1 gradient pass; the caller ran dg_gradient
                                     and refreshed the halo rows of dg_gradient_buffer() */
+/* Split face pass (the halo exchange overlapped with the faces
+ * that do not touch it; runtime-order path only, non-isolated variant, NS with
+ * DG_FLAG_GRADIENT_READY).  DG_FLAG_FACES_INTERIOR launches only the numerical
+ * fluxes of the faces with no halo side and returns (nothing else runs); the
+ * caller then completes the halo trace exchange on the same stream and calls
+ * again with DG_FLAG_FACES_HALO and the same arguments: the faces with a halo
+ * side, then the element kernel.  The pair is bit-identical to one call. */
+#define DG_FLAG_FACES_INTERIOR 2
+#define DG_FLAG_FACES_HALO 4
 /* NS: BR1 gradient of q (eq DGSEMsystem:2) of the owned elements
  * into the context's gradient buffer (15 doubles per node, [k][v] = d q_v /
  * d x_k, element e at 3 x its state offset); the buffer's device pointer is
@@ -215,6 +224,11 @@ dg_status dg_rk_stage(dg_ctx* ctx, int stage, const double* q_in_dev, double* q_
  * Every non-isolated residual, RK stage and tau-estimate (non-isolated coarse
  * levels included: their contexts borrow this buffer) overwrites it. */
 dg_status dg_gradient(dg_ctx* ctx, int variant, const double* q_dev, void* stream);
+/* dg_gradient with the split BR1 face pass (DG_FLAG_FACES_INTERIOR: only the
+ * face states q^ of the faces without a halo side, nothing else; then
+ * DG_FLAG_FACES_HALO after the state-trace exchange: the remaining faces and
+ * the gradient kernel).  Non-isolated variant only. */
+dg_status dg_gradient_flags(dg_ctx* ctx, int variant, const double* q_dev, int flags, void* stream);
 double* dg_gradient_buffer(dg_ctx* ctx);
 /* Non-isolated tau-estimation of ONE coarse level (d, p) on a rank-local mesh
  * (reading R7), in two phases.  phase 0:

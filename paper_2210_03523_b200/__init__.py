@@ -35,13 +35,14 @@ SELECT_DYNAMIC, SELECT_STATIC_ACCUM, SELECT_STATIC_FINAL, SELECT_A1_ACCUM, SELEC
 COMBINE_MAX, COMBINE_AV = 0, 1
 TAU_STRIDE = 9
 FLAG_GRADIENT_READY = 1
+FLAG_FACES_INTERIOR, FLAG_FACES_HALO = 2, 4
 NMAX = 8
 
 EXPORTS = ["dg_create", "dg_destroy", "dg_last_error", "dg_mesh_upload", "dg_set_orders", "dg_state_len", "dg_ndof",
            "dg_node_coords", "dg_rhs_eval", "dg_compute_dt", "dg_rk_step", "dg_tau_estimate", "dg_select_orders",
            "dg_transfer", "dg_diagnostics", "dg_launch_count", "dg_rk_step_dt", "dg_set_owned", "dg_rk_stage",
            "dg_dt_accumulate", "dg_dt_finalize", "dg_select_local", "dg_jump_sweep", "dg_owned_state_len", "dg_gradient",
-           "dg_gradient_buffer", "dg_rhs_eval_flags", "dg_rk_steps", "dg_trace_copy", "dg_tau_level", "dg_set_path"]
+           "dg_gradient_buffer", "dg_rhs_eval_flags", "dg_rk_steps", "dg_trace_copy", "dg_tau_level", "dg_set_path", "dg_gradient_flags"]
 
 
 def sources():
@@ -352,9 +353,11 @@ class Solver:
                                        _dptr(lam, 2, "rk_stage lam", torch.int64, optional=True), int(flags),
                                        _stream(stream)), "dg_rk_stage")
 
-    def gradient(self, q, variant=NONISOLATED, stream=None):
-        self._check(self.L.dg_gradient(self.ctx, int(variant), _dptr(q, self.state_len, "gradient q"), _stream(stream)),
-                    "dg_gradient")
+    def gradient(self, q, variant=NONISOLATED, stream=None, flags=0):
+        """BR1 gradient into gradient_buffer(); flags FLAG_FACES_INTERIOR /
+        FLAG_FACES_HALO split its face pass around a halo exchange."""
+        self._check(self.L.dg_gradient_flags(self.ctx, int(variant), _dptr(q, self.state_len, "gradient q"), int(flags),
+                                             _stream(stream)), "dg_gradient_flags")
 
     def gradient_buffer(self):
         """torch view of the context's gradient buffer (15 doubles per node)."""

@@ -208,6 +208,7 @@ struct dg_ctx {
     std::vector<int> nscls_swH, nscls_swG;  // per class: max stage words of an item (gradient / residual kernel)
     NsFace* d_nsfaces = nullptr;
     int nsf_cls[4] = {0, 0, 0, 0};  // faces of W = 1..3 warps: [nsf_cls[W-1], nsf_cls[W])
+    int nsf_mid[4] = {0, 0, 0, 0};  // inside class W: faces with a halo side from nsf_mid[W] on
     double* d_fg = nullptr;         // face metrics at the mortar points
     double* d_nsG = nullptr;        // numerical-flux blocks (scratch per residual)
     double* d_nsH = nullptr;        // BR1 face-term blocks (scratch per residual)
@@ -915,9 +916,13 @@ static dg_status build_ns_plans(dg_ctx* ctx, PlanTimer& tm)
         std::vector<NsFace> sorted;
         sorted.reserve(fl.size());
         ctx->nsf_cls[0] = 0;
-        for (int w = 1; w <= 3; ++w) {
+        auto halo = [&](const NsFace& F) { return F.eL >= ctx->n_own || F.eR >= ctx->n_own; };
+        for (int w = 1; w <= 3; ++w) {  // per class: interior faces, then those with a halo side
             for (size_t i = 0; i < fl.size(); ++i)
-                if (fw[i] == w) sorted.push_back(fl[i]);
+                if (fw[i] == w && !halo(fl[i])) sorted.push_back(fl[i]);
+            ctx->nsf_mid[w] = (int)sorted.size();
+            for (size_t i = 0; i < fl.size(); ++i)
+                if (fw[i] == w && halo(fl[i])) sorted.push_back(fl[i]);
             ctx->nsf_cls[w] = (int)sorted.size();
         }
         if (sorted.size() != fl.size()) return fail(ctx, DG_EINVAL, "set_orders: face with more than 96 mortar points");
@@ -1359,13 +1364,16 @@ dg_status dg_node_coords(dg_ctx* ctx, double* X)
 }
 
 }  // extern "C"
+// part: FACES_ALL, FACES_INTERIOR (no halo side: may run while the halo
+// traces are in flight), FACES_HALO (the rest)
+enum { FACES_ALL = 0, FACES_INTERIOR = 1, FACES_HALO = 2 };
 template <int MODE>
-static void launch_ns_faces(dg_ctx* ctx, const NsFaceParams& base, cudaStream_t st)
+static void launch_ns_faces(dg_ctx* ctx, const NsFaceParams& base, cudaStream_t st, int part = FACES_ALL)
 {
     for (int w = 1; w <= 3; ++w) {
         NsFaceParams P = base;
-        P.fbase = ctx->nsf_cls[w - 1];
-        P.fend = ctx->nsf_cls[w];
+        P.fbase = part == FACES_HALO ? ctx->nsf_mid[w] : ctx->nsf_cls[w - 1];
+        P.fend = part == FACES_INTERIOR ? ctx->nsf_mid[w] : ctx->nsf_cls[w];
         const int nf = P.fend - P.fbase;
         if (nf <= 0) continue;
         if (w == 1) k_ns_face<1, MODE><<<(nf + FaceCfg<1>::G - 1) / FaceCfg<1>::G, FaceCfg<1>::BS, FaceCfg<1>::smem, st>>>(P);
@@ -1407,13 +1415,14 @@ static NsFaceParams ns_face_params(dg_ctx* ctx, const double* q)
 
 // BR1 gradient of the owned elements into d_grad (eq DGSEMsystem:2):
 // face terms H (non-isolated), then the element kernel.
-static dg_status launch_ns_gradient(dg_ctx* ctx, int variant, const double* q, cudaStream_t st)
+static dg_status launch_ns_gradient(dg_ctx* ctx, int variant, const double* q, cudaStream_t st, int part = FACES_ALL)
 {
     const bool noniso = variant == DG_NONISOLATED;
     if (noniso) {
         NsFaceParams F = ns_face_params(ctx, q);
         F.out = ctx->d_nsH;
-        launch_ns_faces<MODE_QHAT>(ctx, F, st);
+        launch_ns_faces<MODE_QHAT>(ctx, F, st, part);
+        if (part == FACES_INTERIOR) return check_stream_error(ctx, "k_ns_face launch");
     }
     NsElemParams P = ns_elem_params(ctx, q);
     P.gout = ctx->d_grad;
@@ -1442,6 +1451,9 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
 {
     const bool ns = ctx->prm.physics == DG_NS;
     const bool noniso = variant == DG_NONISOLATED;
+    const int part = (flags & DG_FLAG_FACES_INTERIOR) ? FACES_INTERIOR : ((flags & DG_FLAG_FACES_HALO) ? FACES_HALO : FACES_ALL);
+    if (part != FACES_ALL && (!noniso || (ns && !(flags & DG_FLAG_GRADIENT_READY))))
+        return fail(ctx, DG_EINVAL, "residual: split face passes need the non-isolated variant (NS: and the gradient formed)");
     if (ns && !(flags & 1)) {  // flag 1: the caller already formed the gradient (multi-rank halo)
         dg_status s = launch_ns_gradient(ctx, variant, q, st);
         if (s != DG_OK) return s;
@@ -1449,8 +1461,9 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
     if (noniso) {
         NsFaceParams F = ns_face_params(ctx, q);
         F.out = ctx->d_nsG;
-        if (ns) launch_ns_faces<MODE_FLUX_NS>(ctx, F, st);
-        else launch_ns_faces<MODE_FLUX_EULER>(ctx, F, st);
+        if (ns) launch_ns_faces<MODE_FLUX_NS>(ctx, F, st, part);
+        else launch_ns_faces<MODE_FLUX_EULER>(ctx, F, st, part);
+        if (part == FACES_INTERIOR) return check_stream_error(ctx, "k_ns_face launch");
     }
     NsElemParams P = ns_elem_params(ctx, q);
     P.grad = ctx->d_grad;
@@ -1860,8 +1873,10 @@ dg_status dg_rk_stage(dg_ctx* ctx, int stage, const double* q_in, double* q_out,
     if (ctx->prm.physics == DG_NS && !ctx->curved) return fail(ctx, DG_EUNSUPPORTED, "rk_stage: NS needs the curved path");
     static const double A[3] = {0.0, -5.0 / 9.0, -153.0 / 128.0};
     static const double B[3] = {1.0 / 3.0, 15.0 / 16.0, 8.0 / 15.0};
+    if ((flags & (DG_FLAG_FACES_INTERIOR | DG_FLAG_FACES_HALO)) && !ctx->curved)
+        return fail(ctx, DG_EUNSUPPORTED, "rk_stage: split face passes need the runtime-order path (dg_set_path)");
     return launch_residual(ctx, DG_NONISOLATED, q_in, q_out, g, dt_dev, A[stage], B[stage], 1, (cudaStream_t)stream,
-                           lam_accum_dev, flags & DG_FLAG_GRADIENT_READY);
+                           lam_accum_dev, flags & (DG_FLAG_GRADIENT_READY | DG_FLAG_FACES_INTERIOR | DG_FLAG_FACES_HALO));
 }
 
 dg_status dg_gradient(dg_ctx* ctx, int variant, const double* q_dev, void* stream)
@@ -1870,6 +1885,16 @@ dg_status dg_gradient(dg_ctx* ctx, int variant, const double* q_dev, void* strea
     if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "gradient: orders not set");
     if (ctx->prm.physics != DG_NS || !ctx->curved) return fail(ctx, DG_EUNSUPPORTED, "gradient: NS on the curved path only");
     return launch_ns_gradient(ctx, variant, q_dev, (cudaStream_t)stream);
+}
+
+dg_status dg_gradient_flags(dg_ctx* ctx, int variant, const double* q_dev, int flags, void* stream)
+{
+    if (!ctx || !q_dev) return DG_EINVAL;
+    if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "gradient: orders not set");
+    if (ctx->prm.physics != DG_NS || !ctx->curved) return fail(ctx, DG_EUNSUPPORTED, "gradient: NS on the curved path only");
+    const int part = (flags & DG_FLAG_FACES_INTERIOR) ? FACES_INTERIOR : ((flags & DG_FLAG_FACES_HALO) ? FACES_HALO : FACES_ALL);
+    if (part != FACES_ALL && variant != DG_NONISOLATED) return fail(ctx, DG_EINVAL, "gradient: split face passes are non-isolated");
+    return launch_ns_gradient(ctx, variant, q_dev, (cudaStream_t)stream, part);
 }
 
 double* dg_gradient_buffer(dg_ctx* ctx) { return ctx ? ctx->d_grad : nullptr; }
@@ -1893,8 +1918,10 @@ dg_status dg_rhs_eval_flags(dg_ctx* ctx, int variant, const double* q_dev, doubl
 {
     if (!ctx || !q_dev || !qdot_dev) return DG_EINVAL;
     if (!ctx->have_orders) return fail(ctx, DG_ESTATE, "rhs_eval: orders not set");
+    if ((flags & (DG_FLAG_FACES_INTERIOR | DG_FLAG_FACES_HALO)) && !ctx->curved)
+        return fail(ctx, DG_EUNSUPPORTED, "rhs_eval: split face passes need the runtime-order path (dg_set_path)");
     return launch_residual(ctx, variant, q_dev, qdot_dev, nullptr, nullptr, 0.0, 0.0, 0, (cudaStream_t)stream, nullptr,
-                           flags & DG_FLAG_GRADIENT_READY);
+                           flags & (DG_FLAG_GRADIENT_READY | DG_FLAG_FACES_INTERIOR | DG_FLAG_FACES_HALO));
 }
 
 dg_status dg_dt_finalize(dg_ctx* ctx, unsigned long long* lam_accum_dev, double cfl, double* dt_dev, void* stream)

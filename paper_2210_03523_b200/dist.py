@@ -71,7 +71,9 @@ class TraceExchange:
     def bytes_per_exchange(self):
         return 8 * sum(self.plan.send_len.values())
 
-    def __call__(self, field, group=None):
+    def start(self, field, group=None):
+        """pack on the current stream and post the P2P operations (NCCL runs
+        them on its own stream once the packs are done); returns the requests"""
         import torch.distributed as dist
 
         nc = self.plan.ncomp
@@ -80,11 +82,18 @@ class TraceExchange:
             self.S.trace_copy(self.send[r], field, nc, self.sbuf[r], 0)
             ops.append(dist.P2POp(dist.isend, self.sbuf[r][: max(1, self.plan.send_len[r])], r, group))
             ops.append(dist.P2POp(dist.irecv, self.rbuf[r][: max(1, self.plan.recv_len[r])], r, group))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        return dist.batch_isend_irecv(ops) if ops else []
+
+    def finish(self, field, reqs):
+        """the current stream waits for the transfers, then unpacks"""
+        for req in reqs:
+            req.wait()
+        nc = self.plan.ncomp
         for r in sorted(self.recv):
             self.S.trace_copy(self.recv[r], field, nc, self.rbuf[r], 1)
+
+    def __call__(self, field, group=None):
+        self.finish(field, self.start(field, group))
 
 
 def migrate(q_owned, plan: "part.MigrationPlan", group=None):
@@ -123,10 +132,14 @@ class DistSolver:
     """A `Solver` on this rank's local mesh (owned + halo elements) plus the
     exchanges that make owned results identical to the single-rank ones."""
 
-    def __init__(self, global_mesh, owner: np.ndarray, rank: int, world: int, group=None, **solver_kw):
+    def __init__(self, global_mesh, owner: np.ndarray, rank: int, world: int, group=None, overlap=False,
+                 **solver_kw):
+        """overlap: each RK stage launches the faces without a halo side while
+        the halo traces are in flight (runtime-order path: curved meshes, or
+        path=PATH_RUNTIME on affine ones)."""
         from . import Solver
 
-        self.rank, self.world, self.group = rank, world, group
+        self.rank, self.world, self.group, self.overlap = rank, world, group, overlap
         self.mesh, self.owner, self.solver_kw = global_mesh, np.asarray(owner), dict(solver_kw)
         self.lm = part.local_mesh(global_mesh, owner, rank)
         self.physics = solver_kw.get("physics", 0)
@@ -213,12 +226,37 @@ class DistSolver:
         src, dst = [q_in, q_out, q_in], [q_out, q_in, q_out]
         self._lam.zero_()
         for k in range(3):
+            if self.overlap:
+                self._stage_overlapped(k, src[k], dst[k], g, dt)
+                continue
             self.halo(src[k])
             flags = self._gradient_halo(src[k])
             self.S.rk_stage(k, src[k], dst[k], g, dt, self._lam if k == 2 else None, flags)
         dist.all_reduce(self._lam, op=dist.ReduceOp.MAX, group=self.group)
         self.S._check(self.S.L.dg_dt_finalize(self.S.ctx, C.c_void_p(self._lam.data_ptr()), C.c_double(cfl),
                                               C.c_void_p(dt_next.data_ptr()), self._stream()), "dg_dt_finalize")
+
+    def _stage_overlapped(self, k, q, q_out, g, dt):
+        """One RK stage with the trace exchanges overlapped: the faces with no
+        halo side run while the traces are in flight; the halo
+        faces and the element kernels after the exchange completes."""
+        from . import FLAG_FACES_HALO, FLAG_FACES_INTERIOR, FLAG_GRADIENT_READY, NS
+
+        lam = self._lam if k == 2 else None
+        reqs = self.tq.start(q, self.group)
+        if self.physics == NS:
+            self.S.gradient(q, flags=FLAG_FACES_INTERIOR)
+            self.tq.finish(q, reqs)
+            self.S.gradient(q, flags=FLAG_FACES_HALO)
+            gb = self.S.gradient_buffer()
+            reqs = self.tg.start(gb, self.group)
+            self.S.rk_stage(k, q, q_out, g, dt, lam, FLAG_GRADIENT_READY | FLAG_FACES_INTERIOR)
+            self.tg.finish(gb, reqs)
+            self.S.rk_stage(k, q, q_out, g, dt, lam, FLAG_GRADIENT_READY | FLAG_FACES_HALO)
+        else:
+            self.S.rk_stage(k, q, q_out, g, dt, lam, FLAG_FACES_INTERIOR)
+            self.tq.finish(q, reqs)
+            self.S.rk_stage(k, q, q_out, g, dt, lam, FLAG_FACES_HALO)
 
     def tau_estimate(self, q, qdot_ref=None, noniso=False, **kw):
         """Isolated levels: element-local.  noniso (SURVEY 8(f) rank 1,
@@ -308,7 +346,7 @@ def rebalance(ds: DistSolver, global_orders, q_local, axis: int = 2):
     new_owner = part.dof_owner(ds.mesh.dims, go, ds.world, axis)
     plan = part.MigrationPlan(ds.owner, new_owner, go, ds.rank, ds.world)
     q_own = migrate(q_local[: int(plan.old_off[-1])], plan, ds.group)
-    nd = DistSolver(ds.mesh, new_owner, ds.rank, ds.world, ds.group, **ds.solver_kw)
+    nd = DistSolver(ds.mesh, new_owner, ds.rank, ds.world, ds.group, overlap=ds.overlap, **ds.solver_kw)
     nd.set_orders(go)
     n = part.element_offsets(go[nd.lm.gids])
     q_new = torch.zeros(int(n[-1]), dtype=q_local.dtype, device=q_local.device)

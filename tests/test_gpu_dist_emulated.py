@@ -334,3 +334,87 @@ def test_two_rank_noniso_tau(dg, orc, case):
         got = taus[r][: lm.n_own].cpu().numpy()
         want = t0[lm.gids[: lm.n_own]]
         assert np.array_equal(got, want, equal_nan=True), np.nanmax(np.abs(got - want))
+
+
+@pytest.mark.parametrize("case", ["cube_mixed_runtime", "ogrid_ns"])
+def test_two_rank_split_faces(dg, orc, case):
+    """The overlapped stage of DistSolver (DG_FLAG_FACES_INTERIOR, then the
+    trace exchange, then DG_FLAG_FACES_HALO): before every
+    interior-face call the halo copies of the state (and of the gradient) are
+    reset to NaN, so the interior faces provably read no halo data; two RK
+    steps give owned states bit-identical to the single-rank solver."""
+    import torch
+
+    from paper_2210_03523_b200 import partition as part
+
+    if case == "cube_mixed_runtime":
+        mesh = W.cube_mesh(4, 4, 6)
+        g_orders = W.orders_random(mesh.E, 2, 6, 31)
+        kw = dict(path=dg.PATH_RUNTIME)
+        P = orc.Problem(mesh)
+        q_g = W.pulse_state(P.node_coords(g_orders), g_orders, sigma=0.2)
+        owner = part.slab_owner(mesh.dims, 2, axis=2)
+    else:
+        mesh = W.ogrid_mesh(4, 8, 2, ratio=1.1 ** 12, g_eta=2)
+        g_orders = W.orders_random(mesh.E, (2, 2, 2), (6, 6, 2), 32)
+        nsp = W.ns_params()
+        kw = dict(physics=dg.NS, mu=nsp["mu"], Pr=nsp["Pr"], qinf=nsp["qinf"])
+        q_g = W.freestream_noise_state(g_orders, (1.0, 1.0, 0.0, 0.0, nsp["p_inf"]))
+        owner = part.slab_owner(mesh.dims, 2, axis=1)
+    ns = case == "ogrid_ns"
+    S0 = dg.Solver(mesh, **kw)
+    S0.set_orders(g_orders)
+    q0 = torch.from_numpy(q_g).cuda()
+    qa0, qb0, g0 = q0.clone(), torch.empty_like(q0), torch.empty_like(q0)
+    dt = torch.full((1,), 1e-4, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        S0.rk_step(qa0, qb0, g0, dt)
+        qa0, qb0 = qb0, qa0
+    lms = [part.local_mesh(mesh, owner, r) for r in range(2)]
+    off = W.offsets(g_orders)
+    blocks = [q_g[a:b] for a, b in zip(off[:-1], off[1:])]
+    solvers, tq, tg, qa, qb, gg = [], [], [], [], [], []
+    for lm in lms:
+        S = dg.Solver(lm, **kw)
+        S.set_owned(lm.n_own)
+        lo = g_orders[lm.gids]
+        S.set_orders(lo)
+        solvers.append(S)
+        tq.append(part.TracePlan(lm, lo, 5))
+        tg.append(part.TracePlan(lm, lo, 15))
+        x = torch.from_numpy(np.concatenate([blocks[g] if i < lm.n_own else np.full_like(blocks[g], np.nan)
+                                             for i, g in enumerate(lm.gids)])).cuda()
+        qa.append(x)
+        qb.append(torch.empty_like(x))
+        gg.append(torch.zeros_like(x))
+    own = [S.owned_len() for S in solvers]
+    for _ in range(2):
+        src, dst = [qa, qb, qa], [qb, qa, qb]
+        for k in range(3):
+            for r in range(2):
+                src[k][r][own[r]:] = float("nan")
+            if ns:
+                for r in range(2):
+                    solvers[r].gradient(src[k][r], flags=dg.FLAG_FACES_INTERIOR)
+                _copy_traces(solvers, tq, src[k], 5)
+                for r in range(2):
+                    solvers[r].gradient(src[k][r], flags=dg.FLAG_FACES_HALO)
+                    solvers[r].gradient_buffer()[3 * own[r]:] = float("nan")
+                    solvers[r].rk_stage(k, src[k][r], dst[k][r], gg[r], dt, None,
+                                        dg.FLAG_GRADIENT_READY | dg.FLAG_FACES_INTERIOR)
+                _copy_traces(solvers, tg, [S.gradient_buffer() for S in solvers], 15)
+                for r in range(2):
+                    solvers[r].rk_stage(k, src[k][r], dst[k][r], gg[r], dt, None,
+                                        dg.FLAG_GRADIENT_READY | dg.FLAG_FACES_HALO)
+            else:
+                for r in range(2):
+                    solvers[r].rk_stage(k, src[k][r], dst[k][r], gg[r], dt, None, dg.FLAG_FACES_INTERIOR)
+                _copy_traces(solvers, tq, src[k], 5)
+                for r in range(2):
+                    solvers[r].rk_stage(k, src[k][r], dst[k][r], gg[r], dt, None, dg.FLAG_FACES_HALO)
+        qa, qb = qb, qa
+    ref = qa0.cpu().numpy()
+    for r, lm in enumerate(lms):
+        got = qa[r][: own[r]].cpu().numpy()
+        want = np.concatenate([ref[off[g]:off[g + 1]] for g in lm.gids[: lm.n_own]])
+        assert np.array_equal(got, want), np.nanmax(np.abs(got - want))
