@@ -492,10 +492,11 @@ def run_e2e(R, args, stream, ev, world):
     out_pinned = [torch.empty(total_len, dtype=torch.float64).pin_memory() for _ in range(2)]
     bufs = [torch.zeros(total_len, dtype=torch.float64, device=stream.device) for _ in range(2)]
     if isinstance(R, Cfg2Run):
-        bufs = [torch.zeros(R.S.state_len, dtype=torch.float64, device=stream.device) for _ in range(2)]
+        R.S.set_orders(R.orders)  # the IC layout (the timed run left an adapted one)
+        bufs = [torch.zeros(max(R.S.state_len, R.buf[0].numel()), dtype=torch.float64, device=stream.device)
+                for _ in range(2)]
         pinned = torch.from_numpy(R.q0_host).pin_memory()
         owned = R.q0_host.size
-        R.S.set_orders(R.orders)
         R.S.compute_dt(R.buf[R.cur][: R.S.state_len], CFL, R.dts[0])
     cs = torch.cuda.Stream()
     ev_in = [torch.cuda.Event() for _ in range(args.steps + 1)]

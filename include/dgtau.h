@@ -59,7 +59,7 @@ enum { DG_JUMP_A = 0, DG_JUMP_B = 1 };
 enum { DG_SELECT_DYNAMIC = 0, DG_SELECT_STATIC_ACCUM = 1, DG_SELECT_STATIC_FINAL = 2,
        DG_SELECT_A1_ACCUM = 3, DG_SELECT_A1_FINAL = 4 };
 enum { DG_COMBINE_MAX = 0, DG_COMBINE_AV = 1 };
-enum { DG_PATH_AUTO = 0, DG_PATH_RUNTIME = 1 };
+enum { DG_PATH_AUTO = 0, DG_PATH_RUNTIME = 1, DG_PATH_BUCKETED = 2 };
 
 #define DG_NMAX 8
 #define DG_TAU_STRIDE 9
@@ -116,15 +116,18 @@ void dg_destroy(dg_ctx* ctx);
 const char* dg_last_error(const dg_ctx* ctx);
 
 /* Kernel path of the residual (same discretisation, equal up to
- * rounding): DG_PATH_AUTO (default) runs affine meshes on the
- * order-specialised kernels, one launch per (N1,N2,N3) bucket, replayed as a
- * CUDA graph -- fastest for uniform or few-bucket layouts; DG_PATH_RUNTIME
- * runs them on the runtime-order kernels of the curved path (element items of
- * any orders in three size-class launches, faces in three warp-width
- * classes) -- for many-bucket layouts that change every few steps (dynamic
- * adaptation), where launch count and re-planning dominate.
- * Curved meshes always take the runtime-order kernels.  Call before
- * dg_mesh_upload (DG_ESTATE after it); DG_EINVAL for an unknown path. */
+ * rounding).  Two kernel families: the order-specialised kernels (affine Euler
+ * only; one launch per (N1,N2,N3) bucket, replayed as a CUDA graph -- fastest
+ * for uniform or few-bucket layouts) and the runtime-order kernels of the
+ * curved path (element items of any orders in three size-class launches,
+ * faces in three warp-width classes -- for many-bucket layouts, which dynamic
+ * adaptation changes every few steps).  DG_PATH_AUTO (default):
+ * curved meshes and NS take the runtime-order kernels; affine Euler layouts
+ * are decided at every dg_set_orders by their bucket count (more than 24:
+ * runtime-order).  DG_PATH_RUNTIME / DG_PATH_BUCKETED force one family
+ * (BUCKETED: affine Euler only; curved meshes and NS still run the
+ * runtime-order kernels).  Call before dg_mesh_upload (DG_ESTATE after it);
+ * DG_EINVAL for an unknown path. */
 dg_status dg_set_path(dg_ctx* ctx, int path);
 
 /* Upload the mesh (copied).  gorder[3] geometry orders (1..4).  Elements

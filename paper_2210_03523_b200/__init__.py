@@ -28,7 +28,7 @@ EULER, NS = 0, 1
 ROE, LLF = 0, 1
 NONISOLATED, ISOLATED = 0, 1
 TAU_NEW, TAU_TRADITIONAL = 0, 1
-PATH_AUTO, PATH_RUNTIME = 0, 1
+PATH_AUTO, PATH_RUNTIME, PATH_BUCKETED = 0, 1, 2
 REF_SOLVER, REF_SAME = 0, 1
 JUMP_A, JUMP_B = 0, 1
 SELECT_DYNAMIC, SELECT_STATIC_ACCUM, SELECT_STATIC_FINAL, SELECT_A1_ACCUM, SELECT_A1_FINAL = 0, 1, 2, 3, 4

@@ -324,6 +324,12 @@ inline bool getenv_flag(const char* name)
     return g && g[0] == '1';
 }
 
+// DG_PATH_AUTO on affine Euler meshes: layouts with more (N1,N2,N3) buckets
+// than this take the runtime-order kernels (profiles/r02_prof_adapt_n32.txt:
+// 343 buckets, 1.54 -> 1.15 ms per residual; uniform orders stay 2.2x faster
+// on the order-specialised kernels)
+constexpr int RT_BUCKETS = 24;
+
 // DGTAU_TIMING=1: host-side section times of dg_set_orders on stderr (device
 // work synchronised at each mark)
 struct PlanTimer {
@@ -627,7 +633,8 @@ int64_t dg_launch_count(const dg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 dg_status dg_set_path(dg_ctx* ctx, int path)
 {
     if (!ctx) return DG_EINVAL;
-    if (path != DG_PATH_AUTO && path != DG_PATH_RUNTIME) return fail(ctx, DG_EINVAL, "set_path: unknown path");
+    if (path != DG_PATH_AUTO && path != DG_PATH_RUNTIME && path != DG_PATH_BUCKETED)
+        return fail(ctx, DG_EINVAL, "set_path: unknown path");
     if (ctx->E != 0) return fail(ctx, DG_ESTATE, "set_path: call before dg_mesh_upload");
     ctx->path = path;
     return DG_OK;
@@ -672,14 +679,15 @@ dg_status dg_mesh_upload(dg_ctx* ctx, int E, const int32_t* nbr_host, const int3
             if (!(hi > lo)) affine = false;
         }
     }
-    // DG_PATH_RUNTIME (dg_set_path): affine meshes take the runtime-order
-    // (class-batched) kernels of the curved path too
+    // kernel path (dg_set_path): curved meshes and NS take the runtime-order
+    // kernels; affine Euler meshes are decided per layout in dg_set_orders
+    // (AUTO: runtime-order kernels when the layout has many (N1,N2,N3) buckets)
     ctx->affine_geo = affine;
-    ctx->curved = !affine || ctx->path == DG_PATH_RUNTIME;
+    ctx->curved = !affine || ctx->path == DG_PATH_RUNTIME || ctx->prm.physics == DG_NS;
     ctx->tau_curved = ctx->curved && !(affine && ctx->prm.physics == DG_EULER);
     // extruded mesh (ns.cuh): linear in zeta, x and y independent of zeta, z
     // independent of xi and eta and increasing with zeta
-    bool ext = ctx->curved && gorder_host[2] == 1 && !getenv_flag("DGTAU_NO_EXT");
+    bool ext = gorder_host[2] == 1 && !getenv_flag("DGTAU_NO_EXT");
     {
         const int L2 = (gorder_host[0] + 1) * (gorder_host[1] + 1);
         for (int e = 0; e < E && ext; ++e) {
@@ -692,11 +700,9 @@ dg_status dg_mesh_upload(dg_ctx* ctx, int E, const int32_t* nbr_host, const int3
         }
     }
     ctx->extruded = ext;
-    if (ctx->curved) {
-        if (!affine)
-            for (long long i = 0; i < 3LL * E; ++i) ctx->h[i] = 1.0;  // unused by the curved kernels
-        CK(upload(ctx->d_geo, ctx->geo));
-    }
+    if (!affine)
+        for (long long i = 0; i < 3LL * E; ++i) ctx->h[i] = 1.0;  // unused by the curved kernels
+    CK(upload(ctx->d_geo, ctx->geo));  // (affine layouts may take the runtime-order kernels too)
     CK(upload(ctx->d_nbr, ctx->nbr));
     CK(upload(ctx->d_h, ctx->h));
     ctx->have_orders = false;
@@ -1007,6 +1013,20 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
     for (long long i = 0; i < 3LL * E; ++i)
         if (orders_host[i] < 1 || orders_host[i] > NMAX) return fail(ctx, DG_EINVAL, "set_orders: order out of 1..8");
     ctx->orders.assign(orders_host, orders_host + 3LL * E);
+    if (ctx->affine_geo && ctx->prm.physics == DG_EULER && ctx->path != DG_PATH_RUNTIME) {
+        // AUTO: many (N1,N2,N3) buckets -> the class-batched runtime-order
+        // kernels (a handful of launches; section 7.3 of DESIGN.md); few ->
+        // the order-specialised ones (one launch per bucket, CUDA graph)
+        bool seen[NMAX * NMAX * NMAX] = {};
+        int nb = 0;
+        for (int e = 0; e < ctx->n_own; ++e) {
+            const int* N = &ctx->orders[3 * e];
+            const int k = (N[0] - 1) + NMAX * ((N[1] - 1) + NMAX * (N[2] - 1));
+            if (!seen[k]) { seen[k] = true; ++nb; }
+        }
+        ctx->curved = ctx->path == DG_PATH_AUTO && nb > RT_BUCKETS;
+        ctx->tau_curved = false;  // affine Euler: k_tau5 on either path
+    }
     ctx->off.assign(E + 1, 0);
     ctx->ndof = 0;
     ctx->maxn = 0;

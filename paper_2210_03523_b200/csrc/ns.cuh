@@ -539,6 +539,13 @@ __device__ __forceinline__ void ns_produce(const NsElemParams& P, int item, doub
     if (lane < it.count) {
         // residual kernel, RK stages 2-3: the register g is read in the epilogue -> into L2 now
         if (!hblk && P.mode == 1 && P.rkA != 0.0) bulk_prefetch_l2(P.g + a, (unsigned)((b - a) * 8));
+        // residual kernel (NS): the node phase reads the element's gradient
+        // (15 n, plain loads) -> into L2 one stage ahead (the buffer is
+        // allocated with 2 doubles of slack: the rounded end stays inside)
+        if (!hblk && P.grad) {
+            const long long g0 = (3 * M.off[lane]) & ~1LL, g1 = (3 * M.off[lane] + 15LL * n + 1) & ~1LL;
+            bulk_prefetch_l2(P.grad + g0, (unsigned)((g1 - g0) * 8));
+        }
         bulk_g2s(st + Lo.q0 + lane * Lo.qs, P.q + a, (unsigned)((b - a) * 8), full);
         bulk_g2s(st + Lo.m0 + lane * Lo.ms, (EXT ? P.metc : P.met) + mo, (unsigned)(Lo.ms * 8), full);
         if (faces) {

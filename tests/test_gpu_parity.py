@@ -533,9 +533,11 @@ def test_graph_repoint_bitwise(dg, orc, monkeypatch):
     import torch
 
     mesh, orders, kw = CASES["cfg3_subbox_mixed"]()
-    P, Sg, q, qd = setup(dg, orc, mesh, orders, **kw)
+    P, _, q, qd = setup(dg, orc, mesh, orders, **kw)
+    Sg = dg.Solver(mesh, path=dg.PATH_BUCKETED)  # the order-specialised kernels (AUTO picks the runtime-order ones)
+    Sg.set_orders(orders)
     monkeypatch.setenv("DGTAU_NO_GRAPHS", "1")
-    Sd = dg.Solver(mesh)
+    Sd = dg.Solver(mesh, path=dg.PATH_BUCKETED)
     Sd.set_orders(orders)
     outs = []
     for S in (Sg, Sd):

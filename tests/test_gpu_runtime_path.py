@@ -24,13 +24,13 @@ def dg():
     return m
 
 
-def setup_rt(dg, orc, case):
+def setup_rt(dg, orc, case, path=None):
     import torch
 
     mesh, orders, kw = CASES[case]()
     P = orc.Problem(mesh)
     q = W.pulse_state(P.node_coords(orders), orders, **kw)
-    S = dg.Solver(mesh, path=dg.PATH_RUNTIME)
+    S = dg.Solver(mesh, path=dg.PATH_RUNTIME if path is None else path)
     S.set_orders(orders)
     return mesh, orders, P, S, q, torch.from_numpy(q).cuda()
 
@@ -111,3 +111,49 @@ def test_ns_on_affine_mesh(dg, orc):
     c = (1.4 * nsp["p_inf"]) ** 0.5
     assert rel_linf(rg.cpu().numpy(), ro, orders, floor=(1.0, c, c, c, nsp["p_inf"] / 0.4)) < RES_TOL
     assert tau_rel(S.tau_estimate(qd, rg).cpu().numpy(), P.tau_estimate(orders, q, ro)) < TAU_TOL
+
+
+@pytest.mark.parametrize("case", list(CASES))
+@pytest.mark.parametrize("variant", [0, 1])
+def test_rhs_bucketed_path(dg, orc, case, variant):
+    """The order-specialised kernels forced on every layout (DG_PATH_BUCKETED;
+    AUTO hands many-bucket layouts to the runtime-order kernels)."""
+    mesh, orders, P, S, q, qd = setup_rt(dg, orc, case, dg.PATH_BUCKETED)
+    r = S.rhs_eval(qd, variant=variant).cpu().numpy()
+    assert rel_linf(r, P.rhs(orders, q, variant), orders) < RES_TOL
+
+
+@pytest.mark.parametrize("case", ["cfg3_subbox_mixed", "ragged_1to8"])
+def test_rk_and_tau_bucketed_path(dg, orc, case):
+    import torch
+
+    mesh, orders, P, S, q, qd = setup_rt(dg, orc, case, dg.PATH_BUCKETED)
+    dts = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in range(2)]
+    S.compute_dt(qd, 0.5, dts[0])
+    qa, qb, g = qd.clone(), torch.empty_like(qd), torch.empty_like(qd)
+    qs, _ = S.rk_steps(3, qa, qb, g, dts[0], dts[1], 0.5)
+    qo = q.copy()
+    for _ in range(3):
+        qo = P.rk3_step(orders, qo, P.dt(orders, qo, 0.5))
+    assert rel_linf(qs.cpu().numpy(), qo, orders) < RES_TOL
+    tg = S.tau_estimate(qd, S.rhs_eval(qd), noniso=True).cpu().numpy()
+    assert tau_rel(tg, P.tau_estimate_noniso(orders, q, P.rhs(orders, q))) < TAU_TOL
+
+
+def test_auto_path_switches_per_layout(dg, orc):
+    """AUTO: a uniform layout launches one order-specialised kernel per
+    residual; a many-bucket layout of the same solver a handful of
+    runtime-order launches; both against the oracle."""
+    import torch
+
+    mesh = W.cube_mesh(6)
+    P = orc.Problem(mesh)
+    S = dg.Solver(mesh)
+    for orders in (W.orders_uniform(mesh.E, 4), W.orders_random(mesh.E, 2, 7, 5), W.orders_uniform(mesh.E, 3)):
+        S.set_orders(orders)
+        q = W.pulse_state(P.node_coords(orders), orders, sigma=0.15)
+        qd = torch.from_numpy(q).cuda()
+        n0 = S.launches
+        r = S.rhs_eval(qd).cpu().numpy()
+        assert rel_linf(r, P.rhs(orders, q), orders) < RES_TOL
+        assert S.launches - n0 <= 8
