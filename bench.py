@@ -45,6 +45,8 @@ import numpy as np  # noqa: E402
 
 import workloads as W  # noqa: E402
 
+PATHS = {"auto": lambda dg: dg.PATH_AUTO, "runtime": lambda dg: dg.PATH_RUNTIME, "bucketed": lambda dg: dg.PATH_BUCKETED}
+
 METRIC = "DGSEM residual GDOF/s (fp64) + tau-estimation elems/s"
 CFL = 0.5
 CFG5_RK = 20             # RK3 steps per measurement
@@ -350,7 +352,7 @@ class Cfg2Run:
         self.dg, self.world = dg, world
         self.mesh = W.cube_mesh(16)
         self.orders = W.orders_uniform(self.mesh.E, 6)
-        self.S = dg.Solver(self.mesh)
+        self.S = dg.Solver(self.mesh, path=PATHS[os.environ.get("BENCH_PATH", "auto")](dg))
         self.S.set_orders(self.orders)
         self.core = self.S
         self.E_loc = self.n_own = self.mesh.E
@@ -640,7 +642,10 @@ def main():
     ap.add_argument("--workload", default="cfg5", choices=["cfg5", "cfg2"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--path", default="auto", choices=["auto", "runtime", "bucketed"],
+                    help="cfg2: residual kernel family (dg_set_path); AUTO decides per layout")
     args = ap.parse_args()
+    os.environ["BENCH_PATH"] = args.path
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     if world > 1:

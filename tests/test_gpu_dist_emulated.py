@@ -63,7 +63,9 @@ def test_two_rank_emulated(dg, orc, case, halo):
     if case in ("cube_mixed", "cube_rebalanced"):
         mesh = W.cube_mesh(4, 4, 6)
         g_orders = W.orders_random(mesh.E, 2, 6, 31)
-        kw = {}
+        # bitwise comparison across solvers of different bucket counts: one
+        # kernel family for all (AUTO would pick per layout)
+        kw = dict(path=dg.PATH_BUCKETED)
         P = orc.Problem(mesh)
         if case == "cube_rebalanced":  # adapted orders skewed to low z, DOF-balanced slabs (dist.rebalance)
             g_orders[np.arange(mesh.E) // 16 < 2] = np.minimum(g_orders[np.arange(mesh.E) // 16 < 2] + 2, 8)
@@ -282,7 +284,7 @@ def test_two_rank_noniso_tau(dg, orc, case):
     if case == "cube_mixed":
         mesh = W.cube_mesh(4, 4, 6)
         g_orders = W.orders_random(mesh.E, 2, 6, 31)
-        kw = {}
+        kw = dict(path=dg.PATH_BUCKETED)  # one kernel family on every solver (bitwise comparison)
         P = orc.Problem(mesh)
         q_g = W.pulse_state(P.node_coords(g_orders), g_orders, sigma=0.2)
         owner = part.slab_owner(mesh.dims, 2, axis=2)
@@ -418,3 +420,54 @@ def test_two_rank_split_faces(dg, orc, case):
         got = qa[r][: own[r]].cpu().numpy()
         want = np.concatenate([ref[off[g]:off[g + 1]] for g in lm.gids[: lm.n_own]])
         assert np.array_equal(got, want), np.nanmax(np.abs(got - want))
+
+
+@pytest.mark.parametrize("physics", ["euler", "ns"])
+def test_distsolver_overlap_single_rank(dg, orc, physics):
+    """DistSolver(overlap=True) on a one-rank gloo group: the overlapped stage
+    (interior faces, exchange, halo faces + element kernels) through its
+    Python driver gives the plain solver's RK step bit for bit."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2210_03523_b200 import partition as part
+    from paper_2210_03523_b200.dist import DistSolver
+
+    if not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=0, world_size=1)
+    if physics == "euler":
+        mesh = W.cube_mesh(4, 4, 4)
+        orders = W.orders_random(mesh.E, 2, 6, 41)
+        kw = dict(path=dg.PATH_RUNTIME)
+        q = W.pulse_state(orc.Problem(mesh).node_coords(orders), orders, sigma=0.2)
+    else:
+        mesh = W.ogrid_mesh(4, 8, 2, ratio=1.1 ** 12, g_eta=2)
+        orders = W.orders_random(mesh.E, (2, 2, 2), (6, 6, 2), 32)
+        nsp = W.ns_params()
+        kw = dict(physics=dg.NS, mu=nsp["mu"], Pr=nsp["Pr"], qinf=nsp["qinf"])
+        q = W.freestream_noise_state(orders, (1.0, 1.0, 0.0, 0.0, nsp["p_inf"]))
+    S = dg.Solver(mesh, **kw)
+    S.set_orders(orders)
+    D = DistSolver(mesh, part.slab_owner(mesh.dims, 1), 0, 1, overlap=True, **kw)
+    D.set_orders(orders)
+    qd = torch.from_numpy(q).cuda()
+    outs = []
+    for step in (lambda a, b, g, dt, dn: S.rk_step_dt(a, b, g, dt, 0.5, dn),
+                 lambda a, b, g, dt, dn: D.rk_step_dt(a, b, g, dt, 0.5, dn)):
+        dt = torch.zeros(1, dtype=torch.float64, device="cuda")
+        S.compute_dt(qd, 0.5, dt)
+        dn = torch.zeros_like(dt)
+        qa, qb, g = qd.clone(), torch.empty_like(qd), torch.empty_like(qd)
+        step(qa, qb, g, dt, dn)
+        outs.append((qb.cpu().numpy(), dn.item()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert outs[0][1] == outs[1][1]
