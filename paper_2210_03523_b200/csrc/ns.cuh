@@ -1130,9 +1130,12 @@ __device__ __forceinline__ void mortar_to_side(const double* Fm, int nc, int ma,
 
 // resident CTAs per SM the register budget targets: the BR1 qhat pass fits in
 // 80 registers without spills (more faces in flight), the NS flux needs 128
+#ifndef NS_FLUX_MINB1
+#define NS_FLUX_MINB1 4
+#endif
 __host__ __device__ constexpr int face_minb(int W, int MODE)
 {
-    return MODE == MODE_QHAT ? (W == 1 ? 6 : 4) : (W == 3 ? 2 : 4);
+    return MODE == MODE_QHAT ? (W == 1 ? 6 : 4) : (W == 3 ? 2 : (W == 1 ? NS_FLUX_MINB1 : 4));
 }
 
 template <int W, int MODE>
