@@ -89,12 +89,15 @@ def _compile(srcs, verbose=False, force_all=False):
         elif s.endswith((".cu", ".cpp")):
             units.append((s, [], os.path.basename(s) + ".o"))
     hdr_t = max(os.path.getmtime(s) for s in srcs if s.endswith((".cuh", ".h")))
+    # the 512 order-specialised residual instances include residual_t.cuh only
+    res_t = max(os.path.getmtime(os.path.join(_CSRC, h)) for h in ("residual_t.cuh", "common.cuh", "basis.h"))
     cflags = [f for f in NVCC_FLAGS if f != "-shared"]
 
     def one(u):
         src, defs, name = u
         obj = os.path.join(objdir, name)
-        if not force_all and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(src), hdr_t):
+        dep_t = res_t if defs else hdr_t
+        if not force_all and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(src), dep_t):
             return obj
         cmd = ["nvcc", *cflags, *defs, "-c", src, "-o", obj] + (["-Xptxas=-v"] if verbose else [])
         subprocess.check_call(cmd)
@@ -130,9 +133,10 @@ def lib():
     """Load libdgtau.so; raises if it is missing (no fallback)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(_SO):
-            raise DGError(f"{_SO} not built: run __graft_entry__.build() (no CPU fallback exists)")
-        L = C.CDLL(_SO)
+        so = os.environ.get("DGTAU_SO", _SO)  # A/B timing of in-tree kernel variants (tools/)
+        if not os.path.exists(so):
+            raise DGError(f"{so} not built: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(so)
         L.dg_last_error.restype = C.c_char_p
         L.dg_state_len.restype = C.c_int64
         L.dg_ndof.restype = C.c_int64

@@ -36,6 +36,7 @@ struct PhysDev {
     int physics;
     double mu, Pr;
     double qinf[5];
+    double kappa;  // mu gamma / ((gamma - 1) Pr), formed once on the host
 };
 
 struct WorkItem {
@@ -70,6 +71,19 @@ __device__ __forceinline__ double rcp_nr(double x)
     y = fma(y, e, y);
     e = fma(-x, y, 1.0);
     return fma(y, e, y);
+}
+
+#ifndef DG_FAST_DIV
+#define DG_FAST_DIV 1
+#endif
+// 1/x of the face and viscous point fluxes: rcp_nr (branch-free, ~1 ulp) or IEEE
+__device__ __forceinline__ double inv_pos(double x)
+{
+#if DG_FAST_DIV
+    return rcp_nr(x);
+#else
+    return 1.0 / x;
+#endif
 }
 
 __device__ __forceinline__ double rsqrt_nr(double x)
@@ -147,14 +161,14 @@ __device__ __forceinline__ void roe_flux(const double* qL, const double* qR, con
                                          double* F)
 {
     const double gm1 = gamma - 1.0;
-    const double irL = 1.0 / qL[0], irR = 1.0 / qR[0];
+    const double irL = inv_pos(qL[0]), irR = inv_pos(qR[0]);
     double uL[3], uR[3];
     for (int k = 0; k < 3; ++k) { uL[k] = qL[1 + k] * irL; uR[k] = qR[1 + k] * irR; }
     const double pL = gm1 * (qL[4] - 0.5 * qL[0] * (uL[0] * uL[0] + uL[1] * uL[1] + uL[2] * uL[2]));
     const double pR = gm1 * (qR[4] - 0.5 * qR[0] * (uR[0] * uR[0] + uR[1] * uR[1] + uR[2] * uR[2]));
     const double HL = (qL[4] + pL) * irL, HR = (qR[4] + pR) * irR;
     const double sL = sqrt(qL[0]), sR = sqrt(qR[0]);
-    const double is = 1.0 / (sL + sR);
+    const double is = inv_pos(sL + sR);
     double u[3];
     for (int k = 0; k < 3; ++k) u[k] = (sL * uL[k] + sR * uR[k]) * is;
     const double H = (sL * HL + sR * HR) * is;
@@ -168,7 +182,7 @@ __device__ __forceinline__ void roe_flux(const double* qL, const double* qR, con
     const double dr = qR[0] - qL[0], dp = pR - pL, dun = unR - unL;
     double du[3];
     for (int k = 0; k < 3; ++k) du[k] = uR[k] - uL[k];
-    const double ic2 = 1.0 / c2;
+    const double ic2 = inv_pos(c2);
     const double a1 = 0.5 * (dp - rho * c * dun) * ic2;
     const double a5 = 0.5 * (dp + rho * c * dun) * ic2;
     const double a2 = dr - dp * ic2;

@@ -40,7 +40,7 @@ __device__ __forceinline__ void visc_dot(const double* q, const double* g /*[15]
                                          double az, const PhysDev& ph, double* fv)
 {
     const double gam = ph.gamma, mu = ph.mu;
-    const double ir = 1.0 / q[0];
+    const double ir = inv_pos(q[0]);
     const double u = q[1] * ir, v = q[2] * ir, w = q[3] * ir;
     const double p = (gam - 1.0) * (q[4] - 0.5 * q[0] * (u * u + v * v + w * w));
     const double T = p * ir;
@@ -55,7 +55,7 @@ __device__ __forceinline__ void visc_dot(const double* q, const double* g /*[15]
         dT[j] = (dp - T * gj[0]) * ir;
     }
     const double div = du[0][0] + du[1][1] + du[2][2];
-    const double kappa = mu * gam / ((gam - 1.0) * ph.Pr);
+    const double kappa = ph.kappa;
     const double a[3] = {ax, ay, az};
     double ta[3];  // tau . a
 #pragma unroll
@@ -74,7 +74,8 @@ __device__ __forceinline__ void visc_dot(const double* q, const double* g /*[15]
 
 // visc_dot split in two: the node's stress tensor and temperature gradient
 // once (from q and its gradient), then the flux along any vector a with the
-// same operations in the same order (bit-identical to visc_dot)
+// same operations in the same order as visc_dot, except 1/rho: IEEE division
+// here (rcp_nr measured slower in k_ns_res), inv_pos in the face kernels
 struct ViscNode {
     double T[3][3];   // mu (du_i/dx_j + du_j/dx_i - 2/3 div delta_ij)
     double dT[3];     // grad T
@@ -107,7 +108,7 @@ __device__ __forceinline__ void visc_node(const double* q, const double* g, cons
     V.u[0] = u;
     V.u[1] = v;
     V.u[2] = w;
-    V.kappa = mu * gam / ((gam - 1.0) * ph.Pr);
+    V.kappa = ph.kappa;
 }
 
 __device__ __forceinline__ void visc_along(const ViscNode& V, double ax, double ay, double az, double* fv)

@@ -312,6 +312,7 @@ PhysDev phys_dev(const dg_params& p)
     ph.physics = p.physics;
     ph.mu = p.mu;
     ph.Pr = p.Pr;
+    ph.kappa = p.mu * p.gamma / ((p.gamma - 1.0) * p.Pr);
     for (int v = 0; v < 5; ++v) ph.qinf[v] = p.qinf[v];
     return ph;
 }

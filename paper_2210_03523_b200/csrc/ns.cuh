@@ -1077,15 +1077,107 @@ __device__ __forceinline__ void side_to_mortar(const double* __restrict__ qsrc, 
     grp_sync<W>(gid);  // X / Y free for the next call
 }
 
+// measured on cfg5: the one-latency gather pays for the W = 1 flux pass
+// (d = 0, 1 faces of the O-grid, 5.19 -> 4.37 ms), not for the qhat pass or
+// the W = 2, 3 classes (extra registers / code: slower)
+#ifndef NS_FACE_DIRECT
+#define NS_FACE_DIRECT 1
+#endif
+#ifndef NS_FACE_DIRECT_MAXW
+#define NS_FACE_DIRECT_MAXW 1
+#endif
+
+// A side needs at most one interpolation pass (s_a = m_a or s_b = m_b): the
+// pass-A thread (b, i) of side_to_mortar is then the owner of mortar point
+// p = i + m_a b, so the pass runs straight from the gathered trace into val
+// (no Y round trip, no barrier), and both sides' traces can be gathered at
+// once (X: L, Y: R) -- one memory latency per face instead of two.
+__device__ __forceinline__ bool one_pass(const FSide& s, int ma, int mb) { return s.sa == ma || s.sb == mb; }
+
+template <int W, int NCM>
+__device__ __forceinline__ void side_gather(const double* __restrict__ qsrc, const double* __restrict__ gsrc,
+                                            const FSide& s, double* X, int l)
+{
+    constexpr int CAP = 32 * W;
+    const int sa = s.sa, ns = sa * s.sb;
+    if (l < ns) {
+        const int b = l / sa, a = l - b * sa;
+        const long long node = s.base + a * s.sta + b * s.stb;
+#pragma unroll
+        for (int c = 0; c < NCM; ++c)
+            X[c * CAP + l] = c < NV ? __ldg(qsrc + (long long)c * s.n + node) : __ldg(gsrc + (long long)(c - NV) * s.n + node);
+    }
+}
+
+// val at mortar point p (< m_a m_b) from the gathered trace X of a one-pass
+// side: the same fma sequence as side_to_mortar's single pass
+template <int W, int NCM>
+__device__ __forceinline__ void side_direct(const double* X, const FSide& s, int ma, int mb, const Tables* tab, int p,
+                                            double* val)
+{
+    constexpr int CAP = 32 * W;
+    const int sa = s.sa, sb = s.sb;
+    const int j = p / ma, i = p - j * ma;
+    if (sa < ma) {  // sb == mb: row j of the trace along a
+        const double* Ta = tab->T[sa - 1][ma - 1];
+        double t[NP];
+#pragma unroll
+        for (int a = 0; a < NP; ++a) t[a] = a < sa ? __ldg(Ta + i * sa + a) : 0.0;
+#pragma unroll
+        for (int c = 0; c < NCM; ++c) {
+            const double* x = X + c * CAP + j * sa;
+            double acc = 0.0;
+#pragma unroll
+            for (int a = 0; a < NP; ++a)
+                if (a < sa) acc = fma(t[a], x[a], acc);
+            val[c] = acc;
+        }
+    } else if (sb < mb) {  // sa == ma: column i along b
+        const double* Tb = tab->T[sb - 1][mb - 1];
+        double t[NP];
+#pragma unroll
+        for (int b = 0; b < NP; ++b) t[b] = b < sb ? __ldg(Tb + j * sb + b) : 0.0;
+#pragma unroll
+        for (int c = 0; c < NCM; ++c) {
+            double acc = 0.0;
+#pragma unroll
+            for (int b = 0; b < NP; ++b)
+                if (b < sb) acc = fma(t[b], X[c * CAP + b * ma + i], acc);
+            val[c] = acc;
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < NCM; ++c) val[c] = X[c * CAP + p];
+    }
+}
+
 // Project nc components held at the mortar points (Fm[c CAP + p]) onto a
 // side's own face nodes, stored to out[c (sa sb) + a + sa b].
-template <int W>
+template <int W, bool DIR>
 __device__ __forceinline__ void mortar_to_side(const double* Fm, int nc, int ma, int mb, int sa, int sb, const Tables* tab,
                                                double* Y, double* __restrict__ out, int l, int gid)
 {
     constexpr int CAP = 32 * W;
     const double* Z = Fm;
     int zrow = ma;
+    if (DIR && sa < ma && sb == mb) {  // one pass: thread (b, i) owns side node i + sa b
+        if (l < mb * sa) {
+            const double* Pa = tab->P[ma - 1][sa - 1];
+            const int b = l / sa, i = l - b * sa;
+            double t[NP];
+#pragma unroll
+            for (int k = 0; k < NP; ++k) t[k] = k < ma ? __ldg(Pa + i * ma + k) : 0.0;
+            for (int c = 0; c < nc; ++c) {
+                const double* f = Fm + c * CAP + b * ma;
+                double acc = 0.0;
+#pragma unroll
+                for (int k = 0; k < NP; ++k)
+                    if (k < ma) acc = fma(t[k], f[k], acc);
+                out[(long long)c * (sa * sb) + l] = acc;
+            }
+        }
+        return;  // Fm is only read; Y untouched
+    }
     if (sa < ma) {
         if (l < mb * sa) {
             const double* Pa = tab->P[ma - 1][sa - 1];  // [i * ma + k]
@@ -1130,8 +1222,9 @@ __device__ __forceinline__ void mortar_to_side(const double* Fm, int nc, int ma,
 
 // resident CTAs per SM the register budget targets: the BR1 qhat pass fits in
 // 80 registers without spills (more faces in flight), the NS flux needs 128
+// (W = 1 with the one-latency gather: 168 at 3 CTAs, cfg5 3.90 -> 3.80 ms)
 #ifndef NS_FLUX_MINB1
-#define NS_FLUX_MINB1 4
+#define NS_FLUX_MINB1 3
 #endif
 __host__ __device__ constexpr int face_minb(int W, int MODE)
 {
@@ -1167,9 +1260,20 @@ __global__ void __launch_bounds__(FaceCfg<W>::BS, face_minb(W, MODE)) k_ns_face(
     const int kind = F.kind;
     double qL[NV] = {0, 0, 0, 0, 0}, qR[NV] = {0, 0, 0, 0, 0};
     int nout;
+    constexpr bool DIRECT_OK = NS_FACE_DIRECT && MODE != MODE_QHAT && W <= NS_FACE_DIRECT_MAXW;
+    const bool direct = DIRECT_OK && (!hasL || one_pass(SL, ma, mb)) && (!hasR || one_pass(SR, ma, mb));
     if (MODE == MODE_QHAT) {
-        if (hasL) side_to_mortar<W, NV>(P.q + SL.off, nullptr, SL, NV, ma, mb, P.tab, X, Y, l, gid, p, qL);
-        if (hasR) side_to_mortar<W, NV>(P.q + SR.off, nullptr, SR, NV, ma, mb, P.tab, X, Y, l, gid, p, qR);
+        if (direct) {
+            if (hasL) side_gather<W, NV>(P.q + SL.off, nullptr, SL, X, l);
+            if (hasR) side_gather<W, NV>(P.q + SR.off, nullptr, SR, Y, l);
+            grp_sync<W>(gid);
+            if (pon && hasL) side_direct<W, NV>(X, SL, ma, mb, P.tab, p, qL);
+            if (pon && hasR) side_direct<W, NV>(Y, SR, ma, mb, P.tab, p, qR);
+            grp_sync<W>(gid);  // X is overwritten below
+        } else {
+            if (hasL) side_to_mortar<W, NV>(P.q + SL.off, nullptr, SL, NV, ma, mb, P.tab, X, Y, l, gid, p, qL);
+            if (hasR) side_to_mortar<W, NV>(P.q + SR.off, nullptr, SR, NV, ma, mb, P.tab, X, Y, l, gid, p, qR);
+        }
         const int nk = P.ext ? ext_nk(d) : 3;
         nout = NV * nk;
         if (pon) {
@@ -1200,13 +1304,22 @@ __global__ void __launch_bounds__(FaceCfg<W>::BS, face_minb(W, MODE)) k_ns_face(
         // viscous flux along Ja_f formed at once (one side's gradient live)
         double fsum[NV] = {0, 0, 0, 0, 0};
         constexpr int NCI = MODE == MODE_FLUX_NS ? 20 : NV;
+        if (direct) {
+            if (hasL) side_gather<W, NCI>(P.q + SL.off, MODE == MODE_FLUX_NS ? P.grad + 3 * SL.off : nullptr, SL, X, l);
+            if (hasR) side_gather<W, NCI>(P.q + SR.off, MODE == MODE_FLUX_NS ? P.grad + 3 * SR.off : nullptr, SR, Y, l);
+            grp_sync<W>(gid);
+        }
         for (int side = 0; side < 2; ++side) {
             const bool has = side ? hasR : hasL;
             if (!has) continue;
             const FSide& S = side ? SR : SL;
             double val[NCI];
-            side_to_mortar<W, NCI>(P.q + S.off, MODE == MODE_FLUX_NS ? P.grad + 3 * S.off : nullptr, S, NCI, ma, mb, P.tab,
-                                   X, Y, l, gid, p, val);
+            if (direct) {
+                if (pon) side_direct<W, NCI>(side ? Y : X, S, ma, mb, P.tab, p, val);
+            } else {
+                side_to_mortar<W, NCI>(P.q + S.off, MODE == MODE_FLUX_NS ? P.grad + 3 * S.off : nullptr, S, NCI, ma, mb,
+                                       P.tab, X, Y, l, gid, p, val);
+            }
             if (pon) {
                 double* qs = side ? qR : qL;
 #pragma unroll
@@ -1219,10 +1332,16 @@ __global__ void __launch_bounds__(FaceCfg<W>::BS, face_minb(W, MODE)) k_ns_face(
                 }
             }
         }
+        if (direct) grp_sync<W>(gid);  // every lane's reads of X / Y done: X takes G below
         if (pon) {
             double G[NV];
             const double S = sqrt(jf[0] * jf[0] + jf[1] * jf[1] + jf[2] * jf[2]);
+#if DG_FAST_DIV
+            const double iS = inv_pos(S);
+            const double nrm[3] = {jf[0] * iS, jf[1] * iS, jf[2] * iS};
+#else
             const double nrm[3] = {jf[0] / S, jf[1] / S, jf[2] / S};
+#endif
             if (kind >= 2) {
                 double qg[NV];
                 ghost_state(hasL ? qL : qR, kind == 2 ? -1 : -2, P.ph, qg);
@@ -1260,8 +1379,8 @@ __global__ void __launch_bounds__(FaceCfg<W>::BS, face_minb(W, MODE)) k_ns_face(
         }
         return;
     }
-    if (hasL) mortar_to_side<W>(X, nout, ma, mb, SL.sa, SL.sb, P.tab, Y, P.out + oL, l, gid);
-    if (hasR) mortar_to_side<W>(X, nout, ma, mb, SR.sa, SR.sb, P.tab, Y, P.out + oR, l, gid);
+    if (hasL) mortar_to_side<W, DIRECT_OK>(X, nout, ma, mb, SL.sa, SL.sb, P.tab, Y, P.out + oL, l, gid);
+    if (hasR) mortar_to_side<W, DIRECT_OK>(X, nout, ma, mb, SR.sa, SR.sb, P.tab, Y, P.out + oR, l, gid);
 }
 
 }  // namespace dgtau
