@@ -500,7 +500,8 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         cudaFuncSetAttribute(k_ns_res<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
         cudaFuncSetAttribute(k_ns_res<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, lns);
 #define NSF_ATTR(W)                                                                                                   \
-    cudaFuncSetAttribute(k_ns_face<W, MODE_QHAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FaceCfg<W>::smem);  \
+    cudaFuncSetAttribute(k_ns_face<W, MODE_QHAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,                          \
+                         (int)FaceCfg<W, MODE_QHAT>::smem);                                                             \
     cudaFuncSetAttribute(k_ns_face<W, MODE_FLUX_EULER>, cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
                          (int)FaceCfg<W>::smem);                                                                        \
     cudaFuncSetAttribute(k_ns_face<W, MODE_FLUX_NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FaceCfg<W>::smem);
@@ -1397,9 +1398,12 @@ static void launch_ns_faces(dg_ctx* ctx, const NsFaceParams& base, cudaStream_t 
         P.fend = part == FACES_INTERIOR ? ctx->nsf_mid[w] : ctx->nsf_cls[w];
         const int nf = P.fend - P.fbase;
         if (nf <= 0) continue;
-        if (w == 1) k_ns_face<1, MODE><<<(nf + FaceCfg<1>::G - 1) / FaceCfg<1>::G, FaceCfg<1>::BS, FaceCfg<1>::smem, st>>>(P);
-        else if (w == 2) k_ns_face<2, MODE><<<(nf + FaceCfg<2>::G - 1) / FaceCfg<2>::G, FaceCfg<2>::BS, FaceCfg<2>::smem, st>>>(P);
-        else k_ns_face<3, MODE><<<(nf + FaceCfg<3>::G - 1) / FaceCfg<3>::G, FaceCfg<3>::BS, FaceCfg<3>::smem, st>>>(P);
+        using C1 = FaceCfg<1, MODE>;
+        using C2 = FaceCfg<2, MODE>;
+        using C3 = FaceCfg<3, MODE>;
+        if (w == 1) k_ns_face<1, MODE><<<(nf + C1::G - 1) / C1::G, C1::BS, C1::smem, st>>>(P);
+        else if (w == 2) k_ns_face<2, MODE><<<(nf + C2::G - 1) / C2::G, C2::BS, C2::smem, st>>>(P);
+        else k_ns_face<3, MODE><<<(nf + C3::G - 1) / C3::G, C3::BS, C3::smem, st>>>(P);
         ctx->launches++;
     }
 }

@@ -973,15 +973,15 @@ __device__ __forceinline__ void grp_sync(int gid)
     }
 }
 
-// groups per CTA and buffer sizes: a buffer holds 20 component slots of CAP points
-template <int W>
+// groups per CTA and buffer sizes: a buffer holds 20 component slots of CAP
+// points (flux passes: q and the gradient), 15 in the qhat pass (5 nk outputs)
+template <int W, int MODE = MODE_FLUX_NS>
 struct FaceCfg {
     static constexpr int G = W == 1 ? 4 : 2;      // groups per CTA
     static constexpr int BS = G * 32 * W;
     static constexpr int CAP = 32 * W;
-    static constexpr int BUF = 20 * CAP;
+    static constexpr int BUF = (MODE == MODE_QHAT ? 15 : 20) * CAP;
     static constexpr size_t smem = sizeof(double) * (size_t)G * 2 * BUF;
-    static constexpr int MINB = W == 1 ? 4 : (W == 2 ? 4 : 2);
 };
 
 struct FSide {
@@ -1226,15 +1226,27 @@ __device__ __forceinline__ void mortar_to_side(const double* Fm, int nc, int ma,
 #ifndef NS_FLUX_MINB1
 #define NS_FLUX_MINB1 3
 #endif
+#ifndef NS_FLUX_MINB2
+#define NS_FLUX_MINB2 3
+#endif
+#ifndef NS_FLUX_MINB3
+#define NS_FLUX_MINB3 2
+#endif
+#ifndef NS_QHAT_MINB1
+#define NS_QHAT_MINB1 6
+#endif
+#ifndef NS_QHAT_MINB2
+#define NS_QHAT_MINB2 4
+#endif
 __host__ __device__ constexpr int face_minb(int W, int MODE)
 {
-    return MODE == MODE_QHAT ? (W == 1 ? 6 : 4) : (W == 3 ? 2 : (W == 1 ? NS_FLUX_MINB1 : 4));
+    return MODE == MODE_QHAT ? (W == 1 ? NS_QHAT_MINB1 : NS_QHAT_MINB2) : (W == 3 ? NS_FLUX_MINB3 : (W == 1 ? NS_FLUX_MINB1 : NS_FLUX_MINB2));
 }
 
 template <int W, int MODE>
 __global__ void __launch_bounds__(FaceCfg<W>::BS, face_minb(W, MODE)) k_ns_face(NsFaceParams P)
 {
-    using C = FaceCfg<W>;
+    using C = FaceCfg<W, MODE>;
     constexpr int CAP = C::CAP;
     extern __shared__ __align__(16) double fsm[];
     const int gid = threadIdx.x / (32 * W), l = threadIdx.x - gid * 32 * W;
