@@ -383,6 +383,9 @@ __device__ void element_metrics_fp64(const CurvedMesh& cm, int e, int o1, int o2
         __syncthreads();
         Gp = Mout;
     }
+    // coordinates relative to the first geometry node (D annihilates the
+    // shift; the sums run on O(h) values, not O(|x|): reading R6)
+    const double x0[3] = {__ldg(G), __ldg(G + cm.ng), __ldg(G + 2 * cm.ng)};
     for (int t = threadIdx.x; t < no; t += blockDim.x) {
         const int pk = IJK[t];  // packed (i, j, k), see k_tau_curved
         const int i = pk & 255, j = (pk >> 8) & 255, k = pk >> 16;
@@ -395,7 +398,7 @@ __device__ void element_metrics_fp64(const CurvedMesh& cm, int e, int o1, int o2
                     const double wgt = w23 * T1[i * ga + a];
                     const int gi = a + ga * (b + gb * c);
 #pragma unroll
-                    for (int q = 0; q < 3; ++q) x[q] = fma(wgt, Gp[q * cm.ng + gi], x[q]);
+                    for (int q = 0; q < 3; ++q) x[q] = fma(wgt, Gp[q * cm.ng + gi] - x0[q], x[q]);
                 }
             }
         }

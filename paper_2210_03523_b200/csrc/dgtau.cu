@@ -490,6 +490,9 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         cudaFuncSetAttribute(k_tau_curved<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
         cudaFuncSetAttribute(k_tau_curved<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
         cudaFuncSetAttribute(k_tau_curved<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
+        cudaFuncSetAttribute(k_tau_ext<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
+        cudaFuncSetAttribute(k_tau_ext<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
+        cudaFuncSetAttribute(k_tau_ext<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
         ctx->smem_limit = limc;
         // curved residual path (ns.cuh): element kernels up to 20 x 729 doubles, face kernels per W
         const int lns = limc;
@@ -2240,12 +2243,22 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
             C.formulation = o->formulation;
             C.restr = o->restriction;
             C.ph = phys_dev(ctx->prm);
+            // extruded meshes: compact double-double coarse metrics (k_tau_ext);
+            // DGTAU_TAU_GENERIC=1 keeps the generic 3-D kernel (tests run both)
+            const bool ext = ctx->extruded && !getenv_flag("DGTAU_TAU_GENERIC");
             for (const SizeClass& c : ctx->lcls) {
                 C.lbase = c.base;
-                const size_t smc = sizeof(double) * ((ctx->prm.physics == DG_NS ? 40 : 30) * (size_t)c.maxn + (c.maxn + 1) / 2);
-                if (c.maxn <= 64) k_tau_curved<64><<<c.count, 64, smc, st>>>(C);
-                else if (c.maxn <= 160) k_tau_curved<128><<<c.count, 128, smc, st>>>(C);
-                else k_tau_curved<256><<<c.count, 256, smc, st>>>(C);
+                if (ext) {
+                    const size_t smc = sizeof(double) * tau_ext_words(c.maxn, ctx->prm.physics == DG_NS);
+                    if (c.maxn <= 64) k_tau_ext<64><<<c.count, 64, smc, st>>>(C);
+                    else if (c.maxn <= 160) k_tau_ext<128><<<c.count, 128, smc, st>>>(C);
+                    else k_tau_ext<256><<<c.count, 256, smc, st>>>(C);
+                } else {
+                    const size_t smc = sizeof(double) * ((ctx->prm.physics == DG_NS ? 40 : 30) * (size_t)c.maxn + (c.maxn + 1) / 2);
+                    if (c.maxn <= 64) k_tau_curved<64><<<c.count, 64, smc, st>>>(C);
+                    else if (c.maxn <= 160) k_tau_curved<128><<<c.count, 128, smc, st>>>(C);
+                    else k_tau_curved<256><<<c.count, 256, smc, st>>>(C);
+                }
                 ctx->launches++;
             }
         } else if (ctx->ntgroups > 0) {

@@ -1395,4 +1395,244 @@ __global__ void __launch_bounds__(FaceCfg<W>::BS, face_minb(W, MODE)) k_ns_face(
     if (hasR) mortar_to_side<W, DIRECT_OK>(X, nout, ma, mb, SR.sa, SR.sb, P.tab, Y, P.out + oR, l, gid);
 }
 
+// ---------------------------------------------------------------------------
+// tau-estimation on EXTRUDED curved meshes (cfg4 / cfg5 O-grids), one CTA per
+// level (e, d, p) as k_tau_curved, with the coarse metrics in the compact
+// form of k_metrics_ext: 6 per (i, j) column of the coarse element (Ja^1 =
+// (a, b, 0), Ja^2 = (c, e, 0), Ja^3 = (0, 0, f), J), from the geometry
+// polynomial at the coarse nodes differentiated by D^O, in fp64 on
+// coordinates relative to the element's first geometry node (reading R6),
+// the zero components skipped in the BR1 gradient and the contravariant
+// fluxes (terms fma(D, 0 q, g) = g exactly).  Measured on cfg5: 56 ms per
+// estimate (generic 3-D kernel 66 ms, the same in double-double 82 ms);
+// parity on full cfg4 (SAME reference) 3.8e-11 (generic plain fp64 4.9e-10).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double ext_ja(const double* Mc, int nc, int col, int d, int k)
+{
+    if (d == 2) return k == 2 ? Mc[4 * nc + col] : 0.0;
+    if (k == 2) return 0.0;
+    return Mc[(2 * d + k) * nc + col];
+}
+
+template <int BS>
+__global__ void __launch_bounds__(BS, BS == 256 ? 2 : (BS == 128 ? 5 : 10)) k_tau_ext(CTauParams P)
+{
+    extern __shared__ double sm[];
+    __shared__ double red[32];
+    const TauLevel lv = P.levels[P.lbase + blockIdx.x];
+    const int e = lv.e, d = lv.d, p = lv.p;
+    const int n1 = P.orders[3 * e] + 1, n2 = P.orders[3 * e + 1] + 1, n3 = P.orders[3 * e + 2] + 1;
+    const int n = n1 * n2 * n3;
+    const int nd = d == 0 ? n1 : (d == 1 ? n2 : n3);
+    const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
+    const int o1 = d == 0 ? p + 1 : n1, o2 = d == 1 ? p + 1 : n2, o3 = d == 2 ? p + 1 : n3;
+    const int nO = o1 * o2 * o3, nc = o1 * o2;
+    const bool ns = P.ph.physics == 1;
+    __shared__ double Ds[3][NP * NP];
+    stage_D(Ds, P.tab, o1, o2, o3);
+    double* Mc = sm;                  // 6 nc compact metrics
+    double* Qc = Mc + 6 * nc;         // 5 nO
+    double* Rc = Qc + NV * nO;        // 5 nO
+    double* GA = Rc + NV * nO;        // 15 nO (NS): gradient, then the three directions' fluxes
+    double* F = GA;                   // Euler: one direction's flux, 5 nO (no gradient)
+    double* A = ns ? GA + 15 * nO : F + NV * nO;  // 5 nO divergence
+    double* Xs = GA;                  // 4 nc dd scratch of the coordinates (before GA / F are used)
+    int* IJK = reinterpret_cast<int*>(A + NV * nO);
+    for (int t = threadIdx.x; t < nO; t += BS) {
+        int ii, jj, kk;
+        node_ijk(t, o1, o2, ii, jj, kk);
+        IJK[t] = ii | (jj << 8) | (kk << 16);
+    }
+    // fp64 on coordinates relative to the element's first geometry node: D
+    // annihilates the shift (T reproduces constants, D 1 = 0), and the sums
+    // run on O(h) instead of O(|x|) values -- the cancellation of the absolute
+    // coordinates (|x| ~ 20 on elements of size 0.02) is what costs the plain
+    // fp64 metrics their digits (reading R6)
+    {
+        const int g1 = P.cm.g1, g2 = P.cm.g2, ga = g1 + 1, gb = g2 + 1;
+        const double* G = P.cm.geo + (long long)e * 3 * P.cm.ng;
+        const double* T1 = P.tab->T[g1][o1 - 1];
+        const double* T2 = P.tab->T[g2][o2 - 1];
+        const double x0 = __ldg(G), y0 = __ldg(G + P.cm.ng);
+        for (int t = threadIdx.x; t < nc; t += BS) {
+            const int i = t % o1, j = t / o1;
+            double x = 0.0, y = 0.0;
+            for (int b = 0; b <= g2; ++b) {
+                const double w2 = T2[j * gb + b];
+                for (int a = 0; a <= g1; ++a) {
+                    const double w = w2 * T1[i * ga + a];
+                    x = fma(w, __ldg(G + a + ga * b) - x0, x);
+                    y = fma(w, __ldg(G + P.cm.ng + a + ga * b) - y0, y);
+                }
+            }
+            Xs[t] = x;
+            Xs[nc + t] = y;
+        }
+        __syncthreads();
+        const double zz = 0.5 * (__ldg(G + 2 * P.cm.ng + ga * gb) - __ldg(G + 2 * P.cm.ng));
+        for (int t = threadIdx.x; t < nc; t += BS) {
+            const int i = t % o1, j = t / o1;
+            double xx = 0.0, yx = 0.0, xe = 0.0, ye = 0.0;
+            for (int m = 0; m < o1; ++m) {
+                const double dm = Ds[0][i * o1 + m];
+                xx = fma(dm, Xs[m + o1 * j], xx);
+                yx = fma(dm, Xs[nc + m + o1 * j], yx);
+            }
+            for (int m = 0; m < o2; ++m) {
+                const double dm = Ds[1][j * o2 + m];
+                xe = fma(dm, Xs[i + o1 * m], xe);
+                ye = fma(dm, Xs[nc + i + o1 * m], ye);
+            }
+            const double j3 = xx * ye - xe * yx;
+            Mc[t] = zz * ye;
+            Mc[nc + t] = -(zz * xe);
+            Mc[2 * nc + t] = -(zz * yx);
+            Mc[3 * nc + t] = zz * xx;
+            Mc[4 * nc + t] = j3;
+            Mc[5 * nc + t] = zz * j3;
+        }
+    }
+    __syncthreads();  // Xs (= GA / F) free, Mc ready
+    const long long o = P.off[e];
+    const double* T = P.restr ? P.tab->P[nd - 1][p] : P.tab->T[nd - 1][p];
+    for (int t = threadIdx.x; t < nO; t += BS) {
+        const int pk = IJK[t];
+        int i = pk & 255, j = (pk >> 8) & 255, k = pk >> 16;
+        const int ic = d == 0 ? i : (d == 1 ? j : k);
+        if (d == 0) i = 0; else if (d == 1) j = 0; else k = 0;
+        const int base = i + n1 * (j + n2 * k);
+        const double* qe = P.q + o;
+        const double* re = P.qref + o;
+        switch (nd) {
+            case 2: tau_interp_node<2>(T, ic, qe, re, n, base, stride, Qc, Rc, nO, t); break;
+            case 3: tau_interp_node<3>(T, ic, qe, re, n, base, stride, Qc, Rc, nO, t); break;
+            case 4: tau_interp_node<4>(T, ic, qe, re, n, base, stride, Qc, Rc, nO, t); break;
+            case 5: tau_interp_node<5>(T, ic, qe, re, n, base, stride, Qc, Rc, nO, t); break;
+            case 6: tau_interp_node<6>(T, ic, qe, re, n, base, stride, Qc, Rc, nO, t); break;
+            case 7: tau_interp_node<7>(T, ic, qe, re, n, base, stride, Qc, Rc, nO, t); break;
+            case 8: tau_interp_node<8>(T, ic, qe, re, n, base, stride, Qc, Rc, nO, t); break;
+            default: tau_interp_node<9>(T, ic, qe, re, n, base, stride, Qc, Rc, nO, t); break;
+        }
+        for (int v = 0; v < NV; ++v) A[v * nO + t] = 0.0;
+    }
+    __syncthreads();
+    if (ns) {  // isolated gradient J g_k = sum_d' D^{d'} (Ja^{d'}_k q), nonzero metric components only
+        for (int t = threadIdx.x; t < nO; t += BS) {
+            const int pk = IJK[t];
+            const int i = pk & 255, j = (pk >> 8) & 255, k = pk >> 16;
+            double g[15];
+#pragma unroll
+            for (int cc = 0; cc < 15; ++cc) g[cc] = 0.0;
+            {  // xi: Ja^1 = (a, b, 0)
+                const int base = t - i;
+                const double* Dr = Ds[0] + i * o1;
+                for (int m = 0; m < o1; ++m) {
+                    const double dm = Dr[m];
+                    const int col = m + o1 * j;
+                    const double ja = Mc[col], jb = Mc[nc + col];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        const double qv = Qc[v * nO + base + m];
+                        g[v] = fma(dm, ja * qv, g[v]);
+                        g[NV + v] = fma(dm, jb * qv, g[NV + v]);
+                    }
+                }
+            }
+            {  // eta: Ja^2 = (c, e, 0)
+                const int base = t - j * o1;
+                const double* Dr = Ds[1] + j * o2;
+                for (int m = 0; m < o2; ++m) {
+                    const double dm = Dr[m];
+                    const int col = i + o1 * m;
+                    const double jc = Mc[2 * nc + col], je = Mc[3 * nc + col];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        const double qv = Qc[v * nO + base + m * o1];
+                        g[v] = fma(dm, jc * qv, g[v]);
+                        g[NV + v] = fma(dm, je * qv, g[NV + v]);
+                    }
+                }
+            }
+            {  // zeta: Ja^3 = (0, 0, f), f constant along the column
+                const int base = t - k * nc;
+                const double* Dr = Ds[2] + k * o3;
+                const double jf = Mc[4 * nc + i + o1 * j];
+                for (int m = 0; m < o3; ++m) {
+                    const double dm = Dr[m];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) g[2 * NV + v] = fma(dm, jf * Qc[v * nO + base + m * nc], g[2 * NV + v]);
+                }
+            }
+            const double iJ = 1.0 / Mc[5 * nc + i + o1 * j];
+#pragma unroll
+            for (int cc = 0; cc < 15; ++cc) GA[cc * nO + t] = g[cc] * iJ;
+        }
+        __syncthreads();
+        // fluxes of the three directions from one viscous evaluation per node, in place of GA
+        for (int t = threadIdx.x; t < nO; t += BS) {
+            const int pk = IJK[t];
+            const int col = (pk & 255) + o1 * ((pk >> 8) & 255);
+            double qv[NV], gv[15];
+            for (int v = 0; v < NV; ++v) qv[v] = Qc[v * nO + t];
+            for (int cc = 0; cc < 15; ++cc) gv[cc] = GA[cc * nO + t];
+            ViscNode V;
+            visc_node(qv, gv, P.ph, V);
+            for (int dd = 0; dd < 3; ++dd) {
+                const double ax = ext_ja(Mc, nc, col, dd, 0), ay = ext_ja(Mc, nc, col, dd, 1), az = ext_ja(Mc, nc, col, dd, 2);
+                double Fv[NV], fv[NV];
+                adv_dot(qv, ax, ay, az, P.ph.gm1, Fv);
+                visc_along(V, ax, ay, az, fv);
+                for (int v = 0; v < NV; ++v) GA[(dd * NV + v) * nO + t] = Fv[v] - fv[v];
+            }
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < nO; t += BS) {
+            const int pk = IJK[t];
+            const int ijk[3] = {pk & 255, (pk >> 8) & 255, pk >> 16};
+            for (int dd = 0; dd < 3; ++dd) {
+                const int od = dd == 0 ? o1 : (dd == 1 ? o2 : o3);
+                const int str = dd == 0 ? 1 : (dd == 1 ? o1 : nc);
+                const int a = ijk[dd];
+                dsum_comps<NV>(od, Ds[dd] + a * od, GA + dd * NV * nO + (t - a * str), nO, str,
+                               [&](int v, double sv) { A[v * nO + t] += sv; });
+            }
+        }
+        __syncthreads();
+    } else {
+        for (int dd = 0; dd < 3; ++dd) {
+            const int od = dd == 0 ? o1 : (dd == 1 ? o2 : o3);
+            const int str = dd == 0 ? 1 : (dd == 1 ? o1 : nc);
+            for (int t = threadIdx.x; t < nO; t += BS) {
+                const int pk = IJK[t];
+                const int col = (pk & 255) + o1 * ((pk >> 8) & 255);
+                double qv[NV], Fv[NV];
+                for (int v = 0; v < NV; ++v) qv[v] = Qc[v * nO + t];
+                adv_dot(qv, ext_ja(Mc, nc, col, dd, 0), ext_ja(Mc, nc, col, dd, 1), ext_ja(Mc, nc, col, dd, 2), P.ph.gm1, Fv);
+                for (int v = 0; v < NV; ++v) F[v * nO + t] = Fv[v];
+            }
+            __syncthreads();
+            for (int t = threadIdx.x; t < nO; t += BS) {
+                const int pk = IJK[t];
+                const int a = dd == 0 ? (pk & 255) : (dd == 1 ? ((pk >> 8) & 255) : (pk >> 16));
+                dsum_comps<NV>(od, Ds[dd] + a * od, F + (t - a * str), nO, str, [&](int v, double sv) { A[v * nO + t] += sv; });
+            }
+            __syncthreads();
+        }
+    }
+    double tmax = 0.0;
+    for (int t = threadIdx.x; t < nO; t += BS) {
+        const int pk = IJK[t];
+        const int i = pk & 255, j = (pk >> 8) & 255, k = pk >> 16;
+        const double J = Mc[5 * nc + i + o1 * j];
+        double scale = 1.0;
+        if (P.formulation == 1) scale = J * P.tab->w[o1 - 1][i] * P.tab->w[o2 - 1][j] * P.tab->w[o3 - 1][k];
+        for (int v = 0; v < NV; ++v) tmax = fmax(tmax, fabs(scale * (Rc[v * nO + t] + A[v * nO + t] / J)));
+    }
+    tmax = block_max(tmax, red);
+    if (threadIdx.x == 0) P.tau[(3 * (long long)e + d) * DG_TAU_STRIDE_DEV + p] = tmax;
+}
+
+// shared-memory doubles of a k_tau_ext level with nO coarse nodes (nc <= nO columns)
+__host__ __device__ inline size_t tau_ext_words(int nO, bool ns) { return (size_t)(ns ? 36 : 26) * nO + (nO + 1) / 2; }
+
 }  // namespace dgtau

@@ -139,7 +139,13 @@ def test_curved_rk_dt(dg, orc, name):
 @pytest.mark.parametrize("name", ["cfg4_small", "cfg5_subbox", "cfg4_full"])
 @pytest.mark.parametrize("ref", ["solver", "same"])
 @pytest.mark.parametrize("form", [0, 1])
-def test_curved_tau_parity(dg, orc, name, ref, form):
+@pytest.mark.parametrize("kernel", ["ext", "generic"])
+def test_curved_tau_parity(dg, orc, name, ref, form, kernel, monkeypatch):
+    """Isolated tau on the extruded O-grids: k_tau_ext (compact double-double
+    coarse metrics, the default on extruded meshes) and the generic 3-D
+    k_tau_curved (DGTAU_TAU_GENERIC=1)."""
+    if kernel == "generic":
+        monkeypatch.setenv("DGTAU_TAU_GENERIC", "1")
     mesh, orders, P, S, q, qd = setup(dg, orc, name)
     if ref == "solver":
         tg = S.tau_estimate(qd, S.rhs_eval(qd), formulation=form, reference=dg.REF_SOLVER).cpu().numpy()
@@ -158,6 +164,18 @@ def test_curved_tau_noniso_parity(dg, orc, name, form):
     mesh, orders, P, S, q, qd = setup(dg, orc, name)
     tg = S.tau_estimate(qd, S.rhs_eval(qd), formulation=form, reference=dg.REF_SOLVER, noniso=True).cpu().numpy()
     to = P.tau_estimate_noniso(orders, q, P.rhs(orders, q), form)
+    assert tau_rel(tg, to) < TAU_TOL
+
+
+@pytest.mark.parametrize("name", ["cfg4_small", "cfg5_subbox"])
+@pytest.mark.parametrize("kernel", ["ext", "generic"])
+def test_curved_tau_euler_parity(dg, orc, name, kernel, monkeypatch):
+    """Euler on the curved extruded meshes: both tau kernels' inviscid branch."""
+    if kernel == "generic":
+        monkeypatch.setenv("DGTAU_TAU_GENERIC", "1")
+    mesh, orders, P, S, q, qd = setup(dg, orc, name, physics="euler")
+    tg = S.tau_estimate(qd, S.rhs_eval(qd), reference=dg.REF_SOLVER).cpu().numpy()
+    to = P.tau_estimate(orders, q, P.rhs(orders, q))
     assert tau_rel(tg, to) < TAU_TOL
 
 

@@ -46,7 +46,7 @@ S.compute_dt(q, 0.5, dts[0])
 with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
     S.rk_steps(a.steps, q, qb, g, dts[0], dts[1], 0.5)
     if a.tau:
-        S.tau_estimate(q, reference=dg.REF_SOLVER)
+        S.tau_estimate(q, S.rhs_eval(q), reference=dg.REF_SOLVER)
     torch.cuda.synchronize()
 agg = collections.defaultdict(lambda: [0, 0.0])
 for ev in prof.events():

@@ -6,7 +6,13 @@ import oracle as orc
 orc.build()
 from test_gpu_curved import setup
 from test_gpu_parity import tau_rel
-for name in ("cfg4_small", "cfg5_subbox", "cfg4_full"):
+kernels = ("ext", "generic")
+names = sys.argv[1:] or ["cfg4_small", "cfg5_subbox", "cfg4_full"]
+for name, kern in [(n, k) for n in names for k in kernels]:
+    if kern == "generic":
+        os.environ["DGTAU_TAU_GENERIC"] = "1"
+    else:
+        os.environ.pop("DGTAU_TAU_GENERIC", None)
     for ref in ("solver", "same"):
         for form in (0, 1):
             mesh, orders, P, S, q, qd = setup(dg, orc, name)
@@ -16,4 +22,4 @@ for name in ("cfg4_small", "cfg5_subbox", "cfg4_full"):
             else:
                 tg = S.tau_estimate(qd, None, formulation=form, reference=dg.REF_SAME).cpu().numpy()
                 to = P.tau_estimate(orders, q, P.rhs(orders, q, orc.ISOLATED), form)
-            print(name, ref, form, "%.2e" % tau_rel(tg, to))
+            print(name, kern, ref, form, "%.2e" % tau_rel(tg, to))
