@@ -325,6 +325,14 @@ inline bool getenv_flag(const char* name)
     return g && g[0] == '1';
 }
 
+// pipeline depth of the NS element kernels (DGTAU_NS_NST=1..4 for A/B; default 2)
+inline int ns_stages()
+{
+    const char* g = getenv("DGTAU_NS_NST");
+    const int v = g ? atoi(g) : 2;
+    return v < 1 ? 1 : (v > NS_MAXST ? NS_MAXST : v);
+}
+
 // DG_PATH_AUTO on affine Euler meshes: layouts with more (N1,N2,N3) buckets
 // than this take the runtime-order kernels (profiles/r02_prof_adapt_n32.txt:
 // 343 buckets, 1.54 -> 1.15 ms per residual; uniform orders stay 2.2x faster
@@ -1392,6 +1400,22 @@ dg_status dg_node_coords(dg_ctx* ctx, double* X)
 // part: FACES_ALL, FACES_INTERIOR (no halo side: may run while the halo
 // traces are in flight), FACES_HALO (the rest)
 enum { FACES_ALL = 0, FACES_INTERIOR = 1, FACES_HALO = 2 };
+// CTAs of a face launch: one group per face, or (NS_FACE_PERSIST) the
+// resident CTAs, each group walking faces with a stride
+template <int W, int MODE>
+static int face_grid(dg_ctx* ctx, int nf)
+{
+    using C = FaceCfg<W, MODE>;
+    const int need = (nf + C::G - 1) / C::G;
+    if (!face_persist(MODE)) return need;
+    static int occ = 0;  // per instantiation, one device per process
+    if (occ == 0) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ns_face<W, MODE>, C::BS, C::smem);
+        if (occ < 1) occ = 1;
+    }
+    return std::min(need, occ * ctx->nsm);
+}
+
 template <int MODE>
 static void launch_ns_faces(dg_ctx* ctx, const NsFaceParams& base, cudaStream_t st, int part = FACES_ALL)
 {
@@ -1404,9 +1428,9 @@ static void launch_ns_faces(dg_ctx* ctx, const NsFaceParams& base, cudaStream_t 
         using C1 = FaceCfg<1, MODE>;
         using C2 = FaceCfg<2, MODE>;
         using C3 = FaceCfg<3, MODE>;
-        if (w == 1) k_ns_face<1, MODE><<<(nf + C1::G - 1) / C1::G, C1::BS, C1::smem, st>>>(P);
-        else if (w == 2) k_ns_face<2, MODE><<<(nf + C2::G - 1) / C2::G, C2::BS, C2::smem, st>>>(P);
-        else k_ns_face<3, MODE><<<(nf + C3::G - 1) / C3::G, C3::BS, C3::smem, st>>>(P);
+        if (w == 1) k_ns_face<1, MODE><<<face_grid<1, MODE>(ctx, nf), C1::BS, C1::smem, st>>>(P);
+        else if (w == 2) k_ns_face<2, MODE><<<face_grid<2, MODE>(ctx, nf), C2::BS, C2::smem, st>>>(P);
+        else k_ns_face<3, MODE><<<face_grid<3, MODE>(ctx, nf), C3::BS, C3::smem, st>>>(P);
         ctx->launches++;
     }
 }
@@ -1459,8 +1483,8 @@ static dg_status launch_ns_gradient(dg_ctx* ctx, int variant, const double* q, c
     for (const SizeClass& c : ctx->nscls) {
         P.ibase = c.base;
         const int sw = ctx->nscls_swH[&c - &ctx->nscls[0]];
-        int nst = 2;
-        if (sizeof(double) * 2 * (size_t)sw > (size_t)ctx->smem_limit) nst = 1;
+        int nst = ns_stages();
+        while (nst > 1 && sizeof(double) * nst * (size_t)sw > (size_t)ctx->smem_limit) --nst;
         const size_t sm = sizeof(double) * nst * (size_t)sw;
         if (sm > (size_t)ctx->smem_limit) return fail(ctx, DG_EINVAL, "k_ns_grad: element item exceeds shared memory");
         auto kern = ctx->extruded ? k_ns_grad<true> : k_ns_grad<false>;
@@ -1508,8 +1532,8 @@ static dg_status launch_residual_curved(dg_ctx* ctx, int variant, const double* 
         P.ibase = c.base;
         const int sw = ctx->nscls_swG[&c - &ctx->nscls[0]];
         const size_t fw = (size_t)15 * c.maxn;  // F work area
-        int nst = 2;
-        if (sizeof(double) * (2 * (size_t)sw + fw) > (size_t)ctx->smem_limit) nst = 1;
+        int nst = ns_stages();
+        while (nst > 1 && sizeof(double) * (nst * (size_t)sw + fw) > (size_t)ctx->smem_limit) --nst;
         const size_t sm = sizeof(double) * (nst * (size_t)sw + fw);
         if (sm > (size_t)ctx->smem_limit) return fail(ctx, DG_EINVAL, "k_ns_res: element item exceeds shared memory");
         auto kern = ctx->extruded ? (ns ? k_ns_res<true, true> : k_ns_res<true, false>)

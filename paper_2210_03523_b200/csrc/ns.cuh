@@ -442,6 +442,7 @@ __device__ __forceinline__ void split_nk(int nk, int r, int& kk, int& rest)
 // ===========================================================================
 constexpr int NS_PROD = 32;           // producer warp
 constexpr int NS_THREADS = NS_BS + NS_PROD;
+constexpr int NS_MAXST = 4;           // pipeline stages (host picks 1..NS_MAXST)
 
 __device__ __forceinline__ void mbar_arrive(unsigned long long* b)
 {
@@ -701,12 +702,12 @@ template <bool EXT>
 __global__ void __launch_bounds__(NS_THREADS, 2) k_ns_grad(NsElemParams P, int nitems, int NST, int SW, long long qlen)
 {
     extern __shared__ __align__(16) double sm[];
-    __shared__ NsStageMeta meta[2];
-    __shared__ __align__(8) unsigned long long full[2], empty[2];
+    __shared__ NsStageMeta meta[NS_MAXST];
+    __shared__ __align__(8) unsigned long long full[NS_MAXST], empty[NS_MAXST];
     __shared__ double Ds[3 * NP * NP];
     if (blockIdx.x >= nitems) return;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < NS_MAXST; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], NS_BS);
         }
@@ -762,12 +763,12 @@ __global__ void __launch_bounds__(NS_THREADS, 2) k_ns_res(NsElemParams P, int ni
                                                           long long qlen)
 {
     extern __shared__ __align__(16) double sm[];
-    __shared__ NsStageMeta meta[2];
-    __shared__ __align__(8) unsigned long long full[2], empty[2];
+    __shared__ NsStageMeta meta[NS_MAXST];
+    __shared__ __align__(8) unsigned long long full[NS_MAXST], empty[NS_MAXST];
     __shared__ double red[32];
     if (blockIdx.x >= nitems) return;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < NS_MAXST; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], NS_BS);
         }
@@ -1086,6 +1087,9 @@ __device__ __forceinline__ void side_to_mortar(const double* __restrict__ qsrc, 
 #ifndef NS_FACE_DIRECT_MAXW
 #define NS_FACE_DIRECT_MAXW 1
 #endif
+#ifndef NS_QHAT_DIRECT
+#define NS_QHAT_DIRECT 0
+#endif
 
 // A side needs at most one interpolation pass (s_a = m_a or s_b = m_b): the
 // pass-A thread (b, i) of side_to_mortar is then the owner of mortar point
@@ -1243,18 +1247,12 @@ __host__ __device__ constexpr int face_minb(int W, int MODE)
     return MODE == MODE_QHAT ? (W == 1 ? NS_QHAT_MINB1 : NS_QHAT_MINB2) : (W == 3 ? NS_FLUX_MINB3 : (W == 1 ? NS_FLUX_MINB1 : NS_FLUX_MINB2));
 }
 
+// one face of a group (X, Y: the group's buffers; every branch below is
+// uniform over the group, so the group barriers inside are safe)
 template <int W, int MODE>
-__global__ void __launch_bounds__(FaceCfg<W>::BS, face_minb(W, MODE)) k_ns_face(NsFaceParams P)
+__device__ __forceinline__ void ns_face_one(const NsFaceParams& P, const NsFace& F, double* X, double* Y, int l, int gid)
 {
-    using C = FaceCfg<W, MODE>;
-    constexpr int CAP = C::CAP;
-    extern __shared__ __align__(16) double fsm[];
-    const int gid = threadIdx.x / (32 * W), l = threadIdx.x - gid * 32 * W;
-    const int fi = P.fbase + blockIdx.x * C::G + gid;
-    if (fi >= P.fend) return;  // the whole group leaves (named barriers are per group)
-    double* X = fsm + gid * 2 * C::BUF;
-    double* Y = X + C::BUF;
-    const NsFace F = P.faces[fi];
+    constexpr int CAP = FaceCfg<W, MODE>::CAP;
     const int d = F.d;
     const bool hasL = F.offL >= 0, hasR = F.offR >= 0;
     const FSide SL = face_side(F.offL, F.ordL, d, true);
@@ -1272,7 +1270,7 @@ __global__ void __launch_bounds__(FaceCfg<W>::BS, face_minb(W, MODE)) k_ns_face(
     const int kind = F.kind;
     double qL[NV] = {0, 0, 0, 0, 0}, qR[NV] = {0, 0, 0, 0, 0};
     int nout;
-    constexpr bool DIRECT_OK = NS_FACE_DIRECT && MODE != MODE_QHAT && W <= NS_FACE_DIRECT_MAXW;
+    constexpr bool DIRECT_OK = NS_FACE_DIRECT && (MODE != MODE_QHAT || NS_QHAT_DIRECT) && W <= NS_FACE_DIRECT_MAXW;
     const bool direct = DIRECT_OK && (!hasL || one_pass(SL, ma, mb)) && (!hasR || one_pass(SR, ma, mb));
     if (MODE == MODE_QHAT) {
         if (direct) {
@@ -1393,6 +1391,58 @@ __global__ void __launch_bounds__(FaceCfg<W>::BS, face_minb(W, MODE)) k_ns_face(
     }
     if (hasL) mortar_to_side<W, DIRECT_OK>(X, nout, ma, mb, SL.sa, SL.sb, P.tab, Y, P.out + oL, l, gid);
     if (hasR) mortar_to_side<W, DIRECT_OK>(X, nout, ma, mb, SR.sa, SR.sb, P.tab, Y, P.out + oR, l, gid);
+}
+
+// measured on cfg5: pays for the qhat passes (1.68 -> 1.57 ms, W = 1), not for
+// the flux passes (their record slot costs spills at 168 registers)
+#ifndef NS_FACE_PERSIST
+#define NS_FACE_PERSIST 1
+#endif
+__host__ __device__ constexpr bool face_persist(int MODE) { return NS_FACE_PERSIST && MODE == MODE_QHAT; }
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src)
+{
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+
+// Persistent groups (grid = resident CTAs): each group walks faces fi, fi +
+// G gridDim.x, ...; the next face's 80-byte record is fetched by cp.async into
+// a double-buffered shared slot while the current face is processed (the
+// record load heads every face's dependency chain: orders -> offsets ->
+// trace gathers).
+template <int W, int MODE>
+__global__ void __launch_bounds__(FaceCfg<W>::BS, face_minb(W, MODE)) k_ns_face(NsFaceParams P)
+{
+    using C = FaceCfg<W, MODE>;
+    extern __shared__ __align__(16) double fsm[];
+    const int gid = threadIdx.x / (32 * W), l = threadIdx.x - gid * 32 * W;
+    int fi = P.fbase + blockIdx.x * C::G + gid;
+    if (fi >= P.fend) return;  // the whole group leaves (named barriers are per group)
+    double* X = fsm + gid * 2 * C::BUF;
+    double* Y = X + C::BUF;
+    if constexpr (face_persist(MODE)) {
+    static_assert(sizeof(NsFace) == 80, "NsFace record: 5 x 16 bytes");
+    __shared__ __align__(16) NsFace fq[C::G][2];
+    const int gstride = gridDim.x * C::G;
+    if (l < 5) cp_async16(reinterpret_cast<char*>(&fq[gid][0]) + 16 * l, reinterpret_cast<const char*>(P.faces + fi) + 16 * l);
+    asm volatile("cp.async.commit_group;\n" ::);
+    for (int it = 0; fi < P.fend; fi += gstride, ++it) {
+        const int nf = fi + gstride;
+        if (nf < P.fend && l < 5)
+            cp_async16(reinterpret_cast<char*>(&fq[gid][(it + 1) & 1]) + 16 * l,
+                       reinterpret_cast<const char*>(P.faces + nf) + 16 * l);
+        asm volatile("cp.async.commit_group;\n" ::);
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // this face's record landed
+        grp_sync<W>(gid);
+        const NsFace F = fq[gid][it & 1];
+        ns_face_one<W, MODE>(P, F, X, Y, l, gid);
+        grp_sync<W>(gid);  // X, Y and the record slot free for the next face
+    }
+    } else {
+        const NsFace F = P.faces[fi];
+        ns_face_one<W, MODE>(P, F, X, Y, l, gid);
+    }
 }
 
 // ---------------------------------------------------------------------------

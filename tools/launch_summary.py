@@ -4,8 +4,10 @@ import csv
 import sys
 
 rows = list(csv.reader(open(sys.argv[1])))
+LAST = int(sys.argv[2]) if len(sys.argv) > 2 else 0  # only the last LAST launches (one bench step)
 hdr = None
 tot = collections.OrderedDict()
+launches = []
 for r in rows:
     if "Kernel Name" in r and "Metric Value" in r:
         hdr = r
@@ -21,7 +23,8 @@ for r in rows:
         v /= 1e3
     elif unit in ("msecond", "ms"):
         v *= 1e3
-    k = d["Kernel Name"]
+    launches.append((d["Kernel Name"], v))
+for k, v in launches[-LAST:] if LAST else launches:
     c = tot.setdefault(k, [0, 0.0])
     c[0] += 1
     c[1] += v
