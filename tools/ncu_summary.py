@@ -43,7 +43,8 @@ def main(rep, out):
         res.append({
             "kernel": d.get("Kernel Name"),
             "grid": d.get("launch__grid_size"), "block": d.get("launch__block_size"),
-            "duration_us": dur / 1e3 if dur and u.get("gpu__time_duration.sum") == "nsecond" else dur,
+            "duration_us": (dur * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}.get(
+                u.get("gpu__time_duration.sum"), 1.0)) if dur else dur,
             "dram_read_bytes": scaled_bytes("dram__bytes_read.sum"),
             "dram_write_bytes": scaled_bytes("dram__bytes_write.sum"),
             "registers": num("launch__registers_per_thread"),
