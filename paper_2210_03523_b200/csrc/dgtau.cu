@@ -514,7 +514,7 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
     cudaFuncSetAttribute(k_ns_face<W, MODE_QHAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,                          \
                          (int)FaceCfg<W, MODE_QHAT>::smem);                                                             \
     cudaFuncSetAttribute(k_ns_face<W, MODE_FLUX_EULER>, cudaFuncAttributeMaxDynamicSharedMemorySize,                    \
-                         (int)FaceCfg<W>::smem);                                                                        \
+                         (int)FaceCfg<W, MODE_FLUX_EULER>::smem);                                                       \
     cudaFuncSetAttribute(k_ns_face<W, MODE_FLUX_NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FaceCfg<W>::smem);
         NSF_ATTR(1)
         NSF_ATTR(2)

@@ -975,13 +975,14 @@ __device__ __forceinline__ void grp_sync(int gid)
 }
 
 // groups per CTA and buffer sizes: a buffer holds 20 component slots of CAP
-// points (flux passes: q and the gradient), 15 in the qhat pass (5 nk outputs)
+// points (NS flux passes: q and the gradient), 15 in the qhat pass (5 nk
+// outputs), 5 in the Euler flux pass
 template <int W, int MODE = MODE_FLUX_NS>
 struct FaceCfg {
     static constexpr int G = W == 1 ? 4 : 2;      // groups per CTA
     static constexpr int BS = G * 32 * W;
     static constexpr int CAP = 32 * W;
-    static constexpr int BUF = (MODE == MODE_QHAT ? 15 : 20) * CAP;
+    static constexpr int BUF = (MODE == MODE_QHAT ? 15 : (MODE == MODE_FLUX_EULER ? NV : 20)) * CAP;
     static constexpr size_t smem = sizeof(double) * (size_t)G * 2 * BUF;
 };
 
@@ -990,20 +991,21 @@ struct FSide {
     int n, sa, sb, base, sta, stb;
 };
 
+// (selects on the runtime direction d instead of small arrays indexed by it:
+// no local memory in the persistent face loops; measured faster in every pass,
+// cfg5 qhat W = 1 1.57 -> 1.45 ms)
 __device__ __forceinline__ FSide face_side(long long off, int ord, int d, bool isL)
 {
-    int N[3];
-    mt_unpack(ord, N);
-    const int ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
-    const int st[3] = {1, N[0] + 1, (N[0] + 1) * (N[1] + 1)};
+    const int N0 = ord & 15, N1 = (ord >> 4) & 15, N2 = (ord >> 8) & 15;  // mt_unpack's packing
+    const int st1 = N0 + 1, st2 = (N0 + 1) * (N1 + 1);
     FSide s;
     s.off = off;
-    s.n = st[2] * (N[2] + 1);
-    s.sa = N[ta] + 1;
-    s.sb = N[tb] + 1;
-    s.base = isL ? N[d] * st[d] : 0;
-    s.sta = st[ta];
-    s.stb = st[tb];
+    s.n = st2 * (N2 + 1);
+    s.sa = (d == 0 ? N1 : N0) + 1;  // ta = 1 for d = 0, else 0
+    s.sb = (d == 2 ? N1 : N2) + 1;  // tb = 1 for d = 2, else 2
+    s.base = isL ? (d == 0 ? N0 : (d == 1 ? N1 * st1 : N2 * st2)) : 0;
+    s.sta = d == 0 ? st1 : 1;
+    s.stb = d == 2 ? st1 : st2;
     return s;
 }
 
@@ -1242,9 +1244,20 @@ __device__ __forceinline__ void mortar_to_side(const double* Fm, int nc, int ma,
 #ifndef NS_QHAT_MINB2
 #define NS_QHAT_MINB2 4
 #endif
+#ifndef NS_EULER_MINB1
+#define NS_EULER_MINB1 4
+#endif
+#ifndef NS_EULER_MINB3
+#define NS_EULER_MINB3 2
+#endif
+#ifndef NS_EULER_MINB2
+#define NS_EULER_MINB2 4
+#endif
 __host__ __device__ constexpr int face_minb(int W, int MODE)
 {
-    return MODE == MODE_QHAT ? (W == 1 ? NS_QHAT_MINB1 : NS_QHAT_MINB2) : (W == 3 ? NS_FLUX_MINB3 : (W == 1 ? NS_FLUX_MINB1 : NS_FLUX_MINB2));
+    return MODE == MODE_QHAT ? (W == 1 ? NS_QHAT_MINB1 : NS_QHAT_MINB2)
+         : MODE == MODE_FLUX_EULER ? (W == 1 ? NS_EULER_MINB1 : (W == 2 ? NS_EULER_MINB2 : NS_EULER_MINB3))
+                                   : (W == 3 ? NS_FLUX_MINB3 : (W == 1 ? NS_FLUX_MINB1 : NS_FLUX_MINB2));
 }
 
 // one face of a group (X, Y: the group's buffers; every branch below is
@@ -1319,6 +1332,7 @@ __device__ __forceinline__ void ns_face_one(const NsFaceParams& P, const NsFace&
             if (hasR) side_gather<W, NCI>(P.q + SR.off, MODE == MODE_FLUX_NS ? P.grad + 3 * SR.off : nullptr, SR, Y, l);
             grp_sync<W>(gid);
         }
+#pragma unroll 1  // measured: the unrolled two-side loop slows the W = 1 NS flux pass (3.74 -> 4.30 ms)
         for (int side = 0; side < 2; ++side) {
             const bool has = side ? hasR : hasL;
             if (!has) continue;
@@ -1394,11 +1408,15 @@ __device__ __forceinline__ void ns_face_one(const NsFaceParams& P, const NsFace&
 }
 
 // measured on cfg5: pays for the qhat passes (1.68 -> 1.57 ms, W = 1), not for
-// the flux passes (their record slot costs spills at 168 registers)
+// the NS flux passes (their record slot costs spills at 168 registers); the
+// Euler flux passes (few registers) take it too
 #ifndef NS_FACE_PERSIST
 #define NS_FACE_PERSIST 1
 #endif
-__host__ __device__ constexpr bool face_persist(int MODE) { return NS_FACE_PERSIST && MODE == MODE_QHAT; }
+#ifndef NS_FACE_PERSIST_NS
+#define NS_FACE_PERSIST_NS 0
+#endif
+__host__ __device__ constexpr bool face_persist(int MODE) { return NS_FACE_PERSIST && (MODE != MODE_FLUX_NS || NS_FACE_PERSIST_NS); }
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src)
 {

@@ -18,12 +18,13 @@ ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--save", default=None)
 ap.add_argument("--cfg", default="cfg5")
 ap.add_argument("--tau", action="store_true")
+ap.add_argument("--euler", action="store_true", help="Euler (cfg2 / cfg3 are Euler configurations)")
 a = ap.parse_args()
 spec = W.CONFIGS[a.cfg]
 mesh = W.make_mesh(spec["mesh"])
 orders = W.make_orders(spec["orders"], mesh.E)
 nsp = W.ns_params()
-S = dg.Solver(mesh, physics=dg.NS, mu=nsp["mu"], Pr=nsp["Pr"], qinf=nsp["qinf"])
+S = (dg.Solver(mesh) if a.euler else dg.Solver(mesh, physics=dg.NS, mu=nsp["mu"], Pr=nsp["Pr"], qinf=nsp["qinf"]))
 S.set_orders(orders)
 q0 = torch.from_numpy(W.freestream_noise_state(orders, (1.0, 1.0, 0.0, 0.0, nsp["p_inf"]), noise=1e-3, seed=5)).cuda()
 q, qb, g = q0.clone(), torch.empty_like(q0), torch.empty_like(q0)
