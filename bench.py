@@ -418,6 +418,46 @@ class Cfg2Run:
         return qn, sel
 
 
+def run_e2e_cfg2(R, args, stream, ev):
+    """cfg2 end to end: the SAME adaptation intervals as the device-timed run
+    (its starting layout and state saved before the timed region), each step's
+    input state uploaded from pinned host memory and its result (state +
+    selected orders) read back; the result read back IS the next step's input
+    (the host is in the loop: upload, interval, download, serialised)."""
+    import torch
+
+    orders0, q0 = R.e2e_start
+    R.S.set_orders(orders0)
+    cap = R.buf[0].numel()
+    pin = [torch.zeros(cap, dtype=torch.float64).pin_memory() for _ in range(2)]
+    pin[0][: q0.size].copy_(torch.from_numpy(q0))
+    n_in = q0.size
+    dbuf = torch.zeros(cap, dtype=torch.float64, device=stream.device)
+    torch.cuda.synchronize()
+    e0, e1 = ev(), ev()
+    e0.record(stream)
+    h2d = d2h = dof_res = 0
+    for k in range(args.steps):
+        dbuf[:n_in].copy_(pin[k % 2][:n_in], non_blocking=True)
+        h2d += n_in * 8
+        R.S.compute_dt(dbuf[:n_in], CFL, R.dts[0])
+        dof_res += R.ndof_global * R.residuals_per_step
+        qn, sel = R.step(qin=dbuf[:n_in])
+        n_in = qn.numel()
+        pin[(k + 1) % 2][:n_in].copy_(qn, non_blocking=True)
+        sel_h = sel.cpu() if hasattr(sel, "cpu") else sel
+        d2h += n_in * 8 + np.asarray(sel_h).nbytes
+        stream.synchronize()  # the host holds the result before the next upload
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    return {"value": dof_res / (e2e_ms * 1e-3) / 1e9, "unit": "GDOF/s",
+            "h2d_bytes_per_step": int(h2d // args.steps), "d2h_bytes_per_step": int(d2h // args.steps),
+            "copies": "the device-timed run's intervals again from its saved starting layout and state: each "
+                      "interval's input uploaded from pinned host memory, its result state and orders read back "
+                      "and uploaded as the next input (host in the loop, serialised)"}
+
+
 # ----------------------------------------------------------------------------
 # GPU arm
 # ----------------------------------------------------------------------------
@@ -437,6 +477,8 @@ def run_gpu(args, rank, world):
         R.step()
     torch.cuda.synchronize()
     timers = {"rk": [], "tau": [], "adapt": []}
+    if isinstance(R, Cfg2Run):  # the e2e leg re-runs the SAME intervals from here (layout + state)
+        R.e2e_start = (np.array(R.S.orders, copy=True), R._q(0).cpu().numpy().copy())
     launches0 = R.core.launches
     clocks = ClockSampler(dev.index)
     if rank == 0:
@@ -488,18 +530,13 @@ def run_e2e(R, args, stream, ev, world):
     dist = None
     if world > 1:
         import torch.distributed as dist
+    if isinstance(R, Cfg2Run):
+        return run_e2e_cfg2(R, args, stream, ev)
     owned = R.owned_len
     pinned = torch.from_numpy(np.ascontiguousarray(R.q0_host[:owned])).pin_memory()
     total_len = R.qa.numel() if hasattr(R, "qa") else R.buf[0].numel()
     out_pinned = [torch.empty(total_len, dtype=torch.float64).pin_memory() for _ in range(2)]
     bufs = [torch.zeros(total_len, dtype=torch.float64, device=stream.device) for _ in range(2)]
-    if isinstance(R, Cfg2Run):
-        R.S.set_orders(R.orders)  # the IC layout (the timed run left an adapted one)
-        bufs = [torch.zeros(max(R.S.state_len, R.buf[0].numel()), dtype=torch.float64, device=stream.device)
-                for _ in range(2)]
-        pinned = torch.from_numpy(R.q0_host).pin_memory()
-        owned = R.q0_host.size
-        R.S.compute_dt(R.buf[R.cur][: R.S.state_len], CFL, R.dts[0])
     cs = torch.cuda.Stream()
     ev_in = [torch.cuda.Event() for _ in range(args.steps + 1)]
     ev_step = [torch.cuda.Event() for _ in range(args.steps)]
@@ -516,8 +553,6 @@ def run_e2e(R, args, stream, ev, world):
     d2h = 0
     dof_res = 0
     for k in range(args.steps):
-        if isinstance(R, Cfg2Run):  # each interval restarts from the uploaded IC at N=6 (same work as the GPU arm's first step)
-            R.S.set_orders(R.orders)
         if k + 1 < args.steps:  # input of step k+1 while step k runs
             if k >= 1:
                 cs.wait_event(ev_step[k - 1])
@@ -528,10 +563,7 @@ def run_e2e(R, args, stream, ev, world):
         if k >= 2:
             stream.wait_event(ev_out[k - 2])
         dof_res += R.ndof_global * R.residuals_per_step
-        if isinstance(R, Cfg2Run):
-            R.S.compute_dt(bufs[k % 2], CFL, R.dts[0])
-        else:
-            R.dts[0].copy_(R.dt0)
+        R.dts[0].copy_(R.dt0)
         qn, sel = R.step(qin=bufs[k % 2])
         ev_step[k].record(stream)
         cs.wait_event(ev_step[k])
