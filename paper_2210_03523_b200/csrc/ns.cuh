@@ -1482,8 +1482,17 @@ __device__ __forceinline__ double ext_ja(const double* Mc, int nc, int col, int 
     return Mc[(2 * d + k) * nc + col];
 }
 
+#ifndef TAU_EXT_MINB64
+#define TAU_EXT_MINB64 14
+#endif
+#ifndef TAU_EXT_MINB128
+#define TAU_EXT_MINB128 7
+#endif
+#ifndef TAU_EXT_MINB256
+#define TAU_EXT_MINB256 3
+#endif
 template <int BS>
-__global__ void __launch_bounds__(BS, BS == 256 ? 2 : (BS == 128 ? 5 : 10)) k_tau_ext(CTauParams P)
+__global__ void __launch_bounds__(BS, BS == 256 ? TAU_EXT_MINB256 : (BS == 128 ? TAU_EXT_MINB128 : TAU_EXT_MINB64)) k_tau_ext(CTauParams P)
 {
     extern __shared__ double sm[];
     __shared__ double red[32];
