@@ -974,12 +974,15 @@ __device__ __forceinline__ void grp_sync(int gid)
     }
 }
 
+// groups per CTA (measured on cfg5: W = 1 4 groups; W = 2, 3 NS flux one
+// group per CTA, 2.77 -> 2.56 and 1.25 -> 1.13 ms; qhat 2 groups)
+__host__ __device__ constexpr int face_groups(int W, int MODE) { return W == 1 ? 4 : (MODE == MODE_FLUX_NS ? 1 : 2); }
 // groups per CTA and buffer sizes: a buffer holds 20 component slots of CAP
 // points (NS flux passes: q and the gradient), 15 in the qhat pass (5 nk
 // outputs), 5 in the Euler flux pass
 template <int W, int MODE = MODE_FLUX_NS>
 struct FaceCfg {
-    static constexpr int G = W == 1 ? 4 : 2;      // groups per CTA
+    static constexpr int G = face_groups(W, MODE);  // groups per CTA
     static constexpr int BS = G * 32 * W;
     static constexpr int CAP = 32 * W;
     static constexpr int BUF = (MODE == MODE_QHAT ? 15 : (MODE == MODE_FLUX_EULER ? NV : 20)) * CAP;
@@ -1253,11 +1256,17 @@ __device__ __forceinline__ void mortar_to_side(const double* Fm, int nc, int ma,
 #ifndef NS_EULER_MINB2
 #define NS_EULER_MINB2 4
 #endif
-__host__ __device__ constexpr int face_minb(int W, int MODE)
+// (the budgets are per 4 groups for W = 1 and 2 groups for W = 2, 3: the same
+// threads per SM whatever the groups per CTA)
+__host__ __device__ constexpr int face_minb_base(int W, int MODE)
 {
     return MODE == MODE_QHAT ? (W == 1 ? NS_QHAT_MINB1 : NS_QHAT_MINB2)
          : MODE == MODE_FLUX_EULER ? (W == 1 ? NS_EULER_MINB1 : (W == 2 ? NS_EULER_MINB2 : NS_EULER_MINB3))
                                    : (W == 3 ? NS_FLUX_MINB3 : (W == 1 ? NS_FLUX_MINB1 : NS_FLUX_MINB2));
+}
+__host__ __device__ constexpr int face_minb(int W, int MODE)
+{
+    return face_minb_base(W, MODE) * (W == 1 ? 4 : 2) / face_groups(W, MODE);
 }
 
 // one face of a group (X, Y: the group's buffers; every branch below is
@@ -1430,7 +1439,7 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src)
 // record load heads every face's dependency chain: orders -> offsets ->
 // trace gathers).
 template <int W, int MODE>
-__global__ void __launch_bounds__(FaceCfg<W>::BS, face_minb(W, MODE)) k_ns_face(NsFaceParams P)
+__global__ void __launch_bounds__(FaceCfg<W, MODE>::BS, face_minb(W, MODE)) k_ns_face(NsFaceParams P)
 {
     using C = FaceCfg<W, MODE>;
     extern __shared__ __align__(16) double fsm[];
