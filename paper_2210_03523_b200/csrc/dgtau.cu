@@ -132,6 +132,8 @@ struct dg_ctx {
     FaceInfo* d_finfo = nullptr;
     SlotInfo* d_slots = nullptr;
     TauLevel* d_levels = nullptr;
+    TauLevel* d_tgrp = nullptr;  // extruded meshes: level groups of one element (k_tau_grp)
+    int ntgrp = 0, tgrp_cap = 0;
     // curved kernels run one CTA per element (level): elements sorted by node
     // count into size classes, each launched with its own dynamic shared memory
     int* d_eperm = nullptr;
@@ -499,6 +501,7 @@ dg_status dg_create(const dg_params* params, dg_ctx** out)
         cudaFuncSetAttribute(k_tau_curved<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
         cudaFuncSetAttribute(k_tau_curved<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
         cudaFuncSetAttribute(k_tau_ext<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
+        cudaFuncSetAttribute(k_tau_grp, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
         cudaFuncSetAttribute(k_tau_ext<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
         cudaFuncSetAttribute(k_tau_ext<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, limc);
         ctx->smem_limit = limc;
@@ -612,6 +615,7 @@ void dg_destroy(dg_ctx* ctx)
     dfree(ctx->d_fcta);
     dfree(ctx->d_slots);
     dfree(ctx->d_levels);
+    dfree(ctx->d_tgrp);
     dfree(ctx->d_eperm);
     dfree(ctx->d_tgroups);
     dfree(ctx->d_ref_scratch);
@@ -1298,6 +1302,37 @@ dg_status dg_set_orders(dg_ctx* ctx, const int32_t* orders_host)
         lv.swap(ls);
     }
     CK(upload(ctx->d_levels, lv));
+    // extruded meshes: consecutive (d, p) levels of an element, d-major, in
+    // groups of <= cap coarse nodes (k_tau_grp: one CTA per group)
+    {
+        std::vector<TauLevel> gr;
+        ctx->tgrp_cap = std::max(256, ctx->max_level);
+        if (ctx->tau_curved && ctx->extruded) {
+            for (int e = 0; e < ctx->n_own; ++e) {
+                const int* No = &ctx->orders[3 * e];
+                TauLevel cur{e, -1, 0, 0};
+                int sum = 0;
+                for (int d = 0; d < 3; ++d)
+                    for (int p = 1; p < No[d]; ++p) {
+                        const int nO = npts(No) / (No[d] + 1) * (p + 1);
+                        if (cur.pad > 0 && (sum + nO > ctx->tgrp_cap || cur.pad == TAU_GRP_MAXLV)) {
+                            gr.push_back(cur);
+                            cur.pad = 0;
+                            sum = 0;
+                        }
+                        if (cur.pad == 0) {
+                            cur.d = d;
+                            cur.p = p;
+                        }
+                        cur.pad++;
+                        sum += nO;
+                    }
+                if (cur.pad > 0) gr.push_back(cur);
+            }
+        }
+        ctx->ntgrp = (int)gr.size();
+        CK(upload(ctx->d_tgrp, gr));
+    }
     tm.mark("tau levels");
     ctx->ecls_own.clear();
     ctx->ecls_all.clear();
@@ -2270,6 +2305,13 @@ dg_status dg_tau_estimate(dg_ctx* ctx, const dg_tau_opts* o, const double* q_dev
             // extruded meshes: compact double-double coarse metrics (k_tau_ext);
             // DGTAU_TAU_GENERIC=1 keeps the generic 3-D kernel (tests run both)
             const bool ext = ctx->extruded && !getenv_flag("DGTAU_TAU_GENERIC");
+            const size_t gsm = tau_grp_bytes(ctx->tgrp_cap);
+            if (ext && ctx->ntgrp > 0 && !getenv_flag("DGTAU_TAU_PERLEVEL") && (long long)gsm <= ctx->smem_limit) {
+                C.levels = ctx->d_tgrp;
+                C.lbase = 0;
+                k_tau_grp<<<ctx->ntgrp, TAU_GRP_BS, gsm, st>>>(C, ctx->tgrp_cap);
+                ctx->launches++;
+            } else
             for (const SizeClass& c : ctx->lcls) {
                 C.lbase = c.base;
                 if (ext) {

@@ -1721,4 +1721,297 @@ __global__ void __launch_bounds__(BS, BS == 256 ? TAU_EXT_MINB256 : (BS == 128 ?
 // shared-memory doubles of a k_tau_ext level with nO coarse nodes (nc <= nO columns)
 __host__ __device__ inline size_t tau_ext_words(int nO, bool ns) { return (size_t)(ns ? 36 : 26) * nO + (nO + 1) / 2; }
 
+// ---------------------------------------------------------------------------
+// k_tau_grp: the k_tau_ext levels of ONE element batched in a CTA (groups of
+// consecutive (d, p) levels, d-major, whose coarse nodes sum to <= cap): each
+// phase (coarse metrics, interpolation, BR1 gradient, fluxes, divergence,
+// level maxima) runs over the nodes of all the group's levels between two
+// barriers, instead of one CTA and ~7 barriers per level.  The same
+// operations per node and level as k_tau_ext (agreement to a few ulp: the
+// compiler's fma contraction differs between the kernels).  cfg5: 50.8 ms per
+// estimate against 53.3 (the estimate is fp64-bound: ~20 % of the DFMA peak).
+// Group record: TauLevel{e, d0, p0, count} (levels (d0, p0), (d0, p0 + 1), ...
+// continuing with p = 1 of the next direction with N_d >= 2).
+// ---------------------------------------------------------------------------
+constexpr int TAU_GRP_BS = 256;
+constexpr int TAU_GRP_MAXLV = 24;
+struct TauLvDesc {
+    int d, p, o1, o2, o3, nO, nc, nb, cb;  // nb / cb: node / column base in the group
+};
+// shared-memory bytes of a group kernel with node capacity cap
+__host__ __device__ inline size_t tau_grp_bytes(int cap) { return sizeof(double) * 36 * (size_t)cap + 4 * (size_t)cap + 2 * (size_t)cap + 16; }
+
+__global__ void __launch_bounds__(TAU_GRP_BS, 3) k_tau_grp(CTauParams P, int cap)
+{
+    extern __shared__ __align__(16) double sm[];
+    __shared__ TauLvDesc L[TAU_GRP_MAXLV];
+    __shared__ unsigned long long lmax[TAU_GRP_MAXLV];
+    __shared__ int nlev_s, nOt_s, nct_s;
+    const TauLevel G = P.levels[P.lbase + blockIdx.x];
+    const int e = G.e;
+    const int n1 = P.orders[3 * e] + 1, n2 = P.orders[3 * e + 1] + 1, n3 = P.orders[3 * e + 2] + 1;
+    const int n = n1 * n2 * n3;
+    const bool ns = P.ph.physics == 1;
+    double* Mc = sm;                 // 6 cap
+    double* Qc = Mc + 6 * cap;       // 5 cap
+    double* Rc = Qc + 5 * cap;       // 5 cap
+    double* GA = Rc + 5 * cap;       // 15 cap (coordinates scratch first)
+    double* A = GA + 15 * cap;       // 5 cap
+    int* IJK = reinterpret_cast<int*>(A + 5 * cap);      // cap
+    unsigned char* LV = reinterpret_cast<unsigned char*>(IJK + cap);  // cap: level of a node
+    unsigned char* LC = LV + cap;                        // cap: level of a column
+    if (threadIdx.x == 0) {
+        const int nn[3] = {n1, n2, n3};
+        int d = G.d, p = G.p, nb = 0, cb = 0;
+        for (int l = 0; l < G.pad; ++l) {
+            TauLvDesc D;
+            D.d = d;
+            D.p = p;
+            D.o1 = d == 0 ? p + 1 : n1;
+            D.o2 = d == 1 ? p + 1 : n2;
+            D.o3 = d == 2 ? p + 1 : n3;
+            D.nc = D.o1 * D.o2;
+            D.nO = D.nc * D.o3;
+            D.nb = nb;
+            D.cb = cb;
+            nb += D.nO;
+            cb += D.nc;
+            L[l] = D;
+            lmax[l] = 0ull;
+            if (++p >= nn[d] - 1) {  // levels p = 1 .. N_d - 1 (N_d = nn[d] - 1)
+                p = 1;
+                do { ++d; } while (d < 3 && nn[d] < 3);
+            }
+        }
+        nlev_s = G.pad;
+        nOt_s = nb;
+        nct_s = cb;
+    }
+    __syncthreads();
+    const int nlev = nlev_s, nOt = nOt_s, nct = nct_s;
+    for (int g = threadIdx.x; g < nOt; g += TAU_GRP_BS) {
+        int l = 0;
+        while (l + 1 < nlev && g >= L[l + 1].nb) ++l;
+        const int t = g - L[l].nb;
+        int ii, jj, kk;
+        node_ijk(t, L[l].o1, L[l].o2, ii, jj, kk);
+        IJK[g] = ii | (jj << 8) | (kk << 16);
+        LV[g] = (unsigned char)l;
+    }
+    for (int c = threadIdx.x; c < nct; c += TAU_GRP_BS) {
+        int l = 0;
+        while (l + 1 < nlev && c >= L[l + 1].cb) ++l;
+        LC[c] = (unsigned char)l;
+    }
+    const int g1 = P.cm.g1, g2 = P.cm.g2, ga = g1 + 1, gb = g2 + 1;
+    const double* Gg = P.cm.geo + (long long)e * 3 * P.cm.ng;
+    const double x0 = __ldg(Gg), y0 = __ldg(Gg + P.cm.ng);
+    __syncthreads();
+    // coarse metrics, phase 1: x, y (relative to the first geometry node) at the columns
+    for (int cg = threadIdx.x; cg < nct; cg += TAU_GRP_BS) {
+        const TauLvDesc& D = L[LC[cg]];
+        const int t = cg - D.cb, o1 = D.o1, o2 = D.o2, nc = D.nc;
+        const int i = t % o1, j = t / o1;
+        const double* T1 = P.tab->T[g1][o1 - 1];
+        const double* T2 = P.tab->T[g2][o2 - 1];
+        double x = 0.0, y = 0.0;
+        for (int b = 0; b <= g2; ++b) {
+            const double w2 = T2[j * gb + b];
+            for (int a = 0; a <= g1; ++a) {
+                const double w = w2 * T1[i * ga + a];
+                x = fma(w, __ldg(Gg + a + ga * b) - x0, x);
+                y = fma(w, __ldg(Gg + P.cm.ng + a + ga * b) - y0, y);
+            }
+        }
+        double* Xs = GA + 15 * D.nb;
+        Xs[t] = x;
+        Xs[nc + t] = y;
+    }
+    __syncthreads();
+    {
+        const double zz = 0.5 * (__ldg(Gg + 2 * P.cm.ng + ga * gb) - __ldg(Gg + 2 * P.cm.ng));
+        for (int cg = threadIdx.x; cg < nct; cg += TAU_GRP_BS) {
+            const TauLvDesc& D = L[LC[cg]];
+            const int t = cg - D.cb, o1 = D.o1, o2 = D.o2, nc = D.nc;
+            const int i = t % o1, j = t / o1;
+            const double* Xs = GA + 15 * D.nb;
+            const double* D1 = P.tab->D[o1 - 1];
+            const double* D2 = P.tab->D[o2 - 1];
+            double xx = 0.0, yx = 0.0, xe = 0.0, ye = 0.0;
+            for (int m = 0; m < o1; ++m) {
+                const double dm = D1[i * o1 + m];
+                xx = fma(dm, Xs[m + o1 * j], xx);
+                yx = fma(dm, Xs[nc + m + o1 * j], yx);
+            }
+            for (int m = 0; m < o2; ++m) {
+                const double dm = D2[j * o2 + m];
+                xe = fma(dm, Xs[i + o1 * m], xe);
+                ye = fma(dm, Xs[nc + i + o1 * m], ye);
+            }
+            const double j3 = xx * ye - xe * yx;
+            double* M = Mc + 6 * D.cb;
+            M[t] = zz * ye;
+            M[nc + t] = -(zz * xe);
+            M[2 * nc + t] = -(zz * yx);
+            M[3 * nc + t] = zz * xx;
+            M[4 * nc + t] = j3;
+            M[5 * nc + t] = zz * j3;
+        }
+    }
+    __syncthreads();  // Xs (= GA) free, metrics ready
+    const long long o = P.off[e];
+    for (int g = threadIdx.x; g < nOt; g += TAU_GRP_BS) {
+        const TauLvDesc& D = L[LV[g]];
+        const int t = g - D.nb, nO = D.nO, d = D.d;
+        const int nd = d == 0 ? n1 : (d == 1 ? n2 : n3);
+        const int stride = d == 0 ? 1 : (d == 1 ? n1 : n1 * n2);
+        const double* T = P.restr ? P.tab->P[nd - 1][D.p] : P.tab->T[nd - 1][D.p];
+        const int pk = IJK[g];
+        int i = pk & 255, j = (pk >> 8) & 255, k = pk >> 16;
+        const int ic = d == 0 ? i : (d == 1 ? j : k);
+        if (d == 0) i = 0; else if (d == 1) j = 0; else k = 0;
+        const int base = i + n1 * (j + n2 * k);
+        const double* qe = P.q + o;
+        const double* re = P.qref + o;
+        double* Qd = Qc + 5 * D.nb;
+        double* Rd = Rc + 5 * D.nb;
+        switch (nd) {
+            case 2: tau_interp_node<2>(T, ic, qe, re, n, base, stride, Qd, Rd, nO, t); break;
+            case 3: tau_interp_node<3>(T, ic, qe, re, n, base, stride, Qd, Rd, nO, t); break;
+            case 4: tau_interp_node<4>(T, ic, qe, re, n, base, stride, Qd, Rd, nO, t); break;
+            case 5: tau_interp_node<5>(T, ic, qe, re, n, base, stride, Qd, Rd, nO, t); break;
+            case 6: tau_interp_node<6>(T, ic, qe, re, n, base, stride, Qd, Rd, nO, t); break;
+            case 7: tau_interp_node<7>(T, ic, qe, re, n, base, stride, Qd, Rd, nO, t); break;
+            case 8: tau_interp_node<8>(T, ic, qe, re, n, base, stride, Qd, Rd, nO, t); break;
+            default: tau_interp_node<9>(T, ic, qe, re, n, base, stride, Qd, Rd, nO, t); break;
+        }
+        double* Ad = A + 5 * D.nb;
+        for (int v = 0; v < NV; ++v) Ad[v * nO + t] = 0.0;
+    }
+    __syncthreads();
+    if (ns) {  // isolated gradient (nonzero metric components), as k_tau_ext
+        for (int g = threadIdx.x; g < nOt; g += TAU_GRP_BS) {
+            const TauLvDesc& D = L[LV[g]];
+            const int t = g - D.nb, nO = D.nO, o1 = D.o1, o2 = D.o2, o3 = D.o3, nc = D.nc;
+            const double* Q = Qc + 5 * D.nb;
+            const double* M = Mc + 6 * D.cb;
+            const int pk = IJK[g];
+            const int i = pk & 255, j = (pk >> 8) & 255, k = pk >> 16;
+            double gr[15];
+#pragma unroll
+            for (int cc = 0; cc < 15; ++cc) gr[cc] = 0.0;
+            {
+                const int base = t - i;
+                const double* Dr = P.tab->D[o1 - 1] + i * o1;
+                for (int m = 0; m < o1; ++m) {
+                    const double dm = Dr[m];
+                    const int col = m + o1 * j;
+                    const double ja = M[col], jb = M[nc + col];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        const double qv = Q[v * nO + base + m];
+                        gr[v] = fma(dm, ja * qv, gr[v]);
+                        gr[NV + v] = fma(dm, jb * qv, gr[NV + v]);
+                    }
+                }
+            }
+            {
+                const int base = t - j * o1;
+                const double* Dr = P.tab->D[o2 - 1] + j * o2;
+                for (int m = 0; m < o2; ++m) {
+                    const double dm = Dr[m];
+                    const int col = i + o1 * m;
+                    const double jc = M[2 * nc + col], je = M[3 * nc + col];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        const double qv = Q[v * nO + base + m * o1];
+                        gr[v] = fma(dm, jc * qv, gr[v]);
+                        gr[NV + v] = fma(dm, je * qv, gr[NV + v]);
+                    }
+                }
+            }
+            {
+                const int base = t - k * nc;
+                const double* Dr = P.tab->D[o3 - 1] + k * o3;
+                const double jf = M[4 * nc + i + o1 * j];
+                for (int m = 0; m < o3; ++m) {
+                    const double dm = Dr[m];
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) gr[2 * NV + v] = fma(dm, jf * Q[v * nO + base + m * nc], gr[2 * NV + v]);
+                }
+            }
+            const double iJ = 1.0 / M[5 * nc + i + o1 * j];
+            double* GAd = GA + 15 * D.nb;
+#pragma unroll
+            for (int cc = 0; cc < 15; ++cc) GAd[cc * nO + t] = gr[cc] * iJ;
+        }
+        __syncthreads();
+    }
+    // contravariant fluxes of the three directions (NS: one viscous evaluation per node), in place of GA
+    for (int g = threadIdx.x; g < nOt; g += TAU_GRP_BS) {
+        const TauLvDesc& D = L[LV[g]];
+        const int t = g - D.nb, nO = D.nO, nc = D.nc;
+        const double* Q = Qc + 5 * D.nb;
+        const double* M = Mc + 6 * D.cb;
+        double* GAd = GA + 15 * D.nb;
+        const int pk = IJK[g];
+        const int col = (pk & 255) + D.o1 * ((pk >> 8) & 255);
+        double qv[NV];
+        for (int v = 0; v < NV; ++v) qv[v] = Q[v * nO + t];
+        ViscNode V;
+        if (ns) {
+            double gv[15];
+            for (int cc = 0; cc < 15; ++cc) gv[cc] = GAd[cc * nO + t];
+            visc_node(qv, gv, P.ph, V);
+        }
+        for (int dd = 0; dd < 3; ++dd) {
+            const double ax = ext_ja(M, nc, col, dd, 0), ay = ext_ja(M, nc, col, dd, 1), az = ext_ja(M, nc, col, dd, 2);
+            double Fv[NV];
+            adv_dot(qv, ax, ay, az, P.ph.gm1, Fv);
+            if (ns) {
+                double fv[NV];
+                visc_along(V, ax, ay, az, fv);
+                for (int v = 0; v < NV; ++v) Fv[v] -= fv[v];
+            }
+            for (int v = 0; v < NV; ++v) GAd[(dd * NV + v) * nO + t] = Fv[v];
+        }
+    }
+    __syncthreads();
+    for (int g = threadIdx.x; g < nOt; g += TAU_GRP_BS) {
+        const TauLvDesc& D = L[LV[g]];
+        const int t = g - D.nb, nO = D.nO;
+        const double* GAd = GA + 15 * D.nb;
+        double* Ad = A + 5 * D.nb;
+        const int pk = IJK[g];
+        const int ijk[3] = {pk & 255, (pk >> 8) & 255, pk >> 16};
+        for (int dd = 0; dd < 3; ++dd) {
+            const int od = dd == 0 ? D.o1 : (dd == 1 ? D.o2 : D.o3);
+            const int str = dd == 0 ? 1 : (dd == 1 ? D.o1 : D.nc);
+            const int a = ijk[dd];
+            dsum_comps<NV>(od, P.tab->D[od - 1] + a * od, GAd + dd * NV * nO + (t - a * str), nO, str,
+                           [&](int v, double sv) { Ad[v * nO + t] += sv; });
+        }
+    }
+    __syncthreads();
+    for (int g = threadIdx.x; g < nOt; g += TAU_GRP_BS) {
+        const int l = LV[g];
+        const TauLvDesc& D = L[l];
+        const int t = g - D.nb, nO = D.nO;
+        const int pk = IJK[g];
+        const int i = pk & 255, j = (pk >> 8) & 255, k = pk >> 16;
+        const double J = Mc[6 * D.cb + 5 * D.nc + i + D.o1 * j];
+        double scale = 1.0;
+        if (P.formulation == 1) scale = J * P.tab->w[D.o1 - 1][i] * P.tab->w[D.o2 - 1][j] * P.tab->w[D.o3 - 1][k];
+        const double* Rd = Rc + 5 * D.nb;
+        const double* Ad = A + 5 * D.nb;
+        double tm = 0.0;
+        for (int v = 0; v < NV; ++v) tm = fmax(tm, fabs(scale * (Rd[v * nO + t] + Ad[v * nO + t] / J)));
+        atomicMax(&lmax[l], (unsigned long long)__double_as_longlong(tm));  // tm >= 0: bit order = value order
+    }
+    __syncthreads();
+    if (threadIdx.x < nlev)
+        P.tau[(3 * (long long)e + L[threadIdx.x].d) * DG_TAU_STRIDE_DEV + L[threadIdx.x].p] =
+            __longlong_as_double((long long)lmax[threadIdx.x]);
+}
+
 }  // namespace dgtau

@@ -139,13 +139,16 @@ def test_curved_rk_dt(dg, orc, name):
 @pytest.mark.parametrize("name", ["cfg4_small", "cfg5_subbox", "cfg4_full"])
 @pytest.mark.parametrize("ref", ["solver", "same"])
 @pytest.mark.parametrize("form", [0, 1])
-@pytest.mark.parametrize("kernel", ["ext", "generic"])
+@pytest.mark.parametrize("kernel", ["grp", "ext", "generic"])
 def test_curved_tau_parity(dg, orc, name, ref, form, kernel, monkeypatch):
-    """Isolated tau on the extruded O-grids: k_tau_ext (compact double-double
-    coarse metrics, the default on extruded meshes) and the generic 3-D
-    k_tau_curved (DGTAU_TAU_GENERIC=1)."""
+    """Isolated tau on the extruded O-grids: k_tau_grp (an element's levels
+    batched per CTA, the default on extruded meshes), k_tau_ext (one CTA per
+    level, DGTAU_TAU_PERLEVEL=1; both with compact coarse metrics) and the
+    generic 3-D k_tau_curved (DGTAU_TAU_GENERIC=1)."""
     if kernel == "generic":
         monkeypatch.setenv("DGTAU_TAU_GENERIC", "1")
+    if kernel == "ext":
+        monkeypatch.setenv("DGTAU_TAU_PERLEVEL", "1")
     mesh, orders, P, S, q, qd = setup(dg, orc, name)
     if ref == "solver":
         tg = S.tau_estimate(qd, S.rhs_eval(qd), formulation=form, reference=dg.REF_SOLVER).cpu().numpy()
@@ -168,11 +171,13 @@ def test_curved_tau_noniso_parity(dg, orc, name, form):
 
 
 @pytest.mark.parametrize("name", ["cfg4_small", "cfg5_subbox"])
-@pytest.mark.parametrize("kernel", ["ext", "generic"])
+@pytest.mark.parametrize("kernel", ["grp", "ext", "generic"])
 def test_curved_tau_euler_parity(dg, orc, name, kernel, monkeypatch):
-    """Euler on the curved extruded meshes: both tau kernels' inviscid branch."""
+    """Euler on the curved extruded meshes: the tau kernels' inviscid branch."""
     if kernel == "generic":
         monkeypatch.setenv("DGTAU_TAU_GENERIC", "1")
+    if kernel == "ext":
+        monkeypatch.setenv("DGTAU_TAU_PERLEVEL", "1")
     mesh, orders, P, S, q, qd = setup(dg, orc, name, physics="euler")
     tg = S.tau_estimate(qd, S.rhs_eval(qd), reference=dg.REF_SOLVER).cpu().numpy()
     to = P.tau_estimate(orders, q, P.rhs(orders, q))
@@ -273,3 +278,19 @@ def test_full_size_cfg5_sampled(dg, orc):
     r_o = np.concatenate([rl[offl[i]:offl[i + 1]] for i in li])
     assert rel_linf(r_g, r_o, orders[samp]) < RES_TOL
     assert tau_rel(tg[samp], tl[li]) < TAU_TOL
+
+
+@pytest.mark.parametrize("name", ["cfg5_subbox", "cfg4_adapted"])
+@pytest.mark.parametrize("physics", ["ns", "euler"])
+def test_tau_grp_vs_perlevel(dg, orc, name, physics, monkeypatch):
+    """k_tau_grp does the same operations per node and level as k_tau_ext
+    (only the CTA batching differs); the compiler's fma contraction may differ
+    between the two kernels, so they agree to a few ulp of the level maxima."""
+    mesh, orders, P, S, q, qd = setup(dg, orc, name, physics=physics)
+    r = S.rhs_eval(qd)
+    tg = S.tau_estimate(qd, r).cpu().numpy()
+    monkeypatch.setenv("DGTAU_TAU_PERLEVEL", "1")
+    tl = S.tau_estimate(qd, r).cpu().numpy()
+    assert np.array_equal(np.isnan(tg), np.isnan(tl))
+    ok = ~np.isnan(tg)
+    assert np.all(np.abs(tg[ok] - tl[ok]) <= 1e-13 * np.abs(tl[ok]).max())

@@ -6,13 +6,15 @@ import oracle as orc
 orc.build()
 from test_gpu_curved import setup
 from test_gpu_parity import tau_rel
-kernels = ("ext", "generic")
+kernels = ("grp", "ext", "generic")
 names = sys.argv[1:] or ["cfg4_small", "cfg5_subbox", "cfg4_full"]
 for name, kern in [(n, k) for n in names for k in kernels]:
+    os.environ.pop("DGTAU_TAU_GENERIC", None)
+    os.environ.pop("DGTAU_TAU_PERLEVEL", None)
     if kern == "generic":
         os.environ["DGTAU_TAU_GENERIC"] = "1"
-    else:
-        os.environ.pop("DGTAU_TAU_GENERIC", None)
+    if kern == "ext":
+        os.environ["DGTAU_TAU_PERLEVEL"] = "1"
     for ref in ("solver", "same"):
         for form in (0, 1):
             mesh, orders, P, S, q, qd = setup(dg, orc, name)
