@@ -15,6 +15,6 @@ ncu --set full --clock-control none --import-source on --kernel-name regex:k_ns_
     -o $O/face12 python tools/prof_stage_ns.py > $O/ncu_face.log 2>&1
 ncu --set full --clock-control none --import-source on --kernel-name regex:k_ns_res --launch-skip 3 --launch-count 1 \
     -o $O/res python tools/prof_stage_ns.py > $O/ncu_res.log 2>&1
-ncu --set full --clock-control none --import-source on --kernel-name regex:k_tau_ext --launch-skip 0 --launch-count 1 \
+ncu --set full --clock-control none --import-source on --kernel-name regex:k_tau_grp --launch-skip 0 --launch-count 1 \
     -o $O/tau python tools/prof_tau_ns.py > $O/ncu_tau.log 2>&1
 ls -la $O
