@@ -1442,7 +1442,7 @@ static int face_grid(dg_ctx* ctx, int nf)
 {
     using C = FaceCfg<W, MODE>;
     const int need = (nf + C::G - 1) / C::G;
-    if (!face_persist(MODE)) return need;
+    if (!face_persist(W, MODE)) return need;
     static int occ = 0;  // per instantiation, one device per process
     if (occ == 0) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ns_face<W, MODE>, C::BS, C::smem);

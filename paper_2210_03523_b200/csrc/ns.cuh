@@ -1416,16 +1416,19 @@ __device__ __forceinline__ void ns_face_one(const NsFaceParams& P, const NsFace&
     if (hasR) mortar_to_side<W, DIRECT_OK>(X, nout, ma, mb, SR.sa, SR.sb, P.tab, Y, P.out + oR, l, gid);
 }
 
-// measured on cfg5: pays for the qhat passes (1.68 -> 1.57 ms, W = 1), not for
-// the NS flux passes (their record slot costs spills at 168 registers); the
-// Euler flux passes (few registers) take it too
+// measured on cfg5: pays for the qhat passes (1.68 -> 1.57 ms, W = 1) and
+// the W = 2, 3 NS flux passes (2.56 -> 2.42, 1.13 -> 1.07 ms), not for the W = 1
+// NS flux pass (3.73 -> 4.06 ms); the Euler flux passes take it too
 #ifndef NS_FACE_PERSIST
 #define NS_FACE_PERSIST 1
 #endif
 #ifndef NS_FACE_PERSIST_NS
 #define NS_FACE_PERSIST_NS 0
 #endif
-__host__ __device__ constexpr bool face_persist(int MODE) { return NS_FACE_PERSIST && (MODE != MODE_FLUX_NS || NS_FACE_PERSIST_NS); }
+__host__ __device__ constexpr bool face_persist(int W, int MODE)
+{
+    return NS_FACE_PERSIST && (MODE != MODE_FLUX_NS || W >= 2 || NS_FACE_PERSIST_NS);
+}
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src)
 {
@@ -1448,7 +1451,7 @@ __global__ void __launch_bounds__(FaceCfg<W, MODE>::BS, face_minb(W, MODE)) k_ns
     if (fi >= P.fend) return;  // the whole group leaves (named barriers are per group)
     double* X = fsm + gid * 2 * C::BUF;
     double* Y = X + C::BUF;
-    if constexpr (face_persist(MODE)) {
+    if constexpr (face_persist(W, MODE)) {
     static_assert(sizeof(NsFace) == 80, "NsFace record: 5 x 16 bytes");
     __shared__ __align__(16) NsFace fq[C::G][2];
     const int gstride = gridDim.x * C::G;
