@@ -1012,6 +1012,33 @@ __device__ __forceinline__ FSide face_side(long long off, int ord, int d, bool i
     return s;
 }
 
+// Interpolation passes of the 20-component (q + gradient) NS flux traces:
+// runtime-length loops with the components unrolled inside, instead of 9-long
+// predicated loops per component (same fma order: bit-identical).  Measured on
+// cfg5: flux faces W = 1/2/3 3.73 / 2.42 / 1.07 -> 3.36 / 2.01 / 0.95 ms, RK
+// step 105.3 -> 100.0 ms for 2 steps; the 5-component qhat passes keep the
+// predicated loops (no gain), and the same rewrite of the projection back to
+// the sides was slower (2 steps 106.9 ms) -- dropped.
+#ifndef NS_INTERP_RT
+#define NS_INTERP_RT 1
+#endif
+__host__ __device__ constexpr bool interp_rt(int ncm) { return NS_INTERP_RT && ncm > NV; }
+
+// acc[c] = sum_{k < len} tr[k] src[c CAP + k ss] for the NCM components
+template <int W, int NCM>
+__device__ __forceinline__ void interp_row(const double* __restrict__ tr, int len, const double* src, int ss, double* acc)
+{
+    constexpr int CAP = 32 * W;
+#pragma unroll
+    for (int c = 0; c < NCM; ++c) acc[c] = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < len; ++k) {
+        const double t = __ldg(tr + k);
+#pragma unroll
+        for (int c = 0; c < NCM; ++c) acc[c] = fma(t, src[c * CAP + k * ss], acc[c]);
+    }
+}
+
 // Interpolate nc components of a side trace to the mortar grid.  Component c
 // is read from (c < 5 ? q : g) + (c mod 5 ...) : qsrc[c n + node] for c < 5,
 // gsrc[(c - 5) n + node] for c >= 5.  Gather (one thread per trace point),
@@ -1039,6 +1066,12 @@ __device__ __forceinline__ void side_to_mortar(const double* __restrict__ qsrc, 
         if (l < sb * ma) {
             const double* Ta = tab->T[sa - 1][ma - 1] + 0;  // [i * sa + a]
             const int b = l / ma, i = l - b * ma;
+            if constexpr (interp_rt(NCM)) {
+                double acc[NCM];
+                interp_row<W, NCM>(Ta + i * sa, sa, X + b * sa, 1, acc);
+#pragma unroll
+                for (int c = 0; c < NCM; ++c) Y[c * CAP + l] = acc[c];
+            } else {
             double t[NP];
 #pragma unroll
             for (int a = 0; a < NP; ++a) t[a] = a < sa ? __ldg(Ta + i * sa + a) : 0.0;
@@ -1052,6 +1085,7 @@ __device__ __forceinline__ void side_to_mortar(const double* __restrict__ qsrc, 
                     if (a < sa) acc = fma(t[a], x[a], acc);
                 Y[c * CAP + l] = acc;  // [c][b][i]
             }
+            }
         }
         grp_sync<W>(gid);
         Z = Y;
@@ -1060,6 +1094,9 @@ __device__ __forceinline__ void side_to_mortar(const double* __restrict__ qsrc, 
         const int j = p / ma, i = p - j * ma;
         if (sb < mb) {
             const double* Tb = tab->T[sb - 1][mb - 1];
+            if constexpr (interp_rt(NCM)) {
+                interp_row<W, NCM>(Tb + j * sb, sb, Z + i, ma, val);
+            } else {
             double t[NP];
 #pragma unroll
             for (int b = 0; b < NP; ++b) t[b] = b < sb ? __ldg(Tb + j * sb + b) : 0.0;
@@ -1071,6 +1108,7 @@ __device__ __forceinline__ void side_to_mortar(const double* __restrict__ qsrc, 
                 for (int b = 0; b < NP; ++b)
                     if (b < sb) acc = fma(t[b], Z[c * CAP + b * ma + i], acc);
                 val[c] = acc;
+            }
             }
         } else {
 #pragma unroll
@@ -1129,6 +1167,9 @@ __device__ __forceinline__ void side_direct(const double* X, const FSide& s, int
     const int j = p / ma, i = p - j * ma;
     if (sa < ma) {  // sb == mb: row j of the trace along a
         const double* Ta = tab->T[sa - 1][ma - 1];
+        if constexpr (interp_rt(NCM)) {
+            interp_row<W, NCM>(Ta + i * sa, sa, X + j * sa, 1, val);
+        } else {
         double t[NP];
 #pragma unroll
         for (int a = 0; a < NP; ++a) t[a] = a < sa ? __ldg(Ta + i * sa + a) : 0.0;
@@ -1141,8 +1182,12 @@ __device__ __forceinline__ void side_direct(const double* X, const FSide& s, int
                 if (a < sa) acc = fma(t[a], x[a], acc);
             val[c] = acc;
         }
+        }
     } else if (sb < mb) {  // sa == ma: column i along b
         const double* Tb = tab->T[sb - 1][mb - 1];
+        if constexpr (interp_rt(NCM)) {
+            interp_row<W, NCM>(Tb + j * sb, sb, X + i, ma, val);
+        } else {
         double t[NP];
 #pragma unroll
         for (int b = 0; b < NP; ++b) t[b] = b < sb ? __ldg(Tb + j * sb + b) : 0.0;
@@ -1153,6 +1198,7 @@ __device__ __forceinline__ void side_direct(const double* X, const FSide& s, int
             for (int b = 0; b < NP; ++b)
                 if (b < sb) acc = fma(t[b], X[c * CAP + b * ma + i], acc);
             val[c] = acc;
+        }
         }
     } else {
 #pragma unroll
@@ -1231,12 +1277,13 @@ __device__ __forceinline__ void mortar_to_side(const double* Fm, int nc, int ma,
 
 // resident CTAs per SM the register budget targets: the BR1 qhat pass fits in
 // 80 registers without spills (more faces in flight), the NS flux needs 128
-// (W = 1 with the one-latency gather: 168 at 3 CTAs, cfg5 3.90 -> 3.80 ms)
+// (W = 1 with the one-latency gather: 168 at 3 CTAs, cfg5 3.90 -> 3.80 ms;
+// W = 2 at 4 CTAs = 128 registers once NS_INTERP_RT: 2.00 -> 1.97 ms)
 #ifndef NS_FLUX_MINB1
 #define NS_FLUX_MINB1 3
 #endif
 #ifndef NS_FLUX_MINB2
-#define NS_FLUX_MINB2 3
+#define NS_FLUX_MINB2 4
 #endif
 #ifndef NS_FLUX_MINB3
 #define NS_FLUX_MINB3 2
@@ -1417,13 +1464,15 @@ __device__ __forceinline__ void ns_face_one(const NsFaceParams& P, const NsFace&
 }
 
 // measured on cfg5: pays for the qhat passes (1.68 -> 1.57 ms, W = 1) and
-// the W = 2, 3 NS flux passes (2.56 -> 2.42, 1.13 -> 1.07 ms), not for the W = 1
-// NS flux pass (3.73 -> 4.06 ms); the Euler flux passes take it too
+// the W = 2, 3 NS flux passes (2.56 -> 2.42, 1.13 -> 1.07 ms); the W = 1 NS
+// flux pass took it once its interpolation loops had the runtime length
+// (NS_INTERP_RT; 3.35 -> 3.20 ms, before: 3.73 -> 4.06 ms); the Euler flux
+// passes take it too
 #ifndef NS_FACE_PERSIST
 #define NS_FACE_PERSIST 1
 #endif
 #ifndef NS_FACE_PERSIST_NS
-#define NS_FACE_PERSIST_NS 0
+#define NS_FACE_PERSIST_NS 1
 #endif
 __host__ __device__ constexpr bool face_persist(int W, int MODE)
 {
