@@ -22,10 +22,12 @@
  * 1 for the +1 side.  neighbour[e][f] >= 0: element across f (whose face
  * 2d+(1-s) touches it); -1: no-slip adiabatic wall; -2: far field.
  *
- * Parity unpinned: Roe flux on general states, BR1 on general states, the
- * wall/far-field boundary states, the extrapolation law and the CFL
- * constants are pinned only structurally (free stream, rest state,
- * conservation, consistency, symmetry); see DESIGN.md "Parity pins".
+ * Parity unpinned: the extrapolation law (A13) and the advective CFL
+ * constants (A11) are pinned only by consistency pins and hand values.
+ * Pinned since round 2: the Roe flux on general subsonic states (Q25, |A~|
+ * as a matrix square root), BR1 / the viscous terms / wall and far-field
+ * states (Q19-Q22 exact NS solutions and closed forms), the assembly (Q24
+ * dense Galerkin form); see DESIGN.md section 2.
  */
 #include <math.h>
 #include <stdint.h>

@@ -214,3 +214,48 @@ def test_q24_dense_navier_stokes(dims, N):
     # the viscous part is visible at this mu: the Euler residual differs by far more than the bar
     eul = O.Problem(mesh, O.phys(O.EULER, O.LLF, GAMMA)).rhs(orders, q)
     assert np.abs(eul - ref).max() > 1e-3 * np.abs(ref).max()
+
+
+# ----------------------------------------------------------------------------
+# Q25 Roe flux on general subsonic states (reading A7: no entropy fix)
+# ----------------------------------------------------------------------------
+
+def test_q25_roe_matrix_absolute_value():
+    """Roe's solver is F = 1/2 (f_L + f_R).n - 1/2 |A~| (q_R - q_L), A~ the
+    flux Jacobian d(f.n)/dq at the Roe-averaged velocity and total enthalpy
+    (the Jacobian is homogeneous of degree 0: it depends on u and H only).
+    Here A~ is the complex-step derivative of the numpy Euler flux and |A~| =
+    sqrt(A~ A~) the principal matrix square root (scipy): no eigenvectors,
+    no wave strengths.  Also Roe's property A~ dq = df, which pins the
+    averaging itself."""
+    from scipy.linalg import sqrtm
+    rng = np.random.default_rng(25)
+
+    def fn(q, n):
+        return sum(n[k] * _euler(q, k) for k in range(3))
+
+    worst = 0.0
+    for _ in range(200):
+        prim = lambda: (rng.uniform(0.5, 2.0), rng.uniform(-0.6, 0.6, 3), rng.uniform(0.7, 2.0))  # noqa: E731
+        (rL, uL, pL), (rR, uR, pR) = prim(), prim()
+        qL = np.array([rL, *(rL * uL), pL / (GAMMA - 1) + 0.5 * rL * uL @ uL])
+        qR = np.array([rR, *(rR * uR), pR / (GAMMA - 1) + 0.5 * rR * uR @ uR])
+        n = rng.normal(size=3)
+        n /= np.linalg.norm(n)
+        sl, sr = np.sqrt(rL), np.sqrt(rR)
+        u = (sl * uL + sr * uR) / (sl + sr)
+        H = (sl * (qL[4] + pL) / rL + sr * (qR[4] + pR) / rR) / (sl + sr)
+        if abs(u @ n) < 0.02:      # |A| is not smooth at a vanishing eigenvalue: stay off it
+            continue
+        qt = np.array([1.0, *u, (H + 0.5 * (GAMMA - 1) * u @ u) / GAMMA])
+        A = np.empty((5, 5))
+        for j in range(5):
+            qc = qt.astype(complex)
+            qc[j] += 1e-30j
+            A[:, j] = fn(qc, n).imag / 1e-30
+        assert np.abs(A @ (qR - qL) - (fn(qR, n) - fn(qL, n))).max() < 1e-13     # Roe's property
+        absA = sqrtm(A @ A).real
+        ref = 0.5 * (fn(qL, n) + fn(qR, n)) - 0.5 * absA @ (qR - qL)
+        got = O.roe_flux(qL, qR, n, GAMMA)
+        worst = max(worst, np.abs(got - ref).max() / np.abs(ref).max())
+    assert worst < 1e-11
