@@ -260,10 +260,12 @@ class Cfg5Run:
         import torch
 
         self.dg, self.world = dg, world
+        # BENCH_FORCE_DIST=1 (diagnostic): the N > 1 code path (DistSolver, per-step exchange calls) on one rank
+        self.single = world == 1 and os.environ.get("BENCH_FORCE_DIST") != "1"
         mesh, orders, nsp = cfg5_problem()
         self.mesh, self.orders_g = mesh, orders
         kw = dict(physics=dg.NS, mu=nsp["mu"], Pr=nsp["Pr"], qinf=nsp["qinf"])
-        if world == 1:
+        if self.single:
             self.S = dg.Solver(mesh, **kw)
             self.S.set_orders(orders)
             self.core = self.S
@@ -296,7 +298,7 @@ class Cfg5Run:
         self.ref = torch.empty_like(self.qa)
         self.tau = torch.empty((self.E_loc, 3, 9), dtype=torch.float64, device=dev)
         self.dts = [torch.zeros(1, dtype=torch.float64, device=dev) for _ in range(2)]
-        if world == 1:
+        if self.single:
             self.S.compute_dt(self.qa, CFL, self.dts[0])
         else:
             self.D.compute_dt(self.qa, CFL, self.dts[0])
@@ -311,7 +313,7 @@ class Cfg5Run:
         if timers is not None:
             e0 = ev()
             e0.record(stream)
-        if self.world == 1:
+        if self.single:
             self.S.rk_steps(CFG5_RK, self.qa, self.qb, self.g, self.dts[0], self.dts[1], CFL)  # even: ends in qa
         else:
             for _ in range(CFG5_RK):
@@ -321,7 +323,7 @@ class Cfg5Run:
         if timers is not None:
             e1 = ev()
             e1.record(stream)
-        if self.world == 1:
+        if self.single:
             self.S.rhs_eval(self.qa, self.ref)
             self.S.tau_estimate(self.qa, self.ref, reference=dg.REF_SOLVER, tau=self.tau)
         else:
@@ -330,7 +332,7 @@ class Cfg5Run:
         if timers is not None:
             e2 = ev()
             e2.record(stream)
-        if self.world == 1:
+        if self.single:
             sel = self.S.select_orders(self.tau, CFG5_TAU_MAX, CFG5_NMIN, CFG5_NMAX, mode=dg.SELECT_DYNAMIC,
                                        jump_rule=dg.JUMP_B, dec_cap=1)[0]
         else:
@@ -717,10 +719,14 @@ def main():
     os.environ["BENCH_PATH"] = args.path
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
-    if world > 1:
+    if world > 1 or os.environ.get("BENCH_FORCE_DIST") == "1":
         import torch
         import torch.distributed as dist
 
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
         backend = "nccl" if args.impl == "ours" else "gloo"
         if args.impl == "ours":
             torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
@@ -834,4 +840,11 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    try:
+        main()
+    finally:
+        if "torch.distributed" in sys.modules:
+            import torch.distributed as _dist
+
+            if _dist.is_initialized():
+                _dist.destroy_process_group()
