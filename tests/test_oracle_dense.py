@@ -187,10 +187,10 @@ def _state(prob, orders, seed):
 
 
 @pytest.mark.parametrize("dims,N", [((2, 2, 1), (3, 2, 4)), ((2, 2, 2), (2, 3, 1)), ((1, 2, 2), (5, 1, 2))])
-def test_q24_dense_euler(dims, N):
+def test_q24_dense_euler(dims, N, handle=None):
     mesh = W.cube_mesh(*dims, L=(1.0, 0.8, 1.3))
     orders = W.orders_uniform(mesh.E, N)
-    prob = O.Problem(mesh, O.phys(O.EULER, O.LLF, GAMMA))
+    prob = O.Problem(mesh, O.phys(O.EULER, O.LLF, GAMMA), handle=handle)
     q = _state(prob, orders, 11)
     ref, _ = _dense_rhs(mesh, N, q)
     got = prob.rhs(orders, q)
@@ -200,11 +200,11 @@ def test_q24_dense_euler(dims, N):
 
 
 @pytest.mark.parametrize("dims,N", [((2, 2, 1), (3, 2, 4)), ((2, 1, 2), (2, 4, 3))])
-def test_q24_dense_navier_stokes(dims, N):
+def test_q24_dense_navier_stokes(dims, N, handle=None):
     mesh = W.cube_mesh(*dims, L=(1.0, 0.8, 1.3))
     orders = W.orders_uniform(mesh.E, N)
     ph = O.phys(O.NS, O.LLF, GAMMA, mu=0.05, Pr=0.72)
-    prob = O.Problem(mesh, ph)
+    prob = O.Problem(mesh, ph, handle=handle)
     q = _state(prob, orders, 12)
     ref, g = _dense_rhs(mesh, N, q, ph)
     gg = prob.gradient(orders, q).reshape(g.shape)
@@ -220,7 +220,16 @@ def test_q24_dense_navier_stokes(dims, N):
 # Q25 Roe flux on general subsonic states (reading A7: no entropy fix)
 # ----------------------------------------------------------------------------
 
-def test_q25_roe_matrix_absolute_value():
+def _roe(handle, qL, qR, n):
+    if handle is None:
+        return O.roe_flux(qL, qR, n, GAMMA)
+    import ctypes as C
+    F = np.empty(5)
+    handle.orc_roe_flux(*(C.c_void_p(a.ctypes.data) for a in (qL, qR, n)), C.c_double(GAMMA), C.c_void_p(F.ctypes.data))
+    return F
+
+
+def test_q25_roe_matrix_absolute_value(handle=None):
     """Roe's solver is F = 1/2 (f_L + f_R).n - 1/2 |A~| (q_R - q_L), A~ the
     flux Jacobian d(f.n)/dq at the Roe-averaged velocity and total enthalpy
     (the Jacobian is homogeneous of degree 0: it depends on u and H only).
@@ -256,6 +265,6 @@ def test_q25_roe_matrix_absolute_value():
         assert np.abs(A @ (qR - qL) - (fn(qR, n) - fn(qL, n))).max() < 1e-13     # Roe's property
         absA = sqrtm(A @ A).real
         ref = 0.5 * (fn(qL, n) + fn(qR, n)) - 0.5 * absA @ (qR - qL)
-        got = O.roe_flux(qL, qR, n, GAMMA)
+        got = _roe(handle, qL, qR, n)
         worst = max(worst, np.abs(got - ref).max() / np.abs(ref).max())
     assert worst < 1e-11

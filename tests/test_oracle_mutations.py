@@ -14,6 +14,7 @@ import subprocess
 import pytest
 
 import oracle as O
+import test_oracle_dense as DP
 import test_oracle_ns_pins as NSP
 
 SRC = os.path.join(os.path.dirname(O.__file__), "dgsem_oracle.c")
@@ -53,6 +54,21 @@ MUTATIONS = [
     ("tau_field_reference_restriction", "tapply(5, qdot_ref + off[e], np, d, T, p + 1, rc);",
      "tapply(5, qdot_ref + off[e], np, d, Pm[N[d]][p], p + 1, rc);", None,
      lambda h: NSP.test_q9_decoupling(handle=h)),
+    # mistakes that stay consistent and conservative (free stream and sum M Qdot blind): the dense
+    # assembly pin Q24 and the |A~| pin Q25 of tests/test_oracle_dense.py
+    ("llf_dissipation_factor", "- 0.5 * lam * (qR[v] - qL[v])", "- lam * (qR[v] - qL[v])", None,
+     lambda h: DP.test_q24_dense_euler((2, 2, 1), (3, 2, 4), handle=h)),
+    ("lifting_face_index_transposed", "int fi = idx[TAN[d][0]] + (N[TAN[d][0]] + 1) * idx[TAN[d][1]];",
+     "int fi = idx[TAN[d][1]] + (N[TAN[d][1]] + 1) * idx[TAN[d][0]];", None,
+     lambda h: DP.test_q24_dense_euler((2, 2, 1), (3, 2, 4), handle=h)),
+    ("br1_lifting_face_index_transposed", "int fi = t1 + (N[TAN[d][0]] + 1) * t2;",
+     "int fi = t2 + (N[TAN[d][1]] + 1) * t1;", None,
+     lambda h: DP.test_q24_dense_navier_stokes((2, 2, 1), (3, 2, 4), handle=h)),
+    ("roe_no_absolute_value", "fabs(lam[k]) * (double)B[k]", "lam[k] * (double)B[k]", None,
+     lambda h: DP.test_q25_roe_matrix_absolute_value(handle=h)),
+    ("roe_enthalpy_plain_mean", "H = ((qL[4] + pL) / rl + (qR[4] + pR) / rr) / (rl + rr);",
+     "H = 0.5 * ((qL[4] + pL) / qL[0] + (qR[4] + pR) / qR[0]);", None,
+     lambda h: DP.test_q25_roe_matrix_absolute_value(handle=h)),
 ]
 
 
