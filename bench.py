@@ -106,7 +106,7 @@ def interior_faces(mesh, orders):
     return out
 
 
-def flops_residual(mesh, orders, ns=True):
+def flops_residual(mesh, orders, ns=True, parts=False):
     """fp64 flops of one non-isolated residual:
       per node: primitives (12); NS: products (Ja^d)_k q (45), the BR1 volume
       sums D^d along each line for 15 components (30 n_d per direction), 1/J
@@ -126,11 +126,13 @@ def flops_residual(mesh, orders, ns=True):
     lines = (30 if ns else 0) + 10
     vol = float((n * (per_node + lines * o.sum(1))).sum())
     face = 0.0
+    face_pts = mortar_unit = 0.0
     pt_cost = (150 + 2 * 138 + 30 + 2 * 20 + 2 * 45) if ns else (150 + 2 * 20)
     for d, tl, tr in interior_faces(mesh, np.asarray(orders)):
         sl, sr = tl + 1, tr + 1
         m = np.maximum(sl, sr)
         face += float((m.prod(1) * pt_cost).sum())
+        face_pts += float(m.prod(1).sum())
         for side in (sl, sr):
             ncin = (5 + 20) if ns else 5
             ncout = (15 + 5) if ns else 5
@@ -140,12 +142,22 @@ def flops_residual(mesh, orders, ns=True):
             pa = np.where(a_diff, 2 * m[:, 0] * side[:, 0] * side[:, 1], 0)
             pb = np.where(b_diff, 2 * m[:, 0] * m[:, 1] * side[:, 1], 0)
             face += float(((ncin + ncout) * (pa + pb)).sum())
+            mortar_unit += float((pa + pb).sum())
     nb = np.asarray(mesh.nbr)
     bnd = 0.0
     for d in range(3):
         for s in range(2):
             e = np.flatnonzero(nb[:, 2 * d + s] < 0)
             bnd += float((n[e] // o[e, d] * pt_cost).sum())
+    if parts and ns:
+        # the same counts split by the kernel that carries them (cfg5 stage kernels)
+        pts = (face_pts + bnd / pt_cost)
+        split = {"k_ns_res": float((n * (12 + 110 + 3 * 55 + 35 + 40 + 10 * o.sum(1))).sum()) + 2 * 20 * pts,
+                 "k_ns_grad": float((n * (45 + 15 + 30 * o.sum(1))).sum()) + 2 * 45 * pts,
+                 "qhat_faces": 30 * pts + (5 + 15) * mortar_unit,
+                 "flux_faces": (150 + 2 * 138) * pts + (20 + 5) * mortar_unit}
+        assert abs(sum(split.values()) - (vol + face + bnd)) < 1e-6 * (vol + face + bnd)
+        return split
     return vol + face + bnd
 
 
@@ -549,6 +561,8 @@ def run_gpu(args, rank, world):
     res["rk_stages"] = 3 * R.rk_steps_per_step * args.steps
     res["tau_elems"] = n_elem * args.steps / (tau_ms * 1e-3)
     res["e2e"] = None if args.no_e2e else run_e2e(R, args, stream, ev, world)
+    res["stage_kernels"] = (stage_kernel_times(R, stream, ev)
+                            if isinstance(R, Cfg5Run) and R.single and not args.no_stage_kernels else None)
     return res
 
 
@@ -616,6 +630,71 @@ def run_e2e(R, args, stream, ev, world):
             "h2d_bytes_per_step": int(owned * 8), "d2h_bytes_per_step": int(d2h // args.steps),
             "copies": "pinned H2D of each step's input state and D2H of its result state + selected orders on a "
                       "copy stream, double-buffered, overlapping the neighbouring steps"}
+
+
+def stage_kernel_block(times, mesh, orders, peak_f, peak_bw):
+    """Per-kernel rooflines of a cfg5 RK stage: the live times of
+    stage_kernel_times with the algorithmic flops of flops_residual(parts)
+    and the DRAM bytes per launch of the committed ncu capture
+    (profiles/traffic_cfg5_stage.json: 3 stages per kernel)."""
+    if not times:
+        return None
+    fl = flops_residual(mesh, orders, ns=True, parts=True)
+    tr = {}
+    p = os.path.join(ROOT, "profiles", "traffic_cfg5_stage.json")
+    if os.path.exists(p):
+        for k, v in json.load(open(p)).get("per_kernel_per_step", {}).items():
+            g = ("k_ns_grad" if "k_ns_grad" in k else "k_ns_res" if "k_ns_res" in k else
+                 "qhat_faces" if k.rstrip(">").endswith(", 0") else "flux_faces" if k.rstrip(">").endswith(", 2") else None)
+            if g:
+                tr[g] = tr.get(g, 0.0) + v["dram_bytes"] / 3.0
+    out = {"how": "each group launched alone through the split-pass flags of dg_gradient_flags / dg_rk_stage, "
+                  "CUDA events on the launch stream, same buffers and launch configuration as the timed steps",
+           "sum_ms": sum(t["ms"] for t in times.values())}
+    for k, t in times.items():
+        tf = fl[k] / (t["ms"] * 1e-3) / 1e12
+        d = {"ms": t["ms"], "launches": t["launches"], "flops": fl[k], "tflops": tf, "frac_dfma": tf / peak_f}
+        if k in tr:
+            d["dram_bytes_ncu"] = tr[k]
+            d["dram_gbs"] = tr[k] / (t["ms"] * 1e-3) / 1e9
+            d["frac_hbm_actual_traffic"] = d["dram_gbs"] / peak_bw
+        out[k] = d
+    return out
+
+
+def stage_kernel_times(R, stream, ev, reps=5):
+    """The four kernel groups of one cfg5 RK stage, each launched ALONE through
+    the C-ABI's split-pass flags (on one rank no face has a halo side, so
+    FLAG_FACES_INTERIOR = the face kernels only, FLAG_FACES_HALO = the element
+    kernel only) and timed with CUDA events on the launch stream; same launch
+    configuration, buffers and state as in the timed steps (stage 2 of the
+    Williamson scheme: the RK register is read and written)."""
+    import torch
+
+    dg, S = R.dg, R.S
+    flux = dg.FLAG_GRADIENT_READY
+    groups = [
+        ("qhat_faces", 3, lambda: S.gradient(R.qa, flags=dg.FLAG_FACES_INTERIOR)),
+        ("k_ns_grad", 1, lambda: S.gradient(R.qa, flags=dg.FLAG_FACES_HALO)),
+        ("flux_faces", 3, lambda: S.rk_stage(1, R.qa, R.qb, R.g, R.dts[0], None, flags=flux | dg.FLAG_FACES_INTERIOR)),
+        ("k_ns_res", 1, lambda: S.rk_stage(1, R.qa, R.qb, R.g, R.dts[0], None, flags=flux | dg.FLAG_FACES_HALO)),
+    ]
+    S.rk_stage(1, R.qa, R.qb, R.g, R.dts[0], None)  # a whole stage: gradient and face blocks of this state in place
+    torch.cuda.synchronize()
+    out = {}
+    for name, nl, fn in groups:
+        fn()
+        l0 = S.launches
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        out[name] = {"ms": e0.elapsed_time(e1) / reps, "launches": (S.launches - l0) // reps}
+        if out[name]["launches"] != nl:
+            raise RuntimeError(f"stage_kernel_times: {name} launched {out[name]['launches']} kernels, expected {nl}")
+    return out
 
 
 # ----------------------------------------------------------------------------
@@ -707,6 +786,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg5", choices=["cfg5", "cfg2"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-stage-kernels", action="store_true", help="skip the per-kernel timings of a cfg5 stage")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--path", default="auto", choices=["auto", "runtime", "bucketed"],
                     help="cfg2: residual kernel family (dg_set_path); AUTO decides per layout")
@@ -831,6 +911,7 @@ def main():
         "roofline_tau": {"bound": "alu", "achieved": tau_tf, "peak": peak_f, "unit": "TFLOP/s",
                          "frac": tau_tf / peak_f, "flops_per_estimate": f_tau,
                          "note": "tau time includes the SOLVER reference residual"},
+        "stage_kernels": stage_kernel_block(res.get("stage_kernels"), mesh, orders, peak_f, peak_bw) if ns else None,
         "cpu_baseline": cpu,
         "e2e": res["e2e"],
         "gpu_launches": res["launches"],
