@@ -738,10 +738,39 @@ def oracle_cfg5(nth, rk_steps, threads=None):
                        f"+ SOLVER residual + tau-estimate + dynamic selection")
 
 
-def oracle_one_thread(nth, rk_steps):
+def oracle_cfg2(rk_steps, threads=None):
+    """The oracle on the whole cfg2 problem (16^3, N = 6, Euler pulse): rk_steps
+    RK3 steps, SOLVER reference residual, isolated tau-estimate, dynamic
+    selection (rule b) and the transfer to the selected orders."""
+    import oracle
+
+    mesh = W.cube_mesh(16)
+    orders = W.orders_uniform(mesh.E, 6)
+    P = oracle.Problem(mesh, oracle.phys(oracle.EULER))
+    q = W.pulse_state(P.node_coords(orders), orders, center=W.cfg2_center(), sigma=0.08)
+    t0 = time.perf_counter()
+    for _ in range(rk_steps):
+        q = P.rk3_step(orders, q, P.dt(orders, q, CFL))
+    t1 = time.perf_counter()
+    r = P.rhs(orders, q)
+    tau = P.tau_estimate(orders, q, r)
+    sel = oracle.select_dynamic(orders, tau, mesh.nbr, CFG2_TAU_MAX, CFG2_NMIN, CFG2_NMAX)
+    sel = sel[0] if isinstance(sel, tuple) else sel
+    oracle.transfer(orders, q, np.ascontiguousarray(sel, np.int32))
+    t2 = time.perf_counter()
+    nd = W.ndof(orders)
+    return dict(gdofs=nd * (3 * rk_steps + 1) / (t2 - t0) / 1e9, res_gdofs=nd * 3 * rk_steps / (t1 - t0) / 1e9,
+                tau_elems=mesh.E / (t2 - t1), cores=int(threads or os.environ.get("OMP_NUM_THREADS") or os.cpu_count()),
+                sample=f"cfg2 (16^3 elements, N = 6, {nd} DOF): {rk_steps} RK3 step(s) + SOLVER residual + tau-estimate + "
+                       f"dynamic selection + transfer")
+
+
+def oracle_one_thread(nth, rk_steps, fn="oracle_cfg5"):
     """The same oracle step at 1 thread (a subprocess with OMP_NUM_THREADS=1)."""
+    call = "bench.oracle_cfg5(%d, %d, threads=1)" % (nth, rk_steps) if fn == "oracle_cfg5" else \
+        "bench.oracle_cfg2(%d, threads=1)" % rk_steps
     code = ("import json,sys; sys.path.insert(0, %r); import bench; "
-            "print(json.dumps(bench.oracle_cfg5(%d, %d, threads=1)))" % (ROOT, nth, rk_steps))
+            "print(json.dumps(%s))" % (ROOT, call))
     env = dict(os.environ, OMP_NUM_THREADS="1")
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     if out.returncode != 0:
@@ -867,6 +896,17 @@ def main():
                {"value": one["gdofs"], "residual_gdofs": one["res_gdofs"], "tau_elems_per_s": one["tau_elems"],
                 "sample": one["sample"], "cores": 1},
                "residual_gdofs": cb["res_gdofs"]}
+    if not args.no_cpu_baseline and world == 1 and args.workload == "cfg2":
+        import oracle
+
+        oracle.build()
+        cb = oracle_cfg2(4)
+        one = oracle_one_thread(0, 1, fn="oracle_cfg2")
+        cpu = {"value": cb["gdofs"], "unit": "GDOF/s", "cores": cb["cores"], "kind": "oracle", "sample": cb["sample"],
+               "tau_elems_per_s": cb["tau_elems"], "residual_gdofs": cb["res_gdofs"],
+               "one_thread": None if one is None else
+               {"value": one["gdofs"], "residual_gdofs": one["res_gdofs"], "tau_elems_per_s": one["tau_elems"],
+                "sample": one["sample"], "cores": 1}}
     peak_bw, peak_bw_src = load_peaks()
     peak_f, peak_f_src = load_fp64_peak()
     ns = args.workload == "cfg5"
