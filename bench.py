@@ -328,10 +328,13 @@ class Cfg5Run:
         if self.single:
             self.S.rk_steps(CFG5_RK, self.qa, self.qb, self.g, self.dts[0], self.dts[1], CFL)  # even: ends in qa
         else:
+            h0 = time.perf_counter()
             for _ in range(CFG5_RK):
                 self.D.rk_step_dt(self.qa, self.qb, self.g, self.dts[0], CFL, self.dts[1])
                 self.qa, self.qb = self.qb, self.qa
                 self.dts.reverse()
+            self.host_rk_s = getattr(self, "host_rk_s", 0.0) + time.perf_counter() - h0  # host time to enqueue
+            self.host_rk_n = getattr(self, "host_rk_n", 0) + 3 * CFG5_RK
         if timers is not None:
             e1 = ev()
             e1.record(stream)
@@ -807,6 +810,25 @@ def config_block(args, world, R=None):
     return c
 
 
+_JSON_OUT = None
+
+
+def claim_stdout():
+    """The contract is ONE JSON line on stdout: libraries that write to fd 1
+    (NCCL prints its version banner there when the first communicator is
+    created) are sent to stderr, and the line goes to the saved descriptor."""
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
+def emit(line):
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -820,6 +842,7 @@ def main():
     ap.add_argument("--path", default="auto", choices=["auto", "runtime", "bucketed"],
                     help="cfg2: residual kernel family (dg_set_path); AUTO decides per layout")
     args = ap.parse_args()
+    claim_stdout()
     if args.workload == "cfg2":
         # the dynamic run meets new (N1,N2,N3) kernel instances as the layout
         # changes: load every kernel at context creation (setup), not lazily
@@ -876,7 +899,7 @@ def main():
                 "cpu_baseline": {"value": value, "unit": "GDOF/s", "cores": cores, "kind": "oracle",
                                  "sample": sample},
                 "e2e": {"value": value, "unit": "GDOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line))
+        emit(line)
         return
 
     res = run_gpu(args, rank, world)
@@ -952,12 +975,13 @@ def main():
                          "frac": tau_tf / peak_f, "flops_per_estimate": f_tau,
                          "note": "tau time includes the SOLVER reference residual"},
         "stage_kernels": stage_kernel_block(res.get("stage_kernels"), mesh, orders, peak_f, peak_bw) if ns else None,
+        "host_enqueue_ms_per_stage": (R.host_rk_s / R.host_rk_n * 1e3) if getattr(R, "host_rk_n", 0) else None,
         "cpu_baseline": cpu,
         "e2e": res["e2e"],
         "gpu_launches": res["launches"],
         "clocks": res["clocks"],
     }
-    print(json.dumps(line))
+    emit(line)
 
 
 if __name__ == "__main__":

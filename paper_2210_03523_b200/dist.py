@@ -309,7 +309,9 @@ class DistSolver:
         S._check(S.L.dg_select_local(S.ctx, C.byref(pol), C.c_void_p(tau.data_ptr()),
                                      C.c_void_p(0 if total_map is None else total_map.data_ptr()),
                                      C.c_void_p(a.data_ptr()), None, self._stream()), "dg_select_local")
-        oplan = part.HaloPlan(self.lm, np.zeros((E, 3), np.int32), 3)  # 3 ints per element, n = 1 node
+        if getattr(self, "_oplan", None) is None:  # depends on the local mesh only
+            self._oplan = part.HaloPlan(self.lm, np.zeros((E, 3), np.int32), 3)  # 3 ints per element, n = 1 node
+        oplan = self._oplan
         changed = torch.zeros(1, dtype=torch.int32, device="cuda")
         for _ in range(64):
             flat = a.view(-1)
@@ -321,16 +323,31 @@ class DistSolver:
             dist.all_reduce(changed, op=dist.ReduceOp.MAX, group=self.group)
             if int(changed.item()) == 0:
                 break
-        own = a[: self.lm.n_own].cpu().numpy()
-        out = [torch.zeros(0)] * self.world
-        gathered = [None] * self.world
-        dist.all_gather_object(gathered, (self.lm.gids[: self.lm.n_own], own), group=self.group)
-        total = sum(len(g[0]) for g in gathered)
-        res = np.zeros((total, 3), np.int32)
-        for gid, o in gathered:
-            res[gid] = o
-        del out
-        return res
+        n_own = self.lm.n_own
+        if dist.get_backend(self.group) != "nccl":  # gloo (CPU tests): no device all_gather
+            own = a[:n_own].cpu().numpy()
+            gathered = [None] * self.world
+            dist.all_gather_object(gathered, (self.lm.gids[:n_own], own), group=self.group)
+            total = sum(len(g[0]) for g in gathered)
+            res = np.zeros((total, 3), np.int32)
+            for gid, o in gathered:
+                res[gid] = o
+            return res
+        # NCCL: the owned global ids of every rank are gathered once per local
+        # mesh; each call then moves 12 bytes per element, device to device
+        if getattr(self, "_gather_layout", None) is None:
+            gathered = [None] * self.world
+            dist.all_gather_object(gathered, np.asarray(self.lm.gids[:n_own], np.int64), group=self.group)
+            counts = [len(g) for g in gathered]
+            self._gather_layout = (counts, max(counts), torch.from_numpy(np.concatenate(gathered)).to("cuda"))
+        counts, nmax, gidx = self._gather_layout
+        send = torch.zeros((nmax, 3), dtype=torch.int32, device="cuda")
+        send[:n_own] = a[:n_own]
+        recv = torch.empty((self.world, nmax, 3), dtype=torch.int32, device="cuda")
+        dist.all_gather_into_tensor(recv, send, group=self.group)
+        res = torch.empty((sum(counts), 3), dtype=torch.int32, device="cuda")
+        res[gidx] = torch.cat([recv[r, : counts[r]] for r in range(self.world)])
+        return res.cpu().numpy()
 
 
 def rebalance(ds: DistSolver, global_orders, q_local, axis: int = 2):

@@ -264,6 +264,11 @@ def test_rebalance_single_rank_nccl(dg, orc):
         r_s = S.rhs_eval(q2)
         assert torch.equal(q_new, q2)
         assert torch.equal(r_d, r_s)
+        # the NCCL branch of DistSolver.select_orders (device all_gather of the owned orders), twice (cached layout)
+        tau = S.tau_estimate(q2, r_s)
+        sel_s, _ = S.select_orders(tau, 1e-4, 2, 8)
+        for _ in range(2):
+            assert np.array_equal(nd.select_orders(tau, 1e-4, 2, 8), sel_s)
     finally:
         dist.destroy_process_group(grp)
         if created:
