@@ -851,7 +851,7 @@ def main():
     os.environ["BENCH_PATH"] = args.path
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
-    if world > 1 or os.environ.get("BENCH_FORCE_DIST") == "1":
+    if args.impl == "ours" and (world > 1 or os.environ.get("BENCH_FORCE_DIST") == "1"):
         import torch
         import torch.distributed as dist
 
@@ -859,10 +859,8 @@ def main():
         os.environ.setdefault("MASTER_PORT", "29533")
         os.environ.setdefault("RANK", "0")
         os.environ.setdefault("WORLD_SIZE", "1")
-        backend = "nccl" if args.impl == "ours" else "gloo"
-        if args.impl == "ours":
-            torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group(backend=backend)
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group(backend="nccl")
 
     if args.impl == "reference":
         if rank != 0:
@@ -870,6 +868,10 @@ def main():
         # The reference arm for this tier is the CPU oracle, timed as it stands,
         # on a bounded sample of the cfg5 step: the same 20 RK steps + reference
         # residual + tau + selection on 96 x 4 x 1 elements of the cfg5 recipe.
+        if world > 1 and os.environ.get("OMP_NUM_THREADS") == "1":
+            # torchrun pins every rank to one OpenMP thread; only rank 0 works here: it takes the host's cores,
+            # as the N = 1 run of this arm does (set before the oracle's OpenMP runtime is loaded)
+            os.environ["OMP_NUM_THREADS"] = str(os.cpu_count())
         import oracle
 
         oracle.build()
