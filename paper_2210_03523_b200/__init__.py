@@ -64,14 +64,18 @@ def _digest(srcs):
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile libdgtau.so for sm_100a with nvcc (cross-compiles without a GPU).
     Skipped when the library's stamp matches the sources' content hash."""
+    import fcntl
+
     srcs = sources()
     stamp = _SO + ".stamp"
     dig = _digest(srcs)
-    fresh = os.path.exists(_SO) and os.path.exists(stamp) and open(stamp).read().strip() == dig
-    if force or not fresh:
-        _compile(srcs, verbose)
-        with open(stamp, "w") as f:
-            f.write(dig)
+    with open(_SO + ".lock", "w") as lk:  # the ranks of a torchrun job call this at once: one compiles
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        fresh = os.path.exists(_SO) and os.path.exists(stamp) and open(stamp).read().strip() == dig
+        if force or not fresh:
+            _compile(srcs, verbose)
+            with open(stamp, "w") as f:
+                f.write(dig)
     return _SO
 
 
