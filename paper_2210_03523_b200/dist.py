@@ -128,6 +128,37 @@ def migrate(q_owned, plan: "part.MigrationPlan", group=None):
     return out
 
 
+def gather_layout(own_gids, world, group=None, device="cuda"):
+    """(counts, max count, global row index of every gathered row in rank
+    order): the owned global element ids of every rank, gathered once per
+    local mesh."""
+    import torch
+    import torch.distributed as dist
+
+    gathered = [None] * world
+    dist.all_gather_object(gathered, np.asarray(own_gids, np.int64), group=group)
+    counts = [len(g) for g in gathered]
+    return counts, max(counts), torch.from_numpy(np.concatenate(gathered)).to(device)
+
+
+def gather_rows(own_rows, layout, world, group=None):
+    """Global [sum(counts), k] tensor from every rank's owned rows [n_own, k]
+    (row i of rank r lands at its global id): one all_gather of equal-sized
+    padded blocks, 4k bytes per element, on the rows' device."""
+    import torch
+    import torch.distributed as dist
+
+    counts, nmax, gidx = layout
+    k = own_rows.shape[1]
+    send = torch.zeros((nmax, k), dtype=own_rows.dtype, device=own_rows.device)
+    send[: own_rows.shape[0]] = own_rows
+    recv = torch.empty((world * nmax, k), dtype=own_rows.dtype, device=own_rows.device)
+    dist.all_gather_into_tensor(recv, send, group=group)
+    res = torch.empty((sum(counts), k), dtype=own_rows.dtype, device=own_rows.device)
+    res[gidx] = torch.cat([recv[r * nmax: r * nmax + counts[r]] for r in range(world)])
+    return res
+
+
 class DistSolver:
     """A `Solver` on this rank's local mesh (owned + halo elements) plus the
     exchanges that make owned results identical to the single-rank ones."""
@@ -324,30 +355,11 @@ class DistSolver:
             if int(changed.item()) == 0:
                 break
         n_own = self.lm.n_own
-        if dist.get_backend(self.group) != "nccl":  # gloo (CPU tests): no device all_gather
-            own = a[:n_own].cpu().numpy()
-            gathered = [None] * self.world
-            dist.all_gather_object(gathered, (self.lm.gids[:n_own], own), group=self.group)
-            total = sum(len(g[0]) for g in gathered)
-            res = np.zeros((total, 3), np.int32)
-            for gid, o in gathered:
-                res[gid] = o
-            return res
-        # NCCL: the owned global ids of every rank are gathered once per local
-        # mesh; each call then moves 12 bytes per element, device to device
-        if getattr(self, "_gather_layout", None) is None:
-            gathered = [None] * self.world
-            dist.all_gather_object(gathered, np.asarray(self.lm.gids[:n_own], np.int64), group=self.group)
-            counts = [len(g) for g in gathered]
-            self._gather_layout = (counts, max(counts), torch.from_numpy(np.concatenate(gathered)).to("cuda"))
-        counts, nmax, gidx = self._gather_layout
-        send = torch.zeros((nmax, 3), dtype=torch.int32, device="cuda")
-        send[:n_own] = a[:n_own]
-        recv = torch.empty((self.world, nmax, 3), dtype=torch.int32, device="cuda")
-        dist.all_gather_into_tensor(recv, send, group=self.group)
-        res = torch.empty((sum(counts), 3), dtype=torch.int32, device="cuda")
-        res[gidx] = torch.cat([recv[r, : counts[r]] for r in range(self.world)])
-        return res.cpu().numpy()
+        # NCCL: device to device; gloo (CPU tests): the same gather on host tensors
+        dev = "cuda" if dist.get_backend(self.group) == "nccl" else "cpu"
+        if getattr(self, "_gather_layout", None) is None:  # once per local mesh
+            self._gather_layout = gather_layout(self.lm.gids[:n_own], self.world, self.group, dev)
+        return gather_rows(a[:n_own].to(dev), self._gather_layout, self.world, self.group).cpu().numpy()
 
 
 def rebalance(ds: DistSolver, global_orders, q_local, axis: int = 2):

@@ -375,3 +375,48 @@ def test_dof_owner_properties():
         ldof = np.bincount(layer, weights=dof)
         share = np.array([dof[owner == r].sum() for r in range(world)])
         assert share.max() <= dof.sum() / world + 2 * ldof.max()
+
+
+def _gather_worker(rank, world, port, out_q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2210_03523_b200 import dist as D
+    from paper_2210_03523_b200 import partition as part
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mesh = W.cube_mesh(3, 4, 5)
+        owner = part.dof_owner(mesh.dims, W.orders_random(mesh.E, 2, 7, 9), world, 2)  # unequal owned counts
+        lm = part.local_mesh(mesh, owner, rank)
+        g_rows = np.arange(3 * mesh.E, dtype=np.int32).reshape(mesh.E, 3) * 7 + 1
+        own = torch.from_numpy(g_rows[lm.gids[: lm.n_own]])
+        lay = D.gather_layout(lm.gids[: lm.n_own], world, None, "cpu")
+        ok = True
+        for _ in range(2):  # the cached layout serves every later call
+            ok = ok and bool(np.array_equal(D.gather_rows(own, lay, world).numpy(), g_rows))
+        out_q.put((rank, {"ok": ok, "n_own": int(lm.n_own)}))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_two_rank_gather_rows():
+    """DistSolver.select_orders' gather of the owned rows into the global
+    array (the device path of the N > 1 bench, here on host tensors over
+    gloo): rows land at their global ids with unequal owned counts."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_gather_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=250) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert out[0]["ok"] and out[1]["ok"]
+    assert out[0]["n_own"] != out[1]["n_own"]
