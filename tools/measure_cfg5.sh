@@ -7,6 +7,8 @@
 set -x
 O=gpurun_out/m; mkdir -p $O
 python bench.py > $O/bench.json 2> $O/bench.err
+# the N > 1 code path (DistSolver, NCCL group, per-stage exchange calls) on this one rank
+BENCH_FORCE_DIST=1 python bench.py --no-cpu-baseline > $O/bench_forcedist.json 2> $O/bench_forcedist.err
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv \
     python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $O/bench_ncu.log 2>&1
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv \
